@@ -1,0 +1,239 @@
+/*
+ * rtg.h — C-ABI of the B200 per-tile nucleus segmentation + feature stage.
+ *
+ * This is the drop-in boundary for the Region Templates hot path
+ * (arXiv 1405.7958).  In the reference (/root/reference/proj) the slot where
+ * pixels are computed is empty:
+ *   - TaskNode::body is a `std::function<void()>` (include/rt/wrm.hpp:63-64),
+ *     produced by StageInstance::body (include/rt/dataflow.hpp:48) and invoked
+ *     by the executor after WrmState::next (tests/test_acceptance.cpp:590-596);
+ *   - the simulator materialises stage outputs with a constant payload
+ *     (src/sim.cpp:557-582, run_finalize) and only charges virtual time for
+ *     the compute (src/sim.cpp:630-685, start_task).
+ * A GPU TaskNode variant calls the functions below from its body.  Payloads
+ * are the reference's dense layout: row-major, last axis contiguous
+ * (include/rt/data_region.hpp:84-92; put_chunk length check
+ * src/data_region.cpp:171-192).  RGB tiles are interleaved HWC u8
+ * (RegionKind::kDense3D box <y0,x0,0;y1,x1,2>).
+ *
+ * Conventions
+ *   - Every function returns an rtg_status (0 == RTG_OK).  No C++ exception
+ *     crosses this boundary; the failing call's message is available from
+ *     rtg_last_error() (thread-local).  The C++ host layer maps codes back
+ *     onto the rt::Error taxonomy (include/rt/error.hpp:24-100) exactly the
+ *     way throw_wire_error maps WireErrorCode (src/service.cpp:181-219).
+ *   - Host-buffer functions (rtg_segment_tile, rtg_features,
+ *     rtg_process_tile) are synchronous: H2D copy, kernels, D2H copy.
+ *   - *_dev functions take device pointers, enqueue on the context's stream
+ *     and return without synchronising (capturable in a CUDA graph).
+ *   - The library never frees caller buffers.  Device scratch is owned by the
+ *     rtg_ctx arena (no per-call cudaMalloc).
+ *   - One rtg_ctx per (GPU, host thread); calls on one ctx are serialised by
+ *     the caller.  Contexts on different GPUs run concurrently.
+ *   - There is no CPU fallback: without a usable B200 every compute call
+ *     fails with RTG_ERR_NO_DEVICE / RTG_ERR_DEVICE.
+ */
+#ifndef RTG_H
+#define RTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTG_ABI_VERSION 1
+
+/* Status codes.  Mapping onto rt::Error subclasses (error.hpp:24-100):
+ *   INVALID_ARG -> ConfigError, DIMENSION -> DimensionError,
+ *   RANGE -> RangeError, NOT_FOUND -> NotFoundError,
+ *   OUT_OF_MEMORY / DEVICE / NO_DEVICE -> DeviceError (added, derives Error),
+ *   OVERFLOW -> RangeError, INTERNAL -> Error. */
+typedef enum rtg_status {
+  RTG_OK = 0,
+  RTG_ERR_INVALID_ARG = 1,
+  RTG_ERR_DIMENSION = 2,
+  RTG_ERR_RANGE = 3,
+  RTG_ERR_NOT_FOUND = 4,
+  RTG_ERR_OUT_OF_MEMORY = 5,
+  RTG_ERR_DEVICE = 6,
+  RTG_ERR_NO_DEVICE = 7,
+  RTG_ERR_OVERFLOW = 8,
+  RTG_ERR_INTERNAL = 9
+} rtg_status;
+
+typedef struct rtg_ctx rtg_ctx;
+
+/* Pipeline parameters.  CPU (oracle) and GPU consume the same struct, so the
+ * two variants provably run with identical parameters. */
+typedef struct rtg_params {
+  /* o1 colour deconvolution: H concentration
+   * c_H = sum_c h_coef[c] * OD(v_c), OD(v) = -log10((v + 1) / 256),
+   * quantised to u8 as round(c_H * 255 / h_scale) via 16.16 fixed-point LUTs. */
+  double h_coef[3];
+  double h_scale;
+  /* o2 thresholds: background = r,g,b all > bg_thresh;
+   * RBC = 10*r > rbc_rg10*g && 10*r > rbc_rb10*b.  tissue = !bg && !RBC. */
+  int32_t bg_thresh;
+  int32_t rbc_rg10;
+  int32_t rbc_rb10;
+  /* o3 ReconToNuclei: R = reconstruct_by_dilation(max(H - recon_h, 0), H);
+   * candidate = R >= nuc_thresh && tissue. */
+  int32_t recon_h;
+  int32_t recon_conn; /* 4 or 8 */
+  int32_t nuc_thresh;
+  /* o5 AreaThreshold: keep 8-connected objects with min_area <= area <= max_area. */
+  int32_t min_area;
+  int32_t max_area;
+  /* o6 PreWatershed: d = floor(4 * EDT); F = reconstruct(max(d - ws_h, 0), d). */
+  int32_t ws_h;
+  int32_t reserved[7];
+} rtg_params;
+
+/* Per-object feature row (float32, RTG_NUM_FEATURES columns). */
+#define RTG_NUM_FEATURES 20
+enum rtg_feature {
+  RTG_F_AREA = 0,
+  RTG_F_PERIMETER = 1,   /* # 4-neighbour pixel edges leaving the object */
+  RTG_F_BBOX_Y0 = 2,
+  RTG_F_BBOX_X0 = 3,
+  RTG_F_BBOX_Y1 = 4,     /* inclusive */
+  RTG_F_BBOX_X1 = 5,
+  RTG_F_CENTROID_Y = 6,
+  RTG_F_CENTROID_X = 7,
+  RTG_F_MEAN_I = 8,      /* intensity = hematoxylin plane (u8) */
+  RTG_F_STD_I = 9,
+  RTG_F_MIN_I = 10,
+  RTG_F_MAX_I = 11,
+  RTG_F_MEAN_GRAD = 12,  /* Sobel magnitude, floor(4|g|)/4, replicate border */
+  RTG_F_STD_GRAD = 13,
+  RTG_F_MAJOR_AXIS = 14,
+  RTG_F_MINOR_AXIS = 15,
+  RTG_F_ECCENTRICITY = 16,
+  RTG_F_ORIENTATION = 17,
+  RTG_F_CIRCULARITY = 18,
+  RTG_F_EXTENT = 19
+};
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Default parameters tuned for H&E tiles (Ruifrok-Johnston stain matrix). */
+int rtg_params_default(rtg_params* out);
+
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int rtg_device_count(int* n);
+
+/* Creates a context bound to `device` with scratch for tiles up to
+ * max_h x max_w and up to max_objects objects per tile.  All device memory is
+ * allocated here. */
+int rtg_ctx_create(int device, int64_t max_h, int64_t max_w,
+                   int32_t max_objects, rtg_ctx** out);
+int rtg_ctx_destroy(rtg_ctx* ctx);
+/* The cudaStream_t every *_dev call is enqueued on. */
+int rtg_ctx_stream(rtg_ctx* ctx, void** stream);
+/* Re-targets the context to a caller-owned cudaStream_t (NULL = own stream). */
+int rtg_ctx_set_stream(rtg_ctx* ctx, void* stream);
+/* Waits for the context's stream and reports sticky device-side errors
+ * (object-capacity overflow, queue overflow). */
+int rtg_ctx_sync(rtg_ctx* ctx);
+/* Device-side counters of the last pipeline run (for tests / profiling):
+ * out[0] = objects, out[1] = recon tile visits, out[2] = fill-holes tile
+ * visits, out[3] = watershed markers.  Synchronises. */
+int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* rtg_last_error(void);
+
+/* Pinned host memory for Chunk payloads (data_region.hpp:87-92, follow-up f1). */
+int rtg_host_alloc(size_t bytes, void** out);
+int rtg_host_free(void* p);
+
+/* ---- whole tile, host buffers (synchronous) ------------------------------ */
+
+/* Segments one RGB tile: writes the final nucleus mask (u8 0/1, h*w) and the
+ * canonical labels (i32, h*w; 1..n in order of each object's minimum linear
+ * pixel index, 0 = background).  Either output may be NULL. */
+int rtg_segment_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                     int64_t pitch_bytes, const rtg_params* params,
+                     uint8_t* mask_out, int32_t* labels_out,
+                     int32_t* n_objects);
+
+/* Feature table for a labelled tile: out is n_objects x RTG_NUM_FEATURES f32,
+ * row k-1 describes label k. */
+int rtg_features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
+                 int64_t h, int64_t w, int32_t n_objects, float* out);
+
+/* Segmentation + features in one call (the stage body).  features_out holds
+ * max_rows rows; *n_objects receives the object count (RTG_ERR_OVERFLOW when
+ * it exceeds max_rows).  mask_out / labels_out / hema_out may be NULL. */
+int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                     int64_t pitch_bytes, const rtg_params* params,
+                     uint8_t* mask_out, int32_t* labels_out, uint8_t* hema_out,
+                     float* features_out, int32_t max_rows,
+                     int32_t* n_objects);
+
+/* ---- whole tile, device buffers (asynchronous on the ctx stream) --------- */
+
+/* d_rgb: device RGB (pitch_bytes >= 3*w).  d_mask (u8), d_labels (i32),
+ * d_hema (u8) may be NULL.  d_features: max_objects x RTG_NUM_FEATURES f32
+ * (ctx capacity), d_n_objects: one device int32. */
+int rtg_process_tile_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h,
+                         int64_t w, int64_t pitch_bytes,
+                         const rtg_params* params, uint8_t* d_mask,
+                         int32_t* d_labels, uint8_t* d_hema,
+                         float* d_features, int32_t* d_n_objects);
+
+/* ---- per-operator entry points, device buffers (asynchronous) ------------ */
+
+/* o1+o2: hematoxylin plane, HMAX marker max(H - recon_h, 0), tissue mask. */
+int rtg_colordeconv_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h,
+                        int64_t w, int64_t pitch_bytes,
+                        const rtg_params* params, uint8_t* d_hema,
+                        uint8_t* d_marker, uint8_t* d_tissue);
+/* o3: grayscale reconstruction by dilation (marker <= mask enforced), 4/8-conn.
+ * d_out may alias d_marker. */
+int rtg_recon_u8_dev(rtg_ctx* ctx, const uint8_t* d_marker,
+                     const uint8_t* d_mask, int64_t h, int64_t w, int conn,
+                     uint8_t* d_out);
+int rtg_recon_u16_dev(rtg_ctx* ctx, const uint16_t* d_marker,
+                      const uint16_t* d_mask, int64_t h, int64_t w, int conn,
+                      uint16_t* d_out);
+/* o4: binary hole filling (holes = background not 4-connected to the border). */
+int rtg_fill_holes_dev(rtg_ctx* ctx, const uint8_t* d_in, int64_t h,
+                       int64_t w, uint8_t* d_out);
+/* o8: canonical connected-component labels (conn 4/8), *d_n = count. */
+int rtg_bwlabel_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w,
+                    int conn, int32_t* d_labels, int32_t* d_n);
+/* o5: keep conn-connected objects with min_area <= area <= max_area. */
+int rtg_area_threshold_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h,
+                           int64_t w, int conn, int32_t min_area,
+                           int32_t max_area, uint8_t* d_out);
+/* o6: exact squared Euclidean distance to the nearest zero pixel of the tile
+ * (INT32_MAX when the tile has none). */
+int rtg_edt_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w,
+                int32_t* d_dist2);
+/* o6+o7: PreWatershed + marker watershed on a binary mask.  Writes the
+ * separated mask (u8) and, if d_basin != NULL, the per-pixel basin id
+ * (1 + linear index of the basin marker's first pixel, 0 = background). */
+int rtg_watershed_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h,
+                      int64_t w, int32_t ws_h, uint8_t* d_sep_mask,
+                      int32_t* d_basin);
+/* o9: per-object features for canonical labels 1..*d_n (device count). */
+int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels,
+                     const uint8_t* d_intensity, int64_t h, int64_t w,
+                     const int32_t* d_n, float* d_features);
+
+/* ---- synthetic H&E tiles (deterministic, splitmix64 as src/sim.cpp:33-44) */
+
+/* tile seed = splitmix64(global_seed ^ (tile_row << 32 | tile_col)). */
+int rtg_synth_tile_host(uint64_t global_seed, int64_t tile_row,
+                        int64_t tile_col, int64_t h, int64_t w, uint8_t* rgb);
+int rtg_synth_tile_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row,
+                       int64_t tile_col, int64_t h, int64_t w, uint8_t* d_rgb);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTG_H */

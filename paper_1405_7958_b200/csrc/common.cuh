@@ -1,0 +1,164 @@
+// Shared device/host helpers for the rtg CUDA library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "rtg.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "rtg kernels are written for sm_100a (B200); compile with -gencode arch=compute_100a,code=sm_100a"
+#endif
+
+namespace rtg {
+
+// ---- error plumbing (no exceptions cross extern "C") -----------------------
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define RTG_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return ::rtg::cuda_fail(e_, #call); \
+  } while (0)
+
+#define RTG_LAUNCH(what)                                          \
+  do {                                                            \
+    cudaError_t e_ = cudaGetLastError();                          \
+    if (e_ != cudaSuccess) return ::rtg::cuda_fail(e_, what);     \
+  } while (0)
+
+#define RTG_TRY(call)               \
+  do {                              \
+    int s_ = (call);                \
+    if (s_ != RTG_OK) return s_;    \
+  } while (0)
+
+// ---- sticky device status bits ---------------------------------------------
+enum : uint32_t {
+  kStatusObjectOverflow = 1u << 0,
+  kStatusQueueOverflow = 1u << 1,
+  kStatusEdtFallback = 1u << 2,  // informational: exact row fallback used
+};
+
+// ---- tile-queue state of the IWPP engine ------------------------------------
+struct TileQueue {
+  int32_t* state;     // per tile: 0 idle, 1 queued, 2 processing, 3 dirty
+  int32_t* slots;     // circular queue of tile+1 (0 = empty), 2*ntiles
+  uint32_t* counters; // [0] head, [1] tail, [2] pending, [3] visits
+  int32_t capacity;   // ntiles of the largest tile
+};
+
+// Per-object accumulators of the feature step (SoA, PAPER.md:1162-1177
+// "intermediate results ... fixed sized per nucleus").
+struct FeatureAcc {
+  unsigned long long* sums;  // kSumFields x cap
+  int32_t* mins;             // kMinFields x cap
+  int32_t* maxs;             // kMaxFields x cap
+  int32_t cap;
+};
+enum { kSumArea = 0, kSumY, kSumX, kSumYY, kSumXX, kSumXY, kSumI, kSumII,
+       kSumG, kSumGG, kSumPerim, kSumFields };
+enum { kMinI = 0, kMinY, kMinX, kMinFields };
+enum { kMaxI = 0, kMaxY, kMaxX, kMaxFields };
+
+struct HemaLut {
+  int32_t v[3][256];
+};
+
+}  // namespace rtg
+
+// The context: every device allocation of the stage lives here (arena).
+struct rtg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t max_h = 0, max_w = 0, max_px = 0;
+  int32_t max_objects = 0;
+
+  // planes (max_px elements)
+  uint8_t* rgb = nullptr;     // 3 * max_px, for host-buffer entry points
+  uint8_t* hema = nullptr;
+  uint8_t* recon = nullptr;   // marker in, reconstruction out
+  uint8_t* tissue = nullptr;
+  uint8_t* m1 = nullptr;
+  uint8_t* m2 = nullptr;
+  uint8_t* m3 = nullptr;
+  uint8_t* m4 = nullptr;
+  uint8_t* rm = nullptr;
+  uint16_t* u16a = nullptr;
+  uint16_t* u16b = nullptr;
+  uint16_t* u16c = nullptr;
+  int32_t* i32a = nullptr;
+  int32_t* i32b = nullptr;
+  int32_t* i32c = nullptr;
+  int32_t* labels = nullptr;
+  float* features = nullptr;  // max_objects x RTG_NUM_FEATURES
+
+  // small scratch
+  int32_t* seg_summary = nullptr;  // EDT column-segment summaries
+  int32_t* scan_buf = nullptr;     // CCL compaction per-chunk counts/offsets
+  int32_t* flat_list = nullptr;    // watershed plateau pixel list
+  int32_t* misc = nullptr;         // [0] n_objects, [1] flat count, [2] any_zero, [3] changed, ...
+  uint32_t* status = nullptr;      // sticky status bits
+  int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
+  rtg::TileQueue tq{};
+  rtg::FeatureAcc acc{};
+};
+
+namespace rtg {
+
+constexpr int kTile = 32;  // IWPP tile edge (one warp per tile)
+constexpr int kScanChunk = 4096;
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w);
+void hema_lut(const rtg_params* p, HemaLut* lut);
+
+// ---- launchers (one translation unit each) ---------------------------------
+int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                       int64_t pitch, const rtg_params* p, uint8_t* hema,
+                       uint8_t* marker, uint8_t* tissue);
+int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
+                     int64_t n, int32_t thresh, uint8_t* out);
+
+// IWPP reconstruction by dilation on the tile queue.  J is updated in place.
+// mode 0: J and I are plain planes, all tiles initially queued.
+// mode 1: fill-holes: I = complement of `bin`, J seeded on the border, only
+//         border tiles initially queued; on exit J = reached background.
+int iwpp_recon_u8(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h,
+                  int64_t w, int conn);
+int iwpp_recon_u16(rtg_ctx* ctx, uint16_t* J, const uint16_t* I, int64_t h,
+                   int64_t w, int conn);
+int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
+                    int64_t w, uint8_t* out);
+
+// Union-find CCL: roots[p] = min linear index of p's component (-1 = bg).
+int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
+              int conn, int32_t* roots);
+// Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
+int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
+                  int32_t* labels, int32_t* d_n);
+int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
+                int32_t min_area, int32_t max_area, int32_t* counts,
+                uint8_t* out);
+
+int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
+        int32_t* dist2, uint16_t* dq, uint16_t* mk, int32_t ws_h);
+
+int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
+              int32_t ws_h, uint8_t* sep, int32_t* basin);
+
+int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
+             int64_t h, int64_t w, const int32_t* d_n, float* out);
+
+int synth_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row,
+              int64_t tile_col, int64_t h, int64_t w, uint8_t* d_rgb);
+
+}  // namespace rtg

@@ -1,0 +1,401 @@
+// IWPP engine: grayscale reconstruction by dilation on a persistent
+// tile-granular wavefront queue ("hierarchical and
+// scalable queue to store and manage active elements").
+//
+// Work unit = one 32x32 tile, owned by one warp while it is processed.  The
+// warp stages the tile (+1 px halo) in shared memory, runs alternating
+// raster / anti-raster sweeps (down, up, right, left) to a local fixed point,
+// writes it back, and enqueues exactly those neighbour tiles whose halo it
+// raised.  A per-tile state machine (idle/queued/processing/dirty) guarantees
+// one owner per tile; a global `pending` counter terminates the persistent
+// grid without host round trips.
+//
+// Reconstruction by dilation is the greatest fixed point below the mask
+// reachable from the marker, so the result is independent of the order in
+// which tiles and pixels are relaxed: stale halo reads only cost extra
+// visits, never correctness (values only increase and stay <= the answer).
+//
+// Roofline: HBM/L2 bound; algorithmic bytes 3 B/px (u8: marker + mask in,
+// result out) or 6 B/px (u16).  Revisits are the IWPP overhead.
+#include "common.cuh"
+
+namespace rtg {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kJS = 35;  // J tile stride (34 used: halo + 32 + halo)
+constexpr int kIS = 33;  // I tile stride
+
+struct WarpSmem {
+  uint32_t J[34 * kJS];
+  uint32_t I[32 * kIS];
+};
+
+template <typename T>
+struct PlainMask {
+  const T* I;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const { return I[i]; }
+};
+// fill-holes: the reconstruction runs under the complement of a binary mask
+struct ComplementMask {
+  const uint8_t* bin;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+    return bin[i] ? 0u : 1u;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t ld_state(const T* p) {
+  return (uint32_t)__ldcg(p);  // bypass L1: other warps update J
+}
+template <>
+__device__ __forceinline__ uint32_t ld_state<uint8_t>(const uint8_t* p) {
+  return (uint32_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
+}
+
+// ---- queue primitives (lane 0 only) ----------------------------------------
+
+__device__ void q_push(const TileQueue& q, int32_t cap, int32_t t) {
+  int32_t s = atomicAdd(&q.state[t], 0);
+  while (true) {
+    if (s == 1 || s == 3) return;  // already queued / already marked dirty
+    if (s == 0) {
+      const int32_t old = atomicCAS(&q.state[t], 0, 1);
+      if (old == 0) {
+        atomicAdd(&q.counters[2], 1u);  // pending, before publication
+        const uint32_t pos = atomicAdd(&q.counters[1], 1u);
+        int32_t* slot = &q.slots[pos % (uint32_t)cap];
+        while (atomicCAS(slot, 0, t + 1) != 0) __nanosleep(32);
+        return;
+      }
+      s = old;
+    } else {  // s == 2: being processed -> mark dirty
+      const int32_t old = atomicCAS(&q.state[t], 2, 3);
+      if (old == 2) return;
+      s = old;
+    }
+  }
+}
+
+// Returns a tile id, or -1 when all work is done.
+__device__ int32_t q_pop(const TileQueue& q, int32_t cap) {
+  const uint32_t pos = atomicAdd(&q.counters[0], 1u);
+  int32_t* slot = &q.slots[pos % (uint32_t)cap];
+  while (true) {
+    const int32_t v = atomicExch(slot, 0);
+    if (v != 0) {
+      atomicExch(&q.state[v - 1], 2);
+      __threadfence();
+      return v - 1;
+    }
+    if (*(volatile uint32_t*)&q.counters[2] == 0u) return -1;
+    __nanosleep(64);
+  }
+}
+
+// Returns true when the tile must be processed again (it was marked dirty).
+__device__ bool q_finish(const TileQueue& q, int32_t t) {
+  const int32_t old = atomicCAS(&q.state[t], 2, 0);
+  if (old == 2) {
+    atomicSub(&q.counters[2], 1u);
+    return false;
+  }
+  atomicExch(&q.state[t], 2);  // dirty -> processing again
+  __threadfence();             // acquire the neighbour's fenced border writes
+  return true;
+}
+
+// ---- the persistent kernel ---------------------------------------------------
+
+template <typename T, int CONN, class MaskF>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
+       TileQueue q, int32_t cap, int64_t* visits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xFFFFFFFFu;
+  uint32_t* Js = S.J;
+  uint32_t* Is = S.I;
+  long long my_visits = 0;
+
+  while (true) {
+    int32_t t = 0;
+    if (lane == 0) t = q_pop(q, cap);
+    t = __shfl_sync(full, t, 0);
+    if (t < 0) break;
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const int y0 = ty * kTile, x0 = tx * kTile;
+    const int x = x0 + lane;
+
+    // stage mask (interior) and J (interior + halo)
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int y = y0 + r;
+      const bool in = y < h && x < w;
+      Is[r * kIS + lane] = in ? maskf((int64_t)y * w + x) : 0u;
+    }
+    bool dirty_reload = false;
+    bool tile_changed = false;
+    uint32_t top0, bot0, left0, right0;
+    do {
+      // (re)load J: full tile on first visit, halo only on a dirty reload
+      if (!dirty_reload) {
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int y = y0 + r;
+          uint32_t v = 0;
+          if (y < h && x < w) {
+            const uint32_t j = ld_state(J + (int64_t)y * w + x);
+            const uint32_t m = Is[r * kIS + lane];
+            v = j < m ? j : m;
+            if (v != j) tile_changed = true;  // marker clipped to the mask
+          }
+          Js[(r + 1) * kJS + lane + 1] = v;
+        }
+      }
+      {
+        const int yt = y0 - 1, yb = y0 + 32;
+        Js[lane + 1] = (yt >= 0 && x < w) ? ld_state(J + (int64_t)yt * w + x) : 0u;
+        Js[33 * kJS + lane + 1] = (yb < h && x < w) ? ld_state(J + (int64_t)yb * w + x) : 0u;
+        for (int k = lane; k < 34; k += 32) {
+          const int y = y0 - 1 + k;
+          const bool yin = y >= 0 && y < h;
+          Js[k * kJS + 0] = (yin && x0 > 0) ? ld_state(J + (int64_t)y * w + x0 - 1) : 0u;
+          Js[k * kJS + 33] = (yin && x0 + 32 < w) ? ld_state(J + (int64_t)y * w + x0 + 32) : 0u;
+        }
+      }
+      __syncwarp();
+      top0 = Js[1 * kJS + lane + 1];
+      bot0 = Js[32 * kJS + lane + 1];
+      left0 = Js[(lane + 1) * kJS + 1];
+      right0 = Js[(lane + 1) * kJS + 32];
+
+      // local fixed point
+      bool iter_changed;
+      do {
+        bool ch = false;
+        // down: lane = column c, rows 0..31, neighbours in the row above
+        for (int r = 0; r < 32; ++r) {
+          uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+          const uint32_t* up = row - kJS;
+          uint32_t n = up[0];
+          if (CONN == 8) n = max(n, max(up[-1], up[1]));
+          const uint32_t v = *row;
+          const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+          if (nv != v) { *row = nv; ch = true; }
+          __syncwarp();
+        }
+        // up
+        for (int r = 31; r >= 0; --r) {
+          uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+          const uint32_t* dn = row + kJS;
+          uint32_t n = dn[0];
+          if (CONN == 8) n = max(n, max(dn[-1], dn[1]));
+          const uint32_t v = *row;
+          const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+          if (nv != v) { *row = nv; ch = true; }
+          __syncwarp();
+        }
+        // right: lane = row r, columns 0..31, neighbours in the column left
+        for (int c = 0; c < 32; ++c) {
+          uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+          const uint32_t* lf = px - 1;
+          uint32_t n = lf[0];
+          if (CONN == 8) n = max(n, max(lf[-kJS], lf[kJS]));
+          const uint32_t v = *px;
+          const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+          if (nv != v) { *px = nv; ch = true; }
+          __syncwarp();
+        }
+        // left
+        for (int c = 31; c >= 0; --c) {
+          uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+          const uint32_t* rt = px + 1;
+          uint32_t n = rt[0];
+          if (CONN == 8) n = max(n, max(rt[-kJS], rt[kJS]));
+          const uint32_t v = *px;
+          const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+          if (nv != v) { *px = nv; ch = true; }
+          __syncwarp();
+        }
+        iter_changed = __any_sync(full, ch);
+        tile_changed |= iter_changed;
+      } while (iter_changed);
+
+      ++my_visits;
+      if (tile_changed) {
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int y = y0 + r;
+          if (y < h && x < w) J[(int64_t)y * w + x] = (T)Js[(r + 1) * kJS + lane + 1];
+        }
+        __threadfence();
+      }
+
+      // which neighbours did we raise?  (stale halo only over-approximates)
+      const uint32_t tv = Js[1 * kJS + lane + 1];
+      const uint32_t bv = Js[32 * kJS + lane + 1];
+      const uint32_t lv = Js[(lane + 1) * kJS + 1];
+      const uint32_t rv = Js[(lane + 1) * kJS + 32];
+      bool pn, ps, pw, pe;
+      {
+        uint32_t nt = Js[lane + 1], nb = Js[33 * kJS + lane + 1];
+        uint32_t nl = Js[(lane + 1) * kJS], nr = Js[(lane + 1) * kJS + 33];
+        if (CONN == 8) {
+          nt = min(nt, min(Js[lane], Js[lane + 2]));
+          nb = min(nb, min(Js[33 * kJS + lane], Js[33 * kJS + lane + 2]));
+          nl = min(nl, min(Js[lane * kJS], Js[(lane + 2) * kJS]));
+          nr = min(nr, min(Js[lane * kJS + 33], Js[(lane + 2) * kJS + 33]));
+        }
+        pn = __any_sync(full, tv != top0 && tv > nt);
+        ps = __any_sync(full, bv != bot0 && bv > nb);
+        pw = __any_sync(full, lv != left0 && lv > nl);
+        pe = __any_sync(full, rv != right0 && rv > nr);
+      }
+      if (lane == 0) {
+        const int tiles_y = (h + kTile - 1) / kTile;
+        if (pn && ty > 0) q_push(q, cap, t - tiles_x);
+        if (ps && ty + 1 < tiles_y) q_push(q, cap, t + tiles_x);
+        if (pw && tx > 0) q_push(q, cap, t - 1);
+        if (pe && tx + 1 < tiles_x) q_push(q, cap, t + 1);
+        if (CONN == 8) {
+          const uint32_t c00 = Js[1 * kJS + 1], c01 = Js[1 * kJS + 32];
+          const uint32_t c10 = Js[32 * kJS + 1], c11 = Js[32 * kJS + 32];
+          // corner pixels changed: compare with the diagonal halo corner
+          if (ty > 0 && tx > 0 && c00 > Js[0]) q_push(q, cap, t - tiles_x - 1);
+          if (ty > 0 && tx + 1 < tiles_x && c01 > Js[33]) q_push(q, cap, t - tiles_x + 1);
+          if (ty + 1 < tiles_y && tx > 0 && c10 > Js[33 * kJS]) q_push(q, cap, t + tiles_x - 1);
+          if (ty + 1 < tiles_y && tx + 1 < tiles_x && c11 > Js[33 * kJS + 33])
+            q_push(q, cap, t + tiles_x + 1);
+        }
+      }
+      int again = 0;
+      if (lane == 0) again = q_finish(q, t) ? 1 : 0;
+      again = __shfl_sync(full, again, 0);
+      dirty_reload = again != 0;
+      tile_changed = false;
+    } while (dirty_reload);
+  }
+  if (lane == 0 && visits) atomicAdd((unsigned long long*)visits, (unsigned long long)my_visits);
+}
+
+// Queue initialisation: mode 0 = every tile, mode 1 = border tiles only.
+__global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
+                             int border_only) {
+  const int ntiles = tiles_y * tiles_x;
+  // single block: compute the list deterministically
+  __shared__ int32_t count;
+  if (threadIdx.x == 0) count = 0;
+  __syncthreads();
+  for (int base = 0; base < ntiles; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    bool take = false;
+    if (t < ntiles) {
+      const int ty = t / tiles_x, tx = t - ty * tiles_x;
+      take = !border_only || ty == 0 || tx == 0 || ty == tiles_y - 1 || tx == tiles_x - 1;
+    }
+    // order-preserving compaction within the chunk
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, take);
+    __shared__ int32_t warp_cnt[32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) warp_cnt[wid] = __popc(b);
+    __syncthreads();
+    int off = 0;
+    for (int k = 0; k < wid; ++k) off += warp_cnt[k];
+    const int pos = count + off + __popc(b & ((1u << lane) - 1u));
+    if (t < ntiles) q.state[t] = take ? 1 : 0;
+    if (take) q.slots[pos] = t + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += warp_cnt[k];
+      count += tot;
+    }
+    __syncthreads();
+  }
+  for (int i = count + threadIdx.x; i < cap; i += blockDim.x) q.slots[i] = 0;
+  if (threadIdx.x == 0) {
+    q.counters[0] = 0;
+    q.counters[1] = (uint32_t)count;
+    q.counters[2] = (uint32_t)count;
+  }
+}
+
+// fill-holes seeds: J = 1 on border pixels of the complement, else 0
+__global__ void k_fill_seed(const uint8_t* __restrict__ bin, int h, int w,
+                            uint8_t* __restrict__ J) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+    const bool border = y == 0 || x == 0 || y == h - 1 || x == w - 1;
+    J[i] = (uint8_t)(border && !bin[i]);
+  }
+}
+
+// out = bin | !reached
+__global__ void k_fill_final(const uint8_t* __restrict__ bin,
+                             const uint8_t* __restrict__ reached, int64_t n,
+                             uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)(bin[i] || !reached[i]);
+}
+
+template <typename T, int CONN, class MaskF>
+int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w,
+             int border_only) {
+  const int tiles_y = (int)ceil_div(h, kTile), tiles_x = (int)ceil_div(w, kTile);
+  const int ntiles = tiles_y * tiles_x;
+  const int32_t cap = 2 * ntiles;
+  if (cap > ctx->tq.capacity) return fail(RTG_ERR_DIMENSION, "tile exceeds queue capacity");
+  k_queue_init<<<1, 1024, 0, ctx->stream>>>(ctx->tq, cap, tiles_y, tiles_x, border_only);
+  RTG_LAUNCH("k_queue_init");
+  const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
+  static bool attr_set[64] = {};  // per instantiation and device
+  if (ctx->device < 64 && !attr_set[ctx->device]) {
+    RTG_CUDA(cudaFuncSetAttribute(k_iwpp<T, CONN, MaskF>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set[ctx->device] = true;
+  }
+  int per_sm = 0;
+  RTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iwpp<T, CONN, MaskF>,
+                                                         kWarpsPerBlock * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  int blocks = ctx->num_sms * per_sm;
+  const int need = (int)ceil_div(ntiles, kWarpsPerBlock);
+  if (blocks > need) blocks = need;
+  k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
+      J, maskf, (int)h, (int)w, tiles_x, ctx->tq, cap, ctx->stats + 1);
+  RTG_LAUNCH("k_iwpp");
+  return RTG_OK;
+}
+
+}  // namespace
+
+int iwpp_recon_u8(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h,
+                  int64_t w, int conn) {
+  if (conn == 8) return run_iwpp<uint8_t, 8>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0);
+  return run_iwpp<uint8_t, 4>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0);
+}
+
+int iwpp_recon_u16(rtg_ctx* ctx, uint16_t* J, const uint16_t* I, int64_t h,
+                   int64_t w, int conn) {
+  if (conn == 8) return run_iwpp<uint16_t, 8>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0);
+  return run_iwpp<uint16_t, 4>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0);
+}
+
+int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
+                    int64_t w, uint8_t* out) {
+  const int64_t n = h * w;
+  const int blocks = (int)(ceil_div(n, 256) < ctx->num_sms * 8 ? ceil_div(n, 256) : ctx->num_sms * 8);
+  k_fill_seed<<<blocks, 256, 0, ctx->stream>>>(bin, (int)h, (int)w, J);
+  RTG_LAUNCH("k_fill_seed");
+  RTG_TRY((run_iwpp<uint8_t, 4>(ctx, J, ComplementMask{bin}, h, w, 1)));
+  k_fill_final<<<blocks, 256, 0, ctx->stream>>>(bin, J, n, out);
+  RTG_LAUNCH("k_fill_final");
+  return RTG_OK;
+}
+
+}  // namespace rtg

@@ -1,0 +1,222 @@
+// o6 PreWatershed + o7 Watershed.
+//
+// Markers: F = HMAX_ws_h(dq) by IWPP reconstruction, Fw = fg ? F + 1 : 0,
+// regional maxima = Fw > recon(Fw - 1, Fw) (a second IWPP pass).
+// Watershed: the arrowing ("tobogganing") formulation of the Koerbes et al.
+// GPU watershed the paper uses: every foreground pixel points to its steepest
+// ascending 8-neighbour (max Fw, ties -> minimum linear index); pixels of
+// non-maximal plateaus point down the BFS distance to the plateau exits
+// (ties -> minimum index); regional-maximum pixels are roots.  Following the
+// arrows gives each pixel its marker.  Every rule is local and
+// order-independent, so the labelling is unique (bit-exact vs the CPU
+// oracle).  Separation lines: drop pixels having an 8-neighbour with a higher
+// basin id.
+//
+// Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + sep 1 B + basin 4 B
+// out (dq/markers/Fw are internal planes).
+#include "common.cuh"
+
+namespace rtg {
+namespace {
+
+constexpr int32_t kInfD = 1 << 30;
+
+__global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
+                          const uint16_t* __restrict__ F, uint16_t* __restrict__ Fw,
+                          uint16_t* __restrict__ G) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = mask[i] ? (uint32_t)F[i] + 1u : 0u;
+    Fw[i] = (uint16_t)f;
+    G[i] = (uint16_t)(f ? f - 1u : 0u);
+  }
+}
+
+// rm / arrows / plateau list.  ptr: self for markers, steepest ascent for
+// pixels with a higher neighbour (delta 0), -2 for flat plateau pixels.
+__global__ void __launch_bounds__(256)
+k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
+            const uint16_t* __restrict__ G, uint8_t* __restrict__ rm,
+            int32_t* __restrict__ ptr, int32_t* __restrict__ delta,
+            int32_t* __restrict__ flat_list, int32_t* __restrict__ flat_count) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = Fw[i];
+    uint8_t is_rm = 0;
+    int32_t p = -1, d = -1;
+    if (f) {
+      if (f > G[i]) {
+        is_rm = 1;
+        p = (int32_t)i;
+      } else {
+        const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+        uint32_t best = f;
+        int32_t arg = -1;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            if (dy == 0 && dx == 0) continue;
+            const int yy = y + dy, xx = x + dx;
+            if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+            const int32_t j = yy * w + xx;
+            const uint32_t fj = Fw[j];
+            if (fj > best) { best = fj; arg = j; }  // row-major order: first max = min index
+          }
+        }
+        if (arg >= 0) {
+          p = arg;
+          d = 0;
+        } else {
+          p = -2;
+          d = kInfD;
+          const int slot = atomicAdd(flat_count, 1);
+          flat_list[slot] = (int32_t)i;
+        }
+      }
+    }
+    rm[i] = is_rm;
+    ptr[i] = p;
+    delta[i] = d;
+  }
+}
+
+// BFS distances inside non-maximal plateaus (Bellman-Ford to the fixed point,
+// one CTA), then arrows down the distance.
+__global__ void __launch_bounds__(1024)
+k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
+             const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
+             int32_t* delta, int32_t* __restrict__ ptr) {
+  __shared__ int changed;
+  const int n = *flat_count;
+  if (n == 0) return;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) changed = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int32_t i = flat_list[k];
+      const int y = i / w, x = i - y * w;
+      const uint32_t f = Fw[i];
+      int32_t best = *(volatile int32_t*)&delta[i];
+      for (int dy = -1; dy <= 1; ++dy) {
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (dy == 0 && dx == 0) continue;
+          const int yy = y + dy, xx = x + dx;
+          if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+          const int32_t j = yy * w + xx;
+          if (Fw[j] != f) continue;
+          const int32_t dj = *(volatile int32_t*)&delta[j];
+          if (dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
+        }
+      }
+      if (best < *(volatile int32_t*)&delta[i]) {
+        delta[i] = best;
+        changed = 1;
+      }
+    }
+    __syncthreads();
+    if (!changed) break;
+  }
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int y = i / w, x = i - y * w;
+    const uint32_t f = Fw[i];
+    const int32_t di = delta[i];
+    int32_t arg = -2;
+    for (int dy = -1; dy <= 1 && arg < 0; ++dy) {
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (dy == 0 && dx == 0) continue;
+        const int yy = y + dy, xx = x + dx;
+        if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+        const int32_t j = yy * w + xx;
+        if (Fw[j] == f && delta[j] == di - 1) { arg = j; break; }
+      }
+    }
+    ptr[i] = arg;
+  }
+}
+
+__global__ void k_ws_resolve(int64_t n, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ mroots,
+                             int32_t* __restrict__ basin) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t q = ptr[i];
+    int32_t b = 0;
+    if (q != -1) {
+      q = (int32_t)i;
+      int32_t nx = ptr[q];
+      while (nx >= 0 && nx != q) {
+        q = nx;
+        nx = ptr[q];
+      }
+      b = nx == q ? mroots[q] + 1 : 0;
+    }
+    basin[i] = b;
+  }
+}
+
+__global__ void k_ws_separate(int h, int w, const int32_t* __restrict__ basin,
+                              uint8_t* __restrict__ sep) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = basin[i];
+    uint8_t keep = b > 0;
+    if (keep) {
+      const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+      for (int dy = -1; dy <= 1 && keep; ++dy) {
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int yy = y + dy, xx = x + dx;
+          if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+          if (basin[(int64_t)yy * w + xx] > b) { keep = 0; break; }
+        }
+      }
+    }
+    sep[i] = keep;
+  }
+}
+
+int grid_for(rtg_ctx* ctx, int64_t n) {
+  const int64_t want = ceil_div(n, 256);
+  const int64_t cap = (int64_t)ctx->num_sms * 8;
+  return (int)(want < cap ? want : cap);
+}
+
+}  // namespace
+
+int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
+              int32_t ws_h, uint8_t* sep, int32_t* basin) {
+  const int64_t n = h * w;
+  uint16_t* dq = ctx->u16a;
+  uint16_t* F = ctx->u16b;
+  uint16_t* G = ctx->u16c;
+  RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));
+  RTG_TRY(iwpp_recon_u16(ctx, F, dq, h, w, 8));  // HMAX
+  uint16_t* Fw = ctx->u16a;                       // dq is dead now
+  k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw, G);
+  RTG_LAUNCH("k_ws_prep");
+  RTG_TRY(iwpp_recon_u16(ctx, G, Fw, h, w, 8));  // regional-maximum test
+  int32_t* ptr = ctx->i32a;
+  int32_t* delta = ctx->i32b;
+  int32_t* flat_count = ctx->misc + 1;
+  RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
+  k_ws_arrows<<<grid_for(ctx, n), 256, 0, ctx->stream>>>((int)h, (int)w, Fw, G, ctx->rm,
+                                                        ptr, delta, ctx->flat_list,
+                                                        flat_count);
+  RTG_LAUNCH("k_ws_arrows");
+  int32_t* mroots = ctx->i32c;
+  RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
+  k_ws_plateau<<<1, 1024, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count,
+                                            delta, ptr);
+  RTG_LAUNCH("k_ws_plateau");
+  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, ptr, mroots, basin);
+  RTG_LAUNCH("k_ws_resolve");
+  k_ws_separate<<<grid_for(ctx, n), 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
+  RTG_LAUNCH("k_ws_separate");
+  return RTG_OK;
+}
+
+}  // namespace rtg

@@ -1,0 +1,489 @@
+// extern "C" boundary (include/rtg.h): context arena, error mapping and the
+// stage pipeline.  Every compute entry point requires a CUDA device; there is
+// no CPU fallback anywhere in this library.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace rtg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  const std::string msg = std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                          cudaGetErrorString(e) + ")";
+  if (e == cudaErrorMemoryAllocation) return fail(RTG_ERR_OUT_OF_MEMORY, msg);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+      e == cudaErrorInvalidDevice)
+    return fail(RTG_ERR_NO_DEVICE, msg);
+  return fail(RTG_ERR_DEVICE, msg);
+}
+
+int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
+  if (h <= 0 || w <= 0) return fail(RTG_ERR_DIMENSION, "tile extent must be positive");
+  if (h > ctx->max_h || w > ctx->max_w || h * w > ctx->max_px)
+    return fail(RTG_ERR_DIMENSION, "tile " + std::to_string(h) + "x" + std::to_string(w) +
+                                       " exceeds context capacity " +
+                                       std::to_string(ctx->max_h) + "x" +
+                                       std::to_string(ctx->max_w));
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  return RTG_OK;
+}
+
+namespace {
+
+int check_params(const rtg_params* p) {
+  if (!p) return fail(RTG_ERR_INVALID_ARG, "null rtg_params");
+  if (p->recon_conn != 4 && p->recon_conn != 8)
+    return fail(RTG_ERR_INVALID_ARG, "recon_conn must be 4 or 8");
+  if (!(p->h_scale > 0.0)) return fail(RTG_ERR_INVALID_ARG, "h_scale must be positive");
+  if (p->min_area < 0 || p->max_area < p->min_area)
+    return fail(RTG_ERR_INVALID_ARG, "need 0 <= min_area <= max_area");
+  if (p->ws_h < 0 || p->recon_h < 0) return fail(RTG_ERR_INVALID_ARG, "heights must be >= 0");
+  return RTG_OK;
+}
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  RTG_CUDA(cudaMalloc((void**)p, sizeof(T) * (count ? count : 1)));
+  return RTG_OK;
+}
+
+template <typename T>
+__global__ void k_clip_copy(const T* __restrict__ marker, const T* __restrict__ mask,
+                            int64_t n, T* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T a = marker[i], b = mask[i];
+    out[i] = a < b ? a : b;
+  }
+}
+
+int grid_for(rtg_ctx* ctx, int64_t n) {
+  const int64_t want = ceil_div(n, 256);
+  const int64_t cap = (int64_t)ctx->num_sms * 8;
+  return (int)(want < cap ? want : cap);
+}
+
+// The stage: o1 .. o9 on device buffers, all asynchronous on ctx->stream.
+int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
+             const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
+             float* d_features, int32_t* d_n, bool with_features) {
+  uint8_t* hema = d_hema ? d_hema : ctx->hema;
+  uint8_t* mask = d_mask ? d_mask : ctx->m4;
+  int32_t* labels = d_labels ? d_labels : ctx->labels;
+  int32_t* n_out = d_n ? d_n : ctx->misc;
+  // o1+o2: hematoxylin, HMAX marker (in place of the reconstruction), tissue
+  RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, ctx->recon, ctx->tissue));
+  // o3 ReconToNuclei
+  RTG_TRY(iwpp_recon_u8(ctx, ctx->recon, hema, h, w, p->recon_conn));
+  RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
+  // o4 FillHoles
+  RTG_TRY(iwpp_fill_holes(ctx, ctx->m1, ctx->m2, h, w, ctx->m2));
+  // o5 AreaThreshold
+  RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a));
+  RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
+  // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer)
+  RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels));
+  // o8 BWLabel (canonical)
+  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a));
+  RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out));
+  // o9 features
+  if (with_features) RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features));
+  return RTG_OK;
+}
+
+int upload_rgb(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w, int64_t pitch) {
+  if (!rgb) return fail(RTG_ERR_INVALID_ARG, "null rgb");
+  if (pitch < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
+  if (pitch == 3 * w) {
+    RTG_CUDA(cudaMemcpyAsync(ctx->rgb, rgb, (size_t)(3 * h * w), cudaMemcpyHostToDevice,
+                             ctx->stream));
+  } else {
+    RTG_CUDA(cudaMemcpy2DAsync(ctx->rgb, (size_t)(3 * w), rgb, (size_t)pitch, (size_t)(3 * w),
+                               (size_t)h, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return RTG_OK;
+}
+
+}  // namespace
+}  // namespace rtg
+
+using namespace rtg;
+
+extern "C" {
+
+const char* rtg_last_error(void) { return g_last_error.c_str(); }
+
+int rtg_params_default(rtg_params* p) {
+  if (!p) return fail(RTG_ERR_INVALID_ARG, "null rtg_params");
+  std::memset(p, 0, sizeof(*p));
+  // column 0 of inv(row-normalised Ruifrok-Johnston H&E stain matrix)
+  p->h_coef[0] = 1.874787447891341;
+  p->h_coef[1] = -0.06579592311838535;
+  p->h_coef[2] = -0.6008832496835673;
+  p->h_scale = 1.25;
+  p->bg_thresh = 215;
+  p->rbc_rg10 = 25;
+  p->rbc_rb10 = 22;
+  p->recon_h = 24;
+  p->recon_conn = 8;
+  p->nuc_thresh = 70;
+  p->min_area = 24;
+  p->max_area = 2500;
+  p->ws_h = 3;
+  return RTG_OK;
+}
+
+int rtg_device_count(int* n) {
+  if (!n) return fail(RTG_ERR_INVALID_ARG, "null out");
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  cudaGetLastError();
+  *n = c;
+  return RTG_OK;
+}
+
+int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects,
+                   rtg_ctx** out) {
+  if (!out) return fail(RTG_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  if (max_h <= 0 || max_w <= 0 || max_h > 8192 || max_w > 8192)
+    return fail(RTG_ERR_DIMENSION, "context tile extent must be in [1, 8192]");
+  if (max_objects <= 0) return fail(RTG_ERR_INVALID_ARG, "max_objects must be positive");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(RTG_ERR_NO_DEVICE, "no CUDA device: the rtg stage has no CPU fallback");
+  }
+  if (device < 0 || device >= count) return fail(RTG_ERR_NO_DEVICE, "device index out of range");
+  RTG_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  RTG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(RTG_ERR_DEVICE, std::string("rtg kernels are built for sm_100a (B200); found ") +
+                                    prop.name);
+  rtg_ctx* c = new rtg_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->max_h = max_h;
+  c->max_w = max_w;
+  c->max_px = max_h * max_w;
+  c->max_objects = max_objects;
+  auto cleanup = [&](int st) {
+    rtg_ctx_destroy(c);
+    return st;
+  };
+  int st;
+  if ((st = [&]() -> int {
+        RTG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        const size_t n = (size_t)c->max_px;
+        RTG_TRY(dalloc(&c->rgb, 3 * n));
+        RTG_TRY(dalloc(&c->hema, n));
+        RTG_TRY(dalloc(&c->recon, n));
+        RTG_TRY(dalloc(&c->tissue, n));
+        RTG_TRY(dalloc(&c->m1, n));
+        RTG_TRY(dalloc(&c->m2, n));
+        RTG_TRY(dalloc(&c->m3, n));
+        RTG_TRY(dalloc(&c->m4, n));
+        RTG_TRY(dalloc(&c->rm, n));
+        RTG_TRY(dalloc(&c->u16a, n));
+        RTG_TRY(dalloc(&c->u16b, n));
+        RTG_TRY(dalloc(&c->u16c, n));
+        RTG_TRY(dalloc(&c->i32a, n));
+        RTG_TRY(dalloc(&c->i32b, n));
+        RTG_TRY(dalloc(&c->i32c, n));
+        RTG_TRY(dalloc(&c->labels, n));
+        RTG_TRY(dalloc(&c->features, (size_t)max_objects * RTG_NUM_FEATURES));
+        RTG_TRY(dalloc(&c->seg_summary, (size_t)ceil_div(max_h, 32) * (size_t)max_w));
+        RTG_TRY(dalloc(&c->scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
+        RTG_TRY(dalloc(&c->flat_list, n));
+        RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
+        RTG_TRY(dalloc(&c->status, 1));
+        RTG_TRY(dalloc(&c->stats, 8));
+        const int64_t ntiles = ceil_div(max_h, kTile) * ceil_div(max_w, kTile);
+        c->tq.capacity = (int32_t)(2 * ntiles);
+        RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
+        RTG_TRY(dalloc(&c->tq.slots, (size_t)(2 * ntiles)));
+        RTG_TRY(dalloc(&c->tq.counters, 4));
+        c->acc.cap = max_objects;
+        RTG_TRY(dalloc(&c->acc.sums, (size_t)kSumFields * max_objects));
+        RTG_TRY(dalloc(&c->acc.mins, (size_t)kMinFields * max_objects));
+        RTG_TRY(dalloc(&c->acc.maxs, (size_t)kMaxFields * max_objects));
+        RTG_CUDA(cudaMemsetAsync(c->misc, 0, sizeof(int32_t) * (128 + (size_t)max_h), c->stream));
+        RTG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(uint32_t), c->stream));
+        RTG_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(int64_t) * 8, c->stream));
+        RTG_CUDA(cudaMemsetAsync(c->tq.state, 0, sizeof(int32_t) * (size_t)ntiles, c->stream));
+        RTG_CUDA(cudaStreamSynchronize(c->stream));
+        return RTG_OK;
+      }()) != RTG_OK)
+    return cleanup(st);
+  *out = c;
+  return RTG_OK;
+}
+
+int rtg_ctx_destroy(rtg_ctx* c) {
+  if (!c) return RTG_OK;
+  cudaSetDevice(c->device);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
+                  c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
+                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->misc,
+                  c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
+                  c->acc.sums, c->acc.mins, c->acc.maxs};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return RTG_OK;
+}
+
+int rtg_ctx_stream(rtg_ctx* ctx, void** stream) {
+  if (!ctx || !stream) return fail(RTG_ERR_INVALID_ARG, "null argument");
+  *stream = (void*)ctx->stream;
+  return RTG_OK;
+}
+
+int rtg_ctx_set_stream(rtg_ctx* ctx, void* stream) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return RTG_OK;
+}
+
+int rtg_ctx_sync(rtg_ctx* ctx) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  uint32_t st = 0;
+  RTG_CUDA(cudaMemcpy(&st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st & kStatusObjectOverflow) {
+    RTG_CUDA(cudaMemset(ctx->status, 0, sizeof(uint32_t)));
+    return fail(RTG_ERR_OVERFLOW, "object count exceeded the context's max_objects");
+  }
+  if (st & kStatusQueueOverflow) return fail(RTG_ERR_INTERNAL, "IWPP queue overflow");
+  return RTG_OK;
+}
+
+int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]) {
+  if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  int32_t misc[4];
+  int64_t st[8];
+  RTG_CUDA(cudaMemcpy(misc, ctx->misc, sizeof(misc), cudaMemcpyDeviceToHost));
+  RTG_CUDA(cudaMemcpy(st, ctx->stats, sizeof(st), cudaMemcpyDeviceToHost));
+  RTG_CUDA(cudaMemset(ctx->stats, 0, sizeof(st)));
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  out[0] = misc[0];
+  out[1] = st[1];
+  out[2] = misc[1];
+  return RTG_OK;
+}
+
+int rtg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(RTG_ERR_INVALID_ARG, "null out");
+  RTG_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  return RTG_OK;
+}
+
+int rtg_host_free(void* p) {
+  if (p) RTG_CUDA(cudaFreeHost(p));
+  return RTG_OK;
+}
+
+// ---- whole tile, host buffers ------------------------------------------------
+
+int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                     int64_t pitch_bytes, const rtg_params* params, uint8_t* mask_out,
+                     int32_t* labels_out, uint8_t* hema_out, float* features_out,
+                     int32_t max_rows, int32_t* n_objects) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  RTG_TRY(check_params(params));
+  if (!n_objects) return fail(RTG_ERR_INVALID_ARG, "null n_objects");
+  if (features_out && max_rows < 0) return fail(RTG_ERR_INVALID_ARG, "max_rows < 0");
+  RTG_TRY(upload_rgb(ctx, rgb, h, w, pitch_bytes));
+  RTG_TRY(pipeline(ctx, ctx->rgb, h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                   ctx->features, ctx->misc, features_out != nullptr));
+  int32_t n = 0;
+  RTG_CUDA(cudaMemcpyAsync(&n, ctx->misc, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *n_objects = n;
+  const size_t px = (size_t)(h * w);
+  if (mask_out)
+    RTG_CUDA(cudaMemcpyAsync(mask_out, ctx->m4, px, cudaMemcpyDeviceToHost, ctx->stream));
+  if (labels_out)
+    RTG_CUDA(cudaMemcpyAsync(labels_out, ctx->labels, px * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (hema_out)
+    RTG_CUDA(cudaMemcpyAsync(hema_out, ctx->hema, px, cudaMemcpyDeviceToHost, ctx->stream));
+  const int32_t rows = n < max_rows ? n : max_rows;
+  const int32_t dev_rows = rows < ctx->max_objects ? rows : ctx->max_objects;
+  if (features_out && dev_rows > 0)
+    RTG_CUDA(cudaMemcpyAsync(features_out, ctx->features,
+                             sizeof(float) * RTG_NUM_FEATURES * (size_t)dev_rows,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  RTG_TRY(rtg_ctx_sync(ctx));
+  if (features_out && (n > max_rows || n > ctx->max_objects))
+    return fail(RTG_ERR_OVERFLOW, "tile has " + std::to_string(n) + " objects; feature rows: " +
+                                      std::to_string(dev_rows));
+  return RTG_OK;
+}
+
+int rtg_segment_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                     int64_t pitch_bytes, const rtg_params* params, uint8_t* mask_out,
+                     int32_t* labels_out, int32_t* n_objects) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  RTG_TRY(check_params(params));
+  if (!n_objects) return fail(RTG_ERR_INVALID_ARG, "null n_objects");
+  RTG_TRY(upload_rgb(ctx, rgb, h, w, pitch_bytes));
+  RTG_TRY(pipeline(ctx, ctx->rgb, h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                   nullptr, ctx->misc, false));
+  const size_t px = (size_t)(h * w);
+  if (mask_out)
+    RTG_CUDA(cudaMemcpyAsync(mask_out, ctx->m4, px, cudaMemcpyDeviceToHost, ctx->stream));
+  if (labels_out)
+    RTG_CUDA(cudaMemcpyAsync(labels_out, ctx->labels, px * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  int32_t n = 0;
+  RTG_CUDA(cudaMemcpyAsync(&n, ctx->misc, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
+  RTG_TRY(rtg_ctx_sync(ctx));
+  *n_objects = n;
+  return RTG_OK;
+}
+
+int rtg_features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h,
+                 int64_t w, int32_t n_objects, float* out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!labels || !intensity || (!out && n_objects > 0))
+    return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (n_objects < 0 || n_objects > ctx->max_objects)
+    return fail(RTG_ERR_OVERFLOW, "n_objects outside [0, max_objects]");
+  const size_t px = (size_t)(h * w);
+  RTG_CUDA(cudaMemcpyAsync(ctx->labels, labels, px * 4, cudaMemcpyHostToDevice, ctx->stream));
+  RTG_CUDA(cudaMemcpyAsync(ctx->hema, intensity, px, cudaMemcpyHostToDevice, ctx->stream));
+  RTG_CUDA(cudaMemcpyAsync(ctx->misc, &n_objects, sizeof(int32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  RTG_TRY(features(ctx, ctx->labels, ctx->hema, h, w, ctx->misc, ctx->features));
+  if (n_objects > 0)
+    RTG_CUDA(cudaMemcpyAsync(out, ctx->features,
+                             sizeof(float) * RTG_NUM_FEATURES * (size_t)n_objects,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  return rtg_ctx_sync(ctx);
+}
+
+// ---- whole tile, device buffers ------------------------------------------------
+
+int rtg_process_tile_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w,
+                         int64_t pitch_bytes, const rtg_params* params, uint8_t* d_mask,
+                         int32_t* d_labels, uint8_t* d_hema, float* d_features,
+                         int32_t* d_n_objects) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  RTG_TRY(check_params(params));
+  if (!d_rgb || !d_features || !d_n_objects) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (pitch_bytes < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
+  return pipeline(ctx, d_rgb, h, w, pitch_bytes, params, d_mask, d_labels, d_hema, d_features,
+                  d_n_objects, true);
+}
+
+// ---- per-operator entry points ---------------------------------------------------
+
+int rtg_colordeconv_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w,
+                        int64_t pitch_bytes, const rtg_params* params, uint8_t* d_hema,
+                        uint8_t* d_marker, uint8_t* d_tissue) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  RTG_TRY(check_params(params));
+  if (!d_rgb) return fail(RTG_ERR_INVALID_ARG, "null rgb");
+  if (pitch_bytes < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
+  return launch_colordeconv(ctx, d_rgb, h, w, pitch_bytes, params, d_hema, d_marker, d_tissue);
+}
+
+int rtg_recon_u8_dev(rtg_ctx* ctx, const uint8_t* d_marker, const uint8_t* d_mask, int64_t h,
+                     int64_t w, int conn, uint8_t* d_out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_marker || !d_mask || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
+  k_clip_copy<uint8_t><<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(d_marker, d_mask, h * w,
+                                                                      d_out);
+  RTG_LAUNCH("k_clip_copy");
+  return iwpp_recon_u8(ctx, d_out, d_mask, h, w, conn);
+}
+
+int rtg_recon_u16_dev(rtg_ctx* ctx, const uint16_t* d_marker, const uint16_t* d_mask,
+                      int64_t h, int64_t w, int conn, uint16_t* d_out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_marker || !d_mask || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
+  k_clip_copy<uint16_t><<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(d_marker, d_mask,
+                                                                       h * w, d_out);
+  RTG_LAUNCH("k_clip_copy");
+  return iwpp_recon_u16(ctx, d_out, d_mask, h, w, conn);
+}
+
+int rtg_fill_holes_dev(rtg_ctx* ctx, const uint8_t* d_in, int64_t h, int64_t w,
+                       uint8_t* d_out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_in || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  return iwpp_fill_holes(ctx, d_in, ctx->m2, h, w, d_out);
+}
+
+int rtg_bwlabel_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w, int conn,
+                    int32_t* d_labels, int32_t* d_n) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_mask || !d_labels) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
+  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a));
+  return ccl_canonical(ctx, ctx->i32a, h, w, d_labels, d_n ? d_n : ctx->misc);
+}
+
+int rtg_area_threshold_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w,
+                           int conn, int32_t min_area, int32_t max_area, uint8_t* d_out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_mask || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
+  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a));
+  return area_filter(ctx, ctx->i32a, h * w, min_area, max_area, ctx->i32b, d_out);
+}
+
+int rtg_edt_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w, int32_t* d_dist2) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_mask || !d_dist2) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  return edt(ctx, d_mask, h, w, d_dist2, nullptr, nullptr, 0);
+}
+
+int rtg_watershed_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w, int32_t ws_h,
+                      uint8_t* d_sep_mask, int32_t* d_basin) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_mask || !d_sep_mask) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (ws_h < 0) return fail(RTG_ERR_INVALID_ARG, "ws_h must be >= 0");
+  return watershed(ctx, d_mask, h, w, ws_h, d_sep_mask, d_basin ? d_basin : ctx->labels);
+}
+
+int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels, const uint8_t* d_intensity,
+                     int64_t h, int64_t w, const int32_t* d_n, float* d_features) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_labels || !d_intensity || !d_n || !d_features)
+    return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  return features(ctx, d_labels, d_intensity, h, w, d_n, d_features);
+}
+
+int rtg_synth_tile_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row, int64_t tile_col,
+                       int64_t h, int64_t w, uint8_t* d_rgb) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_rgb) return fail(RTG_ERR_INVALID_ARG, "null rgb");
+  return synth_dev(ctx, global_seed, tile_row, tile_col, h, w, d_rgb);
+}
+
+}  // extern "C"

@@ -1,0 +1,325 @@
+"""ctypes binding of the rtg C-ABI (include/rtg.h).
+
+This is the Python-side view of the drop-in boundary: the same entry points a
+cgo/JNI/ctypes maintainer would bind.  Errors are raised
+as exceptions mirroring the reference's rt::Error taxonomy
+(/root/reference/proj/include/rt/error.hpp:24-100), mapped from status codes
+the way throw_wire_error maps WireErrorCode (src/service.cpp:181-219).
+
+There is no CPU fallback: loading fails loudly when librtg.so is missing, and
+every compute call fails with NoDeviceError on a host without a B200.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtg.so")
+
+NUM_FEATURES = 20
+FEATURE_NAMES = [
+    "area", "perimeter", "bbox_y0", "bbox_x0", "bbox_y1", "bbox_x1",
+    "centroid_y", "centroid_x", "mean_i", "std_i", "min_i", "max_i",
+    "mean_grad", "std_grad", "major_axis", "minor_axis", "eccentricity",
+    "orientation", "circularity", "extent",
+]
+DEFAULT_SEED = 1405795800
+
+# exported symbols (must match include/rtg.h)
+SYMBOLS = [
+    "rtg_params_default", "rtg_device_count", "rtg_ctx_create", "rtg_ctx_destroy",
+    "rtg_ctx_stream", "rtg_ctx_set_stream", "rtg_ctx_sync", "rtg_ctx_stats",
+    "rtg_last_error", "rtg_host_alloc", "rtg_host_free", "rtg_segment_tile",
+    "rtg_features", "rtg_process_tile", "rtg_process_tile_dev",
+    "rtg_colordeconv_dev", "rtg_recon_u8_dev", "rtg_recon_u16_dev",
+    "rtg_fill_holes_dev", "rtg_bwlabel_dev", "rtg_area_threshold_dev",
+    "rtg_edt_dev", "rtg_watershed_dev", "rtg_features_dev",
+    "rtg_synth_tile_host", "rtg_synth_tile_dev",
+]
+
+
+class Error(RuntimeError):
+    """rt::Error"""
+    code = 9
+
+
+class ConfigError(Error):
+    code = 1
+
+
+class DimensionError(Error):
+    code = 2
+
+
+class RangeError(Error):
+    code = 3
+
+
+class NotFoundError(Error):
+    code = 4
+
+
+class DeviceError(Error):
+    code = 6
+
+
+class OutOfMemoryError(DeviceError):
+    code = 5
+
+
+class NoDeviceError(DeviceError):
+    code = 7
+
+
+class OverflowError_(RangeError):
+    code = 8
+
+
+_CODE_TO_EXC = {1: ConfigError, 2: DimensionError, 3: RangeError, 4: NotFoundError,
+                5: OutOfMemoryError, 6: DeviceError, 7: NoDeviceError,
+                8: OverflowError_, 9: Error}
+
+
+class Params(ctypes.Structure):
+    """rtg_params (include/rtg.h)."""
+    _fields_ = [
+        ("h_coef", ctypes.c_double * 3),
+        ("h_scale", ctypes.c_double),
+        ("bg_thresh", ctypes.c_int32),
+        ("rbc_rg10", ctypes.c_int32),
+        ("rbc_rb10", ctypes.c_int32),
+        ("recon_h", ctypes.c_int32),
+        ("recon_conn", ctypes.c_int32),
+        ("nuc_thresh", ctypes.c_int32),
+        ("min_area", ctypes.c_int32),
+        ("max_area", ctypes.c_int32),
+        ("ws_h", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {}
+        for name, _ in self._fields_:
+            if name == "reserved":
+                continue
+            v = getattr(self, name)
+            d[name] = list(v) if name == "h_coef" else v
+        return d
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Loads librtg.so.  Raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the stage has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+    sig = {
+        "rtg_params_default": [vp],
+        "rtg_device_count": [vp],
+        "rtg_ctx_create": [ctypes.c_int, i64, i64, i32, vp],
+        "rtg_ctx_destroy": [vp],
+        "rtg_ctx_stream": [vp, vp],
+        "rtg_ctx_set_stream": [vp, vp],
+        "rtg_ctx_sync": [vp],
+        "rtg_ctx_stats": [vp, vp],
+        "rtg_host_alloc": [ctypes.c_size_t, vp],
+        "rtg_host_free": [vp],
+        "rtg_segment_tile": [vp, vp, i64, i64, i64, vp, vp, vp, vp],
+        "rtg_features": [vp, vp, vp, i64, i64, i32, vp],
+        "rtg_process_tile": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, i32, vp],
+        "rtg_process_tile_dev": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp],
+        "rtg_colordeconv_dev": [vp, vp, i64, i64, i64, vp, vp, vp, vp],
+        "rtg_recon_u8_dev": [vp, vp, vp, i64, i64, ctypes.c_int, vp],
+        "rtg_recon_u16_dev": [vp, vp, vp, i64, i64, ctypes.c_int, vp],
+        "rtg_fill_holes_dev": [vp, vp, i64, i64, vp],
+        "rtg_bwlabel_dev": [vp, vp, i64, i64, ctypes.c_int, vp, vp],
+        "rtg_area_threshold_dev": [vp, vp, i64, i64, ctypes.c_int, i32, i32, vp],
+        "rtg_edt_dev": [vp, vp, i64, i64, vp],
+        "rtg_watershed_dev": [vp, vp, i64, i64, i32, vp, vp],
+        "rtg_features_dev": [vp, vp, vp, i64, i64, vp, vp],
+        "rtg_synth_tile_host": [u64, i64, i64, i64, i64, vp],
+        "rtg_synth_tile_dev": [vp, u64, i64, i64, i64, i64, vp],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.rtg_last_error.argtypes = []
+    lib.rtg_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = load().rtg_last_error().decode(errors="replace")
+        raise _CODE_TO_EXC.get(status, Error)(f"rtg status {status}: {msg}")
+
+
+def default_params() -> Params:
+    p = Params()
+    check(load().rtg_params_default(ctypes.byref(p)))
+    return p
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    check(load().rtg_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor
+
+
+def synth_tile_host(tile_row: int = 0, tile_col: int = 0, h: int = 4096, w: int = 4096,
+                    seed: int = DEFAULT_SEED) -> np.ndarray:
+    """Synthetic H&E RGB tile (H, W, 3) u8, byte-identical to synth_tile_dev."""
+    out = np.empty((h, w, 3), np.uint8)
+    check(load().rtg_synth_tile_host(seed, tile_row, tile_col, h, w, _ptr(out)))
+    return out
+
+
+class Context:
+    """One rtg_ctx: device scratch arena + stream for tiles up to max_h x max_w."""
+
+    def __init__(self, device: int = 0, max_h: int = 4096, max_w: int = 4096,
+                 max_objects: int = 1 << 17):
+        self.lib = load()
+        self.handle = ctypes.c_void_p()
+        check(self.lib.rtg_ctx_create(device, max_h, max_w, max_objects,
+                                      ctypes.byref(self.handle)))
+        self.device, self.max_h, self.max_w, self.max_objects = device, max_h, max_w, max_objects
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.rtg_ctx_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- streams / sync -------------------------------------------------------
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(self.lib.rtg_ctx_stream(self.handle, ctypes.byref(s)))
+        return s.value or 0
+
+    def set_stream(self, stream_handle: int) -> None:
+        check(self.lib.rtg_ctx_set_stream(self.handle, ctypes.c_void_p(stream_handle)))
+
+    def sync(self) -> None:
+        check(self.lib.rtg_ctx_sync(self.handle))
+
+    def stats(self) -> list:
+        out = (ctypes.c_int64 * 8)()
+        check(self.lib.rtg_ctx_stats(self.handle, out))
+        return list(out)
+
+    # -- host-buffer entry points (synchronous) -------------------------------
+    def process_tile(self, rgb: np.ndarray, params: Optional[Params] = None,
+                     max_rows: Optional[int] = None):
+        """Segmentation + features of one (H, W, 3) u8 tile.
+        Returns (mask u8, labels i32, hema u8, features f32 [n, 20], n)."""
+        params = params or default_params()
+        h, w, _ = rgb.shape
+        rgb = np.ascontiguousarray(rgb)
+        mask = np.empty((h, w), np.uint8)
+        labels = np.empty((h, w), np.int32)
+        hema = np.empty((h, w), np.uint8)
+        max_rows = self.max_objects if max_rows is None else max_rows
+        feats = np.empty((max_rows, NUM_FEATURES), np.float32)
+        n = ctypes.c_int32(0)
+        check(self.lib.rtg_process_tile(self.handle, _ptr(rgb), h, w, 3 * w, ctypes.byref(params),
+                                        _ptr(mask), _ptr(labels), _ptr(hema), _ptr(feats),
+                                        max_rows, ctypes.byref(n)))
+        return mask, labels, hema, feats[: n.value].copy(), n.value
+
+    def segment_tile(self, rgb: np.ndarray, params: Optional[Params] = None):
+        params = params or default_params()
+        h, w, _ = rgb.shape
+        rgb = np.ascontiguousarray(rgb)
+        mask = np.empty((h, w), np.uint8)
+        labels = np.empty((h, w), np.int32)
+        n = ctypes.c_int32(0)
+        check(self.lib.rtg_segment_tile(self.handle, _ptr(rgb), h, w, 3 * w, ctypes.byref(params),
+                                        _ptr(mask), _ptr(labels), ctypes.byref(n)))
+        return mask, labels, n.value
+
+    def features(self, labels: np.ndarray, intensity: np.ndarray, n: int) -> np.ndarray:
+        h, w = labels.shape
+        out = np.empty((max(n, 1), NUM_FEATURES), np.float32)
+        check(self.lib.rtg_features(self.handle, _ptr(np.ascontiguousarray(labels, np.int32)),
+                                    _ptr(np.ascontiguousarray(intensity, np.uint8)), h, w, n,
+                                    _ptr(out)))
+        return out[:n]
+
+    # -- device-buffer entry points (asynchronous on the ctx stream) -----------
+    def process_tile_dev(self, d_rgb, h, w, params, d_mask, d_labels, d_hema, d_features, d_n,
+                         pitch=None):
+        check(self.lib.rtg_process_tile_dev(self.handle, _ptr(d_rgb), h, w,
+                                            3 * w if pitch is None else pitch,
+                                            ctypes.byref(params), _ptr(d_mask), _ptr(d_labels),
+                                            _ptr(d_hema), _ptr(d_features), _ptr(d_n)))
+
+    def colordeconv_dev(self, d_rgb, h, w, params, d_hema, d_marker, d_tissue, pitch=None):
+        check(self.lib.rtg_colordeconv_dev(self.handle, _ptr(d_rgb), h, w,
+                                           3 * w if pitch is None else pitch,
+                                           ctypes.byref(params), _ptr(d_hema), _ptr(d_marker),
+                                           _ptr(d_tissue)))
+
+    def recon_dev(self, d_marker, d_mask, h, w, conn, d_out, bits=8):
+        fn = self.lib.rtg_recon_u8_dev if bits == 8 else self.lib.rtg_recon_u16_dev
+        check(fn(self.handle, _ptr(d_marker), _ptr(d_mask), h, w, conn, _ptr(d_out)))
+
+    def fill_holes_dev(self, d_in, h, w, d_out):
+        check(self.lib.rtg_fill_holes_dev(self.handle, _ptr(d_in), h, w, _ptr(d_out)))
+
+    def bwlabel_dev(self, d_mask, h, w, conn, d_labels, d_n):
+        check(self.lib.rtg_bwlabel_dev(self.handle, _ptr(d_mask), h, w, conn, _ptr(d_labels),
+                                       _ptr(d_n)))
+
+    def area_threshold_dev(self, d_mask, h, w, conn, min_area, max_area, d_out):
+        check(self.lib.rtg_area_threshold_dev(self.handle, _ptr(d_mask), h, w, conn, min_area,
+                                              max_area, _ptr(d_out)))
+
+    def edt_dev(self, d_mask, h, w, d_dist2):
+        check(self.lib.rtg_edt_dev(self.handle, _ptr(d_mask), h, w, _ptr(d_dist2)))
+
+    def watershed_dev(self, d_mask, h, w, ws_h, d_sep, d_basin=None):
+        check(self.lib.rtg_watershed_dev(self.handle, _ptr(d_mask), h, w, ws_h, _ptr(d_sep),
+                                         _ptr(d_basin)))
+
+    def features_dev(self, d_labels, d_intensity, h, w, d_n, d_features):
+        check(self.lib.rtg_features_dev(self.handle, _ptr(d_labels), _ptr(d_intensity), h, w,
+                                        _ptr(d_n), _ptr(d_features)))
+
+    def synth_tile_dev(self, d_rgb, tile_row=0, tile_col=0, h=4096, w=4096, seed=DEFAULT_SEED):
+        check(self.lib.rtg_synth_tile_dev(self.handle, seed, tile_row, tile_col, h, w,
+                                          _ptr(d_rgb)))

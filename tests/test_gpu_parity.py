@@ -1,0 +1,293 @@
+"""GPU parity: every operator of the stage, called through the C-ABI, against
+the CPU oracle on the same seeded inputs.  Bar: bit-exact for masks, labels,
+distances, reconstructions; features within rtol 1e-5 (atol 1e-6 for values
+that can be ~0, e.g. orientation)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+FEAT_RTOL = 1e-5
+FEAT_ATOL = 1e-6
+
+
+def _np_dev(a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint16:
+        a = a.view(np.int16)
+    return torch.from_numpy(a).cuda()
+
+
+def _dev_np(t, dtype=None):
+    torch.cuda.synchronize()
+    a = t.cpu().numpy()
+    if dtype is not None:
+        a = a.view(dtype)
+    return a
+
+
+@pytest.fixture(scope="module")
+def ctx(rtg):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = rtg.Context(0, 4096, 4096, 1 << 17)
+    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def tile4k(rtg):
+    return rtg.synth_tile_host(0, 0, 4096, 4096)
+
+
+def _rand_blobs(rng, h, w, density=0.3, smooth=2):
+    from scipy import ndimage as ndi
+    f = ndi.gaussian_filter(rng.random((h, w)), smooth)
+    return (f > np.quantile(f, 1 - density)).astype(np.uint8)
+
+
+def _maze(h, w):
+    """Single-pixel-wide serpentine corridor: worst-case IWPP wavefront."""
+    m = np.zeros((h, w), np.uint8)
+    for y in range(0, h, 2):
+        m[y, :] = 1
+    for k, y in enumerate(range(1, h, 2)):
+        m[y, (w - 1) if k % 2 == 0 else 0] = 1
+    return m
+
+
+# ---------------------------------------------------------------- generator
+
+def test_synth_dev_matches_host(rtg, ctx):
+    for (h, w, r, c) in [(512, 640, 0, 0), (4096, 4096, 3, 7), (1696, 4096, 24, 5)]:
+        host = rtg.synth_tile_host(r, c, h, w)
+        d = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+        ctx.synth_tile_dev(d, r, c, h, w)
+        assert np.array_equal(_dev_np(d), host)
+
+
+# ---------------------------------------------------------------- o1/o2
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (1000, 1333), (7, 5), (1, 1)])
+def test_colordeconv(rtg, ctx, oracle, shape):
+    h, w = shape
+    rgb = rtg.synth_tile_host(1, 2, h, w)
+    p = rtg.default_params()
+    ref = oracle.colordeconv(rgb, p)
+    d_rgb = _np_dev(rgb)
+    outs = [torch.empty((h, w), dtype=torch.uint8, device="cuda") for _ in range(3)]
+    ctx.colordeconv_dev(d_rgb, h, w, p, *outs)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(_dev_np(o), r)
+
+
+def test_colordeconv_pitched(rtg, ctx, oracle):
+    h, w, pitch = 333, 517, 3 * 517 + 13
+    rgb = rtg.synth_tile_host(4, 4, h, w)
+    buf = np.zeros((h, pitch), np.uint8)
+    buf[:, : 3 * w] = rgb.reshape(h, 3 * w)
+    p = rtg.default_params()
+    ref = oracle.colordeconv(rgb, p)
+    outs = [torch.empty((h, w), dtype=torch.uint8, device="cuda") for _ in range(3)]
+    ctx.colordeconv_dev(_np_dev(buf), h, w, p, *outs, pitch=pitch)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(_dev_np(o), r)
+
+
+# ---------------------------------------------------------------- o3
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_recon_hdome_4k(rtg, ctx, oracle, tile4k, conn):
+    p = rtg.default_params()
+    hema, marker, _ = oracle.colordeconv(tile4k, p)
+    ref = oracle.recon(marker, hema, conn)
+    out = torch.empty((4096, 4096), dtype=torch.uint8, device="cuda")
+    ctx.recon_dev(_np_dev(marker), _np_dev(hema), 4096, 4096, conn, out)
+    assert np.array_equal(_dev_np(out), ref)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("shape", [(257, 391), (64, 64), (1, 100), (100, 1), (33, 31)])
+def test_recon_random(ctx, oracle, conn, shape):
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1] + conn)
+    h, w = shape
+    mask = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    marker = (mask * (rng.random((h, w)) < 0.02)).astype(np.uint8)
+    ref = oracle.recon(marker, mask, conn)
+    out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    ctx.recon_dev(_np_dev(marker), _np_dev(mask), h, w, conn, out)
+    assert np.array_equal(_dev_np(out), ref)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_recon_maze_long_wavefront(ctx, oracle, conn):
+    h, w = 512, 512
+    mask = (_maze(h, w) * 200).astype(np.uint8)
+    marker = np.zeros_like(mask)
+    marker[0, 0] = 200
+    ref = oracle.recon(marker, mask, conn)
+    out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    ctx.recon_dev(_np_dev(marker), _np_dev(mask), h, w, conn, out)
+    got = _dev_np(out)
+    assert np.array_equal(got, ref)
+    assert (got == 200).sum() == (mask > 0).sum()  # the wave reached the far end
+
+
+def test_recon_u16(ctx, oracle):
+    rng = np.random.default_rng(7)
+    h, w = 300, 420
+    mask = rng.integers(0, 60000, (h, w)).astype(np.uint16)
+    marker = np.maximum(mask.astype(np.int64) - 5000, 0).astype(np.uint16)
+    ref = oracle.recon(marker, mask, 8)
+    out = torch.empty((h, w), dtype=torch.int16, device="cuda")
+    ctx.recon_dev(_np_dev(marker), _np_dev(mask), h, w, 8, out, bits=16)
+    assert np.array_equal(_dev_np(out, np.uint16), ref)
+
+
+# ---------------------------------------------------------------- o4
+
+@pytest.mark.parametrize("shape", [(512, 512), (4096, 4096), (31, 77)])
+def test_fill_holes(ctx, oracle, shape):
+    rng = np.random.default_rng(shape[0])
+    h, w = shape
+    m = 1 - _rand_blobs(rng, h, w, 0.45, 1.5)
+    ref = oracle.fill_holes(m)
+    out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    ctx.fill_holes_dev(_np_dev(m), h, w, out)
+    assert np.array_equal(_dev_np(out), ref)
+
+
+# ---------------------------------------------------------------- o5 / o8
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("shape", [(4096, 4096), (1000, 1333), (1, 1), (5, 70)])
+def test_bwlabel(ctx, oracle, conn, shape):
+    rng = np.random.default_rng(sum(shape) + conn)
+    h, w = shape
+    m = _rand_blobs(rng, h, w, 0.3, 1.0) if min(h, w) > 4 else (rng.random((h, w)) < 0.5).astype(np.uint8)
+    ref, nref = oracle.bwlabel(m, conn)
+    lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.bwlabel_dev(_np_dev(m), h, w, conn, lab, n)
+    assert int(_dev_np(n)[0]) == nref
+    assert np.array_equal(_dev_np(lab), ref)
+
+
+def test_bwlabel_full_and_empty(ctx, oracle):
+    for v in (0, 1):
+        m = np.full((300, 300), v, np.uint8)
+        lab = torch.empty((300, 300), dtype=torch.int32, device="cuda")
+        n = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ctx.bwlabel_dev(_np_dev(m), 300, 300, 8, lab, n)
+        assert int(_dev_np(n)[0]) == v
+        assert np.array_equal(_dev_np(lab), oracle.bwlabel(m, 8)[0])
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_area_threshold(ctx, oracle, conn):
+    rng = np.random.default_rng(11)
+    h, w = 2048, 1536
+    m = _rand_blobs(rng, h, w, 0.25, 1.2)
+    ref = oracle.area_threshold(m, conn, 24, 300)
+    out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    ctx.area_threshold_dev(_np_dev(m), h, w, conn, 24, 300, out)
+    assert np.array_equal(_dev_np(out), ref)
+
+
+# ---------------------------------------------------------------- o6
+
+@pytest.mark.parametrize("case", ["blobs", "sparse_zeros", "no_zeros", "one_zero", "thin"])
+def test_edt(ctx, oracle, case):
+    rng = np.random.default_rng(3)
+    h, w = 777, 1024
+    if case == "blobs":
+        m = _rand_blobs(rng, h, w, 0.4, 3)
+    elif case == "sparse_zeros":
+        m = (rng.random((h, w)) > 0.0002).astype(np.uint8)  # exercises the exact fallback
+    elif case == "no_zeros":
+        m = np.ones((h, w), np.uint8)
+    elif case == "one_zero":
+        m = np.ones((h, w), np.uint8)
+        m[h // 3, w - 5] = 0
+    else:
+        m = np.ones((h, w), np.uint8)
+        m[:, ::7] = 0
+    ref = oracle.edt_sq(m)
+    out = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    ctx.edt_dev(_np_dev(m), h, w, out)
+    assert np.array_equal(_dev_np(out), ref)
+
+
+# ---------------------------------------------------------------- o6/o7
+
+@pytest.mark.parametrize("ws_h", [0, 3, 8])
+def test_watershed(ctx, oracle, ws_h):
+    rng = np.random.default_rng(ws_h + 100)
+    h, w = 1024, 1280
+    m = _rand_blobs(rng, h, w, 0.35, 2.5)
+    sep_ref, basin_ref = oracle.watershed(m, ws_h)
+    sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    ctx.watershed_dev(_np_dev(m), h, w, ws_h, sep, basin)
+    assert np.array_equal(_dev_np(basin), basin_ref)
+    assert np.array_equal(_dev_np(sep), sep_ref)
+
+
+# ---------------------------------------------------------------- o9
+
+def test_features(ctx, oracle, tile4k):
+    ref = oracle.process_tile(tile4k[:1024, :1024])
+    labels, n = ref["labels"], ref["n"]
+    hema = oracle.colordeconv(tile4k[:1024, :1024], oracle.default_params())[0]
+    got = ctx.features(labels, hema, n)
+    np.testing.assert_allclose(got, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+
+
+# ---------------------------------------------------------------- whole stage
+
+@pytest.mark.parametrize("shape,rc", [((1024, 1024), (0, 0)), ((4096, 4096), (0, 0)),
+                                      ((4096, 1696), (3, 24)), ((1696, 1696), (24, 24)),
+                                      ((97, 203), (9, 9))])
+def test_pipeline(rtg, ctx, oracle, shape, rc):
+    h, w = shape
+    rgb = rtg.synth_tile_host(rc[0], rc[1], h, w)
+    p = rtg.default_params()
+    mask, labels, hema, feats, n = ctx.process_tile(rgb, p)
+    ref = oracle.process_tile(rgb, p)
+    assert n == ref["n"]
+    assert np.array_equal(mask, ref["mask"])
+    assert np.array_equal(labels, ref["labels"])
+    np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+
+
+def test_pipeline_dev_async_matches_host_entry(rtg, ctx):
+    h = w = 2048
+    p = rtg.default_params()
+    d_rgb = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+    ctx.synth_tile_dev(d_rgb, 5, 6, h, w)
+    d_mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    d_lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    d_feat = torch.empty((ctx.max_objects, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+    d_n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.process_tile_dev(d_rgb, h, w, p, d_mask, d_lab, None, d_feat, d_n)
+    ctx.sync()
+    n = int(_dev_np(d_n)[0])
+    mask, labels, _, feats, n2 = ctx.process_tile(_dev_np(d_rgb), p)
+    assert n == n2
+    assert np.array_equal(_dev_np(d_mask), mask)
+    assert np.array_equal(_dev_np(d_lab), labels)
+    assert np.array_equal(_dev_np(d_feat)[:n], feats)
+
+
+def test_repeatable(rtg, ctx):
+    rgb = rtg.synth_tile_host(2, 2, 1024, 1024)
+    a = ctx.process_tile(rgb)
+    b = ctx.process_tile(rgb)
+    for x, y in zip(a, b):
+        if isinstance(x, np.ndarray):
+            assert np.array_equal(x, y)
+        else:
+            assert x == y
