@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 segmentation + feature stage (BASELINE.json metric:
+"tile Mpixel/s (segment+features) at 1/2/4/8 B200, % of HBM roofline").
+
+Workload (BASELINE.json configs[4], "C5"): the synthetic 100k x 100k
+whole-slide image cut into 4K tiles exactly as the reference's
+partition_regular does (/root/reference/proj/src/partition.cpp:23-54: 25 x 25
+tiles, 576 full + 48 edge 4096x1696 + 1 corner 1696x1696).  Tiles are a bag of
+tasks: one process per GPU, each rank owns a fixed shard of tiles per step
+(weak scaling), no data-path collective; the per-step feature tables are
+gathered to rank 0 with NCCL (the only cross-GPU traffic).
+
+A step = every rank runs the full stage (o1..o9) over its shard, then the
+gather.  `value` is measured with inputs already resident in HBM; `e2e` goes
+through the C-ABI host-buffer entry point rtg_process_tile with pinned host
+tiles (H2D of RGB and D2H of the feature table inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WSI = 100_000
+TILE = 4096
+METRIC = "tile Mpixel/s (segment+features) at 1/2/4/8 B200, % of HBM roofline"
+
+# Algorithmic bytes per pixel of each stage: compulsory inputs
+# read once + outputs written once.
+STAGE_BYTES_PER_PX = {
+    "colordeconv": 6,   # RGB 3 in; hematoxylin, marker, tissue 1 each out
+    "recon": 3,         # marker + mask in, reconstruction out (u8)
+    "fill_holes": 3,    # reconstruction + tissue in, filled mask out
+    "area": 2,          # mask in, filtered mask out
+    "edt": 5,           # mask in, dq u16 + HMAX marker u16 out
+    "markers": 9,       # dq + marker u16 + mask in, Fw + G u16 out
+    "watershed": 9,     # Fw + G u16 in, basin i32 + separated mask out
+    "label": 5,         # separated mask in, labels i32 out
+    "features": 5,      # labels i32 + intensity u8 in (table out is ~0.1 B/px)
+}
+
+
+def wsi_tiles():
+    """partition_regular(<0,0;99999,99999>, {4096,4096}): row-major tiles."""
+    n = math.ceil(WSI / TILE)
+    out = []
+    for i in range(n):
+        for j in range(n):
+            h = min(TILE, WSI - i * TILE)
+            w = min(TILE, WSI - j * TILE)
+            out.append((i, j, h, w))
+    return out
+
+
+def global_tile(g):
+    """Global tile sequence: slide s = g // 625, tile t of that slide."""
+    tiles = wsi_tiles()
+    s, t = divmod(g, len(tiles))
+    i, j, h, w = tiles[t]
+    return s * 25 + i, j, h, w  # seed row includes the slide index
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if parts[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_sample(n_tiles, threads):
+    """The oracle on the host cores over a bounded sample of WSI tiles (bag of
+    tasks over a thread pool, like ManagerState::dispatch).  Returns
+    (Mpixel/s, seconds, pixels)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import pyoracle
+    from paper_1405_7958_b200 import rtg
+
+    pyoracle.load()
+    params = pyoracle.default_params()
+    tiles = [global_tile(g) for g in range(n_tiles)]
+    rgbs = [rtg.synth_tile_host(r, c, h, w) for (r, c, h, w) in tiles]
+    px = sum(h * w for (_, _, h, w) in tiles)
+
+    def run(k):
+        pyoracle.process_tile(rgbs[k], params, max_rows=1 << 16)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(run, range(n_tiles)))
+    dt = time.perf_counter() - t0
+    return px / dt / 1e6, dt, px
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference has no implementation of this path
+    (SPEC.md:15), so its CPU arm is the oracle port timed on the host cores."""
+    if rank != 0:
+        return
+    cores = host_cores()
+    n_tiles = max(1, min(cores, 64))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(min(n_tiles, cores), cores)
+    vals, secs, pxs = [], 0.0, 0
+    for _ in range(args.steps):
+        v, dt, px = cpu_oracle_sample(n_tiles, cores)
+        vals.append(v)
+        secs += dt
+        pxs += px
+    value = pxs / secs / 1e6
+    sample = (f"{n_tiles} WSI tiles (first {n_tiles} of the 625-tile 100k^2 slide) per step, "
+              f"oracle pipeline o1..o9, {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C5 100k x 100k WSI as 4K tiles (bounded CPU sample)",
+                   "path": "CPU oracle port (reference ships no pixel code)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rtg", choices=["rtg", "reference"])
+    ap.add_argument("--tiles-per-rank", type=int, default=80,
+                    help="tiles each rank processes per step (80 x 8 GPUs ~ one 625-tile WSI)")
+    ap.add_argument("--streams", type=int, default=2, help="concurrent contexts per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1405_7958_b200 import rtg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    T = args.tiles_per_rank
+    S = max(1, args.streams)
+    cap = 32768
+    params = rtg.default_params()
+    ctxs = [rtg.Context(local, TILE, TILE, cap) for _ in range(S)]
+    ext = [torch.cuda.ExternalStream(c.stream()) for c in ctxs]
+    my_tiles = [global_tile(rank * T + k) for k in range(T)]
+    px_rank = sum(h * w for (_, _, h, w) in my_tiles)
+
+    # inputs resident in HBM (T x 48 MiB), generated on the device
+    rgbs = []
+    for (r, c, h, w) in my_tiles:
+        t = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+        ctxs[0].synth_tile_dev(t, r, c, h, w)
+        rgbs.append(t)
+    ctxs[0].sync()
+    feats = torch.empty((T, cap, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+    counts = torch.zeros((T,), dtype=torch.int32, device="cuda")
+
+    def gather(n_host):
+        """Pack this rank's tables and gather them on rank 0 (NCCL)."""
+        rows = int(n_host.sum())
+        packed = torch.empty((max(rows, 1), rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+        off = 0
+        for k in range(T):
+            nk = int(n_host[k])
+            if nk:
+                packed[off:off + nk].copy_(feats[k, :nk])
+                off += nk
+        if world == 1:
+            return packed[:rows], rows
+        sizes = torch.tensor([rows], dtype=torch.int64, device="cuda")
+        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(all_sizes, sizes)
+        mx = int(max(int(s) for s in all_sizes))
+        buf = torch.zeros((max(mx, 1), rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+        buf[:rows].copy_(packed[:rows])
+        if rank == 0:
+            outs = [torch.empty_like(buf) for _ in range(world)]
+            ops = [dist.P2POp(dist.irecv, outs[r], r) for r in range(1, world)]
+            reqs = dist.batch_isend_irecv(ops) if ops else []
+            for q in reqs:
+                q.wait()
+            outs[0] = buf
+            total = sum(int(s) for s in all_sizes)
+            return torch.cat([outs[r][: int(all_sizes[r])] for r in range(world)]), total
+        reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, buf, 0)])
+        for q in reqs:
+            q.wait()
+        return None, rows
+
+    cur = torch.cuda.current_stream()
+
+    def step():
+        ev0 = torch.cuda.Event()
+        ev0.record(cur)
+        for e in ext:
+            e.wait_event(ev0)
+        for k, (r, c, h, w) in enumerate(my_tiles):
+            ctx = ctxs[k % S]
+            ctx.process_tile_dev(rgbs[k], h, w, params, None, None, None, feats[k], counts[k:k + 1])
+        for e in ext:
+            cur.wait_stream(e)
+        n_host = counts.cpu()
+        return gather(n_host)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.sync()
+    launches0 = sum(c.launches() for c in ctxs)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(cur)
+    total_rows = 0
+    for _ in range(args.steps):
+        _, rows = step()
+        total_rows += rows
+    t_end.record(cur)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    gpu_launches = sum(c.launches() for c in ctxs) - launches0
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    total_px = px_rank * world * args.steps
+    value = total_px / (ms_max / 1e3) / 1e6
+
+    # ---- roofline: dedicated timed pass, one stream, stage events on the
+    # launching stream (rtg_ctx_profile)
+    ctx = ctxs[0]
+    ctx.profile(True)
+    n_prof = min(T, 16)
+    for k in range(n_prof):
+        r, c, h, w = my_tiles[k]
+        ctx.process_tile_dev(rgbs[k], h, w, params, None, None, None, feats[k], counts[k:k + 1])
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    prof_px = sum(h * w for (_, _, h, w) in my_tiles[:n_prof])
+    stage_ms = {s: v[0] for s, v in prof.items()}
+    tot_stage = sum(stage_ms.values())
+    dom = max(stage_ms, key=stage_ms.get)
+    peak, peak_kind = measured_peaks()
+
+    def roof(stage):
+        calls = prof[stage][1]
+        avg_ms = stage_ms[stage] / max(calls, 1)
+        bytes_per_launch = STAGE_BYTES_PER_PX[stage] * prof_px / max(calls, 1)
+        ach = bytes_per_launch / (avg_ms / 1e3) / 1e9
+        return {"stage": stage, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                "peak_kind": peak_kind, "avg_launch_ms": round(avg_ms, 4),
+                "algorithmic_bytes_per_launch": int(bytes_per_launch),
+                "share_of_stage_time": round(stage_ms[stage] / tot_stage, 4)}
+
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    roofline = roof(dom)
+    roof_stream = roof("colordeconv")
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as f:
+            tr = json.load(f)
+        for rf in (roofline, roof_stream):
+            if rf["stage"] in tr:
+                rf["traffic"] = tr[rf["stage"]]
+
+    # ---- e2e through the C-ABI host-buffer entry point (pinned host tiles)
+    e2e = None
+    if not args.no_e2e:
+        pool = min(T, 8)
+        host = []
+        for k in range(pool):
+            r, c, h, w = my_tiles[k]
+            hb = torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True)
+            hb.copy_(rgbs[k].cpu())
+            host.append(hb.numpy())
+        fbufs = [torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy()
+                 for _ in range(S)]
+        d2h = [0] * S
+        e2e_tiles = list(range(T))
+
+        def worker(si, ks):
+            cx = ctxs[si]
+            cx.set_stream(0)
+            for k in ks:
+                r, c, h, w = my_tiles[k]
+                rgb = host[k % pool]
+                # rtg_process_tile: H2D RGB, o1..o9, D2H of the feature table
+                n = ctypes_process(cx, rgb, h, w, fbufs[si])
+                d2h[si] += n * rtg.NUM_FEATURES * 4 + 4
+
+        def run_e2e():
+            th = [threading.Thread(target=worker, args=(si, e2e_tiles[si::S])) for si in range(S)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+
+        run_e2e()  # warm-up
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(S):
+            d2h[i] = 0
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(args.e2e_steps):
+            run_e2e()
+        e1.record(cur)
+        torch.cuda.synchronize()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e_ms = float(ems.item())
+        e2e = {"value": round(px_rank * world * args.e2e_steps / (e_ms / 1e3) / 1e6, 3),
+               "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(3 * px_rank),
+               "d2h_bytes_per_step": int(sum(d2h) / args.e2e_steps),
+               "steps": args.e2e_steps,
+               "path": "rtg_process_tile (host buffers, pinned; H2D RGB + D2H features)",
+               "host_tile_pool": pool}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        n_s = max(1, min(cores, 32))
+        v, dt, px = cpu_oracle_sample(n_s, cores)
+        cpu = {"value": round(v, 3), "unit": "Mpixel/s", "cores": cores, "kind": "port",
+               "sample": f"{n_s} WSI tiles through the oracle (o1..o9) on {cores} threads, "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded H&E-like tiles generated on device)",
+            "config": {"workload": "C5: 100k x 100k synthetic WSI as 4K tiles "
+                                   "(partition_regular: 576 full, 48 edge, 1 corner), "
+                                   "bag of tasks, per-step NCCL gather of feature tables",
+                       "tiles_per_rank_per_step": T, "streams_per_gpu": S,
+                       "pixels_per_step": px_rank * world,
+                       "l2": "inputs larger than L2 (48 MiB RGB + ~400 MiB planes per tile)",
+                       "feature_rows_per_step": int(total_rows / max(args.steps, 1))},
+            "roofline": roofline,
+            "roofline_streaming": roof_stream,
+            "stage_ms_per_tile": {s: round(v / n_prof, 4) for s, v in stage_ms.items()},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(gpu_launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    for c in ctxs:
+        c.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_process(ctx, rgb, h, w, fbuf):
+    import ctypes
+    from paper_1405_7958_b200 import rtg
+    n = ctypes.c_int32(0)
+    rtg.check(ctx.lib.rtg_process_tile(ctx.handle, rgb.ctypes.data, h, w, 3 * w,
+                                       ctypes.byref(_PARAMS()), None, None, None,
+                                       fbuf.ctypes.data, fbuf.shape[0], ctypes.byref(n)))
+    return n.value
+
+
+_P = None
+
+
+def _PARAMS():
+    global _P
+    if _P is None:
+        from paper_1405_7958_b200 import rtg
+        _P = rtg.default_params()
+    return _P
+
+
+if __name__ == "__main__":
+    main()

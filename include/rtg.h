@@ -142,6 +142,27 @@ int rtg_ctx_sync(rtg_ctx* ctx);
  * visits, out[3] = watershed markers.  Synchronises. */
 int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]);
 
+/* Stage timing (CUDA events on the ctx stream, bracketing each stage of the
+ * pipeline).  rtg_ctx_profile_read synchronises, returns the accumulated
+ * milliseconds and call counts per stage since the last read, and resets. */
+enum rtg_stage {
+  RTG_STAGE_COLORDECONV = 0, /* k_colordeconv_vec (o1+o2)                  */
+  RTG_STAGE_RECON = 1,       /* IWPP reconstruction (o3)                  */
+  RTG_STAGE_FILL_HOLES = 2,  /* candidate threshold + IWPP fill (o4)      */
+  RTG_STAGE_AREA = 3,        /* union-find CCL + area filter (o5)         */
+  RTG_STAGE_EDT = 4,         /* exact EDT (o6)                            */
+  RTG_STAGE_MARKERS = 5,     /* HMAX + regional-maxima IWPP (o6)          */
+  RTG_STAGE_WATERSHED = 6,   /* arrows, marker CCL, plateaus, basins (o7) */
+  RTG_STAGE_LABEL = 7,       /* final CCL + canonical relabel (o8)        */
+  RTG_STAGE_FEATURES = 8,    /* two-step features (o9)                    */
+  RTG_NUM_STAGES = 9
+};
+int rtg_ctx_profile(rtg_ctx* ctx, int enable);
+int rtg_ctx_profile_read(rtg_ctx* ctx, double ms[RTG_NUM_STAGES],
+                         int64_t calls[RTG_NUM_STAGES]);
+/* Kernels launched through this ctx since creation (host-side counter). */
+int rtg_ctx_launches(rtg_ctx* ctx, int64_t* out);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* rtg_last_error(void);
 

@@ -26,8 +26,10 @@ int cuda_fail(cudaError_t e, const char* what);
     if (e_ != cudaSuccess) return ::rtg::cuda_fail(e_, #call); \
   } while (0)
 
+// every kernel launch site goes through this (counts launches per ctx)
 #define RTG_LAUNCH(what)                                          \
   do {                                                            \
+    ++ctx->launches;                                              \
     cudaError_t e_ = cudaGetLastError();                          \
     if (e_ != cudaSuccess) return ::rtg::cuda_fail(e_, what);     \
   } while (0)
@@ -109,6 +111,15 @@ struct rtg_ctx {
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
   rtg::TileQueue tq{};
   rtg::FeatureAcc acc{};
+
+  // host-side instrumentation
+  int64_t launches = 0;           // kernels launched through this ctx
+  bool prof = false;              // stage timing with CUDA events
+  cudaEvent_t* prof_ev = nullptr; // ring of boundary events
+  int32_t* prof_stage = nullptr;  // stage id that starts at each event (-1 = end)
+  int prof_cap = 0, prof_used = 0;
+  double prof_ms[RTG_NUM_STAGES] = {};
+  int64_t prof_calls[RTG_NUM_STAGES] = {};
 };
 
 namespace rtg {
@@ -119,6 +130,9 @@ constexpr int kScanChunk = 4096;
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w);
+// Stage boundary for rtg_ctx_profile (no-op unless profiling is enabled):
+// stage >= 0 starts that stage, -1 closes the current one.
+void prof_mark(rtg_ctx* ctx, int stage);
 void hema_lut(const rtg_params* p, HemaLut* lut);
 
 // ---- launchers (one translation unit each) ---------------------------------

@@ -42,6 +42,13 @@ int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w) {
   return RTG_OK;
 }
 
+void prof_mark(rtg_ctx* ctx, int stage) {
+  if (!ctx->prof || ctx->prof_used >= ctx->prof_cap) return;
+  const int k = ctx->prof_used++;
+  cudaEventRecord(ctx->prof_ev[k], ctx->stream);
+  ctx->prof_stage[k] = stage;
+}
+
 namespace {
 
 int check_params(const rtg_params* p) {
@@ -86,22 +93,32 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   int32_t* labels = d_labels ? d_labels : ctx->labels;
   int32_t* n_out = d_n ? d_n : ctx->misc;
   // o1+o2: hematoxylin, HMAX marker (in place of the reconstruction), tissue
+  prof_mark(ctx, RTG_STAGE_COLORDECONV);
   RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, ctx->recon, ctx->tissue));
   // o3 ReconToNuclei
+  prof_mark(ctx, RTG_STAGE_RECON);
   RTG_TRY(iwpp_recon_u8(ctx, ctx->recon, hema, h, w, p->recon_conn));
+  // o4 FillHoles of the nucleus candidates
+  prof_mark(ctx, RTG_STAGE_FILL_HOLES);
   RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
-  // o4 FillHoles
   RTG_TRY(iwpp_fill_holes(ctx, ctx->m1, ctx->m2, h, w, ctx->m2));
   // o5 AreaThreshold
+  prof_mark(ctx, RTG_STAGE_AREA);
   RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a));
   RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
-  // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer)
+  // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
+  // watershed() marks its own EDT / MARKERS / WATERSHED stages
   RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels));
   // o8 BWLabel (canonical)
+  prof_mark(ctx, RTG_STAGE_LABEL);
   RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a));
   RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out));
   // o9 features
-  if (with_features) RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features));
+  if (with_features) {
+    prof_mark(ctx, RTG_STAGE_FEATURES);
+    RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features));
+  }
+  prof_mark(ctx, -1);
   return RTG_OK;
 }
 
@@ -247,6 +264,11 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->prof_ev) {
+    for (int i = 0; i < c->prof_cap; ++i) cudaEventDestroy(c->prof_ev[i]);
+    delete[] c->prof_ev;
+    delete[] c->prof_stage;
+  }
   delete c;
   return RTG_OK;
 }
@@ -290,6 +312,52 @@ int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]) {
   out[0] = misc[0];
   out[1] = st[1];
   out[2] = misc[1];
+  return RTG_OK;
+}
+
+int rtg_ctx_profile(rtg_ctx* ctx, int enable) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  if (enable && !ctx->prof_ev) {
+    ctx->prof_cap = 1 << 15;
+    ctx->prof_ev = new cudaEvent_t[ctx->prof_cap];
+    ctx->prof_stage = new int32_t[ctx->prof_cap];
+    for (int i = 0; i < ctx->prof_cap; ++i) RTG_CUDA(cudaEventCreate(&ctx->prof_ev[i]));
+  }
+  ctx->prof = enable != 0;
+  ctx->prof_used = 0;
+  for (int i = 0; i < RTG_NUM_STAGES; ++i) {
+    ctx->prof_ms[i] = 0.0;
+    ctx->prof_calls[i] = 0;
+  }
+  return RTG_OK;
+}
+
+int rtg_ctx_profile_read(rtg_ctx* ctx, double ms[RTG_NUM_STAGES], int64_t calls[RTG_NUM_STAGES]) {
+  if (!ctx || !ms || !calls) return fail(RTG_ERR_INVALID_ARG, "null argument");
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k + 1 < ctx->prof_used; ++k) {
+    const int st = ctx->prof_stage[k];
+    if (st < 0) continue;
+    float e = 0.f;
+    RTG_CUDA(cudaEventElapsedTime(&e, ctx->prof_ev[k], ctx->prof_ev[k + 1]));
+    ctx->prof_ms[st] += e;
+    ctx->prof_calls[st] += 1;
+  }
+  for (int i = 0; i < RTG_NUM_STAGES; ++i) {
+    ms[i] = ctx->prof_ms[i];
+    calls[i] = ctx->prof_calls[i];
+    ctx->prof_ms[i] = 0.0;
+    ctx->prof_calls[i] = 0;
+  }
+  ctx->prof_used = 0;
+  return RTG_OK;
+}
+
+int rtg_ctx_launches(rtg_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
+  *out = ctx->launches;
   return RTG_OK;
 }
 

@@ -1,0 +1,74 @@
+// The per-tile segmentation + feature stage as a Region Templates stage
+// whose task has a B200 variant calling the C-ABI (include/rtg.h).
+//
+// This fills the slot the reference leaves empty: its simulator materialises
+// stage outputs with a constant payload (src/sim.cpp:557-582) and charges
+// virtual time in start_task (src/sim.cpp:630-685).  Region naming follows the
+// paper's application: "RGB" input, "Mask" output (
+// test_runtime.cpp:525-526 uses img::rgb -> img::mask).
+#pragma once
+
+#include <memory>
+
+#include "rt/runtime.hpp"
+#include "rtg.h"
+
+namespace rt {
+
+// Maps an rtg_status onto the rt::Error taxonomy (the same pattern as the
+// reference's throw_wire_error, src/service.cpp:181-219).
+[[noreturn]] void throw_rtg_error(int status);
+inline void rtg_check(int status) {
+  if (status != RTG_OK) throw_rtg_error(status);
+}
+
+// RAII owner of one rtg_ctx (device arena + stream) — one per GPU worker.
+class GpuDevice {
+ public:
+  explicit GpuDevice(int device, std::int64_t max_h = 4096, std::int64_t max_w = 4096,
+                     std::int32_t max_objects = 1 << 16);
+  ~GpuDevice();
+  GpuDevice(const GpuDevice&) = delete;
+  GpuDevice& operator=(const GpuDevice&) = delete;
+  rtg_ctx* ctx() const { return ctx_; }
+  int device() const { return device_; }
+  std::int32_t max_objects() const { return max_objects_; }
+
+ private:
+  rtg_ctx* ctx_ = nullptr;
+  int device_ = 0;
+  std::int32_t max_objects_ = 0;
+};
+
+struct SegmentationRegions {
+  DataRegionId rgb{"img", "RGB", "raw", 0, 0};
+  DataRegionId mask{"img", "Mask", "label", 0, 0};
+  DataRegionId labels{"img", "Labels", "label", 0, 0};
+  DataRegionId features{"img", "Features", "table", 0, 0};
+  std::string binding = "store";
+};
+
+// Task name of the stage's single fine-grain task in a VariantRegistry.
+inline constexpr const char* kSegmentFeaturesTask = "segment_features";
+
+// Registers the B200 variant of "segment_features".  The body reads the
+// tile from the worker's local template, runs rtg_process_tile on the
+// worker's GpuDevice and installs Mask (Dense2D u8), Labels (Dense2D i32) and
+// Features (Dense2D f32, n x RTG_NUM_FEATURES) into the local template.
+void register_gpu_segmentation(VariantRegistry& reg, const SegmentationRegions& ids,
+                               const rtg_params& params);
+
+// A stage over one tile: descriptors RGB (Dense3D <y0,x0,0;y1,x1,2>) in,
+// Mask / Labels / Features out; body expands to one "segment_features" task
+// with whatever variants `reg` holds (kGpuOnly for the product registry).
+StageInstance make_segmentation_stage(std::uint64_t stage_id, const BoundingBox& tile,
+                                      const SegmentationRegions& ids,
+                                      std::shared_ptr<const VariantRegistry> reg);
+
+// Output installation helper shared by variants: replaces the metadata-only
+// shell worker_prepare created with a typed, zero-filled dense region that
+// keeps the shell's io mode and storage binding.
+DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, RegionKind kind,
+                           ElementKind elem, const BoundingBox& box);
+
+}  // namespace rt

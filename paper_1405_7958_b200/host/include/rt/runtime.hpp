@@ -1,0 +1,212 @@
+// Stage/task dataflow, worker scheduler (variant surface), storage and the
+// executor that runs stage bodies on CPU slots or B200 contexts.
+//
+// API mirror of the reference's runtime surface (re-implemented):
+//   StorageBackend / StorageRegistry / Completion  include/rt/storage.hpp:34-162
+//   TaskNode / TaskVariants / DeviceKind / WrmState  include/rt/wrm.hpp:29-137
+//     (FCFS and PATS device picks, src/wrm.cpp:246-273; DL reuse / prefetch
+//     model are out of scope for this hot-path build)
+//   RegionDescriptor / StageInstance / ManagerState / worker_prepare /
+//   stage_finalize                                   include/rt/dataflow.hpp:33-114
+// New here: VariantRegistry (function-variant registration by name) and
+// WorkerContext (what a TaskNode::body reaches while it runs: the stage's
+// local RegionTemplate and the device the WRM picked).
+#pragma once
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "rt/region.hpp"
+
+namespace rt {
+
+// ---- storage ------------------------------------------------------------------
+// Completion of a staging operation (always complete for the in-memory store).
+class Completion {
+ public:
+  Completion() = default;
+  void wait() const {}
+  bool ready() const { return true; }
+};
+
+class StorageBackend {
+ public:
+  virtual ~StorageBackend() = default;
+  virtual const std::string& name() const = 0;
+  // Persists every chunk of a materialised region (last writer wins).
+  virtual Completion stage_region(const DataRegion& region, int origin_node) = 0;
+  // Assembles the query box from staged chunks; NotFoundError when any cell
+  // was never written.
+  virtual DataRegion read_region(const DataRegionId& id, const BoundingBox& query) = 0;
+};
+
+// Process-local store keyed by region tuple; thread-safe.
+class MemoryStore : public StorageBackend {
+ public:
+  explicit MemoryStore(std::string name) : name_(std::move(name)) {}
+  const std::string& name() const override { return name_; }
+  Completion stage_region(const DataRegion& region, int origin_node) override;
+  DataRegion read_region(const DataRegionId& id, const BoundingBox& query) override;
+
+ private:
+  struct Piece {
+    BoundingBox box;
+    RegionKind kind;
+    ElementKind elem;
+    std::vector<std::uint8_t> payload;
+  };
+  std::string name_;
+  std::mutex mu_;
+  std::map<DataRegionId, std::vector<Piece>> pieces_;
+};
+
+class StorageRegistry {
+ public:
+  void add(std::shared_ptr<StorageBackend> b);
+  StorageBackend& at(const std::string& name) const;
+
+ private:
+  std::map<std::string, std::shared_ptr<StorageBackend>> backends_;
+};
+
+// ---- tasks and the worker scheduler ------------------------------------------------
+enum class DeviceKind : std::uint8_t { kCpu = 0, kGpu = 1 };
+enum class TaskVariants : std::uint8_t { kCpuOnly = 0, kGpuOnly = 1, kBoth = 2 };
+enum class SchedulerKind : std::uint8_t { kFcfs = 0, kPats = 1 };
+
+struct TaskNode {
+  std::uint64_t task_id = 0;
+  std::set<std::uint64_t> deps;
+  TaskVariants variants = TaskVariants::kBoth;
+  // GPU acceleration vs one CPU core; required exactly when variants == kBoth.
+  std::optional<double> speedup_estimate;
+  double cost_cpu = 1.0;
+  std::uint64_t stage_id = 0;
+  // Runs the task; reaches its data through worker_context().
+  std::function<void()> body;
+};
+
+double effective_speedup(const TaskNode& t);
+bool device_compatible(const TaskNode& t, DeviceKind d);
+
+class WrmState {
+ public:
+  explicit WrmState(SchedulerKind s = SchedulerKind::kFcfs) : sched_(s) {}
+  void submit(std::vector<TaskNode> tasks);
+  std::optional<std::uint64_t> next(DeviceKind device);
+  std::vector<std::uint64_t> complete(std::uint64_t task_id);
+  const TaskNode& task(std::uint64_t id) const;
+  bool all_done() const;
+  std::size_t ready_count() const { return ready_.size(); }
+
+ private:
+  struct Entry {
+    TaskNode node;
+    int state = 0;  // 0 pending, 1 ready, 2 running, 3 done
+    std::size_t remaining = 0;
+    std::uint64_t seq = 0;
+  };
+  SchedulerKind sched_;
+  std::uint64_t seq_ = 0;
+  std::map<std::uint64_t, Entry> tasks_;
+  std::map<std::uint64_t, std::vector<std::uint64_t>> dependents_;
+  std::vector<std::uint64_t> ready_;  // readiness order
+};
+
+// ---- function variants ----------------------------------------------------------------
+// name -> {CPU implementation, GPU implementation, speedup estimate}.
+// make_task() derives TaskNode::variants from which implementations exist
+// and dispatches body() on the device the executor assigned.
+class VariantRegistry {
+ public:
+  using Fn = std::function<void()>;
+  void register_variant(const std::string& name, DeviceKind device, Fn fn);
+  void set_speedup(const std::string& name, double s);
+  bool has(const std::string& name, DeviceKind device) const;
+  TaskNode make_task(const std::string& name, std::uint64_t task_id, std::uint64_t stage_id) const;
+
+ private:
+  struct Entry {
+    Fn cpu, gpu;
+    std::optional<double> speedup;
+  };
+  std::map<std::string, Entry> entries_;
+};
+
+class GpuDevice;  // rt/rtg_stage.hpp
+
+// What a running TaskNode::body can see (set by the executor per task).
+struct WorkerContext {
+  RegionTemplate* local = nullptr;
+  DeviceKind device = DeviceKind::kCpu;
+  GpuDevice* gpu = nullptr;
+  int worker = 0;
+};
+WorkerContext& worker_context();
+
+// ---- dataflow ---------------------------------------------------------------------------
+struct RegionDescriptor {
+  DataRegionId id;
+  BoundingBox query;
+  IoMode io_mode = IoMode::kInput;
+  std::string storage_binding;
+  bool lazy = false;
+};
+
+struct StageInstance {
+  std::uint64_t stage_id = 0;
+  std::string stage_kind;
+  std::vector<RegionDescriptor> region_descriptors;
+  std::set<std::uint64_t> deps;
+  std::function<std::vector<TaskNode>()> body;
+};
+
+class ManagerState {
+ public:
+  void add_stage(StageInstance stage);
+  std::optional<std::uint64_t> dispatch(int worker);
+  std::vector<std::uint64_t> stage_complete(std::uint64_t stage_id);
+  const StageInstance& stage(std::uint64_t id) const;
+  std::size_t size() const { return stages_.size(); }
+  bool all_done() const { return done_ == stages_.size(); }
+
+ private:
+  struct E {
+    StageInstance stage;
+    bool assigned = false, done = false;
+  };
+  bool eligible(const E& e) const;
+  std::map<std::uint64_t, E> stages_;
+  std::vector<std::uint64_t> order_;
+  std::size_t done_ = 0;
+};
+
+// Reads non-lazy inputs into a fresh local template; outputs are created
+// metadata-only (Dense2D/U8 shells, as the reference does) — stage bodies
+// replace them with correctly typed regions.
+RegionTemplate worker_prepare(const StageInstance& stage, StorageRegistry& storage);
+// Stages materialised outputs and drops inputs; completions in descriptor order.
+std::vector<Completion> stage_finalize(RegionTemplate& local, const StageInstance& stage,
+                                       StorageRegistry& storage, int origin_node);
+
+// ---- executor ------------------------------------------------------------------------------
+// Demand-driven loop over the manager's stages (the real counterpart of the
+// simulator's start_task slot, /root/reference/proj/src/sim.cpp:630-685):
+// prepare -> expand body -> WRM picks device per task -> run -> finalize.
+struct ExecutorConfig {
+  SchedulerKind scheduler = SchedulerKind::kPats;
+  std::vector<GpuDevice*> gpus;  // empty: CPU only
+};
+struct ExecutorStats {
+  std::size_t stages = 0, cpu_tasks = 0, gpu_tasks = 0;
+};
+ExecutorStats run_stages(ManagerState& manager, StorageRegistry& storage,
+                         const ExecutorConfig& cfg);
+
+}  // namespace rt

@@ -1,0 +1,282 @@
+// Region Templates containers (see rt/region.hpp for the reference anchors).
+#include "rt/region.hpp"
+
+#include <algorithm>
+#include <sstream>
+
+namespace rt {
+
+// ---- BoundingBox ------------------------------------------------------------
+
+BoundingBox::BoundingBox(std::initializer_list<std::int64_t> lo,
+                         std::initializer_list<std::int64_t> hi) {
+  if (lo.size() != hi.size()) throw DimensionError("lo/hi rank mismatch");
+  if (lo.size() == 0 || lo.size() > kMaxDims) throw DimensionError("box rank must be 1..4");
+  dims_ = int(lo.size());
+  std::copy(lo.begin(), lo.end(), lo_.begin());
+  std::copy(hi.begin(), hi.end(), hi_.begin());
+  for (int a = 0; a < dims_; ++a)
+    if (lo_[a] > hi_[a]) throw DimensionError("box lo exceeds hi on axis " + std::to_string(a));
+}
+
+BoundingBox::BoundingBox(int dims, const std::int64_t* lo, const std::int64_t* hi) {
+  if (dims <= 0 || dims > kMaxDims) throw DimensionError("box rank must be 1..4");
+  dims_ = dims;
+  for (int a = 0; a < dims; ++a) {
+    lo_[a] = lo[a];
+    hi_[a] = hi[a];
+    if (lo_[a] > hi_[a]) throw DimensionError("box lo exceeds hi on axis " + std::to_string(a));
+  }
+}
+
+int BoundingBox::axis(int a) const {
+  if (a < 0 || a >= dims_) throw DimensionError("axis out of range");
+  return a;
+}
+
+void BoundingBox::same_dims(const BoundingBox& o) const {
+  if (dims_ != o.dims_) throw DimensionError("combining boxes of different rank");
+}
+
+std::int64_t BoundingBox::volume() const {
+  if (empty()) return 0;
+  std::int64_t v = 1;
+  for (int a = 0; a < dims_; ++a) v *= hi_[a] - lo_[a] + 1;
+  return v;
+}
+
+bool BoundingBox::contains(const BoundingBox& o) const {
+  if (empty() || o.empty()) return false;
+  same_dims(o);
+  for (int a = 0; a < dims_; ++a)
+    if (o.lo_[a] < lo_[a] || o.hi_[a] > hi_[a]) return false;
+  return true;
+}
+
+BoundingBox BoundingBox::unioned(const BoundingBox& o) const {
+  if (empty()) return o;
+  if (o.empty()) return *this;
+  same_dims(o);
+  BoundingBox r = *this;
+  for (int a = 0; a < dims_; ++a) {
+    r.lo_[a] = std::min(lo_[a], o.lo_[a]);
+    r.hi_[a] = std::max(hi_[a], o.hi_[a]);
+  }
+  return r;
+}
+
+std::optional<BoundingBox> BoundingBox::intersected(const BoundingBox& o) const {
+  if (empty() || o.empty()) return std::nullopt;
+  same_dims(o);
+  BoundingBox r = *this;
+  for (int a = 0; a < dims_; ++a) {
+    r.lo_[a] = std::max(lo_[a], o.lo_[a]);
+    r.hi_[a] = std::min(hi_[a], o.hi_[a]);
+    if (r.lo_[a] > r.hi_[a]) return std::nullopt;
+  }
+  return r;
+}
+
+bool BoundingBox::operator==(const BoundingBox& o) const {
+  if (dims_ != o.dims_) return false;
+  for (int a = 0; a < dims_; ++a)
+    if (lo_[a] != o.lo_[a] || hi_[a] != o.hi_[a]) return false;
+  return true;
+}
+
+bool BoundingBox::operator<(const BoundingBox& o) const {
+  if (dims_ != o.dims_) return dims_ < o.dims_;
+  for (int a = 0; a < dims_; ++a) {
+    if (lo_[a] != o.lo_[a]) return lo_[a] < o.lo_[a];
+  }
+  for (int a = 0; a < dims_; ++a) {
+    if (hi_[a] != o.hi_[a]) return hi_[a] < o.hi_[a];
+  }
+  return false;
+}
+
+std::string BoundingBox::to_string() const {
+  if (empty()) return "<empty>";
+  std::ostringstream s;
+  s << '<';
+  for (int a = 0; a < dims_; ++a) s << (a ? "," : "") << lo_[a];
+  s << ';';
+  for (int a = 0; a < dims_; ++a) s << (a ? "," : "") << hi_[a];
+  s << '>';
+  return s.str();
+}
+
+// ---- element kinds ------------------------------------------------------------
+
+std::size_t element_size(ElementKind k) {
+  switch (k) {
+    case ElementKind::kU8: return 1;
+    case ElementKind::kU16: return 2;
+    case ElementKind::kI32: return 4;
+    case ElementKind::kF32: return 4;
+    case ElementKind::kF64: return 8;
+  }
+  throw ConfigError("unknown element kind");
+}
+
+bool is_dense(RegionKind k) {
+  return k == RegionKind::kDense1D || k == RegionKind::kDense2D || k == RegionKind::kDense3D;
+}
+
+int dense_rank(RegionKind k) {
+  switch (k) {
+    case RegionKind::kDense1D: return 1;
+    case RegionKind::kDense2D: return 2;
+    case RegionKind::kDense3D: return 3;
+    default: return 0;
+  }
+}
+
+std::string DataRegionId::to_string() const {
+  return name() + "[" + type_tag + ",t=" + std::to_string(timestamp) + ",v=" +
+         std::to_string(version) + "]";
+}
+
+// ---- DataRegion ---------------------------------------------------------------
+
+DataRegion::DataRegion(DataRegionId id, RegionKind kind, ElementKind element_kind,
+                       BoundingBox bbox)
+    : id_(std::move(id)), kind_(kind), element_kind_(element_kind), bbox_(bbox), roi_(bbox) {
+  // dense boxes carry the kind's rank, optionally plus a trailing time axis
+  if (is_dense(kind_) && !bbox_.empty() && bbox_.dims() != dense_rank(kind_) &&
+      bbox_.dims() != dense_rank(kind_) + 1)
+    throw DimensionError("region box rank " + std::to_string(bbox_.dims()) +
+                         " does not match its kind");
+}
+
+void DataRegion::set_roi(const BoundingBox& roi) {
+  if (!roi.empty() && (bbox_.empty() || !bbox_.contains(roi)))
+    throw DimensionError("roi must lie inside the region box");
+  roi_ = roi;
+}
+
+Chunk& DataRegion::put_chunk(const BoundingBox& box, std::vector<std::uint8_t> payload) {
+  if (box.empty()) throw DimensionError("empty chunk box");
+  if (bbox_.empty() || !bbox_.contains(box))
+    throw DimensionError("chunk " + box.to_string() + " escapes region " + bbox_.to_string());
+  if (is_dense(kind_) &&
+      payload.size() != std::uint64_t(box.volume()) * element_size(element_kind_))
+    throw DimensionError("dense chunk payload length " + std::to_string(payload.size()) +
+                         " != volume * element size");
+  auto [it, fresh] = chunks_.try_emplace(box);
+  if (fresh) it->second.chunk_id = next_chunk_id_++;
+  it->second.bbox = box;
+  it->second.element_kind = element_kind_;
+  it->second.payload = std::move(payload);
+  materialized_ = true;
+  return it->second;
+}
+
+const Chunk* DataRegion::find_chunk(const BoundingBox& box) const {
+  auto it = chunks_.find(box);
+  return it == chunks_.end() ? nullptr : &it->second;
+}
+
+Chunk* DataRegion::find_chunk(const BoundingBox& box) {
+  auto it = chunks_.find(box);
+  return it == chunks_.end() ? nullptr : &it->second;
+}
+
+void DataRegion::drop_payload() {
+  chunks_.clear();
+  materialized_ = false;
+}
+
+std::uint64_t DataRegion::payload_bytes() const {
+  std::uint64_t n = 0;
+  for (const auto& [b, c] : chunks_) n += c.payload.size();
+  return n;
+}
+
+bool DataRegion::operator==(const DataRegion& o) const {
+  if (!(id_ == o.id_) || kind_ != o.kind_ || element_kind_ != o.element_kind_ ||
+      bbox_ != o.bbox_ || chunks_.size() != o.chunks_.size())
+    return false;
+  auto a = chunks_.begin();
+  auto b = o.chunks_.begin();
+  for (; a != chunks_.end(); ++a, ++b)
+    if (a->first != b->first || a->second.payload != b->second.payload) return false;
+  return true;
+}
+
+void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
+                      std::span<const std::uint8_t> src, const BoundingBox& src_box,
+                      std::size_t elem) {
+  const auto ov = dst_box.intersected(src_box);
+  if (!ov) return;
+  const int d = ov->dims();
+  const std::size_t run = std::size_t(ov->extent(d - 1)) * elem;
+  // offsets of the overlap's first element along every axis, then walk rows
+  std::array<std::int64_t, BoundingBox::kMaxDims> p{};
+  for (int a = 0; a < d; ++a) p[a] = ov->lo(a);
+  auto offset = [&](const BoundingBox& b) {
+    std::int64_t o = 0;
+    for (int a = 0; a < d; ++a) o = o * b.extent(a) + (p[a] - b.lo(a));
+    return std::size_t(o) * elem;
+  };
+  for (;;) {
+    std::memcpy(dst.data() + offset(dst_box), src.data() + offset(src_box), run);
+    int a = d - 2;
+    while (a >= 0 && ++p[a] > ov->hi(a)) {
+      p[a] = ov->lo(a);
+      --a;
+    }
+    if (a < 0) break;
+  }
+}
+
+// ---- RegionTemplate -------------------------------------------------------------
+
+DataRegion& RegionTemplate::insert_data_region(DataRegion region) {
+  const DataRegionId id = region.id();
+  if (regions_.count(id)) throw DuplicateRegionError("duplicate region " + id.to_string());
+  bbox_ = bbox_.empty() ? region.bbox()
+          : region.bbox().empty() || region.bbox().dims() != bbox_.dims()
+              ? bbox_
+              : bbox_.unioned(region.bbox());
+  return regions_.emplace(id, std::move(region)).first->second;
+}
+
+const DataRegion* RegionTemplate::get_data_region(const DataRegionId& id) const {
+  auto it = regions_.find(id);
+  return it == regions_.end() ? nullptr : &it->second;
+}
+
+DataRegion* RegionTemplate::get_data_region(const DataRegionId& id) {
+  auto it = regions_.find(id);
+  return it == regions_.end() ? nullptr : &it->second;
+}
+
+const DataRegion* RegionTemplate::get_newest(const std::string& ns, const std::string& key,
+                                             const std::string& type_tag) const {
+  const DataRegion* best = nullptr;
+  for (const auto& [id, r] : regions_) {
+    if (id.ns != ns || id.key != key || id.type_tag != type_tag) continue;
+    if (!best || std::tie(id.timestamp, id.version) >
+                     std::tie(best->id().timestamp, best->id().version))
+      best = &r;
+  }
+  return best;
+}
+
+bool RegionTemplate::remove_data_region(const DataRegionId& id) {
+  if (!regions_.erase(id)) return false;
+  refold();
+  return true;
+}
+
+void RegionTemplate::refold() {
+  bbox_ = BoundingBox();
+  for (const auto& [id, r] : regions_) {
+    if (r.bbox().empty()) continue;
+    if (bbox_.empty()) bbox_ = r.bbox();
+    else if (bbox_.dims() == r.bbox().dims()) bbox_ = bbox_.unioned(r.bbox());
+  }
+}
+
+}  // namespace rt

@@ -38,8 +38,11 @@ SYMBOLS = [
     "rtg_colordeconv_dev", "rtg_recon_u8_dev", "rtg_recon_u16_dev",
     "rtg_fill_holes_dev", "rtg_bwlabel_dev", "rtg_area_threshold_dev",
     "rtg_edt_dev", "rtg_watershed_dev", "rtg_features_dev",
-    "rtg_synth_tile_host", "rtg_synth_tile_dev",
+    "rtg_synth_tile_host", "rtg_synth_tile_dev", "rtg_ctx_profile",
+    "rtg_ctx_profile_read", "rtg_ctx_launches",
 ]
+STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
+          "label", "features"]
 
 
 class Error(RuntimeError):
@@ -151,6 +154,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_features_dev": [vp, vp, vp, i64, i64, vp, vp],
         "rtg_synth_tile_host": [u64, i64, i64, i64, i64, vp],
         "rtg_synth_tile_dev": [vp, u64, i64, i64, i64, i64, vp],
+        "rtg_ctx_profile": [vp, ctypes.c_int],
+        "rtg_ctx_profile_read": [vp, vp, vp],
+        "rtg_ctx_launches": [vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -241,6 +247,21 @@ class Context:
         out = (ctypes.c_int64 * 8)()
         check(self.lib.rtg_ctx_stats(self.handle, out))
         return list(out)
+
+    def profile(self, enable: bool = True) -> None:
+        check(self.lib.rtg_ctx_profile(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
+        """{stage: (total_ms, calls)} since the last read (synchronises)."""
+        ms = (ctypes.c_double * len(STAGES))()
+        calls = (ctypes.c_int64 * len(STAGES))()
+        check(self.lib.rtg_ctx_profile_read(self.handle, ms, calls))
+        return {s: (ms[i], calls[i]) for i, s in enumerate(STAGES)}
+
+    def launches(self) -> int:
+        n = ctypes.c_int64(0)
+        check(self.lib.rtg_ctx_launches(self.handle, ctypes.byref(n)))
+        return n.value
 
     # -- host-buffer entry points (synchronous) -------------------------------
     def process_tile(self, rgb: np.ndarray, params: Optional[Params] = None,

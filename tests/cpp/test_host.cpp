@@ -1,0 +1,324 @@
+// Framework-free checks of the C++ Region Templates host layer, in the style
+// of the reference's acceptance gate (tests/test_acceptance.cpp: one PASS/FAIL
+// line per check).  `test_host` runs the CPU checks; `test_host --gpu` adds the
+// stage executed through StageInstance -> WRM -> TaskNode::body -> C-ABI on a
+// B200, checked bit-exactly against the oracle (linked here as the checker).
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../oracle/rtg_oracle.h"
+#include "rt/region.hpp"
+#include "rt/rtg_stage.hpp"
+#include "rt/runtime.hpp"
+
+using namespace rt;
+
+namespace {
+
+int g_fail = 0;
+
+void check(const std::string& name, const std::function<void()>& fn) {
+  try {
+    fn();
+    std::printf("PASS %s\n", name.c_str());
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::printf("FAIL %s: %s\n", name.c_str(), e.what());
+  }
+}
+
+void require(bool ok, const std::string& what) {
+  if (!ok) throw std::runtime_error(what);
+}
+
+template <typename E>
+void require_throws(const std::function<void()>& fn, const std::string& what) {
+  try {
+    fn();
+  } catch (const E&) {
+    return;
+  }
+  throw std::runtime_error("expected exception: " + what);
+}
+
+BoundingBox box2(std::int64_t a, std::int64_t b, std::int64_t c, std::int64_t d) {
+  return BoundingBox({a, b}, {c, d});
+}
+
+DataRegion u8_region(const std::string& key, const BoundingBox& b, std::int64_t ts = 0,
+                     std::int64_t ver = 0) {
+  return DataRegion(DataRegionId{"t", key, "raw", ts, ver}, RegionKind::kDense2D,
+                    ElementKind::kU8, b);
+}
+
+// ---------------------------------------------------------------- containers
+
+void containers() {
+  check("copy_box_overlap KAT (reference test_region.cpp:277-285 restated)", [] {
+    std::vector<std::uint8_t> src(25), dst(9, 0);
+    for (int i = 0; i < 25; ++i) src[i] = std::uint8_t(i + 1);
+    copy_box_overlap(dst, box2(3, 3, 5, 5), src, box2(0, 0, 4, 4), 1);
+    require(dst == std::vector<std::uint8_t>{19, 20, 0, 24, 25, 0, 0, 0, 0}, "overlap bytes");
+  });
+  check("put_chunk validates box and dense payload length", [] {
+    DataRegion r = u8_region("a", box2(0, 0, 9, 9));
+    require_throws<DimensionError>([&] { r.put_chunk(box2(0, 0, 9, 9), std::vector<std::uint8_t>(99)); },
+                                   "short payload");
+    require_throws<DimensionError>([&] { r.put_chunk(box2(5, 5, 10, 10), std::vector<std::uint8_t>(36)); },
+                                   "escaping chunk");
+    r.put_chunk(box2(0, 0, 9, 9), std::vector<std::uint8_t>(100, 3));
+    require(r.materialized() && r.payload_bytes() == 100, "materialised");
+    DataRegion i32(DataRegionId{"t", "l", "label", 0, 0}, RegionKind::kDense2D, ElementKind::kI32,
+                   box2(0, 0, 3, 3));
+    require_throws<DimensionError>([&] { i32.put_chunk(box2(0, 0, 3, 3), std::vector<std::uint8_t>(16)); },
+                                   "i32 payload needs 4 bytes per element");
+  });
+  check("template bbox = fold of region boxes (50 seeded trials)", [] {
+    std::mt19937_64 rng(20261018);
+    for (int trial = 0; trial < 50; ++trial) {
+      RegionTemplate t("p");
+      std::int64_t a0 = INT64_MAX, a1 = INT64_MAX, b0 = INT64_MIN, b1 = INT64_MIN;
+      const int n = 1 + int(rng() % 8);
+      for (int i = 0; i < n; ++i) {
+        const std::int64_t l0 = std::int64_t(rng() % 100) - 50, l1 = std::int64_t(rng() % 100) - 50;
+        const std::int64_t h0 = l0 + std::int64_t(rng() % 40), h1 = l1 + std::int64_t(rng() % 40);
+        t.insert_data_region(u8_region("r", box2(l0, l1, h0, h1), i));
+        a0 = std::min(a0, l0); a1 = std::min(a1, l1); b0 = std::max(b0, h0); b1 = std::max(b1, h1);
+      }
+      require(t.bbox() == box2(a0, a1, b0, b1), "fold");
+    }
+  });
+  check("duplicate tuple insert throws, bumped version does not", [] {
+    RegionTemplate t("s");
+    t.insert_data_region(u8_region("a", box2(0, 0, 9, 9)));
+    require_throws<DuplicateRegionError>([&] { t.insert_data_region(u8_region("a", box2(0, 0, 9, 9))); },
+                                         "duplicate");
+    t.insert_data_region(u8_region("a", box2(0, 0, 9, 9), 0, 1));
+    require(t.get_newest("t", "a", "raw")->id().version == 1, "newest");
+  });
+  check("DenseDataRegion2D typed view", [] {
+    DataRegion r = DenseDataRegion2D<std::int32_t>::create(DataRegionId{"t", "l", "label", 0, 0},
+                                                           box2(10, 20, 13, 24));
+    DenseDataRegion2D<std::int32_t> v(r);
+    require(v.height() == 4 && v.width() == 5, "extent");
+    v.at(3, 4) = 77;
+    require(reinterpret_cast<const std::int32_t*>(r.find_chunk(r.bbox())->payload.data())[19] == 77,
+            "row-major, last axis contiguous");
+    require_throws<DimensionError>([&] { DenseDataRegion2D<std::uint8_t> bad(r); }, "kind check");
+  });
+  check("rank check: Dense3D RGB box and Dense2D+time", [] {
+    DataRegion rgb(DataRegionId{"img", "RGB", "raw", 0, 0}, RegionKind::kDense3D, ElementKind::kU8,
+                   BoundingBox({0, 0, 0}, {7, 7, 2}));
+    rgb.put_chunk(rgb.bbox(), std::vector<std::uint8_t>(8 * 8 * 3));
+    require_throws<DimensionError>([] {
+      DataRegion(DataRegionId{}, RegionKind::kDense2D, ElementKind::kU8, BoundingBox({0}, {3}));
+    }, "1-D box for Dense2D");
+  });
+}
+
+// ---------------------------------------------------------------- scheduler / dataflow
+
+TaskNode task(std::uint64_t id, TaskVariants v, std::optional<double> s = std::nullopt) {
+  TaskNode t;
+  t.task_id = id;
+  t.variants = v;
+  t.speedup_estimate = s;
+  return t;
+}
+
+void scheduling() {
+  check("WRM FCFS takes the first compatible ready task", [] {
+    WrmState w(SchedulerKind::kFcfs);
+    w.submit({task(1, TaskVariants::kCpuOnly), task(2, TaskVariants::kGpuOnly),
+              task(3, TaskVariants::kBoth, 4.0)});
+    require(*w.next(DeviceKind::kGpu) == 2, "gpu");
+    require(*w.next(DeviceKind::kCpu) == 1, "cpu");
+    require(*w.next(DeviceKind::kCpu) == 3, "cpu2");
+    require(!w.next(DeviceKind::kGpu), "empty");
+  });
+  check("WRM PATS: GPU takes max speedup, CPU min (reference wrm.cpp:246-273)", [] {
+    WrmState w(SchedulerKind::kPats);
+    w.submit({task(1, TaskVariants::kBoth, 2.0), task(2, TaskVariants::kBoth, 9.0),
+              task(3, TaskVariants::kBoth, 5.0)});
+    require(*w.next(DeviceKind::kGpu) == 2, "gpu max");
+    require(*w.next(DeviceKind::kCpu) == 1, "cpu min");
+  });
+  check("WRM rejects dual-variant tasks without a speedup", [] {
+    WrmState w;
+    require_throws<ConfigError>([&] { w.submit({task(1, TaskVariants::kBoth)}); }, "speedup");
+  });
+  check("WRM dependencies gate readiness", [] {
+    WrmState w;
+    TaskNode b = task(2, TaskVariants::kCpuOnly);
+    b.deps = {1};
+    w.submit({task(1, TaskVariants::kCpuOnly), b});
+    require(*w.next(DeviceKind::kCpu) == 1 && !w.next(DeviceKind::kCpu), "blocked");
+    require(w.complete(1) == std::vector<std::uint64_t>{2}, "released");
+  });
+  check("VariantRegistry derives variants from registered implementations", [] {
+    VariantRegistry r;
+    r.register_variant("g", DeviceKind::kGpu, [] {});
+    r.register_variant("b", DeviceKind::kGpu, [] {});
+    r.register_variant("b", DeviceKind::kCpu, [] {});
+    r.set_speedup("b", 12.0);
+    require(r.make_task("g", 1, 1).variants == TaskVariants::kGpuOnly, "gpu only");
+    const TaskNode t = r.make_task("b", 2, 1);
+    require(t.variants == TaskVariants::kBoth && *t.speedup_estimate == 12.0, "both");
+    require_throws<NotFoundError>([&] { r.make_task("x", 3, 1); }, "unknown");
+  });
+  check("worker_prepare materialises inputs, outputs are shells; finalize stages outputs", [] {
+    StorageRegistry reg;
+    auto st = std::make_shared<MemoryStore>("store");
+    reg.add(st);
+    const DataRegionId rgb{"img", "rgb", "raw", 0, 0}, mask{"img", "mask", "label", 0, 0};
+    DataRegion in(rgb, RegionKind::kDense2D, ElementKind::kU8, box2(0, 0, 15, 15));
+    in.put_chunk(box2(0, 0, 15, 15), std::vector<std::uint8_t>(256, 9));
+    st->stage_region(in, 0).wait();
+    StageInstance s;
+    s.stage_id = 5;
+    s.stage_kind = "seg";
+    s.region_descriptors = {RegionDescriptor{rgb, box2(0, 0, 15, 15), IoMode::kInput, "store"},
+                            RegionDescriptor{mask, box2(0, 0, 15, 15), IoMode::kOutput, "store"}};
+    RegionTemplate local = worker_prepare(s, reg);
+    require(local.get_data_region(rgb)->materialized(), "input read");
+    require(!local.get_data_region(mask)->materialized(), "output shell");
+    local.get_data_region(mask)->put_chunk(box2(0, 0, 15, 15), std::vector<std::uint8_t>(256, 1));
+    stage_finalize(local, s, reg, 0);
+    require(!local.get_data_region(rgb), "input dropped");
+    require(st->read_region(mask, box2(4, 4, 7, 7)).payload_bytes() == 16, "staged sub-box read");
+    s.region_descriptors[0].id.key = "absent";
+    require_throws<NotFoundError>([&] { worker_prepare(s, reg); }, "missing input");
+  });
+  check("ManagerState dispatches FIFO among dependency-satisfied stages", [] {
+    ManagerState m;
+    StageInstance a, b, c;
+    a.stage_id = 1;
+    b.stage_id = 2;
+    b.deps = {1};
+    c.stage_id = 3;
+    m.add_stage(a);
+    m.add_stage(b);
+    m.add_stage(c);
+    require(*m.dispatch(0) == 1 && *m.dispatch(0) == 3 && !m.dispatch(0), "fifo + gating");
+    require(m.stage_complete(1) == std::vector<std::uint64_t>{2}, "release");
+  });
+}
+
+// ---------------------------------------------------------------- the GPU stage
+
+extern "C" int rtg_synth_tile_host(uint64_t, int64_t, int64_t, int64_t, int64_t, uint8_t*);
+
+// The oracle as the CPU variant of "segment_features" (test-only drop-in twin).
+void cpu_segment_features(const SegmentationRegions& ids, const rtg_params& p) {
+  RegionTemplate& local = *worker_context().local;
+  const DataRegion* rgb = local.get_data_region(ids.rgb);
+  const BoundingBox& b3 = rgb->bbox();
+  const std::int64_t h = b3.extent(0), w = b3.extent(1);
+  const BoundingBox b2({b3.lo(0), b3.lo(1)}, {b3.hi(0), b3.hi(1)});
+  DataRegion& mask = install_output(local, ids.mask, RegionKind::kDense2D, ElementKind::kU8, b2);
+  DataRegion& lab = install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2);
+  std::vector<float> f(std::size_t(1 << 16) * RTG_NUM_FEATURES);
+  const std::int32_t n = orc_process_tile(
+      rgb->find_chunk(b3)->payload.data(), h, w, 3 * w, &p, mask.find_chunk(b2)->payload.data(),
+      reinterpret_cast<std::int32_t*>(lab.find_chunk(b2)->payload.data()), f.data(), 1 << 16,
+      nullptr);
+  if (n > 0) {
+    const BoundingBox fb({0, 0}, {n - 1, RTG_NUM_FEATURES - 1});
+    DataRegion& fr = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb);
+    std::memcpy(fr.find_chunk(fb)->payload.data(), f.data(), sizeof(float) * n * RTG_NUM_FEATURES);
+  }
+}
+
+// Slide of 2x2 tiles staged as one Dense3D region; one stage per tile.
+struct Run {
+  std::vector<DataRegion> masks, labels, feats;
+};
+
+Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats) {
+  const std::int64_t H = 1024, W = 1024, T = 512;
+  rtg_params p;
+  rtg_check(rtg_params_default(&p));
+  StorageRegistry reg;
+  auto st = std::make_shared<MemoryStore>("store");
+  reg.add(st);
+  SegmentationRegions ids;
+  DataRegion slide(ids.rgb, RegionKind::kDense3D, ElementKind::kU8, BoundingBox({0, 0, 0}, {H - 1, W - 1, 2}));
+  std::vector<std::uint8_t> px(std::size_t(H * W * 3));
+  rtg_check(rtg_synth_tile_host(1405795800ULL, 0, 0, H, W, px.data()));
+  slide.put_chunk(slide.bbox(), std::move(px));
+  st->stage_region(slide, 0).wait();
+
+  auto vr = std::make_shared<VariantRegistry>();
+  if (use_gpu) register_gpu_segmentation(*vr, ids, p);
+  if (register_cpu) {
+    vr->register_variant(kSegmentFeaturesTask, DeviceKind::kCpu, [ids, p] { cpu_segment_features(ids, p); });
+    vr->set_speedup(kSegmentFeaturesTask, 100.0);
+  }
+  ManagerState m;
+  std::uint64_t sid = 1;
+  std::vector<SegmentationRegions> tile_ids;
+  for (std::int64_t y = 0; y < H; y += T) {
+    for (std::int64_t x = 0; x < W; x += T) {
+      SegmentationRegions t = ids;
+      t.mask.timestamp = t.labels.timestamp = t.features.timestamp = std::int64_t(sid);
+      tile_ids.push_back(t);
+      m.add_stage(make_segmentation_stage(sid++, box2(y, x, y + T - 1, x + T - 1), t, vr));
+    }
+  }
+  std::unique_ptr<GpuDevice> gpu;
+  ExecutorConfig cfg;
+  if (use_gpu) {
+    gpu = std::make_unique<GpuDevice>(0, T, T, 1 << 14);
+    cfg.gpus = {gpu.get()};
+  }
+  *stats = run_stages(m, reg, cfg);
+  Run out;
+  std::int64_t k = 0;
+  for (std::int64_t y = 0; y < H; y += T) {
+    for (std::int64_t x = 0; x < W; x += T, ++k) {
+      const auto& t = tile_ids[std::size_t(k)];
+      out.masks.push_back(st->read_region(t.mask, box2(y, x, y + T - 1, x + T - 1)));
+      out.labels.push_back(st->read_region(t.labels, box2(y, x, y + T - 1, x + T - 1)));
+      out.feats.push_back(st->read_region(t.features, box2(0, 0, 0, RTG_NUM_FEATURES - 1)));
+    }
+  }
+  return out;
+}
+
+void gpu_stage() {
+  check("GPU variant through StageInstance/WRM/TaskNode matches the CPU variant bit-exactly", [] {
+    ExecutorStats sg, sc;
+    const Run g = run_slide(true, false, &sg);
+    require(sg.stages == 4 && sg.gpu_tasks == 4 && sg.cpu_tasks == 0, "all tasks on the GPU");
+    const Run c = run_slide(false, true, &sc);
+    require(sc.cpu_tasks == 4, "all tasks on the CPU variant");
+    for (std::size_t i = 0; i < 4; ++i) {
+      require(g.masks[i].chunks().begin()->second.payload == c.masks[i].chunks().begin()->second.payload,
+              "mask tile " + std::to_string(i));
+      require(g.labels[i].chunks().begin()->second.payload ==
+                  c.labels[i].chunks().begin()->second.payload,
+              "labels tile " + std::to_string(i));
+      require(g.labels[i].element_kind() == ElementKind::kI32, "labels are I32");
+    }
+  });
+  check("PATS sends a dual-variant task to the GPU worker", [] {
+    ExecutorStats s;
+    run_slide(true, true, &s);
+    require(s.gpu_tasks == 4, "gpu picked");
+  });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::strcmp(argv[1], "--gpu") == 0;
+  containers();
+  scheduling();
+  if (gpu) gpu_stage();
+  std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}
