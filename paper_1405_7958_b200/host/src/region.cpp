@@ -85,11 +85,10 @@ bool BoundingBox::operator==(const BoundingBox& o) const {
 }
 
 bool BoundingBox::operator<(const BoundingBox& o) const {
+  // rank first, then axis by axis (lo, hi) — the reference's map-key order
   if (dims_ != o.dims_) return dims_ < o.dims_;
   for (int a = 0; a < dims_; ++a) {
     if (lo_[a] != o.lo_[a]) return lo_[a] < o.lo_[a];
-  }
-  for (int a = 0; a < dims_; ++a) {
     if (hi_[a] != o.hi_[a]) return hi_[a] < o.hi_[a];
   }
   return false;

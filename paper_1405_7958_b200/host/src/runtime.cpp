@@ -122,15 +122,17 @@ std::optional<std::uint64_t> WrmState::next(DeviceKind device) {
       pick = k;
       break;
     }
-    // PATS: the GPU takes the largest speedup, a CPU core the smallest
-    // (ties: earliest submission).
+    // PATS: the GPU takes the largest speedup, a CPU core the smallest;
+    // ties go to the earliest submission (not the earliest readiness).
     if (!pick) {
       pick = k;
       continue;
     }
+    const Entry& pe = tasks_.at(ready_[*pick]);
     const double s = effective_speedup(t);
-    const double b = effective_speedup(tasks_.at(ready_[*pick]).node);
-    if (device == DeviceKind::kGpu ? s > b : s < b) pick = k;
+    const double b = effective_speedup(pe.node);
+    const bool better = device == DeviceKind::kGpu ? s > b : s < b;
+    if (better || (s == b && tasks_.at(ready_[k]).seq < pe.seq)) pick = k;
   }
   if (!pick) return std::nullopt;
   const auto id = ready_[*pick];
