@@ -34,7 +34,6 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WSI = 100_000
 TILE = 4096
 METRIC = "tile Mpixel/s (segment+features) at 1/2/4/8 B200, % of HBM roofline"
 
@@ -53,24 +52,7 @@ STAGE_BYTES_PER_PX = {
 }
 
 
-def wsi_tiles():
-    """partition_regular(<0,0;99999,99999>, {4096,4096}): row-major tiles."""
-    n = math.ceil(WSI / TILE)
-    out = []
-    for i in range(n):
-        for j in range(n):
-            h = min(TILE, WSI - i * TILE)
-            w = min(TILE, WSI - j * TILE)
-            out.append((i, j, h, w))
-    return out
-
-
-def global_tile(g):
-    """Global tile sequence: slide s = g // 625, tile t of that slide."""
-    tiles = wsi_tiles()
-    s, t = divmod(g, len(tiles))
-    i, j, h, w = tiles[t]
-    return s * 25 + i, j, h, w  # seed row includes the slide index
+from paper_1405_7958_b200.wsi import gather_tables, global_tile, rank_tiles  # noqa: E402
 
 
 def measured_peaks():
@@ -243,7 +225,7 @@ def main():
     params = rtg.default_params()
     ctxs = [rtg.Context(local, TILE, TILE, cap) for _ in range(S)]
     ext = [torch.cuda.ExternalStream(c.stream()) for c in ctxs]
-    my_tiles = [global_tile(rank * T + k) for k in range(T)]
+    my_tiles = rank_tiles(rank, T)
     px_rank = sum(h * w for (_, _, h, w) in my_tiles)
 
     # inputs resident in HBM (T x 48 MiB), generated on the device
@@ -257,7 +239,7 @@ def main():
     counts = torch.zeros((T,), dtype=torch.int32, device="cuda")
 
     def gather(n_host):
-        """Pack this rank's tables and gather them on rank 0 (NCCL)."""
+        """Pack this rank's per-tile tables and gather them on rank 0 (NCCL)."""
         rows = int(n_host.sum())
         packed = torch.empty((max(rows, 1), rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
         off = 0
@@ -266,27 +248,7 @@ def main():
             if nk:
                 packed[off:off + nk].copy_(feats[k, :nk])
                 off += nk
-        if world == 1:
-            return packed[:rows], rows
-        sizes = torch.tensor([rows], dtype=torch.int64, device="cuda")
-        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
-        dist.all_gather(all_sizes, sizes)
-        mx = int(max(int(s) for s in all_sizes))
-        buf = torch.zeros((max(mx, 1), rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
-        buf[:rows].copy_(packed[:rows])
-        if rank == 0:
-            outs = [torch.empty_like(buf) for _ in range(world)]
-            ops = [dist.P2POp(dist.irecv, outs[r], r) for r in range(1, world)]
-            reqs = dist.batch_isend_irecv(ops) if ops else []
-            for q in reqs:
-                q.wait()
-            outs[0] = buf
-            total = sum(int(s) for s in all_sizes)
-            return torch.cat([outs[r][: int(all_sizes[r])] for r in range(world)]), total
-        reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, buf, 0)])
-        for q in reqs:
-            q.wait()
-        return None, rows
+        return gather_tables(packed, rows, rank, world, dist)
 
     cur = torch.cuda.current_stream()
 

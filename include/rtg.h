@@ -163,6 +163,15 @@ int rtg_ctx_profile_read(rtg_ctx* ctx, double ms[RTG_NUM_STAGES],
 /* Kernels launched through this ctx since creation (host-side counter). */
 int rtg_ctx_launches(rtg_ctx* ctx, int64_t* out);
 
+/* Implementation choices that do not change results (all bit-identical). */
+enum rtg_option {
+  /* FillHoles: 0 = union-find labelling of the 4-connected background
+   * (default), 1 = IWPP binary reconstruction from the border on the tile
+   * queue. */
+  RTG_OPT_FILL_HOLES_IMPL = 0
+};
+int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* rtg_last_error(void);
 

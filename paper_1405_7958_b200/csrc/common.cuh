@@ -112,6 +112,9 @@ struct rtg_ctx {
   rtg::TileQueue tq{};
   rtg::FeatureAcc acc{};
 
+  // implementation options (rtg_ctx_set_option)
+  int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
+
   // host-side instrumentation
   int64_t launches = 0;           // kernels launched through this ctx
   bool prof = false;              // stage timing with CUDA events
@@ -159,6 +162,9 @@ int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n);
+// FillHoles via union-find of the 4-connected background; scratch may alias out.
+int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
+                  uint8_t* scratch, uint8_t* out);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
                 int32_t min_area, int32_t max_area, int32_t* counts,
                 uint8_t* out);

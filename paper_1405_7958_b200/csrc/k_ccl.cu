@@ -277,7 +277,59 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
   return (int)(want < cap ? want : cap);
 }
 
+// ---- FillHoles by union-find: background components (4-conn) that touch the
+// tile border are "reached"; every other background pixel is a hole.
+__global__ void k_invert(int64_t n, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)(in[i] == 0);
+}
+
+__global__ void k_mark_border_roots(int h, int w, const int32_t* __restrict__ roots,
+                                    int32_t* __restrict__ flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;  // walks the perimeter
+  const int per = 2 * (h + w);
+  if (k >= per) return;
+  int y, x;
+  if (k < w) { y = 0; x = k; }
+  else if (k < 2 * w) { y = h - 1; x = k - w; }
+  else if (k < 2 * w + h) { y = k - 2 * w; x = 0; }
+  else { y = k - 2 * w - h; x = w - 1; }
+  const int32_t r = roots[(int64_t)y * w + x];
+  if (r >= 0) flag[r] = 1;
+}
+
+__global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
+                                const int32_t* __restrict__ roots,
+                                const int32_t* __restrict__ flag, uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = roots[i];
+    out[i] = (uint8_t)(bin[i] || (r >= 0 && !flag[r]));
+  }
+}
+
 }  // namespace
+
+int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_t* scratch,
+                  uint8_t* out) {
+  const int64_t n = h * w;
+  k_invert<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, scratch);
+  RTG_LAUNCH("k_invert");
+  int32_t* roots = ctx->i32a;
+  int32_t* flag = ctx->i32b;
+  RTG_TRY(ccl_roots(ctx, scratch, h, w, 4, roots));
+  // zero the flags at root positions only (reuses the counter-zeroing pass)
+  k_ccl_flatten<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag);
+  RTG_LAUNCH("k_ccl_flatten(flags)");
+  const int per = (int)(2 * (h + w));
+  k_mark_border_roots<<<(unsigned)ceil_div(per, 256), 256, 0, ctx->stream>>>((int)h, (int)w,
+                                                                             roots, flag);
+  RTG_LAUNCH("k_mark_border_roots");
+  k_fill_uf_final<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, roots, flag, out);
+  RTG_LAUNCH("k_fill_uf_final");
+  return RTG_OK;
+}
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
               int conn, int32_t* roots) {

@@ -84,6 +84,13 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
   return (int)(want < cap ? want : cap);
 }
 
+// o4 with the context's implementation choice; `out` may be any buffer except
+// `bin` (ctx->m2 is the IWPP J plane / union-find scratch when out differs).
+int run_fill_holes(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_t* out) {
+  if (ctx->fill_impl == 1) return iwpp_fill_holes(ctx, bin, out == bin ? ctx->m2 : out, h, w, out);
+  return fill_holes_uf(ctx, bin, h, w, out, out);
+}
+
 // The stage: o1 .. o9 on device buffers, all asynchronous on ctx->stream.
 int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
              const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
@@ -101,7 +108,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o4 FillHoles of the nucleus candidates
   prof_mark(ctx, RTG_STAGE_FILL_HOLES);
   RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
-  RTG_TRY(iwpp_fill_holes(ctx, ctx->m1, ctx->m2, h, w, ctx->m2));
+  RTG_TRY(run_fill_holes(ctx, ctx->m1, h, w, ctx->m2));
   // o5 AreaThreshold
   prof_mark(ctx, RTG_STAGE_AREA);
   RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a));
@@ -355,6 +362,18 @@ int rtg_ctx_profile_read(rtg_ctx* ctx, double ms[RTG_NUM_STAGES], int64_t calls[
   return RTG_OK;
 }
 
+int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
+  switch (option) {
+    case RTG_OPT_FILL_HOLES_IMPL:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "fill impl must be 0 or 1");
+      ctx->fill_impl = (int)value;
+      return RTG_OK;
+    default:
+      return fail(RTG_ERR_INVALID_ARG, "unknown option " + std::to_string(option));
+  }
+}
+
 int rtg_ctx_launches(rtg_ctx* ctx, int64_t* out) {
   if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
   *out = ctx->launches;
@@ -504,7 +523,8 @@ int rtg_fill_holes_dev(rtg_ctx* ctx, const uint8_t* d_in, int64_t h, int64_t w,
                        uint8_t* d_out) {
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_in || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
-  return iwpp_fill_holes(ctx, d_in, ctx->m2, h, w, d_out);
+  if (d_in == d_out) return fail(RTG_ERR_INVALID_ARG, "fill holes cannot run in place");
+  return run_fill_holes(ctx, d_in, h, w, d_out);
 }
 
 int rtg_bwlabel_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w, int conn,

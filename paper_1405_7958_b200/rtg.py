@@ -39,8 +39,9 @@ SYMBOLS = [
     "rtg_fill_holes_dev", "rtg_bwlabel_dev", "rtg_area_threshold_dev",
     "rtg_edt_dev", "rtg_watershed_dev", "rtg_features_dev",
     "rtg_synth_tile_host", "rtg_synth_tile_dev", "rtg_ctx_profile",
-    "rtg_ctx_profile_read", "rtg_ctx_launches",
+    "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
 ]
+OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features"]
 
@@ -157,6 +158,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_ctx_profile": [vp, ctypes.c_int],
         "rtg_ctx_profile_read": [vp, vp, vp],
         "rtg_ctx_launches": [vp, vp],
+        "rtg_ctx_set_option": [vp, ctypes.c_int, i64],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -257,6 +259,9 @@ class Context:
         calls = (ctypes.c_int64 * len(STAGES))()
         check(self.lib.rtg_ctx_profile_read(self.handle, ms, calls))
         return {s: (ms[i], calls[i]) for i, s in enumerate(STAGES)}
+
+    def set_option(self, option: int, value: int) -> None:
+        check(self.lib.rtg_ctx_set_option(self.handle, option, value))
 
     def launches(self) -> int:
         n = ctypes.c_int64(0)

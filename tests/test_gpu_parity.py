@@ -149,15 +149,31 @@ def test_recon_u16(ctx, oracle):
 
 # ---------------------------------------------------------------- o4
 
+@pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("shape", [(512, 512), (4096, 4096), (31, 77)])
-def test_fill_holes(ctx, oracle, shape):
+def test_fill_holes(rtg, ctx, oracle, shape, impl):
     rng = np.random.default_rng(shape[0])
     h, w = shape
     m = 1 - _rand_blobs(rng, h, w, 0.45, 1.5)
     ref = oracle.fill_holes(m)
     out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
-    ctx.fill_holes_dev(_np_dev(m), h, w, out)
-    assert np.array_equal(_dev_np(out), ref)
+    ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, impl)
+    try:
+        ctx.fill_holes_dev(_np_dev(m), h, w, out)
+        assert np.array_equal(_dev_np(out), ref)
+    finally:
+        ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
+
+
+def test_pipeline_fill_impls_agree(rtg, ctx):
+    rgb = rtg.synth_tile_host(7, 7, 2048, 2048)
+    a = ctx.process_tile(rgb)
+    ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 1)
+    try:
+        b = ctx.process_tile(rgb)
+    finally:
+        ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
+    assert a[4] == b[4] and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
 
 
 # ---------------------------------------------------------------- o5 / o8
