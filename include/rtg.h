@@ -168,7 +168,10 @@ enum rtg_option {
   /* FillHoles: 0 = union-find labelling of the 4-connected background
    * (default), 1 = IWPP binary reconstruction from the border on the tile
    * queue. */
-  RTG_OPT_FILL_HOLES_IMPL = 0
+  RTG_OPT_FILL_HOLES_IMPL = 0,
+  /* rtg_process_tile_dev replays a cached CUDA graph of the whole stage per
+   * distinct argument tuple (1, default) or launches kernel by kernel (0). */
+  RTG_OPT_USE_GRAPHS = 1
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

@@ -114,6 +114,18 @@ struct rtg_ctx {
 
   // implementation options (rtg_ctx_set_option)
   int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
+  int use_graphs = 1; // replay rtg_process_tile_dev as a cached CUDA graph
+
+  // CUDA-graph cache of whole-tile pipelines, keyed by every argument
+  struct GraphEntry {
+    std::string key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // kernel launches one replay stands for
+    uint64_t last_use = 0;
+  };
+  GraphEntry* graphs = nullptr;
+  int n_graphs = 0;
+  uint64_t graph_clock = 0;
 
   // host-side instrumentation
   int64_t launches = 0;           // kernels launched through this ctx

@@ -129,6 +129,68 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   return RTG_OK;
 }
 
+constexpr int kGraphCap = 256;
+
+// Replays the whole-tile pipeline as a CUDA graph.  The pipeline makes no
+// host-side decisions (persistent IWPP queues, device-side counts), so one
+// capture per distinct argument tuple is exact; the cache holds kGraphCap
+// instantiated graphs (least recently used evicted).
+int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
+                   const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
+                   float* d_features, int32_t* d_n) {
+  std::string key(sizeof(rtg_params) + 12 * sizeof(int64_t), '\0');
+  const int64_t fields[12] = {(int64_t)d_rgb, h, w, pitch, (int64_t)d_mask, (int64_t)d_labels,
+                              (int64_t)d_hema, (int64_t)d_features, (int64_t)d_n,
+                              (int64_t)ctx->fill_impl, (int64_t)ctx->stream, 0};
+  std::memcpy(&key[0], fields, sizeof(fields));
+  std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
+  if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
+  ++ctx->graph_clock;
+  for (int i = 0; i < ctx->n_graphs; ++i) {
+    rtg_ctx::GraphEntry& g = ctx->graphs[i];
+    if (g.key == key) {
+      g.last_use = ctx->graph_clock;
+      RTG_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+      ctx->launches += g.launches;
+      return RTG_OK;
+    }
+  }
+  // capture (kernels are not executed while capturing)
+  const int64_t before = ctx->launches;
+  RTG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  const int st = pipeline(ctx, d_rgb, h, w, pitch, p, d_mask, d_labels, d_hema, d_features, d_n,
+                          true);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+  if (st != RTG_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+  const int64_t per_replay = ctx->launches - before;
+  ctx->launches = before;
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
+  int slot = ctx->n_graphs;
+  if (slot == kGraphCap) {
+    slot = 0;
+    for (int i = 1; i < kGraphCap; ++i)
+      if (ctx->graphs[i].last_use < ctx->graphs[slot].last_use) slot = i;
+    cudaGraphExecDestroy(ctx->graphs[slot].exec);
+  } else {
+    ++ctx->n_graphs;
+  }
+  ctx->graphs[slot].key = key;
+  ctx->graphs[slot].exec = exec;
+  ctx->graphs[slot].launches = per_replay;
+  ctx->graphs[slot].last_use = ctx->graph_clock;
+  RTG_CUDA(cudaGraphLaunch(exec, ctx->stream));
+  ctx->launches += per_replay;
+  return RTG_OK;
+}
+
 int upload_rgb(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w, int64_t pitch) {
   if (!rgb) return fail(RTG_ERR_INVALID_ARG, "null rgb");
   if (pitch < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
@@ -276,6 +338,10 @@ int rtg_ctx_destroy(rtg_ctx* c) {
     delete[] c->prof_ev;
     delete[] c->prof_stage;
   }
+  if (c->graphs) {
+    for (int i = 0; i < c->n_graphs; ++i) cudaGraphExecDestroy(c->graphs[i].exec);
+    delete[] c->graphs;
+  }
   delete c;
   return RTG_OK;
 }
@@ -368,6 +434,9 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
     case RTG_OPT_FILL_HOLES_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "fill impl must be 0 or 1");
       ctx->fill_impl = (int)value;
+      return RTG_OK;
+    case RTG_OPT_USE_GRAPHS:
+      ctx->use_graphs = value != 0;
       return RTG_OK;
     default:
       return fail(RTG_ERR_INVALID_ARG, "unknown option " + std::to_string(option));
@@ -481,8 +550,11 @@ int rtg_process_tile_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t 
   RTG_TRY(check_params(params));
   if (!d_rgb || !d_features || !d_n_objects) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (pitch_bytes < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
-  return pipeline(ctx, d_rgb, h, w, pitch_bytes, params, d_mask, d_labels, d_hema, d_features,
-                  d_n_objects, true);
+  if (!ctx->use_graphs || ctx->prof)
+    return pipeline(ctx, d_rgb, h, w, pitch_bytes, params, d_mask, d_labels, d_hema, d_features,
+                    d_n_objects, true);
+  return pipeline_graph(ctx, d_rgb, h, w, pitch_bytes, params, d_mask, d_labels, d_hema,
+                        d_features, d_n_objects);
 }
 
 // ---- per-operator entry points ---------------------------------------------------

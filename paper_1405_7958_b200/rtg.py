@@ -42,6 +42,7 @@ SYMBOLS = [
     "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
 ]
 OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
+OPT_USE_GRAPHS = 1       # 1 replay cached CUDA graphs in process_tile_dev (default)
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features"]
 

@@ -298,6 +298,28 @@ def test_pipeline_dev_async_matches_host_entry(rtg, ctx):
     assert np.array_equal(_dev_np(d_feat)[:n], feats)
 
 
+def test_graph_replay_matches_eager(rtg, ctx):
+    """process_tile_dev: first call captures a CUDA graph, later calls replay
+    it; both must equal the kernel-by-kernel path."""
+    h, w = 1536, 2048
+    p = rtg.default_params()
+    d_rgb = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+    ctx.synth_tile_dev(d_rgb, 9, 1, h, w)
+    outs = []
+    for graphs in (1, 1, 0):
+        ctx.set_option(rtg.OPT_USE_GRAPHS, graphs)
+        d_lab = torch.zeros((h, w), dtype=torch.int32, device="cuda")
+        d_feat = torch.zeros((ctx.max_objects, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+        d_n = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ctx.process_tile_dev(d_rgb, h, w, p, None, d_lab, None, d_feat, d_n)
+        ctx.sync()
+        n = int(_dev_np(d_n)[0])
+        outs.append((n, _dev_np(d_lab), _dev_np(d_feat)[:n]))
+    ctx.set_option(rtg.OPT_USE_GRAPHS, 1)
+    for o in outs[1:]:
+        assert o[0] == outs[0][0] and np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])
+
+
 def test_repeatable(rtg, ctx):
     rgb = rtg.synth_tile_host(2, 2, 1024, 1024)
     a = ctx.process_tile(rgb)
