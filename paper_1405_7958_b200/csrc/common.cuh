@@ -51,7 +51,7 @@ enum : uint32_t {
 struct TileQueue {
   int32_t* state;     // per tile: 0 idle, 1 queued, 2 processing, 3 dirty
   int32_t* slots;     // circular queue of tile+1 (0 = empty), 2*ntiles
-  uint32_t* counters; // [0] head, [1] tail, [2] pending, [3] visits
+  uint32_t* counters; // [0] head, [1] tail, [2] pending, [3] visits, [4] abort
   int32_t capacity;   // ntiles of the largest tile
 };
 

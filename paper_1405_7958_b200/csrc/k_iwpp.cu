@@ -89,6 +89,7 @@ __device__ int32_t q_pop(const TileQueue& q, int32_t cap) {
       return v - 1;
     }
     if (*(volatile uint32_t*)&q.counters[2] == 0u) return -1;
+    if (*(volatile uint32_t*)&q.counters[4] != 0u) return -1;  // aborted
     __nanosleep(64);
   }
 }
@@ -110,7 +111,8 @@ __device__ bool q_finish(const TileQueue& q, int32_t t) {
 template <typename T, int CONN, class MaskF>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
-       TileQueue q, int32_t cap, int64_t* visits) {
+       TileQueue q, int32_t cap, int64_t* visits, uint32_t max_visits,
+       uint32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -121,7 +123,16 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
 
   while (true) {
     int32_t t = 0;
-    if (lane == 0) t = q_pop(q, cap);
+    if (lane == 0) {
+      t = q_pop(q, cap);
+      // visit budget: a bug that livelocks the queue must not hang the GPU;
+      // exceeding it aborts every warp and raises a sticky status bit
+      if (t >= 0 && atomicAdd(&q.counters[3], 1u) > max_visits) {
+        atomicExch(&q.counters[4], 1u);
+        atomicOr(status, kStatusQueueOverflow);
+        t = -1;
+      }
+    }
     t = __shfl_sync(full, t, 0);
     if (t < 0) break;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -171,9 +182,16 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
       left0 = Js[(lane + 1) * kJS + 1];
       right0 = Js[(lane + 1) * kJS + 32];
 
+      // a tile already at its upper bound (J == mask everywhere, e.g. an
+      // all-background tile of a distance map) cannot change: skip the sweeps
+      bool saturated = true;
+      for (int r = 0; r < 32; ++r)
+        saturated &= Js[(r + 1) * kJS + lane + 1] == Is[r * kIS + lane];
+      saturated = __all_sync(full, saturated);
+
       // local fixed point
-      bool iter_changed;
-      do {
+      bool iter_changed = !saturated;
+      while (iter_changed) {
         bool ch = false;
         // down: lane = column c, rows 0..31, neighbours in the row above
         for (int r = 0; r < 32; ++r) {
@@ -221,7 +239,7 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
         }
         iter_changed = __any_sync(full, ch);
         tile_changed |= iter_changed;
-      } while (iter_changed);
+      }
 
       ++my_visits;
       if (tile_changed) {
@@ -253,6 +271,11 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
         pw = __any_sync(full, lv != left0 && lv > nl);
         pe = __any_sync(full, rv != right0 && rv > nr);
       }
+      // corner values at the start of this visit (diagonal neighbours):
+      // a diagonal push needs the corner to have CHANGED in this visit, else
+      // static corner inequalities between tiles could cycle forever
+      const uint32_t c00_0 = __shfl_sync(full, top0, 0), c01_0 = __shfl_sync(full, top0, 31);
+      const uint32_t c10_0 = __shfl_sync(full, bot0, 0), c11_0 = __shfl_sync(full, bot0, 31);
       if (lane == 0) {
         const int tiles_y = (h + kTile - 1) / kTile;
         if (pn && ty > 0) q_push(q, cap, t - tiles_x);
@@ -262,11 +285,13 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
         if (CONN == 8) {
           const uint32_t c00 = Js[1 * kJS + 1], c01 = Js[1 * kJS + 32];
           const uint32_t c10 = Js[32 * kJS + 1], c11 = Js[32 * kJS + 32];
-          // corner pixels changed: compare with the diagonal halo corner
-          if (ty > 0 && tx > 0 && c00 > Js[0]) q_push(q, cap, t - tiles_x - 1);
-          if (ty > 0 && tx + 1 < tiles_x && c01 > Js[33]) q_push(q, cap, t - tiles_x + 1);
-          if (ty + 1 < tiles_y && tx > 0 && c10 > Js[33 * kJS]) q_push(q, cap, t + tiles_x - 1);
-          if (ty + 1 < tiles_y && tx + 1 < tiles_x && c11 > Js[33 * kJS + 33])
+          if (ty > 0 && tx > 0 && c00 != c00_0 && c00 > Js[0])
+            q_push(q, cap, t - tiles_x - 1);
+          if (ty > 0 && tx + 1 < tiles_x && c01 != c01_0 && c01 > Js[33])
+            q_push(q, cap, t - tiles_x + 1);
+          if (ty + 1 < tiles_y && tx > 0 && c10 != c10_0 && c10 > Js[33 * kJS])
+            q_push(q, cap, t + tiles_x - 1);
+          if (ty + 1 < tiles_y && tx + 1 < tiles_x && c11 != c11_0 && c11 > Js[33 * kJS + 33])
             q_push(q, cap, t + tiles_x + 1);
         }
       }
@@ -319,6 +344,8 @@ __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
     q.counters[0] = 0;
     q.counters[1] = (uint32_t)count;
     q.counters[2] = (uint32_t)count;
+    q.counters[3] = 0;  // visits
+    q.counters[4] = 0;  // abort flag
   }
 }
 
@@ -367,7 +394,8 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w,
   const int need = (int)ceil_div(ntiles, kWarpsPerBlock);
   if (blocks > need) blocks = need;
   k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
-      J, maskf, (int)h, (int)w, tiles_x, ctx->tq, cap, ctx->stats + 1);
+      J, maskf, (int)h, (int)w, tiles_x, ctx->tq, cap, ctx->stats + 1,
+      (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
   RTG_LAUNCH("k_iwpp");
   return RTG_OK;
 }

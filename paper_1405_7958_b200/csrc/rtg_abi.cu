@@ -304,7 +304,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         c->tq.capacity = (int32_t)(2 * ntiles);
         RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
         RTG_TRY(dalloc(&c->tq.slots, (size_t)(2 * ntiles)));
-        RTG_TRY(dalloc(&c->tq.counters, 4));
+        RTG_TRY(dalloc(&c->tq.counters, 8));
         c->acc.cap = max_objects;
         RTG_TRY(dalloc(&c->acc.sums, (size_t)kSumFields * max_objects));
         RTG_TRY(dalloc(&c->acc.mins, (size_t)kMinFields * max_objects));
@@ -368,7 +368,10 @@ int rtg_ctx_sync(rtg_ctx* ctx) {
     RTG_CUDA(cudaMemset(ctx->status, 0, sizeof(uint32_t)));
     return fail(RTG_ERR_OVERFLOW, "object count exceeded the context's max_objects");
   }
-  if (st & kStatusQueueOverflow) return fail(RTG_ERR_INTERNAL, "IWPP queue overflow");
+  if (st & kStatusQueueOverflow) {
+    RTG_CUDA(cudaMemset(ctx->status, 0, sizeof(uint32_t)));
+    return fail(RTG_ERR_INTERNAL, "IWPP visit budget exceeded (reconstruction aborted)");
+  }
   return RTG_OK;
 }
 
