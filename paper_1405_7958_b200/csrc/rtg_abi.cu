@@ -474,8 +474,12 @@ int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
   if (!n_objects) return fail(RTG_ERR_INVALID_ARG, "null n_objects");
   if (features_out && max_rows < 0) return fail(RTG_ERR_INVALID_ARG, "max_rows < 0");
   RTG_TRY(upload_rgb(ctx, rgb, h, w, pitch_bytes));
-  RTG_TRY(pipeline(ctx, ctx->rgb, h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
-                   ctx->features, ctx->misc, features_out != nullptr));
+  if (ctx->use_graphs && !ctx->prof)
+    RTG_TRY(pipeline_graph(ctx, ctx->rgb, h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                           ctx->features, ctx->misc));
+  else
+    RTG_TRY(pipeline(ctx, ctx->rgb, h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                     ctx->features, ctx->misc, true));
   int32_t n = 0;
   RTG_CUDA(cudaMemcpyAsync(&n, ctx->misc, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
   RTG_CUDA(cudaStreamSynchronize(ctx->stream));
