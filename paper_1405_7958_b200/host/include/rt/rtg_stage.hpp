@@ -65,6 +65,10 @@ StageInstance make_segmentation_stage(std::uint64_t stage_id, const BoundingBox&
                                       const SegmentationRegions& ids,
                                       std::shared_ptr<const VariantRegistry> reg);
 
+// Resolves the stage's concrete region tuples (timestamp / version are per
+// stage) from the local template by (ns, key, type_tag).
+SegmentationRegions resolve_regions(const RegionTemplate& local, const SegmentationRegions& names);
+
 // Output installation helper shared by variants: replaces the metadata-only
 // shell worker_prepare created with a typed, zero-filled dense region that
 // keeps the shell's io mode and storage binding.

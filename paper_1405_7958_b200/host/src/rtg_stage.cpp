@@ -46,13 +46,28 @@ DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, Region
   return local.insert_data_region(std::move(r));
 }
 
+SegmentationRegions resolve_regions(const RegionTemplate& local, const SegmentationRegions& names) {
+  SegmentationRegions out = names;
+  auto pick = [&](DataRegionId& id) {
+    // the stage's own instance of this (ns, key, type) — timestamps and
+    // versions are per stage, so look the tuple up in the local template
+    if (const DataRegion* r = local.get_newest(id.ns, id.key, id.type_tag)) id = r->id();
+  };
+  pick(out.rgb);
+  pick(out.mask);
+  pick(out.labels);
+  pick(out.features);
+  return out;
+}
+
 namespace {
 
-void gpu_segment_features(const SegmentationRegions& ids, const rtg_params& params) {
+void gpu_segment_features(const SegmentationRegions& names, const rtg_params& params) {
   WorkerContext& wc = worker_context();
   if (!wc.local) throw ProtocolError("segment_features ran outside a worker context");
   if (!wc.gpu) throw DeviceError("segment_features GPU variant scheduled without a GpuDevice");
   RegionTemplate& local = *wc.local;
+  const SegmentationRegions ids = resolve_regions(local, names);
   const DataRegion* rgb = local.get_data_region(ids.rgb);
   if (!rgb) throw NotFoundError("stage input " + ids.rgb.to_string() + " missing");
   const BoundingBox& b3 = rgb->bbox();

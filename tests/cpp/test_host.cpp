@@ -213,8 +213,9 @@ void scheduling() {
 extern "C" int rtg_synth_tile_host(uint64_t, int64_t, int64_t, int64_t, int64_t, uint8_t*);
 
 // The oracle as the CPU variant of "segment_features" (test-only drop-in twin).
-void cpu_segment_features(const SegmentationRegions& ids, const rtg_params& p) {
+void cpu_segment_features(const SegmentationRegions& names, const rtg_params& p) {
   RegionTemplate& local = *worker_context().local;
+  const SegmentationRegions ids = resolve_regions(local, names);
   const DataRegion* rgb = local.get_data_region(ids.rgb);
   const BoundingBox& b3 = rgb->bbox();
   const std::int64_t h = b3.extent(0), w = b3.extent(1);
