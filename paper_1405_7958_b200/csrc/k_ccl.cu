@@ -25,19 +25,36 @@ __device__ __forceinline__ int32_t find_root(const int32_t* par, int32_t a) {
   return a;
 }
 
+// Global find with path halving.  Only non-root entries are rewritten, and
+// only to an ancestor, so concurrent unions (which touch roots only) stay
+// correct: a non-root never becomes a root again.
 __device__ __forceinline__ int32_t find_root_g(int32_t* par, int32_t a) {
   int32_t p = __ldcg(par + a);
   while (p != a) {
+    const int32_t gp = __ldcg(par + p);
+    if (gp != p) __stcg(par + a, gp);
     a = p;
-    p = __ldcg(par + a);
+    p = gp;
+  }
+  return a;
+}
+
+// Shared-memory find with path halving (same argument as above).
+__device__ __forceinline__ int32_t find_root_c(int32_t* par, int32_t a) {
+  int32_t p = par[a];
+  while (p != a) {
+    const int32_t gp = par[p];
+    if (gp != p) par[a] = gp;
+    a = p;
+    p = gp;
   }
   return a;
 }
 
 __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
   while (true) {
-    a = find_root(par, a);
-    b = find_root(par, b);
+    a = find_root_c(par, a);
+    b = find_root_c(par, b);
     if (a == b) return;
     if (a < b) { const int32_t t = a; a = b; b = t; }  // a is the larger root
     const int32_t old = atomicMin(&par[a], b);
@@ -64,33 +81,51 @@ k_ccl_local(const uint8_t* __restrict__ mask, int h, int w,
             int32_t* __restrict__ roots) {
   __shared__ int32_t par[1024];
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  __shared__ uint32_t rowbits[32];
   const int c = threadIdx.x & 31, rb = threadIdx.x >> 5;
   bool fg[4];
+  // 1. rows as bit masks; every pixel points at the start of its horizontal
+  //    run (no unions needed inside a run)
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = rb + 8 * k, y = y0 + r, x = x0 + c;
     fg[k] = y < h && x < w && mask[(int64_t)y * w + x];
-    par[r * 32 + c] = fg[k] ? r * 32 + c : -1;
+    const uint32_t bits = __ballot_sync(0xFFFFFFFFu, fg[k]);
+    if (c == 0) rowbits[r] = bits;
+    int32_t v = -1;
+    if (fg[k]) {
+      const uint32_t upto = c == 31 ? 0xFFFFFFFFu : ((2u << c) - 1u);
+      const uint32_t zeros = ~bits & upto;  // background at or left of c
+      const int start = zeros ? 32 - __clz(zeros) : 0;
+      v = r * 32 + start;
+    }
+    par[r * 32 + c] = v;
   }
   __syncthreads();
+  // 2. one union per run adjacency with the row above: at the first pixel of
+  //    every vertical overlap, plus the two diagonal run-end contacts (8-conn)
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (!fg[k]) continue;
-    const int r = rb + 8 * k, i = r * 32 + c;
-    if (c > 0 && par[i - 1] >= 0) unite_s(par, i, i - 1);
-    if (r > 0) {
-      if (par[i - 32] >= 0) unite_s(par, i, i - 32);
-      if (CONN == 8) {
-        if (c > 0 && par[i - 33] >= 0) unite_s(par, i, i - 33);
-        if (c < 31 && par[i - 31] >= 0) unite_s(par, i, i - 31);
-      }
+    const int r = rb + 8 * k;
+    if (!fg[k] || r == 0) continue;
+    const int i = r * 32 + c;
+    const uint32_t up = rowbits[r - 1], cur = rowbits[r];
+    const bool a = (up >> c) & 1u;
+    const bool aL = c > 0 && ((up >> (c - 1)) & 1u);
+    const bool aR = c < 31 && ((up >> (c + 1)) & 1u);
+    const bool cL = c > 0 && ((cur >> (c - 1)) & 1u);
+    const bool cR = c < 31 && ((cur >> (c + 1)) & 1u);
+    if (a && !(cL && aL)) unite_s(par, i, i - 32);
+    if (CONN == 8) {
+      if (!a && aL && !cL) unite_s(par, i, i - 33);
+      if (!a && aR && !cR) unite_s(par, i, i - 31);
     }
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = rb + 8 * k, i = r * 32 + c;
-    if (fg[k]) par[i] = find_root(par, i);
+    if (fg[k]) par[i] = find_root_c(par, i);
   }
   __syncthreads();
 #pragma unroll

@@ -10,10 +10,16 @@
 // one owner per tile; a global `pending` counter terminates the persistent
 // grid without host round trips.
 //
+// When every tile starts active (grayscale reconstruction), the first visit
+// of each tile is statically assigned (warp w takes tiles w, w+W, ...) instead
+// of going through the queue, and pushes are batched per visit, so the hot
+// queue counters only see the (much smaller) wavefront traffic.
+//
 // Reconstruction by dilation is the greatest fixed point below the mask
 // reachable from the marker, so the result is independent of the order in
 // which tiles and pixels are relaxed: stale halo reads only cost extra
 // visits, never correctness (values only increase and stay <= the answer).
+// Precondition: J <= I everywhere on entry (callers clip).
 //
 // Roofline: HBM/L2 bound; algorithmic bytes 3 B/px (u8: marker + mask in,
 // result out) or 6 B/px (u16).  Revisits are the IWPP overhead.
@@ -55,29 +61,37 @@ __device__ __forceinline__ uint32_t ld_state<uint8_t>(const uint8_t* p) {
 
 // ---- queue primitives (lane 0 only) ----------------------------------------
 
-__device__ void q_push(const TileQueue& q, int32_t cap, int32_t t) {
+// Marks tile t for processing.  Returns true when the caller must enqueue it
+// (state went idle -> queued); a queued tile stays queued, a tile being
+// processed is marked dirty (its owner re-runs it).
+__device__ bool q_mark(const TileQueue& q, int32_t t) {
   int32_t s = atomicAdd(&q.state[t], 0);
   while (true) {
-    if (s == 1 || s == 3) return;  // already queued / already marked dirty
+    if (s == 1 || s == 3) return false;
     if (s == 0) {
       const int32_t old = atomicCAS(&q.state[t], 0, 1);
-      if (old == 0) {
-        atomicAdd(&q.counters[2], 1u);  // pending, before publication
-        const uint32_t pos = atomicAdd(&q.counters[1], 1u);
-        int32_t* slot = &q.slots[pos % (uint32_t)cap];
-        while (atomicCAS(slot, 0, t + 1) != 0) __nanosleep(32);
-        return;
-      }
+      if (old == 0) return true;
       s = old;
-    } else {  // s == 2: being processed -> mark dirty
+    } else {
       const int32_t old = atomicCAS(&q.state[t], 2, 3);
-      if (old == 2) return;
+      if (old == 2) return false;
       s = old;
     }
   }
 }
 
-// Returns a tile id, or -1 when all work is done.
+// Publishes k marked tiles with one pending and one tail update.
+__device__ void q_enqueue(const TileQueue& q, int32_t cap, const int32_t* ids, int k) {
+  if (k == 0) return;
+  atomicAdd(&q.counters[2], (uint32_t)k);  // pending, before publication
+  const uint32_t pos = atomicAdd(&q.counters[1], (uint32_t)k);
+  for (int i = 0; i < k; ++i) {
+    int32_t* slot = &q.slots[(pos + (uint32_t)i) % (uint32_t)cap];
+    while (atomicCAS(slot, 0, ids[i] + 1) != 0) __nanosleep(32);
+  }
+}
+
+// Returns a tile id, or -1 when all work is done (or the run was aborted).
 __device__ int32_t q_pop(const TileQueue& q, int32_t cap) {
   const uint32_t pos = atomicAdd(&q.counters[0], 1u);
   int32_t* slot = &q.slots[pos % (uint32_t)cap];
@@ -89,7 +103,7 @@ __device__ int32_t q_pop(const TileQueue& q, int32_t cap) {
       return v - 1;
     }
     if (*(volatile uint32_t*)&q.counters[2] == 0u) return -1;
-    if (*(volatile uint32_t*)&q.counters[4] != 0u) return -1;  // aborted
+    if (*(volatile uint32_t*)&q.counters[4] != 0u) return -1;
     __nanosleep(64);
   }
 }
@@ -106,211 +120,239 @@ __device__ bool q_finish(const TileQueue& q, int32_t t) {
   return true;
 }
 
+// ---- one tile visit ------------------------------------------------------------
+
+template <typename T, int CONN, class MaskF>
+__device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int h, int w,
+                           int tiles_x, const TileQueue& q, int32_t cap, uint32_t* Js,
+                           uint32_t* Is, long long& visits) {
+  const unsigned full = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const int ty = t / tiles_x, tx = t - ty * tiles_x;
+  const int tiles_y = (h + kTile - 1) / kTile;
+  const int y0 = ty * kTile, x0 = tx * kTile;
+  const int x = x0 + lane;
+
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const int y = y0 + r;
+    Is[r * kIS + lane] = (y < h && x < w) ? maskf((int64_t)y * w + x) : 0u;
+  }
+  bool dirty_reload = false;
+  do {
+    bool tile_changed = false;
+    // (re)load J: full tile on the first pass, halo only on a dirty reload
+    if (!dirty_reload) {
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int y = y0 + r;
+        uint32_t v = 0;
+        if (y < h && x < w) {
+          const uint32_t j = ld_state(J + (int64_t)y * w + x);
+          const uint32_t m = Is[r * kIS + lane];
+          v = j < m ? j : m;
+          if (v != j) tile_changed = true;  // defensive: marker above the mask
+        }
+        Js[(r + 1) * kJS + lane + 1] = v;
+      }
+    }
+    {
+      const int yt = y0 - 1, yb = y0 + 32;
+      Js[lane + 1] = (yt >= 0 && x < w) ? ld_state(J + (int64_t)yt * w + x) : 0u;
+      Js[33 * kJS + lane + 1] = (yb < h && x < w) ? ld_state(J + (int64_t)yb * w + x) : 0u;
+      for (int k = lane; k < 34; k += 32) {
+        const int y = y0 - 1 + k;
+        const bool yin = y >= 0 && y < h;
+        Js[k * kJS + 0] = (yin && x0 > 0) ? ld_state(J + (int64_t)y * w + x0 - 1) : 0u;
+        Js[k * kJS + 33] = (yin && x0 + 32 < w) ? ld_state(J + (int64_t)y * w + x0 + 32) : 0u;
+      }
+    }
+    __syncwarp();
+    const uint32_t top0 = Js[1 * kJS + lane + 1];
+    const uint32_t bot0 = Js[32 * kJS + lane + 1];
+    const uint32_t left0 = Js[(lane + 1) * kJS + 1];
+    const uint32_t right0 = Js[(lane + 1) * kJS + 32];
+
+    // a tile already at its upper bound (J == mask everywhere, e.g. an
+    // all-background tile of a distance map) cannot change: skip the sweeps
+    bool saturated = true;
+    for (int r = 0; r < 32; ++r) saturated &= Js[(r + 1) * kJS + lane + 1] == Is[r * kIS + lane];
+    bool iter_changed = !__all_sync(full, saturated);
+    while (iter_changed) {
+      bool ch = false;
+      // down: lane = column c, rows 0..31, neighbours in the row above
+      for (int r = 0; r < 32; ++r) {
+        uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+        const uint32_t* up = row - kJS;
+        uint32_t n = up[0];
+        if (CONN == 8) n = max(n, max(up[-1], up[1]));
+        const uint32_t v = *row;
+        const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+        if (nv != v) { *row = nv; ch = true; }
+        __syncwarp();
+      }
+      // up
+      for (int r = 31; r >= 0; --r) {
+        uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+        const uint32_t* dn = row + kJS;
+        uint32_t n = dn[0];
+        if (CONN == 8) n = max(n, max(dn[-1], dn[1]));
+        const uint32_t v = *row;
+        const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+        if (nv != v) { *row = nv; ch = true; }
+        __syncwarp();
+      }
+      // right: lane = row r, columns 0..31, neighbours in the column left
+      for (int c = 0; c < 32; ++c) {
+        uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+        const uint32_t* lf = px - 1;
+        uint32_t n = lf[0];
+        if (CONN == 8) n = max(n, max(lf[-kJS], lf[kJS]));
+        const uint32_t v = *px;
+        const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+        if (nv != v) { *px = nv; ch = true; }
+        __syncwarp();
+      }
+      // left
+      for (int c = 31; c >= 0; --c) {
+        uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+        const uint32_t* rt = px + 1;
+        uint32_t n = rt[0];
+        if (CONN == 8) n = max(n, max(rt[-kJS], rt[kJS]));
+        const uint32_t v = *px;
+        const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+        if (nv != v) { *px = nv; ch = true; }
+        __syncwarp();
+      }
+      iter_changed = __any_sync(full, ch);
+      tile_changed |= iter_changed;
+    }
+    ++visits;
+    tile_changed = __any_sync(full, tile_changed);
+    if (tile_changed) {
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int y = y0 + r;
+        if (y < h && x < w) J[(int64_t)y * w + x] = (T)Js[(r + 1) * kJS + lane + 1];
+      }
+      __threadfence();
+    }
+
+    // which neighbours did we raise?  A border pixel must have changed in this
+    // visit and exceed the neighbour's value we saw (stale halo only
+    // over-approximates).  Diagonal neighbours need the corner itself to have
+    // changed: static corner inequalities alone could cycle forever.
+    bool pn = false, ps = false, pw = false, pe = false;
+    if (tile_changed) {
+      const uint32_t tv = Js[1 * kJS + lane + 1];
+      const uint32_t bv = Js[32 * kJS + lane + 1];
+      const uint32_t lv = Js[(lane + 1) * kJS + 1];
+      const uint32_t rv = Js[(lane + 1) * kJS + 32];
+      uint32_t nt = Js[lane + 1], nb = Js[33 * kJS + lane + 1];
+      uint32_t nl = Js[(lane + 1) * kJS], nr = Js[(lane + 1) * kJS + 33];
+      if (CONN == 8) {
+        nt = min(nt, min(Js[lane], Js[lane + 2]));
+        nb = min(nb, min(Js[33 * kJS + lane], Js[33 * kJS + lane + 2]));
+        nl = min(nl, min(Js[lane * kJS], Js[(lane + 2) * kJS]));
+        nr = min(nr, min(Js[lane * kJS + 33], Js[(lane + 2) * kJS + 33]));
+      }
+      pn = __any_sync(full, tv != top0 && tv > nt);
+      ps = __any_sync(full, bv != bot0 && bv > nb);
+      pw = __any_sync(full, lv != left0 && lv > nl);
+      pe = __any_sync(full, rv != right0 && rv > nr);
+    }
+    const uint32_t c00_0 = __shfl_sync(full, top0, 0), c01_0 = __shfl_sync(full, top0, 31);
+    const uint32_t c10_0 = __shfl_sync(full, bot0, 0), c11_0 = __shfl_sync(full, bot0, 31);
+    int again = 0;
+    if (lane == 0) {
+      int32_t ids[8];
+      int k = 0;
+      auto mark = [&](bool cond, int32_t nt) {
+        if (cond && q_mark(q, nt)) ids[k++] = nt;
+      };
+      mark(pn && ty > 0, t - tiles_x);
+      mark(ps && ty + 1 < tiles_y, t + tiles_x);
+      mark(pw && tx > 0, t - 1);
+      mark(pe && tx + 1 < tiles_x, t + 1);
+      if (CONN == 8 && tile_changed) {
+        const uint32_t c00 = Js[1 * kJS + 1], c01 = Js[1 * kJS + 32];
+        const uint32_t c10 = Js[32 * kJS + 1], c11 = Js[32 * kJS + 32];
+        mark(ty > 0 && tx > 0 && c00 != c00_0 && c00 > Js[0], t - tiles_x - 1);
+        mark(ty > 0 && tx + 1 < tiles_x && c01 != c01_0 && c01 > Js[33], t - tiles_x + 1);
+        mark(ty + 1 < tiles_y && tx > 0 && c10 != c10_0 && c10 > Js[33 * kJS], t + tiles_x - 1);
+        mark(ty + 1 < tiles_y && tx + 1 < tiles_x && c11 != c11_0 && c11 > Js[33 * kJS + 33],
+             t + tiles_x + 1);
+      }
+      q_enqueue(q, cap, ids, k);
+      again = q_finish(q, t) ? 1 : 0;
+    }
+    again = __shfl_sync(full, again, 0);
+    dirty_reload = again != 0;
+  } while (dirty_reload);
+}
+
 // ---- the persistent kernel ---------------------------------------------------
 
 template <typename T, int CONN, class MaskF>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x,
-       TileQueue q, int32_t cap, int64_t* visits, uint32_t max_visits,
+k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
+       int static_first, TileQueue q, int32_t cap, int64_t* visits, uint32_t max_visits,
        uint32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xFFFFFFFFu;
-  uint32_t* Js = S.J;
-  uint32_t* Is = S.I;
-  long long my_visits = 0;
+  long long my_visits = 0, charged = 0;
 
-  while (true) {
-    int32_t t = 0;
-    if (lane == 0) {
-      t = q_pop(q, cap);
-      // visit budget: a bug that livelocks the queue must not hang the GPU;
-      // exceeding it aborts every warp and raises a sticky status bit
-      if (t >= 0 && atomicAdd(&q.counters[3], 1u) > max_visits) {
+  // budget: a bug that livelocks the queue must not hang the GPU; exceeding
+  // it aborts every warp and raises a sticky status bit
+  auto over_budget = [&]() -> bool {
+    int bad = 0;
+    if (lane == 0 && my_visits - charged >= 32) {
+      const uint32_t prev = atomicAdd(&q.counters[3], (uint32_t)(my_visits - charged));
+      charged = my_visits;
+      if (prev > max_visits) {
         atomicExch(&q.counters[4], 1u);
         atomicOr(status, kStatusQueueOverflow);
-        t = -1;
+        bad = 1;
       }
     }
-    t = __shfl_sync(full, t, 0);
-    if (t < 0) break;
-    const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    const int y0 = ty * kTile, x0 = tx * kTile;
-    const int x = x0 + lane;
+    return __shfl_sync(full, bad, 0) != 0 ||
+           *(volatile uint32_t*)&q.counters[4] != 0u;
+  };
 
-    // stage mask (interior) and J (interior + halo)
-#pragma unroll 4
-    for (int r = 0; r < 32; ++r) {
-      const int y = y0 + r;
-      const bool in = y < h && x < w;
-      Is[r * kIS + lane] = in ? maskf((int64_t)y * w + x) : 0u;
-    }
-    bool dirty_reload = false;
-    bool tile_changed = false;
-    uint32_t top0, bot0, left0, right0;
-    do {
-      // (re)load J: full tile on first visit, halo only on a dirty reload
-      if (!dirty_reload) {
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-          const int y = y0 + r;
-          uint32_t v = 0;
-          if (y < h && x < w) {
-            const uint32_t j = ld_state(J + (int64_t)y * w + x);
-            const uint32_t m = Is[r * kIS + lane];
-            v = j < m ? j : m;
-            if (v != j) tile_changed = true;  // marker clipped to the mask
-          }
-          Js[(r + 1) * kJS + lane + 1] = v;
-        }
-      }
-      {
-        const int yt = y0 - 1, yb = y0 + 32;
-        Js[lane + 1] = (yt >= 0 && x < w) ? ld_state(J + (int64_t)yt * w + x) : 0u;
-        Js[33 * kJS + lane + 1] = (yb < h && x < w) ? ld_state(J + (int64_t)yb * w + x) : 0u;
-        for (int k = lane; k < 34; k += 32) {
-          const int y = y0 - 1 + k;
-          const bool yin = y >= 0 && y < h;
-          Js[k * kJS + 0] = (yin && x0 > 0) ? ld_state(J + (int64_t)y * w + x0 - 1) : 0u;
-          Js[k * kJS + 33] = (yin && x0 + 32 < w) ? ld_state(J + (int64_t)y * w + x0 + 32) : 0u;
-        }
-      }
-      __syncwarp();
-      top0 = Js[1 * kJS + lane + 1];
-      bot0 = Js[32 * kJS + lane + 1];
-      left0 = Js[(lane + 1) * kJS + 1];
-      right0 = Js[(lane + 1) * kJS + 32];
-
-      // a tile already at its upper bound (J == mask everywhere, e.g. an
-      // all-background tile of a distance map) cannot change: skip the sweeps
-      bool saturated = true;
-      for (int r = 0; r < 32; ++r)
-        saturated &= Js[(r + 1) * kJS + lane + 1] == Is[r * kIS + lane];
-      saturated = __all_sync(full, saturated);
-
-      // local fixed point
-      bool iter_changed = !saturated;
-      while (iter_changed) {
-        bool ch = false;
-        // down: lane = column c, rows 0..31, neighbours in the row above
-        for (int r = 0; r < 32; ++r) {
-          uint32_t* row = Js + (r + 1) * kJS + lane + 1;
-          const uint32_t* up = row - kJS;
-          uint32_t n = up[0];
-          if (CONN == 8) n = max(n, max(up[-1], up[1]));
-          const uint32_t v = *row;
-          const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
-          if (nv != v) { *row = nv; ch = true; }
-          __syncwarp();
-        }
-        // up
-        for (int r = 31; r >= 0; --r) {
-          uint32_t* row = Js + (r + 1) * kJS + lane + 1;
-          const uint32_t* dn = row + kJS;
-          uint32_t n = dn[0];
-          if (CONN == 8) n = max(n, max(dn[-1], dn[1]));
-          const uint32_t v = *row;
-          const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
-          if (nv != v) { *row = nv; ch = true; }
-          __syncwarp();
-        }
-        // right: lane = row r, columns 0..31, neighbours in the column left
-        for (int c = 0; c < 32; ++c) {
-          uint32_t* px = Js + (lane + 1) * kJS + c + 1;
-          const uint32_t* lf = px - 1;
-          uint32_t n = lf[0];
-          if (CONN == 8) n = max(n, max(lf[-kJS], lf[kJS]));
-          const uint32_t v = *px;
-          const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
-          if (nv != v) { *px = nv; ch = true; }
-          __syncwarp();
-        }
-        // left
-        for (int c = 31; c >= 0; --c) {
-          uint32_t* px = Js + (lane + 1) * kJS + c + 1;
-          const uint32_t* rt = px + 1;
-          uint32_t n = rt[0];
-          if (CONN == 8) n = max(n, max(rt[-kJS], rt[kJS]));
-          const uint32_t v = *px;
-          const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
-          if (nv != v) { *px = nv; ch = true; }
-          __syncwarp();
-        }
-        iter_changed = __any_sync(full, ch);
-        tile_changed |= iter_changed;
-      }
-
-      ++my_visits;
-      if (tile_changed) {
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-          const int y = y0 + r;
-          if (y < h && x < w) J[(int64_t)y * w + x] = (T)Js[(r + 1) * kJS + lane + 1];
-        }
+  if (static_first) {
+    const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * kWarpsPerBlock;
+    for (int t = warp; t < ntiles; t += nwarps) {
+      if (lane == 0) {
+        atomicExch(&q.state[t], 2);
         __threadfence();
       }
-
-      // which neighbours did we raise?  (stale halo only over-approximates)
-      const uint32_t tv = Js[1 * kJS + lane + 1];
-      const uint32_t bv = Js[32 * kJS + lane + 1];
-      const uint32_t lv = Js[(lane + 1) * kJS + 1];
-      const uint32_t rv = Js[(lane + 1) * kJS + 32];
-      bool pn, ps, pw, pe;
-      {
-        uint32_t nt = Js[lane + 1], nb = Js[33 * kJS + lane + 1];
-        uint32_t nl = Js[(lane + 1) * kJS], nr = Js[(lane + 1) * kJS + 33];
-        if (CONN == 8) {
-          nt = min(nt, min(Js[lane], Js[lane + 2]));
-          nb = min(nb, min(Js[33 * kJS + lane], Js[33 * kJS + lane + 2]));
-          nl = min(nl, min(Js[lane * kJS], Js[(lane + 2) * kJS]));
-          nr = min(nr, min(Js[lane * kJS + 33], Js[(lane + 2) * kJS + 33]));
-        }
-        pn = __any_sync(full, tv != top0 && tv > nt);
-        ps = __any_sync(full, bv != bot0 && bv > nb);
-        pw = __any_sync(full, lv != left0 && lv > nl);
-        pe = __any_sync(full, rv != right0 && rv > nr);
-      }
-      // corner values at the start of this visit (diagonal neighbours):
-      // a diagonal push needs the corner to have CHANGED in this visit, else
-      // static corner inequalities between tiles could cycle forever
-      const uint32_t c00_0 = __shfl_sync(full, top0, 0), c01_0 = __shfl_sync(full, top0, 31);
-      const uint32_t c10_0 = __shfl_sync(full, bot0, 0), c11_0 = __shfl_sync(full, bot0, 31);
-      if (lane == 0) {
-        const int tiles_y = (h + kTile - 1) / kTile;
-        if (pn && ty > 0) q_push(q, cap, t - tiles_x);
-        if (ps && ty + 1 < tiles_y) q_push(q, cap, t + tiles_x);
-        if (pw && tx > 0) q_push(q, cap, t - 1);
-        if (pe && tx + 1 < tiles_x) q_push(q, cap, t + 1);
-        if (CONN == 8) {
-          const uint32_t c00 = Js[1 * kJS + 1], c01 = Js[1 * kJS + 32];
-          const uint32_t c10 = Js[32 * kJS + 1], c11 = Js[32 * kJS + 32];
-          if (ty > 0 && tx > 0 && c00 != c00_0 && c00 > Js[0])
-            q_push(q, cap, t - tiles_x - 1);
-          if (ty > 0 && tx + 1 < tiles_x && c01 != c01_0 && c01 > Js[33])
-            q_push(q, cap, t - tiles_x + 1);
-          if (ty + 1 < tiles_y && tx > 0 && c10 != c10_0 && c10 > Js[33 * kJS])
-            q_push(q, cap, t + tiles_x - 1);
-          if (ty + 1 < tiles_y && tx + 1 < tiles_x && c11 != c11_0 && c11 > Js[33 * kJS + 33])
-            q_push(q, cap, t + tiles_x + 1);
-        }
-      }
-      int again = 0;
-      if (lane == 0) again = q_finish(q, t) ? 1 : 0;
-      again = __shfl_sync(full, again, 0);
-      dirty_reload = again != 0;
-      tile_changed = false;
-    } while (dirty_reload);
+      __syncwarp();
+      visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits);
+      if (over_budget()) break;
+    }
+  }
+  while (true) {
+    int32_t t = 0;
+    if (lane == 0) t = q_pop(q, cap);
+    t = __shfl_sync(full, t, 0);
+    if (t < 0) break;
+    visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits);
+    if (over_budget()) break;
   }
   if (lane == 0 && visits) atomicAdd((unsigned long long*)visits, (unsigned long long)my_visits);
 }
 
-// Queue initialisation: mode 0 = every tile, mode 1 = border tiles only.
+// Queue initialisation.  mode 0: every tile starts active (state queued,
+// visited by the static first pass, nothing in the slot ring); mode 1: only
+// border tiles, published in the slot ring.
 __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
                              int border_only) {
   const int ntiles = tiles_y * tiles_x;
-  // single block: compute the list deterministically
   __shared__ int32_t count;
+  __shared__ int32_t warp_cnt[32];
   if (threadIdx.x == 0) count = 0;
   __syncthreads();
   for (int base = 0; base < ntiles; base += blockDim.x) {
@@ -320,9 +362,12 @@ __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
       const int ty = t / tiles_x, tx = t - ty * tiles_x;
       take = !border_only || ty == 0 || tx == 0 || ty == tiles_y - 1 || tx == tiles_x - 1;
     }
+    if (!border_only) {
+      if (t < ntiles) q.state[t] = 1;
+      continue;
+    }
     // order-preserving compaction within the chunk
     const unsigned b = __ballot_sync(0xFFFFFFFFu, take);
-    __shared__ int32_t warp_cnt[32];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) warp_cnt[wid] = __popc(b);
     __syncthreads();
@@ -339,11 +384,12 @@ __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
     }
     __syncthreads();
   }
-  for (int i = count + threadIdx.x; i < cap; i += blockDim.x) q.slots[i] = 0;
+  const int queued = border_only ? count : 0;
+  for (int i = queued + threadIdx.x; i < cap; i += blockDim.x) q.slots[i] = 0;
   if (threadIdx.x == 0) {
     q.counters[0] = 0;
-    q.counters[1] = (uint32_t)count;
-    q.counters[2] = (uint32_t)count;
+    q.counters[1] = (uint32_t)queued;
+    q.counters[2] = (uint32_t)(border_only ? count : ntiles);  // pending
     q.counters[3] = 0;  // visits
     q.counters[4] = 0;  // abort flag
   }
@@ -371,8 +417,7 @@ __global__ void k_fill_final(const uint8_t* __restrict__ bin,
 }
 
 template <typename T, int CONN, class MaskF>
-int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w,
-             int border_only) {
+int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_only) {
   const int tiles_y = (int)ceil_div(h, kTile), tiles_x = (int)ceil_div(w, kTile);
   const int ntiles = tiles_y * tiles_x;
   const int32_t cap = 2 * ntiles;
@@ -394,8 +439,8 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w,
   const int need = (int)ceil_div(ntiles, kWarpsPerBlock);
   if (blocks > need) blocks = need;
   k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
-      J, maskf, (int)h, (int)w, tiles_x, ctx->tq, cap, ctx->stats + 1,
-      (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
+      J, maskf, (int)h, (int)w, tiles_x, ntiles, border_only ? 0 : 1, ctx->tq, cap,
+      ctx->stats + 1, (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
   RTG_LAUNCH("k_iwpp");
   return RTG_OK;
 }

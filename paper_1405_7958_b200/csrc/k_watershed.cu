@@ -82,6 +82,37 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
   }
 }
 
+// One grid-wide relaxation pass over the plateau list (chaotic Bellman-Ford:
+// values only decrease and always equal the length of some real path, so
+// passes in any order converge to the unique fixed point).  A few of these
+// resolve almost every plateau before the single-CTA pass below, which owns
+// the convergence test, has to iterate.
+__global__ void __launch_bounds__(256)
+k_ws_plateau_relax(int h, int w, const uint16_t* __restrict__ Fw,
+                   const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
+                   int32_t* delta) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int y = i / w, x = i - y * w;
+    const uint32_t f = Fw[i];
+    const int32_t cur = __ldcg(&delta[i]);
+    int32_t best = cur;
+    for (int dy = -1; dy <= 1; ++dy) {
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (dy == 0 && dx == 0) continue;
+        const int yy = y + dy, xx = x + dx;
+        if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+        const int32_t j = yy * w + xx;
+        if (Fw[j] != f) continue;
+        const int32_t dj = __ldcg(&delta[j]);
+        if (dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
+      }
+    }
+    if (best < cur) __stcg(&delta[i], best);
+  }
+}
+
 // BFS distances inside non-maximal plateaus (Bellman-Ford to the fixed point,
 // one CTA), then arrows down the distance.
 __global__ void __launch_bounds__(1024)
@@ -212,6 +243,11 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_arrows");
   int32_t* mroots = ctx->i32c;
   RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
+  for (int pass = 0; pass < 8; ++pass) {
+    k_ws_plateau_relax<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
+                                                                  ctx->flat_list, flat_count, delta);
+    RTG_LAUNCH("k_ws_plateau_relax");
+  }
   k_ws_plateau<<<1, 1024, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count,
                                             delta, ptr);
   RTG_LAUNCH("k_ws_plateau");
