@@ -106,6 +106,7 @@ struct rtg_ctx {
   int32_t* seg_summary = nullptr;  // EDT column-segment summaries
   int32_t* scan_buf = nullptr;     // CCL compaction per-chunk counts/offsets
   int32_t* flat_list = nullptr;    // watershed plateau pixel list
+  int32_t* lroots = nullptr;       // CCL tile-local root list (max_px)
   int32_t* misc = nullptr;         // [0] n_objects, [1] flat count, [2] any_zero, [3] changed, ...
   uint32_t* status = nullptr;      // sticky status bits
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
@@ -168,9 +169,16 @@ int iwpp_recon_u16(rtg_ctx* ctx, uint16_t* J, const uint16_t* I, int64_t h,
 int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
                     int64_t w, uint8_t* out);
 
-// Union-find CCL: roots[p] = min linear index of p's component (-1 = bg).
+// Union-find CCL into a two-level forest: roots[p] is p's tile-local root
+// (or, for a local root, the global root); root_of(roots, p) is the minimum
+// linear index of p's component (-1 = background).  zero_at_roots, when
+// given, is zeroed at every global root (per-object counters / flags).
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots);
+              int conn, int32_t* roots, int32_t* zero_at_roots = nullptr);
+__device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, int64_t i) {
+  const int32_t v = roots[i];
+  return v < 0 ? -1 : roots[v];
+}
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n);

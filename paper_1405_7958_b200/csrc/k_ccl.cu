@@ -2,13 +2,21 @@
 // (Oliveira & Lotufo union-find: "a forest in which each
 // pixel is a tree ... merges adjacent trees ... flattening the trees").
 //
-// 1. k_ccl_local   one CTA per 32x32 tile: union-find in shared memory.
-// 2. k_ccl_border  union across tile seams in global memory (atomicMin links).
-// 3. k_ccl_flatten path compression; every root is the minimum linear index
-//                  of its component because links always go larger->smaller.
-// 4. canonical compaction: roots ranked in raster order by a chunked scan, so
-//    labels are 1..n ordered by each object's minimum pixel index (scipy's
-//    ndimage.label order).
+// 1. k_ccl_local   one CTA per 32x32 tile.  Each row is a ballot bit mask, so
+//                  a pixel's horizontal run needs no union at all (it points at
+//                  the run start); vertical unions are issued once per run
+//                  adjacency; shared-memory union-find with path halving.
+//                  Every tile-local root is appended to a short global list.
+// 2. k_ccl_seam_*  union across tile seams in global memory (atomicMin links,
+//                  larger root -> smaller root, path halving).
+// 3. k_ccl_flatten_roots  only the local roots are flattened, so the forest
+//                  is two-level: pixel -> local root -> global root, and
+//                  consumers read root_of(i) = roots[roots[i]] instead of a
+//                  full-image flatten pass.  The global root is the minimum
+//                  linear index of the component.
+// 4. canonical compaction: global roots ranked in raster order by a chunked
+//    scan, so labels are 1..n ordered by each object's minimum pixel index
+//    (scipy's ndimage.label order).
 //
 // Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + labels 4 B out.
 #include "common.cuh"
@@ -16,30 +24,23 @@
 namespace rtg {
 namespace {
 
-__device__ __forceinline__ int32_t find_root(const int32_t* par, int32_t a) {
-  int32_t p = par[a];
-  while (p != a) {
-    a = p;
-    p = par[a];
-  }
-  return a;
-}
-
-// Global find with path halving.  Only non-root entries are rewritten, and
-// only to an ancestor, so concurrent unions (which touch roots only) stay
-// correct: a non-root never becomes a root again.
+// Global find with path halving by atomicMin: every link points to a
+// smaller index and the global root is the component minimum, so lowering an
+// entry to a grand-parent never passes the root and never disconnects a
+// node; concurrent unions only touch roots (entries equal to themselves).
 __device__ __forceinline__ int32_t find_root_g(int32_t* par, int32_t a) {
   int32_t p = __ldcg(par + a);
   while (p != a) {
     const int32_t gp = __ldcg(par + p);
-    if (gp != p) __stcg(par + a, gp);
+    if (gp != p) atomicMin(par + a, gp);
     a = p;
     p = gp;
   }
   return a;
 }
 
-// Shared-memory find with path halving (same argument as above).
+// Shared-memory find with path halving (plain stores are fine inside the CTA
+// for the same reason).
 __device__ __forceinline__ int32_t find_root_c(int32_t* par, int32_t a) {
   int32_t p = par[a];
   while (p != a) {
@@ -77,12 +78,14 @@ __device__ __forceinline__ void unite_g(int32_t* par, int32_t a, int32_t b) {
 
 template <int CONN>
 __global__ void __launch_bounds__(256)
-k_ccl_local(const uint8_t* __restrict__ mask, int h, int w,
-            int32_t* __restrict__ roots) {
+k_ccl_local(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__ roots,
+            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount) {
   __shared__ int32_t par[1024];
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   __shared__ uint32_t rowbits[32];
+  __shared__ int32_t n_local, base;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int c = threadIdx.x & 31, rb = threadIdx.x >> 5;
+  if (threadIdx.x == 0) n_local = 0;
   bool fg[4];
   // 1. rows as bit masks; every pixel points at the start of its horizontal
   //    run (no unions needed inside a run)
@@ -122,11 +125,18 @@ k_ccl_local(const uint8_t* __restrict__ mask, int h, int w,
     }
   }
   __syncthreads();
+  int slot[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = rb + 8 * k, i = r * 32 + c;
-    if (fg[k]) par[i] = find_root_c(par, i);
+    slot[k] = -1;
+    if (fg[k]) {
+      par[i] = find_root_c(par, i);
+      if (par[i] == i) slot[k] = atomicAdd(&n_local, 1);
+    }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) base = n_local ? atomicAdd(lcount, n_local) : 0;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -136,6 +146,7 @@ k_ccl_local(const uint8_t* __restrict__ mask, int h, int w,
       if (fg[k]) {
         const int32_t lr = par[r * 32 + c];
         out = (y0 + (lr >> 5)) * w + x0 + (lr & 31);
+        if (slot[k] >= 0) lroots[base + slot[k]] = out;
       }
       roots[(int64_t)y * w + x] = out;
     }
@@ -174,16 +185,16 @@ __global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
   }
 }
 
-// Path compression; zero per-root counters when requested.
-__global__ void k_ccl_flatten(int64_t n, int32_t* __restrict__ roots,
-                              int32_t* __restrict__ counts) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = roots[i];
-    if (v < 0) continue;
-    const int32_t r = find_root_g(roots, (int32_t)i);
-    if (r != v) roots[i] = r;
-    if (counts && r == (int32_t)i) counts[i] = 0;
+// Flattens the local roots only; zeroes per-root counters when requested.
+__global__ void k_ccl_flatten_roots(const int32_t* __restrict__ lroots,
+                                    const int32_t* __restrict__ lcount, int32_t* roots,
+                                    int32_t* __restrict__ zero) {
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t r = lroots[k];
+    const int32_t g = find_root_g(roots, r);
+    if (g != r) atomicMin(roots + r, g);
+    else if (zero) zero[r] = 0;
   }
 }
 
@@ -194,7 +205,7 @@ __global__ void k_area_count(int64_t n, const int32_t* __restrict__ roots,
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    const int32_t r = i < n ? roots[i] : -1;
+    const int32_t r = i < n ? root_of(roots, i) : -1;
     const unsigned act = __ballot_sync(full, r >= 0);
     if (r >= 0) {
       const unsigned grp = __match_any_sync(act, r);
@@ -208,7 +219,7 @@ __global__ void k_area_filter(int64_t n, const int32_t* __restrict__ roots,
                               int32_t hi, uint8_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = roots[i];
+    const int32_t r = root_of(roots, i);
     uint8_t keep = 0;
     if (r >= 0) {
       const int32_t a = counts[r];
@@ -241,6 +252,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
   return off + incl - v;
 }
 
+// global roots are exactly the pixels with roots[i] == i
 __global__ void __launch_bounds__(256)
 k_root_count(int64_t n, const int32_t* __restrict__ roots,
              int32_t* __restrict__ chunk_cnt) {
@@ -301,7 +313,7 @@ __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
                           int32_t* __restrict__ labels) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = roots[i];
+    const int32_t r = root_of(roots, i);
     labels[i] = r >= 0 ? rank[r] + 1 : 0;
   }
 }
@@ -330,7 +342,7 @@ __global__ void k_mark_border_roots(int h, int w, const int32_t* __restrict__ ro
   else if (k < 2 * w) { y = h - 1; x = k - w; }
   else if (k < 2 * w + h) { y = k - 2 * w; x = 0; }
   else { y = k - 2 * w - h; x = w - 1; }
-  const int32_t r = roots[(int64_t)y * w + x];
+  const int32_t r = root_of(roots, (int64_t)y * w + x);
   if (r >= 0) flag[r] = 1;
 }
 
@@ -339,38 +351,22 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
                                 const int32_t* __restrict__ flag, uint8_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = roots[i];
+    const int32_t r = root_of(roots, i);
     out[i] = (uint8_t)(bin[i] || (r >= 0 && !flag[r]));
   }
 }
 
 }  // namespace
 
-int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_t* scratch,
-                  uint8_t* out) {
-  const int64_t n = h * w;
-  k_invert<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, scratch);
-  RTG_LAUNCH("k_invert");
-  int32_t* roots = ctx->i32a;
-  int32_t* flag = ctx->i32b;
-  RTG_TRY(ccl_roots(ctx, scratch, h, w, 4, roots));
-  // zero the flags at root positions only (reuses the counter-zeroing pass)
-  k_ccl_flatten<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag);
-  RTG_LAUNCH("k_ccl_flatten(flags)");
-  const int per = (int)(2 * (h + w));
-  k_mark_border_roots<<<(unsigned)ceil_div(per, 256), 256, 0, ctx->stream>>>((int)h, (int)w,
-                                                                             roots, flag);
-  RTG_LAUNCH("k_mark_border_roots");
-  k_fill_uf_final<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, roots, flag, out);
-  RTG_LAUNCH("k_fill_uf_final");
-  return RTG_OK;
-}
-
-int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots) {
+int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
+              int32_t* roots, int32_t* zero_at_roots) {
+  int32_t* lcount = ctx->misc + 8;
+  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
   const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
-  if (conn == 8) k_ccl_local<8><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots);
-  else k_ccl_local<4><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots);
+  if (conn == 8)
+    k_ccl_local<8><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots, ctx->lroots, lcount);
+  else
+    k_ccl_local<4><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots, ctx->lroots, lcount);
   RTG_LAUNCH("k_ccl_local");
   if (tiles.y > 1) {
     const dim3 g((unsigned)ceil_div(w, 256), tiles.y - 1);
@@ -384,8 +380,9 @@ int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     else k_ccl_seam_cols<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
     RTG_LAUNCH("k_ccl_seam_cols");
   }
-  k_ccl_flatten<<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(h * w, roots, nullptr);
-  RTG_LAUNCH("k_ccl_flatten");
+  k_ccl_flatten_roots<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots,
+                                                                 zero_at_roots);
+  RTG_LAUNCH("k_ccl_flatten_roots");
   return RTG_OK;
 }
 
@@ -407,17 +404,31 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   return RTG_OK;
 }
 
-int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
-                int32_t min_area, int32_t max_area, int32_t* counts,
-                uint8_t* out) {
-  // roots are already flat; zero the counters at root positions only
-  k_ccl_flatten<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, const_cast<int32_t*>(roots), counts);
-  RTG_LAUNCH("k_ccl_flatten(counts)");
+int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
+                int32_t max_area, int32_t* counts, uint8_t* out) {
+  // counts were zeroed at the global roots by ccl_roots(..., counts)
   k_area_count<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts);
   RTG_LAUNCH("k_area_count");
   k_area_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts, min_area,
                                                          max_area, out);
   RTG_LAUNCH("k_area_filter");
+  return RTG_OK;
+}
+
+int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_t* scratch,
+                  uint8_t* out) {
+  const int64_t n = h * w;
+  k_invert<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, scratch);
+  RTG_LAUNCH("k_invert");
+  int32_t* roots = ctx->i32a;
+  int32_t* flag = ctx->i32b;
+  RTG_TRY(ccl_roots(ctx, scratch, h, w, 4, roots, flag));  // flags zeroed at roots
+  const int per = (int)(2 * (h + w));
+  k_mark_border_roots<<<(unsigned)ceil_div(per, 256), 256, 0, ctx->stream>>>((int)h, (int)w,
+                                                                             roots, flag);
+  RTG_LAUNCH("k_mark_border_roots");
+  k_fill_uf_final<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, roots, flag, out);
+  RTG_LAUNCH("k_fill_uf_final");
   return RTG_OK;
 }
 

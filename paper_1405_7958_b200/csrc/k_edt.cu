@@ -109,30 +109,27 @@ k_edt_row(const uint16_t* __restrict__ g, int h, int w,
   __syncthreads();
   const bool none = *any_zero == 0;
   bool unresolved = false;
+  // 32-bit arithmetic: g <= 8193 and k <= kCap, so k^2 + g^2 < 2^31
   for (int x = threadIdx.x; x < w; x += blockDim.x) {
     const uint32_t gx = gs[x];
-    int64_t best;
+    uint32_t best;
     if (none) {
       best = INT32_MAX;
     } else if (gx == 0) {
       best = 0;
     } else {
-      best = gx == kInfG ? INT64_MAX : (int64_t)gx * gx;
-      int k = 1;
-      for (; (int64_t)k * k < best && k <= kCap; ++k) {
-        const int64_t k2 = (int64_t)k * k;
-        if (x - k >= 0) {
-          const uint32_t gl = gs[x - k];
-          if (gl != kInfG) best = min(best, k2 + (int64_t)gl * gl);
-        }
-        if (x + k < w) {
-          const uint32_t gr = gs[x + k];
-          if (gr != kInfG) best = min(best, k2 + (int64_t)gr * gr);
-        }
+      best = gx == kInfG ? 0xFFFFFFFFu : gx * gx;
+      uint32_t k = 1;
+      for (; k * k < best && k <= (uint32_t)kCap; ++k) {
+        const uint32_t k2 = k * k;
+        const uint32_t gl = x >= (int)k ? gs[x - k] : kInfG;
+        const uint32_t gr = x + (int)k < w ? gs[x + k] : kInfG;
+        const uint32_t gm = min(gl, gr);
+        if (gm != kInfG) best = min(best, k2 + gm * gm);
       }
-      if ((int64_t)k * k < best) unresolved = true;  // hit the cap
+      if (k * k < best) unresolved = true;  // hit the cap: exact row pass below
     }
-    edt_emit(rb + x, best, dist2, dq, mk, ws_h);
+    edt_emit(rb + x, (int64_t)best, dist2, dq, mk, ws_h);
   }
   if (__syncthreads_or(unresolved) && threadIdx.x == 0) row_flag[y] = 1;
   else if (threadIdx.x == 0) row_flag[y] = 0;

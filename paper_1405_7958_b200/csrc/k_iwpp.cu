@@ -133,7 +133,9 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
   const int y0 = ty * kTile, x0 = tx * kTile;
   const int x = x0 + lane;
 
-#pragma unroll 4
+  // fully unrolled: all 32 row loads of a lane are in flight at once (the
+  // visit is latency-bound, not bandwidth-bound)
+#pragma unroll
   for (int r = 0; r < 32; ++r) {
     const int y = y0 + r;
     Is[r * kIS + lane] = (y < h && x < w) ? maskf((int64_t)y * w + x) : 0u;
@@ -143,7 +145,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
     bool tile_changed = false;
     // (re)load J: full tile on the first pass, halo only on a dirty reload
     if (!dirty_reload) {
-#pragma unroll 4
+#pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int y = y0 + r;
         uint32_t v = 0;
@@ -294,7 +296,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
 // ---- the persistent kernel ---------------------------------------------------
 
 template <typename T, int CONN, class MaskF>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
 k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
        int static_first, TileQueue q, int32_t cap, int64_t* visits, uint32_t max_visits,
        uint32_t* status) {

@@ -113,12 +113,13 @@ k_ws_plateau_relax(int h, int w, const uint16_t* __restrict__ Fw,
   }
 }
 
-// BFS distances inside non-maximal plateaus (Bellman-Ford to the fixed point,
-// one CTA), then arrows down the distance.
+// Convergence owner: Bellman-Ford passes in one CTA until a pass changes
+// nothing (after the grid-wide passes above this is normally one pass).
+// Loads are ld.global.cg (L2-coherent, batched), never volatile.
 __global__ void __launch_bounds__(1024)
 k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
              const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-             int32_t* delta, int32_t* __restrict__ ptr) {
+             int32_t* delta) {
   __shared__ int changed;
   const int n = *flat_count;
   if (n == 0) return;
@@ -130,27 +131,39 @@ k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
       const int32_t i = flat_list[k];
       const int y = i / w, x = i - y * w;
       const uint32_t f = Fw[i];
-      int32_t best = *(volatile int32_t*)&delta[i];
+      const int32_t cur = __ldcg(&delta[i]);
+      int32_t best = cur;
+#pragma unroll
       for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
         for (int dx = -1; dx <= 1; ++dx) {
           if (dy == 0 && dx == 0) continue;
           const int yy = y + dy, xx = x + dx;
           if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
           const int32_t j = yy * w + xx;
-          if (Fw[j] != f) continue;
-          const int32_t dj = *(volatile int32_t*)&delta[j];
-          if (dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
+          const int32_t dj = __ldcg(&delta[j]);
+          if (Fw[j] == f && dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
         }
       }
-      if (best < *(volatile int32_t*)&delta[i]) {
-        delta[i] = best;
+      if (best < cur) {
+        __stcg(&delta[i], best);
         changed = 1;
       }
     }
     __syncthreads();
     if (!changed) break;
   }
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+}
+
+// Arrows of plateau pixels: the same-level neighbour at distance delta-1
+// with the minimum linear index (grid-wide).
+__global__ void __launch_bounds__(256)
+k_ws_plateau_arrows(int h, int w, const uint16_t* __restrict__ Fw,
+                    const int32_t* __restrict__ flat_list,
+                    const int32_t* __restrict__ flat_count, const int32_t* __restrict__ delta,
+                    int32_t* __restrict__ ptr) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
     const int y = i / w, x = i - y * w;
     const uint32_t f = Fw[i];
@@ -183,7 +196,7 @@ __global__ void k_ws_resolve(int64_t n, const int32_t* __restrict__ ptr,
         q = nx;
         nx = ptr[q];
       }
-      b = nx == q ? mroots[q] + 1 : 0;
+      b = nx == q ? root_of(mroots, q) + 1 : 0;
     }
     basin[i] = b;
   }
@@ -243,14 +256,18 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_arrows");
   int32_t* mroots = ctx->i32c;
   RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
-  for (int pass = 0; pass < 8; ++pass) {
+  for (int pass = 0; pass < 6; ++pass) {
     k_ws_plateau_relax<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
                                                                   ctx->flat_list, flat_count, delta);
     RTG_LAUNCH("k_ws_plateau_relax");
   }
   k_ws_plateau<<<1, 1024, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count,
-                                            delta, ptr);
+                                            delta);
   RTG_LAUNCH("k_ws_plateau");
+  k_ws_plateau_arrows<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
+                                                                 ctx->flat_list, flat_count,
+                                                                 delta, ptr);
+  RTG_LAUNCH("k_ws_plateau_arrows");
   k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, ptr, mroots, basin);
   RTG_LAUNCH("k_ws_resolve");
   k_ws_separate<<<grid_for(ctx, n), 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);

@@ -111,7 +111,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   RTG_TRY(run_fill_holes(ctx, ctx->m1, h, w, ctx->m2));
   // o5 AreaThreshold
   prof_mark(ctx, RTG_STAGE_AREA);
-  RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a));
+  RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a, ctx->i32b));
   RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
   // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
   // watershed() marks its own EDT / MARKERS / WATERSHED stages
@@ -297,6 +297,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->seg_summary, (size_t)ceil_div(max_h, 32) * (size_t)max_w));
         RTG_TRY(dalloc(&c->scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
         RTG_TRY(dalloc(&c->flat_list, n));
+        RTG_TRY(dalloc(&c->lroots, n));
         RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
         RTG_TRY(dalloc(&c->status, 1));
         RTG_TRY(dalloc(&c->stats, 8));
@@ -327,7 +328,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
-                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->misc,
+                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots, c->misc,
                   c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs};
   for (void* b : bufs)
@@ -620,7 +621,7 @@ int rtg_area_threshold_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_mask || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
-  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a));
+  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a, ctx->i32b));
   return area_filter(ctx, ctx->i32a, h * w, min_area, max_area, ctx->i32b, d_out);
 }
 
