@@ -39,18 +39,20 @@ __global__ void __launch_bounds__(256)
 k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
              int h, int w, const int32_t* __restrict__ d_n, FeatureAcc acc) {
   const unsigned full = 0xFFFFFFFFu;
-  const int64_t n = (int64_t)h * w;
   const int nobj = min(*d_n, acc.cap);
   const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t l = i < n ? labels[i] : 0;
+  // 2-D grid-stride (rows x column chunks): a warp covers 32 consecutive
+  // pixels of one row, no per-pixel division
+  const int wpad = (w + 31) & ~31;
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+  for (int xb = blockIdx.x * blockDim.x; xb < wpad; xb += gridDim.x * blockDim.x) {
+    const int x = xb + threadIdx.x;
+    const int64_t i = (int64_t)y * w + x;
+    const int32_t l = x < w ? labels[i] : 0;
     const bool on = l > 0 && l <= nobj;
     const unsigned act = __ballot_sync(full, on);
     if (!act) continue;
     if (!on) continue;
-    const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
     const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
     const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
     const uint8_t* rm = I + (int64_t)ym * w;
@@ -179,11 +181,8 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
   const int gclear = (int)ceil_div(cap, 256);
   k_feat_clear<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc);
   RTG_LAUNCH("k_feat_clear");
-  const int64_t n = h * w;
-  const int64_t want = ceil_div(n, 256);
-  const int blocks = (int)(want < (int64_t)ctx->num_sms * 8 ? want : (int64_t)ctx->num_sms * 8);
-  k_feat_accum<<<blocks, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n,
-                                               ctx->acc);
+  const dim3 grid((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
+  k_feat_accum<<<grid, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n, ctx->acc);
   RTG_LAUNCH("k_feat_accum");
   k_feat_finalize<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc, out, ctx->status);
   RTG_LAUNCH("k_feat_finalize");

@@ -34,14 +34,16 @@ __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
 
 // rm / arrows / plateau list.  ptr: self for markers, steepest ascent for
 // pixels with a higher neighbour (delta 0), -2 for flat plateau pixels.
+// ptr / delta are written for foreground pixels only (consumers test Fw / the
+// mask first); rm is written everywhere (the marker CCL reads it).
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
             const uint16_t* __restrict__ G, uint8_t* __restrict__ rm,
             int32_t* __restrict__ ptr, int32_t* __restrict__ delta,
             int32_t* __restrict__ flat_list, int32_t* __restrict__ flat_count) {
-  const int64_t n = (int64_t)h * w;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)y * w + x;
     const uint32_t f = Fw[i];
     uint8_t is_rm = 0;
     int32_t p = -1, d = -1;
@@ -50,7 +52,6 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
         is_rm = 1;
         p = (int32_t)i;
       } else {
-        const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
         uint32_t best = f;
         int32_t arg = -1;
 #pragma unroll
@@ -77,8 +78,10 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
       }
     }
     rm[i] = is_rm;
-    ptr[i] = p;
-    delta[i] = d;
+    if (f) {
+      ptr[i] = p;
+      delta[i] = d;
+    }
   }
 }
 
@@ -182,15 +185,15 @@ k_ws_plateau_arrows(int h, int w, const uint16_t* __restrict__ Fw,
   }
 }
 
-__global__ void k_ws_resolve(int64_t n, const int32_t* __restrict__ ptr,
+__global__ void k_ws_resolve(int64_t n, const uint8_t* __restrict__ mask,
+                             const int32_t* __restrict__ ptr,
                              const int32_t* __restrict__ mroots,
                              int32_t* __restrict__ basin) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t q = ptr[i];
     int32_t b = 0;
-    if (q != -1) {
-      q = (int32_t)i;
+    if (mask[i]) {
+      int32_t q = (int32_t)i;
       int32_t nx = ptr[q];
       while (nx >= 0 && nx != q) {
         q = nx;
@@ -204,13 +207,12 @@ __global__ void k_ws_resolve(int64_t n, const int32_t* __restrict__ ptr,
 
 __global__ void k_ws_separate(int h, int w, const int32_t* __restrict__ basin,
                               uint8_t* __restrict__ sep) {
-  const int64_t n = (int64_t)h * w;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)y * w + x;
     const int32_t b = basin[i];
     uint8_t keep = b > 0;
     if (keep) {
-      const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
       for (int dy = -1; dy <= 1 && keep; ++dy) {
         for (int dx = -1; dx <= 1; ++dx) {
           const int yy = y + dy, xx = x + dx;
@@ -250,9 +252,9 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* delta = ctx->i32b;
   int32_t* flat_count = ctx->misc + 1;
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
-  k_ws_arrows<<<grid_for(ctx, n), 256, 0, ctx->stream>>>((int)h, (int)w, Fw, G, ctx->rm,
-                                                        ptr, delta, ctx->flat_list,
-                                                        flat_count);
+  const dim3 grid2d((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
+  k_ws_arrows<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, G, ctx->rm, ptr, delta,
+                                               ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
   int32_t* mroots = ctx->i32c;
   RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
@@ -268,9 +270,9 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                                                                  ctx->flat_list, flat_count,
                                                                  delta, ptr);
   RTG_LAUNCH("k_ws_plateau_arrows");
-  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, ptr, mroots, basin);
+  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, mroots, basin);
   RTG_LAUNCH("k_ws_resolve");
-  k_ws_separate<<<grid_for(ctx, n), 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
+  k_ws_separate<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
 }

@@ -165,15 +165,21 @@ def test_fill_holes(rtg, ctx, oracle, shape, impl):
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
 
 
-def test_pipeline_fill_impls_agree(rtg, ctx):
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_pipeline_fill_impls(rtg, ctx, oracle, impl, graphs):
     rgb = rtg.synth_tile_host(7, 7, 2048, 2048)
-    a = ctx.process_tile(rgb)
-    ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 1)
+    ref = oracle.process_tile(rgb)
+    ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, impl)
+    ctx.set_option(rtg.OPT_USE_GRAPHS, graphs)
     try:
-        b = ctx.process_tile(rgb)
+        mask, labels, _, feats, n = ctx.process_tile(rgb)
     finally:
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
-    assert a[4] == b[4] and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+        ctx.set_option(rtg.OPT_USE_GRAPHS, 1)
+    assert n == ref["n"]
+    assert np.array_equal(mask, ref["mask"])
+    assert np.array_equal(labels, ref["labels"])
 
 
 # ---------------------------------------------------------------- o5 / o8
