@@ -90,66 +90,64 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
 // passes in any order converge to the unique fixed point).  A few of these
 // resolve almost every plateau before the single-CTA pass below, which owns
 // the convergence test, has to iterate.
+// Relaxes plateau pixel i once; returns true when its distance dropped.
+// Branch-free neighbour gathers (out-of-tile neighbours alias i), so the 16
+// loads of a pixel are issued back to back.
+__device__ __forceinline__ bool relax_plateau_px(int h, int w, const uint16_t* __restrict__ Fw,
+                                                 int32_t i, int32_t* delta) {
+  const int y = i / w, x = i - y * w;
+  const uint32_t f = Fw[i];
+  const int32_t cur = __ldcg(&delta[i]);
+  int32_t best = cur;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dy == 0 && dx == 0) continue;
+      const int yy = y + dy, xx = x + dx;
+      const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
+      const int32_t j = in ? yy * w + xx : i;
+      const uint32_t fj = Fw[j];
+      const int32_t dj = __ldcg(&delta[j]);
+      const int32_t cand = (in && fj == f && dj >= 0 && dj < kInfD) ? dj + 1 : kInfD;
+      best = min(best, cand);
+    }
+  }
+  if (best < cur) {
+    __stcg(&delta[i], best);
+    return true;
+  }
+  return false;
+}
+
 __global__ void __launch_bounds__(256)
 k_ws_plateau_relax(int h, int w, const uint16_t* __restrict__ Fw,
                    const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-                   int32_t* delta) {
+                   int32_t* delta, int32_t* __restrict__ changed) {
   const int n = *flat_count;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = flat_list[k];
-    const int y = i / w, x = i - y * w;
-    const uint32_t f = Fw[i];
-    const int32_t cur = __ldcg(&delta[i]);
-    int32_t best = cur;
-    for (int dy = -1; dy <= 1; ++dy) {
-      for (int dx = -1; dx <= 1; ++dx) {
-        if (dy == 0 && dx == 0) continue;
-        const int yy = y + dy, xx = x + dx;
-        if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-        const int32_t j = yy * w + xx;
-        if (Fw[j] != f) continue;
-        const int32_t dj = __ldcg(&delta[j]);
-        if (dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
-      }
-    }
-    if (best < cur) __stcg(&delta[i], best);
-  }
+  bool any = false;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    any |= relax_plateau_px(h, w, Fw, flat_list[k], delta);
+  if (__any_sync(0xFFFFFFFFu, any) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
 // Convergence owner: Bellman-Ford passes in one CTA until a pass changes
-// nothing (after the grid-wide passes above this is normally one pass).
-// Loads are ld.global.cg (L2-coherent, batched), never volatile.
+// nothing.  When the last grid-wide pass already changed nothing (the usual
+// case: plateaus are a few pixels across) the distances are final and it
+// returns at once.
 __global__ void __launch_bounds__(1024)
 k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
              const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-             int32_t* delta) {
+             int32_t* delta, const int32_t* __restrict__ last_pass_changed) {
   __shared__ int changed;
   const int n = *flat_count;
-  if (n == 0) return;
+  if (n == 0 || *last_pass_changed == 0) return;
   while (true) {
     __syncthreads();
     if (threadIdx.x == 0) changed = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
-      const int32_t i = flat_list[k];
-      const int y = i / w, x = i - y * w;
-      const uint32_t f = Fw[i];
-      const int32_t cur = __ldcg(&delta[i]);
-      int32_t best = cur;
-#pragma unroll
-      for (int dy = -1; dy <= 1; ++dy) {
-#pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) {
-          if (dy == 0 && dx == 0) continue;
-          const int yy = y + dy, xx = x + dx;
-          if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-          const int32_t j = yy * w + xx;
-          const int32_t dj = __ldcg(&delta[j]);
-          if (Fw[j] == f && dj >= 0 && dj < kInfD && dj + 1 < best) best = dj + 1;
-        }
-      }
-      if (best < cur) {
-        __stcg(&delta[i], best);
+      if (relax_plateau_px(h, w, Fw, flat_list[k], delta)) {
         changed = 1;
       }
     }
@@ -258,13 +256,16 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_arrows");
   int32_t* mroots = ctx->i32c;
   RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
-  for (int pass = 0; pass < 6; ++pass) {
-    k_ws_plateau_relax<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
-                                                                  ctx->flat_list, flat_count, delta);
+  constexpr int kRelaxPasses = 6;
+  int32_t* pass_changed = ctx->misc + 16;  // one flag per pass
+  RTG_CUDA(cudaMemsetAsync(pass_changed, 0, sizeof(int32_t) * kRelaxPasses, ctx->stream));
+  for (int pass = 0; pass < kRelaxPasses; ++pass) {
+    k_ws_plateau_relax<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(
+        (int)h, (int)w, Fw, ctx->flat_list, flat_count, delta, pass_changed + pass);
     RTG_LAUNCH("k_ws_plateau_relax");
   }
   k_ws_plateau<<<1, 1024, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count,
-                                            delta);
+                                            delta, pass_changed + kRelaxPasses - 1);
   RTG_LAUNCH("k_ws_plateau");
   k_ws_plateau_arrows<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
                                                                  ctx->flat_list, flat_count,
