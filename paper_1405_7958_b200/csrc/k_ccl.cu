@@ -39,8 +39,19 @@ __device__ __forceinline__ int32_t find_root_g(int32_t* par, int32_t a) {
   return a;
 }
 
-// Shared-memory find with path halving (plain stores are fine inside the CTA
-// for the same reason).
+// Read-only shared-memory find.
+__device__ __forceinline__ int32_t find_root(const int32_t* par, int32_t a) {
+  int32_t p = par[a];
+  while (p != a) {
+    a = p;
+    p = par[a];
+  }
+  return a;
+}
+
+// Shared-memory find with path halving, used while unions are running (only
+// connectivity matters there; a stale halving store can only move an entry
+// to another ancestor).
 __device__ __forceinline__ int32_t find_root_c(int32_t* par, int32_t a) {
   int32_t p = par[a];
   while (p != a) {
@@ -125,16 +136,21 @@ k_ccl_local(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict_
     }
   }
   __syncthreads();
-  int slot[4];
+  // 3. flatten: read-only finds, then (after a barrier) every thread writes
+  //    only its own entries — a halving store racing with a finished entry
+  //    could otherwise regress it to a non-root ancestor
+  int slot[4], lroot[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = rb + 8 * k, i = r * 32 + c;
     slot[k] = -1;
-    if (fg[k]) {
-      par[i] = find_root_c(par, i);
-      if (par[i] == i) slot[k] = atomicAdd(&n_local, 1);
-    }
+    lroot[k] = fg[k] ? find_root(par, i) : -1;
+    if (fg[k] && lroot[k] == i) slot[k] = atomicAdd(&n_local, 1);
   }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (fg[k]) par[(rb + 8 * k) * 32 + c] = lroot[k];
   __syncthreads();
   if (threadIdx.x == 0) base = n_local ? atomicAdd(lcount, n_local) : 0;
   __syncthreads();
