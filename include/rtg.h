@@ -137,10 +137,14 @@ int rtg_ctx_set_stream(rtg_ctx* ctx, void* stream);
 /* Waits for the context's stream and reports sticky device-side errors
  * (object-capacity overflow, queue overflow). */
 int rtg_ctx_sync(rtg_ctx* ctx);
-/* Device-side counters of the last pipeline run (for tests / profiling):
- * out[0] = objects, out[1] = recon tile visits, out[2] = fill-holes tile
- * visits, out[3] = watershed markers.  Synchronises. */
-int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]);
+/* Device-side counters accumulated since the last call (then reset),
+ * for tests / profiling; synchronises:
+ *   out[0] objects of the last tile, out[1] IWPP tile visits (all kinds),
+ *   out[2] watershed plateau pixels of the last tile,
+ *   out[4 + 2k] tile visits and out[5 + 2k] sweep iterations of IWPP kind k
+ *   (k = 0 ReconToNuclei, 1 HMAX, 2 regional maxima, 3 IWPP fill-holes). */
+#define RTG_NUM_STATS 16
+int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[RTG_NUM_STATS]);
 
 /* Stage timing (CUDA events on the ctx stream, bracketing each stage of the
  * pipeline).  rtg_ctx_profile_read synchronises, returns the accumulated

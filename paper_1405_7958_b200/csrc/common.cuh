@@ -164,8 +164,9 @@ int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
 //         border tiles initially queued; on exit J = reached background.
 int iwpp_recon_u8(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h,
                   int64_t w, int conn);
+// kind selects the rtg_ctx_stats slot: 1 = HMAX, 2 = regional maxima
 int iwpp_recon_u16(rtg_ctx* ctx, uint16_t* J, const uint16_t* I, int64_t h,
-                   int64_t w, int conn);
+                   int64_t w, int conn, int kind = 1);
 int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
                     int64_t w, uint8_t* out);
 

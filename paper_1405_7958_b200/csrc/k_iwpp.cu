@@ -125,7 +125,7 @@ __device__ bool q_finish(const TileQueue& q, int32_t t) {
 template <typename T, int CONN, class MaskF>
 __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int h, int w,
                            int tiles_x, const TileQueue& q, int32_t cap, uint32_t* Js,
-                           uint32_t* Is, long long& visits) {
+                           uint32_t* Is, long long& visits, long long& iters) {
   const unsigned full = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -227,6 +227,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
         __syncwarp();
       }
       iter_changed = __any_sync(full, ch);
+      ++iters;
       tile_changed |= iter_changed;
     }
     ++visits;
@@ -298,13 +299,13 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
 template <typename T, int CONN, class MaskF>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
 k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
-       int static_first, TileQueue q, int32_t cap, int64_t* visits, uint32_t max_visits,
+       int static_first, TileQueue q, int32_t cap, int64_t* kstats, uint32_t max_visits,
        uint32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xFFFFFFFFu;
-  long long my_visits = 0, charged = 0;
+  long long my_visits = 0, charged = 0, my_iters = 0;
 
   // budget: a bug that livelocks the queue must not hang the GPU; exceeding
   // it aborts every warp and raises a sticky status bit
@@ -332,7 +333,7 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
         __threadfence();
       }
       __syncwarp();
-      visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits);
+      visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters);
       if (over_budget()) break;
     }
   }
@@ -341,10 +342,13 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
     if (lane == 0) t = q_pop(q, cap);
     t = __shfl_sync(full, t, 0);
     if (t < 0) break;
-    visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits);
+    visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters);
     if (over_budget()) break;
   }
-  if (lane == 0 && visits) atomicAdd((unsigned long long*)visits, (unsigned long long)my_visits);
+  if (lane == 0 && kstats) {
+    atomicAdd((unsigned long long*)&kstats[0], (unsigned long long)my_visits);
+    atomicAdd((unsigned long long*)&kstats[1], (unsigned long long)my_iters);
+  }
 }
 
 // Queue initialisation.  mode 0: every tile starts active (state queued,
@@ -419,7 +423,8 @@ __global__ void k_fill_final(const uint8_t* __restrict__ bin,
 }
 
 template <typename T, int CONN, class MaskF>
-int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_only) {
+int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_only,
+             int kind) {
   const int tiles_y = (int)ceil_div(h, kTile), tiles_x = (int)ceil_div(w, kTile);
   const int ntiles = tiles_y * tiles_x;
   const int32_t cap = 2 * ntiles;
@@ -442,7 +447,7 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
   if (blocks > need) blocks = need;
   k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
       J, maskf, (int)h, (int)w, tiles_x, ntiles, border_only ? 0 : 1, ctx->tq, cap,
-      ctx->stats + 1, (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
+      ctx->stats + 4 + 2 * kind, (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
   RTG_LAUNCH("k_iwpp");
   return RTG_OK;
 }
@@ -451,14 +456,14 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
 
 int iwpp_recon_u8(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h,
                   int64_t w, int conn) {
-  if (conn == 8) return run_iwpp<uint8_t, 8>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0);
-  return run_iwpp<uint8_t, 4>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0);
+  if (conn == 8) return run_iwpp<uint8_t, 8>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0, 0);
+  return run_iwpp<uint8_t, 4>(ctx, J, PlainMask<uint8_t>{I}, h, w, 0, 0);
 }
 
 int iwpp_recon_u16(rtg_ctx* ctx, uint16_t* J, const uint16_t* I, int64_t h,
-                   int64_t w, int conn) {
-  if (conn == 8) return run_iwpp<uint16_t, 8>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0);
-  return run_iwpp<uint16_t, 4>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0);
+                   int64_t w, int conn, int kind) {
+  if (conn == 8) return run_iwpp<uint16_t, 8>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0, kind);
+  return run_iwpp<uint16_t, 4>(ctx, J, PlainMask<uint16_t>{I}, h, w, 0, kind);
 }
 
 int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
@@ -467,7 +472,7 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
   const int blocks = (int)(ceil_div(n, 256) < ctx->num_sms * 8 ? ceil_div(n, 256) : ctx->num_sms * 8);
   k_fill_seed<<<blocks, 256, 0, ctx->stream>>>(bin, (int)h, (int)w, J);
   RTG_LAUNCH("k_fill_seed");
-  RTG_TRY((run_iwpp<uint8_t, 4>(ctx, J, ComplementMask{bin}, h, w, 1)));
+  RTG_TRY((run_iwpp<uint8_t, 4>(ctx, J, ComplementMask{bin}, h, w, 1, 3)));
   k_fill_final<<<blocks, 256, 0, ctx->stream>>>(bin, J, n, out);
   RTG_LAUNCH("k_fill_final");
   return RTG_OK;

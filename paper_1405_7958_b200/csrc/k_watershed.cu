@@ -244,7 +244,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   uint16_t* Fw = ctx->u16a;                       // dq is dead now
   k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw, G);
   RTG_LAUNCH("k_ws_prep");
-  RTG_TRY(iwpp_recon_u16(ctx, G, Fw, h, w, 8));  // regional-maximum test
+  RTG_TRY(iwpp_recon_u16(ctx, G, Fw, h, w, 8, 2));  // regional-maximum test
   prof_mark(ctx, RTG_STAGE_WATERSHED);
   int32_t* ptr = ctx->i32a;
   int32_t* delta = ctx->i32b;

@@ -300,7 +300,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->lroots, n));
         RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
         RTG_TRY(dalloc(&c->status, 1));
-        RTG_TRY(dalloc(&c->stats, 8));
+        RTG_TRY(dalloc(&c->stats, RTG_NUM_STATS));
         const int64_t ntiles = ceil_div(max_h, kTile) * ceil_div(max_w, kTile);
         c->tq.capacity = (int32_t)(2 * ntiles);
         RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
@@ -312,7 +312,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->acc.maxs, (size_t)kMaxFields * max_objects));
         RTG_CUDA(cudaMemsetAsync(c->misc, 0, sizeof(int32_t) * (128 + (size_t)max_h), c->stream));
         RTG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(uint32_t), c->stream));
-        RTG_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(int64_t) * 8, c->stream));
+        RTG_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(int64_t) * RTG_NUM_STATS, c->stream));
         RTG_CUDA(cudaMemsetAsync(c->tq.state, 0, sizeof(int32_t) * (size_t)ntiles, c->stream));
         RTG_CUDA(cudaStreamSynchronize(c->stream));
         return RTG_OK;
@@ -376,19 +376,20 @@ int rtg_ctx_sync(rtg_ctx* ctx) {
   return RTG_OK;
 }
 
-int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[8]) {
+int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[RTG_NUM_STATS]) {
   if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
   RTG_CUDA(cudaSetDevice(ctx->device));
   RTG_CUDA(cudaStreamSynchronize(ctx->stream));
   int32_t misc[4];
-  int64_t st[8];
+  int64_t st[RTG_NUM_STATS];
   RTG_CUDA(cudaMemcpy(misc, ctx->misc, sizeof(misc), cudaMemcpyDeviceToHost));
   RTG_CUDA(cudaMemcpy(st, ctx->stats, sizeof(st), cudaMemcpyDeviceToHost));
   RTG_CUDA(cudaMemset(ctx->stats, 0, sizeof(st)));
-  for (int i = 0; i < 8; ++i) out[i] = 0;
+  for (int i = 0; i < RTG_NUM_STATS; ++i) out[i] = st[i];
   out[0] = misc[0];
-  out[1] = st[1];
+  out[1] = st[4] + st[6] + st[8] + st[10];
   out[2] = misc[1];
+  out[3] = 0;
   return RTG_OK;
 }
 

@@ -247,7 +247,7 @@ class Context:
         check(self.lib.rtg_ctx_sync(self.handle))
 
     def stats(self) -> list:
-        out = (ctypes.c_int64 * 8)()
+        out = (ctypes.c_int64 * 16)()
         check(self.lib.rtg_ctx_stats(self.handle, out))
         return list(out)
 
