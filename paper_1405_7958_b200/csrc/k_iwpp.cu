@@ -179,56 +179,70 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
     // all-background tile of a distance map) cannot change: skip the sweeps
     bool saturated = true;
     for (int r = 0; r < 32; ++r) saturated &= Js[(r + 1) * kJS + lane + 1] == Is[r * kIS + lane];
-    bool iter_changed = !__all_sync(full, saturated);
-    while (iter_changed) {
-      bool ch = false;
-      // down: lane = column c, rows 0..31, neighbours in the row above
-      for (int r = 0; r < 32; ++r) {
-        uint32_t* row = Js + (r + 1) * kJS + lane + 1;
-        const uint32_t* up = row - kJS;
-        uint32_t n = up[0];
-        if (CONN == 8) n = max(n, max(up[-1], up[1]));
-        const uint32_t v = *row;
-        const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
-        if (nv != v) { *row = nv; ch = true; }
-        __syncwarp();
+    // Sweeps run cyclically (down, up, right, left).  A sweep leaves its own
+    // relation satisfied, and a sweep that changes nothing certifies its
+    // relation, so the tile is at its local fixed point once the three sweeps
+    // after the last changing sweep were quiet (4 quiet sweeps if none ever
+    // changed anything).
+    if (!__all_sync(full, saturated)) {
+      int quiet = 0, done = 0;
+      for (int s = 0;; s = (s + 1) & 3) {
+        bool ch = false;
+        if (s == 0) {  // down: lane = column c, neighbours in the row above
+          for (int r = 0; r < 32; ++r) {
+            uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+            const uint32_t* up = row - kJS;
+            uint32_t n = up[0];
+            if (CONN == 8) n = max(n, max(up[-1], up[1]));
+            const uint32_t v = *row;
+            const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+            if (nv != v) { *row = nv; ch = true; }
+            __syncwarp();
+          }
+        } else if (s == 1) {  // up
+          for (int r = 31; r >= 0; --r) {
+            uint32_t* row = Js + (r + 1) * kJS + lane + 1;
+            const uint32_t* dn = row + kJS;
+            uint32_t n = dn[0];
+            if (CONN == 8) n = max(n, max(dn[-1], dn[1]));
+            const uint32_t v = *row;
+            const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
+            if (nv != v) { *row = nv; ch = true; }
+            __syncwarp();
+          }
+        } else if (s == 2) {  // right: lane = row r, neighbours in the column left
+          for (int c = 0; c < 32; ++c) {
+            uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+            const uint32_t* lf = px - 1;
+            uint32_t n = lf[0];
+            if (CONN == 8) n = max(n, max(lf[-kJS], lf[kJS]));
+            const uint32_t v = *px;
+            const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+            if (nv != v) { *px = nv; ch = true; }
+            __syncwarp();
+          }
+        } else {  // left
+          for (int c = 31; c >= 0; --c) {
+            uint32_t* px = Js + (lane + 1) * kJS + c + 1;
+            const uint32_t* rt = px + 1;
+            uint32_t n = rt[0];
+            if (CONN == 8) n = max(n, max(rt[-kJS], rt[kJS]));
+            const uint32_t v = *px;
+            const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
+            if (nv != v) { *px = nv; ch = true; }
+            __syncwarp();
+          }
+        }
+        ++done;
+        if (__any_sync(full, ch)) {
+          tile_changed = true;
+          quiet = 0;
+        } else {
+          ++quiet;
+        }
+        if ((quiet >= 3 && done > quiet) || quiet >= 4) break;
       }
-      // up
-      for (int r = 31; r >= 0; --r) {
-        uint32_t* row = Js + (r + 1) * kJS + lane + 1;
-        const uint32_t* dn = row + kJS;
-        uint32_t n = dn[0];
-        if (CONN == 8) n = max(n, max(dn[-1], dn[1]));
-        const uint32_t v = *row;
-        const uint32_t nv = min(max(v, n), Is[r * kIS + lane]);
-        if (nv != v) { *row = nv; ch = true; }
-        __syncwarp();
-      }
-      // right: lane = row r, columns 0..31, neighbours in the column left
-      for (int c = 0; c < 32; ++c) {
-        uint32_t* px = Js + (lane + 1) * kJS + c + 1;
-        const uint32_t* lf = px - 1;
-        uint32_t n = lf[0];
-        if (CONN == 8) n = max(n, max(lf[-kJS], lf[kJS]));
-        const uint32_t v = *px;
-        const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
-        if (nv != v) { *px = nv; ch = true; }
-        __syncwarp();
-      }
-      // left
-      for (int c = 31; c >= 0; --c) {
-        uint32_t* px = Js + (lane + 1) * kJS + c + 1;
-        const uint32_t* rt = px + 1;
-        uint32_t n = rt[0];
-        if (CONN == 8) n = max(n, max(rt[-kJS], rt[kJS]));
-        const uint32_t v = *px;
-        const uint32_t nv = min(max(v, n), Is[lane * kIS + c]);
-        if (nv != v) { *px = nv; ch = true; }
-        __syncwarp();
-      }
-      iter_changed = __any_sync(full, ch);
-      ++iters;
-      tile_changed |= iter_changed;
+      iters += (done + 3) / 4;
     }
     ++visits;
     tile_changed = __any_sync(full, tile_changed);
@@ -299,7 +313,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
 template <typename T, int CONN, class MaskF>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
 k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
-       int static_first, TileQueue q, int32_t cap, int64_t* kstats, uint32_t max_visits,
+       int phase, TileQueue q, int32_t cap, int64_t* kstats, uint32_t max_visits,
        uint32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
@@ -324,10 +338,18 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
            *(volatile uint32_t*)&q.counters[4] != 0u;
   };
 
-  if (static_first) {
+  if (phase >= 0) {
+    // static pass over one colour class: tiles (ty, tx) with ty % 2 == py and
+    // tx % 2 == px are never 8-neighbours of each other, so a phase never
+    // races with itself and each later phase sees final-ish halos.  Pushes go
+    // to the queue, which the phase == -1 launch drains.
+    const int tiles_y = (h + kTile - 1) / kTile;
+    const int py = phase >> 1, px = phase & 1;
+    const int cy = (tiles_y - py + 1) / 2, cx = (tiles_x - px + 1) / 2;
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * kWarpsPerBlock;
-    for (int t = warp; t < ntiles; t += nwarps) {
+    for (int k = warp; k < cy * cx; k += nwarps) {
+      const int t = (py + 2 * (k / cx)) * tiles_x + px + 2 * (k % cx);
       if (lane == 0) {
         atomicExch(&q.state[t], 2);
         __threadfence();
@@ -336,8 +358,7 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
       visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters);
       if (over_budget()) break;
     }
-  }
-  while (true) {
+  } else while (true) {
     int32_t t = 0;
     if (lane == 0) t = q_pop(q, cap);
     t = __shfl_sync(full, t, 0);
@@ -442,13 +463,28 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
   RTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iwpp<T, CONN, MaskF>,
                                                          kWarpsPerBlock * 32, smem));
   if (per_sm < 1) per_sm = 1;
-  int blocks = ctx->num_sms * per_sm;
+  const int max_blocks = ctx->num_sms * per_sm;
+  int64_t* kstats = ctx->stats + 4 + 2 * kind;
+  const uint32_t budget = (uint32_t)(256u * (uint32_t)ntiles + 65536u);
+  if (!border_only) {
+    // four colour-class static passes, then the queue drains the wavefronts
+    for (int phase = 0; phase < 4; ++phase) {
+      const int cy = (tiles_y - (phase >> 1) + 1) / 2, cx = (tiles_x - (phase & 1) + 1) / 2;
+      if (cy <= 0 || cx <= 0) continue;
+      int blocks = (int)ceil_div((int64_t)cy * cx, kWarpsPerBlock);
+      if (blocks > max_blocks) blocks = max_blocks;
+      k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
+          J, maskf, (int)h, (int)w, tiles_x, ntiles, phase, ctx->tq, cap, kstats, budget,
+          ctx->status);
+      RTG_LAUNCH("k_iwpp(phase)");
+    }
+  }
+  int blocks = max_blocks;
   const int need = (int)ceil_div(ntiles, kWarpsPerBlock);
   if (blocks > need) blocks = need;
   k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
-      J, maskf, (int)h, (int)w, tiles_x, ntiles, border_only ? 0 : 1, ctx->tq, cap,
-      ctx->stats + 4 + 2 * kind, (uint32_t)(256u * (uint32_t)ntiles + 65536u), ctx->status);
-  RTG_LAUNCH("k_iwpp");
+      J, maskf, (int)h, (int)w, tiles_x, ntiles, -1, ctx->tq, cap, kstats, budget, ctx->status);
+  RTG_LAUNCH("k_iwpp(queue)");
   return RTG_OK;
 }
 
