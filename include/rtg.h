@@ -175,7 +175,13 @@ enum rtg_option {
   RTG_OPT_FILL_HOLES_IMPL = 0,
   /* rtg_process_tile_dev replays a cached CUDA graph of the whole stage per
    * distinct argument tuple (1, default) or launches kernel by kernel (0). */
-  RTG_OPT_USE_GRAPHS = 1
+  RTG_OPT_USE_GRAPHS = 1,
+  /* ReconToNuclei inside the stage: 0 = threshold decomposition (default:
+   * the stage only consumes recon >= nuc_thresh, which equals the union-find
+   * components of {H >= nuc_thresh} holding a pixel with H >= nuc_thresh +
+   * recon_h), 1 = full grayscale IWPP reconstruction then threshold.  The
+   * per-operator rtg_recon_*_dev entry points are always the grayscale IWPP. */
+  RTG_OPT_RECON_IMPL = 2
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

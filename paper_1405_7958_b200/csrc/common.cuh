@@ -116,6 +116,7 @@ struct rtg_ctx {
   // implementation options (rtg_ctx_set_option)
   int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
   int use_graphs = 1; // replay rtg_process_tile_dev as a cached CUDA graph
+  int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {
@@ -183,6 +184,12 @@ __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, in
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n);
+// ReconToNuclei candidates = (recon(max(H - h, 0), H) >= t) && tissue by
+// threshold decomposition: union-find components of {H >= t} holding a pixel
+// with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.
+int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
+                       int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
+                       uint8_t* out);
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);

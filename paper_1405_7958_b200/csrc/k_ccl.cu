@@ -372,7 +372,63 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
   }
 }
 
+// ---- thresholded reconstruction (ReconToNuclei candidates) ----------------
+// Threshold decomposition: with flat connectivity, R = recon(marker, H)
+// satisfies  R(p) >= t  <=>  p lies in a conn-component of {H >= t} that
+// contains a pixel with marker >= t.  With marker = max(H - h, 0) and t >= 1
+// that is a pixel with H >= t + h.
+__global__ void k_thresh(int64_t n, const uint8_t* __restrict__ hema, int32_t t,
+                         uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)(hema[i] >= t);
+}
+
+__global__ void k_mark_seeds(int64_t n, const uint8_t* __restrict__ hema, int32_t seed_t,
+                             const int32_t* __restrict__ roots, int32_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (hema[i] >= seed_t) {
+      const int32_t r = root_of(roots, i);
+      if (r >= 0 && !flag[r]) flag[r] = 1;
+    }
+  }
+}
+
+__global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
+                             const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
+                             uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = root_of(roots, i);
+    out[i] = (uint8_t)(r >= 0 && flag[r] && tissue[i]);
+  }
+}
+
 }  // namespace
+
+int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
+                       int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
+                       uint8_t* out) {
+  const int64_t n = h * w;
+  if (t <= 0) {  // R >= t everywhere: the candidates are the tissue mask
+    RTG_CUDA(cudaMemcpyAsync(out, tissue, (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
+    return RTG_OK;
+  }
+  k_thresh<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, hema, t, scratch);
+  RTG_LAUNCH("k_thresh");
+  int32_t* roots = ctx->i32a;
+  int32_t* flag = ctx->i32b;
+  RTG_TRY(ccl_roots(ctx, scratch, h, w, conn, roots, flag));
+  const int64_t seed_t = (int64_t)t + recon_h;
+  if (seed_t <= 255) {
+    k_mark_seeds<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, hema, (int32_t)seed_t, roots, flag);
+    RTG_LAUNCH("k_mark_seeds");
+  }
+  k_seeded_and<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag, tissue, out);
+  RTG_LAUNCH("k_seeded_and");
+  return RTG_OK;
+}
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
               int32_t* roots, int32_t* zero_at_roots) {

@@ -99,15 +99,22 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   uint8_t* mask = d_mask ? d_mask : ctx->m4;
   int32_t* labels = d_labels ? d_labels : ctx->labels;
   int32_t* n_out = d_n ? d_n : ctx->misc;
-  // o1+o2: hematoxylin, HMAX marker (in place of the reconstruction), tissue
+  const bool iwpp_recon = ctx->recon_impl == 1;
+  // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
-  RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, ctx->recon, ctx->tissue));
-  // o3 ReconToNuclei
+  RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, iwpp_recon ? ctx->recon : nullptr,
+                             ctx->tissue));
+  // o3 ReconToNuclei: candidates = recon(max(H - h, 0), H) >= nuc_thresh && tissue
   prof_mark(ctx, RTG_STAGE_RECON);
-  RTG_TRY(iwpp_recon_u8(ctx, ctx->recon, hema, h, w, p->recon_conn));
+  if (iwpp_recon) {
+    RTG_TRY(iwpp_recon_u8(ctx, ctx->recon, hema, h, w, p->recon_conn));
+    RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
+  } else {
+    RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
+                               p->recon_conn, ctx->m1, ctx->m1));
+  }
   // o4 FillHoles of the nucleus candidates
   prof_mark(ctx, RTG_STAGE_FILL_HOLES);
-  RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
   RTG_TRY(run_fill_holes(ctx, ctx->m1, h, w, ctx->m2));
   // o5 AreaThreshold
   prof_mark(ctx, RTG_STAGE_AREA);
@@ -141,7 +148,8 @@ int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int
   std::string key(sizeof(rtg_params) + 12 * sizeof(int64_t), '\0');
   const int64_t fields[12] = {(int64_t)d_rgb, h, w, pitch, (int64_t)d_mask, (int64_t)d_labels,
                               (int64_t)d_hema, (int64_t)d_features, (int64_t)d_n,
-                              (int64_t)ctx->fill_impl, (int64_t)ctx->stream, 0};
+                              (int64_t)ctx->fill_impl, (int64_t)ctx->stream,
+                              (int64_t)ctx->recon_impl};
   std::memcpy(&key[0], fields, sizeof(fields));
   std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
   if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
@@ -442,6 +450,10 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
       return RTG_OK;
     case RTG_OPT_USE_GRAPHS:
       ctx->use_graphs = value != 0;
+      return RTG_OK;
+    case RTG_OPT_RECON_IMPL:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "recon impl must be 0 or 1");
+      ctx->recon_impl = (int)value;
       return RTG_OK;
     default:
       return fail(RTG_ERR_INVALID_ARG, "unknown option " + std::to_string(option));

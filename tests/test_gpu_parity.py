@@ -165,18 +165,24 @@ def test_fill_holes(rtg, ctx, oracle, shape, impl):
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
 
 
+@pytest.mark.parametrize("recon", [0, 1])
 @pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("graphs", [0, 1])
-def test_pipeline_fill_impls(rtg, ctx, oracle, impl, graphs):
+def test_pipeline_impl_options(rtg, ctx, oracle, impl, graphs, recon):
+    """Every implementation option of the stage (fill-holes union-find vs
+    IWPP, ReconToNuclei threshold decomposition vs grayscale IWPP, graph
+    replay vs eager) gives the oracle's result bit for bit."""
     rgb = rtg.synth_tile_host(7, 7, 2048, 2048)
     ref = oracle.process_tile(rgb)
     ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, impl)
     ctx.set_option(rtg.OPT_USE_GRAPHS, graphs)
+    ctx.set_option(rtg.OPT_RECON_IMPL, recon)
     try:
         mask, labels, _, feats, n = ctx.process_tile(rgb)
     finally:
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
         ctx.set_option(rtg.OPT_USE_GRAPHS, 1)
+        ctx.set_option(rtg.OPT_RECON_IMPL, 0)
     assert n == ref["n"]
     assert np.array_equal(mask, ref["mask"])
     assert np.array_equal(labels, ref["labels"])

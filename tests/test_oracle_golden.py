@@ -105,6 +105,28 @@ def test_recon_properties(oracle):
         assert (oracle.recon(marker, mask, 4) <= r).all()
 
 
+@pytest.mark.parametrize("conn", [4, 8])
+def test_threshold_decomposition_of_recon(oracle, conn):
+    """The identity the GPU stage's default ReconToNuclei path relies on:
+    recon(max(H-h,0), H) >= t  <=>  the pixel's conn-component of {H >= t}
+    holds a pixel with H >= t + h (flat connectivity commutes with
+    thresholding).  Checked against the oracle's grayscale reconstruction."""
+    from scipy import ndimage as ndi
+    rng = np.random.default_rng(77 + conn)
+    st = np.ones((3, 3), bool) if conn == 8 else ndi.generate_binary_structure(2, 1)
+    for trial in range(12):
+        hh, ww = rng.integers(8, 90, 2)
+        H = ndi.gaussian_filter(rng.integers(0, 256, (hh, ww)).astype(float), 1.2).astype(np.uint8)
+        hd = int(rng.integers(0, 40))
+        marker = np.maximum(H.astype(int) - hd, 0).astype(np.uint8)
+        R = oracle.recon(marker, H, conn)
+        for t in (1, 30, 70, 120, 200):
+            lab, _ = ndi.label(H >= t, structure=st)
+            seeded = np.unique(lab[(H.astype(int) >= t + hd) & (lab > 0)])
+            got = np.isin(lab, seeded) & (lab > 0)
+            assert np.array_equal(R >= t, got), (trial, t)
+
+
 def test_watershed_properties(oracle):
     """Every basin carries exactly one marker id, basins stay inside the mask,
     and the separated mask has no 8-adjacent pixels of different basins."""
