@@ -125,7 +125,8 @@ __device__ bool q_finish(const TileQueue& q, int32_t t) {
 template <typename T, int CONN, class MaskF>
 __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int h, int w,
                            int tiles_x, const TileQueue& q, int32_t cap, uint32_t* Js,
-                           uint32_t* Is, long long& visits, long long& iters) {
+                           uint32_t* Is, long long& visits, long long& iters,
+                           bool static_visit) {
   const unsigned full = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const int ty = t / tiles_x, tx = t - ty * tiles_x;
@@ -300,8 +301,19 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
         mark(ty + 1 < tiles_y && tx + 1 < tiles_x && c11 != c11_0 && c11 > Js[33 * kJS + 33],
              t + tiles_x + 1);
       }
-      q_enqueue(q, cap, ids, k);
-      again = q_finish(q, t) ? 1 : 0;
+      if (static_visit) {
+        // colour-phase pass: marked tiles (state 1) are collected into the
+        // queue by k_queue_build afterwards; no hot counters touched here
+        const int32_t old = atomicCAS(&q.state[t], 2, 0);
+        if (old != 2) {
+          atomicExch(&q.state[t], 2);
+          __threadfence();
+          again = 1;
+        }
+      } else {
+        q_enqueue(q, cap, ids, k);
+        again = q_finish(q, t) ? 1 : 0;
+      }
     }
     again = __shfl_sync(full, again, 0);
     dirty_reload = again != 0;
@@ -341,8 +353,9 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
   if (phase >= 0) {
     // static pass over one colour class: tiles (ty, tx) with ty % 2 == py and
     // tx % 2 == px are never 8-neighbours of each other, so a phase never
-    // races with itself and each later phase sees final-ish halos.  Pushes go
-    // to the queue, which the phase == -1 launch drains.
+    // races with itself and each later phase sees final-ish halos.  A push
+    // only marks the neighbour (state 1); k_queue_build collects the marked
+    // tiles and the phase == -1 launch drains them.
     const int tiles_y = (h + kTile - 1) / kTile;
     const int py = phase >> 1, px = phase & 1;
     const int cy = (tiles_y - py + 1) / 2, cx = (tiles_x - px + 1) / 2;
@@ -355,7 +368,8 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
         __threadfence();
       }
       __syncwarp();
-      visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters);
+      visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters,
+                          true);
       if (over_budget()) break;
     }
   } else while (true) {
@@ -363,7 +377,8 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
     if (lane == 0) t = q_pop(q, cap);
     t = __shfl_sync(full, t, 0);
     if (t < 0) break;
-    visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters);
+    visit_tile<T, CONN>(t, J, maskf, h, w, tiles_x, q, cap, S.J, S.I, my_visits, my_iters,
+                        false);
     if (over_budget()) break;
   }
   if (lane == 0 && kstats) {
@@ -375,24 +390,31 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
 // Queue initialisation.  mode 0: every tile starts active (state queued,
 // visited by the static first pass, nothing in the slot ring); mode 1: only
 // border tiles, published in the slot ring.
-__global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
-                             int border_only) {
+// Tile states before a run: 1 ("to visit") for every tile when the colour
+// phases visit them all, else for border tiles only (fill-holes seeds).
+__global__ void k_tiles_init(TileQueue q, int tiles_y, int tiles_x, int border_only) {
   const int ntiles = tiles_y * tiles_x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const bool take = !border_only || ty == 0 || tx == 0 || ty == tiles_y - 1 || tx == tiles_x - 1;
+    q.state[t] = take ? 1 : 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    q.counters[3] = 0;  // visits (budget)
+    q.counters[4] = 0;  // abort flag
+  }
+}
+
+// Publishes every tile in state 1 (in tile order) into the slot ring and arms
+// the queue counters for the draining launch.
+__global__ void k_queue_build(TileQueue q, int32_t cap, int ntiles) {
   __shared__ int32_t count;
   __shared__ int32_t warp_cnt[32];
   if (threadIdx.x == 0) count = 0;
   __syncthreads();
   for (int base = 0; base < ntiles; base += blockDim.x) {
     const int t = base + threadIdx.x;
-    bool take = false;
-    if (t < ntiles) {
-      const int ty = t / tiles_x, tx = t - ty * tiles_x;
-      take = !border_only || ty == 0 || tx == 0 || ty == tiles_y - 1 || tx == tiles_x - 1;
-    }
-    if (!border_only) {
-      if (t < ntiles) q.state[t] = 1;
-      continue;
-    }
+    const bool take = t < ntiles && q.state[t] == 1;
     // order-preserving compaction within the chunk
     const unsigned b = __ballot_sync(0xFFFFFFFFu, take);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -400,9 +422,7 @@ __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
     __syncthreads();
     int off = 0;
     for (int k = 0; k < wid; ++k) off += warp_cnt[k];
-    const int pos = count + off + __popc(b & ((1u << lane) - 1u));
-    if (t < ntiles) q.state[t] = take ? 1 : 0;
-    if (take) q.slots[pos] = t + 1;
+    if (take) q.slots[count + off + __popc(b & ((1u << lane) - 1u))] = t + 1;
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
@@ -411,14 +431,11 @@ __global__ void k_queue_init(TileQueue q, int32_t cap, int tiles_y, int tiles_x,
     }
     __syncthreads();
   }
-  const int queued = border_only ? count : 0;
-  for (int i = queued + threadIdx.x; i < cap; i += blockDim.x) q.slots[i] = 0;
+  for (int i = count + threadIdx.x; i < cap; i += blockDim.x) q.slots[i] = 0;
   if (threadIdx.x == 0) {
-    q.counters[0] = 0;
-    q.counters[1] = (uint32_t)queued;
-    q.counters[2] = (uint32_t)(border_only ? count : ntiles);  // pending
-    q.counters[3] = 0;  // visits
-    q.counters[4] = 0;  // abort flag
+    q.counters[0] = 0;                 // head
+    q.counters[1] = (uint32_t)count;   // tail
+    q.counters[2] = (uint32_t)count;   // pending
   }
 }
 
@@ -450,8 +467,9 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
   const int ntiles = tiles_y * tiles_x;
   const int32_t cap = 2 * ntiles;
   if (cap > ctx->tq.capacity) return fail(RTG_ERR_DIMENSION, "tile exceeds queue capacity");
-  k_queue_init<<<1, 1024, 0, ctx->stream>>>(ctx->tq, cap, tiles_y, tiles_x, border_only);
-  RTG_LAUNCH("k_queue_init");
+  k_tiles_init<<<(unsigned)ceil_div(ntiles, 256), 256, 0, ctx->stream>>>(ctx->tq, tiles_y, tiles_x,
+                                                                          border_only);
+  RTG_LAUNCH("k_tiles_init");
   const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
   static bool attr_set[64] = {};  // per instantiation and device
   if (ctx->device < 64 && !attr_set[ctx->device]) {
@@ -479,6 +497,8 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
       RTG_LAUNCH("k_iwpp(phase)");
     }
   }
+  k_queue_build<<<1, 1024, 0, ctx->stream>>>(ctx->tq, cap, ntiles);
+  RTG_LAUNCH("k_queue_build");
   int blocks = max_blocks;
   const int need = (int)ceil_div(ntiles, kWarpsPerBlock);
   if (blocks > need) blocks = need;

@@ -120,50 +120,48 @@ __device__ __forceinline__ bool relax_plateau_px(int h, int w, const uint16_t* _
   return false;
 }
 
-__global__ void __launch_bounds__(256)
-k_ws_plateau_relax(int h, int w, const uint16_t* __restrict__ Fw,
-                   const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-                   int32_t* delta, int32_t* __restrict__ changed) {
-  const int n = *flat_count;
-  bool any = false;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-    any |= relax_plateau_px(h, w, Fw, flat_list[k], delta);
-  if (__any_sync(0xFFFFFFFFu, any) && (threadIdx.x & 31) == 0) *changed = 1;
+// Software grid barrier (sense by generation).  Only used by kernels launched
+// with cudaLaunchCooperativeKernel, which guarantees co-residency.
+__device__ __forceinline__ void grid_barrier(unsigned* arrive, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = atomicAdd(gen, 0u);
+    __threadfence();
+    if (atomicAdd(arrive, 1u) == gridDim.x - 1) {
+      atomicExch(arrive, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (atomicAdd(gen, 0u) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
-// Convergence owner: Bellman-Ford passes in one CTA until a pass changes
-// nothing.  When the last grid-wide pass already changed nothing (the usual
-// case: plateaus are a few pixels across) the distances are final and it
-// returns at once.
-__global__ void __launch_bounds__(1024)
+// Plateau distances and arrows in one cooperative launch: rounds of
+// grid-wide chaotic Bellman-Ford over the plateau list until a round changes
+// nothing (values only decrease and always equal some real path length, so
+// the fixed point is the BFS distance), then every plateau pixel points at the
+// same-level neighbour at distance delta-1 with the minimum linear index.
+// flags[0..1] and bar[0..1] must be zero on entry.
+__global__ void __launch_bounds__(256)
 k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
              const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-             int32_t* delta, const int32_t* __restrict__ last_pass_changed) {
-  __shared__ int changed;
+             int32_t* delta, int32_t* __restrict__ ptr, int32_t* flags, unsigned* bar) {
   const int n = *flat_count;
-  if (n == 0 || *last_pass_changed == 0) return;
-  while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) changed = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-      if (relax_plateau_px(h, w, Fw, flat_list[k], delta)) {
-        changed = 1;
-      }
-    }
-    __syncthreads();
+  if (n == 0) return;
+  for (int round = 0; round <= n + 1; ++round) {
+    bool any = false;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+      any |= relax_plateau_px(h, w, Fw, flat_list[k], delta);
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicExch(&flags[round & 1], 1);
+    grid_barrier(bar, bar + 1);
+    const int changed = *(volatile int32_t*)&flags[round & 1];
+    grid_barrier(bar, bar + 1);  // everyone has read the flag
+    if (blockIdx.x == 0 && threadIdx.x == 0) flags[round & 1] = 0;  // reused two rounds later
     if (!changed) break;
   }
-}
-
-// Arrows of plateau pixels: the same-level neighbour at distance delta-1
-// with the minimum linear index (grid-wide).
-__global__ void __launch_bounds__(256)
-k_ws_plateau_arrows(int h, int w, const uint16_t* __restrict__ Fw,
-                    const int32_t* __restrict__ flat_list,
-                    const int32_t* __restrict__ flat_count, const int32_t* __restrict__ delta,
-                    int32_t* __restrict__ ptr) {
-  const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
     const int y = i / w, x = i - y * w;
@@ -256,21 +254,19 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_arrows");
   int32_t* mroots = ctx->i32c;
   RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
-  constexpr int kRelaxPasses = 6;
-  int32_t* pass_changed = ctx->misc + 16;  // one flag per pass
-  RTG_CUDA(cudaMemsetAsync(pass_changed, 0, sizeof(int32_t) * kRelaxPasses, ctx->stream));
-  for (int pass = 0; pass < kRelaxPasses; ++pass) {
-    k_ws_plateau_relax<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(
-        (int)h, (int)w, Fw, ctx->flat_list, flat_count, delta, pass_changed + pass);
-    RTG_LAUNCH("k_ws_plateau_relax");
+  {
+    int32_t* flags = ctx->misc + 16;                              // 2 round flags
+    unsigned* bar = reinterpret_cast<unsigned*>(ctx->misc + 20);  // barrier arrive/gen
+    RTG_CUDA(cudaMemsetAsync(ctx->misc + 16, 0, sizeof(int32_t) * 8, ctx->stream));
+    int hh = (int)h, ww = (int)w;
+    const int32_t* flat = ctx->flat_list;
+    void* args[] = {&hh, &ww, &Fw, &flat, &flat_count, &delta, &ptr, &flags, &bar};
+    // one 256-thread CTA per SM: co-resident by construction, and guaranteed
+    // so by the cooperative launch
+    RTG_CUDA(cudaLaunchCooperativeKernel((const void*)k_ws_plateau, dim3(ctx->num_sms),
+                                         dim3(256), args, 0, ctx->stream));
+    RTG_LAUNCH("k_ws_plateau");
   }
-  k_ws_plateau<<<1, 1024, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count,
-                                            delta, pass_changed + kRelaxPasses - 1);
-  RTG_LAUNCH("k_ws_plateau");
-  k_ws_plateau_arrows<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, Fw,
-                                                                 ctx->flat_list, flat_count,
-                                                                 delta, ptr);
-  RTG_LAUNCH("k_ws_plateau_arrows");
   k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, mroots, basin);
   RTG_LAUNCH("k_ws_resolve");
   k_ws_separate<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
