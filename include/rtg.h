@@ -181,7 +181,12 @@ enum rtg_option {
    * components of {H >= nuc_thresh} holding a pixel with H >= nuc_thresh +
    * recon_h), 1 = full grayscale IWPP reconstruction then threshold.  The
    * per-operator rtg_recon_*_dev entry points are always the grayscale IWPP. */
-  RTG_OPT_RECON_IMPL = 2
+  RTG_OPT_RECON_IMPL = 2,
+  /* PreWatershed + watershed (stage and rtg_watershed_dev): 0 = object-
+   * parallel, each object's bounding-box region processed on-chip by one
+   * warp (default), 1 = tiled whole-tile passes (EDT, IWPP HMAX and
+   * regional maxima, global arrows / plateau BFS). */
+  RTG_OPT_WATERSHED_IMPL = 3
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

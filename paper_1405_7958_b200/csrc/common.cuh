@@ -107,6 +107,10 @@ struct rtg_ctx {
   int32_t* scan_buf = nullptr;     // CCL compaction per-chunk counts/offsets
   int32_t* flat_list = nullptr;    // watershed plateau pixel list
   int32_t* lroots = nullptr;       // CCL tile-local root list (max_px)
+  int32_t* obj_root = nullptr;     // object-parallel watershed: object roots
+  int32_t* obj_box = nullptr;      //   and bounding boxes (4 per object)
+  int64_t obj_cap = 0;
+  unsigned char* arena = nullptr;  //   global scratch for pathological regions
   int32_t* misc = nullptr;         // [0] n_objects, [1] flat count, [2] any_zero, [3] changed, ...
   uint32_t* status = nullptr;      // sticky status bits
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
@@ -117,6 +121,7 @@ struct rtg_ctx {
   int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
   int use_graphs = 1; // replay rtg_process_tile_dev as a cached CUDA graph
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
+  int ws_impl = 0;    // 0: object-parallel watershed, 1: tiled global watershed
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {
@@ -202,6 +207,12 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
               int32_t ws_h, uint8_t* sep, int32_t* basin);
+// Object-parallel o6+o7 (default): objects are the global roots of `roots`
+// (a ccl_roots forest of `mask`) whose counts lie in [lo, hi] (all roots when
+// counts == nullptr).  Writes sep (and basin if non-null) for the whole tile.
+int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
+                      const int32_t* counts, int32_t lo, int32_t hi, int64_t h, int64_t w,
+                      int32_t ws_h, uint8_t* sep, int32_t* basin);
 
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              int64_t h, int64_t w, const int32_t* d_n, float* out);

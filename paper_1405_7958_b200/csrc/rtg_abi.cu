@@ -122,7 +122,14 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
   // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
   // watershed() marks its own EDT / MARKERS / WATERSHED stages
-  RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels));
+  if (ctx->ws_impl == 1) {
+    RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels));
+  } else {
+    // the area-threshold forest and counts already name the kept objects
+    prof_mark(ctx, RTG_STAGE_WATERSHED);
+    RTG_TRY(watershed_objects(ctx, ctx->m3, ctx->i32a, ctx->i32b, p->min_area, p->max_area, h,
+                              w, p->ws_h, mask, nullptr));
+  }
   // o8 BWLabel (canonical)
   prof_mark(ctx, RTG_STAGE_LABEL);
   RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a));
@@ -149,7 +156,7 @@ int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int
   const int64_t fields[12] = {(int64_t)d_rgb, h, w, pitch, (int64_t)d_mask, (int64_t)d_labels,
                               (int64_t)d_hema, (int64_t)d_features, (int64_t)d_n,
                               (int64_t)ctx->fill_impl, (int64_t)ctx->stream,
-                              (int64_t)ctx->recon_impl};
+                              (int64_t)ctx->recon_impl | ((int64_t)ctx->ws_impl << 8)};
   std::memcpy(&key[0], fields, sizeof(fields));
   std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
   if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
@@ -306,6 +313,10 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
         RTG_TRY(dalloc(&c->flat_list, n));
         RTG_TRY(dalloc(&c->lroots, n));
+        c->obj_cap = (int64_t)n / 4 + 16;  // 8-connected objects are >= 1 px, <= 1 per 2x2
+        RTG_TRY(dalloc(&c->obj_root, (size_t)c->obj_cap));
+        RTG_TRY(dalloc(&c->obj_box, 4 * (size_t)c->obj_cap));
+        RTG_TRY(dalloc(&c->arena, 16 * n + 64));
         RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
         RTG_TRY(dalloc(&c->status, 1));
         RTG_TRY(dalloc(&c->stats, RTG_NUM_STATS));
@@ -336,7 +347,8 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
-                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots, c->misc,
+                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
+                  c->obj_root, c->obj_box, c->arena, c->misc,
                   c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs};
   for (void* b : bufs)
@@ -450,6 +462,10 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
       return RTG_OK;
     case RTG_OPT_USE_GRAPHS:
       ctx->use_graphs = value != 0;
+      return RTG_OK;
+    case RTG_OPT_WATERSHED_IMPL:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "watershed impl must be 0 or 1");
+      ctx->ws_impl = (int)value;
       return RTG_OK;
     case RTG_OPT_RECON_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "recon impl must be 0 or 1");
@@ -649,7 +665,10 @@ int rtg_watershed_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w,
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_mask || !d_sep_mask) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (ws_h < 0) return fail(RTG_ERR_INVALID_ARG, "ws_h must be >= 0");
-  return watershed(ctx, d_mask, h, w, ws_h, d_sep_mask, d_basin ? d_basin : ctx->labels);
+  if (ctx->ws_impl == 1)
+    return watershed(ctx, d_mask, h, w, ws_h, d_sep_mask, d_basin ? d_basin : ctx->labels);
+  RTG_TRY(ccl_roots(ctx, d_mask, h, w, 8, ctx->i32a));
+  return watershed_objects(ctx, d_mask, ctx->i32a, nullptr, 0, 0, h, w, ws_h, d_sep_mask, d_basin);
 }
 
 int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels, const uint8_t* d_intensity,

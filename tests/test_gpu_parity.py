@@ -165,24 +165,33 @@ def test_fill_holes(rtg, ctx, oracle, shape, impl):
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
 
 
+@pytest.fixture(scope="module")
+def ref2048(rtg, oracle):
+    rgb = rtg.synth_tile_host(7, 7, 2048, 2048)
+    return rgb, oracle.process_tile(rgb)
+
+
+@pytest.mark.parametrize("ws", [0, 1])
 @pytest.mark.parametrize("recon", [0, 1])
 @pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("graphs", [0, 1])
-def test_pipeline_impl_options(rtg, ctx, oracle, impl, graphs, recon):
+def test_pipeline_impl_options(rtg, ctx, ref2048, impl, graphs, recon, ws):
     """Every implementation option of the stage (fill-holes union-find vs
-    IWPP, ReconToNuclei threshold decomposition vs grayscale IWPP, graph
-    replay vs eager) gives the oracle's result bit for bit."""
-    rgb = rtg.synth_tile_host(7, 7, 2048, 2048)
-    ref = oracle.process_tile(rgb)
+    IWPP, ReconToNuclei threshold decomposition vs grayscale IWPP,
+    object-parallel vs tiled watershed, graph replay vs eager) gives the
+    oracle's result bit for bit."""
+    rgb, ref = ref2048
     ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, impl)
     ctx.set_option(rtg.OPT_USE_GRAPHS, graphs)
     ctx.set_option(rtg.OPT_RECON_IMPL, recon)
+    ctx.set_option(rtg.OPT_WATERSHED_IMPL, ws)
     try:
         mask, labels, _, feats, n = ctx.process_tile(rgb)
     finally:
         ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, 0)
         ctx.set_option(rtg.OPT_USE_GRAPHS, 1)
         ctx.set_option(rtg.OPT_RECON_IMPL, 0)
+        ctx.set_option(rtg.OPT_WATERSHED_IMPL, 0)
     assert n == ref["n"]
     assert np.array_equal(mask, ref["mask"])
     assert np.array_equal(labels, ref["labels"])
@@ -252,14 +261,50 @@ def test_edt(ctx, oracle, case):
 # ---------------------------------------------------------------- o6/o7
 
 @pytest.mark.parametrize("ws_h", [0, 3, 8])
-def test_watershed(ctx, oracle, ws_h):
+@pytest.mark.parametrize("impl", [0, 1])
+def test_watershed(rtg, ctx, oracle, ws_h, impl):
     rng = np.random.default_rng(ws_h + 100)
     h, w = 1024, 1280
     m = _rand_blobs(rng, h, w, 0.35, 2.5)
     sep_ref, basin_ref = oracle.watershed(m, ws_h)
     sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
     basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
-    ctx.watershed_dev(_np_dev(m), h, w, ws_h, sep, basin)
+    ctx.set_option(rtg.OPT_WATERSHED_IMPL, impl)
+    try:
+        ctx.watershed_dev(_np_dev(m), h, w, ws_h, sep, basin)
+    finally:
+        ctx.set_option(rtg.OPT_WATERSHED_IMPL, 0)
+    assert np.array_equal(_dev_np(basin), basin_ref)
+    assert np.array_equal(_dev_np(sep), sep_ref)
+
+
+@pytest.mark.parametrize("case", ["big_blob", "thin_diagonal", "border_touching", "all_fg"])
+def test_watershed_objects_size_classes(rtg, ctx, oracle, case):
+    """Object-parallel watershed on objects beyond the 12 KB per-warp class:
+    a large blob (227 KB CTA class), a long diagonal thread whose bbox region
+    is huge (global-arena class), objects cut by the tile border, and a tile
+    with no background at all."""
+    h, w = 600, 700
+    m = np.zeros((h, w), np.uint8)
+    if case == "big_blob":
+        yy, xx = np.mgrid[0:h, 0:w]
+        m[((yy - 250) / 110.0) ** 2 + ((xx - 300) / 70.0) ** 2 <= 1] = 1
+        m[((yy - 250) / 60.0) ** 2 + ((xx - 420) / 60.0) ** 2 <= 1] = 1
+    elif case == "thin_diagonal":
+        for k in range(560):
+            m[20 + k, 30 + k] = 1
+            m[20 + k, 31 + k] = 1
+        m[300:330, 100:140] = 1
+    elif case == "border_touching":
+        yy, xx = np.mgrid[0:h, 0:w]
+        m[(yy ** 2 + xx ** 2) < 120 ** 2] = 1
+        m[((yy - h) ** 2 + (xx - 350) ** 2) < 90 ** 2] = 1
+    else:
+        m[:] = 1
+    sep_ref, basin_ref = oracle.watershed(m, 3)
+    sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    ctx.watershed_dev(_np_dev(m), h, w, 3, sep, basin)
     assert np.array_equal(_dev_np(basin), basin_ref)
     assert np.array_equal(_dev_np(sep), sep_ref)
 
