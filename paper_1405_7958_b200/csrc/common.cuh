@@ -109,6 +109,7 @@ struct rtg_ctx {
   int32_t* lroots = nullptr;       // CCL tile-local root list (max_px)
   int32_t* obj_root = nullptr;     // object-parallel watershed: object roots
   int32_t* obj_box = nullptr;      //   and bounding boxes (4 per object)
+  int32_t* obj_list = nullptr;     //   big / pathological size-class lists
   int64_t obj_cap = 0;
   unsigned char* arena = nullptr;  //   global scratch for pathological regions
   int32_t* misc = nullptr;         // [0] n_objects, [1] flat count, [2] any_zero, [3] changed, ...

@@ -369,24 +369,39 @@ k_obj_ws_small(int h, int w, const uint8_t* __restrict__ mask, const int32_t* __
   }
 }
 
+// size classes beyond the per-warp budget go to compact lists:
+// big ones at list[0 ..), pathological ones at list[cap-1 ..] downwards
+__global__ void k_obj_classify(int h, int w, const int32_t* __restrict__ nobj,
+                               const int32_t* __restrict__ obj_root,
+                               const int32_t* __restrict__ obj_box, int32_t* __restrict__ list,
+                               int64_t cap, int32_t* __restrict__ counts2) {
+  const int total = *nobj;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    ObjView o;
+    if (!load_view(obj_root, obj_box, k, h, w, o)) continue;
+    const int64_t n = (int64_t)o.RH * o.RW;
+    if (n <= kSmallPx) continue;
+    if (n <= kBigPx) list[atomicAdd(&counts2[0], 1)] = k;
+    else list[cap - 1 - atomicAdd(&counts2[1], 1)] = k;
+  }
+}
+
 // big regions: one warp owns a whole CTA's shared memory
 __global__ void __launch_bounds__(32)
 k_obj_ws_big(int h, int w, const uint8_t* __restrict__ mask, const int32_t* __restrict__ roots,
-             const int32_t* __restrict__ nobj, const int32_t* __restrict__ obj_root,
-             const int32_t* __restrict__ obj_box, int32_t ws_h, uint8_t* __restrict__ sep,
-             int32_t* __restrict__ basin) {
+             const int32_t* __restrict__ list, const int32_t* __restrict__ counts2,
+             const int32_t* __restrict__ obj_root, const int32_t* __restrict__ obj_box,
+             int32_t ws_h, uint8_t* __restrict__ sep, int32_t* __restrict__ basin) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint8_t* F8 = smem;
   uint16_t* A = reinterpret_cast<uint16_t*>(smem + ((kBigPx + 15) & ~15));
   uint16_t* B = A + kBigPx;
   uint16_t* C = B + kBigPx;
   uint16_t* D = C + kBigPx;
-  const int total = *nobj;
-  for (int k = blockIdx.x; k < total; k += gridDim.x) {
+  const int total = counts2[0];
+  for (int j = blockIdx.x; j < total; j += gridDim.x) {
     ObjView o;
-    if (!load_view(obj_root, obj_box, k, h, w, o)) continue;
-    const int n = o.RH * o.RW;
-    if (n <= kSmallPx || n > kBigPx) continue;
+    load_view(obj_root, obj_box, list[j], h, w, o);
     object_watershed<uint16_t>(o, h, w, mask, roots, ws_h, F8, A, B, C, D, sep, basin);
   }
 }
@@ -394,20 +409,19 @@ k_obj_ws_big(int h, int w, const uint8_t* __restrict__ mask, const int32_t* __re
 // pathological regions: one warp, global-memory arena, one object at a time
 __global__ void __launch_bounds__(32)
 k_obj_ws_huge(int h, int w, const uint8_t* __restrict__ mask, const int32_t* __restrict__ roots,
-              const int32_t* __restrict__ nobj, const int32_t* __restrict__ obj_root,
-              const int32_t* __restrict__ obj_box, int32_t ws_h, unsigned char* arena,
-              int64_t arena_px, uint8_t* __restrict__ sep, int32_t* __restrict__ basin) {
+              const int32_t* __restrict__ list, int64_t cap, const int32_t* __restrict__ counts2,
+              const int32_t* __restrict__ obj_root, const int32_t* __restrict__ obj_box,
+              int32_t ws_h, unsigned char* arena, int64_t arena_px, uint8_t* __restrict__ sep,
+              int32_t* __restrict__ basin) {
   uint8_t* F8 = arena;
   uint32_t* A = reinterpret_cast<uint32_t*>(arena + ((arena_px + 15) & ~15ll));
   uint16_t* B = reinterpret_cast<uint16_t*>(A + arena_px);
   uint32_t* C = reinterpret_cast<uint32_t*>(B + ((arena_px + 1) & ~1ll));
   uint32_t* D = C + arena_px;
-  const int total = *nobj;
-  for (int k = 0; k < total; ++k) {
+  const int total = counts2[1];
+  for (int j = 0; j < total; ++j) {
     ObjView o;
-    if (!load_view(obj_root, obj_box, k, h, w, o)) continue;
-    const int64_t n = (int64_t)o.RH * o.RW;
-    if (n <= kBigPx) continue;
+    load_view(obj_root, obj_box, list[cap - 1 - j], h, w, o);
     object_watershed<uint32_t>(o, h, w, mask, roots, ws_h, F8, A, B, C, D, sep, basin);
   }
 }
@@ -484,6 +498,12 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
   const dim3 g2((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
   k_obj_bbox<<<g2, 256, 0, ctx->stream>>>((int)h, (int)w, mask, roots, objmap, ctx->obj_box);
   RTG_LAUNCH("k_obj_bbox");
+  int32_t* counts2 = ctx->misc + 26;  // [0] big, [1] pathological
+  RTG_CUDA(cudaMemsetAsync(counts2, 0, 2 * sizeof(int32_t), ctx->stream));
+  k_obj_classify<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>((int)h, (int)w, nobj, ctx->obj_root,
+                                                            ctx->obj_box, ctx->obj_list,
+                                                            ctx->obj_cap, counts2);
+  RTG_LAUNCH("k_obj_classify");
   {
     const size_t smem = (size_t)kWarpsSmall * (kSmallPx * 9 + 16);
     static bool attr[64] = {};
@@ -504,14 +524,14 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
                                     (int)smem));
       attr[ctx->device] = true;
     }
-    k_obj_ws_big<<<ctx->num_sms, 32, smem, ctx->stream>>>((int)h, (int)w, mask, roots, nobj,
-                                                         ctx->obj_root, ctx->obj_box, ws_h,
-                                                         sep, basin);
+    k_obj_ws_big<<<ctx->num_sms, 32, smem, ctx->stream>>>((int)h, (int)w, mask, roots,
+                                                         ctx->obj_list, counts2, ctx->obj_root,
+                                                         ctx->obj_box, ws_h, sep, basin);
     RTG_LAUNCH("k_obj_ws_big");
   }
-  k_obj_ws_huge<<<1, 32, 0, ctx->stream>>>((int)h, (int)w, mask, roots, nobj, ctx->obj_root,
-                                           ctx->obj_box, ws_h, ctx->arena, ctx->max_px, sep,
-                                           basin);
+  k_obj_ws_huge<<<1, 32, 0, ctx->stream>>>((int)h, (int)w, mask, roots, ctx->obj_list,
+                                           ctx->obj_cap, counts2, ctx->obj_root, ctx->obj_box,
+                                           ws_h, ctx->arena, ctx->max_px, sep, basin);
   RTG_LAUNCH("k_obj_ws_huge");
   return RTG_OK;
 }
