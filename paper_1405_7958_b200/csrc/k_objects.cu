@@ -29,10 +29,10 @@
 namespace rtg {
 namespace {
 
-constexpr int kSmallPx = 1328;    // 9 B/px -> 11952 B per warp
+constexpr int kSmallPx = 2048;    // 9 B/px -> 18432 B per warp
 constexpr int kWarpsSmall = 4;
 constexpr int kBigPx = 25000;     // 9 B/px -> 225000 B per CTA
-constexpr uint32_t kMember = 1u, kZero = 2u, kRm = 4u, kFlat = 8u;
+constexpr uint32_t kMember = 1u, kZero = 2u, kRm = 4u;
 
 struct ObjView {
   int y0, x0, RH, RW;  // region origin (tile coords) and extent
@@ -46,12 +46,15 @@ __device__ __forceinline__ uint32_t isqrt_u64(uint64_t v) {
   return (uint32_t)r;
 }
 
-// Reconstruction by dilation of J under I on an RH x RW region (8-conn),
-// cyclic down/up/right/left sweeps until three quiet sweeps follow the last
-// change.  Pixels outside the region do not exist (the region border is
-// background by construction: non-member pixels have I = 0).
-template <typename JT>
-__device__ void region_recon(JT* J, const uint16_t* I, int RH, int RW) {
+// Directional relaxation sweeps over an RH x RW region (8-connectivity):
+// cyclic down / up / right / left; each sweep relaxes every pixel from its
+// three neighbours in the previous row (column).  relax(l, q0, q1, q2) gets
+// the pixel and its predecessor indices (-1 when outside the region) and
+// returns whether it changed the pixel.  A sweep leaves its own relation
+// satisfied and a quiet sweep certifies its relation, so the fixed point is
+// reached once three quiet sweeps follow the last changing one.
+template <class Relax>
+__device__ void region_sweeps(int RH, int RW, Relax relax) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xFFFFFFFFu;
   int quiet = 0, done = 0;
@@ -64,13 +67,8 @@ __device__ void region_recon(JT* J, const uint16_t* I, int RH, int RW) {
           const int r = s == 0 ? k : RH - 1 - k;
           const int rp = s == 0 ? r - 1 : r + 1;
           if (c < RW) {
-            const int l = r * RW + c, lp = rp * RW + c;
-            uint32_t n = J[lp];
-            if (c > 0) n = max(n, (uint32_t)J[lp - 1]);
-            if (c + 1 < RW) n = max(n, (uint32_t)J[lp + 1]);
-            const uint32_t v = J[l];
-            const uint32_t nv = min(max(v, n), (uint32_t)I[l]);
-            if (nv != v) { J[l] = (JT)nv; ch = true; }
+            const int lp = rp * RW + c;
+            ch |= relax(r * RW + c, lp, c > 0 ? lp - 1 : -1, c + 1 < RW ? lp + 1 : -1);
           }
           __syncwarp();
         }
@@ -82,13 +80,8 @@ __device__ void region_recon(JT* J, const uint16_t* I, int RH, int RW) {
           const int c = s == 2 ? k : RW - 1 - k;
           const int cp = s == 2 ? c - 1 : c + 1;
           if (r < RH) {
-            const int l = r * RW + c, lp = r * RW + cp;
-            uint32_t n = J[lp];
-            if (r > 0) n = max(n, (uint32_t)J[lp - RW]);
-            if (r + 1 < RH) n = max(n, (uint32_t)J[lp + RW]);
-            const uint32_t v = J[l];
-            const uint32_t nv = min(max(v, n), (uint32_t)I[l]);
-            if (nv != v) { J[l] = (JT)nv; ch = true; }
+            const int lp = r * RW + cp;
+            ch |= relax(r * RW + c, lp, r > 0 ? lp - RW : -1, r + 1 < RH ? lp + RW : -1);
           }
           __syncwarp();
         }
@@ -101,18 +94,34 @@ __device__ void region_recon(JT* J, const uint16_t* I, int RH, int RW) {
   }
 }
 
+// Reconstruction by dilation of J under mask(l) on the region.
+template <typename JT, class MaskFn>
+__device__ void region_recon(JT* J, MaskFn mask, int RH, int RW) {
+  region_sweeps(RH, RW, [&](int l, int q0, int q1, int q2) -> bool {
+    uint32_t n = J[q0];
+    if (q1 >= 0) n = max(n, (uint32_t)J[q1]);
+    if (q2 >= 0) n = max(n, (uint32_t)J[q2]);
+    const uint32_t v = J[l];
+    const uint32_t nv = min(max(v, n), (uint32_t)mask(l));
+    if (nv == v) return false;
+    J[l] = (JT)nv;
+    return true;
+  });
+}
+
 // The whole per-object watershed on one region.  IdxT holds local indices
 // (uint16_t when the region has < 65535 pixels, else uint32_t).
+//   F8: flags; A: dq -> marker labels; B: F -> Fw; C: column EDT -> arrows;
+//   D: plateau distance -> basin (local marker root)
 template <typename IdxT>
 __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* __restrict__ mask,
                                  const int32_t* __restrict__ roots, int32_t ws_h,
                                  uint8_t* F8, IdxT* A, uint16_t* B, IdxT* C, IdxT* D,
                                  uint8_t* __restrict__ sep, int32_t* __restrict__ basin) {
   const int lane = threadIdx.x & 31;
-  const unsigned full = 0xFFFFFFFFu;
   const int RH = o.RH, RW = o.RW, n = RH * RW;
   const IdxT kNone = (IdxT)~(IdxT)0;
-  const uint32_t kInfD = (uint32_t)kNone - 1;  // "not yet reached" plateau distance
+  const uint32_t kInfD = (uint32_t)kNone - 1;  // "not reached" plateau distance
 
   // 1. membership / zero flags for the region
   for (int r = 0; r < RH; ++r) {
@@ -129,7 +138,8 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
     }
   }
   __syncwarp();
-  // 2. exact squared EDT: column distances (C), then bounded row search
+  // 2. exact squared EDT: column distances (C), then bounded row search;
+  //    dq = floor(4 * EDT) into A, HMAX marker max(dq - ws_h, 0) into B
   for (int cs = 0; cs < RW; cs += 32) {
     const int c = cs + lane;
     if (c < RW) {
@@ -150,7 +160,6 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
     }
   }
   __syncwarp();
-  // dq = floor(4 * EDT) into A; HMAX marker max(dq - ws_h, 0) into B
   for (int r = 0; r < RH; ++r) {
     for (int c = lane; c < RW; c += 32) {
       const int l = r * RW + c;
@@ -174,62 +183,29 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
     }
   }
   __syncwarp();
-  // 3. HMAX: B = recon(max(dq - h, 0), dq) over member pixels (non-members
-  //    have dq = 0 and act as barriers).  The mask must be a u16 plane: A
-  //    itself when IdxT is u16, else a u16 copy in C (dead after step 2).
-  uint16_t* dq16 = reinterpret_cast<uint16_t*>(A);
+  // 3. HMAX: B = recon(max(dq - h, 0), dq); non-members have dq = 0 (barrier).
+  //    The mask must be read as u16: A itself for u16 indices, else a u16
+  //    copy in C (dead after step 2).
+  const uint16_t* dq16 = reinterpret_cast<const uint16_t*>(A);
   if (sizeof(IdxT) != sizeof(uint16_t)) {
-    dq16 = reinterpret_cast<uint16_t*>(C);
-    for (int l = lane; l < n; l += 32) dq16[l] = (uint16_t)A[l];
+    uint16_t* cp = reinterpret_cast<uint16_t*>(C);
+    for (int l = lane; l < n; l += 32) cp[l] = (uint16_t)A[l];
     __syncwarp();
+    dq16 = cp;
   }
-  region_recon<uint16_t>(B, dq16, RH, RW);
+  region_recon<uint16_t>(B, [&](int l) { return (uint32_t)dq16[l]; }, RH, RW);
   __syncwarp();
-  // 4. Fw = member ? F + 1 : 0 (B);  G = Fw ? Fw - 1 : 0 (A as u16 view)
-  uint16_t* G16 = reinterpret_cast<uint16_t*>(A);
-  for (int l = lane; l < n; l += 32) {
-    const uint32_t f = (F8[l] & kMember) ? (uint32_t)B[l] + 1u : 0u;
-    B[l] = (uint16_t)f;
-  }
+  // 4. Fw = member ? F + 1 : 0
+  for (int l = lane; l < n; l += 32) B[l] = (F8[l] & kMember) ? (uint16_t)(B[l] + 1) : (uint16_t)0;
   __syncwarp();
-  for (int l = lane; l < n; l += 32) G16[l] = B[l] ? (uint16_t)(B[l] - 1) : (uint16_t)0;
-  __syncwarp();
-  region_recon<uint16_t>(G16, B, RH, RW);
-  __syncwarp();
-  // 5. regional maxima
-  for (int l = lane; l < n; l += 32)
-    if (B[l] && B[l] > G16[l]) F8[l] |= (uint8_t)kRm;
-  __syncwarp();
-  // 6. marker labels: minimum local index over each 8-connected marker
-  for (int l = lane; l < n; l += 32) A[l] = (F8[l] & kRm) ? (IdxT)l : kNone;
-  __syncwarp();
-  while (true) {
-    bool ch = false;
-    for (int l = lane; l < n; l += 32) {
-      if (!(F8[l] & kRm)) continue;
-      const int r = l / RW, c = l - r * RW;
-      uint32_t m = (uint32_t)A[l];
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int rr = r + dy, cc = c + dx;
-          if ((dy | dx) == 0 || rr < 0 || rr >= RH || cc < 0 || cc >= RW) continue;
-          const int q = rr * RW + cc;
-          if (F8[q] & kRm) m = min(m, (uint32_t)A[q]);
-        }
-      if (m < (uint32_t)A[l]) { A[l] = (IdxT)m; ch = true; }
-    }
-    __syncwarp();
-    if (!__any_sync(full, ch)) break;
-  }
-  // 7. arrows (C) and plateau distances (D)
-  for (int l = lane; l < n; l += 32) {
-    IdxT p = kNone, d = kNone;
-    const uint32_t f = B[l];
-    if (f) {
-      if (F8[l] & kRm) {
-        p = (IdxT)l;
-      } else {
-        const int r = l / RW, c = l - r * RW;
+  // 5. steepest-ascent arrows (C) for pixels with a higher neighbour (D = 0);
+  //    every other member pixel starts unreached (D = INF)
+  for (int r = 0; r < RH; ++r) {
+    for (int c = lane; c < RW; c += 32) {
+      const int l = r * RW + c;
+      IdxT p = kNone, d = kNone;
+      const uint32_t f = B[l];
+      if (f) {
         uint32_t best = f;
         int arg = -1;
         for (int dy = -1; dy <= 1; ++dy)
@@ -243,52 +219,65 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
           p = (IdxT)arg;
           d = 0;
         } else {
-          F8[l] |= (uint8_t)kFlat;
           d = (IdxT)kInfD;
         }
       }
+      C[l] = p;
+      D[l] = d;
     }
-    C[l] = p;
-    D[l] = d;
   }
   __syncwarp();
-  // 8. plateau BFS (Bellman-Ford to the fixed point), then plateau arrows
-  while (true) {
-    bool ch = false;
-    for (int l = lane; l < n; l += 32) {
-      if (!(F8[l] & kFlat)) continue;
-      const int r = l / RW, c = l - r * RW;
-      const uint32_t f = B[l];
-      uint32_t best = D[l];
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int rr = r + dy, cc = c + dx;
-          if ((dy | dx) == 0 || rr < 0 || rr >= RH || cc < 0 || cc >= RW) continue;
-          const int q = rr * RW + cc;
-          const uint32_t dq = D[q];
-          if (B[q] == f && dq < kInfD && dq + 1 < best) best = dq + 1;
-        }
-      if (best < (uint32_t)D[l]) { D[l] = (IdxT)best; ch = true; }
+  // 6. plateau BFS from the pixels with a higher neighbour through
+  //    equal-level member pixels.  Unreached pixels are exactly the regional
+  //    maxima (their plateau has no exit) == Fw > recon(Fw - 1, Fw).
+  region_sweeps(RH, RW, [&](int l, int q0, int q1, int q2) -> bool {
+    const uint32_t dl = D[l];
+    if (dl == 0 || dl == (uint32_t)kNone) return false;
+    const uint32_t f = B[l];
+    uint32_t best = dl;
+    const int qs[3] = {q0, q1, q2};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int q = qs[j];
+      if (q < 0 || B[q] != f) continue;
+      const uint32_t dq = D[q];
+      if (dq < kInfD && dq + 1 < best) best = dq + 1;
     }
-    __syncwarp();
-    if (!__any_sync(full, ch)) break;
-  }
-  for (int l = lane; l < n; l += 32) {
-    if (!(F8[l] & kFlat)) continue;
-    const int r = l / RW, c = l - r * RW;
-    const uint32_t f = B[l], dl = D[l];
-    IdxT arg = kNone;
-    if (dl < kInfD) {
+    if (best >= dl) return false;
+    D[l] = (IdxT)best;
+    return true;
+  });
+  // 7. markers (self arrows) and plateau arrows: the same-level neighbour at
+  //    distance delta-1 with the minimum linear index
+  for (int r = 0; r < RH; ++r) {
+    for (int c = lane; c < RW; c += 32) {
+      const int l = r * RW + c;
+      const uint32_t dl = D[l];
+      if (dl == 0 || dl == (uint32_t)kNone) continue;
+      if (dl == kInfD) {
+        F8[l] |= (uint8_t)kRm;
+        C[l] = (IdxT)l;
+        continue;
+      }
+      const uint32_t f = B[l];
+      IdxT arg = kNone;
       for (int dy = -1; dy <= 1 && arg == kNone; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {
           const int rr = r + dy, cc = c + dx;
           if ((dy | dx) == 0 || rr < 0 || rr >= RH || cc < 0 || cc >= RW) continue;
           const int q = rr * RW + cc;
-          if (B[q] == f && !(F8[q] & kRm) && (uint32_t)D[q] == dl - 1) { arg = (IdxT)q; break; }
+          if (B[q] == f && (uint32_t)D[q] == dl - 1) { arg = (IdxT)q; break; }
         }
+      C[l] = arg;
     }
-    C[l] = arg;
   }
+  __syncwarp();
+  // 8. marker labels: the minimum local index of each 8-connected marker, as
+  //    a reconstruction of (MAX - index) inside the marker set
+  const uint32_t kMaxIdx = (uint32_t)kNone;
+  for (int l = lane; l < n; l += 32) A[l] = (F8[l] & kRm) ? (IdxT)(kMaxIdx - (uint32_t)l) : (IdxT)0;
+  __syncwarp();
+  region_recon<IdxT>(A, [&](int l) { return (F8[l] & kRm) ? kMaxIdx : 0u; }, RH, RW);
   __syncwarp();
   // 9. basins: follow the arrows to a marker; basin = its marker's local root
   for (int l = lane; l < n; l += 32) {
@@ -300,35 +289,37 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
         q = nx;
         nx = C[q];
       }
-      if (nx == q) b = A[q];
+      if (nx == q) b = (IdxT)(kMaxIdx - (uint32_t)A[q]);
     }
-    D[l] = b;  // plateau distances are dead
+    D[l] = b;
   }
   __syncwarp();
   // 10. separation + write-back (local index order == global index order)
-  for (int l = lane; l < n; l += 32) {
-    if (!(F8[l] & kMember)) continue;
-    const int r = l / RW, c = l - r * RW;
-    const uint32_t b = D[l];
-    uint8_t keep = b != (uint32_t)kNone;
-    if (keep) {
-      for (int dy = -1; dy <= 1 && keep; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int rr = r + dy, cc = c + dx;
-          if ((dy | dx) == 0 || rr < 0 || rr >= RH || cc < 0 || cc >= RW) continue;
-          const uint32_t bq = D[rr * RW + cc];
-          if (bq != (uint32_t)kNone && bq > b) { keep = 0; break; }
-        }
-    }
-    const int64_t g = (int64_t)(o.y0 + r) * w + (o.x0 + c);
-    sep[g] = keep;
-    if (basin) {
-      int32_t gb = 0;
-      if (b != (uint32_t)kNone) {
-        const int br = (int)(b / (uint32_t)RW), bc = (int)(b - (uint32_t)br * RW);
-        gb = (o.y0 + br) * w + (o.x0 + bc) + 1;
+  for (int r = 0; r < RH; ++r) {
+    for (int c = lane; c < RW; c += 32) {
+      const int l = r * RW + c;
+      if (!(F8[l] & kMember)) continue;
+      const uint32_t b = D[l];
+      uint8_t keep = b != (uint32_t)kNone;
+      if (keep) {
+        for (int dy = -1; dy <= 1 && keep; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int rr = r + dy, cc = c + dx;
+            if ((dy | dx) == 0 || rr < 0 || rr >= RH || cc < 0 || cc >= RW) continue;
+            const uint32_t bq = D[rr * RW + cc];
+            if (bq != (uint32_t)kNone && bq > b) { keep = 0; break; }
+          }
       }
-      basin[g] = gb;
+      const int64_t g = (int64_t)(o.y0 + r) * w + (o.x0 + c);
+      sep[g] = keep;
+      if (basin) {
+        int32_t gb = 0;
+        if (b != (uint32_t)kNone) {
+          const int br = (int)(b / (uint32_t)RW), bc = (int)(b - (uint32_t)br * RW);
+          gb = (o.y0 + br) * w + (o.x0 + bc) + 1;
+        }
+        basin[g] = gb;
+      }
     }
   }
   __syncwarp();
