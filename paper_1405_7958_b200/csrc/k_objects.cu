@@ -32,7 +32,7 @@ namespace {
 constexpr int kSmallPx = 2048;    // 9 B/px -> 18432 B per warp
 constexpr int kWarpsSmall = 4;
 constexpr int kBigPx = 25000;     // 9 B/px -> 225000 B per CTA
-constexpr uint32_t kMember = 1u, kZero = 2u, kRm = 4u;
+constexpr uint32_t kMember = 1u, kZero = 2u, kRm = 4u, kFg = 8u;
 
 struct ObjView {
   int y0, x0, RH, RW;  // region origin (tile coords) and extent
@@ -123,21 +123,44 @@ __device__ void object_watershed(const ObjView& o, int h, int w, const uint8_t* 
   const IdxT kNone = (IdxT)~(IdxT)0;
   const uint32_t kInfD = (uint32_t)kNone - 1;  // "not reached" plateau distance
 
-  // 1. membership / zero flags for the region
-  for (int r = 0; r < RH; ++r) {
-    const int gy = o.y0 + r;
-    for (int c = lane; c < RW; c += 32) {
-      const int gx = o.x0 + c;
-      uint32_t f = 0;
-      if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-        const int64_t g = (int64_t)gy * w + gx;
-        if (!mask[g]) f = kZero;
-        else if (root_of(roots, g) == o.root) f = kMember;
+  // 1. foreground / zero flags of the region (regions lie inside the tile):
+  //    flat loop over the region, 8 independent mask loads in flight per lane
+  {
+    int r = lane / RW, c = lane - (lane / RW) * RW;  // (r, c) of l = lane
+    const int dr = 32 / RW, dc = 32 - (32 / RW) * RW;  // step of 32 pixels
+    for (int l0 = 0; l0 < n; l0 += 32 * 8) {
+      uint8_t v[8];
+      int rr[8], cc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        rr[j] = r;
+        cc[j] = c;
+        const int l = l0 + lane + 32 * j;
+        v[j] = l < n ? mask[(int64_t)(o.y0 + r) * w + (o.x0 + c)] : 0;
+        c += dc;
+        r += dr;
+        if (c >= RW) { c -= RW; ++r; }
       }
-      F8[r * RW + c] = (uint8_t)f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int l = l0 + lane + 32 * j;
+        if (l < n) F8[rr[j] * RW + cc[j]] = v[j] ? (uint8_t)kFg : (uint8_t)kZero;
+      }
     }
   }
   __syncwarp();
+  // membership: the 8-connected component of the object's root pixel (its
+  // minimum linear index, inside the region) as a binary reconstruction
+  {
+    const int lr = (o.root / w - o.y0) * RW + (o.root % w - o.x0);
+    for (int l = lane; l < n; l += 32) D[l] = (IdxT)(l == lr ? 1 : 0);
+    __syncwarp();
+    region_recon<IdxT>(D, [&](int l) { return (F8[l] & kFg) ? 1u : 0u; }, RH, RW);
+    __syncwarp();
+    for (int l = lane; l < n; l += 32)
+      if (D[l]) F8[l] |= (uint8_t)kMember;
+    __syncwarp();
+  }
   // 2. exact squared EDT: column distances (C), then bounded row search;
   //    dq = floor(4 * EDT) into A, HMAX marker max(dq - ws_h, 0) into B
   for (int cs = 0; cs < RW; cs += 32) {
