@@ -182,10 +182,10 @@ enum rtg_option {
    * recon_h), 1 = full grayscale IWPP reconstruction then threshold.  The
    * per-operator rtg_recon_*_dev entry points are always the grayscale IWPP. */
   RTG_OPT_RECON_IMPL = 2,
-  /* PreWatershed + watershed (stage and rtg_watershed_dev): 0 = object-
-   * parallel, each object's bounding-box region processed on-chip by one
-   * warp (default), 1 = tiled whole-tile passes (EDT, IWPP HMAX and
-   * regional maxima, global arrows / plateau BFS). */
+  /* PreWatershed + watershed (stage and rtg_watershed_dev): 0 = tiled
+   * whole-tile passes (EDT, IWPP HMAX, global arrows, cooperative plateau
+   * BFS that also yields the regional maxima) (default), 1 = object-parallel:
+   * each object's bounding-box region processed on-chip by one warp. */
   RTG_OPT_WATERSHED_IMPL = 3
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);

@@ -122,7 +122,7 @@ struct rtg_ctx {
   int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
   int use_graphs = 1; // replay rtg_process_tile_dev as a cached CUDA graph
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
-  int ws_impl = 0;    // 0: object-parallel watershed, 1: tiled global watershed
+  int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {

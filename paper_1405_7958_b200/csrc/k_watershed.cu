@@ -22,36 +22,30 @@ namespace {
 constexpr int32_t kInfD = 1 << 30;
 
 __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
-                          const uint16_t* __restrict__ F, uint16_t* __restrict__ Fw,
-                          uint16_t* __restrict__ G) {
+                          const uint16_t* __restrict__ F, uint16_t* __restrict__ Fw) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t f = mask[i] ? (uint32_t)F[i] + 1u : 0u;
-    Fw[i] = (uint16_t)f;
-    G[i] = (uint16_t)(f ? f - 1u : 0u);
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    Fw[i] = (uint16_t)(mask[i] ? (uint32_t)F[i] + 1u : 0u);
 }
 
-// rm / arrows / plateau list.  ptr: self for markers, steepest ascent for
-// pixels with a higher neighbour (delta 0), -2 for flat plateau pixels.
-// ptr / delta are written for foreground pixels only (consumers test Fw / the
-// mask first); rm is written everywhere (the marker CCL reads it).
+// Arrows / plateau list.  ptr: steepest ascent for pixels with a higher
+// neighbour (delta 0); every other foreground pixel goes on the plateau list
+// (delta INF): the plateau BFS either reaches it (non-maximal plateau) or not
+// — then it is a regional maximum, i.e. Fw > recon(Fw - 1, Fw), because its
+// plateau has no pixel with a higher neighbour.  ptr / delta are written for
+// foreground pixels only; rm is cleared everywhere (the BFS sets markers).
 __global__ void __launch_bounds__(256)
-k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw,
-            const uint16_t* __restrict__ G, uint8_t* __restrict__ rm,
+k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw, uint8_t* __restrict__ rm,
             int32_t* __restrict__ ptr, int32_t* __restrict__ delta,
             int32_t* __restrict__ flat_list, int32_t* __restrict__ flat_count) {
   for (int y = blockIdx.y; y < h; y += gridDim.y)
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
     const int64_t i = (int64_t)y * w + x;
     const uint32_t f = Fw[i];
-    uint8_t is_rm = 0;
+    const uint8_t is_rm = 0;
     int32_t p = -1, d = -1;
     if (f) {
-      if (f > G[i]) {
-        is_rm = 1;
-        p = (int32_t)i;
-      } else {
+      {
         uint32_t best = f;
         int32_t arg = -1;
 #pragma unroll
@@ -148,7 +142,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* arrive, unsigned* gen) {
 __global__ void __launch_bounds__(256)
 k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
              const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-             int32_t* delta, int32_t* __restrict__ ptr, int32_t* flags, unsigned* bar) {
+             int32_t* delta, int32_t* __restrict__ ptr, uint8_t* __restrict__ rm,
+             int32_t* flags, unsigned* bar) {
   const int n = *flat_count;
   if (n == 0) return;
   for (int round = 0; round <= n + 1; ++round) {
@@ -164,9 +159,14 @@ k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
   }
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
+    const int32_t di = __ldcg(&delta[i]);
+    if (di >= kInfD) {  // unreachable: a regional-maximum (marker) pixel
+      rm[i] = 1;
+      ptr[i] = i;
+      continue;
+    }
     const int y = i / w, x = i - y * w;
     const uint32_t f = Fw[i];
-    const int32_t di = delta[i];
     int32_t arg = -2;
     for (int dy = -1; dy <= 1 && arg < 0; ++dy) {
       for (int dx = -1; dx <= 1; ++dx) {
@@ -174,7 +174,7 @@ k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
         const int yy = y + dy, xx = x + dx;
         if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
         const int32_t j = yy * w + xx;
-        if (Fw[j] == f && delta[j] == di - 1) { arg = j; break; }
+        if (Fw[j] == f && __ldcg(&delta[j]) == di - 1) { arg = j; break; }
       }
     }
     ptr[i] = arg;
@@ -234,39 +234,39 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   const int64_t n = h * w;
   uint16_t* dq = ctx->u16a;
   uint16_t* F = ctx->u16b;
-  uint16_t* G = ctx->u16c;
   prof_mark(ctx, RTG_STAGE_EDT);
   RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));
   prof_mark(ctx, RTG_STAGE_MARKERS);
   RTG_TRY(iwpp_recon_u16(ctx, F, dq, h, w, 8));  // HMAX
   uint16_t* Fw = ctx->u16a;                       // dq is dead now
-  k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw, G);
+  k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw);
   RTG_LAUNCH("k_ws_prep");
-  RTG_TRY(iwpp_recon_u16(ctx, G, Fw, h, w, 8, 2));  // regional-maximum test
   prof_mark(ctx, RTG_STAGE_WATERSHED);
   int32_t* ptr = ctx->i32a;
   int32_t* delta = ctx->i32b;
   int32_t* flat_count = ctx->misc + 1;
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
   const dim3 grid2d((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
-  k_ws_arrows<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, G, ctx->rm, ptr, delta,
+  k_ws_arrows<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->rm, ptr, delta,
                                                ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
-  int32_t* mroots = ctx->i32c;
-  RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
   {
+    // plateau BFS; unreached plateau pixels become the markers (rm)
     int32_t* flags = ctx->misc + 16;                              // 2 round flags
     unsigned* bar = reinterpret_cast<unsigned*>(ctx->misc + 20);  // barrier arrive/gen
     RTG_CUDA(cudaMemsetAsync(ctx->misc + 16, 0, sizeof(int32_t) * 8, ctx->stream));
     int hh = (int)h, ww = (int)w;
     const int32_t* flat = ctx->flat_list;
-    void* args[] = {&hh, &ww, &Fw, &flat, &flat_count, &delta, &ptr, &flags, &bar};
+    uint8_t* rm = ctx->rm;
+    void* args[] = {&hh, &ww, &Fw, &flat, &flat_count, &delta, &ptr, &rm, &flags, &bar};
     // one 256-thread CTA per SM: co-resident by construction, and guaranteed
     // so by the cooperative launch
     RTG_CUDA(cudaLaunchCooperativeKernel((const void*)k_ws_plateau, dim3(ctx->num_sms),
                                          dim3(256), args, 0, ctx->stream));
     RTG_LAUNCH("k_ws_plateau");
   }
+  int32_t* mroots = ctx->i32c;
+  RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
   k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, mroots, basin);
   RTG_LAUNCH("k_ws_resolve");
   k_ws_separate<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);

@@ -122,7 +122,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
   // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
   // watershed() marks its own EDT / MARKERS / WATERSHED stages
-  if (ctx->ws_impl == 1) {
+  if (ctx->ws_impl == 0) {
     RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels));
   } else {
     // the area-threshold forest and counts already name the kept objects
@@ -666,7 +666,7 @@ int rtg_watershed_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w,
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_mask || !d_sep_mask) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (ws_h < 0) return fail(RTG_ERR_INVALID_ARG, "ws_h must be >= 0");
-  if (ctx->ws_impl == 1)
+  if (ctx->ws_impl == 0)
     return watershed(ctx, d_mask, h, w, ws_h, d_sep_mask, d_basin ? d_basin : ctx->labels);
   RTG_TRY(ccl_roots(ctx, d_mask, h, w, 8, ctx->i32a));
   return watershed_objects(ctx, d_mask, ctx->i32a, nullptr, 0, 0, h, w, ws_h, d_sep_mask, d_basin);
