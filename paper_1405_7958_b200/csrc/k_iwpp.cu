@@ -179,7 +179,22 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
     // a tile already at its upper bound (J == mask everywhere, e.g. an
     // all-background tile of a distance map) cannot change: skip the sweeps
     bool saturated = true;
-    for (int r = 0; r < 32; ++r) saturated &= Js[(r + 1) * kJS + lane + 1] == Is[r * kIS + lane];
+    uint32_t rows_active = 0;  // rows with a pixel that has mask > 0
+    bool col_active = false;
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t m = Is[r * kIS + lane];
+      saturated &= Js[(r + 1) * kJS + lane + 1] == m;
+      col_active |= m != 0;
+      rows_active |= __ballot_sync(full, m != 0) ? (1u << r) : 0u;
+    }
+    // sweeps only need the bounding box of the mask-positive pixels: every
+    // other pixel has mask 0, so J == 0 there and it neither changes nor
+    // feeds a neighbour
+    const uint32_t cols_active = __ballot_sync(full, col_active);
+    const int r0 = rows_active ? __ffs(rows_active) - 1 : 0;
+    const int r1 = rows_active ? 31 - __clz(rows_active) : -1;
+    const int c0 = cols_active ? __ffs(cols_active) - 1 : 0;
+    const int c1 = cols_active ? 31 - __clz(cols_active) : -1;
     // Sweeps run cyclically (down, up, right, left).  A sweep leaves its own
     // relation satisfied, and a sweep that changes nothing certifies its
     // relation, so the tile is at its local fixed point once the three sweeps
@@ -190,7 +205,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
       for (int s = 0;; s = (s + 1) & 3) {
         bool ch = false;
         if (s == 0) {  // down: lane = column c, neighbours in the row above
-          for (int r = 0; r < 32; ++r) {
+          for (int r = r0; r <= r1; ++r) {
             uint32_t* row = Js + (r + 1) * kJS + lane + 1;
             const uint32_t* up = row - kJS;
             uint32_t n = up[0];
@@ -201,7 +216,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
             __syncwarp();
           }
         } else if (s == 1) {  // up
-          for (int r = 31; r >= 0; --r) {
+          for (int r = r1; r >= r0; --r) {
             uint32_t* row = Js + (r + 1) * kJS + lane + 1;
             const uint32_t* dn = row + kJS;
             uint32_t n = dn[0];
@@ -212,7 +227,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
             __syncwarp();
           }
         } else if (s == 2) {  // right: lane = row r, neighbours in the column left
-          for (int c = 0; c < 32; ++c) {
+          for (int c = c0; c <= c1; ++c) {
             uint32_t* px = Js + (lane + 1) * kJS + c + 1;
             const uint32_t* lf = px - 1;
             uint32_t n = lf[0];
@@ -223,7 +238,7 @@ __device__ void visit_tile(int32_t t, T* __restrict__ J, const MaskF& maskf, int
             __syncwarp();
           }
         } else {  // left
-          for (int c = 31; c >= 0; --c) {
+          for (int c = c1; c >= c0; --c) {
             uint32_t* px = Js + (lane + 1) * kJS + c + 1;
             const uint32_t* rt = px + 1;
             uint32_t n = rt[0];
