@@ -366,18 +366,23 @@ k_iwpp(T* __restrict__ J, MaskF maskf, int h, int w, int tiles_x, int ntiles,
   };
 
   if (phase >= 0) {
-    // static pass over one colour class: tiles (ty, tx) with ty % 2 == py and
-    // tx % 2 == px are never 8-neighbours of each other, so a phase never
-    // races with itself and each later phase sees final-ish halos.  A push
-    // only marks the neighbour (state 1); k_queue_build collects the marked
-    // tiles and the phase == -1 launch drains them.
+    // static pass over one checkerboard colour: tiles with (ty + tx) % 2 ==
+    // phase share no edge, so each phase sees final-ish halos from the other
+    // colour (diagonal neighbours may race: that only costs a revisit).  A
+    // push only marks the neighbour (state 1); k_queue_build collects the
+    // marked tiles and the phase == -1 launch drains them.
     const int tiles_y = (h + kTile - 1) / kTile;
-    const int py = phase >> 1, px = phase & 1;
-    const int cy = (tiles_y - py + 1) / 2, cx = (tiles_x - px + 1) / 2;
+    const int first = phase == 0 ? (tiles_x + 1) / 2 : tiles_x / 2;  // in even rows
+    const int count = (tiles_y / 2) * tiles_x + ((tiles_y & 1) ? first : 0);
     const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * kWarpsPerBlock;
-    for (int k = warp; k < cy * cx; k += nwarps) {
-      const int t = (py + 2 * (k / cx)) * tiles_x + px + 2 * (k % cx);
+    for (int k = warp; k < count; k += nwarps) {
+      // k enumerates row pairs (2r, 2r+1): `first` tiles of colour `phase`
+      // in the even row, then the rest in the odd row
+      const int rp = k / tiles_x, rem = k - rp * tiles_x;
+      const int ty = 2 * rp + (rem < first ? 0 : 1);
+      const int tx = rem < first ? phase + 2 * rem : (phase ^ 1) + 2 * (rem - first);
+      const int t = ty * tiles_x + tx;
       if (lane == 0) {
         atomicExch(&q.state[t], 2);
         __threadfence();
@@ -500,11 +505,12 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
   int64_t* kstats = ctx->stats + 4 + 2 * kind;
   const uint32_t budget = (uint32_t)(256u * (uint32_t)ntiles + 65536u);
   if (!border_only) {
-    // four colour-class static passes, then the queue drains the wavefronts
-    for (int phase = 0; phase < 4; ++phase) {
-      const int cy = (tiles_y - (phase >> 1) + 1) / 2, cx = (tiles_x - (phase & 1) + 1) / 2;
-      if (cy <= 0 || cx <= 0) continue;
-      int blocks = (int)ceil_div((int64_t)cy * cx, kWarpsPerBlock);
+    // two checkerboard static passes, then the queue drains the wavefronts
+    for (int phase = 0; phase < 2; ++phase) {
+      const int first = phase == 0 ? (tiles_x + 1) / 2 : tiles_x / 2;
+      const int count = (tiles_y / 2) * tiles_x + ((tiles_y & 1) ? first : 0);
+      if (count <= 0) continue;
+      int blocks = (int)ceil_div((int64_t)count, kWarpsPerBlock);
       if (blocks > max_blocks) blocks = max_blocks;
       k_iwpp<T, CONN, MaskF><<<blocks, kWarpsPerBlock * 32, smem, ctx->stream>>>(
           J, maskf, (int)h, (int)w, tiles_x, ntiles, phase, ctx->tq, cap, kstats, budget,
