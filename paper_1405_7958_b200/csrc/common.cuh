@@ -187,6 +187,33 @@ __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, in
   const int32_t v = roots[i];
   return v < 0 ? -1 : roots[v];
 }
+
+// Global union-find over an i32 parent plane.  Every link points to a smaller
+// index and the root is the component minimum, so path halving by atomicMin
+// never passes the root and never disconnects a node; concurrent unions only
+// touch roots (entries equal to themselves).
+__device__ __forceinline__ int32_t uf_find_g(int32_t* par, int32_t a) {
+  int32_t p = __ldcg(par + a);
+  while (p != a) {
+    const int32_t gp = __ldcg(par + p);
+    if (gp != p) atomicMin(par + a, gp);
+    a = p;
+    p = gp;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void uf_unite_g(int32_t* par, int32_t a, int32_t b) {
+  while (true) {
+    a = uf_find_g(par, a);
+    b = uf_find_g(par, b);
+    if (a == b) return;
+    if (a < b) { const int32_t t = a; a = b; b = t; }  // a is the larger root
+    const int32_t old = atomicMin(&par[a], b);
+    if (old == a) return;
+    a = old;
+  }
+}
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n);

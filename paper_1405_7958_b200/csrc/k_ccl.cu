@@ -24,21 +24,6 @@
 namespace rtg {
 namespace {
 
-// Global find with path halving by atomicMin: every link points to a
-// smaller index and the global root is the component minimum, so lowering an
-// entry to a grand-parent never passes the root and never disconnects a
-// node; concurrent unions only touch roots (entries equal to themselves).
-__device__ __forceinline__ int32_t find_root_g(int32_t* par, int32_t a) {
-  int32_t p = __ldcg(par + a);
-  while (p != a) {
-    const int32_t gp = __ldcg(par + p);
-    if (gp != p) atomicMin(par + a, gp);
-    a = p;
-    p = gp;
-  }
-  return a;
-}
-
 // Read-only shared-memory find.
 __device__ __forceinline__ int32_t find_root(const int32_t* par, int32_t a) {
   int32_t p = par[a];
@@ -69,18 +54,6 @@ __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
     b = find_root_c(par, b);
     if (a == b) return;
     if (a < b) { const int32_t t = a; a = b; b = t; }  // a is the larger root
-    const int32_t old = atomicMin(&par[a], b);
-    if (old == a) return;
-    a = old;
-  }
-}
-
-__device__ __forceinline__ void unite_g(int32_t* par, int32_t a, int32_t b) {
-  while (true) {
-    a = find_root_g(par, a);
-    b = find_root_g(par, b);
-    if (a == b) return;
-    if (a < b) { const int32_t t = a; a = b; b = t; }
     const int32_t old = atomicMin(&par[a], b);
     if (old == a) return;
     a = old;
@@ -178,10 +151,10 @@ __global__ void k_ccl_seam_rows(int h, int w, int32_t* __restrict__ roots) {
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
   const int32_t up = p - w;
-  if (__ldcg(roots + up) >= 0) unite_g(roots, p, up);
+  if (__ldcg(roots + up) >= 0) uf_unite_g(roots, p, up);
   if (CONN == 8) {
-    if (x > 0 && __ldcg(roots + up - 1) >= 0) unite_g(roots, p, up - 1);
-    if (x + 1 < w && __ldcg(roots + up + 1) >= 0) unite_g(roots, p, up + 1);
+    if (x > 0 && __ldcg(roots + up - 1) >= 0) uf_unite_g(roots, p, up - 1);
+    if (x + 1 < w && __ldcg(roots + up + 1) >= 0) uf_unite_g(roots, p, up + 1);
   }
 }
 
@@ -194,10 +167,10 @@ __global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
   const int32_t lf = p - 1;
-  if (__ldcg(roots + lf) >= 0) unite_g(roots, p, lf);
+  if (__ldcg(roots + lf) >= 0) uf_unite_g(roots, p, lf);
   if (CONN == 8) {
-    if (y > 0 && __ldcg(roots + lf - w) >= 0) unite_g(roots, p, lf - w);
-    if (y + 1 < h && __ldcg(roots + lf + w) >= 0) unite_g(roots, p, lf + w);
+    if (y > 0 && __ldcg(roots + lf - w) >= 0) uf_unite_g(roots, p, lf - w);
+    if (y + 1 < h && __ldcg(roots + lf + w) >= 0) uf_unite_g(roots, p, lf + w);
   }
 }
 
@@ -208,7 +181,7 @@ __global__ void k_ccl_flatten_roots(const int32_t* __restrict__ lroots,
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[k];
-    const int32_t g = find_root_g(roots, r);
+    const int32_t g = uf_find_g(roots, r);
     if (g != r) atomicMin(roots + r, g);
     else if (zero) zero[r] = 0;
   }

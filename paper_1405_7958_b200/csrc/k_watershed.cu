@@ -1,7 +1,7 @@
 // o6 PreWatershed + o7 Watershed.
 //
-// Markers: F = HMAX_ws_h(dq) by IWPP reconstruction, Fw = fg ? F + 1 : 0,
-// regional maxima = Fw > recon(Fw - 1, Fw) (a second IWPP pass).
+// Markers: F = HMAX_ws_h(dq) by IWPP reconstruction, Fw = fg ? F + 1 : 0;
+// the markers are the regional maxima of Fw.
 // Watershed: the arrowing ("tobogganing") formulation of the Koerbes et al.
 // GPU watershed the paper uses: every foreground pixel points to its steepest
 // ascending 8-neighbour (max Fw, ties -> minimum linear index); pixels of
@@ -12,6 +12,14 @@
 // oracle).  Separation lines: drop pixels having an 8-neighbour with a higher
 // basin id.
 //
+// Plateaus without a grid-wide BFS: "flat" pixels (no higher neighbour) form
+// plateau components — adjacent flat pixels always share a level, since a
+// flat pixel has no higher neighbour — which are labelled by union-find.  A
+// component is a regional maximum (a marker, labelled by its minimum index,
+// which is what a CCL of the marker mask would give) iff none of its pixels
+// touches a same-level non-flat pixel ("seed", distance 1).  Only the other
+// components need distances; each is small and is solved by one warp.
+//
 // Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + sep 1 B + basin 4 B
 // out (dq/markers/Fw are internal planes).
 #include "common.cuh"
@@ -20,6 +28,8 @@ namespace rtg {
 namespace {
 
 constexpr int32_t kInfD = 1 << 30;
+constexpr int32_t kSeeded = 1 << 30;  // plateau root flag in the count word
+constexpr int32_t kCountMask = kSeeded - 1;
 
 __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
                           const uint16_t* __restrict__ F, uint16_t* __restrict__ Fw) {
@@ -28,162 +38,286 @@ __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
     Fw[i] = (uint16_t)(mask[i] ? (uint32_t)F[i] + 1u : 0u);
 }
 
-// Arrows / plateau list.  ptr: steepest ascent for pixels with a higher
-// neighbour (delta 0); every other foreground pixel goes on the plateau list
-// (delta INF): the plateau BFS either reaches it (non-maximal plateau) or not
-// — then it is a regional maximum, i.e. Fw > recon(Fw - 1, Fw), because its
-// plateau has no pixel with a higher neighbour.  ptr / delta are written for
-// foreground pixels only; rm is cleared everywhere (the BFS sets markers).
+// Arrows, one CTA per 32x32 tile with a 2-pixel halo of Fw in shared memory.
+// Non-flat pixels: steepest ascent (par = -1).  Flat pixels: par = self,
+// cnt = 0, appended to the flat list; a flat pixel with a same-level non-flat
+// neighbour is a seed (distance 1) and points at the first such neighbour in
+// row-major order (the minimum index), every other flat pixel gets ptr = -2.
+// rm is cleared everywhere (markers are set by k_ws_classify).
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw, uint8_t* __restrict__ rm,
-            int32_t* __restrict__ ptr, int32_t* __restrict__ delta,
+            int32_t* __restrict__ ptr, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             int32_t* __restrict__ flat_list, int32_t* __restrict__ flat_count) {
-  for (int y = blockIdx.y; y < h; y += gridDim.y)
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
-    const int64_t i = (int64_t)y * w + x;
-    const uint32_t f = Fw[i];
-    const uint8_t is_rm = 0;
-    int32_t p = -1, d = -1;
-    if (f) {
-      {
-        uint32_t best = f;
-        int32_t arg = -1;
+  __shared__ uint16_t sf[36][36];
+  __shared__ uint8_t shi[34][36];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < 36 * 36; k += 256) {
+    const int yy = k / 36, xx = k - yy * 36;
+    const int y = y0 - 2 + yy, x = x0 - 2 + xx;
+    sf[yy][xx] = (y >= 0 && y < h && x >= 0 && x < w) ? Fw[(int64_t)y * w + x] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int k = tid; k < 34 * 34; k += 256) {
+    const int yy = k / 34 + 1, xx = k - (k / 34) * 34 + 1;
+    const uint32_t f = sf[yy][xx];
+    const bool hi = sf[yy - 1][xx - 1] > f || sf[yy - 1][xx] > f || sf[yy - 1][xx + 1] > f ||
+                    sf[yy][xx - 1] > f || sf[yy][xx + 1] > f || sf[yy + 1][xx - 1] > f ||
+                    sf[yy + 1][xx] > f || sf[yy + 1][xx + 1] > f;
+    shi[yy - 1][xx - 1] = hi;
+  }
+  __syncthreads();
+  const int c = tid & 31;
+  for (int r = tid >> 5; r < 32; r += 8) {
+    const int y = y0 + r, x = x0 + c;
+    bool flat = false;
+    int32_t i32 = 0;
+    if (y < h && x < w) {
+      const int64_t i = (int64_t)y * w + x;
+      i32 = (int32_t)i;
+      const uint32_t f = sf[r + 2][c + 2];
+      rm[i] = 0;
+      if (f) {
+        int32_t p = -2;
+        if (shi[r + 1][c + 1]) {
+          uint32_t best = f;
+          int arg = 0;
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) {
+          for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            if (dy == 0 && dx == 0) continue;
-            const int yy = y + dy, xx = x + dx;
-            if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-            const int32_t j = yy * w + xx;
-            const uint32_t fj = Fw[j];
-            if (fj > best) { best = fj; arg = j; }  // row-major order: first max = min index
-          }
-        }
-        if (arg >= 0) {
-          p = arg;
-          d = 0;
+            for (int dx = -1; dx <= 1; ++dx) {
+              const uint32_t fj = sf[r + 2 + dy][c + 2 + dx];
+              if (fj > best) { best = fj; arg = dy * w + dx; }  // first max = min index
+            }
+          p = (int32_t)(i + arg);
+          par[i] = -1;
         } else {
-          p = -2;
-          d = kInfD;
-          const int slot = atomicAdd(flat_count, 1);
-          flat_list[slot] = (int32_t)i;
+          flat = true;
+#pragma unroll
+          for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx)
+              if (p == -2 && sf[r + 2 + dy][c + 2 + dx] == f && shi[r + 1 + dy][c + 1 + dx])
+                p = (int32_t)(i + dy * w + dx);
+          par[i] = i32;
+          cnt[i] = 0;
         }
+        ptr[i] = p;
       }
     }
-    rm[i] = is_rm;
-    if (f) {
-      ptr[i] = p;
-      delta[i] = d;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, flat);
+    if (b) {
+      int base = 0;
+      if (c == 0) base = atomicAdd(flat_count, __popc(b));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (flat) flat_list[base + __popc(b & ((1u << c) - 1u))] = i32;
     }
   }
 }
 
-// One grid-wide relaxation pass over the plateau list (chaotic Bellman-Ford:
-// values only decrease and always equal the length of some real path, so
-// passes in any order converge to the unique fixed point).  A few of these
-// resolve almost every plateau before the single-CTA pass below, which owns
-// the convergence test, has to iterate.
-// Relaxes plateau pixel i once; returns true when its distance dropped.
-// Branch-free neighbour gathers (out-of-tile neighbours alias i), so the 16
-// loads of a pixel are issued back to back.
-__device__ __forceinline__ bool relax_plateau_px(int h, int w, const uint16_t* __restrict__ Fw,
-                                                 int32_t i, int32_t* delta) {
-  const int y = i / w, x = i - y * w;
-  const uint32_t f = Fw[i];
-  const int32_t cur = __ldcg(&delta[i]);
-  int32_t best = cur;
+// Plateau components: union with the backward same-level flat neighbours
+// (a neighbour is flat iff par >= 0).
+__global__ void k_ws_union(int h, int w, const uint16_t* __restrict__ Fw,
+                           const int32_t* __restrict__ flat_list,
+                           const int32_t* __restrict__ flat_count, int32_t* par) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int y = i / w, x = i - y * w;
+    const uint16_t f = Fw[i];
+    if (y > 0) {
 #pragma unroll
-  for (int dy = -1; dy <= 1; ++dy) {
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int xx = x + dx;
+        if (xx < 0 || xx >= w) continue;
+        const int32_t j = i - w + dx;
+        if (Fw[j] == f && __ldcg(par + j) >= 0) uf_unite_g(par, i, j);
+      }
+    }
+    if (x > 0 && Fw[i - 1] == f && __ldcg(par + i - 1) >= 0) uf_unite_g(par, i, i - 1);
+  }
+}
+
+// Flattens every flat pixel onto its root, flags seeded roots and hands each
+// pixel a slot in its component (slot stored in the delta plane).
+__global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
+                           const int32_t* __restrict__ flat_count,
+                           const int32_t* __restrict__ ptr, int32_t* par, int32_t* cnt,
+                           int32_t* __restrict__ slot) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int32_t r = uf_find_g(par, i);
+    if (r != i) atomicMin(par + i, r);
+    if (ptr[i] >= 0) atomicOr(cnt + r, kSeeded);
+    slot[i] = atomicAdd(cnt + r, 1) & kCountMask;
+  }
+}
+
+// Unseeded components are the markers (rm = 1, ptr = self; the root is the
+// marker label).  Each seeded root reserves its members' range and enters the
+// component list.  alloc = {member cursor, component count} as one u64.
+__global__ void k_ws_classify(const int32_t* __restrict__ flat_list,
+                              const int32_t* __restrict__ flat_count,
+                              const int32_t* __restrict__ par, int32_t* cnt,
+                              int32_t* __restrict__ ptr, uint8_t* __restrict__ rm,
+                              unsigned long long* alloc, int32_t* __restrict__ comp_root,
+                              int32_t* __restrict__ comp_size) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int32_t r = __ldcg(par + i);
+    const int32_t v = __ldcg(cnt + r);
+    if (!(v & kSeeded)) {
+      rm[i] = 1;
+      ptr[i] = i;
+    } else if (r == i) {
+      const int32_t sz = v & kCountMask;
+      const unsigned long long old = atomicAdd(alloc, (1ull << 32) | (unsigned long long)sz);
+      const int32_t base = (int32_t)(old & 0xFFFFFFFFull), c = (int32_t)(old >> 32);
+      __stcg(cnt + r, kSeeded | base);  // members still read the flag: it stays set
+      comp_root[c] = r;
+      comp_size[c] = sz;
+    }
+  }
+}
+
+__global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
+                             const int32_t* __restrict__ flat_count,
+                             const int32_t* __restrict__ par, const int32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ slot, int32_t* __restrict__ members) {
+  const int n = *flat_count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = flat_list[k];
+    const int32_t v = cnt[par[i]];
+    if (v & kSeeded) members[(v & kCountMask) + slot[i]] = i;
+  }
+}
+
+// Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8).
+__device__ __forceinline__ uint32_t plateau_nbrs(int h, int w, const uint16_t* __restrict__ Fw,
+                                                 const int32_t* __restrict__ par, int32_t p,
+                                                 uint16_t f, int32_t r) {
+  const int y = p / w, x = p - y * w;
+  uint32_t m = 0;
+  int t = 0;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
     for (int dx = -1; dx <= 1; ++dx) {
       if (dy == 0 && dx == 0) continue;
       const int yy = y + dy, xx = x + dx;
-      const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
-      const int32_t j = in ? yy * w + xx : i;
-      const uint32_t fj = Fw[j];
-      const int32_t dj = __ldcg(&delta[j]);
-      const int32_t cand = (in && fj == f && dj >= 0 && dj < kInfD) ? dj + 1 : kInfD;
-      best = min(best, cand);
+      if (yy >= 0 && yy < h && xx >= 0 && xx < w) {
+        const int32_t j = p + dy * w + dx;
+        if (Fw[j] == f && __ldcg(par + j) == r) m |= 1u << t;
+      }
+      ++t;
     }
-  }
-  if (best < cur) {
-    __stcg(&delta[i], best);
-    return true;
-  }
-  return false;
+  return m;
 }
 
-// Software grid barrier (sense by generation).  Only used by kernels launched
-// with cudaLaunchCooperativeKernel, which guarantees co-residency.
-__device__ __forceinline__ void grid_barrier(unsigned* arrive, unsigned* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned g = atomicAdd(gen, 0u);
-    __threadfence();
-    if (atomicAdd(arrive, 1u) == gridDim.x - 1) {
-      atomicExch(arrive, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (atomicAdd(gen, 0u) == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
+  const int k = t < 4 ? t : t + 1;  // skip the centre
+  return p + (k / 3 - 1) * w + (k % 3 - 1);
 }
 
-// Plateau distances and arrows in one cooperative launch: rounds of
-// grid-wide chaotic Bellman-Ford over the plateau list until a round changes
-// nothing (values only decrease and always equal some real path length, so
-// the fixed point is the BFS distance), then every plateau pixel points at the
-// same-level neighbour at distance delta-1 with the minimum linear index.
-// flags[0..1] and bar[0..1] must be zero on entry.
+// Plateau distances and arrows, one warp per seeded component: chaotic
+// Bellman-Ford over the members (values only decrease and always equal some
+// real path length, so the fixed point is the BFS distance), then every
+// non-seed member points at its first (minimum-index) same-plateau neighbour
+// at distance d - 1.  Up to 32 * kPer members are kept in registers; larger
+// components re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
-k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw,
-             const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-             int32_t* delta, int32_t* __restrict__ ptr, uint8_t* __restrict__ rm,
-             int32_t* flags, unsigned* bar) {
-  const int n = *flat_count;
-  if (n == 0) return;
-  for (int round = 0; round <= n + 1; ++round) {
-    bool any = false;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-      any |= relax_plateau_px(h, w, Fw, flat_list[k], delta);
-    if (__syncthreads_or(any) && threadIdx.x == 0) atomicExch(&flags[round & 1], 1);
-    grid_barrier(bar, bar + 1);
-    const int changed = *(volatile int32_t*)&flags[round & 1];
-    grid_barrier(bar, bar + 1);  // everyone has read the flag
-    if (blockIdx.x == 0 && threadIdx.x == 0) flags[round & 1] = 0;  // reused two rounds later
-    if (!changed) break;
-  }
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = flat_list[k];
-    const int32_t di = __ldcg(&delta[i]);
-    if (di >= kInfD) {  // unreachable: a regional-maximum (marker) pixel
-      rm[i] = 1;
-      ptr[i] = i;
-      continue;
-    }
-    const int y = i / w, x = i - y * w;
-    const uint32_t f = Fw[i];
-    int32_t arg = -2;
-    for (int dy = -1; dy <= 1 && arg < 0; ++dy) {
-      for (int dx = -1; dx <= 1; ++dx) {
-        if (dy == 0 && dx == 0) continue;
-        const int yy = y + dy, xx = x + dx;
-        if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-        const int32_t j = yy * w + xx;
-        if (Fw[j] == f && __ldcg(&delta[j]) == di - 1) { arg = j; break; }
+k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
+             const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
+             const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
+             const unsigned long long* __restrict__ alloc, int32_t* __restrict__ ptr,
+             int32_t* delta) {
+  constexpr int kPer = 4;
+  const int ncomp = (int)(*alloc >> 32);
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  volatile int32_t* vd = delta;
+  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncomp; c += warps) {
+    const int32_t r = comp_root[c], sz = comp_size[c];
+    const int32_t* mem = members + (cnt[r] & kCountMask);
+    const uint16_t f = Fw[r];
+    if (sz <= 32 * kPer) {
+      int32_t px[kPer], d[kPer];
+      uint32_t nb[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int k = lane + 32 * q;
+        px[q] = -1;
+        d[q] = kInfD;
+        nb[q] = 0;
+        if (k < sz) {
+          px[q] = mem[k];
+          d[q] = ptr[px[q]] >= 0 ? 1 : kInfD;
+          nb[q] = plateau_nbrs(h, w, Fw, par, px[q], f, r);
+          vd[px[q]] = d[q];
+        }
+      }
+      __syncwarp();
+      while (true) {
+        bool changed = false;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          if (px[q] < 0 || d[q] == 1) continue;
+          int32_t best = d[q];
+          for (uint32_t m = nb[q]; m; m &= m - 1)
+            best = min(best, vd[nbr_index(w, px[q], __ffs(m) - 1)] + 1);
+          if (best < d[q]) {
+            d[q] = best;
+            vd[px[q]] = best;
+            changed = true;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, changed)) break;
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        if (px[q] < 0 || d[q] == 1) continue;
+        for (uint32_t m = nb[q]; m; m &= m - 1) {
+          const int32_t j = nbr_index(w, px[q], __ffs(m) - 1);
+          if (vd[j] == d[q] - 1) { ptr[px[q]] = j; break; }
+        }
+      }
+    } else {
+      for (int k = lane; k < sz; k += 32) vd[mem[k]] = ptr[mem[k]] >= 0 ? 1 : kInfD;
+      __syncwarp();
+      while (true) {
+        bool changed = false;
+        for (int k = lane; k < sz; k += 32) {
+          const int32_t p = mem[k];
+          const int32_t dp = vd[p];
+          if (dp == 1) continue;
+          int32_t best = dp;
+          for (uint32_t m = plateau_nbrs(h, w, Fw, par, p, f, r); m; m &= m - 1)
+            best = min(best, vd[nbr_index(w, p, __ffs(m) - 1)] + 1);
+          if (best < dp) {
+            vd[p] = best;
+            changed = true;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, changed)) break;
+      }
+      for (int k = lane; k < sz; k += 32) {
+        const int32_t p = mem[k];
+        const int32_t dp = vd[p];
+        if (dp == 1) continue;
+        for (uint32_t m = plateau_nbrs(h, w, Fw, par, p, f, r); m; m &= m - 1) {
+          const int32_t j = nbr_index(w, p, __ffs(m) - 1);
+          if (vd[j] == dp - 1) { ptr[p] = j; break; }
+        }
       }
     }
-    ptr[i] = arg;
   }
 }
 
 __global__ void k_ws_resolve(int64_t n, const uint8_t* __restrict__ mask,
                              const int32_t* __restrict__ ptr,
-                             const int32_t* __restrict__ mroots,
+                             const int32_t* __restrict__ par,
                              int32_t* __restrict__ basin) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -195,7 +329,7 @@ __global__ void k_ws_resolve(int64_t n, const uint8_t* __restrict__ mask,
         q = nx;
         nx = ptr[q];
       }
-      b = nx == q ? root_of(mroots, q) + 1 : 0;
+      b = nx == q ? par[q] + 1 : 0;
     }
     basin[i] = b;
   }
@@ -244,31 +378,36 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   prof_mark(ctx, RTG_STAGE_WATERSHED);
   int32_t* ptr = ctx->i32a;
   int32_t* delta = ctx->i32b;
+  int32_t* par = ctx->i32c;
   int32_t* flat_count = ctx->misc + 1;
+  auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
-  const dim3 grid2d((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
-  k_ws_arrows<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->rm, ptr, delta,
-                                               ctx->flat_list, flat_count);
+  RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
+  const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
+  k_ws_arrows<<<tiles, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->rm, ptr, par, basin,
+                                              ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
-  {
-    // plateau BFS; unreached plateau pixels become the markers (rm)
-    int32_t* flags = ctx->misc + 16;                              // 2 round flags
-    unsigned* bar = reinterpret_cast<unsigned*>(ctx->misc + 20);  // barrier arrive/gen
-    RTG_CUDA(cudaMemsetAsync(ctx->misc + 16, 0, sizeof(int32_t) * 8, ctx->stream));
-    int hh = (int)h, ww = (int)w;
-    const int32_t* flat = ctx->flat_list;
-    uint8_t* rm = ctx->rm;
-    void* args[] = {&hh, &ww, &Fw, &flat, &flat_count, &delta, &ptr, &rm, &flags, &bar};
-    // one 256-thread CTA per SM: co-resident by construction, and guaranteed
-    // so by the cooperative launch
-    RTG_CUDA(cudaLaunchCooperativeKernel((const void*)k_ws_plateau, dim3(ctx->num_sms),
-                                         dim3(256), args, 0, ctx->stream));
-    RTG_LAUNCH("k_ws_plateau");
-  }
-  int32_t* mroots = ctx->i32c;
-  RTG_TRY(ccl_roots(ctx, ctx->rm, h, w, 8, mroots));
-  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, mroots, basin);
+  const int g = ctx->num_sms * 8;
+  // seeded-component list (root, size): the arena holds 16 B per pixel
+  int32_t* comp_root = reinterpret_cast<int32_t*>(ctx->arena);
+  int32_t* comp_size = comp_root + n;
+  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count, par);
+  RTG_LAUNCH("k_ws_union");
+  k_ws_roots<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, ptr, par, basin, delta);
+  RTG_LAUNCH("k_ws_roots");
+  k_ws_classify<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, ptr, ctx->rm,
+                                            alloc, comp_root, comp_size);
+  RTG_LAUNCH("k_ws_classify");
+  k_ws_scatter<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, delta,
+                                           ctx->lroots);
+  RTG_LAUNCH("k_ws_scatter");
+  k_ws_plateau<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, par, basin,
+                                                          ctx->lroots, comp_root, comp_size,
+                                                          alloc, ptr, delta);
+  RTG_LAUNCH("k_ws_plateau");
+  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, par, basin);
   RTG_LAUNCH("k_ws_resolve");
+  const dim3 grid2d((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
   k_ws_separate<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;

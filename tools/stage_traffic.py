@@ -59,6 +59,12 @@ def split_stages(launches):
 
 
 def main():
+    if sys.argv[1] == "--kernels":  # per-launch listing of the last pass
+        for st, l in split_stages(load(sys.argv[2])):
+            dram = l.get("dram__bytes_read.sum", 0.0) + l.get("dram__bytes_write.sum", 0.0)
+            print(f"{st:12s} {l['name']:28s} {l.get('gpu__time_duration.sum', 0.0) / 1e3:8.1f} us"
+                  f" {dram / 1e6:8.1f} MB")
+        return
     launches = load(sys.argv[1])
     staged = split_stages(launches)
     agg = collections.OrderedDict()
