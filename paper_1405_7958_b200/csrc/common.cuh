@@ -106,7 +106,9 @@ struct rtg_ctx {
   int32_t* seg_summary = nullptr;  // EDT column-segment summaries
   int32_t* scan_buf = nullptr;     // CCL compaction per-chunk counts/offsets
   int32_t* flat_list = nullptr;    // watershed plateau pixel list
-  int32_t* lroots = nullptr;       // CCL tile-local root list (max_px)
+  int32_t* lroots = nullptr;       // CCL tile-local roots: (root, count | seed bit) pairs
+  uint32_t* root_bm = nullptr;     // CCL global-root bitmap (max_px / 32 words)
+  int32_t* root_wprefix = nullptr; //   and its per-word exclusive prefix
   int32_t* obj_root = nullptr;     // object-parallel watershed: object roots
   int32_t* obj_box = nullptr;      //   and bounding boxes (4 per object)
   int32_t* obj_list = nullptr;     //   big / pathological size-class lists
@@ -179,10 +181,10 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
 
 // Union-find CCL into a two-level forest: roots[p] is p's tile-local root
 // (or, for a local root, the global root); root_of(roots, p) is the minimum
-// linear index of p's component (-1 = background).  zero_at_roots, when
-// given, is zeroed at every global root (per-object counters / flags).
+// linear index of p's component (-1 = background).  counts, when given,
+// receives every component's pixel count at its global root.
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots, int32_t* zero_at_roots = nullptr);
+              int conn, int32_t* roots, int32_t* counts = nullptr);
 __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, int64_t i) {
   const int32_t v = roots[i];
   return v < 0 ? -1 : roots[v];
@@ -215,6 +217,8 @@ __device__ __forceinline__ void uf_unite_g(int32_t* par, int32_t a, int32_t b) {
   }
 }
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
+// Must directly follow the ccl_roots call that built `roots` (it reuses that
+// call's local-root list and root bitmap).
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n);
 // ReconToNuclei candidates = (recon(max(H - h, 0), H) >= t) && tissue by

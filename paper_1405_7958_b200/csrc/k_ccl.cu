@@ -1,22 +1,36 @@
-// o5 AreaThreshold + o8 BWLabel: union-find connected-component labelling
-// (Oliveira & Lotufo union-find: "a forest in which each
-// pixel is a tree ... merges adjacent trees ... flattening the trees").
+// o5 AreaThreshold + o8 BWLabel (and the components behind o3 / o4):
+// union-find connected-component labelling (Oliveira &
+// Lotufo union-find: "a forest in which each pixel is a tree ... merges
+// adjacent trees ... flattening the trees").
 //
-// 1. k_ccl_local   one CTA per 32x32 tile.  Each row is a ballot bit mask, so
-//                  a pixel's horizontal run needs no union at all (it points at
-//                  the run start); vertical unions are issued once per run
-//                  adjacency; shared-memory union-find with path halving.
-//                  Every tile-local root is appended to a short global list.
+// 1. k_ccl_tile    one warp per 32x32 tile, no block barriers.  The tile's
+//                  rows become 32 ballot bit masks; then each lane owns one
+//                  ROW and works on runs with bit arithmetic: a run is one
+//                  union-find node (its start), unions are issued once per
+//                  pair of overlapping runs of adjacent rows (shared-memory
+//                  union-find with path halving), run roots are flattened,
+//                  and per-local-root accumulators are built (pixel count,
+//                  a "seed" bit for predicates that carry one).  Each lane
+//                  then owns one COLUMN again to write every pixel's local
+//                  root with coalesced stores.  Tile-local roots go to a short
+//                  global list together with their accumulators.
+//                  The foreground predicate is a functor, so thresholding /
+//                  inversion never needs its own pass over the tile.
 // 2. k_ccl_seam_*  union across tile seams in global memory (atomicMin links,
-//                  larger root -> smaller root, path halving).
-// 3. k_ccl_flatten_roots  only the local roots are flattened, so the forest
-//                  is two-level: pixel -> local root -> global root, and
+//                  larger root -> smaller root, path halving); a seam pair
+//                  already implied by its neighbour pair plus tile-local
+//                  connectivity is skipped, so a large component costs a few
+//                  unions per seam instead of one per pixel.
+// 3. k_ccl_flatten only the local roots are flattened, so the forest is
+//                  two-level: pixel -> local root -> global root, and
 //                  consumers read root_of(i) = roots[roots[i]] instead of a
 //                  full-image flatten pass.  The global root is the minimum
-//                  linear index of the component.
-// 4. canonical compaction: global roots ranked in raster order by a chunked
-//    scan, so labels are 1..n ordered by each object's minimum pixel index
-//    (scipy's ndimage.label order).
+//                  linear index of the component.  The local accumulators are
+//                  added into the global root here (component size, seed
+//                  flag), and global roots are set in a bitmap.
+// 4. canonical compaction: the root bitmap is prefix-summed (2 MB for a
+//    4096^2 tile instead of a 64 MB root plane), so labels are 1..n ordered by
+//    each object's minimum pixel index (scipy's ndimage.label order).
 //
 // Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + labels 4 B out.
 #include "common.cuh"
@@ -60,89 +74,167 @@ __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
   }
 }
 
-template <int CONN>
-__global__ void __launch_bounds__(256)
-k_ccl_local(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__ roots,
-            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount) {
-  __shared__ int32_t par[1024];
-  __shared__ uint32_t rowbits[32];
-  __shared__ int32_t n_local, base;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
-  const int c = threadIdx.x & 31, rb = threadIdx.x >> 5;
-  if (threadIdx.x == 0) n_local = 0;
-  bool fg[4];
-  // 1. rows as bit masks; every pixel points at the start of its horizontal
-  //    run (no unions needed inside a run)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = rb + 8 * k, y = y0 + r, x = x0 + c;
-    fg[k] = y < h && x < w && mask[(int64_t)y * w + x];
-    const uint32_t bits = __ballot_sync(0xFFFFFFFFu, fg[k]);
-    if (c == 0) rowbits[r] = bits;
-    int32_t v = -1;
-    if (fg[k]) {
-      const uint32_t upto = c == 31 ? 0xFFFFFFFFu : ((2u << c) - 1u);
-      const uint32_t zeros = ~bits & upto;  // background at or left of c
-      const int start = zeros ? 32 - __clz(zeros) : 0;
-      v = r * 32 + start;
+// ---- foreground predicates ----------------------------------------------------
+struct FgMask {  // mask != 0
+  static constexpr bool kSeed = false;
+  const uint8_t* m;
+  __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool&) const {
+    fg = m[i] != 0;
+  }
+};
+struct FgThresh {  // v >= t; seed: v >= ts
+  static constexpr bool kSeed = true;
+  const uint8_t* v;
+  int32_t t, ts;
+  __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool& sd) const {
+    const int32_t a = v[i];
+    fg = a >= t;
+    sd = a >= ts;
+  }
+};
+struct FgBackground {  // m == 0; seed: on the image border
+  static constexpr bool kSeed = true;
+  const uint8_t* m;
+  int h, w;
+  __device__ __forceinline__ void eval(int64_t i, int y, int x, bool& fg, bool& sd) const {
+    fg = m[i] == 0;
+    sd = y == 0 || x == 0 || y == h - 1 || x == w - 1;
+  }
+};
+
+constexpr int kTileWarps = 4;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kSeedBit = 0x80000000u;
+
+// lowest run of ones of v (bit 0 of v set)
+__device__ __forceinline__ uint32_t low_run(uint32_t v) { return v & ~(v + 1u); }
+
+template <int CONN, class P>
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ roots,
+           int32_t* __restrict__ lroots, int32_t* __restrict__ lcount,
+           int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b) {
+  __shared__ int32_t s_par[kTileWarps][1024];
+  __shared__ uint32_t s_inf[kTileWarps][1024];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kTileWarps + wid;
+  if (tile >= ntiles) return;  // warp-uniform; the kernel has no block barrier
+  const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
+  int32_t* par = s_par[wid];
+  uint32_t* inf = s_inf[wid];
+  // 1. lane = column: rows as ballot masks (lane r keeps row r)
+  uint32_t bits = 0, seeds = 0;
+  const int x = x0 + lane;
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) {
+    const int y = y0 + r;
+    bool fg = false, sd = false;
+    if (y < h && x < w) pred.eval((int64_t)y * w + x, y, x, fg, sd);
+    const uint32_t b = __ballot_sync(kFull, fg);
+    if (lane == r) bits = b;
+    if (P::kSeed) {
+      const uint32_t sb = __ballot_sync(kFull, fg && sd);
+      if (lane == r) seeds = sb;
     }
-    par[r * 32 + c] = v;
   }
-  __syncthreads();
-  // 2. one union per run adjacency with the row above: at the first pixel of
-  //    every vertical overlap, plus the two diagonal run-end contacts (8-conn)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = rb + 8 * k;
-    if (!fg[k] || r == 0) continue;
-    const int i = r * 32 + c;
-    const uint32_t up = rowbits[r - 1], cur = rowbits[r];
-    const bool a = (up >> c) & 1u;
-    const bool aL = c > 0 && ((up >> (c - 1)) & 1u);
-    const bool aR = c < 31 && ((up >> (c + 1)) & 1u);
-    const bool cL = c > 0 && ((cur >> (c - 1)) & 1u);
-    const bool cR = c < 31 && ((cur >> (c + 1)) & 1u);
-    if (a && !(cL && aL)) unite_s(par, i, i - 32);
-    if (CONN == 8) {
-      if (!a && aL && !cL) unite_s(par, i, i - 33);
-      if (!a && aR && !cR) unite_s(par, i, i - 31);
+  // 2. lane = row: runs are nodes (named by their start), one union per pair
+  //    of overlapping runs of adjacent rows
+  const int rb = lane * 32;
+  const uint32_t starts = bits & ~(bits << 1);
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    par[rb + b] = rb + b;
+  }
+  const uint32_t up = __shfl_up_sync(kFull, bits, 1);
+  __syncwarp();
+  if (lane > 0 && up) {
+    const uint32_t upstarts = up & ~(up << 1);
+    for (uint32_t m = starts; m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const uint32_t run = low_run(bits >> b) << b;
+      uint32_t ov = up & (CONN == 8 ? (run | (run << 1) | (run >> 1)) : run);
+      while (ov) {
+        const int t = __ffs(ov) - 1;
+        const uint32_t below = upstarts & (t == 31 ? kFull : ((2u << t) - 1u));
+        const int su = 31 - __clz(below);
+        unite_s(par, rb + b, rb - 32 + su);
+        ov &= ~(low_run(up >> su) << su);
+      }
     }
   }
-  __syncthreads();
-  // 3. flatten: read-only finds, then (after a barrier) every thread writes
-  //    only its own entries — a halving store racing with a finished entry
-  //    could otherwise regress it to a non-root ancestor
-  int slot[4], lroot[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = rb + 8 * k, i = r * 32 + c;
-    slot[k] = -1;
-    lroot[k] = fg[k] ? find_root(par, i) : -1;
-    if (fg[k] && lroot[k] == i) slot[k] = atomicAdd(&n_local, 1);
+  __syncwarp();
+  // 3. flatten the run forest (read-only finds, then own-entry writes), then
+  //    accumulate pixel counts / seed bits at the local roots
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    inf[rb + b] = (uint32_t)find_root(par, rb + b);
   }
-  __syncthreads();
+  __syncwarp();
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    par[rb + b] = (int32_t)inf[rb + b];
+  }
+  __syncwarp();
+  int nroot = 0;
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    if (par[rb + b] == rb + b) {
+      inf[rb + b] = 0;
+      ++nroot;
+    }
+  }
+  __syncwarp();
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    const uint32_t run = low_run(bits >> b) << b;
+    uint32_t add = (uint32_t)__popc(run);
+    if (P::kSeed && (seeds & run)) add |= kSeedBit;
+    if (add & kSeedBit) atomicOr(&inf[par[rb + b]], kSeedBit);
+    atomicAdd(&inf[par[rb + b]], add & ~kSeedBit);
+  }
+  // publish the local roots (one global atomic per warp)
+  int incl = nroot;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (fg[k]) par[(rb + 8 * k) * 32 + c] = lroot[k];
-  __syncthreads();
-  if (threadIdx.x == 0) base = n_local ? atomicAdd(lcount, n_local) : 0;
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = rb + 8 * k, y = y0 + r, x = x0 + c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int base = 0;
+  if (lane == 31 && incl) base = atomicAdd(lcount, incl);
+  base = __shfl_sync(kFull, base, 31) + incl - nroot;
+  __syncwarp();
+  for (uint32_t m = starts; m; m &= m - 1) {
+    const int b = __ffs(m) - 1;
+    if (par[rb + b] != rb + b) continue;
+    const int32_t g = (y0 + lane) * w + x0 + b;
+    lroots[2 * base] = g;
+    lroots[2 * base + 1] = (int32_t)inf[rb + b];
+    ++base;
+    if (zero_a) zero_a[g] = 0;
+    if (zero_b) zero_b[g] = 0;
+  }
+  // 4. lane = column: every pixel's local root (global index), coalesced
+  const uint32_t upto = lane == 31 ? kFull : ((2u << lane) - 1u);
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const uint32_t b = __shfl_sync(kFull, bits, r);
+    const int y = y0 + r;
     if (y < h && x < w) {
       int32_t out = -1;
-      if (fg[k]) {
-        const int32_t lr = par[r * 32 + c];
+      if ((b >> lane) & 1u) {
+        const uint32_t zeros = ~b & upto;
+        const int start = zeros ? 32 - __clz(zeros) : 0;
+        const int32_t lr = par[r * 32 + start];
         out = (y0 + (lr >> 5)) * w + x0 + (lr & 31);
-        if (slot[k] >= 0) lroots[base + slot[k]] = out;
       }
       roots[(int64_t)y * w + x] = out;
     }
   }
 }
 
-// Seams between tile rows: pixel (y, x) with y = 32k, k >= 1.
+// Seams between tile rows: pixel (y, x) with y = 32k, k >= 1.  A pair is
+// skipped when the same two components are already joined through the pair
+// one column to the left (same tile-local runs on both sides).
 template <int CONN>
 __global__ void k_ccl_seam_rows(int h, int w, int32_t* __restrict__ roots) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -150,15 +242,22 @@ __global__ void k_ccl_seam_rows(int h, int w, int32_t* __restrict__ roots) {
   if (x >= w || y >= h) return;
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
-  const int32_t up = p - w;
-  if (__ldcg(roots + up) >= 0) uf_unite_g(roots, p, up);
+  const int32_t u = p - w;
+  const bool in_run_l = (x & 31) != 0 && __ldcg(roots + p - 1) >= 0;  // p ~ left (same run)
+  const bool fu = __ldcg(roots + u) >= 0;
+  const bool ful = x > 0 && __ldcg(roots + u - 1) >= 0;
+  if (fu && !(in_run_l && ful)) uf_unite_g(roots, p, u);
   if (CONN == 8) {
-    if (x > 0 && __ldcg(roots + up - 1) >= 0) uf_unite_g(roots, p, up - 1);
-    if (x + 1 < w && __ldcg(roots + up + 1) >= 0) uf_unite_g(roots, p, up + 1);
+    // up-left: implied by (left, up-left) when p ~ left, or by (p, up) when up ~ up-left
+    if (ful && !in_run_l && !(fu && (x & 31) != 0)) uf_unite_g(roots, p, u - 1);
+    // up-right: implied by (p, up) when up ~ up-right
+    if (x + 1 < w && __ldcg(roots + u + 1) >= 0 && !(fu && ((x + 1) & 31) != 0))
+      uf_unite_g(roots, p, u + 1);
   }
 }
 
-// Seams between tile columns: pixel (y, x) with x = 32k, k >= 1.
+// Seams between tile columns: pixel (y, x) with x = 32k, k >= 1 (vertically
+// adjacent pixels of one tile are always in one local component).
 template <int CONN>
 __global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
@@ -166,40 +265,35 @@ __global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
   if (y >= h || x >= w) return;
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
-  const int32_t lf = p - 1;
-  if (__ldcg(roots + lf) >= 0) uf_unite_g(roots, p, lf);
+  const int32_t l = p - 1;
+  const bool in_col_u = (y & 31) != 0 && __ldcg(roots + p - w) >= 0;  // p ~ up
+  const bool fl = __ldcg(roots + l) >= 0;
+  const bool ful = y > 0 && __ldcg(roots + l - w) >= 0;
+  if (fl && !(in_col_u && ful)) uf_unite_g(roots, p, l);
   if (CONN == 8) {
-    if (y > 0 && __ldcg(roots + lf - w) >= 0) uf_unite_g(roots, p, lf - w);
-    if (y + 1 < h && __ldcg(roots + lf + w) >= 0) uf_unite_g(roots, p, lf + w);
+    // up-left: implied by (up, up-left) when p ~ up, or by (p, left) when left ~ up-left
+    if (ful && !in_col_u && !(fl && (y & 31) != 0)) uf_unite_g(roots, p, l - w);
+    // down-left: implied by (p, left) when left ~ down-left
+    if (y + 1 < h && __ldcg(roots + l + w) >= 0 && !(fl && ((y + 1) & 31) != 0))
+      uf_unite_g(roots, p, l + w);
   }
 }
 
-// Flattens the local roots only; zeroes per-root counters when requested.
-__global__ void k_ccl_flatten_roots(const int32_t* __restrict__ lroots,
-                                    const int32_t* __restrict__ lcount, int32_t* roots,
-                                    int32_t* __restrict__ zero) {
+// Flattens the local roots onto the global roots and folds the local
+// accumulators into them; global roots are marked in the bitmap.
+__global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
+                              const int32_t* __restrict__ lcount, int32_t* roots,
+                              int32_t* __restrict__ counts, int32_t* __restrict__ flags,
+                              uint32_t* __restrict__ bitmap) {
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t r = lroots[k];
+    const int32_t r = lroots[2 * k];
+    const uint32_t info = (uint32_t)lroots[2 * k + 1];
     const int32_t g = uf_find_g(roots, r);
     if (g != r) atomicMin(roots + r, g);
-    else if (zero) zero[r] = 0;
-  }
-}
-
-// Area per root: warp-aggregated atomics.
-__global__ void k_area_count(int64_t n, const int32_t* __restrict__ roots,
-                             int32_t* __restrict__ counts) {
-  const unsigned full = 0xFFFFFFFFu;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t r = i < n ? root_of(roots, i) : -1;
-    const unsigned act = __ballot_sync(full, r >= 0);
-    if (r >= 0) {
-      const unsigned grp = __match_any_sync(act, r);
-      if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&counts[r], __popc(grp));
-    }
+    else if (bitmap) atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+    if (counts) atomicAdd(counts + g, (int32_t)(info & ~kSeedBit));
+    if (flags && (info & kSeedBit)) flags[g] = 1;
   }
 }
 
@@ -220,8 +314,6 @@ __global__ void k_area_filter(int64_t n, const int32_t* __restrict__ roots,
 
 // ---- canonical compaction -----------------------------------------------------
 
-constexpr int kPerThread = kScanChunk / 256;  // 16 px per thread
-
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int incl = v;
@@ -239,23 +331,6 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
     total += warp_tot[k];
   }
   return off + incl - v;
-}
-
-// global roots are exactly the pixels with roots[i] == i
-__global__ void __launch_bounds__(256)
-k_root_count(int64_t n, const int32_t* __restrict__ roots,
-             int32_t* __restrict__ chunk_cnt) {
-  __shared__ int warp_tot[8];
-  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kPerThread;
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < kPerThread; ++k) {
-    const int64_t i = base + k;
-    if (i < n && roots[i] == (int32_t)i) ++c;
-  }
-  int total;
-  block_excl_scan(c, warp_tot, total);
-  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -278,22 +353,53 @@ k_scan_chunks(int nchunks, const int32_t* __restrict__ cnt,
   if (threadIdx.x == 0 && d_total) *d_total = total;
 }
 
+// Canonical ranks from the root bitmap: per-chunk popcounts, chunk offsets,
+// per-word exclusive prefixes, then one rank per global root.
+constexpr int kBmPerThread = 16;
+constexpr int kBmChunk = 256 * kBmPerThread;  // words per chunk
+
 __global__ void __launch_bounds__(256)
-k_root_rank(int64_t n, const int32_t* __restrict__ roots,
-            const int32_t* __restrict__ chunk_off, int32_t* __restrict__ rank) {
+k_bm_count(int64_t nwords, const uint32_t* __restrict__ bm, int32_t* __restrict__ chunk_cnt) {
   __shared__ int warp_tot[8];
-  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kPerThread;
-  uint32_t bits = 0;
+  const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
+  int c = 0;
 #pragma unroll
-  for (int k = 0; k < kPerThread; ++k) {
-    const int64_t i = base + k;
-    if (i < n && roots[i] == (int32_t)i) bits |= 1u << k;
+  for (int k = 0; k < kBmPerThread; ++k)
+    if (base + k < nwords) c += __popc(bm[base + k]);
+  int total;
+  block_excl_scan(c, warp_tot, total);
+  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(256)
+k_bm_prefix(int64_t nwords, const uint32_t* __restrict__ bm,
+            const int32_t* __restrict__ chunk_off, int32_t* __restrict__ wprefix) {
+  __shared__ int warp_tot[8];
+  const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
+  uint32_t v[kBmPerThread];
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < kBmPerThread; ++k) {
+    v[k] = base + k < nwords ? bm[base + k] : 0u;
+    c += __popc(v[k]);
   }
   int total;
-  int r = block_excl_scan(__popc(bits), warp_tot, total) + chunk_off[blockIdx.x];
+  int run = block_excl_scan(c, warp_tot, total) + chunk_off[blockIdx.x];
 #pragma unroll
-  for (int k = 0; k < kPerThread; ++k) {
-    if (bits & (1u << k)) rank[base + k] = r++;
+  for (int k = 0; k < kBmPerThread; ++k) {
+    if (base + k < nwords) wprefix[base + k] = run;
+    run += __popc(v[k]);
+  }
+}
+
+__global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
+                            const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
+                            const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank) {
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t r = lroots[2 * k];
+    if (roots[r] != r) continue;
+    rank[r] = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u));
   }
 }
 
@@ -314,27 +420,8 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 }
 
 // ---- FillHoles by union-find: background components (4-conn) that touch the
-// tile border are "reached"; every other background pixel is a hole.
-__global__ void k_invert(int64_t n, const uint8_t* __restrict__ in, uint8_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (uint8_t)(in[i] == 0);
-}
-
-__global__ void k_mark_border_roots(int h, int w, const int32_t* __restrict__ roots,
-                                    int32_t* __restrict__ flag) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;  // walks the perimeter
-  const int per = 2 * (h + w);
-  if (k >= per) return;
-  int y, x;
-  if (k < w) { y = 0; x = k; }
-  else if (k < 2 * w) { y = h - 1; x = k - w; }
-  else if (k < 2 * w + h) { y = k - 2 * w; x = 0; }
-  else { y = k - 2 * w - h; x = w - 1; }
-  const int32_t r = root_of(roots, (int64_t)y * w + x);
-  if (r >= 0) flag[r] = 1;
-}
-
+// image border (seed bit of FgBackground) are "reached"; every other
+// background pixel is a hole.
 __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
                                 const int32_t* __restrict__ roots,
                                 const int32_t* __restrict__ flag, uint8_t* __restrict__ out) {
@@ -349,25 +436,7 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
 // Threshold decomposition: with flat connectivity, R = recon(marker, H)
 // satisfies  R(p) >= t  <=>  p lies in a conn-component of {H >= t} that
 // contains a pixel with marker >= t.  With marker = max(H - h, 0) and t >= 1
-// that is a pixel with H >= t + h.
-__global__ void k_thresh(int64_t n, const uint8_t* __restrict__ hema, int32_t t,
-                         uint8_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (uint8_t)(hema[i] >= t);
-}
-
-__global__ void k_mark_seeds(int64_t n, const uint8_t* __restrict__ hema, int32_t seed_t,
-                             const int32_t* __restrict__ roots, int32_t* __restrict__ flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (hema[i] >= seed_t) {
-      const int32_t r = root_of(roots, i);
-      if (r >= 0 && !flag[r]) flag[r] = 1;
-    }
-  }
-}
-
+// that is a pixel with H >= t + h (the seed bit of FgThresh).
 __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
                              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
                              uint8_t* __restrict__ out) {
@@ -378,71 +447,87 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
   }
 }
 
+// Tile pass + seams + flatten for any foreground predicate.  counts (if
+// given) receive component sizes at the global roots, flags (if given) the
+// OR of the seed bits; bitmap (if given, zeroed here) marks global roots.
+template <class P>
+int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
+            int32_t* counts, int32_t* flags, uint32_t* bitmap) {
+  int32_t* lcount = ctx->misc + 8;
+  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
+  if (bitmap)
+    RTG_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)ceil_div(h * w, 32),
+                             ctx->stream));
+  const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
+  const int ntiles = tiles_x * tiles_y;
+  const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
+  if (conn == 8)
+    k_ccl_tile<8, P><<<grid, 32 * kTileWarps, 0, ctx->stream>>>(
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags);
+  else
+    k_ccl_tile<4, P><<<grid, 32 * kTileWarps, 0, ctx->stream>>>(
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags);
+  RTG_LAUNCH("k_ccl_tile");
+  if (tiles_y > 1) {
+    const dim3 g((unsigned)ceil_div(w, 256), (unsigned)(tiles_y - 1));
+    if (conn == 8) k_ccl_seam_rows<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
+    else k_ccl_seam_rows<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
+    RTG_LAUNCH("k_ccl_seam_rows");
+  }
+  if (tiles_x > 1) {
+    const dim3 g((unsigned)ceil_div(h, 256), (unsigned)(tiles_x - 1));
+    if (conn == 8) k_ccl_seam_cols<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
+    else k_ccl_seam_cols<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
+    RTG_LAUNCH("k_ccl_seam_cols");
+  }
+  k_ccl_flatten<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts,
+                                                           flags, bitmap);
+  RTG_LAUNCH("k_ccl_flatten");
+  return RTG_OK;
+}
+
 }  // namespace
 
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
                        uint8_t* out) {
+  (void)scratch;
   const int64_t n = h * w;
   if (t <= 0) {  // R >= t everywhere: the candidates are the tissue mask
     RTG_CUDA(cudaMemcpyAsync(out, tissue, (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
     return RTG_OK;
   }
-  k_thresh<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, hema, t, scratch);
-  RTG_LAUNCH("k_thresh");
   int32_t* roots = ctx->i32a;
   int32_t* flag = ctx->i32b;
-  RTG_TRY(ccl_roots(ctx, scratch, h, w, conn, roots, flag));
-  const int64_t seed_t = (int64_t)t + recon_h;
-  if (seed_t <= 255) {
-    k_mark_seeds<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, hema, (int32_t)seed_t, roots, flag);
-    RTG_LAUNCH("k_mark_seeds");
-  }
+  const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
+  const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
+  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr));
   k_seeded_and<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag, tissue, out);
   RTG_LAUNCH("k_seeded_and");
   return RTG_OK;
 }
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
-              int32_t* roots, int32_t* zero_at_roots) {
-  int32_t* lcount = ctx->misc + 8;
-  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
-  const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
-  if (conn == 8)
-    k_ccl_local<8><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots, ctx->lroots, lcount);
-  else
-    k_ccl_local<4><<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, roots, ctx->lroots, lcount);
-  RTG_LAUNCH("k_ccl_local");
-  if (tiles.y > 1) {
-    const dim3 g((unsigned)ceil_div(w, 256), tiles.y - 1);
-    if (conn == 8) k_ccl_seam_rows<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    else k_ccl_seam_rows<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    RTG_LAUNCH("k_ccl_seam_rows");
-  }
-  if (tiles.x > 1) {
-    const dim3 g((unsigned)ceil_div(h, 256), tiles.x - 1);
-    if (conn == 8) k_ccl_seam_cols<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    else k_ccl_seam_cols<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    RTG_LAUNCH("k_ccl_seam_cols");
-  }
-  k_ccl_flatten_roots<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots,
-                                                                 zero_at_roots);
-  RTG_LAUNCH("k_ccl_flatten_roots");
-  return RTG_OK;
+              int32_t* roots, int32_t* counts) {
+  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm);
 }
 
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n) {
   const int64_t n = h * w;
-  const int nchunks = (int)ceil_div(n, kScanChunk);
+  const int64_t nwords = ceil_div(n, 32);
+  const int nchunks = (int)ceil_div(nwords, kBmChunk);
   int32_t* cnt = ctx->scan_buf;
   int32_t* off = ctx->scan_buf + nchunks;
   int32_t* rank = ctx->i32c;
-  k_root_count<<<nchunks, 256, 0, ctx->stream>>>(n, roots, cnt);
-  RTG_LAUNCH("k_root_count");
+  k_bm_count<<<nchunks, 256, 0, ctx->stream>>>(nwords, ctx->root_bm, cnt);
+  RTG_LAUNCH("k_bm_count");
   k_scan_chunks<<<1, 1024, 0, ctx->stream>>>(nchunks, cnt, off, d_n);
   RTG_LAUNCH("k_scan_chunks");
-  k_root_rank<<<nchunks, 256, 0, ctx->stream>>>(n, roots, off, rank);
+  k_bm_prefix<<<nchunks, 256, 0, ctx->stream>>>(nwords, ctx->root_bm, off, ctx->root_wprefix);
+  RTG_LAUNCH("k_bm_prefix");
+  k_root_rank<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, ctx->misc + 8, roots,
+                                                         ctx->root_bm, ctx->root_wprefix, rank);
   RTG_LAUNCH("k_root_rank");
   k_relabel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, rank, labels);
   RTG_LAUNCH("k_relabel");
@@ -451,9 +536,7 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
 
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
                 int32_t max_area, int32_t* counts, uint8_t* out) {
-  // counts were zeroed at the global roots by ccl_roots(..., counts)
-  k_area_count<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts);
-  RTG_LAUNCH("k_area_count");
+  // counts were accumulated at the global roots by ccl_roots(..., counts)
   k_area_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts, min_area,
                                                          max_area, out);
   RTG_LAUNCH("k_area_filter");
@@ -462,16 +545,12 @@ int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
 
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_t* scratch,
                   uint8_t* out) {
+  (void)scratch;
   const int64_t n = h * w;
-  k_invert<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, scratch);
-  RTG_LAUNCH("k_invert");
   int32_t* roots = ctx->i32a;
   int32_t* flag = ctx->i32b;
-  RTG_TRY(ccl_roots(ctx, scratch, h, w, 4, roots, flag));  // flags zeroed at roots
-  const int per = (int)(2 * (h + w));
-  k_mark_border_roots<<<(unsigned)ceil_div(per, 256), 256, 0, ctx->stream>>>((int)h, (int)w,
-                                                                             roots, flag);
-  RTG_LAUNCH("k_mark_border_roots");
+  RTG_TRY(ccl_run(ctx, FgBackground{bin, (int)h, (int)w}, h, w, 4, roots, nullptr, flag,
+                  nullptr));
   k_fill_uf_final<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, roots, flag, out);
   RTG_LAUNCH("k_fill_uf_final");
   return RTG_OK;

@@ -3,10 +3,9 @@
 // intensity and gradient sums, perimeter edges, bbox, min/max), step 2 runs
 // one thread per object to turn them into the feature row.
 //
-// Step 1 is a warp-level reduction: each warp covers 32 consecutive pixels,
-// groups lanes of equal label with __match_any_sync, reduces every field with
-// redux.sync (__reduce_{add,min,max}_sync) and lets one leader lane issue the
-// global atomics, so atomics scale with object-runs, not pixels.  All
+// Step 1 is a two-level reduction: vertical runs accumulated in registers
+// into a per-block shared-memory table, flushed once per (object, 64x64
+// block).  All
 // intermediates are integers, so step 1 is order-independent and exact; step
 // 2 is fp64 with FMA contraction disabled (--fmad=false), matching the oracle.
 //
@@ -28,89 +27,207 @@ __global__ void k_feat_clear(const int32_t* __restrict__ d_n, FeatureAcc acc) {
   }
 }
 
-__device__ __forceinline__ uint32_t isqrt32(uint32_t v) {
-  uint32_t r = (uint32_t)sqrt((double)v);
-  while ((uint64_t)r * r > v) --r;
-  while ((uint64_t)(r + 1) * (r + 1) <= v) ++r;
+// Step 1, one CTA per 64x64 block: every lane walks 16 rows down one column
+// and accumulates the vertical run of the current label in registers (x is
+// constant along a column, so the x moments follow from n and sum y); a run
+// ends at a label change and is added into a per-block table in shared memory
+// keyed by label (open addressing), in block-local coordinates so the sums
+// fit 32 bits (except sum g^2).  The table is flushed with one set of global
+// atomics per (object, block).  A run whose label finds the table full goes
+// straight to the global accumulators.  Labels and intensities of the block
+// (+ halo) are staged in shared memory first with coalesced loads.
+constexpr int kFB = 64;        // block edge
+constexpr int kStrip = 16;     // rows per lane walk (4 strips x 2 column halves = 8 warps)
+constexpr int kSlots = 256;    // table entries per block
+constexpr int kHalo = kFB + 2; // staged block + 1-pixel halo
+enum { kTA = 0, kTY, kTX, kTYY, kTXX, kTXY, kTI, kTII, kTG, kTP, kTFields };
+
+struct FeatTable {
+  int32_t key[kSlots];
+  uint32_t s[kTFields][kSlots];
+  unsigned long long gg[kSlots];
+  int32_t mn[kMinFields][kSlots];
+  int32_t mx[kMaxFields][kSlots];
+};
+
+__device__ __forceinline__ int table_slot(FeatTable& T, int32_t l) {
+  int s = (int)((uint32_t)l * 2654435761u >> 24);  // 8-bit hash
+  for (int probe = 0; probe < kSlots; ++probe, s = (s + 1) & (kSlots - 1)) {
+    const int32_t k = T.key[s];
+    if (k == l) return s;
+    if (k == 0) {
+      const int32_t old = atomicCAS(&T.key[s], 0, l);
+      if (old == 0 || old == l) return s;
+    }
+  }
+  return -1;
+}
+
+// One vertical run (block-local coordinates; xl fixed).
+struct ColRun {
+  uint32_t n, sy, syy, si, sii, sg, sp, mni, mxi, y0, y1;
+  unsigned long long sgg;
+};
+
+__device__ __forceinline__ void run_flush(FeatTable& T, const FeatureAcc& acc, int32_t l,
+                                          const ColRun& a, uint32_t xl, int by0, int bx0) {
+  const int s = table_slot(T, l);
+  if (s >= 0) {
+    atomicAdd(&T.s[kTA][s], a.n);
+    atomicAdd(&T.s[kTY][s], a.sy);
+    atomicAdd(&T.s[kTX][s], a.n * xl);
+    atomicAdd(&T.s[kTYY][s], a.syy);
+    atomicAdd(&T.s[kTXX][s], a.n * xl * xl);
+    atomicAdd(&T.s[kTXY][s], a.sy * xl);
+    atomicAdd(&T.s[kTI][s], a.si);
+    atomicAdd(&T.s[kTII][s], a.sii);
+    atomicAdd(&T.s[kTG][s], a.sg);
+    atomicAdd(&T.s[kTP][s], a.sp);
+    atomicAdd(&T.gg[s], a.sgg);
+    atomicMin(&T.mn[kMinI][s], (int32_t)a.mni);
+    atomicMin(&T.mn[kMinY][s], (int32_t)a.y0);
+    atomicMin(&T.mn[kMinX][s], (int32_t)xl);
+    atomicMax(&T.mx[kMaxI][s], (int32_t)a.mxi);
+    atomicMax(&T.mx[kMaxY][s], (int32_t)a.y1);
+    atomicMax(&T.mx[kMaxX][s], (int32_t)xl);
+    return;
+  }
+  // table full: global accumulators directly (global coordinates)
+  const int64_t c = acc.cap, k = l - 1;
+  const unsigned long long n = a.n, Y = by0, X = (unsigned long long)bx0 + xl;
+  unsigned long long* S = acc.sums;
+  atomicAdd(&S[kSumArea * c + k], n);
+  atomicAdd(&S[kSumY * c + k], a.sy + n * Y);
+  atomicAdd(&S[kSumX * c + k], n * X);
+  atomicAdd(&S[kSumYY * c + k], a.syy + 2 * Y * a.sy + n * Y * Y);
+  atomicAdd(&S[kSumXX * c + k], n * X * X);
+  atomicAdd(&S[kSumXY * c + k], X * (a.sy + n * Y));
+  atomicAdd(&S[kSumI * c + k], (unsigned long long)a.si);
+  atomicAdd(&S[kSumII * c + k], (unsigned long long)a.sii);
+  atomicAdd(&S[kSumG * c + k], (unsigned long long)a.sg);
+  atomicAdd(&S[kSumGG * c + k], a.sgg);
+  atomicAdd(&S[kSumPerim * c + k], (unsigned long long)a.sp);
+  atomicMin(&acc.mins[kMinI * c + k], (int32_t)a.mni);
+  atomicMin(&acc.mins[kMinY * c + k], by0 + (int32_t)a.y0);
+  atomicMin(&acc.mins[kMinX * c + k], (int32_t)X);
+  atomicMax(&acc.maxs[kMaxI * c + k], (int32_t)a.mxi);
+  atomicMax(&acc.maxs[kMaxY * c + k], by0 + (int32_t)a.y1);
+  atomicMax(&acc.maxs[kMaxX * c + k], (int32_t)X);
+}
+
+__device__ __forceinline__ uint32_t isqrt_small(uint32_t v) {  // v < 2^26
+  uint32_t r = (uint32_t)__fsqrt_rn((float)v);
+  if (r * r > v) --r;
+  if ((r + 1) * (r + 1) <= v) ++r;
   return r;
 }
 
 __global__ void __launch_bounds__(256)
 k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
              int h, int w, const int32_t* __restrict__ d_n, FeatureAcc acc) {
-  const unsigned full = 0xFFFFFFFFu;
+  __shared__ FeatTable T;
+  __shared__ int32_t SL[kHalo][kHalo];
+  __shared__ uint8_t SI[kHalo][kHalo + 2];
   const int nobj = min(*d_n, acc.cap);
-  const int lane = threadIdx.x & 31;
-  // 2-D grid-stride (rows x column chunks): a warp covers 32 consecutive
-  // pixels of one row, no per-pixel division
-  const int wpad = (w + 31) & ~31;
-  for (int y = blockIdx.y; y < h; y += gridDim.y)
-  for (int xb = blockIdx.x * blockDim.x; xb < wpad; xb += gridDim.x * blockDim.x) {
-    const int x = xb + threadIdx.x;
-    const int64_t i = (int64_t)y * w + x;
-    const int32_t l = x < w ? labels[i] : 0;
-    const bool on = l > 0 && l <= nobj;
-    const unsigned act = __ballot_sync(full, on);
-    if (!act) continue;
-    if (!on) continue;
-    const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
-    const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
-    const uint8_t* rm = I + (int64_t)ym * w;
-    const uint8_t* r0 = I + (int64_t)y * w;
-    const uint8_t* rp = I + (int64_t)yp * w;
-    const int gx = ((int)rm[xp] + 2 * (int)r0[xp] + (int)rp[xp]) -
-                   ((int)rm[xm] + 2 * (int)r0[xm] + (int)rp[xm]);
-    const int gy = ((int)rp[xm] + 2 * (int)rp[x] + (int)rp[xp]) -
-                   ((int)rm[xm] + 2 * (int)rm[x] + (int)rm[xp]);
-    const uint32_t gq = isqrt32(16u * (uint32_t)(gx * gx + gy * gy));
-    const uint32_t v = r0[x];
-    uint32_t per = 0;
-    per += (y == 0 || labels[i - w] != l);
-    per += (y == h - 1 || labels[i + w] != l);
-    per += (x == 0 || labels[i - 1] != l);
-    per += (x == w - 1 || labels[i + 1] != l);
-
-    const unsigned grp = __match_any_sync(act, l);
-    const bool leader = lane == __ffs(grp) - 1;
-    const uint32_t uy = (uint32_t)y, ux = (uint32_t)x;
-    const uint32_t s_y = __reduce_add_sync(grp, uy);
-    const uint32_t s_x = __reduce_add_sync(grp, ux);
-    const uint32_t s_yy = __reduce_add_sync(grp, uy * uy);
-    const uint32_t s_xx = __reduce_add_sync(grp, ux * ux);
-    const uint32_t s_xy = __reduce_add_sync(grp, ux * uy);
-    const uint32_t s_i = __reduce_add_sync(grp, v);
-    const uint32_t s_ii = __reduce_add_sync(grp, v * v);
-    const uint32_t s_g = __reduce_add_sync(grp, gq);
-    const uint32_t s_gg = __reduce_add_sync(grp, gq * gq);
-    const uint32_t s_p = __reduce_add_sync(grp, per);
-    const uint32_t mn_i = __reduce_min_sync(grp, v);
-    const uint32_t mx_i = __reduce_max_sync(grp, v);
-    const uint32_t mn_y = __reduce_min_sync(grp, uy);
-    const uint32_t mx_y = __reduce_max_sync(grp, uy);
-    const uint32_t mn_x = __reduce_min_sync(grp, ux);
-    const uint32_t mx_x = __reduce_max_sync(grp, ux);
-    if (leader) {
-      const int64_t k = l - 1;
-      const int64_t c = acc.cap;
-      unsigned long long* S = acc.sums;
-      atomicAdd(&S[kSumArea * c + k], (unsigned long long)__popc(grp));
-      atomicAdd(&S[kSumY * c + k], (unsigned long long)s_y);
-      atomicAdd(&S[kSumX * c + k], (unsigned long long)s_x);
-      atomicAdd(&S[kSumYY * c + k], (unsigned long long)s_yy);
-      atomicAdd(&S[kSumXX * c + k], (unsigned long long)s_xx);
-      atomicAdd(&S[kSumXY * c + k], (unsigned long long)s_xy);
-      atomicAdd(&S[kSumI * c + k], (unsigned long long)s_i);
-      atomicAdd(&S[kSumII * c + k], (unsigned long long)s_ii);
-      atomicAdd(&S[kSumG * c + k], (unsigned long long)s_g);
-      atomicAdd(&S[kSumGG * c + k], (unsigned long long)s_gg);
-      atomicAdd(&S[kSumPerim * c + k], (unsigned long long)s_p);
-      atomicMin(&acc.mins[kMinI * c + k], (int32_t)mn_i);
-      atomicMin(&acc.mins[kMinY * c + k], (int32_t)mn_y);
-      atomicMin(&acc.mins[kMinX * c + k], (int32_t)mn_x);
-      atomicMax(&acc.maxs[kMaxI * c + k], (int32_t)mx_i);
-      atomicMax(&acc.maxs[kMaxY * c + k], (int32_t)mx_y);
-      atomicMax(&acc.maxs[kMaxX * c + k], (int32_t)mx_x);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int bx0 = blockIdx.x * kFB, by0 = blockIdx.y * kFB;
+  for (int k = threadIdx.x; k < kSlots; k += blockDim.x) {
+    T.key[k] = 0;
+#pragma unroll
+    for (int f = 0; f < kTFields; ++f) T.s[f][k] = 0;
+    T.gg[k] = 0;
+#pragma unroll
+    for (int f = 0; f < kMinFields; ++f) T.mn[f][k] = INT32_MAX;
+#pragma unroll
+    for (int f = 0; f < kMaxFields; ++f) T.mx[f][k] = -1;
+  }
+  __syncthreads();
+  // stage labels (invalid -> 0, outside -> 0) and intensities (clamped, the
+  // Sobel border rule) of the block plus a 1-pixel halo
+  for (int k = threadIdx.x; k < kHalo * kHalo; k += blockDim.x) {
+    const int yy = k / kHalo, xx = k - yy * kHalo;
+    const int y = by0 - 1 + yy, x = bx0 - 1 + xx;
+    int32_t l = 0;
+    if (y >= 0 && y < h && x >= 0 && x < w) {
+      l = labels[(int64_t)y * w + x];
+      l = l > 0 && l <= nobj ? l : 0;
     }
+    const int yc = min(max(y, 0), h - 1), xc = min(max(x, 0), w - 1);
+    SL[yy][xx] = l;
+    SI[yy][xx] = I[(int64_t)yc * w + xc];
+  }
+  __syncthreads();
+  const uint32_t xl = (uint32_t)((wid & 1) * 32 + lane);
+  const int x = bx0 + (int)xl;
+  const int rs = (wid >> 1) * kStrip;
+  if (x < w) {
+    const int cx = (int)xl + 1;  // staged column
+    int32_t cur = 0;
+    ColRun a{};
+#pragma unroll 4
+    for (int r = rs; r < rs + kStrip; ++r) {
+      const int y = by0 + r;
+      if (y >= h) break;
+      const int32_t l = SL[r + 1][cx];
+      if (l != cur) {
+        if (cur) run_flush(T, acc, cur, a, xl, by0, bx0);
+        cur = l;
+        a = ColRun{};
+        a.mni = 0xFFFFFFFFu;
+        a.y0 = (uint32_t)r;
+      }
+      if (l) {
+        const int t0 = SI[r][cx - 1], t1 = SI[r][cx], t2 = SI[r][cx + 1];
+        const int m0 = SI[r + 1][cx - 1], m2 = SI[r + 1][cx + 1];
+        const int b0 = SI[r + 2][cx - 1], b1 = SI[r + 2][cx], b2 = SI[r + 2][cx + 1];
+        const int gx = (t2 + 2 * m2 + b2) - (t0 + 2 * m0 + b0);
+        const int gy = (b0 + 2 * b1 + b2) - (t0 + 2 * t1 + t2);
+        const uint32_t gq = isqrt_small(16u * (uint32_t)(gx * gx + gy * gy));
+        const uint32_t v = SI[r + 1][cx], yl = (uint32_t)r;
+        const uint32_t per = (SL[r][cx] != l) + (SL[r + 2][cx] != l) + (SL[r + 1][cx - 1] != l) +
+                             (SL[r + 1][cx + 1] != l);
+        a.n += 1;
+        a.sy += yl;
+        a.syy += yl * yl;
+        a.si += v;
+        a.sii += v * v;
+        a.sg += gq;
+        a.sgg += (unsigned long long)(gq * gq);
+        a.sp += per;
+        a.mni = min(a.mni, v);
+        a.mxi = max(a.mxi, v);
+        a.y1 = yl;
+      }
+    }
+    if (cur) run_flush(T, acc, cur, a, xl, by0, bx0);
+  }
+  __syncthreads();
+  // flush: block-local moments -> global coordinates (exact u64 arithmetic)
+  const int64_t c = acc.cap;
+  for (int s = threadIdx.x; s < kSlots; s += blockDim.x) {
+    const int32_t l = T.key[s];
+    if (l == 0) continue;
+    const int64_t k = l - 1;
+    const unsigned long long n = T.s[kTA][s], Y = by0, X = bx0;
+    const unsigned long long sy = T.s[kTY][s], sx = T.s[kTX][s];
+    unsigned long long* S = acc.sums;
+    atomicAdd(&S[kSumArea * c + k], n);
+    atomicAdd(&S[kSumY * c + k], sy + n * Y);
+    atomicAdd(&S[kSumX * c + k], sx + n * X);
+    atomicAdd(&S[kSumYY * c + k], T.s[kTYY][s] + 2 * Y * sy + n * Y * Y);
+    atomicAdd(&S[kSumXX * c + k], T.s[kTXX][s] + 2 * X * sx + n * X * X);
+    atomicAdd(&S[kSumXY * c + k], T.s[kTXY][s] + X * sy + Y * sx + n * X * Y);
+    atomicAdd(&S[kSumI * c + k], (unsigned long long)T.s[kTI][s]);
+    atomicAdd(&S[kSumII * c + k], (unsigned long long)T.s[kTII][s]);
+    atomicAdd(&S[kSumG * c + k], (unsigned long long)T.s[kTG][s]);
+    atomicAdd(&S[kSumGG * c + k], T.gg[s]);
+    atomicAdd(&S[kSumPerim * c + k], (unsigned long long)T.s[kTP][s]);
+    atomicMin(&acc.mins[kMinI * c + k], T.mn[kMinI][s]);
+    atomicMin(&acc.mins[kMinY * c + k], by0 + T.mn[kMinY][s]);
+    atomicMin(&acc.mins[kMinX * c + k], bx0 + T.mn[kMinX][s]);
+    atomicMax(&acc.maxs[kMaxI * c + k], T.mx[kMaxI][s]);
+    atomicMax(&acc.maxs[kMaxY * c + k], by0 + T.mx[kMaxY][s]);
+    atomicMax(&acc.maxs[kMaxX * c + k], bx0 + T.mx[kMaxX][s]);
   }
 }
 
@@ -181,7 +298,7 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
   const int gclear = (int)ceil_div(cap, 256);
   k_feat_clear<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc);
   RTG_LAUNCH("k_feat_clear");
-  const dim3 grid((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
+  const dim3 grid((unsigned)ceil_div(w, kFB), (unsigned)ceil_div(h, kFB));
   k_feat_accum<<<grid, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n, ctx->acc);
   RTG_LAUNCH("k_feat_accum");
   k_feat_finalize<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc, out, ctx->status);

@@ -16,13 +16,13 @@ import sys
 
 STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("colordeconv", "k_colordeconv_vec", None),
-    ("recon", "k_thresh", None),
-    ("fill_holes", "k_invert", None),
-    ("area", "k_ccl_local", "k_fill_uf_final"),
+    ("recon", "k_ccl_tile", None),
+    ("fill_holes", "k_ccl_tile", "k_seeded_and"),
+    ("area", "k_ccl_tile", "k_fill_uf_final"),
     ("edt", "k_edt_seg", None),
     ("markers", "k_tiles_init", None),
     ("watershed", "k_ws_arrows", None),
-    ("label", "k_ccl_local", "k_ws_separate"),
+    ("label", "k_ccl_tile", "k_ws_separate"),
     ("features", "k_feat_clear", None),
 ]
 
