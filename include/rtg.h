@@ -183,10 +183,15 @@ enum rtg_option {
    * per-operator rtg_recon_*_dev entry points are always the grayscale IWPP. */
   RTG_OPT_RECON_IMPL = 2,
   /* PreWatershed + watershed (stage and rtg_watershed_dev): 0 = tiled
-   * whole-tile passes (EDT, IWPP HMAX, global arrows, cooperative plateau
-   * BFS that also yields the regional maxima) (default), 1 = object-parallel:
-   * each object's bounding-box region processed on-chip by one warp. */
-  RTG_OPT_WATERSHED_IMPL = 3
+   * whole-tile passes (EDT, HMAX, global arrows, plateau components that
+   * also yield the regional maxima) (default), 1 = object-parallel: each
+   * object's bounding-box region processed on-chip by one warp. */
+  RTG_OPT_WATERSHED_IMPL = 3,
+  /* HMAX of the distance map in the tiled watershed: 0 = sparse components
+   * (default: a pixel with a neighbour at least ws_h higher keeps its value;
+   * the few remaining pixels form small components, one warp each),
+   * 1 = IWPP reconstruction on the tile queue. */
+  RTG_OPT_HMAX_IMPL = 4
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

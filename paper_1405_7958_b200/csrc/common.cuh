@@ -125,6 +125,7 @@ struct rtg_ctx {
   int use_graphs = 1; // replay rtg_process_tile_dev as a cached CUDA graph
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
+  int hmax_impl = 0;  // 0: sparse components, 1: IWPP
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {

@@ -149,7 +149,7 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
     const int32_t i = flat_list[k];
     const int32_t r = uf_find_g(par, i);
     if (r != i) atomicMin(par + i, r);
-    if (ptr[i] >= 0) atomicOr(cnt + r, kSeeded);
+    if (ptr && ptr[i] >= 0) atomicOr(cnt + r, kSeeded);
     slot[i] = atomicAdd(cnt + r, 1) & kCountMask;
   }
 }
@@ -315,6 +315,207 @@ k_ws_plateau(int h, int w, const uint16_t* __restrict__ Fw, const int32_t* __res
   }
 }
 
+// ---- HMAX by sparse components ------------------------------------------------
+// F = recon(max(dq - h, 0), dq).  A foreground pixel p with an 8-neighbour q,
+// dq(q) >= dq(p) + h, keeps F(p) = dq(p): q's marker reaches p through two
+// pixels >= dq(p), and F <= dq.  The remaining foreground pixels ("suspects")
+// form small 8-connected components; within one, F is the reconstruction of
+// the marker under dq with the component's fixed neighbours (F = dq, or 0 on
+// background) as boundary values, so each component is independent and one
+// warp iterates it to its fixed point.  Output: Fw = fg ? F + 1 : 0.
+__global__ void __launch_bounds__(256)
+k_hmax_init(int h, int w, const uint16_t* __restrict__ dq, int32_t ws_h,
+            uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
+            int32_t* __restrict__ cnt, int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  __shared__ uint16_t sd[34][36];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < 34 * 34; k += 256) {
+    const int yy = k / 34, xx = k - yy * 34;
+    const int y = y0 - 1 + yy, x = x0 - 1 + xx;
+    sd[yy][xx] = (y >= 0 && y < h && x >= 0 && x < w) ? dq[(int64_t)y * w + x] : (uint16_t)0;
+  }
+  __syncthreads();
+  const int c = tid & 31;
+  for (int r = tid >> 5; r < 32; r += 8) {
+    const int y = y0 + r, x = x0 + c;
+    bool sus = false;
+    int32_t i32 = 0;
+    if (y < h && x < w) {
+      const int64_t i = (int64_t)y * w + x;
+      i32 = (int32_t)i;
+      const int32_t v = sd[r + 1][c + 1];
+      uint32_t fw = 0;
+      if (v) {
+        int32_t mx = 0;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) mx = max(mx, (int32_t)sd[r + dy][c + dx]);
+        if (mx >= v + ws_h) {
+          fw = (uint32_t)v + 1u;
+        } else {
+          sus = true;
+          fw = (uint32_t)(v > ws_h ? v - ws_h : 0) + 1u;
+          par[i] = i32;
+          cnt[i] = 0;
+        }
+      }
+      Fw[i] = (uint16_t)fw;
+      sflag[i] = sus;
+    }
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, sus);
+    if (b) {
+      int base = 0;
+      if (c == 0) base = atomicAdd(count, __popc(b));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (sus) list[base + __popc(b & ((1u << c) - 1u))] = i32;
+    }
+  }
+}
+
+__global__ void k_hmax_union(int h, int w, const uint8_t* __restrict__ sflag,
+                             const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                             int32_t* par) {
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = list[k];
+    const int y = i / w, x = i - y * w;
+    if (y > 0) {
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int xx = x + dx;
+        if (xx >= 0 && xx < w && sflag[i - w + dx]) uf_unite_g(par, i, i - w + dx);
+      }
+    }
+    if (x > 0 && sflag[i - 1]) uf_unite_g(par, i, i - 1);
+  }
+}
+
+// Every component root reserves its members' range (cnt[r] := kSeeded | base,
+// the form k_ws_scatter reads) and enters the component list.
+__global__ void k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                             const int32_t* __restrict__ par, int32_t* cnt,
+                             unsigned long long* alloc, int32_t* __restrict__ comp_root,
+                             int32_t* __restrict__ comp_size) {
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t i = list[k];
+    if (__ldcg(par + i) != i) continue;
+    const int32_t sz = __ldcg(cnt + i) & kCountMask;
+    const unsigned long long old = atomicAdd(alloc, (1ull << 32) | (unsigned long long)sz);
+    const int32_t base = (int32_t)(old & 0xFFFFFFFFull), c = (int32_t)(old >> 32);
+    cnt[i] = kSeeded | base;
+    comp_root[c] = i;
+    comp_size[c] = sz;
+  }
+}
+
+// Neighbour summary of suspect p: bit t set = row-major neighbour t is a
+// suspect (same component); fixed = max F over the other neighbours.
+__device__ __forceinline__ uint32_t hmax_nbrs(int h, int w, const uint16_t* __restrict__ dq,
+                                              const uint8_t* __restrict__ sflag, int32_t p,
+                                              int32_t& fixed) {
+  const int y = p / w, x = p - y * w;
+  uint32_t m = 0;
+  int t = 0;
+  fixed = 0;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dy == 0 && dx == 0) continue;
+      const int yy = y + dy, xx = x + dx;
+      if (yy >= 0 && yy < h && xx >= 0 && xx < w) {
+        const int32_t j = p + dy * w + dx;
+        if (sflag[j]) m |= 1u << t;
+        else fixed = max(fixed, (int32_t)dq[j]);
+      }
+      ++t;
+    }
+  return m;
+}
+
+__global__ void __launch_bounds__(256)
+k_hmax_solve(int h, int w, const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag,
+             int32_t ws_h, const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
+             const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
+             const unsigned long long* __restrict__ alloc, uint16_t* Fw) {
+  constexpr int kPer = 4;
+  const int ncomp = (int)(*alloc >> 32);
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  volatile uint16_t* vf = Fw;
+  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncomp; c += warps) {
+    const int32_t r = comp_root[c], sz = comp_size[c];
+    const int32_t* mem = members + (cnt[r] & kCountMask);
+    if (sz <= 32 * kPer) {
+      int32_t px[kPer], d[kPer], f[kPer];
+      uint32_t nb[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int k = lane + 32 * q;
+        px[q] = -1;
+        d[q] = f[q] = 0;
+        nb[q] = 0;
+        if (k < sz) {
+          px[q] = mem[k];
+          d[q] = dq[px[q]];
+          int32_t fixed;
+          nb[q] = hmax_nbrs(h, w, dq, sflag, px[q], fixed);
+          f[q] = min(d[q], max(d[q] > ws_h ? d[q] - ws_h : 0, fixed));
+          vf[px[q]] = (uint16_t)(f[q] + 1);
+        }
+      }
+      __syncwarp();
+      while (true) {
+        bool changed = false;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          if (px[q] < 0 || f[q] == d[q]) continue;
+          int32_t best = f[q];
+          for (uint32_t m = nb[q]; m; m &= m - 1)
+            best = max(best, (int32_t)vf[nbr_index(w, px[q], __ffs(m) - 1)] - 1);
+          best = min(best, d[q]);
+          if (best > f[q]) {
+            f[q] = best;
+            vf[px[q]] = (uint16_t)(best + 1);
+            changed = true;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, changed)) break;
+      }
+    } else {
+      for (int k = lane; k < sz; k += 32) {
+        const int32_t p = mem[k];
+        const int32_t dp = dq[p];
+        int32_t fixed;
+        hmax_nbrs(h, w, dq, sflag, p, fixed);
+        vf[p] = (uint16_t)(min(dp, max(dp > ws_h ? dp - ws_h : 0, fixed)) + 1);
+      }
+      __syncwarp();
+      while (true) {
+        bool changed = false;
+        for (int k = lane; k < sz; k += 32) {
+          const int32_t p = mem[k];
+          const int32_t dp = dq[p], fp = (int32_t)vf[p] - 1;
+          if (fp == dp) continue;
+          int32_t fixed;
+          int32_t best = fp;
+          for (uint32_t m = hmax_nbrs(h, w, dq, sflag, p, fixed); m; m &= m - 1)
+            best = max(best, (int32_t)vf[nbr_index(w, p, __ffs(m) - 1)] - 1);
+          best = min(best, dp);
+          if (best > fp) {
+            vf[p] = (uint16_t)(best + 1);
+            changed = true;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, changed)) break;
+      }
+    }
+  }
+}
+
 __global__ void k_ws_resolve(int64_t n, const uint8_t* __restrict__ mask,
                              const int32_t* __restrict__ ptr,
                              const int32_t* __restrict__ par,
@@ -369,28 +570,57 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   uint16_t* dq = ctx->u16a;
   uint16_t* F = ctx->u16b;
   prof_mark(ctx, RTG_STAGE_EDT);
-  RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));
+  const bool iwpp_hmax = ctx->hmax_impl == 1;
+  RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, iwpp_hmax ? F : nullptr, ws_h));
   prof_mark(ctx, RTG_STAGE_MARKERS);
-  RTG_TRY(iwpp_recon_u16(ctx, F, dq, h, w, 8));  // HMAX
-  uint16_t* Fw = ctx->u16a;                       // dq is dead now
-  k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw);
-  RTG_LAUNCH("k_ws_prep");
+  uint16_t* Fw;
+  const int g = ctx->num_sms * 8;
+  // component lists (root, size): the arena holds 16 B per pixel
+  int32_t* comp_root = reinterpret_cast<int32_t*>(ctx->arena);
+  int32_t* comp_size = comp_root + n;
+  auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
+  if (iwpp_hmax) {
+    RTG_TRY(iwpp_recon_u16(ctx, F, dq, h, w, 8));  // HMAX
+    Fw = ctx->u16a;                                 // dq is dead now
+    k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw);
+    RTG_LAUNCH("k_ws_prep");
+  } else {
+    Fw = F;
+    int32_t* list = ctx->flat_list;
+    int32_t* count = ctx->misc + 1;
+    int32_t* par = ctx->i32c;
+    int32_t* slot = ctx->i32b;
+    uint8_t* sflag = ctx->m1;
+    RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
+    RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
+    const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
+    k_hmax_init<<<tiles, 256, 0, ctx->stream>>>((int)h, (int)w, dq, ws_h, Fw, sflag, par, basin,
+                                                list, count);
+    RTG_LAUNCH("k_hmax_init");
+    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, sflag, list, count, par);
+    RTG_LAUNCH("k_hmax_union");
+    k_ws_roots<<<g, 256, 0, ctx->stream>>>(list, count, nullptr, par, basin, slot);
+    RTG_LAUNCH("k_ws_roots");
+    k_hmax_alloc<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, alloc, comp_root,
+                                             comp_size);
+    RTG_LAUNCH("k_hmax_alloc");
+    k_ws_scatter<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, slot, ctx->lroots);
+    RTG_LAUNCH("k_ws_scatter");
+    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, dq, sflag, ws_h, basin,
+                                             ctx->lroots, comp_root, comp_size, alloc, Fw);
+    RTG_LAUNCH("k_hmax_solve");
+  }
   prof_mark(ctx, RTG_STAGE_WATERSHED);
   int32_t* ptr = ctx->i32a;
   int32_t* delta = ctx->i32b;
   int32_t* par = ctx->i32c;
   int32_t* flat_count = ctx->misc + 1;
-  auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
   RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
   const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
   k_ws_arrows<<<tiles, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->rm, ptr, par, basin,
                                               ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
-  const int g = ctx->num_sms * 8;
-  // seeded-component list (root, size): the arena holds 16 B per pixel
-  int32_t* comp_root = reinterpret_cast<int32_t*>(ctx->arena);
-  int32_t* comp_size = comp_root + n;
   k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, Fw, ctx->flat_list, flat_count, par);
   RTG_LAUNCH("k_ws_union");
   k_ws_roots<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, ptr, par, basin, delta);

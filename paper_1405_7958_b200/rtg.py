@@ -45,6 +45,7 @@ OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
 OPT_USE_GRAPHS = 1       # 1 replay cached CUDA graphs in process_tile_dev (default)
 OPT_RECON_IMPL = 2       # 0 threshold decomposition (default), 1 grayscale IWPP
 OPT_WATERSHED_IMPL = 3   # 0 tiled whole-tile passes (default), 1 object-parallel
+OPT_HMAX_IMPL = 4        # 0 sparse components (default), 1 IWPP tile queue
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features"]
 

@@ -171,7 +171,7 @@ def ref2048(rtg, oracle):
     return rgb, oracle.process_tile(rgb)
 
 
-@pytest.mark.parametrize("ws", [0, 1])
+@pytest.mark.parametrize("ws", [0, 1, 2])
 @pytest.mark.parametrize("recon", [0, 1])
 @pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("graphs", [0, 1])
@@ -184,7 +184,8 @@ def test_pipeline_impl_options(rtg, ctx, ref2048, impl, graphs, recon, ws):
     ctx.set_option(rtg.OPT_FILL_HOLES_IMPL, impl)
     ctx.set_option(rtg.OPT_USE_GRAPHS, graphs)
     ctx.set_option(rtg.OPT_RECON_IMPL, recon)
-    ctx.set_option(rtg.OPT_WATERSHED_IMPL, ws)
+    ctx.set_option(rtg.OPT_WATERSHED_IMPL, 1 if ws == 1 else 0)
+    ctx.set_option(rtg.OPT_HMAX_IMPL, 1 if ws == 2 else 0)  # ws 2: tiled with IWPP HMAX
     try:
         mask, labels, _, feats, n = ctx.process_tile(rgb)
     finally:
@@ -192,6 +193,7 @@ def test_pipeline_impl_options(rtg, ctx, ref2048, impl, graphs, recon, ws):
         ctx.set_option(rtg.OPT_USE_GRAPHS, 1)
         ctx.set_option(rtg.OPT_RECON_IMPL, 0)
         ctx.set_option(rtg.OPT_WATERSHED_IMPL, 0)
+        ctx.set_option(rtg.OPT_HMAX_IMPL, 0)
     assert n == ref["n"]
     assert np.array_equal(mask, ref["mask"])
     assert np.array_equal(labels, ref["labels"])
@@ -261,8 +263,10 @@ def test_edt(ctx, oracle, case):
 # ---------------------------------------------------------------- o6/o7
 
 @pytest.mark.parametrize("ws_h", [0, 3, 8])
-@pytest.mark.parametrize("impl", [0, 1])
-def test_watershed(rtg, ctx, oracle, ws_h, impl):
+@pytest.mark.parametrize("impl,hmax", [(0, 0), (0, 1), (1, 0)])
+def test_watershed(rtg, ctx, oracle, ws_h, impl, hmax):
+    """Tiled watershed with sparse-component HMAX (default) or IWPP HMAX, and
+    the object-parallel watershed, against the oracle."""
     rng = np.random.default_rng(ws_h + 100)
     h, w = 1024, 1280
     m = _rand_blobs(rng, h, w, 0.35, 2.5)
@@ -270,10 +274,12 @@ def test_watershed(rtg, ctx, oracle, ws_h, impl):
     sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
     basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
     ctx.set_option(rtg.OPT_WATERSHED_IMPL, impl)
+    ctx.set_option(rtg.OPT_HMAX_IMPL, hmax)
     try:
         ctx.watershed_dev(_np_dev(m), h, w, ws_h, sep, basin)
     finally:
         ctx.set_option(rtg.OPT_WATERSHED_IMPL, 0)
+        ctx.set_option(rtg.OPT_HMAX_IMPL, 0)
     assert np.array_equal(_dev_np(basin), basin_ref)
     assert np.array_equal(_dev_np(sep), sep_ref)
 
