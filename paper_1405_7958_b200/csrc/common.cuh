@@ -191,6 +191,66 @@ __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, in
   return v < 0 ? -1 : roots[v];
 }
 
+// Block-wide reservation of `cnt` consecutive slots per thread from a global
+// counter with ONE atomic per block (same-address global atomics serialise
+// at about one per clock, so per-warp appends of a whole-tile pass cost tens
+// of microseconds).  Every thread of the block must call it; sm holds
+// (blockDim.x / 32 + 1) ints.  Returns the thread's first slot.
+__device__ __forceinline__ int32_t block_reserve(int32_t cnt, int32_t* counter, int32_t* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) sm[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t tot = 0;
+    for (int k = 0; k < nw; ++k) {
+      const int32_t t = sm[k];
+      sm[k] = tot;
+      tot += t;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0;
+  }
+  __syncthreads();
+  const int32_t r = sm[nw] + sm[wid] + incl - cnt;
+  __syncthreads();
+  return r;
+}
+
+// Same for (a, b) pairs packed in one u64 counter (hi: a, lo: b); the block's
+// sums must stay below 2^32.  Returns the packed first slots.
+__device__ __forceinline__ unsigned long long block_reserve2(uint32_t a, uint32_t b,
+                                                             unsigned long long* counter,
+                                                             unsigned long long* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned long long v = ((unsigned long long)a << 32) | b;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) sm[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int k = 0; k < nw; ++k) {
+      const unsigned long long t = sm[k];
+      sm[k] = tot;
+      tot += t;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long r = sm[nw] + sm[wid] + incl - v;
+  __syncthreads();
+  return r;
+}
+
 // Global union-find over an i32 parent plane.  Every link points to a smaller
 // index and the root is the component minimum, so path halving by atomicMin
 // never passes the root and never disconnects a node; concurrent unions only

@@ -3,7 +3,8 @@
 // Lotufo union-find: "a forest in which each pixel is a tree ... merges
 // adjacent trees ... flattening the trees").
 //
-// 1. k_ccl_tile    one warp per 32x32 tile, no block barriers.  The tile's
+// 1. k_ccl_tile    one warp per 32x32 tile (the block only meets to reserve
+//                  list slots with one global atomic).  The tile's
 //                  rows become 32 ballot bit masks; then each lane owns one
 //                  ROW and works on runs with bit arithmetic: a run is one
 //                  union-find node (its start), unions are issued once per
@@ -117,8 +118,10 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   __shared__ int32_t s_par[kTileWarps][1024];
   __shared__ uint32_t s_inf[kTileWarps][1024];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kTileWarps + wid;
-  if (tile >= ntiles) return;  // warp-uniform; the kernel has no block barrier
+  const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
+  // a surplus warp of the last block repeats the last tile read-only (it
+  // publishes and writes nothing) so every warp reaches the block barrier
+  const bool active = blockIdx.x * kTileWarps + wid < ntiles;
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   int32_t* par = s_par[wid];
   uint32_t* inf = s_inf[wid];
@@ -192,17 +195,11 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
     if (add & kSeedBit) atomicOr(&inf[par[rb + b]], kSeedBit);
     atomicAdd(&inf[par[rb + b]], add & ~kSeedBit);
   }
-  // publish the local roots (one global atomic per warp)
-  int incl = nroot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
-  }
-  int base = 0;
-  if (lane == 31 && incl) base = atomicAdd(lcount, incl);
-  base = __shfl_sync(kFull, base, 31) + incl - nroot;
+  // publish the local roots (one global atomic per block)
+  __shared__ int32_t s_res[kTileWarps + 1];
   __syncwarp();
+  int base = block_reserve(active ? nroot : 0, lcount, s_res);
+  if (!active) return;
   for (uint32_t m = starts; m; m &= m - 1) {
     const int b = __ffs(m) - 1;
     if (par[rb + b] != rb + b) continue;

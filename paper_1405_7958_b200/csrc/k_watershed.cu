@@ -68,13 +68,14 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw, uint8_t* __restrict__
   }
   __syncthreads();
   const int c = tid & 31;
-  for (int r = tid >> 5; r < 32; r += 8) {
+  int32_t mine[4];
+  int nmine = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = (tid >> 5) + 8 * q;
     const int y = y0 + r, x = x0 + c;
-    bool flat = false;
-    int32_t i32 = 0;
     if (y < h && x < w) {
       const int64_t i = (int64_t)y * w + x;
-      i32 = (int32_t)i;
       const uint32_t f = sf[r + 2][c + 2];
       rm[i] = 0;
       if (f) {
@@ -92,27 +93,25 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw, uint8_t* __restrict__
           p = (int32_t)(i + arg);
           par[i] = -1;
         } else {
-          flat = true;
 #pragma unroll
           for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
             for (int dx = -1; dx <= 1; ++dx)
               if (p == -2 && sf[r + 2 + dy][c + 2 + dx] == f && shi[r + 1 + dy][c + 1 + dx])
                 p = (int32_t)(i + dy * w + dx);
-          par[i] = i32;
+          par[i] = (int32_t)i;
           cnt[i] = 0;
+          mine[nmine++] = (int32_t)i;
         }
         ptr[i] = p;
       }
     }
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, flat);
-    if (b) {
-      int base = 0;
-      if (c == 0) base = atomicAdd(flat_count, __popc(b));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      if (flat) flat_list[base + __popc(b & ((1u << c) - 1u))] = i32;
-    }
   }
+  __shared__ int32_t sm[9];
+  int32_t base = block_reserve(nmine, flat_count, sm);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < nmine) flat_list[base + q] = mine[q];
 }
 
 // Plateau components: union with the backward same-level flat neighbours
@@ -157,26 +156,33 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
 // Unseeded components are the markers (rm = 1, ptr = self; the root is the
 // marker label).  Each seeded root reserves its members' range and enters the
 // component list.  alloc = {member cursor, component count} as one u64.
-__global__ void k_ws_classify(const int32_t* __restrict__ flat_list,
-                              const int32_t* __restrict__ flat_count,
-                              const int32_t* __restrict__ par, int32_t* cnt,
-                              int32_t* __restrict__ ptr, uint8_t* __restrict__ rm,
-                              unsigned long long* alloc, int32_t* __restrict__ comp_root,
-                              int32_t* __restrict__ comp_size) {
+__global__ void __launch_bounds__(256)
+k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
+              const int32_t* __restrict__ par, int32_t* cnt, int32_t* __restrict__ ptr,
+              uint8_t* __restrict__ rm, unsigned long long* alloc,
+              int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+  __shared__ unsigned long long sm[9];
   const int n = *flat_count;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = flat_list[k];
-    const int32_t r = __ldcg(par + i);
-    const int32_t v = __ldcg(cnt + r);
-    if (!(v & kSeeded)) {
-      rm[i] = 1;
-      ptr[i] = i;
-    } else if (r == i) {
-      const int32_t sz = v & kCountMask;
-      const unsigned long long old = atomicAdd(alloc, (1ull << 32) | (unsigned long long)sz);
-      const int32_t base = (int32_t)(old & 0xFFFFFFFFull), c = (int32_t)(old >> 32);
-      __stcg(cnt + r, kSeeded | base);  // members still read the flag: it stays set
-      comp_root[c] = r;
+  for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    int32_t root = -1, sz = 0;
+    if (k < n) {
+      const int32_t i = flat_list[k];
+      const int32_t r = __ldcg(par + i);
+      const int32_t v = __ldcg(cnt + r);
+      if (!(v & kSeeded)) {
+        rm[i] = 1;
+        ptr[i] = i;
+      } else if (r == i) {
+        root = i;
+        sz = v & kCountMask;
+      }
+    }
+    const unsigned long long slot = block_reserve2(root >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
+    if (root >= 0) {
+      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull), c = (int32_t)(slot >> 32);
+      __stcg(cnt + root, kSeeded | base);  // members still read the flag: it stays set
+      comp_root[c] = root;
       comp_size[c] = sz;
     }
   }
@@ -337,15 +343,17 @@ k_hmax_init(int h, int w, const uint16_t* __restrict__ dq, int32_t ws_h,
   }
   __syncthreads();
   const int c = tid & 31;
-  for (int r = tid >> 5; r < 32; r += 8) {
+  int32_t mine[4];
+  int nmine = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = (tid >> 5) + 8 * q;
     const int y = y0 + r, x = x0 + c;
-    bool sus = false;
-    int32_t i32 = 0;
     if (y < h && x < w) {
       const int64_t i = (int64_t)y * w + x;
-      i32 = (int32_t)i;
       const int32_t v = sd[r + 1][c + 1];
       uint32_t fw = 0;
+      bool sus = false;
       if (v) {
         int32_t mx = 0;
 #pragma unroll
@@ -357,21 +365,20 @@ k_hmax_init(int h, int w, const uint16_t* __restrict__ dq, int32_t ws_h,
         } else {
           sus = true;
           fw = (uint32_t)(v > ws_h ? v - ws_h : 0) + 1u;
-          par[i] = i32;
+          par[i] = (int32_t)i;
           cnt[i] = 0;
+          mine[nmine++] = (int32_t)i;
         }
       }
       Fw[i] = (uint16_t)fw;
       sflag[i] = sus;
     }
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, sus);
-    if (b) {
-      int base = 0;
-      if (c == 0) base = atomicAdd(count, __popc(b));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      if (sus) list[base + __popc(b & ((1u << c) - 1u))] = i32;
-    }
   }
+  __shared__ int32_t sm[9];
+  int32_t base = block_reserve(nmine, count, sm);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < nmine) list[base + q] = mine[q];
 }
 
 __global__ void k_hmax_union(int h, int w, const uint8_t* __restrict__ sflag,
@@ -394,20 +401,27 @@ __global__ void k_hmax_union(int h, int w, const uint8_t* __restrict__ sflag,
 
 // Every component root reserves its members' range (cnt[r] := kSeeded | base,
 // the form k_ws_scatter reads) and enters the component list.
-__global__ void k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-                             const int32_t* __restrict__ par, int32_t* cnt,
-                             unsigned long long* alloc, int32_t* __restrict__ comp_root,
-                             int32_t* __restrict__ comp_size) {
+__global__ void __launch_bounds__(256)
+k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+             const int32_t* __restrict__ par, int32_t* cnt, unsigned long long* alloc,
+             int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+  __shared__ unsigned long long sm[9];
   const int n = *count;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = list[k];
-    if (__ldcg(par + i) != i) continue;
-    const int32_t sz = __ldcg(cnt + i) & kCountMask;
-    const unsigned long long old = atomicAdd(alloc, (1ull << 32) | (unsigned long long)sz);
-    const int32_t base = (int32_t)(old & 0xFFFFFFFFull), c = (int32_t)(old >> 32);
-    cnt[i] = kSeeded | base;
-    comp_root[c] = i;
-    comp_size[c] = sz;
+  for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    int32_t i = -1, sz = 0;
+    if (k < n) {
+      i = list[k];
+      if (__ldcg(par + i) == i) sz = __ldcg(cnt + i) & kCountMask;
+      else i = -1;
+    }
+    const unsigned long long slot = block_reserve2(i >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
+    if (i >= 0) {
+      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull), c = (int32_t)(slot >> 32);
+      cnt[i] = kSeeded | base;
+      comp_root[c] = i;
+      comp_size[c] = sz;
+    }
   }
 }
 

@@ -20,7 +20,7 @@ STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("fill_holes", "k_ccl_tile", "k_seeded_and"),
     ("area", "k_ccl_tile", "k_fill_uf_final"),
     ("edt", "k_edt_seg", None),
-    ("markers", "k_tiles_init", None),
+    ("markers", "k_hmax_init", None),
     ("watershed", "k_ws_arrows", None),
     ("label", "k_ccl_tile", "k_ws_separate"),
     ("features", "k_feat_clear", None),
