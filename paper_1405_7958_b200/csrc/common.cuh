@@ -298,8 +298,9 @@ int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
 int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
         int32_t* dist2, uint16_t* dq, uint16_t* mk, int32_t ws_h);
 
+// basin doubles as i32 scratch; the ids are only written when want_basin.
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int32_t ws_h, uint8_t* sep, int32_t* basin);
+              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin = true);
 // Object-parallel o6+o7 (default): objects are the global roots of `roots`
 // (a ccl_roots forest of `mask`) whose counts lie in [lo, hi] (all roots when
 // counts == nullptr).  Writes sep (and basin if non-null) for the whole tile.

@@ -52,27 +52,54 @@ k_ws_arrows(int h, int w, const uint16_t* __restrict__ Fw, uint8_t* __restrict__
   __shared__ uint8_t shi[34][36];
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int tid = threadIdx.x;
-  for (int k = tid; k < 36 * 36; k += 256) {
-    const int yy = k / 36, xx = k - yy * 36;
-    const int y = y0 - 2 + yy, x = x0 - 2 + xx;
-    sf[yy][xx] = (y >= 0 && y < h && x >= 0 && x < w) ? Fw[(int64_t)y * w + x] : (uint16_t)0;
+  const int lane = tid & 31, wr = tid >> 5;
+  // stage rows of 32 (+4) contiguous values per warp: no index division
+  {
+    // all loads first (independent, in flight together), then the stores
+    uint16_t va[5], vb[5];
+    const int x = x0 - 2 + lane, x2 = x0 + 30 + lane;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int yy = wr + 8 * j, y = y0 - 2 + yy;
+      const bool yin = yy < 36 && y >= 0 && y < h;
+      const int64_t rb = (int64_t)y * w;
+      va[j] = (yin && x >= 0 && x < w) ? __ldg(Fw + rb + x) : (uint16_t)0;
+      vb[j] = (yin && lane < 4 && x2 < w) ? __ldg(Fw + rb + x2) : (uint16_t)0;
+    }
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int yy = wr + 8 * j;
+      if (yy < 36) {
+        sf[yy][lane] = va[j];
+        if (lane < 4) sf[yy][32 + lane] = vb[j];
+      }
+    }
   }
   __syncthreads();
-  for (int k = tid; k < 34 * 34; k += 256) {
-    const int yy = k / 34 + 1, xx = k - (k / 34) * 34 + 1;
+  // "has a higher neighbour" for the tile and its 1-pixel ring (foreground
+  // only: background never matches a foreground level)
+  auto hi_at = [&](int yy, int xx) -> uint8_t {
     const uint32_t f = sf[yy][xx];
-    const bool hi = sf[yy - 1][xx - 1] > f || sf[yy - 1][xx] > f || sf[yy - 1][xx + 1] > f ||
-                    sf[yy][xx - 1] > f || sf[yy][xx + 1] > f || sf[yy + 1][xx - 1] > f ||
-                    sf[yy + 1][xx] > f || sf[yy + 1][xx + 1] > f;
-    shi[yy - 1][xx - 1] = hi;
+    if (!f) return 0;
+    return sf[yy - 1][xx - 1] > f || sf[yy - 1][xx] > f || sf[yy - 1][xx + 1] > f ||
+           sf[yy][xx - 1] > f || sf[yy][xx + 1] > f || sf[yy + 1][xx - 1] > f ||
+           sf[yy + 1][xx] > f || sf[yy + 1][xx + 1] > f;
+  };
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const int yy = 1 + wr + 8 * j;
+    if (yy <= 34) {
+      shi[yy - 1][lane] = hi_at(yy, lane + 1);
+      if (lane < 2) shi[yy - 1][32 + lane] = hi_at(yy, 33 + lane);
+    }
   }
   __syncthreads();
-  const int c = tid & 31;
+  const int c = lane;
   int32_t mine[4];
   int nmine = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int r = (tid >> 5) + 8 * q;
+    const int r = wr + 8 * q;
     const int y = y0 + r, x = x0 + c;
     if (y < h && x < w) {
       const int64_t i = (int64_t)y * w + x;
@@ -336,10 +363,26 @@ k_hmax_init(int h, int w, const uint16_t* __restrict__ dq, int32_t ws_h,
   __shared__ uint16_t sd[34][36];
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int tid = threadIdx.x;
-  for (int k = tid; k < 34 * 34; k += 256) {
-    const int yy = k / 34, xx = k - yy * 34;
-    const int y = y0 - 1 + yy, x = x0 - 1 + xx;
-    sd[yy][xx] = (y >= 0 && y < h && x >= 0 && x < w) ? dq[(int64_t)y * w + x] : (uint16_t)0;
+  {
+    const int lane = tid & 31, wr = tid >> 5;
+    uint16_t va[5], vb[5];
+    const int x = x0 - 1 + lane, x2 = x0 + 31 + lane;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int yy = wr + 8 * j, y = y0 - 1 + yy;
+      const bool yin = yy < 34 && y >= 0 && y < h;
+      const int64_t rb = (int64_t)y * w;
+      va[j] = (yin && x >= 0 && x < w) ? __ldg(dq + rb + x) : (uint16_t)0;
+      vb[j] = (yin && lane < 2 && x2 < w) ? __ldg(dq + rb + x2) : (uint16_t)0;
+    }
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int yy = wr + 8 * j;
+      if (yy < 34) {
+        sd[yy][lane] = va[j];
+        if (lane < 2) sd[yy][32 + lane] = vb[j];
+      }
+    }
   }
   __syncthreads();
   const int c = tid & 31;
@@ -530,43 +573,49 @@ k_hmax_solve(int h, int w, const uint16_t* __restrict__ dq, const uint8_t* __res
   }
 }
 
-__global__ void k_ws_resolve(int64_t n, const uint8_t* __restrict__ mask,
-                             const int32_t* __restrict__ ptr,
-                             const int32_t* __restrict__ par,
-                             int32_t* __restrict__ basin) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t b = 0;
-    if (mask[i]) {
-      int32_t q = (int32_t)i;
-      int32_t nx = ptr[q];
-      while (nx >= 0 && nx != q) {
-        q = nx;
-        nx = ptr[q];
-      }
-      b = nx == q ? par[q] + 1 : 0;
+// Basins + separation in one tiled pass: every pixel of the tile and its
+// 1-pixel ring follows its arrows to the marker (basin = 1 + marker root),
+// kept in shared memory; a pixel survives the separation unless an
+// 8-neighbour has a higher basin id.  basin (optional) receives the ids.
+__global__ void __launch_bounds__(256)
+k_ws_basins(int h, int w, const uint8_t* __restrict__ mask, const int32_t* __restrict__ ptr,
+            const int32_t* __restrict__ par, int32_t* __restrict__ basin,
+            uint8_t* __restrict__ sep) {
+  __shared__ int32_t sb[34][35];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, wr = threadIdx.x >> 5;
+  auto resolve = [&](int y, int x) -> int32_t {
+    if (y < 0 || y >= h || x < 0 || x >= w) return 0;
+    int32_t q = y * w + x;
+    if (!mask[q]) return 0;
+    int32_t nx = ptr[q];
+    while (nx >= 0 && nx != q) {
+      q = nx;
+      nx = ptr[q];
     }
-    basin[i] = b;
+    return nx == q ? par[q] + 1 : 0;
+  };
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const int yy = wr + 8 * j;
+    if (yy < 34) {
+      sb[yy][lane] = resolve(y0 - 1 + yy, x0 - 1 + lane);
+      if (lane < 2) sb[yy][32 + lane] = resolve(y0 - 1 + yy, x0 + 31 + lane);
+    }
   }
-}
-
-__global__ void k_ws_separate(int h, int w, const int32_t* __restrict__ basin,
-                              uint8_t* __restrict__ sep) {
-  for (int y = blockIdx.y; y < h; y += gridDim.y)
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < w; x += gridDim.x * blockDim.x) {
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = wr + 8 * q;
+    const int y = y0 + r, x = x0 + lane;
+    if (y >= h || x >= w) continue;
+    const int32_t b = sb[r + 1][lane + 1];
+    const bool keep = b > 0 && sb[r][lane] <= b && sb[r][lane + 1] <= b && sb[r][lane + 2] <= b &&
+                      sb[r + 1][lane] <= b && sb[r + 1][lane + 2] <= b &&
+                      sb[r + 2][lane] <= b && sb[r + 2][lane + 1] <= b && sb[r + 2][lane + 2] <= b;
     const int64_t i = (int64_t)y * w + x;
-    const int32_t b = basin[i];
-    uint8_t keep = b > 0;
-    if (keep) {
-      for (int dy = -1; dy <= 1 && keep; ++dy) {
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int yy = y + dy, xx = x + dx;
-          if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-          if (basin[(int64_t)yy * w + xx] > b) { keep = 0; break; }
-        }
-      }
-    }
     sep[i] = keep;
+    if (basin) basin[i] = b;
   }
 }
 
@@ -579,7 +628,7 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 }  // namespace
 
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int32_t ws_h, uint8_t* sep, int32_t* basin) {
+              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin) {
   const int64_t n = h * w;
   uint16_t* dq = ctx->u16a;
   uint16_t* F = ctx->u16b;
@@ -649,11 +698,9 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                                                           ctx->lroots, comp_root, comp_size,
                                                           alloc, ptr, delta);
   RTG_LAUNCH("k_ws_plateau");
-  k_ws_resolve<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, ptr, par, basin);
-  RTG_LAUNCH("k_ws_resolve");
-  const dim3 grid2d((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
-  k_ws_separate<<<grid2d, 256, 0, ctx->stream>>>((int)h, (int)w, basin, sep);
-  RTG_LAUNCH("k_ws_separate");
+  k_ws_basins<<<tiles, 256, 0, ctx->stream>>>((int)h, (int)w, mask, ptr, par,
+                                              want_basin ? basin : nullptr, sep);
+  RTG_LAUNCH("k_ws_basins");
   return RTG_OK;
 }
 
