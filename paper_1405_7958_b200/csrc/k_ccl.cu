@@ -76,14 +76,27 @@ __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
 }
 
 // ---- foreground predicates ----------------------------------------------------
+// eval: one pixel; eval4: four consecutive pixels packed in a u32 (byte k =
+// pixel x + k), returning 4-bit masks.
+__device__ __forceinline__ uint32_t byte_msbs(uint32_t v) {  // bit 7 of each byte -> nibble
+  return ((v >> 7) & 1u) | ((v >> 14) & 2u) | ((v >> 21) & 4u) | ((v >> 28) & 8u);
+}
+__device__ __forceinline__ uint32_t border_nib(int y, int x, int h, int w) {
+  if (y == 0 || y == h - 1) return 0xFu;
+  return (x == 0 ? 1u : 0u) | (x + 3 == w - 1 ? 8u : 0u);
+}
 struct FgMask {  // mask != 0
   static constexpr bool kSeed = false;
   const uint8_t* m;
   __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool&) const {
     fg = m[i] != 0;
   }
+  __device__ __forceinline__ void eval4(uint32_t v, int, int, uint32_t& fg, uint32_t&) const {
+    fg = byte_msbs(~__vcmpeq4(v, 0u));
+  }
+  __device__ __forceinline__ const uint8_t* plane() const { return m; }
 };
-struct FgThresh {  // v >= t; seed: v >= ts
+struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
   static constexpr bool kSeed = true;
   const uint8_t* v;
   int32_t t, ts;
@@ -92,6 +105,11 @@ struct FgThresh {  // v >= t; seed: v >= ts
     fg = a >= t;
     sd = a >= ts;
   }
+  __device__ __forceinline__ void eval4(uint32_t a, int, int, uint32_t& fg, uint32_t& sd) const {
+    fg = t > 255 ? 0u : byte_msbs(__vcmpgeu4(a, 0x01010101u * (uint32_t)t));
+    sd = ts > 255 ? 0u : byte_msbs(__vcmpgeu4(a, 0x01010101u * (uint32_t)ts));
+  }
+  __device__ __forceinline__ const uint8_t* plane() const { return v; }
 };
 struct FgBackground {  // m == 0; seed: on the image border
   static constexpr bool kSeed = true;
@@ -101,6 +119,12 @@ struct FgBackground {  // m == 0; seed: on the image border
     fg = m[i] == 0;
     sd = y == 0 || x == 0 || y == h - 1 || x == w - 1;
   }
+  __device__ __forceinline__ void eval4(uint32_t v, int y, int x, uint32_t& fg,
+                                        uint32_t& sd) const {
+    fg = byte_msbs(__vcmpeq4(v, 0u));
+    sd = border_nib(y, x, h, w);
+  }
+  __device__ __forceinline__ const uint8_t* plane() const { return m; }
 };
 
 constexpr int kTileWarps = 4;
@@ -110,13 +134,16 @@ constexpr uint32_t kSeedBit = 0x80000000u;
 // lowest run of ones of v (bit 0 of v set)
 __device__ __forceinline__ uint32_t low_run(uint32_t v) { return v & ~(v + 1u); }
 
+// Runs are named compactly: run k of tile row r is node r * 16 + k (a 32-pixel
+// row holds at most 16 runs), so the per-warp forest is 512 entries.
 template <int CONN, class P>
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ roots,
            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount,
            int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b) {
-  __shared__ int32_t s_par[kTileWarps][1024];
-  __shared__ uint32_t s_inf[kTileWarps][1024];
+  __shared__ int32_t s_par[kTileWarps][512];
+  __shared__ uint32_t s_inf[kTileWarps][512];
+  __shared__ uint8_t s_pos[kTileWarps][512];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
   // a surplus warp of the last block repeats the last tile read-only (it
@@ -125,34 +152,71 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   int32_t* par = s_par[wid];
   uint32_t* inf = s_inf[wid];
-  // 1. lane = column: rows as ballot masks (lane r keeps row r)
+  uint8_t* pos = s_pos[wid];
+  // 1. row bit masks; lane r keeps row r
   uint32_t bits = 0, seeds = 0;
   const int x = x0 + lane;
+  if ((w & 3) == 0 && x0 + 32 <= w && (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0) {
+    // 4 pixels per load: lane covers row 4k + lane/8, columns 4 (lane % 8) ..
+    // + 3; the 8 lanes of a row OR their nibbles together
+    const uint8_t* pl = pred.plane();
+    const int g = lane >> 3, cq = (lane & 7) * 4;
+    uint32_t word[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int y = y0 + 4 * k + g;
+      word[k] = y < h ? __ldg(reinterpret_cast<const uint32_t*>(pl + (int64_t)y * w + x0 + cq))
+                      : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int y = y0 + 4 * k + g;
+      uint32_t fn = 0, sn = 0;
+      if (y < h) pred.eval4(word[k], y, x0 + cq, fn, sn);
+      uint32_t m = fn << cq, ms = (fn & sn) << cq;
+      m |= __shfl_xor_sync(kFull, m, 1);
+      m |= __shfl_xor_sync(kFull, m, 2);
+      m |= __shfl_xor_sync(kFull, m, 4);
+      const uint32_t t = __shfl_sync(kFull, m, (lane & 3) * 8);
+      if ((lane >> 2) == k) bits = t;
+      if (P::kSeed) {
+        ms |= __shfl_xor_sync(kFull, ms, 1);
+        ms |= __shfl_xor_sync(kFull, ms, 2);
+        ms |= __shfl_xor_sync(kFull, ms, 4);
+        const uint32_t ts = __shfl_sync(kFull, ms, (lane & 3) * 8);
+        if ((lane >> 2) == k) seeds = ts;
+      }
+    }
+  } else {
 #pragma unroll 8
-  for (int r = 0; r < 32; ++r) {
-    const int y = y0 + r;
-    bool fg = false, sd = false;
-    if (y < h && x < w) pred.eval((int64_t)y * w + x, y, x, fg, sd);
-    const uint32_t b = __ballot_sync(kFull, fg);
-    if (lane == r) bits = b;
-    if (P::kSeed) {
-      const uint32_t sb = __ballot_sync(kFull, fg && sd);
-      if (lane == r) seeds = sb;
+    for (int r = 0; r < 32; ++r) {
+      const int y = y0 + r;
+      bool fg = false, sd = false;
+      if (y < h && x < w) pred.eval((int64_t)y * w + x, y, x, fg, sd);
+      const uint32_t b = __ballot_sync(kFull, fg);
+      if (lane == r) bits = b;
+      if (P::kSeed) {
+        const uint32_t sb = __ballot_sync(kFull, fg && sd);
+        if (lane == r) seeds = sb;
+      }
     }
   }
-  // 2. lane = row: runs are nodes (named by their start), one union per pair
-  //    of overlapping runs of adjacent rows
-  const int rb = lane * 32;
+  // 2. lane = row: one union per pair of overlapping runs of adjacent rows
+  const int rb = lane * 16;
   const uint32_t starts = bits & ~(bits << 1);
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    par[rb + b] = rb + b;
+  {
+    int k = 0;
+    for (uint32_t m = starts; m; m &= m - 1, ++k) {
+      par[rb + k] = rb + k;
+      pos[rb + k] = (uint8_t)(__ffs(m) - 1);
+    }
   }
   const uint32_t up = __shfl_up_sync(kFull, bits, 1);
   __syncwarp();
   if (lane > 0 && up) {
     const uint32_t upstarts = up & ~(up << 1);
-    for (uint32_t m = starts; m; m &= m - 1) {
+    int k = 0;
+    for (uint32_t m = starts; m; m &= m - 1, ++k) {
       const int b = __ffs(m) - 1;
       const uint32_t run = low_run(bits >> b) << b;
       uint32_t ov = up & (CONN == 8 ? (run | (run << 1) | (run >> 1)) : run);
@@ -160,7 +224,8 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
         const int t = __ffs(ov) - 1;
         const uint32_t below = upstarts & (t == 31 ? kFull : ((2u << t) - 1u));
         const int su = 31 - __clz(below);
-        unite_s(par, rb + b, rb - 32 + su);
+        const int ku = __popc(upstarts & ((1u << su) - 1u));
+        unite_s(par, rb + k, rb - 16 + ku);
         ov &= ~(low_run(up >> su) << su);
       }
     }
@@ -168,44 +233,39 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   __syncwarp();
   // 3. flatten the run forest (read-only finds, then own-entry writes), then
   //    accumulate pixel counts / seed bits at the local roots
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    inf[rb + b] = (uint32_t)find_root(par, rb + b);
-  }
+  const int nruns = __popc(starts);
+  for (int k = 0; k < nruns; ++k) inf[rb + k] = (uint32_t)find_root(par, rb + k);
   __syncwarp();
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    par[rb + b] = (int32_t)inf[rb + b];
-  }
+  for (int k = 0; k < nruns; ++k) par[rb + k] = (int32_t)inf[rb + k];
   __syncwarp();
   int nroot = 0;
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    if (par[rb + b] == rb + b) {
-      inf[rb + b] = 0;
+  for (int k = 0; k < nruns; ++k) {
+    if (par[rb + k] == rb + k) {
+      inf[rb + k] = 0;
       ++nroot;
     }
   }
   __syncwarp();
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    const uint32_t run = low_run(bits >> b) << b;
-    uint32_t add = (uint32_t)__popc(run);
-    if (P::kSeed && (seeds & run)) add |= kSeedBit;
-    if (add & kSeedBit) atomicOr(&inf[par[rb + b]], kSeedBit);
-    atomicAdd(&inf[par[rb + b]], add & ~kSeedBit);
+  {
+    int k = 0;
+    for (uint32_t m = starts; m; m &= m - 1, ++k) {
+      const int b = __ffs(m) - 1;
+      const uint32_t run = low_run(bits >> b) << b;
+      const int32_t root = par[rb + k];
+      if (P::kSeed && (seeds & run)) atomicOr(&inf[root], kSeedBit);
+      atomicAdd(&inf[root], (uint32_t)__popc(run));
+    }
   }
   // publish the local roots (one global atomic per block)
   __shared__ int32_t s_res[kTileWarps + 1];
   __syncwarp();
   int base = block_reserve(active ? nroot : 0, lcount, s_res);
   if (!active) return;
-  for (uint32_t m = starts; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    if (par[rb + b] != rb + b) continue;
-    const int32_t g = (y0 + lane) * w + x0 + b;
+  for (int k = 0; k < nruns; ++k) {
+    if (par[rb + k] != rb + k) continue;
+    const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
     lroots[2 * base] = g;
-    lroots[2 * base + 1] = (int32_t)inf[rb + b];
+    lroots[2 * base + 1] = (int32_t)inf[rb + k];
     ++base;
     if (zero_a) zero_a[g] = 0;
     if (zero_b) zero_b[g] = 0;
@@ -221,8 +281,9 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
       if ((b >> lane) & 1u) {
         const uint32_t zeros = ~b & upto;
         const int start = zeros ? 32 - __clz(zeros) : 0;
-        const int32_t lr = par[r * 32 + start];
-        out = (y0 + (lr >> 5)) * w + x0 + (lr & 31);
+        const uint32_t st = b & ~(b << 1);
+        const int32_t lr = par[r * 16 + __popc(st & ((1u << start) - 1u))];
+        out = (y0 + (lr >> 4)) * w + x0 + pos[lr];
       }
       roots[(int64_t)y * w + x] = out;
     }
