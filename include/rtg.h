@@ -141,6 +141,8 @@ int rtg_ctx_sync(rtg_ctx* ctx);
  * for tests / profiling; synchronises:
  *   out[0] objects of the last tile, out[1] IWPP tile visits (all kinds),
  *   out[2] watershed plateau pixels of the last tile,
+ *   out[3] 1 if the last EDT needed the whole-tile exact pass (a distance
+ *   beyond the windowed EDT's exact range), else 0,
  *   out[4 + 2k] tile visits and out[5 + 2k] sweep iterations of IWPP kind k
  *   (k = 0 ReconToNuclei, 1 HMAX, 2 regional maxima, 3 IWPP fill-holes). */
 #define RTG_NUM_STATS 16

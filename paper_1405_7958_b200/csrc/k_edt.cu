@@ -1,6 +1,18 @@
 // o6 distance map for PreWatershed: exact squared
-// Euclidean distance transform, separable.
+// Euclidean distance transform.
 //
+// Fast path, k_edt_tile: one CTA per 64x64 output tile reads the mask of the
+// tile plus a 16-pixel halo (a 96x96 window).  Columns of the window become
+// 96-bit masks of background rows, the vertical distance g of every (tile
+// row, window column) comes from one ffs / clz on them, and every foreground
+// pixel searches outward along its row, stopping as soon as k^2 >= best.  The
+// window holds every point within Chebyshev distance 16 of a tile pixel, so
+// any result <= 16^2 is exact; a larger one raises a flag and the separable
+// whole-tile pass below recomputes everything (it early-exits otherwise).
+// Nuclei after the area filter have distances far below 16, so the fallback
+// costs four empty launches in the normal case.
+//
+// Whole-tile pass (fallback, and the semantics the fast path reproduces):
 // Column phase: the tile is cut into 32-row segments; k_edt_seg summarises
 // each (column, segment) by its first/last zero row, k_edt_col resolves the
 // nearest zero above/below through the summaries and emits the 1-D column
@@ -19,11 +31,16 @@ namespace rtg {
 namespace {
 
 constexpr int kSeg = 32;
+constexpr int kET = 64;               // fast path: output tile edge
+constexpr int kER = 16;               //   halo; exact while d2 <= kER^2
+constexpr int kEW = kET + 2 * kER;    //   window edge (96 = 3 words)
 constexpr uint32_t kInfG = 0xFFFFu;
 constexpr int kCap = 96;
 
 __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
-                          uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero) {
+                          uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero,
+                          const int32_t* __restrict__ gate) {
+  if (gate && !*gate) return;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
   bool z = false;
@@ -43,7 +60,9 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
 }
 
 __global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
-                          const uint16_t* __restrict__ seg, uint16_t* __restrict__ g) {
+                          const uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
+                          const int32_t* __restrict__ gate) {
+  if (gate && !*gate) return;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
   if (x >= w) return;
@@ -101,8 +120,12 @@ __global__ void __launch_bounds__(256)
 k_edt_row(const uint16_t* __restrict__ g, int h, int w,
           const int32_t* __restrict__ any_zero, int32_t* __restrict__ dist2,
           uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
-          int32_t* __restrict__ row_flag) {
+          int32_t* __restrict__ row_flag, const int32_t* __restrict__ gate) {
   extern __shared__ uint16_t gs[];
+  if (gate && !*gate) {
+    if (threadIdx.x == 0) row_flag[blockIdx.x] = 0;
+    return;
+  }
   const int y = blockIdx.x;
   const int64_t rb = (int64_t)y * w;
   for (int x = threadIdx.x; x < w; x += blockDim.x) gs[x] = g[rb + x];
@@ -189,6 +212,120 @@ __global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
   }
 }
 
+__device__ __forceinline__ uint32_t isqrt_small(uint32_t v) {  // v < 2^24
+  uint32_t r = (uint32_t)__fsqrt_rn((float)v);
+  if (r * r > v) --r;
+  if ((r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+__global__ void __launch_bounds__(256)
+k_edt_tile(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__ dist2,
+           uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
+           int32_t* __restrict__ need_full) {
+  __shared__ uint32_t colw[kEW][3];       // bit r of word k: window row 32k + r is background
+  __shared__ uint8_t gdn[kET][kEW + 4];   // tile row -> nearest background row below / above
+  __shared__ uint8_t gup[kET][kEW + 4];   //   (255: none in the window)
+  const int x0 = blockIdx.x * kET, y0 = blockIdx.y * kET;
+  const int wx0 = x0 - kER, wy0 = y0 - kER;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // 1. background bits of the window: a task is (4-column group, 32-row word),
+  //    32 independent u32 loads when the rows are 4-byte aligned and inside
+  const bool vec = (w & 3) == 0 && wx0 >= 0 && wx0 + kEW <= w &&
+                   (reinterpret_cast<uintptr_t>(mask) & 3) == 0;
+  if (vec) {
+    if (tid < (kEW / 4) * 3) {
+      const int k = tid / (kEW / 4), cg = tid - k * (kEW / 4);
+      uint32_t v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int y = wy0 + 32 * k + r;
+        v[r] = (y >= 0 && y < h)
+                   ? __ldg(reinterpret_cast<const uint32_t*>(mask + (int64_t)y * w + wx0 + 4 * cg))
+                   : 0x01010101u;  // outside the image: not background
+      }
+      uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const uint32_t z = __vcmpeq4(v[r], 0u);  // 0xFF per background byte
+        b0 |= ((z >> 7) & 1u) << r;
+        b1 |= ((z >> 15) & 1u) << r;
+        b2 |= ((z >> 23) & 1u) << r;
+        b3 |= ((z >> 31) & 1u) << r;
+      }
+      colw[4 * cg + 0][k] = b0;
+      colw[4 * cg + 1][k] = b1;
+      colw[4 * cg + 2][k] = b2;
+      colw[4 * cg + 3][k] = b3;
+    }
+  } else {
+    for (int t = tid; t < kEW * 3; t += 256) {
+      const int k = t / kEW, c = t - k * kEW;
+      const int x = wx0 + c;
+      uint32_t bits = 0;
+      if (x >= 0 && x < w) {
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+          const int y = wy0 + 32 * k + r;
+          if (y >= 0 && y < h && !__ldg(mask + (int64_t)y * w + x)) bits |= 1u << r;
+        }
+      }
+      colw[c][k] = bits;
+    }
+  }
+  __syncthreads();
+  // 2. vertical distances: one thread sweeps one window column downwards
+  //    (threads 0..95) or upwards (96..191); bits stay in registers
+  if (tid < 2 * kEW) {
+    const int c = tid < kEW ? tid : tid - kEW;
+    const uint32_t cw[3] = {colw[c][0], colw[c][1], colw[c][2]};
+    if (tid < kEW) {
+      int last = -1000;
+#pragma unroll
+      for (int r = 0; r < kER + kET; ++r) {
+        if ((cw[r >> 5] >> (r & 31)) & 1u) last = r;
+        if (r >= kER) gdn[r - kER][c] = (uint8_t)min(r - last, 255);
+      }
+    } else {
+      int next = 1000;
+#pragma unroll
+      for (int r = kEW - 1; r >= kER; --r) {
+        if ((cw[r >> 5] >> (r & 31)) & 1u) next = r;
+        if (r < kER + kET) gup[r - kER][c] = (uint8_t)min(next - r, 255);
+      }
+    }
+  }
+  __syncthreads();
+  // 3. row search for the tile pixels
+  bool far = false;
+#pragma unroll 2
+  for (int q = 0; q < 16; ++q) {
+    const int r = wid * 8 + (q >> 1), c = (q & 1) * 32 + lane;
+    const int y = y0 + r, x = x0 + c;
+    if (y >= h || x >= w) continue;
+    const int wc = c + kER;
+    const uint32_t g0 = min(gdn[r][wc], gup[r][wc]);
+    uint32_t best;
+    if (g0 == 0) {
+      best = 0;
+    } else {
+      best = g0 == 255 ? 0xFFFFFFFFu : g0 * g0;
+      for (uint32_t k = 1; k <= (uint32_t)kER && k * k < best; ++k) {
+        const uint32_t gm = min(min(gdn[r][wc - k], gup[r][wc - k]),
+                                min(gdn[r][wc + k], gup[r][wc + k]));
+        if (gm != 255) best = min(best, k * k + gm * gm);
+      }
+      if (best > (uint32_t)(kER * kER)) far = true;
+    }
+    const int64_t i = (int64_t)y * w + x;
+    if (dist2) dist2[i] = (int32_t)min(best, 0x7FFFFFFFu);
+    const uint32_t v = best > (uint32_t)(kER * kER) ? 65534u : isqrt_small(16u * best);
+    if (dq) dq[i] = (uint16_t)v;
+    if (mk) mk[i] = (uint16_t)(v > (uint32_t)ws_h ? v - (uint32_t)ws_h : 0u);
+  }
+  if (__syncthreads_or(far) && tid == 0) *need_full = 1;
+}
+
 }  // namespace
 
 int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
@@ -197,16 +334,22 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   uint16_t* seg = reinterpret_cast<uint16_t*>(ctx->seg_summary);
   uint16_t* g = ctx->u16c;
   int32_t* any_zero = ctx->misc + 2;
+  int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;  // h entries
-  RTG_CUDA(cudaMemsetAsync(any_zero, 0, sizeof(int32_t), ctx->stream));
+  RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));  // + need_full
+  const dim3 tiles((unsigned)ceil_div(w, kET), (unsigned)ceil_div(h, kET));
+  k_edt_tile<<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, dist2, dq, mk, ws_h,
+                                             need_full);
+  RTG_LAUNCH("k_edt_tile");
+  // exact whole-tile pass, gated on need_full (empty launches otherwise)
   const dim3 gs((unsigned)ceil_div(w, 128), (unsigned)nseg);
-  k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero);
+  k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
   RTG_LAUNCH("k_edt_seg");
-  k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g);
+  k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
   k_edt_row<<<(unsigned)h, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, dist2,
-                                                      dq, mk, ws_h, row_flag);
+                                                      dq, mk, ws_h, row_flag, need_full);
   RTG_LAUNCH("k_edt_row");
   k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
       g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, dist2, dq, mk, ws_h, ctx->status);

@@ -414,7 +414,7 @@ int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[RTG_NUM_STATS]) {
   out[0] = misc[0];
   out[1] = st[4] + st[6] + st[8] + st[10];
   out[2] = misc[1];
-  out[3] = 0;
+  out[3] = misc[3];
   return RTG_OK;
 }
 
