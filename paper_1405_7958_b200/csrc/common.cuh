@@ -108,6 +108,8 @@ struct rtg_ctx {
   int32_t* flat_list = nullptr;    // watershed plateau pixel list
   int32_t* lroots = nullptr;       // CCL tile-local roots: (root, count | seed bit) pairs
   uint32_t* root_bm = nullptr;     // CCL global-root bitmap (max_px / 32 words)
+  int32_t* fg_list = nullptr;      // watershed foreground pixel list (max_px)
+  uint32_t* fg_bits = nullptr;     //   and 1-bit plane (+ pad words)
   int32_t* root_wprefix = nullptr; //   and its per-word exclusive prefix
   int32_t* obj_root = nullptr;     // object-parallel watershed: object roots
   int32_t* obj_box = nullptr;      //   and bounding boxes (4 per object)
@@ -299,6 +301,14 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
         int32_t* dist2, uint16_t* dq, uint16_t* mk, int32_t ws_h);
 
 // basin doubles as i32 scratch; the ids are only written when want_basin.
+// Sparse path: list of the mask's foreground indices + 1-bit plane (bits_base
+// has 2 pad words before the plane), and the EDT of the listed pixels only
+// (dq of background pixels is not written; a gated whole-tile pass takes over
+// when some distance exceeds the windowed search).
+int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
+            int32_t* count, uint32_t* bits_base);
+int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int32_t* list,
+             const int32_t* count, const uint32_t* bits_base, uint16_t* dq);
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
               int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin = true);
 // Object-parallel o6+o7 (default): objects are the global roots of `roots`

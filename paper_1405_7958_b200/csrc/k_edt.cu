@@ -326,6 +326,94 @@ k_edt_tile(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__
   if (__syncthreads_or(far) && tid == 0) *need_full = 1;
 }
 
+// ---- foreground list + bit plane (sparse path of the watershed) ----------------
+// bits: one bit per pixel (raster order, 1 = foreground), with kBitPad zero
+// words before and after so 64-bit windows never leave the allocation.  The
+// list holds every foreground index, in raster order within a block.
+// Each thread covers 16 consecutive pixels (one 16-byte load when aligned), so
+// a block reserves list slots once per 4096 pixels.
+__global__ void __launch_bounds__(256)
+k_fg_list(const uint8_t* __restrict__ mask, int64_t n, uint32_t* __restrict__ bits,
+          int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  __shared__ int32_t sm[9];
+  const bool vec = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
+  for (int64_t b0 = (int64_t)blockIdx.x * 4096; b0 < n; b0 += (int64_t)gridDim.x * 4096) {
+    const int64_t p0 = b0 + 16 * (int64_t)threadIdx.x;
+    uint32_t m = 0;  // bit k: pixel p0 + k is foreground
+    if (vec && p0 + 16 <= n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + p0));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t z = ~__vcmpeq4(wv[q], 0u);  // 0xFF per foreground byte
+        m |= (((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u)) << (4 * q);
+      }
+    } else {
+      for (int k = 0; k < 16; ++k)
+        if (p0 + k < n && mask[p0 + k]) m |= 1u << k;
+    }
+    // 32-pixel words: even lane = low half, odd lane = high half
+    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, m, 1);
+    if (!(threadIdx.x & 1) && p0 < n) bits[p0 >> 5] = m | (other << 16);
+    int32_t slot = block_reserve(__popc(m), count, sm);
+    for (uint32_t r = m; r; r &= r - 1) list[slot++] = (int32_t)(p0 + __ffs(r) - 1);
+  }
+}
+
+// Distance from column x to the nearest background pixel of the row starting
+// at bit `rb`, within +-32 columns; 255 if none.
+__device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ bits, int64_t rb,
+                                                   int x, int w) {
+  const int64_t c = rb + x;
+  const int64_t wa = c >> 5, wb = (c - 32) >> 5;
+  const uint32_t sa = (uint32_t)(c & 31), sb = (uint32_t)((c - 32) & 31);
+  const uint32_t hi = __funnelshift_r(bits[wa], bits[wa + 1], sa);   // columns x .. x+31
+  const uint32_t lo = __funnelshift_r(bits[wb], bits[wb + 1], sb);   // columns x-32 .. x-1
+  const int right_valid = w - x;   // columns x .. w-1
+  const uint32_t mh = right_valid >= 32 ? 0xFFFFFFFFu : ((1u << right_valid) - 1u);
+  const uint32_t ml = x >= 32 ? 0xFFFFFFFFu : ~((1u << (32 - x)) - 1u);
+  const uint32_t bh = ~hi & mh, bl = ~lo & ml;
+  const uint32_t dr = bh ? (uint32_t)(__ffs(bh) - 1) : 255u;
+  const uint32_t dl = bl ? (uint32_t)(__clz(bl) + 1) : 255u;
+  return min(dr, dl);
+}
+
+// Exact EDT of every listed foreground pixel: rows y +- dy are scanned
+// outwards until dy^2 >= best; each row contributes its nearest background
+// pixel within +-32 columns (bit arithmetic on the bit plane).  Exact while
+// the result is <= 32^2 (every background pixel within Chebyshev distance 32
+// is seen); beyond that need_full is raised and the whole-tile pass runs.
+__global__ void __launch_bounds__(256)
+k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+           const uint32_t* __restrict__ bits, int h, int w, int32_t* __restrict__ dist2,
+           uint16_t* __restrict__ dq, int32_t* __restrict__ need_full) {
+  constexpr uint32_t kR = 32;
+  const int n = *count;
+  bool far = false;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t p = list[k];
+    const int y = p / w, x = p - y * w;
+    uint32_t best = 0xFFFFFFFFu;
+    {
+      const uint32_t d0 = row_nearest_bg(bits, (int64_t)y * w, x, w);
+      if (d0 != 255u) best = d0 * d0;
+    }
+    for (uint32_t dy = 1; dy <= kR && dy * dy < best; ++dy) {
+      uint32_t dm = 255u;
+      if (y >= (int)dy) dm = row_nearest_bg(bits, (int64_t)(y - (int)dy) * w, x, w);
+      if (y + (int)dy < h) dm = min(dm, row_nearest_bg(bits, (int64_t)(y + (int)dy) * w, x, w));
+      if (dm != 255u) best = min(best, dy * dy + dm * dm);
+    }
+    if (best > kR * kR) {
+      far = true;
+      continue;
+    }
+    if (dist2) dist2[p] = (int32_t)best;
+    dq[p] = (uint16_t)isqrt_small(16u * best);
+  }
+  if (__any_sync(0xFFFFFFFFu, far) && (threadIdx.x & 31) == 0) *need_full = 1;
+}
+
 }  // namespace
 
 int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
@@ -353,6 +441,54 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_edt_row");
   k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
       g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, dist2, dq, mk, ws_h, ctx->status);
+  RTG_LAUNCH("k_edt_row_exact");
+  return RTG_OK;
+}
+
+}  // namespace rtg
+
+namespace rtg {
+
+constexpr int kBitPad = 2;
+
+int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
+            int32_t* count, uint32_t* bits_base) {
+  const int64_t n = h * w;
+  RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
+  // zero pads (the words past the image end are partly written by the ballots)
+  RTG_CUDA(cudaMemsetAsync(bits_base, 0, sizeof(uint32_t) * kBitPad, ctx->stream));
+  RTG_CUDA(cudaMemsetAsync(bits_base + kBitPad + n / 32, 0, sizeof(uint32_t) * (kBitPad + 1),
+                           ctx->stream));
+  int blocks = (int)ceil_div(n, 4096);
+  if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
+  k_fg_list<<<blocks, 256, 0, ctx->stream>>>(mask, n, bits_base + kBitPad, list, count);
+  RTG_LAUNCH("k_fg_list");
+  return RTG_OK;
+}
+
+int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int32_t* list,
+             const int32_t* count, const uint32_t* bits_base, uint16_t* dq) {
+  const int nseg = (int)ceil_div(h, kSeg);
+  uint16_t* seg = reinterpret_cast<uint16_t*>(ctx->seg_summary);
+  uint16_t* g = ctx->u16c;
+  int32_t* any_zero = ctx->misc + 2;
+  int32_t* need_full = ctx->misc + 3;
+  int32_t* row_flag = ctx->misc + 64;
+  RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));
+  k_edt_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, bits_base + kBitPad, (int)h,
+                                                        (int)w, nullptr, dq, need_full);
+  RTG_LAUNCH("k_edt_list");
+  const dim3 gs((unsigned)ceil_div(w, 128), (unsigned)nseg);
+  k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
+  RTG_LAUNCH("k_edt_seg");
+  k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
+  RTG_LAUNCH("k_edt_col");
+  const size_t smem = sizeof(uint16_t) * (size_t)w;
+  k_edt_row<<<(unsigned)h, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, nullptr, dq,
+                                                      nullptr, 0, row_flag, need_full);
+  RTG_LAUNCH("k_edt_row");
+  k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
+      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, nullptr, dq, nullptr, 0, ctx->status);
   RTG_LAUNCH("k_edt_row_exact");
   return RTG_OK;
 }

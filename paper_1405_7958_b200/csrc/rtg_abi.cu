@@ -316,6 +316,8 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->lroots, n));
         RTG_TRY(dalloc(&c->root_bm, n / 32 + 1));
         RTG_TRY(dalloc(&c->root_wprefix, n / 32 + 1));
+        RTG_TRY(dalloc(&c->fg_list, n));
+        RTG_TRY(dalloc(&c->fg_bits, n / 32 + 8));
         c->obj_cap = (int64_t)n / 4 + 16;  // 8-connected objects are >= 1 px, <= 1 per 2x2
         RTG_TRY(dalloc(&c->obj_root, (size_t)c->obj_cap));
         RTG_TRY(dalloc(&c->obj_box, 4 * (size_t)c->obj_cap));
@@ -352,7 +354,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
                   c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
-                  c->root_bm, c->root_wprefix,
+                  c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
                   c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs};
