@@ -318,8 +318,10 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
                       const int32_t* counts, int32_t lo, int32_t hi, int64_t h, int64_t w,
                       int32_t ws_h, uint8_t* sep, int32_t* basin);
 
+// list (optional): a foreground list covering every labelled pixel.
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
-             int64_t h, int64_t w, const int32_t* d_n, float* out);
+             int64_t h, int64_t w, const int32_t* d_n, float* out,
+             const int32_t* list = nullptr, const int32_t* list_count = nullptr);
 
 int synth_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row,
               int64_t tile_col, int64_t h, int64_t w, uint8_t* d_rgb);

@@ -231,6 +231,88 @@ k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
   }
 }
 
+// Step 1 over a foreground list (the sparse path: a superset of the labelled
+// pixels, raster-ordered within blocks).  A warp takes 32 consecutive list
+// entries; lanes of equal label are grouped with __match_any_sync, every
+// field is reduced with redux.sync and one leader per group issues the global
+// atomics — consecutive foreground pixels mostly share an object, so that is
+// about one group per warp.
+__global__ void __launch_bounds__(256)
+k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+            const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, int w,
+            const int32_t* __restrict__ d_n, FeatureAcc acc) {
+  const unsigned full = 0xFFFFFFFFu;
+  const int nobj = min(*d_n, acc.cap);
+  const int n = *count;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = acc.cap;
+  for (int k0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; k0 < n;
+       k0 += gridDim.x * blockDim.x) {
+    const int k = k0 + lane;
+    int32_t p = 0, l = 0;
+    if (k < n) {
+      p = list[k];
+      l = labels[p];
+    }
+    const bool on = l > 0 && l <= nobj;
+    const unsigned act = __ballot_sync(full, on);
+    if (!on) continue;
+    const int y = p / w, x = p - y * w;
+    const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
+    const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
+    const uint8_t* rm = I + (int64_t)ym * w;
+    const uint8_t* r0 = I + (int64_t)y * w;
+    const uint8_t* rp = I + (int64_t)yp * w;
+    const int gx = ((int)rm[xp] + 2 * (int)r0[xp] + (int)rp[xp]) -
+                   ((int)rm[xm] + 2 * (int)r0[xm] + (int)rp[xm]);
+    const int gy = ((int)rp[xm] + 2 * (int)rp[x] + (int)rp[xp]) -
+                   ((int)rm[xm] + 2 * (int)rm[x] + (int)rm[xp]);
+    const uint32_t gq = isqrt_small(16u * (uint32_t)(gx * gx + gy * gy));
+    const uint32_t v = r0[x];
+    const uint32_t per = (y == 0 || labels[p - w] != l) + (y == h - 1 || labels[p + w] != l) +
+                         (x == 0 || labels[p - 1] != l) + (x == w - 1 || labels[p + 1] != l);
+    const unsigned grp = __match_any_sync(act, l);
+    const uint32_t uy = (uint32_t)y, ux = (uint32_t)x;
+    // u32 partial sums of up to 32 pixels: y^2, x^2, x*y < 2^24 * 32 fits
+    const uint32_t s_y = __reduce_add_sync(grp, uy);
+    const uint32_t s_x = __reduce_add_sync(grp, ux);
+    const uint32_t s_yy = __reduce_add_sync(grp, uy * uy);
+    const uint32_t s_xx = __reduce_add_sync(grp, ux * ux);
+    const uint32_t s_xy = __reduce_add_sync(grp, ux * uy);
+    const uint32_t s_i = __reduce_add_sync(grp, v);
+    const uint32_t s_ii = __reduce_add_sync(grp, v * v);
+    const uint32_t s_g = __reduce_add_sync(grp, gq);
+    const uint32_t s_gg = __reduce_add_sync(grp, gq * gq);
+    const uint32_t s_p = __reduce_add_sync(grp, per);
+    const uint32_t mn_i = __reduce_min_sync(grp, v);
+    const uint32_t mx_i = __reduce_max_sync(grp, v);
+    const uint32_t mn_y = __reduce_min_sync(grp, uy);
+    const uint32_t mx_y = __reduce_max_sync(grp, uy);
+    const uint32_t mn_x = __reduce_min_sync(grp, ux);
+    const uint32_t mx_x = __reduce_max_sync(grp, ux);
+    if (lane != __ffs(grp) - 1) continue;
+    const int64_t o = l - 1;
+    unsigned long long* S = acc.sums;
+    atomicAdd(&S[kSumArea * c + o], (unsigned long long)__popc(grp));
+    atomicAdd(&S[kSumY * c + o], (unsigned long long)s_y);
+    atomicAdd(&S[kSumX * c + o], (unsigned long long)s_x);
+    atomicAdd(&S[kSumYY * c + o], (unsigned long long)s_yy);
+    atomicAdd(&S[kSumXX * c + o], (unsigned long long)s_xx);
+    atomicAdd(&S[kSumXY * c + o], (unsigned long long)s_xy);
+    atomicAdd(&S[kSumI * c + o], (unsigned long long)s_i);
+    atomicAdd(&S[kSumII * c + o], (unsigned long long)s_ii);
+    atomicAdd(&S[kSumG * c + o], (unsigned long long)s_g);
+    atomicAdd(&S[kSumGG * c + o], (unsigned long long)s_gg);
+    atomicAdd(&S[kSumPerim * c + o], (unsigned long long)s_p);
+    atomicMin(&acc.mins[kMinI * c + o], (int32_t)mn_i);
+    atomicMin(&acc.mins[kMinY * c + o], (int32_t)mn_y);
+    atomicMin(&acc.mins[kMinX * c + o], (int32_t)mn_x);
+    atomicMax(&acc.maxs[kMaxI * c + o], (int32_t)mx_i);
+    atomicMax(&acc.maxs[kMaxY * c + o], (int32_t)mx_y);
+    atomicMax(&acc.maxs[kMaxX * c + o], (int32_t)mx_x);
+  }
+}
+
 // Step 2: one thread per object.  Expression order mirrors the oracle
 // (oracle/rtg_oracle.c orc_features) term by term.
 __global__ void k_feat_finalize(const int32_t* __restrict__ d_n, FeatureAcc acc,
@@ -293,14 +375,23 @@ __global__ void k_feat_finalize(const int32_t* __restrict__ d_n, FeatureAcc acc,
 }  // namespace
 
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
-             int64_t h, int64_t w, const int32_t* d_n, float* out) {
+             int64_t h, int64_t w, const int32_t* d_n, float* out, const int32_t* list,
+             const int32_t* list_count) {
   const int cap = ctx->acc.cap;
   const int gclear = (int)ceil_div(cap, 256);
   k_feat_clear<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc);
   RTG_LAUNCH("k_feat_clear");
-  const dim3 grid((unsigned)ceil_div(w, kFB), (unsigned)ceil_div(h, kFB));
-  k_feat_accum<<<grid, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n, ctx->acc);
-  RTG_LAUNCH("k_feat_accum");
+  // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
+  if (list && h <= 4096 && w <= 4096) {
+    k_feat_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, list_count, labels, intensity,
+                                                           (int)h, (int)w, d_n, ctx->acc);
+    RTG_LAUNCH("k_feat_list");
+  } else {
+    const dim3 grid((unsigned)ceil_div(w, kFB), (unsigned)ceil_div(h, kFB));
+    k_feat_accum<<<grid, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n,
+                                                ctx->acc);
+    RTG_LAUNCH("k_feat_accum");
+  }
   k_feat_finalize<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc, out, ctx->status);
   RTG_LAUNCH("k_feat_finalize");
   return RTG_OK;

@@ -137,7 +137,11 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o9 features
   if (with_features) {
     prof_mark(ctx, RTG_STAGE_FEATURES);
-    RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features));
+    // the tiled watershed left the foreground list of the area mask (a
+    // superset of the labelled pixels)
+    const bool sparse = ctx->ws_impl == 0;
+    RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features, sparse ? ctx->fg_list : nullptr,
+                     sparse ? ctx->misc + 4 : nullptr));
   }
   prof_mark(ctx, -1);
   return RTG_OK;
