@@ -233,10 +233,10 @@ k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
 
 // Step 1 over a foreground list (the sparse path: a superset of the labelled
 // pixels, raster-ordered within blocks).  A warp takes 32 consecutive list
-// entries; lanes of equal label are grouped with __match_any_sync, every
-// field is reduced with redux.sync and one leader per group issues the global
-// atomics — consecutive foreground pixels mostly share an object, so that is
-// about one group per warp.
+// entries; consecutive lanes of one label on one row form a run, reduced with
+// a segmented shuffle reduction (runs are contiguous in lane order, so no
+// match/collective loops); the run head issues one set of global atomics.
+// y is constant along a run, so the y moments follow from n and sum x.
 __global__ void __launch_bounds__(256)
 k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, int w,
@@ -254,62 +254,82 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
       p = list[k];
       l = labels[p];
     }
-    const bool on = l > 0 && l <= nobj;
-    const unsigned act = __ballot_sync(full, on);
-    if (!on) continue;
+    if (!(l > 0 && l <= nobj)) l = 0;
+    if (!__any_sync(full, l != 0)) continue;
     const int y = p / w, x = p - y * w;
-    const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
-    const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
-    const uint8_t* rm = I + (int64_t)ym * w;
-    const uint8_t* r0 = I + (int64_t)y * w;
-    const uint8_t* rp = I + (int64_t)yp * w;
-    const int gx = ((int)rm[xp] + 2 * (int)r0[xp] + (int)rp[xp]) -
-                   ((int)rm[xm] + 2 * (int)r0[xm] + (int)rp[xm]);
-    const int gy = ((int)rp[xm] + 2 * (int)rp[x] + (int)rp[xp]) -
-                   ((int)rm[xm] + 2 * (int)rm[x] + (int)rm[xp]);
-    const uint32_t gq = isqrt_small(16u * (uint32_t)(gx * gx + gy * gy));
-    const uint32_t v = r0[x];
-    const uint32_t per = (y == 0 || labels[p - w] != l) + (y == h - 1 || labels[p + w] != l) +
-                         (x == 0 || labels[p - 1] != l) + (x == w - 1 || labels[p + 1] != l);
-    const unsigned grp = __match_any_sync(act, l);
-    const uint32_t uy = (uint32_t)y, ux = (uint32_t)x;
-    // u32 partial sums of up to 32 pixels: y^2, x^2, x*y < 2^24 * 32 fits
-    const uint32_t s_y = __reduce_add_sync(grp, uy);
-    const uint32_t s_x = __reduce_add_sync(grp, ux);
-    const uint32_t s_yy = __reduce_add_sync(grp, uy * uy);
-    const uint32_t s_xx = __reduce_add_sync(grp, ux * ux);
-    const uint32_t s_xy = __reduce_add_sync(grp, ux * uy);
-    const uint32_t s_i = __reduce_add_sync(grp, v);
-    const uint32_t s_ii = __reduce_add_sync(grp, v * v);
-    const uint32_t s_g = __reduce_add_sync(grp, gq);
-    const uint32_t s_gg = __reduce_add_sync(grp, gq * gq);
-    const uint32_t s_p = __reduce_add_sync(grp, per);
-    const uint32_t mn_i = __reduce_min_sync(grp, v);
-    const uint32_t mx_i = __reduce_max_sync(grp, v);
-    const uint32_t mn_y = __reduce_min_sync(grp, uy);
-    const uint32_t mx_y = __reduce_max_sync(grp, uy);
-    const uint32_t mn_x = __reduce_min_sync(grp, ux);
-    const uint32_t mx_x = __reduce_max_sync(grp, ux);
-    if (lane != __ffs(grp) - 1) continue;
+    uint32_t v = 0, gq = 0, per = 0;
+    if (l) {
+      const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
+      const int xm = x > 0 ? x - 1 : 0, xp = x + 1 < w ? x + 1 : w - 1;
+      const uint8_t* rm = I + (int64_t)ym * w;
+      const uint8_t* r0 = I + (int64_t)y * w;
+      const uint8_t* rp = I + (int64_t)yp * w;
+      const int gx = ((int)rm[xp] + 2 * (int)r0[xp] + (int)rp[xp]) -
+                     ((int)rm[xm] + 2 * (int)r0[xm] + (int)rp[xm]);
+      const int gy = ((int)rp[xm] + 2 * (int)rp[x] + (int)rp[xp]) -
+                     ((int)rm[xm] + 2 * (int)rm[x] + (int)rm[xp]);
+      gq = isqrt_small(16u * (uint32_t)(gx * gx + gy * gy));
+      v = r0[x];
+      per = (y == 0 || labels[p - w] != l) + (y == h - 1 || labels[p + w] != l) +
+            (x == 0 || labels[p - 1] != l) + (x == w - 1 || labels[p + 1] != l);
+    }
+    // runs: a lane starts one unless its left lane has the same label and row
+    const int32_t l_prev = __shfl_up_sync(full, l, 1);
+    const int y_prev = __shfl_up_sync(full, y, 1);
+    const unsigned heads = __ballot_sync(full, lane == 0 || l != l_prev || y != y_prev);
+    // segmented reduction towards the run head: lanes (lane, lane + off] must
+    // hold no head
+    uint32_t sx = l ? (uint32_t)x : 0u, sxx = sx * sx, si = v, sii = v * v, sg = gq,
+             sgg = gq * gq, sp = per, mni = l ? v : 0xFFFFFFFFu, mxi = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t ox = __shfl_down_sync(full, sx, off);
+      const uint32_t oxx = __shfl_down_sync(full, sxx, off);
+      const uint32_t oi = __shfl_down_sync(full, si, off);
+      const uint32_t oii = __shfl_down_sync(full, sii, off);
+      const uint32_t og = __shfl_down_sync(full, sg, off);
+      const uint32_t ogg = __shfl_down_sync(full, sgg, off);
+      const uint32_t op = __shfl_down_sync(full, sp, off);
+      const uint32_t omn = __shfl_down_sync(full, mni, off);
+      const uint32_t omx = __shfl_down_sync(full, mxi, off);
+      const uint32_t span = ((heads >> 1) >> lane) & ((1u << off) - 1u);  // heads in (lane, lane+off]
+      if (lane + off < 32 && span == 0) {
+        sx += ox;
+        sxx += oxx;
+        si += oi;
+        sii += oii;
+        sg += og;
+        sgg += ogg;
+        sp += op;
+        mni = min(mni, omn);
+        mxi = max(mxi, omx);
+      }
+    }
+    // run = lanes [lane, end] for a head lane; its last pixel has the largest x
+    const unsigned after = (heads >> 1) >> lane;  // heads strictly after this lane
+    const int end = after ? lane + __ffs(after) - 1 : 31;
+    const int x_end = __shfl_sync(full, x, end);
+    if (!l || !((heads >> lane) & 1u)) continue;
     const int64_t o = l - 1;
+    const unsigned long long nn = (unsigned long long)(end - lane + 1), Y = (unsigned long long)y;
     unsigned long long* S = acc.sums;
-    atomicAdd(&S[kSumArea * c + o], (unsigned long long)__popc(grp));
-    atomicAdd(&S[kSumY * c + o], (unsigned long long)s_y);
-    atomicAdd(&S[kSumX * c + o], (unsigned long long)s_x);
-    atomicAdd(&S[kSumYY * c + o], (unsigned long long)s_yy);
-    atomicAdd(&S[kSumXX * c + o], (unsigned long long)s_xx);
-    atomicAdd(&S[kSumXY * c + o], (unsigned long long)s_xy);
-    atomicAdd(&S[kSumI * c + o], (unsigned long long)s_i);
-    atomicAdd(&S[kSumII * c + o], (unsigned long long)s_ii);
-    atomicAdd(&S[kSumG * c + o], (unsigned long long)s_g);
-    atomicAdd(&S[kSumGG * c + o], (unsigned long long)s_gg);
-    atomicAdd(&S[kSumPerim * c + o], (unsigned long long)s_p);
-    atomicMin(&acc.mins[kMinI * c + o], (int32_t)mn_i);
-    atomicMin(&acc.mins[kMinY * c + o], (int32_t)mn_y);
-    atomicMin(&acc.mins[kMinX * c + o], (int32_t)mn_x);
-    atomicMax(&acc.maxs[kMaxI * c + o], (int32_t)mx_i);
-    atomicMax(&acc.maxs[kMaxY * c + o], (int32_t)mx_y);
-    atomicMax(&acc.maxs[kMaxX * c + o], (int32_t)mx_x);
+    atomicAdd(&S[kSumArea * c + o], nn);
+    atomicAdd(&S[kSumY * c + o], nn * Y);
+    atomicAdd(&S[kSumX * c + o], (unsigned long long)sx);
+    atomicAdd(&S[kSumYY * c + o], nn * Y * Y);
+    atomicAdd(&S[kSumXX * c + o], (unsigned long long)sxx);
+    atomicAdd(&S[kSumXY * c + o], Y * sx);
+    atomicAdd(&S[kSumI * c + o], (unsigned long long)si);
+    atomicAdd(&S[kSumII * c + o], (unsigned long long)sii);
+    atomicAdd(&S[kSumG * c + o], (unsigned long long)sg);
+    atomicAdd(&S[kSumGG * c + o], (unsigned long long)sgg);
+    atomicAdd(&S[kSumPerim * c + o], (unsigned long long)sp);
+    atomicMin(&acc.mins[kMinI * c + o], (int32_t)mni);
+    atomicMin(&acc.mins[kMinY * c + o], y);
+    atomicMin(&acc.mins[kMinX * c + o], x);
+    atomicMax(&acc.maxs[kMaxI * c + o], (int32_t)mxi);
+    atomicMax(&acc.maxs[kMaxY * c + o], y);
+    atomicMax(&acc.maxs[kMaxX * c + o], x_end);
   }
 }
 
