@@ -228,6 +228,17 @@ int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                      float* features_out, int32_t max_rows,
                      int32_t* n_objects);
 
+/* Batch of tiles of one shape (the stage body applied to a bag of tiles).
+ * The upload of tile i+1 overlaps the processing of tile i (two device RGB
+ * buffers, a copy stream, events); returns when every tile is done.
+ * features_out[i] holds max_rows rows (NULL entries skip the table),
+ * n_objects[i] receives tile i's object count; RTG_ERR_OVERFLOW when a tile
+ * exceeds max_rows (its first max_rows rows are still written).  Host RGB and
+ * feature buffers from rtg_host_alloc give full copy/compute overlap. */
+int rtg_process_tiles(rtg_ctx* ctx, int32_t count, const uint8_t* const* rgb, int64_t h,
+                      int64_t w, int64_t pitch_bytes, const rtg_params* params,
+                      float* const* features_out, int32_t max_rows, int32_t* n_objects);
+
 /* ---- whole tile, device buffers (asynchronous on the ctx stream) --------- */
 
 /* d_rgb: device RGB (pitch_bytes >= 3*w).  d_mask (u8), d_labels (i32),

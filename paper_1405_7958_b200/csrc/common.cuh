@@ -85,6 +85,12 @@ struct rtg_ctx {
 
   // planes (max_px elements)
   uint8_t* rgb = nullptr;     // 3 * max_px, for host-buffer entry points
+  uint8_t* rgb2 = nullptr;    //   second buffer (rtg_process_tiles double buffering)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+  int32_t* h_counts = nullptr;  // pinned per-tile object counts (batch entry)
+  int32_t h_counts_cap = 0;
   uint8_t* hema = nullptr;
   uint8_t* recon = nullptr;   // marker in, reconstruction out
   uint8_t* tissue = nullptr;

@@ -224,6 +224,35 @@ int upload_rgb(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w, int64_t p
   return RTG_OK;
 }
 
+// Copies the first min(n, cap) feature rows (n = device object count) into
+// pinned host memory with a kernel (zero-copy stores: exactly the rows that
+// exist cross PCIe); pageable destinations get a cudaMemcpyAsync of cap rows.
+__global__ void k_rows_to_host(const float4* __restrict__ src, const int32_t* __restrict__ d_n,
+                               int32_t cap, float4* __restrict__ dst) {
+  const int64_t rows = min(*d_n, cap);
+  const int64_t n4 = rows * (RTG_NUM_FEATURES / 4);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+int rows_to_host(rtg_ctx* ctx, float* dst, int32_t cap) {
+  cudaPointerAttributes a{};
+  const cudaError_t e = cudaPointerGetAttributes(&a, dst);
+  if (e == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer &&
+      (reinterpret_cast<uintptr_t>(a.devicePointer) & 15) == 0) {
+    k_rows_to_host<<<64, 256, 0, ctx->stream>>>(reinterpret_cast<const float4*>(ctx->features),
+                                                ctx->misc, cap,
+                                                static_cast<float4*>(a.devicePointer));
+    RTG_LAUNCH("k_rows_to_host");
+    return RTG_OK;
+  }
+  cudaGetLastError();  // clear a failed attribute query on pageable memory
+  RTG_CUDA(cudaMemcpyAsync(dst, ctx->features, sizeof(float) * RTG_NUM_FEATURES * (size_t)cap,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  return RTG_OK;
+}
+
 }  // namespace
 }  // namespace rtg
 
@@ -365,6 +394,16 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_copied[b]) cudaEventDestroy(c->ev_copied[b]);
+    if (c->ev_consumed[b]) cudaEventDestroy(c->ev_consumed[b]);
+  }
+  if (c->rgb2) cudaFree(c->rgb2);
+  if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->prof_ev) {
     for (int i = 0; i < c->prof_cap; ++i) cudaEventDestroy(c->prof_ev[i]);
     delete[] c->prof_ev;
@@ -509,6 +548,81 @@ int rtg_host_free(void* p) {
 }
 
 // ---- whole tile, host buffers ------------------------------------------------
+
+int rtg_process_tiles(rtg_ctx* ctx, int32_t count, const uint8_t* const* rgb, int64_t h,
+                      int64_t w, int64_t pitch_bytes, const rtg_params* params,
+                      float* const* features_out, int32_t max_rows, int32_t* n_objects) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  RTG_TRY(check_params(params));
+  if (count < 0 || (count > 0 && (!rgb || !n_objects)))
+    return fail(RTG_ERR_INVALID_ARG, "bad tile batch");
+  if (max_rows < 0) return fail(RTG_ERR_INVALID_ARG, "max_rows < 0");
+  if (pitch_bytes < 3 * w) return fail(RTG_ERR_DIMENSION, "pitch_bytes < 3 * w");
+  for (int32_t i = 0; i < count; ++i)
+    if (!rgb[i]) return fail(RTG_ERR_INVALID_ARG, "null rgb in batch");
+  if (count == 0) return RTG_OK;
+  // lazily created double-buffering resources
+  if (!ctx->rgb2) {
+    void* p = nullptr;
+    RTG_CUDA(cudaMalloc(&p, (size_t)(3 * ctx->max_px)));
+    ctx->rgb2 = static_cast<uint8_t*>(p);
+    RTG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      RTG_CUDA(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+      RTG_CUDA(cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming));
+    }
+  }
+  if (ctx->h_counts_cap < count) {
+    if (ctx->h_counts) RTG_CUDA(cudaFreeHost(ctx->h_counts));
+    ctx->h_counts = nullptr;
+    void* p = nullptr;
+    RTG_CUDA(cudaMallocHost(&p, sizeof(int32_t) * (size_t)count));
+    ctx->h_counts = static_cast<int32_t*>(p);
+    ctx->h_counts_cap = count;
+  }
+  uint8_t* buf[2] = {ctx->rgb, ctx->rgb2};
+  const int32_t rows = max_rows < ctx->max_objects ? max_rows : ctx->max_objects;
+  // both buffers start free
+  for (int b = 0; b < 2; ++b) RTG_CUDA(cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+  for (int32_t i = 0; i < count; ++i) {
+    const int b = i & 1;
+    // upload tile i into buffer b once tile i-2 has released it
+    RTG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));
+    if (pitch_bytes == 3 * w)
+      RTG_CUDA(cudaMemcpyAsync(buf[b], rgb[i], (size_t)(3 * h * w), cudaMemcpyHostToDevice,
+                               ctx->copy_stream));
+    else
+      RTG_CUDA(cudaMemcpy2DAsync(buf[b], (size_t)(3 * w), rgb[i], (size_t)pitch_bytes,
+                                 (size_t)(3 * w), (size_t)h, cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+    RTG_CUDA(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+    RTG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+    if (ctx->use_graphs && !ctx->prof)
+      RTG_TRY(pipeline_graph(ctx, buf[b], h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                             ctx->features, ctx->misc));
+    else
+      RTG_TRY(pipeline(ctx, buf[b], h, w, 3 * w, params, ctx->m4, ctx->labels, ctx->hema,
+                       ctx->features, ctx->misc, true));
+    RTG_CUDA(cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+    RTG_CUDA(cudaMemcpyAsync(ctx->h_counts + i, ctx->misc, sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    if (features_out && features_out[i] && rows > 0)
+      RTG_TRY(rows_to_host(ctx, features_out[i], rows));
+  }
+  RTG_TRY(rtg_ctx_sync(ctx));
+  int over = -1;
+  for (int32_t i = 0; i < count; ++i) {
+    n_objects[i] = ctx->h_counts[i];
+    if (features_out && features_out[i] && (n_objects[i] > max_rows ||
+                                            n_objects[i] > ctx->max_objects) && over < 0)
+      over = i;
+  }
+  if (over >= 0)
+    return fail(RTG_ERR_OVERFLOW, "tile " + std::to_string(over) + " has " +
+                                      std::to_string(n_objects[over]) + " objects; feature rows: " +
+                                      std::to_string(rows));
+  return RTG_OK;
+}
 
 int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                      int64_t pitch_bytes, const rtg_params* params, uint8_t* mask_out,

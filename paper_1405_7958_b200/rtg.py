@@ -34,7 +34,7 @@ SYMBOLS = [
     "rtg_params_default", "rtg_device_count", "rtg_ctx_create", "rtg_ctx_destroy",
     "rtg_ctx_stream", "rtg_ctx_set_stream", "rtg_ctx_sync", "rtg_ctx_stats",
     "rtg_last_error", "rtg_host_alloc", "rtg_host_free", "rtg_segment_tile",
-    "rtg_features", "rtg_process_tile", "rtg_process_tile_dev",
+    "rtg_features", "rtg_process_tile", "rtg_process_tiles", "rtg_process_tile_dev",
     "rtg_colordeconv_dev", "rtg_recon_u8_dev", "rtg_recon_u16_dev",
     "rtg_fill_holes_dev", "rtg_bwlabel_dev", "rtg_area_threshold_dev",
     "rtg_edt_dev", "rtg_watershed_dev", "rtg_features_dev",
@@ -147,6 +147,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_segment_tile": [vp, vp, i64, i64, i64, vp, vp, vp, vp],
         "rtg_features": [vp, vp, vp, i64, i64, i32, vp],
         "rtg_process_tile": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, i32, vp],
+        "rtg_process_tiles": [vp, i32, vp, i64, i64, i64, vp, vp, i32, vp],
         "rtg_process_tile_dev": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp],
         "rtg_colordeconv_dev": [vp, vp, i64, i64, i64, vp, vp, vp, vp],
         "rtg_recon_u8_dev": [vp, vp, vp, i64, i64, ctypes.c_int, vp],
@@ -290,6 +291,26 @@ class Context:
                                         _ptr(mask), _ptr(labels), _ptr(hema), _ptr(feats),
                                         max_rows, ctypes.byref(n)))
         return mask, labels, hema, feats[: n.value].copy(), n.value
+
+    def process_tiles(self, rgbs, params: Optional[Params] = None, feats=None,
+                      max_rows: Optional[int] = None):
+        """Batch of same-shape (H, W, 3) u8 tiles through rtg_process_tiles
+        (upload of tile i+1 overlaps processing of tile i).  feats: optional
+        list of (max_rows, 20) f32 arrays (pinned ones get zero-copy rows).
+        Returns (list of feature arrays [n_i, 20], list of n_i)."""
+        params = params or default_params()
+        k = len(rgbs)
+        h, w, _ = rgbs[0].shape
+        rgbs = [np.ascontiguousarray(r) for r in rgbs]
+        max_rows = self.max_objects if max_rows is None else max_rows
+        if feats is None:
+            feats = [np.empty((max_rows, NUM_FEATURES), np.float32) for _ in range(k)]
+        rp = (ctypes.c_void_p * k)(*[r.ctypes.data for r in rgbs])
+        fp = (ctypes.c_void_p * k)(*[f.ctypes.data for f in feats])
+        ns = np.zeros(k, np.int32)
+        check(self.lib.rtg_process_tiles(self.handle, k, rp, h, w, 3 * w, ctypes.byref(params),
+                                         fp, max_rows, _ptr(ns)))
+        return [f[:n].copy() for f, n in zip(feats, ns)], [int(n) for n in ns]
 
     def segment_tile(self, rgb: np.ndarray, params: Optional[Params] = None):
         params = params or default_params()

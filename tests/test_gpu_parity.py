@@ -392,3 +392,19 @@ def test_repeatable(rtg, ctx):
             assert np.array_equal(x, y)
         else:
             assert x == y
+
+
+def test_process_tiles_batch(rtg, ctx):
+    """rtg_process_tiles (double-buffered batch) returns exactly what
+    rtg_process_tile returns per tile, with pinned (zero-copy rows) and
+    pageable feature buffers."""
+    h, w = 1024, 1536
+    rgbs = [rtg.synth_tile_host(r, 2 * r + 1, h, w) for r in range(5)]
+    ref = [ctx.process_tile(t) for t in rgbs]
+    pinned = [torch.empty((ctx.max_objects, rtg.NUM_FEATURES), dtype=torch.float32,
+                          pin_memory=True).numpy() for _ in rgbs]
+    for feats in (None, pinned):
+        got, ns = ctx.process_tiles(rgbs, feats=feats)
+        for (mask, labels, hema, f_ref, n_ref), f, n in zip(ref, got, ns):
+            assert n == n_ref
+            assert np.array_equal(f, f_ref)
