@@ -156,7 +156,10 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   // 1. row bit masks; lane r keeps row r
   uint32_t bits = 0, seeds = 0;
   const int x = x0 + lane;
-  if ((w & 3) == 0 && x0 + 32 <= w && (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0) {
+  const bool vec = (w & 3) == 0 && x0 + 32 <= w &&
+                   (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
+  if (vec) {
     // 4 pixels per load: lane covers row 4k + lane/8, columns 4 (lane % 8) ..
     // + 3; the 8 lanes of a row OR their nibbles together
     const uint8_t* pl = pred.plane();
@@ -270,22 +273,42 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
     if (zero_a) zero_a[g] = 0;
     if (zero_b) zero_b[g] = 0;
   }
-  // 4. lane = column: every pixel's local root (global index), coalesced
-  const uint32_t upto = lane == 31 ? kFull : ((2u << lane) - 1u);
-#pragma unroll 4
-  for (int r = 0; r < 32; ++r) {
-    const uint32_t b = __shfl_sync(kFull, bits, r);
-    const int y = y0 + r;
-    if (y < h && x < w) {
-      int32_t out = -1;
-      if ((b >> lane) & 1u) {
-        const uint32_t zeros = ~b & upto;
-        const int start = zeros ? 32 - __clz(zeros) : 0;
-        const uint32_t st = b & ~(b << 1);
-        const int32_t lr = par[r * 16 + __popc(st & ((1u << start) - 1u))];
-        out = (y0 + (lr >> 4)) * w + x0 + pos[lr];
+  // global index of every run's local root (inf is free again)
+  __syncwarp();
+  for (int k = 0; k < nruns; ++k) {
+    const int32_t lr = par[rb + k];
+    inf[rb + k] = (uint32_t)((y0 + (lr >> 4)) * w + x0 + pos[lr]);
+  }
+  __syncwarp();
+  // 4. every pixel's local root (global index), coalesced stores
+  if (vec) {
+    // 4 pixels per lane (one 16-byte store): 8 lanes per row, 4 rows per step
+    const int g = lane >> 3, cq = (lane & 7) * 4;
+#pragma unroll 2
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + g;
+      const uint32_t b = __shfl_sync(kFull, bits, r);
+      const int y = y0 + r;
+      if (y >= h) continue;
+      const uint32_t st = b & ~(b << 1);
+      int32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = cq + j;
+        o[j] = ((b >> c) & 1u) ? (int32_t)inf[r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : -1;
       }
-      roots[(int64_t)y * w + x] = out;
+      *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
+    }
+  } else {
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t b = __shfl_sync(kFull, bits, r);
+      const int y = y0 + r;
+      if (y < h && x < w) {
+        const uint32_t st = b & ~(b << 1);
+        roots[(int64_t)y * w + x] =
+            ((b >> lane) & 1u) ? (int32_t)inf[r * 16 + __popc(st & ((2u << lane) - 1u)) - 1] : -1;
+      }
     }
   }
 }
