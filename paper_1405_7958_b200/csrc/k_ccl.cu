@@ -17,7 +17,8 @@
 //                  global list together with their accumulators.
 //                  The foreground predicate is a functor, so thresholding /
 //                  inversion never needs its own pass over the tile.
-// 2. k_ccl_seam_*  union across tile seams in global memory (atomicMin links,
+// 2. k_ccl_seams   union across tile seams (row and column seams in one launch)
+//                  in global memory (atomicMin links,
 //                  larger root -> smaller root, path halving); a seam pair
 //                  already implied by its neighbour pair plus tile-local
 //                  connectivity is skipped, so a large component costs a few
@@ -317,9 +318,8 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
 // skipped when the same two components are already joined through the pair
 // one column to the left (same tile-local runs on both sides).
 template <int CONN>
-__global__ void k_ccl_seam_rows(int h, int w, int32_t* __restrict__ roots) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = (blockIdx.y + 1) * 32;
+__device__ __forceinline__ void seam_row_px(int h, int w, int32_t* __restrict__ roots, int y,
+                                            int x) {
   if (x >= w || y >= h) return;
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
@@ -340,9 +340,8 @@ __global__ void k_ccl_seam_rows(int h, int w, int32_t* __restrict__ roots) {
 // Seams between tile columns: pixel (y, x) with x = 32k, k >= 1 (vertically
 // adjacent pixels of one tile are always in one local component).
 template <int CONN>
-__global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  const int x = (blockIdx.y + 1) * 32;
+__device__ __forceinline__ void seam_col_px(int h, int w, int32_t* __restrict__ roots, int y,
+                                            int x) {
   if (y >= h || x >= w) return;
   const int32_t p = y * w + x;
   if (__ldcg(roots + p) < 0) return;
@@ -358,6 +357,17 @@ __global__ void k_ccl_seam_cols(int h, int w, int32_t* __restrict__ roots) {
     if (y + 1 < h && __ldcg(roots + l + w) >= 0 && !(fl && ((y + 1) & 31) != 0))
       uf_unite_g(roots, p, l + w);
   }
+}
+
+// Both seam families in one launch: blockIdx.y < tiles_y - 1 walks a row
+// seam (y = 32 (k + 1)), the rest walk column seams.
+template <int CONN>
+__global__ void k_ccl_seams(int h, int w, int row_seams, int32_t* __restrict__ roots) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)blockIdx.y < row_seams)
+    seam_row_px<CONN>(h, w, roots, ((int)blockIdx.y + 1) * 32, t);
+  else
+    seam_col_px<CONN>(h, w, roots, t, ((int)blockIdx.y - row_seams + 1) * 32);
 }
 
 // Flattens the local roots onto the global roots and folds the local
@@ -549,17 +559,11 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
     k_ccl_tile<4, P><<<grid, 32 * kTileWarps, 0, ctx->stream>>>(
         pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags);
   RTG_LAUNCH("k_ccl_tile");
-  if (tiles_y > 1) {
-    const dim3 g((unsigned)ceil_div(w, 256), (unsigned)(tiles_y - 1));
-    if (conn == 8) k_ccl_seam_rows<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    else k_ccl_seam_rows<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    RTG_LAUNCH("k_ccl_seam_rows");
-  }
-  if (tiles_x > 1) {
-    const dim3 g((unsigned)ceil_div(h, 256), (unsigned)(tiles_x - 1));
-    if (conn == 8) k_ccl_seam_cols<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    else k_ccl_seam_cols<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, roots);
-    RTG_LAUNCH("k_ccl_seam_cols");
+  if (tiles_x + tiles_y > 2) {
+    const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
+    if (conn == 8) k_ccl_seams<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, tiles_y - 1, roots);
+    else k_ccl_seams<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, tiles_y - 1, roots);
+    RTG_LAUNCH("k_ccl_seams");
   }
   k_ccl_flatten<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts,
                                                            flags, bitmap);
