@@ -299,6 +299,10 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);
+// FillHoles + 8-connected AreaThreshold of the candidates in one joint
+// labelling of foreground (8-conn) and background (4-conn) components.
+int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
+                    int32_t max_area, uint8_t* out);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
                 int32_t min_area, int32_t max_area, int32_t* counts,
                 uint8_t* out);

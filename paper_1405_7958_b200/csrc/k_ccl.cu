@@ -375,7 +375,7 @@ __global__ void k_ccl_seams(int h, int w, int row_seams, int32_t* __restrict__ r
 __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
                               const int32_t* __restrict__ lcount, int32_t* roots,
                               int32_t* __restrict__ counts, int32_t* __restrict__ flags,
-                              uint32_t* __restrict__ bitmap) {
+                              uint32_t* __restrict__ bitmap, bool seed_in_counts = false) {
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
@@ -384,6 +384,7 @@ __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
     if (g != r) atomicMin(roots + r, g);
     else if (bitmap) atomicOr(bitmap + (r >> 5), 1u << (r & 31));
     if (counts) atomicAdd(counts + g, (int32_t)(info & ~kSeedBit));
+    if (seed_in_counts && (info & kSeedBit)) atomicOr(counts + g, (int32_t)kSeedBit);
     if (flags && (info & kSeedBit)) flags[g] = 1;
   }
 }
@@ -510,6 +511,280 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
   return (int)(want < cap ? want : cap);
 }
 
+// ---- FillHoles + AreaThreshold in one labelling ------------------------------
+// The candidates' foreground (8-connected) and background (4-connected)
+// components are labelled together: every pixel belongs to exactly one
+// component.  With this (8, 4) pair, the pixel directly above a component's
+// root (its topmost-leftmost pixel) lies in the component that encloses it:
+// a foreground component's parent is a background component, a hole's parent
+// is the foreground component around it.  Background components touching
+// the image border are the outside; the others are holes.  A filled object is
+// a top-level foreground component (parent = outside) plus every component
+// nested in it, so its area is the sum over that subtree, and the output
+// mask keeps every pixel whose top-level ancestor has an area in range —
+// exactly FillHoles followed by an 8-connected AreaThreshold.
+
+template <int kW>
+struct FbSmem {
+  int32_t par[kW][1024];
+  uint32_t inf[kW][1024];
+  uint8_t pos[kW][1024];
+};
+
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntiles,
+              int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
+              int32_t* __restrict__ lcount, int32_t* __restrict__ counts) {
+  __shared__ FbSmem<kTileWarps> S;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
+  const bool active = blockIdx.x * kTileWarps + wid < ntiles;
+  const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
+  int32_t* par = S.par[wid];
+  uint32_t* inf = S.inf[wid];
+  uint8_t* pos = S.pos[wid];
+  const FgMask pred{m};
+  // 1. foreground row masks (lane r keeps row r)
+  uint32_t fgb = 0;
+  const int x = x0 + lane;
+  const bool vec = (w & 3) == 0 && x0 + 32 <= w && (reinterpret_cast<uintptr_t>(m) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
+  if (vec) {
+    const int g = lane >> 3, cq = (lane & 7) * 4;
+    uint32_t word[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int y = y0 + 4 * k + g;
+      word[k] = y < h ? __ldg(reinterpret_cast<const uint32_t*>(m + (int64_t)y * w + x0 + cq)) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t fn = 0, sn = 0;
+      pred.eval4(word[k], 0, 0, fn, sn);
+      uint32_t v = fn << cq;
+      v |= __shfl_xor_sync(kFull, v, 1);
+      v |= __shfl_xor_sync(kFull, v, 2);
+      v |= __shfl_xor_sync(kFull, v, 4);
+      const uint32_t t = __shfl_sync(kFull, v, (lane & 3) * 8);
+      if ((lane >> 2) == k) fgb = t;
+    }
+  } else {
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const int y = y0 + r;
+      const bool f = y < h && x < w && m[(int64_t)y * w + x] != 0;
+      const uint32_t b = __ballot_sync(kFull, f);
+      if (lane == r) fgb = b;
+    }
+  }
+  const int yr = y0 + lane;  // this lane's row
+  const uint32_t vcols = x0 + 32 <= w ? kFull : ((1u << (w - x0)) - 1u);
+  const uint32_t bgb = yr < h ? (~fgb & vcols) : 0u;
+  if (yr >= h) fgb = 0;
+  uint32_t seeds = 0;  // background pixels on the image border
+  if (yr < h) {
+    if (yr == 0 || yr == h - 1) seeds = bgb;
+    else seeds = bgb & ((x0 == 0 ? 1u : 0u) | (x0 + 32 >= w ? (1u << (w - 1 - x0)) : 0u));
+  }
+  // 2. runs of both kinds; unions with the row above (foreground: 8-conn,
+  //    background: 4-conn)
+  const int rb = lane * 32;
+  const uint32_t fst = fgb & ~(fgb << 1), bst = bgb & ~(bgb << 1);
+  const uint32_t allst = fst | bst;
+  {
+    int k = 0;
+    for (uint32_t q = allst; q; q &= q - 1, ++k) {
+      par[rb + k] = rb + k;
+      pos[rb + k] = (uint8_t)(__ffs(q) - 1);
+    }
+  }
+  const uint32_t upf = __shfl_up_sync(kFull, fgb, 1), upb = __shfl_up_sync(kFull, bgb, 1);
+  const uint32_t upall = (upf & ~(upf << 1)) | (upb & ~(upb << 1));
+  __syncwarp();
+  if (lane > 0 && (upf | upb)) {
+    int k = 0;
+    for (uint32_t q = allst; q; q &= q - 1, ++k) {
+      const int b = __ffs(q) - 1;
+      const bool isf = (fgb >> b) & 1u;
+      const uint32_t cur = isf ? fgb : bgb, U = isf ? upf : upb;
+      const uint32_t run = low_run(cur >> b) << b;
+      uint32_t ov = U & (isf ? (run | (run << 1) | (run >> 1)) : run);
+      const uint32_t ust = U & ~(U << 1);
+      while (ov) {
+        const int t = __ffs(ov) - 1;
+        const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
+        unite_s(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
+        ov &= ~(low_run(U >> su) << su);
+      }
+    }
+  }
+  __syncwarp();
+  // 3. flatten; per local root: pixel count + border-background bit
+  const int nruns = __popc(allst);
+  for (int k = 0; k < nruns; ++k) inf[rb + k] = (uint32_t)find_root(par, rb + k);
+  __syncwarp();
+  for (int k = 0; k < nruns; ++k) par[rb + k] = (int32_t)inf[rb + k];
+  __syncwarp();
+  int nroot = 0;
+  for (int k = 0; k < nruns; ++k)
+    if (par[rb + k] == rb + k) {
+      inf[rb + k] = 0;
+      ++nroot;
+    }
+  __syncwarp();
+  {
+    int k = 0;
+    for (uint32_t q = allst; q; q &= q - 1, ++k) {
+      const int b = __ffs(q) - 1;
+      const uint32_t run = low_run((((fgb >> b) & 1u) ? fgb : bgb) >> b) << b;
+      const int32_t root = par[rb + k];
+      if (seeds & run) atomicOr(&inf[root], kSeedBit);
+      atomicAdd(&inf[root], (uint32_t)__popc(run));
+    }
+  }
+  __shared__ int32_t s_res[kTileWarps + 1];
+  __syncwarp();
+  int base = block_reserve(active ? nroot : 0, lcount, s_res);
+  if (!active) return;
+  for (int k = 0; k < nruns; ++k) {
+    if (par[rb + k] != rb + k) continue;
+    const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
+    lroots[2 * base] = g;
+    lroots[2 * base + 1] = (int32_t)inf[rb + k];
+    ++base;
+    counts[g] = 0;
+  }
+  __syncwarp();
+  for (int k = 0; k < nruns; ++k) {
+    const int32_t lr = par[rb + k];
+    inf[rb + k] = (uint32_t)((y0 + (lr >> 5)) * w + x0 + pos[lr]);
+  }
+  __syncwarp();
+  // 4. every valid pixel's local root
+  if (vec) {
+    const int g = lane >> 3, cq = (lane & 7) * 4;
+#pragma unroll 2
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + g;
+      const int y = y0 + r;
+      const uint32_t st = __shfl_sync(kFull, allst, r);
+      if (y >= h) continue;
+      int32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[j] = (int32_t)inf[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
+      *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
+    }
+  } else {
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t st = __shfl_sync(kFull, allst, r);
+      const int y = y0 + r;
+      if (y < h && x < w)
+        roots[(int64_t)y * w + x] = (int32_t)inf[r * 32 + __popc(st & ((2u << lane) - 1u)) - 1];
+    }
+  }
+}
+
+// Seams of the joint labelling: foreground pairs 8-connected, background
+// pairs 4-connected, with the same redundancy skips as k_ccl_seams.
+__device__ __forceinline__ void seam_fb(const uint8_t* __restrict__ m, int h, int w,
+                                        int32_t* __restrict__ roots, int32_t p, int32_t q,
+                                        int32_t p2, int32_t q2, bool has_prev, int32_t qa,
+                                        bool has_qa, int32_t qb, bool has_qb, bool pref_b,
+                                        bool next_b) {
+  // p: seam pixel, q: its partner across the seam; p2/q2: the pair one step
+  // back along the seam (valid when has_prev, same tiles); qa/qb: q's
+  // neighbours one step back/forward along the seam (the 8-conn diagonals)
+  const bool fp = m[p] != 0;
+  const bool fq = m[q] != 0;
+  if (!fp) {  // background: 4-connected straight pair only
+    if (!fq && !(has_prev && !m[p2] && !m[q2])) uf_unite_g(roots, p, q);
+    return;
+  }
+  const bool in_prev = has_prev && m[p2] != 0;  // p ~ p2 (same tile, same kind)
+  const bool fqa = has_qa && m[qa] != 0;
+  if (fq && !(in_prev && fqa)) uf_unite_g(roots, p, q);
+  if (fqa && !in_prev && !(fq && pref_b)) uf_unite_g(roots, p, qa);
+  if (has_qb && m[qb] != 0 && !(fq && next_b)) uf_unite_g(roots, p, qb);
+}
+
+__global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int row_seams,
+                               int32_t* __restrict__ roots) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)blockIdx.y < row_seams) {
+    const int y = ((int)blockIdx.y + 1) * 32, x = t;
+    if (x >= w || y >= h) return;
+    const int32_t p = y * w + x, u = p - w;
+    seam_fb(m, h, w, roots, p, u, p - 1, u - 1, (x & 31) != 0, u - 1, x > 0, u + 1, x + 1 < w,
+            (x & 31) != 0, ((x + 1) & 31) != 0);
+  } else {
+    const int x = ((int)blockIdx.y - row_seams + 1) * 32, y = t;
+    if (y >= h || x >= w) return;
+    const int32_t p = y * w + x, l = p - 1;
+    seam_fb(m, h, w, roots, p, l, p - w, l - w, (y & 31) != 0, l - w, y > 0, l + w, y + 1 < h,
+            (y & 31) != 0, ((y + 1) & 31) != 0);
+  }
+}
+
+// Top-level ancestor of every global root (-1 for the outside); totals zeroed
+// at the top-level roots.
+__global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
+                          const uint8_t* __restrict__ m, int w,
+                          const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
+                          int32_t* __restrict__ top, int32_t* __restrict__ total) {
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t r = lroots[2 * k];
+    if (roots[r] != r) continue;
+    int32_t cur = r, t = -1;
+    bool fg = m[r] != 0;
+    if (fg || !(counts[r] & (int32_t)kSeedBit)) {
+      for (int guard = 0; guard < (1 << 20); ++guard) {  // nesting depth, never reached
+        if (fg) {
+          if (cur < w) { t = cur; break; }          // touches the top border
+          const int32_t b = root_of(roots, cur - w);  // enclosing background
+          if (counts[b] & (int32_t)kSeedBit) { t = cur; break; }
+          cur = b;
+          fg = false;
+        } else {
+          cur = root_of(roots, cur - w);            // enclosing foreground
+          fg = true;
+        }
+      }
+    }
+    top[r] = t;
+    if (t == r) total[r] = 0;
+  }
+}
+
+__global__ void k_fb_total(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
+                           const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
+                           const int32_t* __restrict__ top, int32_t* __restrict__ total) {
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t r = lroots[2 * k];
+    if (roots[r] != r) continue;
+    const int32_t t = top[r];
+    if (t >= 0) atomicAdd(total + t, counts[r] & ~(int32_t)kSeedBit);
+  }
+}
+
+__global__ void k_fb_filter(int64_t n, const int32_t* __restrict__ roots,
+                            const int32_t* __restrict__ top, const int32_t* __restrict__ total,
+                            int32_t lo, int32_t hi, uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = top[root_of(roots, i)];
+    uint8_t keep = 0;
+    if (t >= 0) {
+      const int32_t a = total[t];
+      keep = (uint8_t)(a >= lo && a <= hi);
+    }
+    out[i] = keep;
+  }
+}
+
 // ---- FillHoles by union-find: background components (4-conn) that touch the
 // image border (seed bit of FgBackground) are "reached"; every other
 // background pixel is a hole.
@@ -625,6 +900,40 @@ int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
   k_area_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts, min_area,
                                                          max_area, out);
   RTG_LAUNCH("k_area_filter");
+  return RTG_OK;
+}
+
+int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
+                    int32_t max_area, uint8_t* out) {
+  const int64_t n = h * w;
+  int32_t* roots = ctx->i32a;
+  int32_t* counts = ctx->i32b;
+  int32_t* top = ctx->i32c;
+  int32_t* total = ctx->labels;
+  int32_t* lcount = ctx->misc + 8;
+  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
+  const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
+  const int ntiles = tiles_x * tiles_y;
+  k_ccl_tile_fb<<<(unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, ctx->stream>>>(
+      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts);
+  RTG_LAUNCH("k_ccl_tile_fb");
+  if (tiles_x + tiles_y > 2) {
+    const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
+    k_ccl_seams_fb<<<g, 256, 0, ctx->stream>>>(cand, (int)h, (int)w, tiles_y - 1, roots);
+    RTG_LAUNCH("k_ccl_seams_fb");
+  }
+  const int gl = ctx->num_sms * 4;
+  k_ccl_flatten<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, nullptr, nullptr,
+                                             true);
+  RTG_LAUNCH("k_ccl_flatten");
+  k_fb_tree<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, cand, (int)w, roots, counts, top,
+                                         total);
+  RTG_LAUNCH("k_fb_tree");
+  k_fb_total<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, top, total);
+  RTG_LAUNCH("k_fb_total");
+  k_fb_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, top, total, min_area,
+                                                         max_area, out);
+  RTG_LAUNCH("k_fb_filter");
   return RTG_OK;
 }
 

@@ -113,13 +113,21 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
                                p->recon_conn, ctx->m1, ctx->m1));
   }
-  // o4 FillHoles of the nucleus candidates
-  prof_mark(ctx, RTG_STAGE_FILL_HOLES);
-  RTG_TRY(run_fill_holes(ctx, ctx->m1, h, w, ctx->m2));
-  // o5 AreaThreshold
-  prof_mark(ctx, RTG_STAGE_AREA);
-  RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a, ctx->i32b));
-  RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
+  if (ctx->fill_impl == 0 && ctx->ws_impl == 0) {
+    // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
+    // mask itself is never materialised)
+    prof_mark(ctx, RTG_STAGE_FILL_HOLES);
+    RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3));
+  } else {
+    // o4 FillHoles of the nucleus candidates
+    prof_mark(ctx, RTG_STAGE_FILL_HOLES);
+    RTG_TRY(run_fill_holes(ctx, ctx->m1, h, w, ctx->m2));
+    // o5 AreaThreshold (its forest + counts also feed the object-parallel
+    // watershed)
+    prof_mark(ctx, RTG_STAGE_AREA);
+    RTG_TRY(ccl_roots(ctx, ctx->m2, h, w, 8, ctx->i32a, ctx->i32b));
+    RTG_TRY(area_filter(ctx, ctx->i32a, h * w, p->min_area, p->max_area, ctx->i32b, ctx->m3));
+  }
   // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
   // watershed() marks its own EDT / MARKERS / WATERSHED stages
   if (ctx->ws_impl == 0) {

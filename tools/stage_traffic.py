@@ -17,9 +17,9 @@ import sys
 STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("colordeconv", "k_colordeconv_vec", None),
     ("recon", "k_ccl_tile", None),
-    ("fill_holes", "k_ccl_tile", "k_seeded_and"),
-    ("area", "k_ccl_tile", "k_fill_uf_final"),
-    ("edt", "k_edt_seg", None),
+    ("fill_holes", "k_ccl_tile_fb", None),
+    ("area", "k_fb_filter", None),
+    ("edt", "k_fg_list", None),
     ("markers", "k_hmax_init", None),
     ("watershed", "k_ws_arrows", None),
     ("label", "k_ccl_tile", "k_ws_separate"),
