@@ -926,6 +926,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   k_ccl_flatten<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, nullptr, nullptr,
                                              true);
   RTG_LAUNCH("k_ccl_flatten");
+  prof_mark(ctx, RTG_STAGE_AREA);  // enclosure tree, subtree areas, filter
   k_fb_tree<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, cand, (int)w, roots, counts, top,
                                          total);
   RTG_LAUNCH("k_fb_tree");

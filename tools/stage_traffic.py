@@ -18,7 +18,7 @@ STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("colordeconv", "k_colordeconv_vec", None),
     ("recon", "k_ccl_tile", None),
     ("fill_holes", "k_ccl_tile_fb", None),
-    ("area", "k_fb_filter", None),
+    ("area", "k_fb_tree", None),
     ("edt", "k_fg_list", None),
     ("markers", "k_hmax_init", None),
     ("watershed", "k_ws_arrows", None),
