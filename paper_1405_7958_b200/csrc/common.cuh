@@ -199,6 +199,23 @@ __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, in
   return v < 0 ? -1 : roots[v];
 }
 
+// Division of pixel indices by the tile width without the ~20-instruction
+// integer divide: q = (umulhi(n, m) + n) >> s with a 33-bit magic (exact for
+// every n < 2^31, d >= 1), built on the host.
+struct FastDiv {
+  uint32_t m, s, d;
+};
+inline FastDiv make_div(uint32_t d) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  const uint64_t m = ((1ull << 32) * ((1ull << s) - d)) / d + 1;
+  return FastDiv{(uint32_t)m, s, d};
+}
+__device__ __forceinline__ int32_t fdiv(int32_t n, const FastDiv& f) {
+  const uint32_t t = __umulhi((uint32_t)n, f.m);
+  return (int32_t)((t + (uint32_t)n) >> f.s);
+}
+
 // Block-wide reservation of `cnt` consecutive slots per thread from a global
 // counter with ONE atomic per block (same-address global atomics serialise
 // at about one per clock, so per-warp appends of a whole-tile pass cost tens
@@ -301,6 +318,8 @@ int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);
 // FillHoles + 8-connected AreaThreshold of the candidates in one joint
 // labelling of foreground (8-conn) and background (4-conn) components.
+// Also builds the foreground list + bit plane of `out` (ctx->fg_list,
+// misc[4], ctx->fg_bits) for the sparse watershed.
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
                     int32_t max_area, uint8_t* out);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
@@ -315,12 +334,16 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 // has 2 pad words before the plane), and the EDT of the listed pixels only
 // (dq of background pixels is not written; a gated whole-tile pass takes over
 // when some distance exceeds the windowed search).
+constexpr int kBitPad = 2;
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base);
 int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int32_t* list,
              const int32_t* count, const uint32_t* bits_base, uint16_t* dq);
+// basin doubles as i32 scratch; the ids are only written when want_basin.
+// list_ready: ctx->fg_list / misc[4] / fg_bits already describe `mask`.
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin = true);
+              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin = true,
+              bool list_ready = false);
 // Object-parallel o6+o7 (default): objects are the global roots of `roots`
 // (a ccl_roots forest of `mask`) whose counts lie in [lo, hi] (all roots when
 // counts == nullptr).  Writes sep (and basin if non-null) for the whole tile.

@@ -770,18 +770,53 @@ __global__ void k_fb_total(const int32_t* __restrict__ lroots, const int32_t* __
   }
 }
 
-__global__ void k_fb_filter(int64_t n, const int32_t* __restrict__ roots,
-                            const int32_t* __restrict__ top, const int32_t* __restrict__ total,
-                            int32_t lo, int32_t hi, uint8_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t t = top[root_of(roots, i)];
-    uint8_t keep = 0;
-    if (t >= 0) {
-      const int32_t a = total[t];
-      keep = (uint8_t)(a >= lo && a <= hi);
+// Output mask of the joint path, 4 pixels per thread (the four dependent
+// gathers per pixel want many threads in flight), plus the foreground list
+// and 1-bit plane of that mask (what k_fg_list would build).
+__global__ void __launch_bounds__(256)
+k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
+            const int32_t* __restrict__ total, int32_t lo, int32_t hi, uint8_t* __restrict__ out,
+            uint32_t* __restrict__ bits, int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  __shared__ int32_t sm[9];
+  const bool vec = (reinterpret_cast<uintptr_t>(out) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t b0 = (int64_t)blockIdx.x * 1024; b0 < n; b0 += (int64_t)gridDim.x * 1024) {
+    const int64_t p0 = b0 + 4 * (int64_t)threadIdx.x;
+    int32_t v[4];
+    if (vec && p0 + 4 <= n) {
+      const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + p0));
+      v[0] = r4.x; v[1] = r4.y; v[2] = r4.z; v[3] = r4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = p0 + k < n ? roots[p0 + k] : -1;
     }
-    out[i] = keep;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;   // global root
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? top[v[k]] : -1;     // top-level ancestor
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (v[k] >= 0) {
+        const int32_t a = total[v[k]];
+        if (a >= lo && a <= hi) m |= 1u << k;
+      }
+    }
+    if (vec && p0 + 4 <= n) {
+      *reinterpret_cast<uint32_t*>(out + p0) =
+          (m & 1u) | ((m & 2u) << 7) | ((m & 4u) << 14) | ((m & 8u) << 21);
+    } else {
+      for (int k = 0; k < 4 && p0 + k < n; ++k) out[p0 + k] = (uint8_t)((m >> k) & 1u);
+    }
+    // 32-pixel words from 8 lanes
+    uint32_t wv = m << (4 * (lane & 7));
+    wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 1);
+    wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 2);
+    wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 4);
+    if (!(lane & 7) && p0 < n) bits[p0 >> 5] = wv;
+    int32_t slot = block_reserve(__popc(m), count, sm);
+    for (uint32_t r = m; r; r &= r - 1) list[slot++] = (int32_t)(p0 + __ffs(r) - 1);
   }
 }
 
@@ -932,8 +967,15 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_LAUNCH("k_fb_tree");
   k_fb_total<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, top, total);
   RTG_LAUNCH("k_fb_total");
-  k_fb_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, top, total, min_area,
-                                                         max_area, out);
+  uint32_t* bits_base = ctx->fg_bits;
+  RTG_CUDA(cudaMemsetAsync(ctx->misc + 4, 0, sizeof(int32_t), ctx->stream));
+  RTG_CUDA(cudaMemsetAsync(bits_base, 0, sizeof(uint32_t) * kBitPad, ctx->stream));
+  RTG_CUDA(cudaMemsetAsync(bits_base + kBitPad + n / 32, 0, sizeof(uint32_t) * (kBitPad + 1),
+                           ctx->stream));
+  int blocks = (int)ceil_div(n, 1024);
+  if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
+  k_fb_filter<<<blocks, 256, 0, ctx->stream>>>(n, roots, top, total, min_area, max_area, out,
+                                               bits_base + kBitPad, ctx->fg_list, ctx->misc + 4);
   RTG_LAUNCH("k_fb_filter");
   return RTG_OK;
 }

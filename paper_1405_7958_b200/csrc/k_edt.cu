@@ -362,13 +362,13 @@ k_fg_list(const uint8_t* __restrict__ mask, int64_t n, uint32_t* __restrict__ bi
 
 // Distance from column x to the nearest background pixel of the row starting
 // at bit `rb`, within +-32 columns; 255 if none.
-__device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ bits, int64_t rb,
+__device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ bits, int32_t rb,
                                                    int x, int w) {
-  const int64_t c = rb + x;
-  const int64_t wa = c >> 5, wb = (c - 32) >> 5;
-  const uint32_t sa = (uint32_t)(c & 31), sb = (uint32_t)((c - 32) & 31);
+  const int32_t c = rb + x;
+  const int32_t wa = c >> 5, wb = (c - 32) >> 5;  // arithmetic shift: -1 for the first word
+  const uint32_t sa = (uint32_t)c & 31u;
   const uint32_t hi = __funnelshift_r(bits[wa], bits[wa + 1], sa);   // columns x .. x+31
-  const uint32_t lo = __funnelshift_r(bits[wb], bits[wb + 1], sb);   // columns x-32 .. x-1
+  const uint32_t lo = __funnelshift_r(bits[wb], bits[wb + 1], sa);   // columns x-32 .. x-1
   const int right_valid = w - x;   // columns x .. w-1
   const uint32_t mh = right_valid >= 32 ? 0xFFFFFFFFu : ((1u << right_valid) - 1u);
   const uint32_t ml = x >= 32 ? 0xFFFFFFFFu : ~((1u << (32 - x)) - 1u);
@@ -378,30 +378,47 @@ __device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ 
   return min(dr, dl);
 }
 
-// Exact EDT of every listed foreground pixel: rows y +- dy are scanned
-// outwards until dy^2 >= best; each row contributes its nearest background
-// pixel within +-32 columns (bit arithmetic on the bit plane).  Exact while
-// the result is <= 32^2 (every background pixel within Chebyshev distance 32
-// is seen); beyond that need_full is raised and the whole-tile pass runs.
+// Separable exact EDT over the foreground list.  Pass 1: every listed pixel's
+// distance to the nearest background pixel of its own row (within +-32
+// columns, 255 beyond), from two funnel-shifted words of the 1-bit plane.
+__global__ void __launch_bounds__(256)
+k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+              const uint32_t* __restrict__ bits, FastDiv dw, uint8_t* __restrict__ hd) {
+  const int w = (int)dw.d;
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t p = list[k];
+    const int y = fdiv(p, dw), x = p - y * w;
+    hd[p] = (uint8_t)row_nearest_bg(bits, y * w, x, w);
+  }
+}
+
+// Pass 2: d2 = min over rows y +- dy of dy^2 + hd^2 (background pixels have
+// hd = 0; the mask bytes tell them apart), scanned outwards until dy^2 >=
+// best.  Exact while the result is <= 32^2 (every background pixel within
+// Chebyshev distance 32 is seen); beyond that need_full is raised and the
+// whole-tile pass runs.
 __global__ void __launch_bounds__(256)
 k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-           const uint32_t* __restrict__ bits, int h, int w, int32_t* __restrict__ dist2,
-           uint16_t* __restrict__ dq, int32_t* __restrict__ need_full) {
+           const uint8_t* __restrict__ mask, const uint8_t* __restrict__ hd, int h, FastDiv dw,
+           int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
+           int32_t* __restrict__ need_full) {
   constexpr uint32_t kR = 32;
+  const int w = (int)dw.d;
   const int n = *count;
   bool far = false;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t p = list[k];
-    const int y = p / w, x = p - y * w;
-    uint32_t best = 0xFFFFFFFFu;
-    {
-      const uint32_t d0 = row_nearest_bg(bits, (int64_t)y * w, x, w);
-      if (d0 != 255u) best = d0 * d0;
-    }
+    const int y = fdiv(p, dw);
+    const uint32_t d0 = hd[p];
+    uint32_t best = d0 == 255u ? 0xFFFFFFFFu : d0 * d0;
+    int32_t up = p, dn = p;
     for (uint32_t dy = 1; dy <= kR && dy * dy < best; ++dy) {
+      up -= w;
+      dn += w;
       uint32_t dm = 255u;
-      if (y >= (int)dy) dm = row_nearest_bg(bits, (int64_t)(y - (int)dy) * w, x, w);
-      if (y + (int)dy < h) dm = min(dm, row_nearest_bg(bits, (int64_t)(y + (int)dy) * w, x, w));
+      if (y >= (int)dy) dm = mask[up] ? hd[up] : 0u;
+      if (y + (int)dy < h) dm = min(dm, mask[dn] ? (uint32_t)hd[dn] : 0u);
       if (dm != 255u) best = min(best, dy * dy + dm * dm);
     }
     if (best > kR * kR) {
@@ -449,8 +466,6 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 
 namespace rtg {
 
-constexpr int kBitPad = 2;
-
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base) {
   const int64_t n = h * w;
@@ -475,8 +490,13 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;
   RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));
-  k_edt_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, bits_base + kBitPad, (int)h,
-                                                        (int)w, nullptr, dq, need_full);
+  uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
+  const FastDiv dwv = make_div((uint32_t)w);
+  k_edt_rowdist<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, bits_base + kBitPad, dwv,
+                                                           hd);
+  RTG_LAUNCH("k_edt_rowdist");
+  k_edt_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, mask, hd, (int)h, dwv,
+                                                        nullptr, dq, need_full);
   RTG_LAUNCH("k_edt_list");
   const dim3 gs((unsigned)ceil_div(w, 128), (unsigned)nseg);
   k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);

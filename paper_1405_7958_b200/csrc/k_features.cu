@@ -239,9 +239,10 @@ k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
 // y is constant along a run, so the y moments follow from n and sum x.
 __global__ void __launch_bounds__(256)
 k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, int w,
+            const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, FastDiv dw,
             const int32_t* __restrict__ d_n, FeatureAcc acc) {
   const unsigned full = 0xFFFFFFFFu;
+  const int w = (int)dw.d;
   const int nobj = min(*d_n, acc.cap);
   const int n = *count;
   const int lane = threadIdx.x & 31;
@@ -256,7 +257,7 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
     }
     if (!(l > 0 && l <= nobj)) l = 0;
     if (!__any_sync(full, l != 0)) continue;
-    const int y = p / w, x = p - y * w;
+    const int y = fdiv(p, dw), x = p - y * w;
     uint32_t v = 0, gq = 0, per = 0;
     if (l) {
       const int ym = y > 0 ? y - 1 : 0, yp = y + 1 < h ? y + 1 : h - 1;
@@ -404,7 +405,8 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
   // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
   if (list && h <= 4096 && w <= 4096) {
     k_feat_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, list_count, labels, intensity,
-                                                           (int)h, (int)w, d_n, ctx->acc);
+                                                           (int)h, make_div((uint32_t)w), d_n,
+                                                           ctx->acc);
     RTG_LAUNCH("k_feat_list");
   } else {
     const dim3 grid((unsigned)ceil_div(w, kFB), (unsigned)ceil_div(h, kFB));

@@ -69,11 +69,12 @@ __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
 // (par = -1, flat byte 0).  Flat pixels: par = self, cnt = 0, flat byte 1,
 // appended to the flat list (their seed arrow is set by k_ws_union).
 __global__ void __launch_bounds__(256)
-k_ws_arrows(int h, int w, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const uint8_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
             int32_t* __restrict__ ptr, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
+  const int w = (int)dw.d;
   __shared__ int32_t sm[9];
   const int n = *count;
   for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
@@ -82,7 +83,7 @@ k_ws_arrows(int h, int w, const int32_t* __restrict__ list, const int32_t* __res
     int32_t p = 0;
     if (k < n) {
       p = list[k];
-      const int y = p / w, x = p - y * w;
+      const int y = fdiv(p, dw), x = p - y * w;
       const uint32_t f = Fw[p];
       uint32_t best = f;
       int32_t arg = -1;
@@ -111,15 +112,16 @@ k_ws_arrows(int h, int w, const int32_t* __restrict__ list, const int32_t* __res
 // Flat pixels: the seed arrow (first row-major same-level non-flat
 // neighbour: distance 1) and plateau unions with the backward same-level flat
 // neighbours.
-__global__ void k_ws_union(int h, int w, const uint8_t* __restrict__ mask,
+__global__ void k_ws_union(int h, FastDiv dw, const uint8_t* __restrict__ mask,
                            const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
                            const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count, int32_t* __restrict__ ptr,
                            int32_t* par) {
+  const int w = (int)dw.d;
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
-    const int y = i / w, x = i - y * w;
+    const int y = fdiv(i, dw), x = i - y * w;
     const uint16_t f = Fw[i];
     int32_t seed = -2;
     for (uint32_t m = fg_nbrs(h, w, mask, i, y, x); m; m &= m - 1) {
@@ -199,11 +201,12 @@ __global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
 }
 
 // Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8).
-__device__ __forceinline__ uint32_t plateau_nbrs(int h, int w, const uint8_t* __restrict__ mask,
+__device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint8_t* __restrict__ mask,
                                                  const uint16_t* __restrict__ Fw,
                                                  const int32_t* __restrict__ par, int32_t p,
                                                  uint16_t f, int32_t r) {
-  const int y = p / w, x = p - y * w;
+  const int w = (int)dw.d;
+  const int y = fdiv(p, dw), x = p - y * w;
   uint32_t m = 0;
   for (uint32_t a = fg_nbrs(h, w, mask, p, y, x); a; a &= a - 1) {
     const int t = __ffs(a) - 1;
@@ -220,12 +223,13 @@ __device__ __forceinline__ uint32_t plateau_nbrs(int h, int w, const uint8_t* __
 // at distance d - 1.  Up to 32 * kPer members are kept in registers; larger
 // components re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
-k_ws_plateau(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
+k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
              const int32_t* __restrict__ par,
              const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
              const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
              const unsigned long long* __restrict__ alloc, int32_t* __restrict__ ptr,
              int32_t* delta) {
+  const int w = (int)dw.d;
   constexpr int kPer = 4;
   const int ncomp = (int)(*alloc >> 32);
   const int lane = threadIdx.x & 31;
@@ -247,7 +251,7 @@ k_ws_plateau(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
         if (k < sz) {
           px[q] = mem[k];
           d[q] = ptr[px[q]] >= 0 ? 1 : kInfD;
-          nb[q] = plateau_nbrs(h, w, mask, Fw, par, px[q], f, r);
+          nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], f, r);
           vd[px[q]] = d[q];
         }
       }
@@ -286,7 +290,7 @@ k_ws_plateau(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
           const int32_t dp = vd[p];
           if (dp == 1) continue;
           int32_t best = dp;
-          for (uint32_t m = plateau_nbrs(h, w, mask, Fw, par, p, f, r); m; m &= m - 1)
+          for (uint32_t m = plateau_nbrs(h, dw, mask, Fw, par, p, f, r); m; m &= m - 1)
             best = min(best, vd[nbr_index(w, p, __ffs(m) - 1)] + 1);
           if (best < dp) {
             vd[p] = best;
@@ -299,7 +303,7 @@ k_ws_plateau(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
         const int32_t p = mem[k];
         const int32_t dp = vd[p];
         if (dp == 1) continue;
-        for (uint32_t m = plateau_nbrs(h, w, mask, Fw, par, p, f, r); m; m &= m - 1) {
+        for (uint32_t m = plateau_nbrs(h, dw, mask, Fw, par, p, f, r); m; m &= m - 1) {
           const int32_t j = nbr_index(w, p, __ffs(m) - 1);
           if (vd[j] == dp - 1) { ptr[p] = j; break; }
         }
@@ -317,11 +321,12 @@ k_ws_plateau(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
 // background) as boundary values, so each component is independent and one
 // warp iterates it to its fixed point.  Output: Fw = fg ? F + 1 : 0.
 __global__ void __launch_bounds__(256)
-k_hmax_init(int h, int w, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const uint8_t* __restrict__ mask, const uint16_t* __restrict__ dq, int32_t ws_h,
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
             int32_t* __restrict__ scount) {
+  const int w = (int)dw.d;
   __shared__ int32_t sm[9];
   const int n = *count;
   for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
@@ -330,7 +335,7 @@ k_hmax_init(int h, int w, const int32_t* __restrict__ list, const int32_t* __res
     int32_t p = 0;
     if (k < n) {
       p = list[k];
-      const int y = p / w, x = p - y * w;
+      const int y = fdiv(p, dw), x = p - y * w;
       const int32_t v = dq[p];
       int32_t mx = 0;
       for (uint32_t m = fg_nbrs(h, w, mask, p, y, x); m; m &= m - 1)
@@ -351,14 +356,15 @@ k_hmax_init(int h, int w, const int32_t* __restrict__ list, const int32_t* __res
   }
 }
 
-__global__ void k_hmax_union(int h, int w, const uint8_t* __restrict__ mask,
+__global__ void k_hmax_union(int h, FastDiv dw, const uint8_t* __restrict__ mask,
                              const uint8_t* __restrict__ sflag,
                              const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                              int32_t* par) {
+  const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = list[k];
-    const int y = i / w, x = i - y * w;
+    const int y = fdiv(i, dw), x = i - y * w;
     // backward neighbours only (bits 0..3: above row and left)
     for (uint32_t m = fg_nbrs(h, w, mask, i, y, x) & 0xFu; m; m &= m - 1) {
       const int32_t j = nbr_index(w, i, __ffs(m) - 1);
@@ -395,11 +401,12 @@ k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count
 
 // Neighbour summary of suspect p: bit t set = row-major neighbour t is a
 // suspect (same component); fixed = max F over the other neighbours.
-__device__ __forceinline__ uint32_t hmax_nbrs(int h, int w, const uint8_t* __restrict__ mask,
+__device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint8_t* __restrict__ mask,
                                               const uint16_t* __restrict__ dq,
                                               const uint8_t* __restrict__ sflag, int32_t p,
                                               int32_t& fixed) {
-  const int y = p / w, x = p - y * w;
+  const int w = (int)dw.d;
+  const int y = fdiv(p, dw), x = p - y * w;
   uint32_t m = 0;
   fixed = 0;  // background neighbours: F = 0
   for (uint32_t a = fg_nbrs(h, w, mask, p, y, x); a; a &= a - 1) {
@@ -412,11 +419,12 @@ __device__ __forceinline__ uint32_t hmax_nbrs(int h, int w, const uint8_t* __res
 }
 
 __global__ void __launch_bounds__(256)
-k_hmax_solve(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ dq,
+k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ dq,
              const uint8_t* __restrict__ sflag,
              int32_t ws_h, const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
              const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
              const unsigned long long* __restrict__ alloc, uint16_t* Fw) {
+  const int w = (int)dw.d;
   constexpr int kPer = 4;
   const int ncomp = (int)(*alloc >> 32);
   const int lane = threadIdx.x & 31;
@@ -438,7 +446,7 @@ k_hmax_solve(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
           px[q] = mem[k];
           d[q] = dq[px[q]];
           int32_t fixed;
-          nb[q] = hmax_nbrs(h, w, mask, dq, sflag, px[q], fixed);
+          nb[q] = hmax_nbrs(h, dw, mask, dq, sflag, px[q], fixed);
           f[q] = min(d[q], max(d[q] > ws_h ? d[q] - ws_h : 0, fixed));
           vf[px[q]] = (uint16_t)(f[q] + 1);
         }
@@ -466,7 +474,7 @@ k_hmax_solve(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
         const int32_t p = mem[k];
         const int32_t dp = dq[p];
         int32_t fixed;
-        hmax_nbrs(h, w, mask, dq, sflag, p, fixed);
+        hmax_nbrs(h, dw, mask, dq, sflag, p, fixed);
         vf[p] = (uint16_t)(min(dp, max(dp > ws_h ? dp - ws_h : 0, fixed)) + 1);
       }
       __syncwarp();
@@ -478,7 +486,7 @@ k_hmax_solve(int h, int w, const uint8_t* __restrict__ mask, const uint16_t* __r
           if (fp == dp) continue;
           int32_t fixed;
           int32_t best = fp;
-          for (uint32_t m = hmax_nbrs(h, w, mask, dq, sflag, p, fixed); m; m &= m - 1)
+          for (uint32_t m = hmax_nbrs(h, dw, mask, dq, sflag, p, fixed); m; m &= m - 1)
             best = max(best, (int32_t)vf[nbr_index(w, p, __ffs(m) - 1)] - 1);
           best = min(best, dp);
           if (best > fp) {
@@ -512,14 +520,15 @@ __global__ void k_ws_basins(const int32_t* __restrict__ list, const int32_t* __r
 
 // Separation: a listed pixel survives unless an 8-neighbour has a higher
 // basin id (background pixels of sep are cleared beforehand).
-__global__ void k_ws_separate(int h, int w, const int32_t* __restrict__ list,
+__global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ list,
                               const int32_t* __restrict__ count,
                               const uint8_t* __restrict__ mask,
                               const int32_t* __restrict__ basin, uint8_t* __restrict__ sep) {
+  const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t p = list[k];
-    const int y = p / w, x = p - y * w;
+    const int y = fdiv(p, dw), x = p - y * w;
     const int32_t b = basin[p];
     bool keep = b > 0;
     for (uint32_t m = fg_nbrs(h, w, mask, p, y, x); m && keep; m &= m - 1)
@@ -537,11 +546,12 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 }  // namespace
 
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin) {
+              int32_t ws_h, uint8_t* sep, int32_t* basin, bool want_basin, bool list_ready) {
   const int64_t n = h * w;
   uint16_t* dq = ctx->u16a;
   uint16_t* F = ctx->u16b;
   const int g = ctx->num_sms * 8;
+  const FastDiv dwv = make_div((uint32_t)w);
   int32_t* fgl = ctx->fg_list;
   int32_t* fgn = ctx->misc + 4;  // foreground count
   // component lists (root, size): the arena holds 16 B per pixel
@@ -551,7 +561,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_CUDA(cudaMemsetAsync(sep, 0, (size_t)n, ctx->stream));
   if (want_basin) RTG_CUDA(cudaMemsetAsync(basin, 0, sizeof(int32_t) * (size_t)n, ctx->stream));
   prof_mark(ctx, RTG_STAGE_EDT);
-  RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
+  if (!list_ready) RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
   const bool iwpp_hmax = ctx->hmax_impl == 1;
   if (iwpp_hmax) {
     RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));  // every pixel (IWPP reads all)
@@ -574,10 +584,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     uint8_t* sflag = ctx->m1;
     RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
     RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-    k_hmax_init<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, fgl, fgn, mask, dq, ws_h, Fw, sflag,
+    k_hmax_init<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, dq, ws_h, Fw, sflag,
                                             par, basin, list, count);
     RTG_LAUNCH("k_hmax_init");
-    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, mask, sflag, list, count, par);
+    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, sflag, list, count, par);
     RTG_LAUNCH("k_hmax_union");
     k_ws_roots<<<g, 256, 0, ctx->stream>>>(list, count, nullptr, par, basin, slot);
     RTG_LAUNCH("k_ws_roots");
@@ -586,7 +596,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_LAUNCH("k_hmax_alloc");
     k_ws_scatter<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, slot, ctx->lroots);
     RTG_LAUNCH("k_ws_scatter");
-    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, mask, dq, sflag, ws_h, basin,
+    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, dq, sflag, ws_h, basin,
                                              ctx->lroots, comp_root, comp_size, alloc, Fw);
     RTG_LAUNCH("k_hmax_solve");
   }
@@ -598,10 +608,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* flat_count = ctx->misc + 1;
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
   RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-  k_ws_arrows<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, fgl, fgn, mask, Fw, ptr, par, basin,
+  k_ws_arrows<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, Fw, ptr, par, basin,
                                           flat, ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
-  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, mask, Fw, flat, ctx->flat_list,
+  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, flat, ctx->flat_list,
                                          flat_count, ptr, par);
   RTG_LAUNCH("k_ws_union");
   k_ws_roots<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, ptr, par, basin, delta);
@@ -612,12 +622,12 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   k_ws_scatter<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots);
   RTG_LAUNCH("k_ws_scatter");
-  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, mask, Fw, par, basin, ctx->lroots,
+  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, par, basin, ctx->lroots,
                                            comp_root, comp_size, alloc, ptr, delta);
   RTG_LAUNCH("k_ws_plateau");
   k_ws_basins<<<g, 256, 0, ctx->stream>>>(fgl, fgn, ptr, par, basin);
   RTG_LAUNCH("k_ws_basins");
-  k_ws_separate<<<g, 256, 0, ctx->stream>>>((int)h, (int)w, fgl, fgn, mask, basin, sep);
+  k_ws_separate<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, basin, sep);
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
 }

@@ -131,7 +131,9 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o6 + o7 PreWatershed + Watershed (basin ids staged in the labels buffer);
   // watershed() marks its own EDT / MARKERS / WATERSHED stages
   if (ctx->ws_impl == 0) {
-    RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels, false));
+    // the joint fill/area path already listed the foreground of m3
+    const bool listed = ctx->fill_impl == 0;
+    RTG_TRY(watershed(ctx, ctx->m3, h, w, p->ws_h, mask, labels, false, listed));
   } else {
     // the area-threshold forest and counts already name the kept objects
     prof_mark(ctx, RTG_STAGE_WATERSHED);
