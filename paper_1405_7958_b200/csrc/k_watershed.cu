@@ -65,6 +65,16 @@ __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
   return p + (k / 3 - 1) * w + (k % 3 - 1);
 }
 
+// The 8 neighbour values selected by mask m (others = fill), as unrolled
+// predicated loads so all of them are in flight together (a loop over the
+// set bits would serialise one memory latency per neighbour).
+template <typename T, typename S>
+__device__ __forceinline__ void gather8(const T* a, int w, int32_t p, uint32_t m, S fill,
+                                        S (&v)[8]) {
+#pragma unroll
+  for (int t = 0; t < 8; ++t) v[t] = ((m >> t) & 1u) ? (S)a[nbr_index(w, p, t)] : fill;
+}
+
 // Arrows over the foreground list.  Non-flat pixels: steepest ascent
 // (par = -1, flat byte 0).  Flat pixels: par = self, cnt = 0, flat byte 1,
 // appended to the flat list (their seed arrow is set by k_ws_union).
@@ -87,11 +97,11 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       const uint32_t f = Fw[p];
       uint32_t best = f;
       int32_t arg = -1;
-      for (uint32_t m = fg_nbrs(h, w, mask, p, y, x); m; m &= m - 1) {
-        const int32_t j = nbr_index(w, p, __ffs(m) - 1);  // row-major: first max = min index
-        const uint32_t fj = Fw[j];
-        if (fj > best) { best = fj; arg = j; }
-      }
+      uint32_t fv[8];
+      gather8(Fw, w, p, fg_nbrs(h, w, mask, p, y, x), 0u, fv);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)  // row-major: first max = min index
+        if (fv[t] > best) { best = fv[t]; arg = nbr_index(w, p, t); }
       if (arg >= 0) {
         ptr[p] = arg;
         par[p] = -1;
@@ -124,11 +134,15 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint8_t* __restrict__ mask,
     const int y = fdiv(i, dw), x = i - y * w;
     const uint16_t f = Fw[i];
     int32_t seed = -2;
-    for (uint32_t m = fg_nbrs(h, w, mask, i, y, x); m; m &= m - 1) {
-      const int t = __ffs(m) - 1;
+    const uint32_t fm = fg_nbrs(h, w, mask, i, y, x);
+    uint32_t fv[8], fl[8];
+    gather8(Fw, w, i, fm, 0u, fv);
+    gather8(flat, w, i, fm, 1u, fl);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (!((fm >> t) & 1u) || fv[t] != f) continue;
       const int32_t j = nbr_index(w, i, t);
-      if (Fw[j] != f) continue;
-      if (!flat[j]) {
+      if (!fl[t]) {
         if (seed == -2) seed = j;
       } else if (t < 4) {  // backward neighbour (above or left)
         uf_unite_g(par, i, j);
@@ -196,7 +210,10 @@ __global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
     const int32_t v = cnt[par[i]];
-    if (v & kSeeded) members[(v & kCountMask) + slot[i]] = i;
+    if (v & kSeeded) {
+      const int32_t sl = slot[i];
+      members[(v & kCountMask) + sl] = sl == 0 ? ~i : i;  // ~: first member of a component
+    }
   }
 }
 
@@ -207,51 +224,79 @@ __device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint8_
                                                  uint16_t f, int32_t r) {
   const int w = (int)dw.d;
   const int y = fdiv(p, dw), x = p - y * w;
+  const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
+  uint32_t fv[8];
+  int32_t pv[8];
+  gather8(Fw, w, p, fm, 0u, fv);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) pv[t] = ((fm >> t) & 1u) ? __ldcg(par + nbr_index(w, p, t)) : -1;
   uint32_t m = 0;
-  for (uint32_t a = fg_nbrs(h, w, mask, p, y, x); a; a &= a - 1) {
-    const int t = __ffs(a) - 1;
-    const int32_t j = nbr_index(w, p, t);
-    if (Fw[j] == f && __ldcg(par + j) == r) m |= 1u << t;
-  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (((fm >> t) & 1u) && fv[t] == f && pv[t] == r) m |= 1u << t;
   return m;
 }
 
-// Plateau distances and arrows, one warp per seeded component: chaotic
-// Bellman-Ford over the members (values only decrease and always equal some
-// real path length, so the fixed point is the BFS distance), then every
-// non-seed member points at its first (minimum-index) same-plateau neighbour
-// at distance d - 1.  Up to 32 * kPer members are kept in registers; larger
-// components re-derive their neighbour masks every pass.
+// Components are laid out back to back in `members` (component order), each
+// flagged at its first entry (~pixel).  Warp chunk [w0, w0 + 32) takes every
+// component that STARTS in it — a whole number of small components per warp,
+// so a warp-wide convergence test is exact and tiny components share a warp.
+// Returns false when no component starts in the chunk; else [s0, e).
+__device__ __forceinline__ bool packed_range(const int32_t* __restrict__ members, int nmem,
+                                             int w0, int lane, int& s0, int& e) {
+  const unsigned full = 0xFFFFFFFFu;
+  const int k = w0 + lane;
+  const unsigned st = __ballot_sync(full, k < nmem && members[k] < 0);
+  if (!st) return false;
+  s0 = w0 + __ffs(st) - 1;
+  e = nmem;
+  for (int b = w0 + 32; b < nmem; b += 32) {
+    const int kk = b + lane;
+    const unsigned nx = __ballot_sync(full, kk < nmem && members[kk] < 0);
+    if (nx) {
+      e = b + __ffs(nx) - 1;
+      break;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ int32_t member_px(int32_t m) { return m < 0 ? ~m : m; }
+
+// Plateau distances and arrows over packed components: chaotic Bellman-Ford
+// over the members (values only decrease and always equal some real path
+// length, so the fixed point is the BFS distance), then every non-seed member
+// points at its first (minimum-index) same-plateau neighbour at distance
+// d - 1.  Up to 32 * kPer members per warp in registers; longer ranges
+// re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
-k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
-             const int32_t* __restrict__ par,
-             const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
-             const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
-             const unsigned long long* __restrict__ alloc, int32_t* __restrict__ ptr,
-             int32_t* delta) {
+k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+             const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
+             const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
+             int32_t* __restrict__ ptr, int32_t* delta, int2* __restrict__ scratch) {
   const int w = (int)dw.d;
   constexpr int kPer = 4;
-  const int ncomp = (int)(*alloc >> 32);
+  const int nmem = (int)(*alloc & 0xFFFFFFFFull);
   const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
   volatile int32_t* vd = delta;
-  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncomp; c += warps) {
-    const int32_t r = comp_root[c], sz = comp_size[c];
-    const int32_t* mem = members + (cnt[r] & kCountMask);
-    const uint16_t f = Fw[r];
-    if (sz <= 32 * kPer) {
+  for (int w0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < nmem;
+       w0 += nwarps * 32) {
+    int s0, e;
+    if (!packed_range(members, nmem, w0, lane, s0, e)) continue;
+    if (e - s0 <= 32 * kPer) {
       int32_t px[kPer], d[kPer];
       uint32_t nb[kPer];
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
-        const int k = lane + 32 * q;
+        const int k = s0 + lane + 32 * q;
         px[q] = -1;
         d[q] = kInfD;
         nb[q] = 0;
-        if (k < sz) {
-          px[q] = mem[k];
+        if (k < e) {
+          px[q] = member_px(members[k]);
           d[q] = ptr[px[q]] >= 0 ? 1 : kInfD;
-          nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], f, r);
+          nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], Fw[px[q]], par[px[q]]);
           vd[px[q]] = d[q];
         }
       }
@@ -261,9 +306,11 @@ k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           if (px[q] < 0 || d[q] == 1) continue;
+          int32_t dv[8];
+          gather8(vd, w, px[q], nb[q], kInfD, dv);
           int32_t best = d[q];
-          for (uint32_t m = nb[q]; m; m &= m - 1)
-            best = min(best, vd[nbr_index(w, px[q], __ffs(m) - 1)] + 1);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) best = min(best, dv[t] + 1);
           if (best < d[q]) {
             d[q] = best;
             vd[px[q]] = best;
@@ -275,38 +322,47 @@ k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         if (px[q] < 0 || d[q] == 1) continue;
-        for (uint32_t m = nb[q]; m; m &= m - 1) {
-          const int32_t j = nbr_index(w, px[q], __ffs(m) - 1);
-          if (vd[j] == d[q] - 1) { ptr[px[q]] = j; break; }
-        }
+        int32_t dv[8];
+        gather8(vd, w, px[q], nb[q], kInfD, dv);
+#pragma unroll
+        for (int t = 7; t >= 0; --t)  // the first (minimum-index) match wins
+          if (dv[t] == d[q] - 1) ptr[px[q]] = nbr_index(w, px[q], t);
       }
     } else {
-      for (int k = lane; k < sz; k += 32) vd[mem[k]] = ptr[mem[k]] >= 0 ? 1 : kInfD;
+      // long range: per-member (pixel, neighbour mask) cached in scratch
+      for (int k = s0 + lane; k < e; k += 32) {
+        const int32_t p = member_px(members[k]);
+        vd[p] = ptr[p] >= 0 ? 1 : kInfD;
+        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, par, p, Fw[p], par[p]));
+      }
       __syncwarp();
       while (true) {
         bool changed = false;
-        for (int k = lane; k < sz; k += 32) {
-          const int32_t p = mem[k];
-          const int32_t dp = vd[p];
+        for (int k = s0 + lane; k < e; k += 32) {
+          const int2 pm = scratch[k];
+          const int32_t dp = vd[pm.x];
           if (dp == 1) continue;
+          int32_t dv[8];
+          gather8(vd, w, pm.x, (uint32_t)pm.y, kInfD, dv);
           int32_t best = dp;
-          for (uint32_t m = plateau_nbrs(h, dw, mask, Fw, par, p, f, r); m; m &= m - 1)
-            best = min(best, vd[nbr_index(w, p, __ffs(m) - 1)] + 1);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) best = min(best, dv[t] + 1);
           if (best < dp) {
-            vd[p] = best;
+            vd[pm.x] = best;
             changed = true;
           }
         }
         if (!__any_sync(0xFFFFFFFFu, changed)) break;
       }
-      for (int k = lane; k < sz; k += 32) {
-        const int32_t p = mem[k];
-        const int32_t dp = vd[p];
+      for (int k = s0 + lane; k < e; k += 32) {
+        const int2 pm = scratch[k];
+        const int32_t dp = vd[pm.x];
         if (dp == 1) continue;
-        for (uint32_t m = plateau_nbrs(h, dw, mask, Fw, par, p, f, r); m; m &= m - 1) {
-          const int32_t j = nbr_index(w, p, __ffs(m) - 1);
-          if (vd[j] == dp - 1) { ptr[p] = j; break; }
-        }
+        int32_t dv[8];
+        gather8(vd, w, pm.x, (uint32_t)pm.y, kInfD, dv);
+#pragma unroll
+        for (int t = 7; t >= 0; --t)
+          if (dv[t] == dp - 1) ptr[pm.x] = nbr_index(w, pm.x, t);
       }
     }
   }
@@ -337,9 +393,11 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       p = list[k];
       const int y = fdiv(p, dw), x = p - y * w;
       const int32_t v = dq[p];
+      int32_t dv[8];
+      gather8(dq, w, p, fg_nbrs(h, w, mask, p, y, x), 0, dv);
       int32_t mx = 0;
-      for (uint32_t m = fg_nbrs(h, w, mask, p, y, x); m; m &= m - 1)
-        mx = max(mx, (int32_t)dq[nbr_index(w, p, __ffs(m) - 1)]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mx = max(mx, dv[t]);
       if (mx >= v + ws_h) {
         Fw[p] = (uint16_t)(v + 1);
         sflag[p] = 0;
@@ -366,10 +424,11 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint8_t* __restrict__ mask
     const int32_t i = list[k];
     const int y = fdiv(i, dw), x = i - y * w;
     // backward neighbours only (bits 0..3: above row and left)
-    for (uint32_t m = fg_nbrs(h, w, mask, i, y, x) & 0xFu; m; m &= m - 1) {
-      const int32_t j = nbr_index(w, i, __ffs(m) - 1);
-      if (sflag[j]) uf_unite_g(par, i, j);
-    }
+    uint32_t sv[8];
+    gather8(sflag, w, i, fg_nbrs(h, w, mask, i, y, x) & 0xFu, 0u, sv);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (sv[t]) uf_unite_g(par, i, nbr_index(w, i, t));
   }
 }
 
@@ -407,43 +466,47 @@ __device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint8_t* 
                                               int32_t& fixed) {
   const int w = (int)dw.d;
   const int y = fdiv(p, dw), x = p - y * w;
+  const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
+  uint32_t sv[8];
+  int32_t dv[8];
+  gather8(sflag, w, p, fm, 0u, sv);
+  gather8(dq, w, p, fm, 0, dv);
   uint32_t m = 0;
   fixed = 0;  // background neighbours: F = 0
-  for (uint32_t a = fg_nbrs(h, w, mask, p, y, x); a; a &= a - 1) {
-    const int t = __ffs(a) - 1;
-    const int32_t j = nbr_index(w, p, t);
-    if (sflag[j]) m |= 1u << t;
-    else fixed = max(fixed, (int32_t)dq[j]);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if (sv[t]) m |= 1u << t;
+    else fixed = max(fixed, dv[t]);
   }
   return m;
 }
 
 __global__ void __launch_bounds__(256)
-k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t* __restrict__ dq,
-             const uint8_t* __restrict__ sflag,
-             int32_t ws_h, const int32_t* __restrict__ cnt, const int32_t* __restrict__ members,
-             const int32_t* __restrict__ comp_root, const int32_t* __restrict__ comp_size,
-             const unsigned long long* __restrict__ alloc, uint16_t* Fw) {
+k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+             const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag, int32_t ws_h,
+             const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
+             uint16_t* Fw, int2* __restrict__ scratch) {
   const int w = (int)dw.d;
   constexpr int kPer = 4;
-  const int ncomp = (int)(*alloc >> 32);
+  const int nmem = (int)(*alloc & 0xFFFFFFFFull);
   const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
   volatile uint16_t* vf = Fw;
-  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncomp; c += warps) {
-    const int32_t r = comp_root[c], sz = comp_size[c];
-    const int32_t* mem = members + (cnt[r] & kCountMask);
-    if (sz <= 32 * kPer) {
+  for (int w0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < nmem;
+       w0 += nwarps * 32) {
+    int s0, e;
+    if (!packed_range(members, nmem, w0, lane, s0, e)) continue;
+    if (e - s0 <= 32 * kPer) {
       int32_t px[kPer], d[kPer], f[kPer];
       uint32_t nb[kPer];
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
-        const int k = lane + 32 * q;
+        const int k = s0 + lane + 32 * q;
         px[q] = -1;
         d[q] = f[q] = 0;
         nb[q] = 0;
-        if (k < sz) {
-          px[q] = mem[k];
+        if (k < e) {
+          px[q] = member_px(members[k]);
           d[q] = dq[px[q]];
           int32_t fixed;
           nb[q] = hmax_nbrs(h, dw, mask, dq, sflag, px[q], fixed);
@@ -457,9 +520,11 @@ k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           if (px[q] < 0 || f[q] == d[q]) continue;
+          int32_t fv[8];
+          gather8(vf, w, px[q], nb[q], 0, fv);
           int32_t best = f[q];
-          for (uint32_t m = nb[q]; m; m &= m - 1)
-            best = max(best, (int32_t)vf[nbr_index(w, px[q], __ffs(m) - 1)] - 1);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) best = max(best, fv[t] - 1);
           best = min(best, d[q]);
           if (best > f[q]) {
             f[q] = best;
@@ -470,27 +535,30 @@ k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask, const uint16_t
         if (!__any_sync(0xFFFFFFFFu, changed)) break;
       }
     } else {
-      for (int k = lane; k < sz; k += 32) {
-        const int32_t p = mem[k];
+      // long range: per-member (pixel, neighbour mask | dq << 8) cached in scratch
+      for (int k = s0 + lane; k < e; k += 32) {
+        const int32_t p = member_px(members[k]);
         const int32_t dp = dq[p];
         int32_t fixed;
-        hmax_nbrs(h, dw, mask, dq, sflag, p, fixed);
+        const uint32_t nbm = hmax_nbrs(h, dw, mask, dq, sflag, p, fixed);
         vf[p] = (uint16_t)(min(dp, max(dp > ws_h ? dp - ws_h : 0, fixed)) + 1);
+        scratch[k] = make_int2(p, (int32_t)(nbm | ((uint32_t)dp << 8)));
       }
       __syncwarp();
       while (true) {
         bool changed = false;
-        for (int k = lane; k < sz; k += 32) {
-          const int32_t p = mem[k];
-          const int32_t dp = dq[p], fp = (int32_t)vf[p] - 1;
+        for (int k = s0 + lane; k < e; k += 32) {
+          const int2 pm = scratch[k];
+          const int32_t dp = (int32_t)((uint32_t)pm.y >> 8), fp = (int32_t)vf[pm.x] - 1;
           if (fp == dp) continue;
-          int32_t fixed;
+          int32_t fv[8];
+          gather8(vf, w, pm.x, (uint32_t)pm.y & 0xFFu, 0, fv);
           int32_t best = fp;
-          for (uint32_t m = hmax_nbrs(h, dw, mask, dq, sflag, p, fixed); m; m &= m - 1)
-            best = max(best, (int32_t)vf[nbr_index(w, p, __ffs(m) - 1)] - 1);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) best = max(best, fv[t] - 1);
           best = min(best, dp);
           if (best > fp) {
-            vf[p] = (uint16_t)(best + 1);
+            vf[pm.x] = (uint16_t)(best + 1);
             changed = true;
           }
         }
@@ -530,9 +598,11 @@ __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ lis
     const int32_t p = list[k];
     const int y = fdiv(p, dw), x = p - y * w;
     const int32_t b = basin[p];
+    int32_t bv[8];
+    gather8(basin, w, p, fg_nbrs(h, w, mask, p, y, x), 0, bv);
     bool keep = b > 0;
-    for (uint32_t m = fg_nbrs(h, w, mask, p, y, x); m && keep; m &= m - 1)
-      keep = basin[nbr_index(w, p, __ffs(m) - 1)] <= b;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) keep &= bv[t] <= b;
     sep[p] = keep;
   }
 }
@@ -557,6 +627,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // component lists (root, size): the arena holds 16 B per pixel
   int32_t* comp_root = reinterpret_cast<int32_t*>(ctx->arena);
   int32_t* comp_size = comp_root + n;
+  // per-member cache of long component ranges (the arena's second half)
+  int2* member_scratch = reinterpret_cast<int2*>(ctx->arena + 8 * n);
   auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
   RTG_CUDA(cudaMemsetAsync(sep, 0, (size_t)n, ctx->stream));
   if (want_basin) RTG_CUDA(cudaMemsetAsync(basin, 0, sizeof(int32_t) * (size_t)n, ctx->stream));
@@ -596,8 +668,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_LAUNCH("k_hmax_alloc");
     k_ws_scatter<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, slot, ctx->lroots);
     RTG_LAUNCH("k_ws_scatter");
-    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, dq, sflag, ws_h, basin,
-                                             ctx->lroots, comp_root, comp_size, alloc, Fw);
+    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, dq, sflag, ws_h, ctx->lroots,
+                                             alloc, Fw, member_scratch);
     RTG_LAUNCH("k_hmax_solve");
   }
   prof_mark(ctx, RTG_STAGE_WATERSHED);
@@ -622,8 +694,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   k_ws_scatter<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots);
   RTG_LAUNCH("k_ws_scatter");
-  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, par, basin, ctx->lroots,
-                                           comp_root, comp_size, alloc, ptr, delta);
+  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, par, ctx->lroots, alloc, ptr,
+                                           delta, member_scratch);
   RTG_LAUNCH("k_ws_plateau");
   k_ws_basins<<<g, 256, 0, ctx->stream>>>(fgl, fgn, ptr, par, basin);
   RTG_LAUNCH("k_ws_basins");
