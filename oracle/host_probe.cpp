@@ -10,9 +10,13 @@
 // validation (data_region.cpp:171-192), RegionTemplate bbox fold / remove
 // (region_template.cpp:19-74), worker_prepare / stage_finalize
 // (dataflow.cpp:113-176) incl. sub-box reads (storage.cpp:21-54), WRM FCFS /
-// PATS picks (wrm.cpp:246-273), ManagerState FIFO dispatch (dataflow.cpp:73-111).
+// PATS picks (wrm.cpp:246-273), ManagerState FIFO dispatch (dataflow.cpp:73-111),
+// RTP1 pack bytes / unpack round trips / decode errors (pack.cpp:33-133),
+// RTS1 session files (disk_store.cpp:150-217).
 #include <cstdint>
+#include <cstring>
 #include <cstdio>
+#include <fstream>
 #include <functional>
 #include <memory>
 #include <random>
@@ -22,11 +26,15 @@
 #ifdef RT_REF
 #include "rt/bounding_box.hpp"
 #include "rt/data_region.hpp"
+#include "rt/pack.hpp"
 #include "rt/dataflow.hpp"
 #include "rt/dms.hpp"
 #include "rt/region_template.hpp"
+#include "rt/disk_store.hpp"
 #include "rt/wrm.hpp"
 #else
+#include "rt/pack.hpp"
+#include "rt/session.hpp"
 #include "rt/region.hpp"
 #include "rt/runtime.hpp"
 #endif
@@ -67,6 +75,10 @@ std::string outcome(F&& f) {
     return "ProtocolError";
   } catch (const ConfigError&) {
     return "ConfigError";
+  } catch (const DecodeError&) {
+    return "DecodeError";
+  } catch (const IoError&) {
+    return "IoError";
   } catch (const Error&) {
     return "Error";
   }
@@ -232,13 +244,163 @@ void scheduler() {
   std::printf("manager double %s\n", outcome([&] { m.stage_complete(1); }).c_str());
 }
 
+// A stage's output template as the hot path leaves it: RGB (Dense3D u8),
+// Mask (Dense2D u8), Labels (Dense2D i32), Features (Dense2D f32, n x 20).
+RegionTemplate stage_template(std::mt19937_64& g, int h, int w, int nobj) {
+  RegionTemplate t("seg_tile");
+  auto fill = [&](std::size_t n) {
+    std::vector<std::uint8_t> v(n);
+    for (auto& b : v) b = std::uint8_t(g());
+    return v;
+  };
+  DataRegion rgb(DataRegionId{"wsi", "RGB", "Dense3D", 3, 1}, RegionKind::kDense3D,
+                 ElementKind::kU8, BoundingBox({8, 16, 0}, {8 + h - 1, 16 + w - 1, 2}));
+  rgb.put_chunk(rgb.bbox(), fill(std::size_t(3 * h * w)));
+  rgb.set_storage_binding("disk");
+  t.insert_data_region(std::move(rgb));
+  // outputs: Dense2D + trailing axis, so all regions share rank 3
+  DataRegion mask(DataRegionId{"seg", "Mask", "Dense2D", 3, 2}, RegionKind::kDense2D,
+                  ElementKind::kU8, BoundingBox({8, 16, 0}, {8 + h - 1, 16 + w - 1, 0}));
+  mask.put_chunk(mask.bbox(), fill(std::size_t(h * w)));
+  mask.set_io_mode(IoMode::kOutput);
+  mask.set_roi(BoundingBox({9, 17, 0}, {8 + h - 2, 16 + w - 2, 0}));
+  t.insert_data_region(std::move(mask));
+  DataRegion labels(DataRegionId{"seg", "Labels", "Dense2D", 3, 2}, RegionKind::kDense2D,
+                    ElementKind::kI32, BoundingBox({8, 16, 0}, {8 + h - 1, 16 + w - 1, 0}));
+  // two row bands as separate chunks
+  const int hh = h / 2;
+  labels.put_chunk(BoundingBox({8, 16, 0}, {8 + hh - 1, 16 + w - 1, 0}),
+                   fill(std::size_t(4 * hh * w)));
+  labels.put_chunk(BoundingBox({8 + hh, 16, 0}, {8 + h - 1, 16 + w - 1, 0}),
+                   fill(std::size_t(4 * (h - hh) * w)));
+  labels.set_io_mode(IoMode::kInputOutput);
+  t.insert_data_region(std::move(labels));
+  DataRegion feats(DataRegionId{"seg", "Features", "Dense2D", 3, 2}, RegionKind::kDense2D,
+                   ElementKind::kF32, BoundingBox({0, 0, 0}, {nobj - 1, 19, 0}));
+  std::vector<std::uint8_t> fp(std::size_t(nobj) * 20 * 4);
+  for (int k = 0; k < nobj * 20; ++k) {
+    const float v = float(int(g() % 100000)) / 7.0f;
+    std::memcpy(fp.data() + 4 * k, &v, 4);
+  }
+  feats.put_chunk(feats.bbox(), std::move(fp));
+  feats.set_io_mode(IoMode::kOutput);
+  t.insert_data_region(std::move(feats));
+  DataRegion lazy(DataRegionId{"wsi", "Next", "Dense2D", 4, 0}, RegionKind::kDense2D,
+                  ElementKind::kU16, BoundingBox({0, 0, 0}, {3, 3, 0}));
+  lazy.set_lazy(true);
+  t.insert_data_region(std::move(lazy));
+  return t;
+}
+
+void packs() {
+  std::mt19937_64 g(1405795800);
+  for (int i = 0; i < 6; ++i) {
+    RegionTemplate t = stage_template(g, 6 + 2 * i, 5 + 3 * i, 1 + 5 * i);
+    for (int pay = 0; pay < 2; ++pay) {
+      const std::vector<std::uint8_t> b = pack_template(t, pay != 0);
+      const RegionTemplate u = unpack_template(b);
+      const std::vector<std::uint8_t> b2 = pack_template(u, pay != 0);
+      std::printf("pack %d %d len=%zu h=%016llx rt=%d regions=%zu box=%s\n", i, pay, b.size(),
+                  (unsigned long long)fnv(b), int(b2 == b), u.regions().size(),
+                  u.bbox().to_string().c_str());
+    }
+    // corruptions
+    const std::vector<std::uint8_t> b = pack_template(t, true);
+    auto bad = [&](const char* what, std::vector<std::uint8_t> v) {
+      std::printf("unpack %d %s %s\n", i, what, outcome([&] { unpack_template(v); }).c_str());
+    };
+    bad("truncated", std::vector<std::uint8_t>(b.begin(), b.end() - 1));
+    bad("trailing", [&] { auto v = b; v.push_back(0); return v; }());
+    bad("magic", [&] { auto v = b; v[0] ^= 1; return v; }());
+    bad("flags", [&] { auto v = b; v[4] = 2; return v; }());
+    bad("empty", std::vector<std::uint8_t>());
+    bad("cut_half", std::vector<std::uint8_t>(b.begin(), b.begin() + b.size() / 2));
+  }
+  // a rank mix: the region is inserted, the box fold throws
+  {
+    RegionTemplate t("mix");
+    t.insert_data_region(DataRegion(DataRegionId{"a", "x", "raw", 0, 0}, RegionKind::kDense3D,
+                                    ElementKind::kU8, BoundingBox({0, 0, 0}, {3, 3, 2})));
+    const std::string o = outcome([&] {
+      t.insert_data_region(DataRegion(DataRegionId{"a", "y", "raw", 0, 0}, RegionKind::kDense2D,
+                                      ElementKind::kU8, BoundingBox({0, 0}, {3, 3})));
+    });
+    std::printf("mix %s size=%zu box=%s\n", o.c_str(), t.regions().size(),
+                t.bbox().to_string().c_str());
+  }
+  RegionTemplate empty("none");
+  const std::vector<std::uint8_t> e = pack_template(empty, true);
+  std::printf("pack empty len=%zu h=%016llx\n", e.size(), (unsigned long long)fnv(e));
+}
+
+std::vector<std::uint8_t> file_bytes(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  return std::vector<std::uint8_t>((std::istreambuf_iterator<char>(f)),
+                                   std::istreambuf_iterator<char>());
+}
+
+void write_bytes(const std::string& path, const std::vector<std::uint8_t>& b) {
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  f.write(reinterpret_cast<const char*>(b.data()), std::streamsize(b.size()));
+}
+
+std::uint64_t record_hash(const DiskRecord& r) {
+  std::vector<std::uint8_t> v(r.payload);
+  const std::string s = r.id.ns + "|" + r.id.key + "|" + r.id.type_tag + "|" +
+                        std::to_string(r.id.timestamp) + "|" + std::to_string(r.id.version) + "|" +
+                        std::to_string(int(r.kind)) + "|" + std::to_string(int(r.element_kind)) +
+                        "|" + r.box.to_string() + "|" + std::to_string(r.seq);
+  v.insert(v.end(), s.begin(), s.end());
+  return fnv(v);
+}
+
+void sessions(const char* dir) {
+  std::mt19937_64 g(7958);
+  for (int i = 0; i < 4; ++i) {
+    RegionTemplate t = stage_template(g, 4 + 3 * i, 6 + i, 2 + 4 * i);
+    std::vector<DiskRecord> recs;
+    std::uint64_t seq = 100 * std::uint64_t(i);
+    for (const auto& [id, r] : t.regions()) {
+      if (!r.materialized()) continue;
+      for (const auto& [box, chunk] : r.chunks())
+        recs.push_back(DiskRecord{id, r.kind(), r.element_kind(), box, seq++, chunk.payload});
+    }
+    const std::string path = std::string(dir) + "/s" + std::to_string(i) + ".rts";
+    const std::vector<std::uint64_t> offs = write_session_file(path, 7 + std::uint64_t(i), recs);
+    const std::vector<std::uint8_t> bytes = file_bytes(path);
+    std::string o;
+    for (auto x : offs) o += std::to_string(x) + ",";
+    std::printf("session %d n=%zu len=%zu h=%016llx offs=%s\n", i, recs.size(), bytes.size(),
+                (unsigned long long)fnv(bytes), o.c_str());
+    const std::vector<DiskRecord> back = read_session_file(path);
+    for (std::size_t k = 0; k < back.size(); ++k)
+      std::printf("record %d %zu %016llx at=%016llx\n", i, k,
+                  (unsigned long long)record_hash(back[k]),
+                  (unsigned long long)record_hash(read_record_at(path, offs[k])));
+    auto bad = [&](const char* what, std::vector<std::uint8_t> v) {
+      write_bytes(path, v);
+      std::printf("session_bad %d %s %s\n", i, what,
+                  outcome([&] { read_session_file(path); }).c_str());
+    };
+    bad("truncated", std::vector<std::uint8_t>(bytes.begin(), bytes.end() - 1));
+    bad("magic", [&] { auto v = bytes; v[0] ^= 4; return v; }());
+    bad("end_magic", [&] { auto v = bytes; v[v.size() - 1] ^= 4; return v; }());
+    bad("footer", [&] { auto v = bytes; v[v.size() - 12] ^= 0x40; return v; }());
+    bad("short", std::vector<std::uint8_t>(bytes.begin(), bytes.begin() + 20));
+  }
+  std::printf("session_missing %s\n",
+              outcome([&] { read_session_file(std::string(dir) + "/nope.rts"); }).c_str());
+}
+
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
   boxes();
   copies();
   regions();
   dataflow();
   scheduler();
+  packs();
+  sessions(argc > 1 ? argv[1] : "/tmp");
   return 0;
 }

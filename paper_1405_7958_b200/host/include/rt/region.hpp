@@ -41,6 +41,7 @@ RT_ERROR_KIND(EmptyRoiError);
 RT_ERROR_KIND(DecodeError);
 RT_ERROR_KIND(RangeError);
 RT_ERROR_KIND(NotFoundError);
+RT_ERROR_KIND(IoError);
 RT_ERROR_KIND(CycleError);
 RT_ERROR_KIND(ProtocolError);
 RT_ERROR_KIND(ConfigError);

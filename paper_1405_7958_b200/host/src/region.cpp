@@ -232,13 +232,14 @@ void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
 // ---- RegionTemplate -------------------------------------------------------------
 
 DataRegion& RegionTemplate::insert_data_region(DataRegion region) {
+  // region_template.cpp:19-29: the region goes in first, then the template box
+  // is folded — a box of another rank throws DimensionError from the union
+  // and leaves the region inserted (the reference's observable behaviour)
   const DataRegionId id = region.id();
   if (regions_.count(id)) throw DuplicateRegionError("duplicate region " + id.to_string());
-  bbox_ = bbox_.empty() ? region.bbox()
-          : region.bbox().empty() || region.bbox().dims() != bbox_.dims()
-              ? bbox_
-              : bbox_.unioned(region.bbox());
-  return regions_.emplace(id, std::move(region)).first->second;
+  DataRegion& r = regions_.emplace(id, std::move(region)).first->second;
+  if (!r.bbox().empty()) bbox_ = bbox_.empty() ? r.bbox() : bbox_.unioned(r.bbox());
+  return r;
 }
 
 const DataRegion* RegionTemplate::get_data_region(const DataRegionId& id) const {
@@ -273,8 +274,7 @@ void RegionTemplate::refold() {
   bbox_ = BoundingBox();
   for (const auto& [id, r] : regions_) {
     if (r.bbox().empty()) continue;
-    if (bbox_.empty()) bbox_ = r.bbox();
-    else if (bbox_.dims() == r.bbox().dims()) bbox_ = bbox_.unioned(r.bbox());
+    bbox_ = bbox_.empty() ? r.bbox() : bbox_.unioned(r.bbox());
   }
 }
 

@@ -76,7 +76,10 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
   const Chunk* c = rgb->find_chunk(b3);
   if (!c) throw NotFoundError("RGB tile has no chunk covering " + b3.to_string());
   const std::int64_t h = b3.extent(0), w = b3.extent(1);
-  const BoundingBox b2({b3.lo(0), b3.lo(1)}, {b3.hi(0), b3.hi(1)});
+  // Outputs are Dense2D with the trailing axis the reference allows
+  // (data_region.cpp:152-157), so every region of the stage template has rank
+  // 3 like the RGB tile (a rank mix throws in RegionTemplate's box fold).
+  const BoundingBox b2({b3.lo(0), b3.lo(1), 0}, {b3.hi(0), b3.hi(1), 0});
 
   DataRegion& mask = install_output(local, ids.mask, RegionKind::kDense2D, ElementKind::kU8, b2);
   DataRegion& labels =
@@ -89,7 +92,7 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
                              reinterpret_cast<std::int32_t*>(labels.find_chunk(b2)->payload.data()),
                              nullptr, feats.data(), cap, &n));
   if (n > 0) {
-    const BoundingBox fb({0, 0}, {n - 1, RTG_NUM_FEATURES - 1});
+    const BoundingBox fb({0, 0, 0}, {n - 1, RTG_NUM_FEATURES - 1, 0});
     DataRegion& f = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb);
     std::memcpy(f.find_chunk(fb)->payload.data(), feats.data(),
                 sizeof(float) * std::size_t(n) * RTG_NUM_FEATURES);
@@ -109,14 +112,15 @@ StageInstance make_segmentation_stage(std::uint64_t stage_id, const BoundingBox&
                                       std::shared_ptr<const VariantRegistry> reg) {
   if (tile.dims() != 2) throw DimensionError("tile box must be 2-D <y0,x0;y1,x1>");
   const BoundingBox rgb_box({tile.lo(0), tile.lo(1), 0}, {tile.hi(0), tile.hi(1), 2});
+  const BoundingBox out_box({tile.lo(0), tile.lo(1), 0}, {tile.hi(0), tile.hi(1), 0});
   StageInstance s;
   s.stage_id = stage_id;
   s.stage_kind = "segmentation";
   s.region_descriptors = {
       RegionDescriptor{ids.rgb, rgb_box, IoMode::kInput, ids.binding, false},
-      RegionDescriptor{ids.mask, tile, IoMode::kOutput, ids.binding, false},
-      RegionDescriptor{ids.labels, tile, IoMode::kOutput, ids.binding, false},
-      RegionDescriptor{ids.features, BoundingBox({0, 0}, {0, RTG_NUM_FEATURES - 1}),
+      RegionDescriptor{ids.mask, out_box, IoMode::kOutput, ids.binding, false},
+      RegionDescriptor{ids.labels, out_box, IoMode::kOutput, ids.binding, false},
+      RegionDescriptor{ids.features, BoundingBox({0, 0, 0}, {0, RTG_NUM_FEATURES - 1, 0}),
                        IoMode::kOutput, ids.binding, false},
   };
   s.body = [reg, stage_id] {

@@ -110,6 +110,21 @@ void containers() {
             "row-major, last axis contiguous");
     require_throws<DimensionError>([&] { DenseDataRegion2D<std::uint8_t> bad(r); }, "kind check");
   });
+  check("template box fold rejects a rank mix but keeps the region (region_template.cpp:19-29)", [] {
+    RegionTemplate t("mix");
+    DataRegion rgb(DataRegionId{"img", "RGB", "raw", 0, 0}, RegionKind::kDense3D, ElementKind::kU8,
+                   BoundingBox({0, 0, 0}, {7, 7, 2}));
+    t.insert_data_region(std::move(rgb));
+    require_throws<DimensionError>([&] {
+      t.insert_data_region(DataRegion(DataRegionId{"img", "m", "raw", 0, 0}, RegionKind::kDense2D,
+                                      ElementKind::kU8, box2(0, 0, 7, 7)));
+    }, "rank mismatch");
+    require(t.size() == 2 && t.bbox() == BoundingBox({0, 0, 0}, {7, 7, 2}), "inserted, box kept");
+    // the same output as Dense2D + trailing axis folds fine
+    t.insert_data_region(DataRegion(DataRegionId{"img", "m", "raw", 1, 0}, RegionKind::kDense2D,
+                                    ElementKind::kU8, BoundingBox({0, 0, 0}, {9, 7, 0})));
+    require(t.bbox() == BoundingBox({0, 0, 0}, {9, 7, 2}), "rank-3 fold");
+  });
   check("rank check: Dense3D RGB box and Dense2D+time", [] {
     DataRegion rgb(DataRegionId{"img", "RGB", "raw", 0, 0}, RegionKind::kDense3D, ElementKind::kU8,
                    BoundingBox({0, 0, 0}, {7, 7, 2}));
@@ -219,7 +234,7 @@ void cpu_segment_features(const SegmentationRegions& names, const rtg_params& p)
   const DataRegion* rgb = local.get_data_region(ids.rgb);
   const BoundingBox& b3 = rgb->bbox();
   const std::int64_t h = b3.extent(0), w = b3.extent(1);
-  const BoundingBox b2({b3.lo(0), b3.lo(1)}, {b3.hi(0), b3.hi(1)});
+  const BoundingBox b2({b3.lo(0), b3.lo(1), 0}, {b3.hi(0), b3.hi(1), 0});
   DataRegion& mask = install_output(local, ids.mask, RegionKind::kDense2D, ElementKind::kU8, b2);
   DataRegion& lab = install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2);
   std::vector<float> f(std::size_t(1 << 16) * RTG_NUM_FEATURES);
@@ -228,7 +243,7 @@ void cpu_segment_features(const SegmentationRegions& names, const rtg_params& p)
       reinterpret_cast<std::int32_t*>(lab.find_chunk(b2)->payload.data()), f.data(), 1 << 16,
       nullptr);
   if (n > 0) {
-    const BoundingBox fb({0, 0}, {n - 1, RTG_NUM_FEATURES - 1});
+    const BoundingBox fb({0, 0, 0}, {n - 1, RTG_NUM_FEATURES - 1, 0});
     DataRegion& fr = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb);
     std::memcpy(fr.find_chunk(fb)->payload.data(), f.data(), sizeof(float) * n * RTG_NUM_FEATURES);
   }
@@ -282,9 +297,12 @@ Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats) {
   for (std::int64_t y = 0; y < H; y += T) {
     for (std::int64_t x = 0; x < W; x += T, ++k) {
       const auto& t = tile_ids[std::size_t(k)];
-      out.masks.push_back(st->read_region(t.mask, box2(y, x, y + T - 1, x + T - 1)));
-      out.labels.push_back(st->read_region(t.labels, box2(y, x, y + T - 1, x + T - 1)));
-      out.feats.push_back(st->read_region(t.features, box2(0, 0, 0, RTG_NUM_FEATURES - 1)));
+      // stage outputs carry a trailing singleton axis (rank 3 like the RGB tile)
+      const BoundingBox tb({y, x, 0}, {y + T - 1, x + T - 1, 0});
+      out.masks.push_back(st->read_region(t.mask, tb));
+      out.labels.push_back(st->read_region(t.labels, tb));
+      out.feats.push_back(
+          st->read_region(t.features, BoundingBox({0, 0, 0}, {0, RTG_NUM_FEATURES - 1, 0})));
     }
   }
   return out;
