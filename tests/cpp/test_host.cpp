@@ -11,7 +11,9 @@
 #include <vector>
 
 #include "../../oracle/rtg_oracle.h"
+#include "rt/pack.hpp"
 #include "rt/region.hpp"
+#include "rt/session.hpp"
 #include "rt/rtg_stage.hpp"
 #include "rt/runtime.hpp"
 
@@ -323,6 +325,25 @@ void gpu_stage() {
               "labels tile " + std::to_string(i));
       require(g.labels[i].element_kind() == ElementKind::kI32, "labels are I32");
     }
+  });
+  check("GPU stage outputs persist as RTP1 packs and RTS1 sessions and read back intact", [] {
+    ExecutorStats st;
+    const Run g = run_slide(true, false, &st);
+    RegionTemplate t("seg_out");
+    t.insert_data_region(g.masks[0]);
+    t.insert_data_region(g.labels[0]);
+    t.insert_data_region(g.feats[0]);
+    const std::vector<std::uint8_t> b = pack_template(t, true);
+    const RegionTemplate u = unpack_template(b);
+    require(pack_template(u, true) == b, "pack round trip");
+    const std::string path = "test_host_session.rts";
+    const std::vector<DiskRecord> recs = template_records(t, 1);
+    const std::vector<std::uint64_t> offs = write_session_file(path, 1, recs);
+    const std::vector<DiskRecord> back = read_session_file(path);
+    require(back.size() == recs.size() && offs.size() == recs.size(), "record count");
+    for (std::size_t k = 0; k < recs.size(); ++k)
+      require(back[k].payload == recs[k].payload && back[k].box == recs[k].box, "record");
+    std::remove(path.c_str());
   });
   check("PATS sends a dual-variant task to the GPU worker", [] {
     ExecutorStats s;
