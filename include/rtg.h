@@ -116,6 +116,29 @@ enum rtg_feature {
   RTG_F_EXTENT = 19
 };
 
+/* Per-object texture row (float32, RTG_NUM_TEXTURE columns): the
+ * "histograms and co-occurrence matrices" intermediates of the paper's
+ * feature stage.  Intensity is the
+ * hematoxylin plane; histogram: 16 bins (v >> 4); grey-level co-occurrence
+ * matrix (GLCM): 8 levels (v >> 5), symmetric, summed over the offsets
+ * (0,1) (1,0) (1,1) (1,-1) for pixel pairs inside the same object.  All
+ * statistics are fp64 over integer intermediates. */
+#define RTG_NUM_TEXTURE 12
+enum rtg_texture_feature {
+  RTG_T_HIST_ENTROPY = 0,   /* -sum p log2 p over the 16-bin histogram */
+  RTG_T_HIST_ENERGY = 1,    /* sum p^2 */
+  RTG_T_SKEWNESS = 2,       /* third standardised moment of intensity */
+  RTG_T_KURTOSIS = 3,       /* fourth standardised moment - 3 */
+  RTG_T_GLCM_ASM = 4,       /* sum P^2 */
+  RTG_T_GLCM_CONTRAST = 5,  /* sum (i-j)^2 P */
+  RTG_T_GLCM_HOMOGENEITY = 6, /* sum P / (1 + (i-j)^2) */
+  RTG_T_GLCM_ENTROPY = 7,   /* -sum P log2 P */
+  RTG_T_GLCM_CORRELATION = 8, /* (sum ij P - mu^2) / sigma^2 */
+  RTG_T_GLCM_DISSIMILARITY = 9, /* sum |i-j| P */
+  RTG_T_GLCM_MAX_PROB = 10, /* max P */
+  RTG_T_GLCM_CLUSTER_SHADE = 11 /* sum (i + j - 2 mu)^3 P */
+};
+
 /* ---- lifecycle ---------------------------------------------------------- */
 
 /* Default parameters tuned for H&E tiles (Ruifrok-Johnston stain matrix). */
@@ -289,6 +312,17 @@ int rtg_watershed_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h,
 int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels,
                      const uint8_t* d_intensity, int64_t h, int64_t w,
                      const int32_t* d_n, float* d_features);
+
+/* Texture table (RTG_NUM_TEXTURE columns) for canonical labels 1..n: one
+ * warp per object bounding box builds the histogram + co-occurrence
+ * intermediates, one thread per object turns them into the row. */
+int rtg_texture_features_dev(rtg_ctx* ctx, const int32_t* d_labels,
+                             const uint8_t* d_intensity, int64_t h, int64_t w,
+                             const int32_t* d_n, float* d_texture);
+/* Host-buffer variant: out is n_objects x RTG_NUM_TEXTURE f32. */
+int rtg_texture_features(rtg_ctx* ctx, const int32_t* labels,
+                         const uint8_t* intensity, int64_t h, int64_t w,
+                         int32_t n_objects, float* out);
 
 /* ---- synthetic H&E tiles (deterministic, splitmix64 as src/sim.cpp:33-44) */
 

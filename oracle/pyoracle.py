@@ -41,6 +41,8 @@ def load() -> ctypes.CDLL:
         "orc_edt_sq": ([vp, i64, i64, vp], None),
         "orc_watershed": ([vp, i64, i64, i32, vp, vp, vp], None),
         "orc_features": ([vp, vp, i64, i64, i32, vp], None),
+        "orc_texture": ([vp, vp, i64, i64, i32, vp], None),
+        "orc_texture_row": ([vp, vp, vp, vp], None),
         "orc_process_tile": ([vp, i64, i64, i64, vp, vp, vp, vp, i32, vp], i32),
     }
     for name, (args, res) in sigs.items():
@@ -144,6 +146,26 @@ def features(labels, intensity, n):
     load().orc_features(_p(np.ascontiguousarray(labels, np.int32)),
                         _p(np.ascontiguousarray(intensity, np.uint8)), h, w, n, _p(out))
     return out[:n]
+
+
+NUM_TEXTURE = 12
+
+
+def texture(labels, intensity, n):
+    """f4 texture table (n x 12), rtg.h enum rtg_texture_feature."""
+    h, w = labels.shape
+    out = np.zeros((max(n, 1), NUM_TEXTURE), np.float32)
+    load().orc_texture(_p(np.ascontiguousarray(labels, np.int32)),
+                       _p(np.ascontiguousarray(intensity, np.uint8)), h, w, n, _p(out))
+    return out[:n]
+
+
+def texture_row(hist, glcm, mom):
+    out = np.zeros(NUM_TEXTURE, np.float32)
+    load().orc_texture_row(_p(np.ascontiguousarray(hist, np.uint32)),
+                           _p(np.ascontiguousarray(glcm, np.uint32)),
+                           _p(np.ascontiguousarray(mom, np.int64)), _p(out))
+    return out
 
 
 def process_tile(rgb, params=None, want_planes=False, max_rows=1 << 20):

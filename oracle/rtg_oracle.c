@@ -497,6 +497,115 @@ void orc_watershed(const uint8_t* mask, int64_t h, int64_t w, int32_t ws_h,
   free(d2);
 }
 
+/* ---- f4: texture features ---------------------------------------------------- */
+
+void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int64_t mom[4],
+                     float* out) {
+  for (int k = 0; k < RTG_NUM_TEXTURE; ++k) out[k] = 0.f;
+  int64_t nn = 0;
+  for (int b = 0; b < 16; ++b) nn += hist[b];
+  if (nn == 0) return;
+  const double N = (double)nn;
+  double hent = 0.0, hen = 0.0;
+  for (int b = 0; b < 16; ++b) {
+    if (!hist[b]) continue;
+    const double p = (double)hist[b] / N;
+    hent -= p * log2(p);
+    hen += p * p;
+  }
+  const double mu = (double)mom[0] / N, e2 = (double)mom[1] / N;
+  const double e3 = (double)mom[2] / N, e4 = (double)mom[3] / N;
+  const double var = e2 - mu * mu;
+  double skew = 0.0, kurt = 0.0;
+  if (var > 0.0) {
+    const double sd = sqrt(var);
+    skew = (e3 - 3.0 * mu * e2 + 2.0 * mu * mu * mu) / (var * sd);
+    kurt = (e4 - 4.0 * mu * e3 + 6.0 * mu * mu * e2 - 3.0 * mu * mu * mu * mu) / (var * var) - 3.0;
+  }
+  out[RTG_T_HIST_ENTROPY] = (float)hent;
+  out[RTG_T_HIST_ENERGY] = (float)hen;
+  out[RTG_T_SKEWNESS] = (float)skew;
+  out[RTG_T_KURTOSIS] = (float)kurt;
+  int64_t tt = 0;
+  for (int k = 0; k < 64; ++k) tt += glcm[k];
+  if (tt == 0) return;
+  const double T = (double)tt;
+  double asm_ = 0.0, con = 0.0, hom = 0.0, ent = 0.0, mui = 0.0, dis = 0.0, mx = 0.0;
+  for (int i = 0; i < 8; ++i) {
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t c = glcm[i * 8 + j];
+      if (!c) continue;
+      const double P = (double)c / T;
+      const int d = i - j;
+      asm_ += P * P;
+      con += (double)(d * d) * P;
+      hom += P / (1.0 + (double)(d * d));
+      ent -= P * log2(P);
+      mui += (double)i * P;
+      dis += (double)(d < 0 ? -d : d) * P;
+      if (P > mx) mx = P;
+    }
+  }
+  double vari = 0.0, sij = 0.0, shade = 0.0;
+  for (int i = 0; i < 8; ++i) {
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t c = glcm[i * 8 + j];
+      if (!c) continue;
+      const double P = (double)c / T;
+      const double di = (double)i - mui;
+      const double t = (double)(i + j) - 2.0 * mui;
+      vari += di * di * P;
+      sij += (double)(i * j) * P;
+      shade += t * t * t * P;
+    }
+  }
+  out[RTG_T_GLCM_ASM] = (float)asm_;
+  out[RTG_T_GLCM_CONTRAST] = (float)con;
+  out[RTG_T_GLCM_HOMOGENEITY] = (float)hom;
+  out[RTG_T_GLCM_ENTROPY] = (float)ent;
+  out[RTG_T_GLCM_CORRELATION] = (float)(vari > 0.0 ? (sij - mui * mui) / vari : 0.0);
+  out[RTG_T_GLCM_DISSIMILARITY] = (float)dis;
+  out[RTG_T_GLCM_MAX_PROB] = (float)mx;
+  out[RTG_T_GLCM_CLUSTER_SHADE] = (float)shade;
+}
+
+void orc_texture(const int32_t* labels, const uint8_t* I, int64_t h, int64_t w, int32_t n,
+                 float* out) {
+  uint32_t* hist = (uint32_t*)calloc((size_t)n * 16 + 1, sizeof(uint32_t));
+  uint32_t* glcm = (uint32_t*)calloc((size_t)n * 64 + 1, sizeof(uint32_t));
+  int64_t* mom = (int64_t*)calloc((size_t)n * 4 + 1, sizeof(int64_t));
+  /* forward offsets: right, down, down-right, down-left */
+  static const int ODY[4] = {0, 1, 1, 1}, ODX[4] = {1, 0, 1, -1};
+  for (int64_t y = 0; y < h; ++y) {
+    for (int64_t x = 0; x < w; ++x) {
+      const int32_t l = labels[y * w + x];
+      if (l <= 0 || l > n) continue;
+      const int64_t k = l - 1;
+      const int64_t v = I[y * w + x];
+      hist[k * 16 + (v >> 4)]++;
+      mom[k * 4 + 0] += v;
+      mom[k * 4 + 1] += v * v;
+      mom[k * 4 + 2] += v * v * v;
+      mom[k * 4 + 3] += v * v * v * v;
+      const int q = (int)(v >> 5);
+      for (int o = 0; o < 4; ++o) {
+        const int64_t yy = y + ODY[o], xx = x + ODX[o];
+        if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+        if (labels[yy * w + xx] != l) continue;
+        const int q2 = I[yy * w + xx] >> 5;
+        glcm[k * 64 + q * 8 + q2]++;
+        glcm[k * 64 + q2 * 8 + q]++;
+      }
+    }
+  }
+  for (int32_t k = 0; k < n; ++k)
+    orc_texture_row(hist + (size_t)k * 16, glcm + (size_t)k * 64, mom + (size_t)k * 4,
+                    out + (size_t)k * RTG_NUM_TEXTURE);
+  free(hist);
+  free(glcm);
+  free(mom);
+}
+
 /* ---- o9: features ----------------------------------------------------------- */
 
 typedef struct {

@@ -73,6 +73,14 @@ void orc_watershed(const uint8_t* mask, int64_t h, int64_t w, int32_t ws_h,
 /* Features for labels 1..n; out = n x RTG_NUM_FEATURES. */
 void orc_features(const int32_t* labels, const uint8_t* intensity, int64_t h,
                   int64_t w, int32_t n, float* out);
+/* Texture table for labels 1..n; out = n x RTG_NUM_TEXTURE (rtg.h enum
+ * rtg_texture_feature).  orc_texture_row turns one object's integer
+ * intermediates (16-bin histogram, 8x8 symmetric GLCM, intensity moments
+ * sum v^1..v^4) into the row; the GPU finalizer mirrors it term by term. */
+void orc_texture(const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
+                 int32_t n, float* out);
+void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int64_t mom[4],
+                     float* out);
 /* Full stage.  Returns object count (features written for min(n, max_rows)). */
 int32_t orc_process_tile(const uint8_t* rgb, int64_t h, int64_t w,
                          int64_t pitch, const rtg_params* p, uint8_t* mask,

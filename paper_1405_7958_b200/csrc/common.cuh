@@ -127,6 +127,11 @@ struct rtg_ctx {
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
   rtg::TileQueue tq{};
   rtg::FeatureAcc acc{};
+  // texture intermediates (max_objects each): bbox, histogram, GLCM, moments
+  int32_t* tex_bbox = nullptr;
+  uint32_t* tex_hist = nullptr;
+  uint32_t* tex_glcm = nullptr;
+  unsigned long long* tex_mom = nullptr;
 
   // implementation options (rtg_ctx_set_option)
   int fill_impl = 0;  // 0: union-find on the background, 1: IWPP tile queue
@@ -355,6 +360,10 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              int64_t h, int64_t w, const int32_t* d_n, float* out,
              const int32_t* list = nullptr, const int32_t* list_count = nullptr);
+
+// f4 texture table for labels 1..*d_n (out: n x RTG_NUM_TEXTURE).
+int texture(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
+            const int32_t* d_n, float* out);
 
 int synth_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row,
               int64_t tile_col, int64_t h, int64_t w, uint8_t* d_rgb);

@@ -378,6 +378,10 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->acc.sums, (size_t)kSumFields * max_objects));
         RTG_TRY(dalloc(&c->acc.mins, (size_t)kMinFields * max_objects));
         RTG_TRY(dalloc(&c->acc.maxs, (size_t)kMaxFields * max_objects));
+        RTG_TRY(dalloc(&c->tex_bbox, 4 * (size_t)max_objects));
+        RTG_TRY(dalloc(&c->tex_hist, 16 * (size_t)max_objects));
+        RTG_TRY(dalloc(&c->tex_glcm, 64 * (size_t)max_objects));
+        RTG_TRY(dalloc(&c->tex_mom, 4 * (size_t)max_objects));
         RTG_CUDA(cudaMemsetAsync(c->misc, 0, sizeof(int32_t) * (128 + (size_t)max_h), c->stream));
         RTG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(uint32_t), c->stream));
         RTG_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(int64_t) * RTG_NUM_STATS, c->stream));
@@ -400,7 +404,8 @@ int rtg_ctx_destroy(rtg_ctx* c) {
                   c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
                   c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
-                  c->acc.sums, c->acc.mins, c->acc.maxs};
+                  c->acc.sums, c->acc.mins, c->acc.maxs, c->tex_bbox, c->tex_hist,
+                  c->tex_glcm, c->tex_mom};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -816,6 +821,35 @@ int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels, const uint8_t* d_int
   if (!d_labels || !d_intensity || !d_n || !d_features)
     return fail(RTG_ERR_INVALID_ARG, "null buffer");
   return features(ctx, d_labels, d_intensity, h, w, d_n, d_features);
+}
+
+int rtg_texture_features_dev(rtg_ctx* ctx, const int32_t* d_labels, const uint8_t* d_intensity,
+                             int64_t h, int64_t w, const int32_t* d_n, float* d_texture) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_labels || !d_intensity || !d_n || !d_texture)
+    return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  return texture(ctx, d_labels, d_intensity, h, w, d_n, d_texture);
+}
+
+int rtg_texture_features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h,
+                         int64_t w, int32_t n_objects, float* out) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!labels || !intensity || (!out && n_objects > 0))
+    return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (n_objects < 0 || n_objects > ctx->max_objects)
+    return fail(RTG_ERR_OVERFLOW, "n_objects outside [0, max_objects]");
+  const size_t px = (size_t)(h * w);
+  RTG_CUDA(cudaMemcpyAsync(ctx->labels, labels, px * 4, cudaMemcpyHostToDevice, ctx->stream));
+  RTG_CUDA(cudaMemcpyAsync(ctx->hema, intensity, px, cudaMemcpyHostToDevice, ctx->stream));
+  RTG_CUDA(cudaMemcpyAsync(ctx->misc, &n_objects, sizeof(int32_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // rows land in the feature buffer (max_objects x 20 >= n x 12 floats)
+  RTG_TRY(texture(ctx, ctx->labels, ctx->hema, h, w, ctx->misc, ctx->features));
+  if (n_objects > 0)
+    RTG_CUDA(cudaMemcpyAsync(out, ctx->features,
+                             sizeof(float) * RTG_NUM_TEXTURE * (size_t)n_objects,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  return rtg_ctx_sync(ctx);
 }
 
 int rtg_synth_tile_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row, int64_t tile_col,

@@ -408,3 +408,37 @@ def test_process_tiles_batch(rtg, ctx):
         for (mask, labels, hema, f_ref, n_ref), f, n in zip(ref, got, ns):
             assert n == n_ref
             assert np.array_equal(f, f_ref)
+
+
+# ---------------------------------------------------------------- f4 texture
+
+TEX_RTOL, TEX_ATOL = 1e-5, 1e-6
+
+
+@pytest.mark.parametrize("case", ["pipeline", "blobs", "single_pixels"])
+def test_texture(rtg, ctx, oracle, tile4k, case):
+    """f4 texture table (histogram + co-occurrence statistics) vs the oracle:
+    labels of a real tile, random 8-connected blobs, and 1-pixel objects (no
+    co-occurrence pairs)."""
+    rng = np.random.default_rng(11)
+    if case == "pipeline":
+        ref = oracle.process_tile(tile4k[:1024, :1536])
+        labels, n = ref["labels"], ref["n"]
+        inten = oracle.colordeconv(tile4k[:1024, :1536], oracle.default_params())[0]
+    elif case == "blobs":
+        m = _rand_blobs(rng, 700, 900, 0.3, 3)
+        labels = np.zeros(m.shape, np.int32)
+        n = oracle.load().orc_bwlabel(m.ctypes.data, 700, 900, 8, labels.ctypes.data)
+        inten = rng.integers(0, 256, m.shape).astype(np.uint8)
+    else:
+        labels = np.zeros((64, 80), np.int32)
+        n = 0
+        for y in range(0, 64, 3):
+            for x in range(0, 80, 3):
+                n += 1
+                labels[y, x] = n
+        inten = rng.integers(0, 256, labels.shape).astype(np.uint8)
+    want = oracle.texture(labels, inten, n)
+    got = ctx.texture(labels, inten, n)
+    assert got.shape == want.shape == (n, rtg.NUM_TEXTURE)
+    np.testing.assert_allclose(got, want, rtol=TEX_RTOL, atol=TEX_ATOL)

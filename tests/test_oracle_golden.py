@@ -140,3 +140,25 @@ def test_watershed_properties(oracle):
     lab, n = oracle.bwlabel(sep, 8)
     for l in range(1, n + 1):
         assert len(np.unique(basin[lab == l])) == 1
+
+
+
+def test_texture_known_answer(oracle):
+    """f4 texture row of a hand-checked 2x2 object with grey levels 0, 1, 2, 3
+    (intensities 0, 32, 64, 96): 6 co-occurrence pairs (T = 12 symmetric
+    counts), uniform 4-bin histogram."""
+    lab = np.zeros((4, 4), np.int32)
+    lab[1:3, 1:3] = 1
+    inten = np.zeros((4, 4), np.uint8)
+    inten[1, 1], inten[1, 2], inten[2, 1], inten[2, 2] = 0, 32, 64, 96
+    t = oracle.texture(lab, inten, 1)[0]
+    np.testing.assert_allclose(t[0], 2.0)            # histogram entropy (4 equal bins)
+    np.testing.assert_allclose(t[1], 0.25)           # histogram energy
+    np.testing.assert_allclose(t[2], 0.0, atol=1e-7)  # skewness
+    np.testing.assert_allclose(t[3], -1.36, rtol=1e-6)  # excess kurtosis of 4 equispaced values
+    np.testing.assert_allclose(t[4], 1 / 12, rtol=1e-6)  # ASM: 12 cells of 1/12
+    np.testing.assert_allclose(t[5], 40 / 12, rtol=1e-6)  # contrast: 2*(1+1+4+4+9+1)/12
+    np.testing.assert_allclose(t[6], 4 / 12, rtol=1e-6)   # homogeneity
+    np.testing.assert_allclose(t[7], np.log2(12), rtol=1e-6)  # GLCM entropy
+    np.testing.assert_allclose(t[9], 20 / 12, rtol=1e-6)  # dissimilarity
+    np.testing.assert_allclose(t[10], 1 / 12, rtol=1e-6)  # max probability
