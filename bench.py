@@ -213,6 +213,8 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        # keep stdout to the one JSON line (NCCL's version banner goes there)
+        os.environ["NCCL_DEBUG"] = os.environ.get("RTG_NCCL_DEBUG", "WARN")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
@@ -391,10 +393,14 @@ def main():
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_ms = float(ems.item())
+        # whole-job bytes per step (all ranks), like `value`
+        d2h_all = torch.tensor([float(sum(d2h))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(d2h_all)
         e2e = {"value": round(px_rank * world * args.e2e_steps / (e_ms / 1e3) / 1e6, 3),
                "unit": "Mpixel/s",
-               "h2d_bytes_per_step": int(3 * px_rank),
-               "d2h_bytes_per_step": int(sum(d2h) / args.e2e_steps),
+               "h2d_bytes_per_step": int(3 * px_rank * world),
+               "d2h_bytes_per_step": int(float(d2h_all.item()) / args.e2e_steps),
                "steps": args.e2e_steps,
                "path": "rtg_process_tiles (host buffers, pinned; H2D RGB + D2H features, "
                        "double-buffered upload)",
