@@ -123,7 +123,7 @@ enum rtg_feature {
  * matrix (GLCM): 8 levels (v >> 5), symmetric, summed over the offsets
  * (0,1) (1,0) (1,1) (1,-1) for pixel pairs inside the same object.  All
  * statistics are fp64 over integer intermediates. */
-#define RTG_NUM_TEXTURE 12
+#define RTG_NUM_TEXTURE 14
 enum rtg_texture_feature {
   RTG_T_HIST_ENTROPY = 0,   /* -sum p log2 p over the 16-bin histogram */
   RTG_T_HIST_ENERGY = 1,    /* sum p^2 */
@@ -136,8 +136,14 @@ enum rtg_texture_feature {
   RTG_T_GLCM_CORRELATION = 8, /* (sum ij P - mu^2) / sigma^2 */
   RTG_T_GLCM_DISSIMILARITY = 9, /* sum |i-j| P */
   RTG_T_GLCM_MAX_PROB = 10, /* max P */
-  RTG_T_GLCM_CLUSTER_SHADE = 11 /* sum (i + j - 2 mu)^3 P */
+  RTG_T_GLCM_CLUSTER_SHADE = 11, /* sum (i + j - 2 mu)^3 P */
+  RTG_T_EDGE_PIXELS = 12,   /* Canny edge pixels inside the object (RTG_CANNY_*) */
+  RTG_T_EDGE_DENSITY = 13   /* edge pixels / area */
 };
+/* Canny thresholds the texture table uses (Sobel magnitude of the smoothed
+ * intensity; see rtg_canny_dev). */
+#define RTG_CANNY_LOW 64
+#define RTG_CANNY_HIGH 128
 
 /* ---- lifecycle ---------------------------------------------------------- */
 
@@ -319,6 +325,14 @@ int rtg_features_dev(rtg_ctx* ctx, const int32_t* d_labels,
 int rtg_texture_features_dev(rtg_ctx* ctx, const int32_t* d_labels,
                              const uint8_t* d_intensity, int64_t h, int64_t w,
                              const int32_t* d_n, float* d_texture);
+/* Canny edges of an intensity plane: 5x5 binomial smoothing ((sum + 128) >>
+ * 8), Sobel, squared magnitude m2 = gx^2 + gy^2, non-maximum suppression
+ * along the quantised gradient direction (keep m2 > m2(prev) && m2 >=
+ * m2(next); outside pixels are 0), then hysteresis: a kept pixel with m2 >
+ * low^2 is an edge iff its 8-connected component of such pixels holds one
+ * with m2 > high^2 (replicate borders throughout).  d_edges: u8 0/1. */
+int rtg_canny_dev(rtg_ctx* ctx, const uint8_t* d_intensity, int64_t h, int64_t w,
+                  int32_t low, int32_t high, uint8_t* d_edges);
 /* Host-buffer variant: out is n_objects x RTG_NUM_TEXTURE f32. */
 int rtg_texture_features(rtg_ctx* ctx, const int32_t* labels,
                          const uint8_t* intensity, int64_t h, int64_t w,

@@ -42,7 +42,8 @@ def load() -> ctypes.CDLL:
         "orc_watershed": ([vp, i64, i64, i32, vp, vp, vp], None),
         "orc_features": ([vp, vp, i64, i64, i32, vp], None),
         "orc_texture": ([vp, vp, i64, i64, i32, vp], None),
-        "orc_texture_row": ([vp, vp, vp, vp], None),
+        "orc_texture_row": ([vp, vp, vp, ctypes.c_uint32, vp], None),
+        "orc_canny": ([vp, i64, i64, i32, i32, vp], None),
         "orc_process_tile": ([vp, i64, i64, i64, vp, vp, vp, vp, i32, vp], i32),
     }
     for name, (args, res) in sigs.items():
@@ -148,7 +149,7 @@ def features(labels, intensity, n):
     return out[:n]
 
 
-NUM_TEXTURE = 12
+NUM_TEXTURE = 14
 
 
 def texture(labels, intensity, n):
@@ -160,11 +161,21 @@ def texture(labels, intensity, n):
     return out[:n]
 
 
-def texture_row(hist, glcm, mom):
+def texture_row(hist, glcm, mom, edge_px=0):
     out = np.zeros(NUM_TEXTURE, np.float32)
     load().orc_texture_row(_p(np.ascontiguousarray(hist, np.uint32)),
                            _p(np.ascontiguousarray(glcm, np.uint32)),
-                           _p(np.ascontiguousarray(mom, np.int64)), _p(out))
+                           _p(np.ascontiguousarray(mom, np.int64)), edge_px, _p(out))
+    return out
+
+
+CANNY_LOW, CANNY_HIGH = 64, 128
+
+
+def canny(intensity, low=CANNY_LOW, high=CANNY_HIGH):
+    h, w = intensity.shape
+    out = np.zeros((h, w), np.uint8)
+    load().orc_canny(_p(np.ascontiguousarray(intensity, np.uint8)), h, w, low, high, _p(out))
     return out
 
 

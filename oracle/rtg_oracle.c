@@ -497,10 +497,82 @@ void orc_watershed(const uint8_t* mask, int64_t h, int64_t w, int32_t ws_h,
   free(d2);
 }
 
+/* ---- f4: Canny edges ------------------------------------------------------------ */
+
+static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : v > hi ? hi : v; }
+
+void orc_canny(const uint8_t* I, int64_t h, int64_t w, int32_t low, int32_t high,
+               uint8_t* edges) {
+  static const int K[5] = {1, 4, 6, 4, 1};
+  const int64_t n = h * w;
+  uint8_t* S = (uint8_t*)malloc((size_t)n + 1);
+  int32_t* M = (int32_t*)malloc(sizeof(int32_t) * ((size_t)n + 1));
+  int32_t* G = (int32_t*)malloc(sizeof(int32_t) * 2 * ((size_t)n + 1));
+  uint8_t* C = (uint8_t*)calloc((size_t)n + 1, 1);
+  for (int64_t y = 0; y < h; ++y)
+    for (int64_t x = 0; x < w; ++x) {
+      int32_t acc = 0;
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx)
+          acc += K[dy + 2] * K[dx + 2] * I[clampi(y + dy, 0, h - 1) * w + clampi(x + dx, 0, w - 1)];
+      S[y * w + x] = (uint8_t)((acc + 128) >> 8);
+    }
+  for (int64_t y = 0; y < h; ++y)
+    for (int64_t x = 0; x < w; ++x) {
+      const int64_t ym = clampi(y - 1, 0, h - 1), yp = clampi(y + 1, 0, h - 1);
+      const int64_t xm = clampi(x - 1, 0, w - 1), xp = clampi(x + 1, 0, w - 1);
+      const int32_t gx = (S[ym * w + xp] + 2 * S[y * w + xp] + S[yp * w + xp]) -
+                         (S[ym * w + xm] + 2 * S[y * w + xm] + S[yp * w + xm]);
+      const int32_t gy = (S[yp * w + xm] + 2 * S[yp * w + x] + S[yp * w + xp]) -
+                         (S[ym * w + xm] + 2 * S[ym * w + x] + S[ym * w + xp]);
+      G[2 * (y * w + x)] = gx;
+      G[2 * (y * w + x) + 1] = gy;
+      M[y * w + x] = gx * gx + gy * gy;
+    }
+  const int64_t lo2 = (int64_t)low * low, hi2 = (int64_t)high * high;
+  for (int64_t y = 0; y < h; ++y)
+    for (int64_t x = 0; x < w; ++x) {
+      const int32_t gx = G[2 * (y * w + x)], gy = G[2 * (y * w + x) + 1];
+      const int64_t ax = gx < 0 ? -gx : gx, ay = gy < 0 ? -gy : gy;
+      const int64_t t22 = ax * 13573, ay15 = ay << 15;  /* tan(22.5) * 2^15 */
+      int64_t ya, xa, yb, xb;
+      if (ay15 < t22) { ya = y; xa = x - 1; yb = y; xb = x + 1; }
+      else if (ay15 > t22 + (ax << 16)) { ya = y - 1; xa = x; yb = y + 1; xb = x; }
+      else {
+        const int64_t s = ((gx ^ gy) < 0) ? -1 : 1;
+        ya = y - 1; xa = x - s; yb = y + 1; xb = x + s;
+      }
+      const int64_t m = M[y * w + x];
+      const int64_t ma = (ya >= 0 && ya < h && xa >= 0 && xa < w) ? M[ya * w + xa] : 0;
+      const int64_t mb = (yb >= 0 && yb < h && xb >= 0 && xb < w) ? M[yb * w + xb] : 0;
+      if (m > ma && m >= mb) C[y * w + x] = m > hi2 ? 2 : (m > lo2 ? 1 : 0);
+    }
+  /* hysteresis: BFS from strong pixels through weak ones (8-connected) */
+  memset(edges, 0, (size_t)n);
+  int64_t* q = (int64_t*)malloc(sizeof(int64_t) * ((size_t)n + 1));
+  int64_t qh = 0, qt = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (C[i] == 2) { edges[i] = 1; q[qt++] = i; }
+  while (qh < qt) {
+    const int64_t i = q[qh++], y = i / w, x = i % w;
+    for (int k = 0; k < 8; ++k) {
+      const int64_t yy = y + DY8[k], xx = x + DX8[k];
+      if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
+      const int64_t j = yy * w + xx;
+      if (C[j] && !edges[j]) { edges[j] = 1; q[qt++] = j; }
+    }
+  }
+  free(q);
+  free(S);
+  free(M);
+  free(G);
+  free(C);
+}
+
 /* ---- f4: texture features ---------------------------------------------------- */
 
 void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int64_t mom[4],
-                     float* out) {
+                     uint32_t edge_px, float* out) {
   for (int k = 0; k < RTG_NUM_TEXTURE; ++k) out[k] = 0.f;
   int64_t nn = 0;
   for (int b = 0; b < 16; ++b) nn += hist[b];
@@ -526,6 +598,8 @@ void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int
   out[RTG_T_HIST_ENERGY] = (float)hen;
   out[RTG_T_SKEWNESS] = (float)skew;
   out[RTG_T_KURTOSIS] = (float)kurt;
+  out[RTG_T_EDGE_PIXELS] = (float)edge_px;
+  out[RTG_T_EDGE_DENSITY] = (float)((double)edge_px / N);
   int64_t tt = 0;
   for (int k = 0; k < 64; ++k) tt += glcm[k];
   if (tt == 0) return;
@@ -574,6 +648,9 @@ void orc_texture(const int32_t* labels, const uint8_t* I, int64_t h, int64_t w, 
   uint32_t* hist = (uint32_t*)calloc((size_t)n * 16 + 1, sizeof(uint32_t));
   uint32_t* glcm = (uint32_t*)calloc((size_t)n * 64 + 1, sizeof(uint32_t));
   int64_t* mom = (int64_t*)calloc((size_t)n * 4 + 1, sizeof(int64_t));
+  uint32_t* edge = (uint32_t*)calloc((size_t)n + 1, sizeof(uint32_t));
+  uint8_t* E = (uint8_t*)malloc((size_t)(h * w) + 1);
+  orc_canny(I, h, w, RTG_CANNY_LOW, RTG_CANNY_HIGH, E);
   /* forward offsets: right, down, down-right, down-left */
   static const int ODY[4] = {0, 1, 1, 1}, ODX[4] = {1, 0, 1, -1};
   for (int64_t y = 0; y < h; ++y) {
@@ -583,6 +660,7 @@ void orc_texture(const int32_t* labels, const uint8_t* I, int64_t h, int64_t w, 
       const int64_t k = l - 1;
       const int64_t v = I[y * w + x];
       hist[k * 16 + (v >> 4)]++;
+      edge[k] += E[y * w + x];
       mom[k * 4 + 0] += v;
       mom[k * 4 + 1] += v * v;
       mom[k * 4 + 2] += v * v * v;
@@ -599,8 +677,10 @@ void orc_texture(const int32_t* labels, const uint8_t* I, int64_t h, int64_t w, 
     }
   }
   for (int32_t k = 0; k < n; ++k)
-    orc_texture_row(hist + (size_t)k * 16, glcm + (size_t)k * 64, mom + (size_t)k * 4,
+    orc_texture_row(hist + (size_t)k * 16, glcm + (size_t)k * 64, mom + (size_t)k * 4, edge[k],
                     out + (size_t)k * RTG_NUM_TEXTURE);
+  free(edge);
+  free(E);
   free(hist);
   free(glcm);
   free(mom);

@@ -80,7 +80,10 @@ void orc_features(const int32_t* labels, const uint8_t* intensity, int64_t h,
 void orc_texture(const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
                  int32_t n, float* out);
 void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int64_t mom[4],
-                     float* out);
+                     uint32_t edge_px, float* out);
+/* Canny edges (rtg.h rtg_canny_dev): BFS hysteresis from the strong pixels. */
+void orc_canny(const uint8_t* I, int64_t h, int64_t w, int32_t low, int32_t high,
+               uint8_t* edges);
 /* Full stage.  Returns object count (features written for min(n, max_rows)). */
 int32_t orc_process_tile(const uint8_t* rgb, int64_t h, int64_t w,
                          int64_t pitch, const rtg_params* p, uint8_t* mask,

@@ -361,6 +361,9 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              int64_t h, int64_t w, const int32_t* d_n, float* out,
              const int32_t* list = nullptr, const int32_t* list_count = nullptr);
 
+// f4 Canny edges (u8 0/1) of an intensity plane; uses i32a/i32b and m1/m2.
+int canny(rtg_ctx* ctx, const uint8_t* intensity, int64_t h, int64_t w, int32_t low, int32_t high,
+          uint8_t* edges);
 // f4 texture table for labels 1..*d_n (out: n x RTG_NUM_TEXTURE).
 int texture(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
             const int32_t* d_n, float* out);

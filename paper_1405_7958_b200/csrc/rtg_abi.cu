@@ -379,7 +379,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->acc.mins, (size_t)kMinFields * max_objects));
         RTG_TRY(dalloc(&c->acc.maxs, (size_t)kMaxFields * max_objects));
         RTG_TRY(dalloc(&c->tex_bbox, 4 * (size_t)max_objects));
-        RTG_TRY(dalloc(&c->tex_hist, 16 * (size_t)max_objects));
+        RTG_TRY(dalloc(&c->tex_hist, 17 * (size_t)max_objects));
         RTG_TRY(dalloc(&c->tex_glcm, 64 * (size_t)max_objects));
         RTG_TRY(dalloc(&c->tex_mom, 4 * (size_t)max_objects));
         RTG_CUDA(cudaMemsetAsync(c->misc, 0, sizeof(int32_t) * (128 + (size_t)max_h), c->stream));
@@ -829,6 +829,15 @@ int rtg_texture_features_dev(rtg_ctx* ctx, const int32_t* d_labels, const uint8_
   if (!d_labels || !d_intensity || !d_n || !d_texture)
     return fail(RTG_ERR_INVALID_ARG, "null buffer");
   return texture(ctx, d_labels, d_intensity, h, w, d_n, d_texture);
+}
+
+int rtg_canny_dev(rtg_ctx* ctx, const uint8_t* d_intensity, int64_t h, int64_t w, int32_t low,
+                  int32_t high, uint8_t* d_edges) {
+  RTG_TRY(check_ctx(ctx, h, w));
+  if (!d_intensity || !d_edges) return fail(RTG_ERR_INVALID_ARG, "null buffer");
+  if (low < 0 || high < low || high > 46341)
+    return fail(RTG_ERR_INVALID_ARG, "Canny thresholds need 0 <= low <= high <= 46341");
+  return canny(ctx, d_intensity, h, w, low, high, d_edges);
 }
 
 int rtg_texture_features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h,

@@ -21,7 +21,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtg.so")
 
 NUM_FEATURES = 20
-NUM_TEXTURE = 12
+NUM_TEXTURE = 14
+CANNY_LOW, CANNY_HIGH = 64, 128
 FEATURE_NAMES = [
     "area", "perimeter", "bbox_y0", "bbox_x0", "bbox_y1", "bbox_x1",
     "centroid_y", "centroid_x", "mean_i", "std_i", "min_i", "max_i",
@@ -41,7 +42,7 @@ SYMBOLS = [
     "rtg_edt_dev", "rtg_watershed_dev", "rtg_features_dev",
     "rtg_synth_tile_host", "rtg_synth_tile_dev", "rtg_ctx_profile",
     "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
-    "rtg_texture_features", "rtg_texture_features_dev",
+    "rtg_texture_features", "rtg_texture_features_dev", "rtg_canny_dev",
 ]
 OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
 OPT_USE_GRAPHS = 1       # 1 replay cached CUDA graphs in process_tile_dev (default)
@@ -162,6 +163,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_features_dev": [vp, vp, vp, i64, i64, vp, vp],
         "rtg_texture_features": [vp, vp, vp, i64, i64, i32, vp],
         "rtg_texture_features_dev": [vp, vp, vp, i64, i64, vp, vp],
+        "rtg_canny_dev": [vp, vp, i64, i64, i32, i32, vp],
         "rtg_synth_tile_host": [u64, i64, i64, i64, i64, vp],
         "rtg_synth_tile_dev": [vp, u64, i64, i64, i64, i64, vp],
         "rtg_ctx_profile": [vp, ctypes.c_int],
@@ -343,6 +345,10 @@ class Context:
             self.handle, _ptr(np.ascontiguousarray(labels, np.int32)),
             _ptr(np.ascontiguousarray(intensity, np.uint8)), h, w, n, _ptr(out)))
         return out[:n]
+
+    def canny_dev(self, d_intensity, h, w, d_edges, low=CANNY_LOW, high=CANNY_HIGH):
+        check(self.lib.rtg_canny_dev(self.handle, _ptr(d_intensity), h, w, low, high,
+                                     _ptr(d_edges)))
 
     def texture_dev(self, d_labels, d_intensity, h, w, d_n, d_texture):
         check(self.lib.rtg_texture_features_dev(self.handle, _ptr(d_labels), _ptr(d_intensity),

@@ -412,6 +412,29 @@ def test_process_tiles_batch(rtg, ctx):
 
 # ---------------------------------------------------------------- f4 texture
 
+@pytest.mark.parametrize("case", ["tile", "noise", "step", "tiny"])
+def test_canny(rtg, ctx, oracle, tile4k, case):
+    """Canny edges (smoothing, Sobel, NMS, hysteresis on the CCL) bit-exact
+    vs the oracle's BFS hysteresis."""
+    rng = np.random.default_rng(5)
+    if case == "tile":
+        inten = oracle.colordeconv(tile4k[:1200, :1000], oracle.default_params())[0]
+    elif case == "noise":
+        inten = rng.integers(0, 256, (333, 517)).astype(np.uint8)
+    elif case == "step":
+        inten = np.zeros((64, 96), np.uint8)
+        inten[:, 40:] = 200
+        inten[30:, :] = 90
+    else:
+        inten = rng.integers(0, 256, (3, 7)).astype(np.uint8)
+    h, w = inten.shape
+    want = oracle.canny(inten)
+    out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    ctx.canny_dev(_np_dev(inten), h, w, out)
+    got = _dev_np(out)
+    assert np.array_equal(got, want)
+
+
 TEX_RTOL, TEX_ATOL = 1e-5, 1e-6
 
 
