@@ -199,9 +199,14 @@ std::vector<Completion> stage_finalize(RegionTemplate& local, const StageInstanc
 // Demand-driven loop over the manager's stages (the real counterpart of the
 // simulator's start_task slot, /root/reference/proj/src/sim.cpp:630-685):
 // prepare -> expand body -> WRM picks device per task -> run -> finalize.
+// Cooperative CPU+GPU execution: one
+// worker thread per GPU plus cpu_workers CPU worker threads pull stages
+// demand-driven from the manager; inside a stage the WRM picks each task's
+// device (PATS: the GPU worker takes the highest-speedup variant first).
 struct ExecutorConfig {
   SchedulerKind scheduler = SchedulerKind::kPats;
-  std::vector<GpuDevice*> gpus;  // empty: CPU only
+  std::vector<GpuDevice*> gpus;  // one worker each
+  int cpu_workers = 0;           // additional CPU-only workers (>= 1 when no GPU)
 };
 struct ExecutorStats {
   std::size_t stages = 0, cpu_tasks = 0, gpu_tasks = 0;

@@ -305,13 +305,14 @@ ExecutorStats run_stages(ManagerState& manager, StorageRegistry& storage,
   ExecutorStats stats;
   std::mutex mu;  // guards manager + stats
   std::exception_ptr failure;
-  const int workers = cfg.gpus.empty() ? 1 : int(cfg.gpus.size());
+  const int ngpu = int(cfg.gpus.size());
+  const int workers = ngpu + std::max(cfg.cpu_workers, ngpu == 0 ? 1 : 0);
 
   auto worker = [&](int w) {
     try {
       WorkerContext& wc = worker_context();
       wc.worker = w;
-      wc.gpu = cfg.gpus.empty() ? nullptr : cfg.gpus[std::size_t(w)];
+      wc.gpu = w < ngpu ? cfg.gpus[std::size_t(w)] : nullptr;
       for (;;) {
         std::optional<std::uint64_t> sid;
         StageInstance stage;

@@ -256,8 +256,8 @@ struct Run {
   std::vector<DataRegion> masks, labels, feats;
 };
 
-Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats) {
-  const std::int64_t H = 1024, W = 1024, T = 512;
+Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats, int cpu_workers = 0,
+              std::int64_t H = 1024, std::int64_t W = 1024, std::int64_t T = 512) {
   rtg_params p;
   rtg_check(rtg_params_default(&p));
   StorageRegistry reg;
@@ -289,6 +289,7 @@ Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats) {
   }
   std::unique_ptr<GpuDevice> gpu;
   ExecutorConfig cfg;
+  cfg.cpu_workers = cpu_workers;
   if (use_gpu) {
     gpu = std::make_unique<GpuDevice>(0, T, T, 1 << 14);
     cfg.gpus = {gpu.get()};
@@ -344,6 +345,21 @@ void gpu_stage() {
     for (std::size_t k = 0; k < recs.size(); ++k)
       require(back[k].payload == recs[k].payload && back[k].box == recs[k].box, "record");
     std::remove(path.c_str());
+  });
+  check("cooperative CPU+GPU workers: both pull tiles, outputs bit-identical", [] {
+    ExecutorStats sg, sm;
+    const Run g = run_slide(true, false, &sg, 0, 1024, 1536, 256);
+    const Run m = run_slide(true, true, &sm, 3, 1024, 1536, 256);
+    require(sm.stages == 24 && sm.gpu_tasks + sm.cpu_tasks == 24, "all 24 tiles");
+    require(sm.gpu_tasks > 0 && sm.cpu_tasks > 0, "both device kinds used");
+    for (std::size_t i = 0; i < g.masks.size(); ++i) {
+      require(g.masks[i].chunks().begin()->second.payload ==
+                  m.masks[i].chunks().begin()->second.payload,
+              "mask tile " + std::to_string(i));
+      require(g.labels[i].chunks().begin()->second.payload ==
+                  m.labels[i].chunks().begin()->second.payload,
+              "labels tile " + std::to_string(i));
+    }
   });
   check("PATS sends a dual-variant task to the GPU worker", [] {
     ExecutorStats s;
