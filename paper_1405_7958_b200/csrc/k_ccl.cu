@@ -601,24 +601,29 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const uint32_t upf = __shfl_up_sync(kFull, fgb, 1), upb = __shfl_up_sync(kFull, bgb, 1);
   const uint32_t upall = (upf & ~(upf << 1)) | (upb & ~(upb << 1));
   __syncwarp();
-  if (lane > 0 && (upf | upb)) {
-    int k = 0;
-    for (uint32_t q = allst; q; q &= q - 1, ++k) {
-      const int b = __ffs(q) - 1;
-      const bool isf = (fgb >> b) & 1u;
-      const uint32_t cur = isf ? fgb : bgb, U = isf ? upf : upb;
-      const uint32_t run = low_run(cur >> b) << b;
-      uint32_t ov = U & (isf ? (run | (run << 1) | (run >> 1)) : run);
-      const uint32_t ust = U & ~(U << 1);
-      while (ov) {
-        const int t = __ffs(ov) - 1;
-        const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
-        unite_s(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
-        ov &= ~(low_run(U >> su) << su);
+  // rows join their upper neighbour in log2(32) rounds (row r in the round
+  // of its lowest set bit), so every union links two already-merged row
+  // blocks and the trees stay shallow
+  for (int sblk = 1; sblk < 32; sblk <<= 1) {
+    if ((lane & (2 * sblk - 1)) == sblk && (upf | upb)) {
+      int k = 0;
+      for (uint32_t q = allst; q; q &= q - 1, ++k) {
+        const int b = __ffs(q) - 1;
+        const bool isf = (fgb >> b) & 1u;
+        const uint32_t cur = isf ? fgb : bgb, U = isf ? upf : upb;
+        const uint32_t run = low_run(cur >> b) << b;
+        uint32_t ov = U & (isf ? (run | (run << 1) | (run >> 1)) : run);
+        const uint32_t ust = U & ~(U << 1);
+        while (ov) {
+          const int t = __ffs(ov) - 1;
+          const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
+          unite_s(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
+          ov &= ~(low_run(U >> su) << su);
+        }
       }
     }
+    __syncwarp();
   }
-  __syncwarp();
   // 3. flatten; per local root: pixel count + border-background bit
   const int nruns = __popc(allst);
   for (int k = 0; k < nruns; ++k) inf[rb + k] = (uint32_t)find_root(par, rb + k);

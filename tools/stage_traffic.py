@@ -19,7 +19,7 @@ STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("recon", "k_ccl_tile", None),
     ("fill_holes", "k_ccl_tile_fb", None),
     ("area", "k_fb_tree", None),
-    ("edt", "k_fg_list", None),
+    ("edt", "k_edt_rowdist", None),
     ("markers", "k_hmax_init", None),
     ("watershed", "k_ws_arrows", None),
     ("label", "k_ccl_tile", "k_ws_separate"),
