@@ -213,9 +213,21 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
-        # keep stdout to the one JSON line (NCCL's version banner goes there)
+        # keep stdout to the one JSON line: NCCL prints its version banner on
+        # fd 1 when the first communicator comes up, so fd 1 points at stderr
+        # until a first collective has run
         os.environ["NCCL_DEBUG"] = os.environ.get("RTG_NCCL_DEBUG", "WARN")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
 
     def barrier():
         if world > 1:
