@@ -306,6 +306,10 @@ class Context:
         Returns (list of feature arrays [n_i, 20], list of n_i)."""
         params = params or default_params()
         k = len(rgbs)
+        if k == 0:
+            check(self.lib.rtg_process_tiles(self.handle, 0, None, 1, 1, 3, ctypes.byref(params),
+                                             None, 0, None))
+            return [], []
         h, w, _ = rgbs[0].shape
         rgbs = [np.ascontiguousarray(r) for r in rgbs]
         max_rows = self.max_objects if max_rows is None else max_rows

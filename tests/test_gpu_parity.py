@@ -465,3 +465,35 @@ def test_texture(rtg, ctx, oracle, tile4k, case):
     got = ctx.texture(labels, inten, n)
     assert got.shape == want.shape == (n, rtg.NUM_TEXTURE)
     np.testing.assert_allclose(got, want, rtol=TEX_RTOL, atol=TEX_ATOL)
+
+
+def test_texture_dev_matches_host(rtg, ctx, oracle, tile4k):
+    """rtg_texture_features_dev on device buffers equals the host variant."""
+    ref = oracle.process_tile(tile4k[:512, :768])
+    labels, n = ref["labels"], ref["n"]
+    inten = oracle.colordeconv(tile4k[:512, :768], oracle.default_params())[0]
+    host = ctx.texture(labels, inten, n)
+    d_out = torch.zeros((ctx.max_objects, rtg.NUM_TEXTURE), dtype=torch.float32, device="cuda")
+    d_n = torch.tensor([n], dtype=torch.int32, device="cuda")
+    ctx.texture_dev(_np_dev(labels), _np_dev(inten), 512, 768, d_n, d_out)
+    ctx.sync()
+    assert np.array_equal(d_out[:n].cpu().numpy(), host)
+
+
+def test_canny_thresholds_validated(rtg, ctx):
+    d = torch.zeros((16, 16), dtype=torch.uint8, device="cuda")
+    e = torch.zeros((16, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(rtg.Error):
+        ctx.canny_dev(d, 16, 16, e, low=100, high=50)
+    with pytest.raises(rtg.Error):
+        ctx.canny_dev(d, 16, 16, e, low=-1, high=50)
+
+
+def test_process_tiles_edge_cases(rtg, ctx):
+    """Empty batch is a no-op; a feature table too small for a tile reports
+    RTG_ERR_OVERFLOW while still filling the counts."""
+    feats, ns = ctx.process_tiles([])
+    assert feats == [] and ns == []
+    rgb = rtg.synth_tile_host(0, 0, 512, 512)
+    with pytest.raises(rtg.Error):
+        ctx.process_tiles([rgb], max_rows=3)
