@@ -495,13 +495,28 @@ __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* _
   }
 }
 
+// 4 pixels per thread with 16-byte loads/stores and staged gathers.
 __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
                           const int32_t* __restrict__ rank,
                           int32_t* __restrict__ labels) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = root_of(roots, i);
-    labels[i] = r >= 0 ? rank[r] + 1 : 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(labels)) &
+                    15) == 0;
+  for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    if (vec && i0 + 4 <= n) {
+      const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
+      int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? rank[v[k]] + 1 : 0;
+      *reinterpret_cast<int4*>(labels + i0) = make_int4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
+        const int32_t r = root_of(roots, i);
+        labels[i] = r >= 0 ? rank[r] + 1 : 0;
+      }
+    }
   }
 }
 
@@ -843,13 +858,33 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
 // satisfies  R(p) >= t  <=>  p lies in a conn-component of {H >= t} that
 // contains a pixel with marker >= t.  With marker = max(H - h, 0) and t >= 1
 // that is a pixel with H >= t + h (the seed bit of FgThresh).
+// 4 pixels per thread: the root, global-root and flag gathers are issued
+// stage by stage for the four, so each stage's loads are in flight together.
 __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
                              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
                              uint8_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = root_of(roots, i);
-    out[i] = (uint8_t)(r >= 0 && flag[r] && tissue[i]);
+  const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(tissue) |
+                     reinterpret_cast<uintptr_t>(out)) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
+  for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    if (vec && i0 + 4 <= n) {
+      const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
+      const uint32_t t4 = __ldg(reinterpret_cast<const uint32_t*>(tissue + i0));
+      int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;
+      uint32_t o = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (v[k] >= 0 && flag[v[k]] && ((t4 >> (8 * k)) & 0xFFu)) o |= 1u << (8 * k);
+      *reinterpret_cast<uint32_t*>(out + i0) = o;
+    } else {
+      for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
+        const int32_t r = root_of(roots, i);
+        out[i] = (uint8_t)(r >= 0 && flag[r] && tissue[i]);
+      }
+    }
   }
 }
 
