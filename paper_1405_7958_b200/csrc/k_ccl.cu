@@ -377,15 +377,29 @@ __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
                               int32_t* __restrict__ counts, int32_t* __restrict__ flags,
                               uint32_t* __restrict__ bitmap, bool seed_in_counts = false) {
   const int n = *lcount;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t r = lroots[2 * k];
-    const uint32_t info = (uint32_t)lroots[2 * k + 1];
-    const int32_t g = uf_find_g(roots, r);
-    if (g != r) atomicMin(roots + r, g);
-    else if (bitmap) atomicOr(bitmap + (r >> 5), 1u << (r & 31));
-    if (counts) atomicAdd(counts + g, (int32_t)(info & ~kSeedBit));
-    if (seed_in_counts && (info & kSeedBit)) atomicOr(counts + g, (int32_t)kSeedBit);
-    if (flags && (info & kSeedBit)) flags[g] = 1;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count: lanes of one warp stay converged, so the count
+  // and flag updates of local roots sharing a global root (a large
+  // component spans many tiles) are combined into one atomic per warp
+  const int stride = gridDim.x * blockDim.x;
+  for (int k0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; k0 < n; k0 += stride) {
+    const int k = k0 + lane;
+    int32_t g = -1;
+    uint32_t info = 0;
+    if (k < n) {
+      const int32_t r = lroots[2 * k];
+      info = (uint32_t)lroots[2 * k + 1];
+      g = uf_find_g(roots, r);
+      if (g != r) atomicMin(roots + r, g);
+      else if (bitmap) atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+    }
+    const unsigned grp = __match_any_sync(0xFFFFFFFFu, g);
+    const uint32_t cnt = __reduce_add_sync(grp, info & ~kSeedBit);
+    const uint32_t seed = __reduce_or_sync(grp, info & kSeedBit);
+    if (g < 0 || lane != __ffs(grp) - 1) continue;
+    if (counts) atomicAdd(counts + g, (int32_t)cnt);
+    if (seed_in_counts && seed) atomicOr(counts + g, (int32_t)kSeedBit);
+    if (flags && seed) flags[g] = 1;
   }
 }
 

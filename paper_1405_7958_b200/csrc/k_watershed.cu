@@ -44,20 +44,21 @@ __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
 }
 
 // 8-neighbour foreground mask of p (bit t = row-major neighbour t of 8).
-__device__ __forceinline__ uint32_t fg_nbrs(int h, int w, const uint8_t* __restrict__ mask,
+// 8-neighbour foreground mask of p (bit t = row-major neighbour t of 8) from
+// the 1-bit foreground plane: three funnel-shifted 3-bit windows instead of
+// eight byte loads (fgb: the plane after its kBitPad leading pad words).
+__device__ __forceinline__ uint32_t fg_nbrs(int h, int w, const uint32_t* __restrict__ fgb,
                                             int32_t p, int y, int x) {
-  uint32_t m = 0;
-  int t = 0;
-#pragma unroll
-  for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
-      if (dy == 0 && dx == 0) continue;
-      const int yy = y + dy, xx = x + dx;
-      if (yy >= 0 && yy < h && xx >= 0 && xx < w && mask[p + dy * w + dx]) m |= 1u << t;
-      ++t;
-    }
-  return m;
+  auto row3 = [&](int32_t q) -> uint32_t {  // bits of columns x-1, x, x+1 of the row of q
+    const int32_t b = q - 1;
+    const int32_t wi = b >> 5;  // arithmetic shift: -1 before the first word (pad)
+    return __funnelshift_r(fgb[wi], fgb[wi + 1], (uint32_t)b & 31u) & 7u;
+  };
+  const uint32_t edge = (x == 0 ? 1u : 0u) | (x == w - 1 ? 4u : 0u);  // columns outside
+  const uint32_t up = y > 0 ? row3(p - w) & ~edge : 0u;
+  const uint32_t mid = row3(p) & ~edge;
+  const uint32_t dn = y + 1 < h ? row3(p + w) & ~edge : 0u;
+  return up | ((mid & 1u) << 3) | ((mid & 4u) << 2) | (dn << 5);
 }
 
 __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
@@ -80,7 +81,7 @@ __device__ __forceinline__ void gather8(const T* a, int w, int32_t p, uint32_t m
 // appended to the flat list (their seed arrow is set by k_ws_union).
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const uint8_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
+            const uint32_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
             int32_t* __restrict__ ptr, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
@@ -122,7 +123,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
 // Flat pixels: the seed arrow (first row-major same-level non-flat
 // neighbour: distance 1) and plateau unions with the backward same-level flat
 // neighbours.
-__global__ void k_ws_union(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+__global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                            const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
                            const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count, int32_t* __restrict__ ptr,
@@ -218,7 +219,7 @@ __global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
 }
 
 // Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8).
-__device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+__device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                                                  const uint16_t* __restrict__ Fw,
                                                  const int32_t* __restrict__ par, int32_t p,
                                                  uint16_t f, int32_t r) {
@@ -270,7 +271,7 @@ __device__ __forceinline__ int32_t member_px(int32_t m) { return m < 0 ? ~m : m;
 // d - 1.  Up to 32 * kPer members per warp in registers; longer ranges
 // re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
-k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              int32_t* __restrict__ ptr, int32_t* delta, int2* __restrict__ scratch) {
@@ -378,7 +379,7 @@ k_ws_plateau(int h, FastDiv dw, const uint8_t* __restrict__ mask,
 // warp iterates it to its fixed point.  Output: Fw = fg ? F + 1 : 0.
 __global__ void __launch_bounds__(256)
 k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const uint8_t* __restrict__ mask, const uint16_t* __restrict__ dq, int32_t ws_h,
+            const uint32_t* __restrict__ mask, const uint16_t* __restrict__ dq, int32_t ws_h,
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
             int32_t* __restrict__ scount) {
@@ -414,7 +415,7 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
   }
 }
 
-__global__ void k_hmax_union(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+__global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                              const uint8_t* __restrict__ sflag,
                              const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                              int32_t* par) {
@@ -460,7 +461,7 @@ k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count
 
 // Neighbour summary of suspect p: bit t set = row-major neighbour t is a
 // suspect (same component); fixed = max F over the other neighbours.
-__device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+__device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                                               const uint16_t* __restrict__ dq,
                                               const uint8_t* __restrict__ sflag, int32_t p,
                                               int32_t& fixed) {
@@ -482,7 +483,7 @@ __device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint8_t* 
 }
 
 __global__ void __launch_bounds__(256)
-k_hmax_solve(int h, FastDiv dw, const uint8_t* __restrict__ mask,
+k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag, int32_t ws_h,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint16_t* Fw, int2* __restrict__ scratch) {
@@ -590,7 +591,7 @@ __global__ void k_ws_basins(const int32_t* __restrict__ list, const int32_t* __r
 // basin id (background pixels of sep are cleared beforehand).
 __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ list,
                               const int32_t* __restrict__ count,
-                              const uint8_t* __restrict__ mask,
+                              const uint32_t* __restrict__ mask,
                               const int32_t* __restrict__ basin, uint8_t* __restrict__ sep) {
   const int w = (int)dw.d;
   const int n = *count;
@@ -634,6 +635,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   if (want_basin) RTG_CUDA(cudaMemsetAsync(basin, 0, sizeof(int32_t) * (size_t)n, ctx->stream));
   prof_mark(ctx, RTG_STAGE_EDT);
   if (!list_ready) RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
+  const uint32_t* fgbits = ctx->fg_bits + kBitPad;  // neighbour tests of the list kernels
   const bool iwpp_hmax = ctx->hmax_impl == 1;
   if (iwpp_hmax) {
     RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));  // every pixel (IWPP reads all)
@@ -656,10 +658,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     uint8_t* sflag = ctx->m1;
     RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
     RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-    k_hmax_init<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, dq, ws_h, Fw, sflag,
+    k_hmax_init<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
                                             par, basin, list, count);
     RTG_LAUNCH("k_hmax_init");
-    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, sflag, list, count, par);
+    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, sflag, list, count, par);
     RTG_LAUNCH("k_hmax_union");
     k_ws_roots<<<g, 256, 0, ctx->stream>>>(list, count, nullptr, par, basin, slot);
     RTG_LAUNCH("k_ws_roots");
@@ -668,7 +670,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_LAUNCH("k_hmax_alloc");
     k_ws_scatter<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, slot, ctx->lroots);
     RTG_LAUNCH("k_ws_scatter");
-    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, dq, sflag, ws_h, ctx->lroots,
+    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
                                              alloc, Fw, member_scratch);
     RTG_LAUNCH("k_hmax_solve");
   }
@@ -680,10 +682,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* flat_count = ctx->misc + 1;
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
   RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-  k_ws_arrows<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, Fw, ptr, par, basin,
+  k_ws_arrows<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, Fw, ptr, par, basin,
                                           flat, ctx->flat_list, flat_count);
   RTG_LAUNCH("k_ws_arrows");
-  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, flat, ctx->flat_list,
+  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
                                          flat_count, ptr, par);
   RTG_LAUNCH("k_ws_union");
   k_ws_roots<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, ptr, par, basin, delta);
@@ -694,12 +696,12 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   k_ws_scatter<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots);
   RTG_LAUNCH("k_ws_scatter");
-  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, mask, Fw, par, ctx->lroots, alloc, ptr,
+  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, ptr,
                                            delta, member_scratch);
   RTG_LAUNCH("k_ws_plateau");
   k_ws_basins<<<g, 256, 0, ctx->stream>>>(fgl, fgn, ptr, par, basin);
   RTG_LAUNCH("k_ws_basins");
-  k_ws_separate<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, mask, basin, sep);
+  k_ws_separate<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, basin, sep);
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
 }
