@@ -41,32 +41,36 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
                           uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero,
                           const int32_t* __restrict__ gate) {
   if (gate && !*gate) return;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s = blockIdx.y;
-  bool z = false;
-  if (x < w) {
-    int first = 0xFF, last = 0xFF;
-    const int y0 = s * kSeg;
-    for (int r = 0; r < kSeg && y0 + r < h; ++r) {
-      if (!mask[(int64_t)(y0 + r) * w + x]) {
-        if (first == 0xFF) first = r;
-        last = r;
+  // grid-stride over (segment, 128-column block) pairs: a capped grid keeps
+  // the gated (normally empty) launch cheap
+  const int nbx = (w + blockDim.x - 1) / blockDim.x, nseg = (h + kSeg - 1) / kSeg;
+  for (int blk = blockIdx.x; blk < nbx * nseg; blk += gridDim.x) {
+    const int s = blk / nbx, x = (blk - s * nbx) * blockDim.x + threadIdx.x;
+    bool z = false;
+    if (x < w) {
+      int first = 0xFF, last = 0xFF;
+      const int y0 = s * kSeg;
+      for (int r = 0; r < kSeg && y0 + r < h; ++r) {
+        if (!mask[(int64_t)(y0 + r) * w + x]) {
+          if (first == 0xFF) first = r;
+          last = r;
+        }
       }
+      seg[(int64_t)s * w + x] = (uint16_t)(first | (last << 8));
+      z = first != 0xFF;
     }
-    seg[(int64_t)s * w + x] = (uint16_t)(first | (last << 8));
-    z = first != 0xFF;
+    if (__any_sync(0xFFFFFFFFu, z) && (threadIdx.x & 31) == 0) atomicOr(any_zero, 1);
   }
-  if (__any_sync(0xFFFFFFFFu, z) && (threadIdx.x & 31) == 0) atomicOr(any_zero, 1);
 }
 
 __global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
                           const uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
                           const int32_t* __restrict__ gate) {
   if (gate && !*gate) return;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s = blockIdx.y;
-  if (x >= w) return;
-  const int nseg = (h + kSeg - 1) / kSeg;
+  const int nbx = (w + blockDim.x - 1) / blockDim.x, nseg = (h + kSeg - 1) / kSeg;
+  for (int blk = blockIdx.x; blk < nbx * nseg; blk += gridDim.x) {
+  const int s = blk / nbx, x = (blk - s * nbx) * blockDim.x + threadIdx.x;
+  if (x >= w) continue;
   const int y0 = s * kSeg;
   int above = -1;  // row of the nearest zero above the segment
   for (int t = s - 1; t >= 0; --t) {
@@ -98,6 +102,7 @@ __global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
       g[(int64_t)y * w + x] = (uint16_t)min(du[r], dd);
     }
   }
+  }
 }
 
 __device__ __forceinline__ uint32_t isqrt64(uint64_t v) {
@@ -122,40 +127,39 @@ k_edt_row(const uint16_t* __restrict__ g, int h, int w,
           uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
           int32_t* __restrict__ row_flag, const int32_t* __restrict__ gate) {
   extern __shared__ uint16_t gs[];
-  if (gate && !*gate) {
-    if (threadIdx.x == 0) row_flag[blockIdx.x] = 0;
-    return;
-  }
-  const int y = blockIdx.x;
-  const int64_t rb = (int64_t)y * w;
-  for (int x = threadIdx.x; x < w; x += blockDim.x) gs[x] = g[rb + x];
-  __syncthreads();
+  if (gate && !*gate) return;  // k_edt_row_exact checks the same gate
   const bool none = *any_zero == 0;
-  bool unresolved = false;
-  // 32-bit arithmetic: g <= 8193 and k <= kCap, so k^2 + g^2 < 2^31
-  for (int x = threadIdx.x; x < w; x += blockDim.x) {
-    const uint32_t gx = gs[x];
-    uint32_t best;
-    if (none) {
-      best = INT32_MAX;
-    } else if (gx == 0) {
-      best = 0;
-    } else {
-      best = gx == kInfG ? 0xFFFFFFFFu : gx * gx;
-      uint32_t k = 1;
-      for (; k * k < best && k <= (uint32_t)kCap; ++k) {
-        const uint32_t k2 = k * k;
-        const uint32_t gl = x >= (int)k ? gs[x - k] : kInfG;
-        const uint32_t gr = x + (int)k < w ? gs[x + k] : kInfG;
-        const uint32_t gm = min(gl, gr);
-        if (gm != kInfG) best = min(best, k2 + gm * gm);
+  for (int y = blockIdx.x; y < h; y += gridDim.x) {  // grid-stride over rows
+    const int64_t rb = (int64_t)y * w;
+    __syncthreads();  // gs of the previous row fully consumed
+    for (int x = threadIdx.x; x < w; x += blockDim.x) gs[x] = g[rb + x];
+    __syncthreads();
+    bool unresolved = false;
+    // 32-bit arithmetic: g <= 8193 and k <= kCap, so k^2 + g^2 < 2^31
+    for (int x = threadIdx.x; x < w; x += blockDim.x) {
+      const uint32_t gx = gs[x];
+      uint32_t best;
+      if (none) {
+        best = INT32_MAX;
+      } else if (gx == 0) {
+        best = 0;
+      } else {
+        best = gx == kInfG ? 0xFFFFFFFFu : gx * gx;
+        uint32_t k = 1;
+        for (; k * k < best && k <= (uint32_t)kCap; ++k) {
+          const uint32_t k2 = k * k;
+          const uint32_t gl = x >= (int)k ? gs[x - k] : kInfG;
+          const uint32_t gr = x + (int)k < w ? gs[x + k] : kInfG;
+          const uint32_t gm = min(gl, gr);
+          if (gm != kInfG) best = min(best, k2 + gm * gm);
+        }
+        if (k * k < best) unresolved = true;  // hit the cap: exact row pass below
       }
-      if (k * k < best) unresolved = true;  // hit the cap: exact row pass below
+      edt_emit(rb + x, (int64_t)best, dist2, dq, mk, ws_h);
     }
-    edt_emit(rb + x, (int64_t)best, dist2, dq, mk, ws_h);
+    const bool any = __syncthreads_or(unresolved);
+    if (threadIdx.x == 0) row_flag[y] = any ? 1 : 0;
   }
-  if (__syncthreads_or(unresolved) && threadIdx.x == 0) row_flag[y] = 1;
-  else if (threadIdx.x == 0) row_flag[y] = 0;
 }
 
 __device__ __forceinline__ int64_t floordiv64(int64_t a, int64_t b) {
@@ -170,7 +174,9 @@ __global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
                                 int32_t* __restrict__ s_buf, int32_t* __restrict__ t_buf,
                                 int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
                                 uint16_t* __restrict__ mk, int32_t ws_h,
-                                uint32_t* __restrict__ status) {
+                                uint32_t* __restrict__ status,
+                                const int32_t* __restrict__ gate = nullptr) {
+  if (gate && !*gate) return;
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
   if (y >= h || !row_flag[y]) return;
   atomicOr(status, kStatusEdtFallback);
@@ -447,17 +453,20 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                                              need_full);
   RTG_LAUNCH("k_edt_tile");
   // exact whole-tile pass, gated on need_full (empty launches otherwise)
-  const dim3 gs((unsigned)ceil_div(w, 128), (unsigned)nseg);
+  const int64_t gblk = ceil_div(w, 128) * nseg;
+  const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
   k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
   RTG_LAUNCH("k_edt_seg");
   k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
-  k_edt_row<<<(unsigned)h, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, dist2,
+  const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
+  k_edt_row<<<grows, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, dist2,
                                                       dq, mk, ws_h, row_flag, need_full);
   RTG_LAUNCH("k_edt_row");
   k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
-      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, dist2, dq, mk, ws_h, ctx->status);
+      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, dist2, dq, mk, ws_h, ctx->status,
+      need_full);
   RTG_LAUNCH("k_edt_row_exact");
   return RTG_OK;
 }
@@ -498,17 +507,20 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   k_edt_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, mask, hd, (int)h, dwv,
                                                         nullptr, dq, need_full);
   RTG_LAUNCH("k_edt_list");
-  const dim3 gs((unsigned)ceil_div(w, 128), (unsigned)nseg);
+  const int64_t gblk = ceil_div(w, 128) * nseg;
+  const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
   k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
   RTG_LAUNCH("k_edt_seg");
   k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
-  k_edt_row<<<(unsigned)h, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, nullptr, dq,
+  const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
+  k_edt_row<<<grows, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, nullptr, dq,
                                                       nullptr, 0, row_flag, need_full);
   RTG_LAUNCH("k_edt_row");
   k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
-      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, nullptr, dq, nullptr, 0, ctx->status);
+      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, nullptr, dq, nullptr, 0, ctx->status,
+      need_full);
   RTG_LAUNCH("k_edt_row_exact");
   return RTG_OK;
 }
