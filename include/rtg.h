@@ -222,7 +222,11 @@ enum rtg_option {
    * (default: a pixel with a neighbour at least ws_h higher keeps its value;
    * the few remaining pixels form small components, one warp each),
    * 1 = IWPP reconstruction on the tile queue. */
-  RTG_OPT_HMAX_IMPL = 4
+  RTG_OPT_HMAX_IMPL = 4,
+  /* Programmatic dependent launch between the stage's kernels (1, default:
+   * each kernel is scheduled while its predecessor drains; 0: plain stream
+   * order).  Results are identical either way. */
+  RTG_OPT_PDL = 5
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

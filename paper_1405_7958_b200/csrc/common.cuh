@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "rtg.h"
 
@@ -139,6 +140,7 @@ struct rtg_ctx {
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
+  int use_pdl = 1;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {
@@ -202,6 +204,34 @@ int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, int64_t i) {
   const int32_t v = roots[i];
   return v < 0 ? -1 : roots[v];
+}
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// The stage is a chain of ~40 short kernels; launched with programmatic
+// stream serialisation, kernel N+1 is scheduled while kernel N drains
+// instead of after it.  Every kernel launched that way begins with
+// pdl_enter(): griddepcontrol.wait blocks until the predecessor grid has
+// completed and its memory is visible, then launch_dependents lets the next
+// kernel be scheduled once all of this grid's CTAs are running.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(rtg_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                            size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->use_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // Division of pixel indices by the tile width without the ~20-instruction

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ roots,
            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount,
            int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b) {
+  pdl_enter();
   __shared__ int32_t s_par[kTileWarps][512];
   __shared__ uint32_t s_inf[kTileWarps][512];
   __shared__ uint8_t s_pos[kTileWarps][512];
@@ -363,6 +364,7 @@ __device__ __forceinline__ void seam_col_px(int h, int w, int32_t* __restrict__ 
 // seam (y = 32 (k + 1)), the rest walk column seams.
 template <int CONN>
 __global__ void k_ccl_seams(int h, int w, int row_seams, int32_t* __restrict__ roots) {
+  pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if ((int)blockIdx.y < row_seams)
     seam_row_px<CONN>(h, w, roots, ((int)blockIdx.y + 1) * 32, t);
@@ -376,6 +378,7 @@ __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
                               const int32_t* __restrict__ lcount, int32_t* roots,
                               int32_t* __restrict__ counts, int32_t* __restrict__ flags,
                               uint32_t* __restrict__ bitmap, bool seed_in_counts = false) {
+  pdl_enter();
   const int n = *lcount;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count: lanes of one warp stay converged, so the count
@@ -406,6 +409,7 @@ __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
 __global__ void k_area_filter(int64_t n, const int32_t* __restrict__ roots,
                               const int32_t* __restrict__ counts, int32_t lo,
                               int32_t hi, uint8_t* __restrict__ out) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = root_of(roots, i);
@@ -442,6 +446,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
 __global__ void __launch_bounds__(1024)
 k_scan_chunks(int nchunks, const int32_t* __restrict__ cnt,
               int32_t* __restrict__ off, int32_t* __restrict__ d_total) {
+  pdl_enter();
   __shared__ int warp_tot[32];
   const int per = (nchunks + 1023) / 1024;
   const int b = threadIdx.x * per;
@@ -466,6 +471,7 @@ constexpr int kBmChunk = 256 * kBmPerThread;  // words per chunk
 
 __global__ void __launch_bounds__(256)
 k_bm_count(int64_t nwords, const uint32_t* __restrict__ bm, int32_t* __restrict__ chunk_cnt) {
+  pdl_enter();
   __shared__ int warp_tot[8];
   const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
   int c = 0;
@@ -480,6 +486,7 @@ k_bm_count(int64_t nwords, const uint32_t* __restrict__ bm, int32_t* __restrict_
 __global__ void __launch_bounds__(256)
 k_bm_prefix(int64_t nwords, const uint32_t* __restrict__ bm,
             const int32_t* __restrict__ chunk_off, int32_t* __restrict__ wprefix) {
+  pdl_enter();
   __shared__ int warp_tot[8];
   const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
   uint32_t v[kBmPerThread];
@@ -501,6 +508,7 @@ k_bm_prefix(int64_t nwords, const uint32_t* __restrict__ bm,
 __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                             const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
                             const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank) {
+  pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
@@ -513,6 +521,7 @@ __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* _
 __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
                           const int32_t* __restrict__ rank,
                           int32_t* __restrict__ labels) {
+  pdl_enter();
   const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(labels)) &
                     15) == 0;
   for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n;
@@ -564,6 +573,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntiles,
               int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
               int32_t* __restrict__ lcount, int32_t* __restrict__ counts) {
+  pdl_enter();
   __shared__ FbSmem<kTileWarps> S;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
@@ -745,6 +755,7 @@ __device__ __forceinline__ void seam_fb(const uint8_t* __restrict__ m, int h, in
 
 __global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int row_seams,
                                int32_t* __restrict__ roots) {
+  pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if ((int)blockIdx.y < row_seams) {
     const int y = ((int)blockIdx.y + 1) * 32, x = t;
@@ -767,6 +778,7 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
                           const uint8_t* __restrict__ m, int w,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
                           int32_t* __restrict__ top, int32_t* __restrict__ total) {
+  pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
@@ -795,6 +807,7 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
 __global__ void k_fb_total(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                            const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
                            const int32_t* __restrict__ top, int32_t* __restrict__ total) {
+  pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
@@ -811,6 +824,7 @@ __global__ void __launch_bounds__(256)
 k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
             const int32_t* __restrict__ total, int32_t lo, int32_t hi, uint8_t* __restrict__ out,
             uint32_t* __restrict__ bits, int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  pdl_enter();
   __shared__ int32_t sm[9];
   const bool vec = (reinterpret_cast<uintptr_t>(out) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
@@ -860,6 +874,7 @@ k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const int32_t* __restr
 __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
                                 const int32_t* __restrict__ roots,
                                 const int32_t* __restrict__ flag, uint8_t* __restrict__ out) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = root_of(roots, i);
@@ -877,6 +892,7 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
 __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
                              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
                              uint8_t* __restrict__ out) {
+  pdl_enter();
   const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(tissue) |
                      reinterpret_cast<uintptr_t>(out)) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
@@ -917,20 +933,20 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
   if (conn == 8)
-    k_ccl_tile<8, P><<<grid, 32 * kTileWarps, 0, ctx->stream>>>(
-        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags);
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<8, P>, grid, 32 * kTileWarps, 0, 
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
   else
-    k_ccl_tile<4, P><<<grid, 32 * kTileWarps, 0, ctx->stream>>>(
-        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags);
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<4, P>, grid, 32 * kTileWarps, 0, 
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
   RTG_LAUNCH("k_ccl_tile");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
-    if (conn == 8) k_ccl_seams<8><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, tiles_y - 1, roots);
-    else k_ccl_seams<4><<<g, 256, 0, ctx->stream>>>((int)h, (int)w, tiles_y - 1, roots);
+    if (conn == 8) RTG_CUDA(launch_k(ctx, k_ccl_seams<8>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
+    else RTG_CUDA(launch_k(ctx, k_ccl_seams<4>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
     RTG_LAUNCH("k_ccl_seams");
   }
-  k_ccl_flatten<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts,
-                                                           flags, bitmap);
+  RTG_CUDA(launch_k(ctx, k_ccl_flatten, ctx->num_sms * 4, 256, 0, ctx->lroots, lcount, roots,
+                    counts, flags, bitmap, false));
   RTG_LAUNCH("k_ccl_flatten");
   return RTG_OK;
 }
@@ -951,7 +967,7 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
   const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
   RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr));
-  k_seeded_and<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag, tissue, out);
+  RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out));
   RTG_LAUNCH("k_seeded_and");
   return RTG_OK;
 }
@@ -969,16 +985,16 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   int32_t* cnt = ctx->scan_buf;
   int32_t* off = ctx->scan_buf + nchunks;
   int32_t* rank = ctx->i32c;
-  k_bm_count<<<nchunks, 256, 0, ctx->stream>>>(nwords, ctx->root_bm, cnt);
+  RTG_CUDA(launch_k(ctx, k_bm_count, nchunks, 256, 0, nwords, ctx->root_bm, cnt));
   RTG_LAUNCH("k_bm_count");
-  k_scan_chunks<<<1, 1024, 0, ctx->stream>>>(nchunks, cnt, off, d_n);
+  RTG_CUDA(launch_k(ctx, k_scan_chunks, 1, 1024, 0, nchunks, cnt, off, d_n));
   RTG_LAUNCH("k_scan_chunks");
-  k_bm_prefix<<<nchunks, 256, 0, ctx->stream>>>(nwords, ctx->root_bm, off, ctx->root_wprefix);
+  RTG_CUDA(launch_k(ctx, k_bm_prefix, nchunks, 256, 0, nwords, ctx->root_bm, off, ctx->root_wprefix));
   RTG_LAUNCH("k_bm_prefix");
-  k_root_rank<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->lroots, ctx->misc + 8, roots,
-                                                         ctx->root_bm, ctx->root_wprefix, rank);
+  RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
+                                                         ctx->root_bm, ctx->root_wprefix, rank));
   RTG_LAUNCH("k_root_rank");
-  k_relabel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, rank, labels);
+  RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
   return RTG_OK;
 }
@@ -986,8 +1002,8 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
                 int32_t max_area, int32_t* counts, uint8_t* out) {
   // counts were accumulated at the global roots by ccl_roots(..., counts)
-  k_area_filter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, counts, min_area,
-                                                         max_area, out);
+  RTG_CUDA(launch_k(ctx, k_area_filter, grid_for(ctx, n), 256, 0, n, roots, counts, min_area,
+                                                         max_area, out));
   RTG_LAUNCH("k_area_filter");
   return RTG_OK;
 }
@@ -1003,23 +1019,23 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
-  k_ccl_tile_fb<<<(unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, ctx->stream>>>(
-      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts);
+  RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 
+      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts));
   RTG_LAUNCH("k_ccl_tile_fb");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
-    k_ccl_seams_fb<<<g, 256, 0, ctx->stream>>>(cand, (int)h, (int)w, tiles_y - 1, roots);
+    RTG_CUDA(launch_k(ctx, k_ccl_seams_fb, g, 256, 0, cand, (int)h, (int)w, tiles_y - 1, roots));
     RTG_LAUNCH("k_ccl_seams_fb");
   }
   const int gl = ctx->num_sms * 4;
-  k_ccl_flatten<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, nullptr, nullptr,
-                                             true);
+  RTG_CUDA(launch_k(ctx, k_ccl_flatten, gl, 256, 0, ctx->lroots, lcount, roots, counts,
+                    (int32_t*)nullptr, (uint32_t*)nullptr, true));
   RTG_LAUNCH("k_ccl_flatten");
   prof_mark(ctx, RTG_STAGE_AREA);  // enclosure tree, subtree areas, filter
-  k_fb_tree<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, cand, (int)w, roots, counts, top,
-                                         total);
+  RTG_CUDA(launch_k(ctx, k_fb_tree, gl, 256, 0, ctx->lroots, lcount, cand, (int)w, roots, counts, top,
+                                         total));
   RTG_LAUNCH("k_fb_tree");
-  k_fb_total<<<gl, 256, 0, ctx->stream>>>(ctx->lroots, lcount, roots, counts, top, total);
+  RTG_CUDA(launch_k(ctx, k_fb_total, gl, 256, 0, ctx->lroots, lcount, roots, counts, top, total));
   RTG_LAUNCH("k_fb_total");
   uint32_t* bits_base = ctx->fg_bits;
   RTG_CUDA(cudaMemsetAsync(ctx->misc + 4, 0, sizeof(int32_t), ctx->stream));
@@ -1028,8 +1044,8 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
                            ctx->stream));
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
-  k_fb_filter<<<blocks, 256, 0, ctx->stream>>>(n, roots, top, total, min_area, max_area, out,
-                                               bits_base + kBitPad, ctx->fg_list, ctx->misc + 4);
+  RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, top, total, min_area, max_area, out,
+                                               bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
   RTG_LAUNCH("k_fb_filter");
   return RTG_OK;
 }
@@ -1042,7 +1058,7 @@ int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8_
   int32_t* flag = ctx->i32b;
   RTG_TRY(ccl_run(ctx, FgBackground{bin, (int)h, (int)w}, h, w, 4, roots, nullptr, flag,
                   nullptr));
-  k_fill_uf_final<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, bin, roots, flag, out);
+  RTG_CUDA(launch_k(ctx, k_fill_uf_final, grid_for(ctx, n), 256, 0, n, bin, roots, flag, out));
   RTG_LAUNCH("k_fill_uf_final");
   return RTG_OK;
 }

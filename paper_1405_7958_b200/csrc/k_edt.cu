@@ -40,6 +40,7 @@ constexpr int kCap = 96;
 __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
                           uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero,
                           const int32_t* __restrict__ gate) {
+  pdl_enter();
   if (gate && !*gate) return;
   // grid-stride over (segment, 128-column block) pairs: a capped grid keeps
   // the gated (normally empty) launch cheap
@@ -66,6 +67,7 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
 __global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
                           const uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
                           const int32_t* __restrict__ gate) {
+  pdl_enter();
   if (gate && !*gate) return;
   const int nbx = (w + blockDim.x - 1) / blockDim.x, nseg = (h + kSeg - 1) / kSeg;
   for (int blk = blockIdx.x; blk < nbx * nseg; blk += gridDim.x) {
@@ -126,6 +128,7 @@ k_edt_row(const uint16_t* __restrict__ g, int h, int w,
           const int32_t* __restrict__ any_zero, int32_t* __restrict__ dist2,
           uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
           int32_t* __restrict__ row_flag, const int32_t* __restrict__ gate) {
+  pdl_enter();
   extern __shared__ uint16_t gs[];
   if (gate && !*gate) return;  // k_edt_row_exact checks the same gate
   const bool none = *any_zero == 0;
@@ -176,6 +179,7 @@ __global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
                                 uint16_t* __restrict__ mk, int32_t ws_h,
                                 uint32_t* __restrict__ status,
                                 const int32_t* __restrict__ gate = nullptr) {
+  pdl_enter();
   if (gate && !*gate) return;
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
   if (y >= h || !row_flag[y]) return;
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(256)
 k_edt_tile(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__ dist2,
            uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
            int32_t* __restrict__ need_full) {
+  pdl_enter();
   __shared__ uint32_t colw[kEW][3];       // bit r of word k: window row 32k + r is background
   __shared__ uint8_t gdn[kET][kEW + 4];   // tile row -> nearest background row below / above
   __shared__ uint8_t gup[kET][kEW + 4];   //   (255: none in the window)
@@ -341,6 +346,7 @@ k_edt_tile(const uint8_t* __restrict__ mask, int h, int w, int32_t* __restrict__
 __global__ void __launch_bounds__(256)
 k_fg_list(const uint8_t* __restrict__ mask, int64_t n, uint32_t* __restrict__ bits,
           int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  pdl_enter();
   __shared__ int32_t sm[9];
   const bool vec = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
   for (int64_t b0 = (int64_t)blockIdx.x * 4096; b0 < n; b0 += (int64_t)gridDim.x * 4096) {
@@ -390,6 +396,7 @@ __device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ 
 __global__ void __launch_bounds__(256)
 k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
               const uint32_t* __restrict__ bits, FastDiv dw, uint8_t* __restrict__ hd) {
+  pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -409,6 +416,7 @@ k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
            const uint8_t* __restrict__ mask, const uint8_t* __restrict__ hd, int h, FastDiv dw,
            int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
            int32_t* __restrict__ need_full) {
+  pdl_enter();
   constexpr uint32_t kR = 32;
   const int w = (int)dw.d;
   const int n = *count;
@@ -449,24 +457,24 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* row_flag = ctx->misc + 64;  // h entries
   RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));  // + need_full
   const dim3 tiles((unsigned)ceil_div(w, kET), (unsigned)ceil_div(h, kET));
-  k_edt_tile<<<tiles, 256, 0, ctx->stream>>>(mask, (int)h, (int)w, dist2, dq, mk, ws_h,
-                                             need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_tile, tiles, 256, 0, mask, (int)h, (int)w, dist2, dq, mk, ws_h,
+                                             need_full));
   RTG_LAUNCH("k_edt_tile");
   // exact whole-tile pass, gated on need_full (empty launches otherwise)
   const int64_t gblk = ceil_div(w, 128) * nseg;
   const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
-  k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_seg, gs, 128, 0, mask, (int)h, (int)w, seg, any_zero, need_full));
   RTG_LAUNCH("k_edt_seg");
-  k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_col, gs, 128, 0, mask, (int)h, (int)w, seg, g, need_full));
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
   const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
-  k_edt_row<<<grows, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, dist2,
-                                                      dq, mk, ws_h, row_flag, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_row, grows, 256, smem, g, (int)h, (int)w, any_zero, dist2,
+                                                      dq, mk, ws_h, row_flag, need_full));
   RTG_LAUNCH("k_edt_row");
-  k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
+  RTG_CUDA(launch_k(ctx, k_edt_row_exact, (unsigned)ceil_div(h, 128), 128, 0, 
       g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, dist2, dq, mk, ws_h, ctx->status,
-      need_full);
+      need_full));
   RTG_LAUNCH("k_edt_row_exact");
   return RTG_OK;
 }
@@ -485,7 +493,7 @@ int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* li
                            ctx->stream));
   int blocks = (int)ceil_div(n, 4096);
   if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
-  k_fg_list<<<blocks, 256, 0, ctx->stream>>>(mask, n, bits_base + kBitPad, list, count);
+  RTG_CUDA(launch_k(ctx, k_fg_list, blocks, 256, 0, mask, n, bits_base + kBitPad, list, count));
   RTG_LAUNCH("k_fg_list");
   return RTG_OK;
 }
@@ -501,26 +509,26 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));
   uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
   const FastDiv dwv = make_div((uint32_t)w);
-  k_edt_rowdist<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, bits_base + kBitPad, dwv,
-                                                           hd);
+  RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,
+                                                           hd));
   RTG_LAUNCH("k_edt_rowdist");
-  k_edt_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, count, mask, hd, (int)h, dwv,
-                                                        nullptr, dq, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, mask, hd, (int)h, dwv,
+                                                        nullptr, dq, need_full));
   RTG_LAUNCH("k_edt_list");
   const int64_t gblk = ceil_div(w, 128) * nseg;
   const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
-  k_edt_seg<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, any_zero, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_seg, gs, 128, 0, mask, (int)h, (int)w, seg, any_zero, need_full));
   RTG_LAUNCH("k_edt_seg");
-  k_edt_col<<<gs, 128, 0, ctx->stream>>>(mask, (int)h, (int)w, seg, g, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_col, gs, 128, 0, mask, (int)h, (int)w, seg, g, need_full));
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
   const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
-  k_edt_row<<<grows, 256, smem, ctx->stream>>>(g, (int)h, (int)w, any_zero, nullptr, dq,
-                                                      nullptr, 0, row_flag, need_full);
+  RTG_CUDA(launch_k(ctx, k_edt_row, grows, 256, smem, g, (int)h, (int)w, any_zero, nullptr, dq,
+                                                      nullptr, 0, row_flag, need_full));
   RTG_LAUNCH("k_edt_row");
-  k_edt_row_exact<<<(unsigned)ceil_div(h, 128), 128, 0, ctx->stream>>>(
+  RTG_CUDA(launch_k(ctx, k_edt_row_exact, (unsigned)ceil_div(h, 128), 128, 0, 
       g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, nullptr, dq, nullptr, 0, ctx->status,
-      need_full);
+      need_full));
   RTG_LAUNCH("k_edt_row_exact");
   return RTG_OK;
 }

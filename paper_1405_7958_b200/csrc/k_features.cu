@@ -16,6 +16,7 @@ namespace rtg {
 namespace {
 
 __global__ void k_feat_clear(const int32_t* __restrict__ d_n, FeatureAcc acc) {
+  pdl_enter();
   const int n = min(*d_n, acc.cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
 #pragma unroll
@@ -125,6 +126,7 @@ __device__ __forceinline__ uint32_t isqrt_small(uint32_t v) {  // v < 2^26
 __global__ void __launch_bounds__(256)
 k_feat_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
              int h, int w, const int32_t* __restrict__ d_n, FeatureAcc acc) {
+  pdl_enter();
   __shared__ FeatTable T;
   __shared__ int32_t SL[kHalo][kHalo];
   __shared__ uint8_t SI[kHalo][kHalo + 2];
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(256)
 k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, FastDiv dw,
             const int32_t* __restrict__ d_n, FeatureAcc acc) {
+  pdl_enter();
   const unsigned full = 0xFFFFFFFFu;
   const int w = (int)dw.d;
   const int nobj = min(*d_n, acc.cap);
@@ -338,6 +341,7 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
 // (oracle/rtg_oracle.c orc_features) term by term.
 __global__ void k_feat_finalize(const int32_t* __restrict__ d_n, FeatureAcc acc,
                                 float* __restrict__ out, uint32_t* __restrict__ status) {
+  pdl_enter();
   const int n_all = *d_n;
   if (n_all > acc.cap && blockIdx.x == 0 && threadIdx.x == 0)
     atomicOr(status, kStatusObjectOverflow);
@@ -400,21 +404,21 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              const int32_t* list_count) {
   const int cap = ctx->acc.cap;
   const int gclear = (int)ceil_div(cap, 256);
-  k_feat_clear<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc);
+  RTG_CUDA(launch_k(ctx, k_feat_clear, gclear, 256, 0, d_n, ctx->acc));
   RTG_LAUNCH("k_feat_clear");
   // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
   if (list && h <= 4096 && w <= 4096) {
-    k_feat_list<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(list, list_count, labels, intensity,
+    RTG_CUDA(launch_k(ctx, k_feat_list, ctx->num_sms * 8, 256, 0, list, list_count, labels, intensity,
                                                            (int)h, make_div((uint32_t)w), d_n,
-                                                           ctx->acc);
+                                                           ctx->acc));
     RTG_LAUNCH("k_feat_list");
   } else {
     const dim3 grid((unsigned)ceil_div(w, kFB), (unsigned)ceil_div(h, kFB));
-    k_feat_accum<<<grid, 256, 0, ctx->stream>>>(labels, intensity, (int)h, (int)w, d_n,
-                                                ctx->acc);
+    RTG_CUDA(launch_k(ctx, k_feat_accum, grid, 256, 0, labels, intensity, (int)h, (int)w, d_n,
+                                                ctx->acc));
     RTG_LAUNCH("k_feat_accum");
   }
-  k_feat_finalize<<<gclear, 256, 0, ctx->stream>>>(d_n, ctx->acc, out, ctx->status);
+  RTG_CUDA(launch_k(ctx, k_feat_finalize, gclear, 256, 0, d_n, ctx->acc, out, ctx->status));
   RTG_LAUNCH("k_feat_finalize");
   return RTG_OK;
 }

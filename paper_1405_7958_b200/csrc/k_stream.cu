@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256)
 k_colordeconv_vec(const uint4* __restrict__ rgb, int64_t ngroups,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
                   uint4* __restrict__ marker, uint4* __restrict__ tissue) {
+  pdl_enter();
   __shared__ int32_t lut[3][256];
   for (int i = threadIdx.x; i < 768; i += blockDim.x)
     lut[i >> 8][i & 255] = p.lut.v[i >> 8][i & 255];
@@ -78,6 +79,7 @@ k_colordeconv_px(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
                  int64_t pitch, int64_t first, const __grid_constant__ CdParams p,
                  uint8_t* __restrict__ hema, uint8_t* __restrict__ marker,
                  uint8_t* __restrict__ tissue) {
+  pdl_enter();
   __shared__ int32_t lut[3][256];
   for (int i = threadIdx.x; i < 768; i += blockDim.x)
     lut[i >> 8][i & 255] = p.lut.v[i >> 8][i & 255];
@@ -100,6 +102,7 @@ k_colordeconv_px(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
 __global__ void __launch_bounds__(256)
 k_candidate(const uint4* __restrict__ recon, const uint4* __restrict__ tissue,
             int64_t ngroups, uint32_t thresh, uint4* __restrict__ out) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
        g += stride) {
@@ -120,6 +123,7 @@ k_candidate(const uint4* __restrict__ recon, const uint4* __restrict__ tissue,
 __global__ void k_candidate_tail(const uint8_t* recon, const uint8_t* tissue,
                                  int64_t first, int64_t n, int32_t thresh,
                                  uint8_t* out) {
+  pdl_enter();
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (uint8_t)(recon[i] >= thresh && tissue[i]);
 }
@@ -159,10 +163,10 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
     if (ngroups > 0) {
       const int64_t want = ceil_div(ngroups, 256);
       const int blocks = (int)(want < (int64_t)ctx->num_sms * 8 ? want : (int64_t)ctx->num_sms * 8);
-      k_colordeconv_vec<<<blocks, 256, 0, ctx->stream>>>(
+      RTG_CUDA(launch_k(ctx, k_colordeconv_vec, blocks, 256, 0, 
           reinterpret_cast<const uint4*>(rgb), ngroups, cp,
           reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-          reinterpret_cast<uint4*>(tissue));
+          reinterpret_cast<uint4*>(tissue)));
       RTG_LAUNCH("k_colordeconv_vec");
     }
     done = ngroups * 16;
@@ -171,8 +175,8 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
     const int64_t rem = n - done;
     const int64_t want = ceil_div(rem, 256);
     const int blocks = (int)(want < (int64_t)ctx->num_sms * 16 ? want : (int64_t)ctx->num_sms * 16);
-    k_colordeconv_px<<<blocks, 256, 0, ctx->stream>>>(rgb, h, w, pitch, done, cp,
-                                                      hema, marker, tissue);
+    RTG_CUDA(launch_k(ctx, k_colordeconv_px, blocks, 256, 0, rgb, h, w, pitch, done, cp,
+                                                      hema, marker, tissue));
     RTG_LAUNCH("k_colordeconv_px");
   }
   return RTG_OK;
@@ -188,18 +192,18 @@ int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
       const int blocks = (int)(want < (int64_t)ctx->num_sms * 8 ? want : (int64_t)ctx->num_sms * 8);
       const uint32_t t = thresh < 0 ? 0u : thresh > 255 ? 256u : (uint32_t)thresh;
       if (t <= 255) {
-        k_candidate<<<blocks, 256, 0, ctx->stream>>>(
+        RTG_CUDA(launch_k(ctx, k_candidate, blocks, 256, 0, 
             reinterpret_cast<const uint4*>(recon),
             reinterpret_cast<const uint4*>(tissue), ngroups, t,
-            reinterpret_cast<uint4*>(out));
+            reinterpret_cast<uint4*>(out)));
         RTG_LAUNCH("k_candidate");
         done = ngroups * 16;
       }
     }
   }
   if (done < n) {
-    k_candidate_tail<<<(unsigned)ceil_div(n - done, 256), 256, 0, ctx->stream>>>(
-        recon, tissue, done, n, thresh, out);
+    RTG_CUDA(launch_k(ctx, k_candidate_tail, (unsigned)ceil_div(n - done, 256), 256, 0, 
+        recon, tissue, done, n, thresh, out));
     RTG_LAUNCH("k_candidate_tail");
   }
   return RTG_OK;

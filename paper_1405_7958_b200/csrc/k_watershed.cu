@@ -38,6 +38,7 @@ constexpr int32_t kCountMask = kSeeded - 1;
 
 __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
                           const uint16_t* __restrict__ F, uint16_t* __restrict__ Fw) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     Fw[i] = (uint16_t)(mask[i] ? (uint32_t)F[i] + 1u : 0u);
@@ -85,6 +86,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
             int32_t* __restrict__ ptr, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
+  pdl_enter();
   const int w = (int)dw.d;
   __shared__ int32_t sm[9];
   const int n = *count;
@@ -128,6 +130,7 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                            const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count, int32_t* __restrict__ ptr,
                            int32_t* par) {
+  pdl_enter();
   const int w = (int)dw.d;
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -159,6 +162,7 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count,
                            const int32_t* __restrict__ ptr, int32_t* par, int32_t* cnt,
                            int32_t* __restrict__ slot) {
+  pdl_enter();
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
@@ -177,6 +181,7 @@ k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__
               const int32_t* __restrict__ par, int32_t* cnt, int32_t* __restrict__ ptr,
               unsigned long long* alloc,
               int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+  pdl_enter();
   __shared__ unsigned long long sm[9];
   const int n = *flat_count;
   for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
@@ -207,6 +212,7 @@ __global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
                              const int32_t* __restrict__ flat_count,
                              const int32_t* __restrict__ par, const int32_t* __restrict__ cnt,
                              const int32_t* __restrict__ slot, int32_t* __restrict__ members) {
+  pdl_enter();
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
@@ -275,6 +281,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              int32_t* __restrict__ ptr, int32_t* delta, int2* __restrict__ scratch) {
+  pdl_enter();
   const int w = (int)dw.d;
   constexpr int kPer = 4;
   const int nmem = (int)(*alloc & 0xFFFFFFFFull);
@@ -383,6 +390,7 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
             int32_t* __restrict__ scount) {
+  pdl_enter();
   const int w = (int)dw.d;
   __shared__ int32_t sm[9];
   const int n = *count;
@@ -419,6 +427,7 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mas
                              const uint8_t* __restrict__ sflag,
                              const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                              int32_t* par) {
+  pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -439,6 +448,7 @@ __global__ void __launch_bounds__(256)
 k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
              const int32_t* __restrict__ par, int32_t* cnt, unsigned long long* alloc,
              int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+  pdl_enter();
   __shared__ unsigned long long sm[9];
   const int n = *count;
   for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
@@ -487,6 +497,7 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag, int32_t ws_h,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint16_t* Fw, int2* __restrict__ scratch) {
+  pdl_enter();
   const int w = (int)dw.d;
   constexpr int kPer = 4;
   const int nmem = (int)(*alloc & 0xFFFFFFFFull);
@@ -574,6 +585,7 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 __global__ void k_ws_basins(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                             const int32_t* __restrict__ ptr, const int32_t* __restrict__ par,
                             int32_t* __restrict__ basin) {
+  pdl_enter();
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int32_t q = list[k];
@@ -593,6 +605,7 @@ __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ lis
                               const int32_t* __restrict__ count,
                               const uint32_t* __restrict__ mask,
                               const int32_t* __restrict__ basin, uint8_t* __restrict__ sep) {
+  pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -647,7 +660,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   if (iwpp_hmax) {
     RTG_TRY(iwpp_recon_u16(ctx, F, dq, h, w, 8));  // HMAX
     Fw = ctx->u16a;                                 // dq is dead now
-    k_ws_prep<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, mask, F, Fw);
+    RTG_CUDA(launch_k(ctx, k_ws_prep, grid_for(ctx, n), 256, 0, n, mask, F, Fw));
     RTG_LAUNCH("k_ws_prep");
   } else {
     Fw = F;
@@ -658,20 +671,20 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     uint8_t* sflag = ctx->m1;
     RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
     RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-    k_hmax_init<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
-                                            par, basin, list, count);
+    RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
+                                            par, basin, list, count));
     RTG_LAUNCH("k_hmax_init");
-    k_hmax_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, sflag, list, count, par);
+    RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)h, dwv, fgbits, sflag, list, count, par));
     RTG_LAUNCH("k_hmax_union");
-    k_ws_roots<<<g, 256, 0, ctx->stream>>>(list, count, nullptr, par, basin, slot);
+    RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, list, count, nullptr, par, basin, slot));
     RTG_LAUNCH("k_ws_roots");
-    k_hmax_alloc<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, alloc, comp_root,
-                                             comp_size);
+    RTG_CUDA(launch_k(ctx, k_hmax_alloc, g, 256, 0, list, count, par, basin, alloc, comp_root,
+                                             comp_size));
     RTG_LAUNCH("k_hmax_alloc");
-    k_ws_scatter<<<g, 256, 0, ctx->stream>>>(list, count, par, basin, slot, ctx->lroots);
+    RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, list, count, par, basin, slot, ctx->lroots));
     RTG_LAUNCH("k_ws_scatter");
-    k_hmax_solve<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
-                                             alloc, Fw, member_scratch);
+    RTG_CUDA(launch_k(ctx, k_hmax_solve, g, 256, 0, (int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
+                                             alloc, Fw, member_scratch));
     RTG_LAUNCH("k_hmax_solve");
   }
   prof_mark(ctx, RTG_STAGE_WATERSHED);
@@ -682,26 +695,26 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* flat_count = ctx->misc + 1;
   RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
   RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
-  k_ws_arrows<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, Fw, ptr, par, basin,
-                                          flat, ctx->flat_list, flat_count);
+  RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, ptr, par, basin,
+                                          flat, ctx->flat_list, flat_count));
   RTG_LAUNCH("k_ws_arrows");
-  k_ws_union<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
-                                         flat_count, ptr, par);
+  RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
+                                         flat_count, ptr, par));
   RTG_LAUNCH("k_ws_union");
-  k_ws_roots<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, ptr, par, basin, delta);
+  RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, ptr, par, basin, delta));
   RTG_LAUNCH("k_ws_roots");
-  k_ws_classify<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, ptr, alloc,
-                                            comp_root, comp_size);
+  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, ptr, alloc,
+                                            comp_root, comp_size));
   RTG_LAUNCH("k_ws_classify");
-  k_ws_scatter<<<g, 256, 0, ctx->stream>>>(ctx->flat_list, flat_count, par, basin, delta,
-                                           ctx->lroots);
+  RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
+                                           ctx->lroots));
   RTG_LAUNCH("k_ws_scatter");
-  k_ws_plateau<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, ptr,
-                                           delta, member_scratch);
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, ptr,
+                                           delta, member_scratch));
   RTG_LAUNCH("k_ws_plateau");
-  k_ws_basins<<<g, 256, 0, ctx->stream>>>(fgl, fgn, ptr, par, basin);
+  RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, fgl, fgn, ptr, par, basin));
   RTG_LAUNCH("k_ws_basins");
-  k_ws_separate<<<g, 256, 0, ctx->stream>>>((int)h, dwv, fgl, fgn, fgbits, basin, sep);
+  RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, basin, sep));
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
 }

@@ -171,7 +171,8 @@ int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int
                               (int64_t)d_hema, (int64_t)d_features, (int64_t)d_n,
                               (int64_t)ctx->fill_impl, (int64_t)ctx->stream,
                               (int64_t)ctx->recon_impl | ((int64_t)ctx->ws_impl << 8) |
-                                  ((int64_t)ctx->hmax_impl << 16)};
+                                  ((int64_t)ctx->hmax_impl << 16) |
+                                  ((int64_t)ctx->use_pdl << 24)};
   std::memcpy(&key[0], fields, sizeof(fields));
   std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
   if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
@@ -531,6 +532,9 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
     case RTG_OPT_WATERSHED_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "watershed impl must be 0 or 1");
       ctx->ws_impl = (int)value;
+      return RTG_OK;
+    case RTG_OPT_PDL:
+      ctx->use_pdl = value != 0;
       return RTG_OK;
     case RTG_OPT_HMAX_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "hmax impl must be 0 or 1");
