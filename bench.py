@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pdl", action="store_true",
+                    help="programmatic dependent launch between kernels (A/B; off by default)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -238,6 +240,9 @@ def main():
     cap = 32768
     params = rtg.default_params()
     ctxs = [rtg.Context(local, TILE, TILE, cap) for _ in range(S)]
+    if args.pdl:
+        for c in ctxs:
+            c.set_option(rtg.OPT_PDL, 1)
     ext = [torch.cuda.ExternalStream(c.stream()) for c in ctxs]
     my_tiles = rank_tiles(rank, T)
     px_rank = sum(h * w for (_, _, h, w) in my_tiles)

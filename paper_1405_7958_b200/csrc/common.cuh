@@ -140,7 +140,7 @@ struct rtg_ctx {
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
-  int use_pdl = 1;    // programmatic dependent launch between the stage's kernels
+  int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
   struct GraphEntry {
@@ -175,6 +175,14 @@ int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w);
 // stage >= 0 starts that stage, -1 closes the current one.
 void prof_mark(rtg_ctx* ctx, int stage);
 void hema_lut(const rtg_params* p, HemaLut* lut);
+
+// Zeroes up to four device regions with one kernel of the launch chain.
+struct ZeroList {
+  void* ptr[4];
+  uint64_t bytes[4];
+  int count;
+};
+int zero_async(rtg_ctx* ctx, const ZeroList& z);
 
 // ---- launchers (one translation unit each) ---------------------------------
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,

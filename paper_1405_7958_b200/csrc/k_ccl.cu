@@ -925,10 +925,10 @@ template <class P>
 int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
             int32_t* counts, int32_t* flags, uint32_t* bitmap) {
   int32_t* lcount = ctx->misc + 8;
-  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
-  if (bitmap)
-    RTG_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)ceil_div(h * w, 32),
-                             ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{lcount, bitmap},
+                                    {sizeof(int32_t),
+                                     bitmap ? sizeof(uint32_t) * (size_t)ceil_div(h * w, 32) : 0},
+                                    2}));
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
@@ -1016,7 +1016,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   int32_t* top = ctx->i32c;
   int32_t* total = ctx->labels;
   int32_t* lcount = ctx->misc + 8;
-  RTG_CUDA(cudaMemsetAsync(lcount, 0, sizeof(int32_t), ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{lcount}, {sizeof(int32_t)}, 1}));
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 
@@ -1038,10 +1038,10 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_CUDA(launch_k(ctx, k_fb_total, gl, 256, 0, ctx->lroots, lcount, roots, counts, top, total));
   RTG_LAUNCH("k_fb_total");
   uint32_t* bits_base = ctx->fg_bits;
-  RTG_CUDA(cudaMemsetAsync(ctx->misc + 4, 0, sizeof(int32_t), ctx->stream));
-  RTG_CUDA(cudaMemsetAsync(bits_base, 0, sizeof(uint32_t) * kBitPad, ctx->stream));
-  RTG_CUDA(cudaMemsetAsync(bits_base + kBitPad + n / 32, 0, sizeof(uint32_t) * (kBitPad + 1),
-                           ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{ctx->misc + 4, bits_base, bits_base + kBitPad + n / 32},
+                                    {sizeof(int32_t), sizeof(uint32_t) * kBitPad,
+                                     sizeof(uint32_t) * (kBitPad + 1)},
+                                    3}));
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
   RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, top, total, min_area, max_area, out,

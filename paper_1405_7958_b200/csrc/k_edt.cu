@@ -455,7 +455,7 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* any_zero = ctx->misc + 2;
   int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;  // h entries
-  RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));  // + need_full
+  RTG_TRY(zero_async(ctx, ZeroList{{any_zero}, {2 * sizeof(int32_t)}, 1}));  // + need_full
   const dim3 tiles((unsigned)ceil_div(w, kET), (unsigned)ceil_div(h, kET));
   RTG_CUDA(launch_k(ctx, k_edt_tile, tiles, 256, 0, mask, (int)h, (int)w, dist2, dq, mk, ws_h,
                                              need_full));
@@ -486,11 +486,11 @@ namespace rtg {
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base) {
   const int64_t n = h * w;
-  RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
-  // zero pads (the words past the image end are partly written by the ballots)
-  RTG_CUDA(cudaMemsetAsync(bits_base, 0, sizeof(uint32_t) * kBitPad, ctx->stream));
-  RTG_CUDA(cudaMemsetAsync(bits_base + kBitPad + n / 32, 0, sizeof(uint32_t) * (kBitPad + 1),
-                           ctx->stream));
+  // count + pads (the words past the image end are partly written by the ballots)
+  RTG_TRY(zero_async(ctx, ZeroList{{count, bits_base, bits_base + kBitPad + n / 32},
+                                    {sizeof(int32_t), sizeof(uint32_t) * kBitPad,
+                                     sizeof(uint32_t) * (kBitPad + 1)},
+                                    3}));
   int blocks = (int)ceil_div(n, 4096);
   if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
   RTG_CUDA(launch_k(ctx, k_fg_list, blocks, 256, 0, mask, n, bits_base + kBitPad, list, count));
@@ -506,7 +506,7 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   int32_t* any_zero = ctx->misc + 2;
   int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;
-  RTG_CUDA(cudaMemsetAsync(any_zero, 0, 2 * sizeof(int32_t), ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{any_zero}, {2 * sizeof(int32_t)}, 1}));
   uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
   const FastDiv dwv = make_div((uint32_t)w);
   RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,

@@ -130,6 +130,26 @@ __global__ void k_candidate_tail(const uint8_t* recon, const uint8_t* tissue,
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// Up to four regions zeroed by one PDL-launched kernel (a cudaMemsetAsync
+// node would cut the programmatic overlap of the kernel chain).
+__global__ void __launch_bounds__(256) k_zero(ZeroList z) {
+  pdl_enter();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < z.count; ++r) {
+    uint8_t* p = static_cast<uint8_t*>(z.ptr[r]);
+    const int64_t n = (int64_t)z.bytes[r];
+    int64_t done = 0;
+    if (((uintptr_t)p & 15u) == 0) {
+      const int64_t n16 = n / 16;
+      uint4* q = reinterpret_cast<uint4*>(p);
+      for (int64_t i = tid; i < n16; i += nth) q[i] = make_uint4(0, 0, 0, 0);
+      done = n16 * 16;
+    }
+    for (int64_t i = done + tid; i < n; i += nth) p[i] = 0;
+  }
+}
+
 }  // namespace
 
 void hema_lut(const rtg_params* p, HemaLut* lut) {
@@ -179,6 +199,16 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                                                       hema, marker, tissue));
     RTG_LAUNCH("k_colordeconv_px");
   }
+  return RTG_OK;
+}
+
+int zero_async(rtg_ctx* ctx, const ZeroList& z) {
+  int64_t big = 0;
+  for (int r = 0; r < z.count; ++r) big = big > (int64_t)z.bytes[r] ? big : (int64_t)z.bytes[r];
+  int64_t blocks = ceil_div(big / 16 + 1, 256);
+  if (blocks > ctx->num_sms * 4) blocks = ctx->num_sms * 4;
+  RTG_CUDA(launch_k(ctx, k_zero, dim3((unsigned)blocks), dim3(256), 0, z));
+  RTG_LAUNCH("k_zero");
   return RTG_OK;
 }
 

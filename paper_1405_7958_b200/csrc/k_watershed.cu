@@ -644,8 +644,9 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // per-member cache of long component ranges (the arena's second half)
   int2* member_scratch = reinterpret_cast<int2*>(ctx->arena + 8 * n);
   auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
-  RTG_CUDA(cudaMemsetAsync(sep, 0, (size_t)n, ctx->stream));
-  if (want_basin) RTG_CUDA(cudaMemsetAsync(basin, 0, sizeof(int32_t) * (size_t)n, ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{sep, basin},
+                                    {(size_t)n, want_basin ? sizeof(int32_t) * (size_t)n : 0},
+                                    2}));
   prof_mark(ctx, RTG_STAGE_EDT);
   if (!list_ready) RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
   const uint32_t* fgbits = ctx->fg_bits + kBitPad;  // neighbour tests of the list kernels
@@ -669,8 +670,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     int32_t* par = ctx->i32c;
     int32_t* slot = ctx->i32b;
     uint8_t* sflag = ctx->m1;
-    RTG_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), ctx->stream));
-    RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
+    RTG_TRY(zero_async(ctx, ZeroList{{count, alloc},
+                                      {sizeof(int32_t), sizeof(unsigned long long)}, 2}));
     RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
                                             par, basin, list, count));
     RTG_LAUNCH("k_hmax_init");
@@ -693,8 +694,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* par = ctx->i32c;
   uint8_t* flat = ctx->m1;
   int32_t* flat_count = ctx->misc + 1;
-  RTG_CUDA(cudaMemsetAsync(flat_count, 0, sizeof(int32_t), ctx->stream));
-  RTG_CUDA(cudaMemsetAsync(alloc, 0, sizeof(unsigned long long), ctx->stream));
+  RTG_TRY(zero_async(ctx, ZeroList{{flat_count, alloc},
+                                    {sizeof(int32_t), sizeof(unsigned long long)}, 2}));
   RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, ptr, par, basin,
                                           flat, ctx->flat_list, flat_count));
   RTG_LAUNCH("k_ws_arrows");

@@ -49,7 +49,7 @@ OPT_USE_GRAPHS = 1       # 1 replay cached CUDA graphs in process_tile_dev (defa
 OPT_RECON_IMPL = 2       # 0 threshold decomposition (default), 1 grayscale IWPP
 OPT_WATERSHED_IMPL = 3   # 0 tiled whole-tile passes (default), 1 object-parallel
 OPT_HMAX_IMPL = 4        # 0 sparse components (default), 1 IWPP tile queue
-OPT_PDL = 5              # 1 programmatic dependent launch between kernels (default), 0 off
+OPT_PDL = 5              # 1 programmatic dependent launch between kernels, 0 off (default)
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features"]
 

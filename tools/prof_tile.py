@@ -14,12 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--tiles", type=int, default=2)
 ap.add_argument("--passes", type=int, default=2)
 ap.add_argument("--size", type=int, default=4096)
-ap.add_argument("--no-pdl", action="store_true")
+ap.add_argument("--pdl", action="store_true")
 a = ap.parse_args()
 h = w = a.size
 ctx = rtg.Context(0, h, w, 32768)
-if a.no_pdl:
-    ctx.set_option(rtg.OPT_PDL, 0)
+if a.pdl:
+    ctx.set_option(rtg.OPT_PDL, 1)
 p = rtg.default_params()
 rgbs = []
 for k in range(a.tiles):
