@@ -32,44 +32,111 @@ __device__ __forceinline__ void cd_pixel(const int32_t (*lut)[256],
   tis = (!bg && !rbc) ? 1u : 0u;
 }
 
-// Flat path: rgb is h*w*3 contiguous, 16-byte aligned; 16 px per thread.
-__global__ void __launch_bounds__(256)
-k_colordeconv_vec(const uint4* __restrict__ rgb, int64_t ngroups,
+// Flat path: rgb is h*w*3 contiguous, 16-byte aligned; 16 px per group.
+// Each thread owns `iters` groups strided by the grid and prefetches group
+// k+1 (3 x LDG.128, evict-first) before it computes group k; the first group
+// is in flight while the block stages the LUTs.  The three 16.16 LUTs (the
+// rounding constant folded into lut[0]) are replicated once per lane
+// (word v*32 + lane, 96 KB per CTA): every LDS of a warp hits 32 distinct
+// banks whatever the pixel values, where a shared 1 KB table averaged two
+// wavefronts per gather (profiles/r1_colordeconv_*).  Per pixel: 3 PRMT
+// byte extracts, 3 LEA + 3 LDS, one IADD3, the shift, and a saturating pack
+// (cvt.pack.sat) of 2 pixels per instruction; the tissue test is integer
+// min/max arithmetic on the same bytes (~22 instructions/px, was ~45).
+__device__ __forceinline__ uint32_t pack_sat_u8(int32_t v0, int32_t v1, int32_t v2,
+                                                int32_t v3) {
+  uint32_t hi, d;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(v3), "r"(v2));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(v1), "r"(v0), "r"(hi));
+  return d;
+}
+
+constexpr int kCdThreads = 512;
+constexpr int kCdBlocksPerSm = 2;
+constexpr size_t kCdSmem = 3 * 256 * 32 * sizeof(int32_t) + 3 * 256 * sizeof(int32_t);
+
+template <bool kMarker>
+__global__ void __launch_bounds__(kCdThreads, kCdBlocksPerSm)
+k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
                   uint4* __restrict__ marker, uint4* __restrict__ tissue) {
   pdl_enter();
-  __shared__ int32_t lut[3][256];
-  for (int i = threadIdx.x; i < 768; i += blockDim.x)
-    lut[i >> 8][i & 255] = p.lut.v[i >> 8][i & 255];
+  extern __shared__ __align__(16) int32_t cd_smem[];
+  int32_t* lrep = cd_smem;                   // [3][256][32]
+  int32_t* lsmall = cd_smem + 3 * 256 * 32;  // [3][256]
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a;
+  if (g < ngroups) {
+    a = __ldcs(rgb + 3 * g);
+    b = __ldcs(rgb + 3 * g + 1);
+    c = __ldcs(rgb + 3 * g + 2);
+  }
+  {
+    // 192 x 16-byte constant-bank reads (divergent LDC replays once per
+    // distinct address, so wide reads keep the staging short) ...
+    const int4* src = reinterpret_cast<const int4*>(&p.lut.v[0][0]);
+    int4* dst = reinterpret_cast<int4*>(lsmall);
+    for (int i = threadIdx.x; i < 192; i += blockDim.x) {
+      int4 v = src[i];
+      if (i < 64) {  // lut[0] carries the +32768 of the rounding shift
+        v.x += 32768; v.y += 32768; v.z += 32768; v.w += 32768;
+      }
+      dst[i] = v;
+    }
+    __syncthreads();
+    // ... then 32 lane copies of each entry, 16 bytes per store
+    int4* rep = reinterpret_cast<int4*>(lrep);
+    for (int i = threadIdx.x; i < 3 * 256 * 8; i += blockDim.x) {
+      const int32_t v = lsmall[i >> 3];
+      rep[i] = make_int4(v, v, v, v);
+    }
+  }
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
-       g += stride) {
-    uint32_t wv[12];
-    {
-      const uint4 a = __ldcs(rgb + 3 * g);
-      const uint4 b = __ldcs(rgb + 3 * g + 1);
-      const uint4 c = __ldcs(rgb + 3 * g + 2);
-      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
-      wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
-      wv[8] = c.x; wv[9] = c.y; wv[10] = c.z; wv[11] = c.w;
+  const int lane = threadIdx.x & 31;
+  const int32_t* l0 = lrep + lane;
+  const int32_t* l1 = lrep + 256 * 32 + lane;
+  const int32_t* l2 = lrep + 2 * 256 * 32 + lane;
+  const int32_t bgt = p.bg, rg10 = p.rg10, rb10 = p.rb10, rh = p.recon_h;
+  for (int it = 0; it < iters && g < ngroups; ++it, g += stride) {
+    const uint32_t wv[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    const uint32_t gn = g + stride;
+    if (it + 1 < iters && gn < ngroups) {
+      a = __ldcs(rgb + 3 * gn);
+      b = __ldcs(rgb + 3 * gn + 1);
+      c = __ldcs(rgb + 3 * gn + 2);
     }
-    uint32_t ho[4] = {0, 0, 0, 0}, mo[4] = {0, 0, 0, 0}, to[4] = {0, 0, 0, 0};
+    uint32_t ho[4], to[4];
 #pragma unroll
-    for (int px = 0; px < 16; ++px) {
-      const int b0 = 3 * px, b1 = 3 * px + 1, b2 = 3 * px + 2;
-      const uint32_t r = (wv[b0 >> 2] >> (8 * (b0 & 3))) & 0xFFu;
-      const uint32_t gg = (wv[b1 >> 2] >> (8 * (b1 & 3))) & 0xFFu;
-      const uint32_t bb = (wv[b2 >> 2] >> (8 * (b2 & 3))) & 0xFFu;
-      uint32_t hv, mk, tis;
-      cd_pixel(lut, p, r, gg, bb, hv, mk, tis);
-      ho[px >> 2] |= hv << (8 * (px & 3));
-      mo[px >> 2] |= mk << (8 * (px & 3));
-      to[px >> 2] |= tis << (8 * (px & 3));
+    for (int k = 0; k < 4; ++k) {
+      int32_t hv[4], tv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int px = 4 * k + q;
+        const int i0 = 3 * px, i1 = 3 * px + 1, i2 = 3 * px + 2;
+        const int32_t r = (int32_t)__byte_perm(wv[i0 >> 2], 0, 0x4440 | (i0 & 3));
+        const int32_t gg = (int32_t)__byte_perm(wv[i1 >> 2], 0, 0x4440 | (i1 & 3));
+        const int32_t bb = (int32_t)__byte_perm(wv[i2 >> 2], 0, 0x4440 | (i2 & 3));
+        hv[q] = (l0[r * 32] + l1[gg * 32] + l2[bb * 32]) >> 16;
+        // tissue = !(min(r,g,b) > bg) && !(10r > rg10*g && 10r > rb10*b)
+        //        = min(bg - min(r,g,b), max(rg10*g, rb10*b) - 10r) >= 0
+        const int32_t nb = bgt - min(min(r, gg), bb);
+        const int32_t nr = max(rg10 * gg, rb10 * bb) - 10 * r;
+        tv[q] = (int32_t)((~(uint32_t)(nb | nr)) >> 31);
+      }
+      ho[k] = pack_sat_u8(hv[0], hv[1], hv[2], hv[3]);
+      to[k] = pack_sat_u8(tv[0], tv[1], tv[2], tv[3]);
     }
-    if (hema) hema[g] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
-    if (marker) marker[g] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
-    if (tissue) tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
+    hema[g] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
+    tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
+    if (kMarker) {
+      // max(H - recon_h, 0) per byte (H in [0,255], recon_h >= 0)
+      uint32_t mo[4];
+      const uint32_t hrep = (uint32_t)(rh > 255 ? 255 : rh) * 0x01010101u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mo[k] = __vsubus4(ho[k], hrep);
+      marker[g] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
+    }
   }
 }
 
@@ -174,19 +241,30 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
   cp.rb10 = p->rbc_rb10;
   cp.recon_h = p->recon_h;
   const int64_t n = h * w;
-  const bool flat = pitch == 3 * w && aligned16(rgb) &&
-                    (!hema || aligned16(hema)) && (!marker || aligned16(marker)) &&
-                    (!tissue || aligned16(tissue));
+  const bool flat = pitch == 3 * w && aligned16(rgb) && hema && aligned16(hema) && tissue &&
+                    aligned16(tissue) && (!marker || aligned16(marker));
   int64_t done = 0;
   if (flat) {
-    const int64_t ngroups = n / 16;
+    const int64_t ngroups = n / 16 < INT32_MAX ? n / 16 : 0;
     if (ngroups > 0) {
-      const int64_t want = ceil_div(ngroups, 256);
-      const int blocks = (int)(want < (int64_t)ctx->num_sms * 8 ? want : (int64_t)ctx->num_sms * 8);
-      RTG_CUDA(launch_k(ctx, k_colordeconv_vec, blocks, 256, 0, 
-          reinterpret_cast<const uint4*>(rgb), ngroups, cp,
-          reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-          reinterpret_cast<uint4*>(tissue)));
+      // all groups in one resident wave: iters per thread, then as few
+      // blocks as cover ngroups at that depth
+      static bool smem_set = false;
+      if (!smem_set) {
+        RTG_CUDA(cudaFuncSetAttribute(k_colordeconv_vec<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCdSmem));
+        RTG_CUDA(cudaFuncSetAttribute(k_colordeconv_vec<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCdSmem));
+        smem_set = true;
+      }
+      const int64_t slots = (int64_t)ctx->num_sms * kCdBlocksPerSm * kCdThreads;
+      const int iters = (int)ceil_div(ngroups, slots);
+      const int blocks = (int)ceil_div(ngroups, (int64_t)kCdThreads * iters);
+      auto kern = marker ? k_colordeconv_vec<true> : k_colordeconv_vec<false>;
+      RTG_CUDA(launch_k(ctx, kern, blocks, kCdThreads, kCdSmem,
+                        reinterpret_cast<const uint4*>(rgb), (uint32_t)ngroups, iters, cp,
+                        reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
+                        reinterpret_cast<uint4*>(tissue)));
       RTG_LAUNCH("k_colordeconv_vec");
     }
     done = ngroups * 16;

@@ -84,6 +84,28 @@ def test_colordeconv(rtg, ctx, oracle, shape):
         assert np.array_equal(_dev_np(o), r)
 
 
+@pytest.mark.parametrize("variant", ["default", "params"])
+def test_colordeconv_random_bytes(rtg, ctx, oracle, variant):
+    """Uniform random RGB (every LUT entry, bg/RBC boundaries) through the
+    vector kernel, with and without the marker plane (the default stage path
+    writes hematoxylin + tissue only)."""
+    h, w = 2048, 1536
+    rgb = np.random.default_rng(7).integers(0, 256, (h, w, 3), dtype=np.uint8)
+    p = rtg.default_params()
+    if variant == "params":
+        p.bg_thresh, p.rbc_rg10, p.rbc_rb10, p.recon_h = 128, 11, 29, 300
+    ref = oracle.colordeconv(rgb, p)
+    d_rgb = _np_dev(rgb)
+    hema, marker, tissue = (torch.empty((h, w), dtype=torch.uint8, device="cuda")
+                            for _ in range(3))
+    ctx.colordeconv_dev(d_rgb, h, w, p, hema, None, tissue)
+    assert np.array_equal(_dev_np(hema), ref[0])
+    assert np.array_equal(_dev_np(tissue), ref[2])
+    ctx.colordeconv_dev(d_rgb, h, w, p, hema, marker, tissue)
+    for o, r in zip((hema, marker, tissue), ref):
+        assert np.array_equal(_dev_np(o), r)
+
+
 def test_colordeconv_pitched(rtg, ctx, oracle):
     h, w, pitch = 333, 517, 3 * 517 + 13
     rgb = rtg.synth_tile_host(4, 4, h, w)
