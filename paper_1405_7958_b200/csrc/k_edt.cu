@@ -426,14 +426,29 @@ k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
     const int y = fdiv(p, dw);
     const uint32_t d0 = hd[p];
     uint32_t best = d0 == 255u ? 0xFFFFFFFFu : d0 * d0;
-    int32_t up = p, dn = p;
-    for (uint32_t dy = 1; dy <= kR && dy * dy < best; ++dy) {
-      up -= w;
-      dn += w;
-      uint32_t dm = 255u;
-      if (y >= (int)dy) dm = mask[up] ? hd[up] : 0u;
-      if (y + (int)dy < h) dm = min(dm, mask[dn] ? (uint32_t)hd[dn] : 0u);
-      if (dm != 255u) best = min(best, dy * dy + dm * dm);
+    // rows are visited in batches of kB with every load of the batch in
+    // flight together (mask and hd bytes unconditionally, selected after):
+    // rows past the stopping point only add candidates >= dy^2 >= best, so
+    // the result is the same as the row-by-row scan
+    constexpr uint32_t kB = 4;
+    for (uint32_t dy0 = 1; dy0 <= kR && dy0 * dy0 < best; dy0 += kB) {
+      uint32_t mu[kB], hu[kB], md[kB], hdn[kB];
+#pragma unroll
+      for (uint32_t j = 0; j < kB; ++j) {
+        const uint32_t dy = dy0 + j;
+        const bool vu = y >= (int)dy, vd = y + (int)dy < h;
+        const int32_t qu = p - (int32_t)dy * w, qd = p + (int32_t)dy * w;
+        mu[j] = vu ? mask[qu] : 1u;
+        hu[j] = vu ? hd[qu] : 255u;
+        md[j] = vd ? mask[qd] : 1u;
+        hdn[j] = vd ? hd[qd] : 255u;
+      }
+#pragma unroll
+      for (uint32_t j = 0; j < kB; ++j) {
+        const uint32_t dy = dy0 + j;
+        const uint32_t dm = min(mu[j] ? hu[j] : 0u, md[j] ? hdn[j] : 0u);
+        if (dm != 255u) best = min(best, dy * dy + dm * dm);
+      }
     }
     if (best > kR * kR) {
       far = true;

@@ -582,20 +582,46 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 
 // Basin of every listed pixel: follow the arrows to the marker (basin = 1 +
 // marker root).
-__global__ void k_ws_basins(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-                            const int32_t* __restrict__ ptr, const int32_t* __restrict__ par,
-                            int32_t* __restrict__ basin) {
+// Four chains per thread followed in lockstep, so four dependent loads are
+// in flight per step instead of one (the kernel is latency-bound: every
+// step of an arrow chain is a dependent L2 load).
+__global__ void __launch_bounds__(256)
+k_ws_basins(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+            const int32_t* __restrict__ ptr, const int32_t* __restrict__ par,
+            int32_t* __restrict__ basin) {
   pdl_enter();
+  constexpr int kC = 4;
   const int n = *count;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    int32_t q = list[k];
-    const int32_t p = q;
-    int32_t nx = ptr[q];
-    while (nx >= 0 && nx != q) {
-      q = nx;
-      nx = ptr[q];
+  const int span = gridDim.x * blockDim.x * kC;
+  for (int k0 = blockIdx.x * blockDim.x * kC + threadIdx.x; k0 < n; k0 += span) {
+    int32_t p[kC], q[kC], nx[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) {
+      const int k = k0 + j * (int)blockDim.x;
+      p[j] = k < n ? list[k] : -1;
     }
-    basin[p] = nx == q ? par[q] + 1 : 0;
+#pragma unroll
+    for (int j = 0; j < kC; ++j) {
+      q[j] = p[j];
+      nx[j] = p[j] >= 0 ? ptr[p[j]] : -1;
+    }
+    bool act[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) act[j] = p[j] >= 0 && nx[j] >= 0 && nx[j] != q[j];
+    while (act[0] || act[1] || act[2] || act[3]) {
+#pragma unroll
+      for (int j = 0; j < kC; ++j) {
+        if (act[j]) {
+          q[j] = nx[j];
+          nx[j] = ptr[q[j]];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kC; ++j) act[j] = act[j] && nx[j] >= 0 && nx[j] != q[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kC; ++j)
+      if (p[j] >= 0) basin[p[j]] = nx[j] == q[j] ? par[q[j]] + 1 : 0;
   }
 }
 
