@@ -43,6 +43,16 @@ __device__ __forceinline__ void cd_pixel(const int32_t (*lut)[256],
 // byte extracts, 3 LEA + 3 LDS, one IADD3, the shift, and a saturating pack
 // (cvt.pack.sat) of 2 pixels per instruction; the tissue test is integer
 // min/max arithmetic on the same bytes (~22 instructions/px, was ~45).
+// Streaming 16-byte load: evict-first in L1/L2, 256-byte L2 prefetch (a
+// warp's three loads cover 1.5 KB of contiguous RGB).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t pack_sat_u8(int32_t v0, int32_t v1, int32_t v2,
                                                 int32_t v3) {
   uint32_t hi, d;
@@ -68,9 +78,9 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
   uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a;
   if (g < ngroups) {
-    a = __ldcs(rgb + 3 * g);
-    b = __ldcs(rgb + 3 * g + 1);
-    c = __ldcs(rgb + 3 * g + 2);
+    a = ld_stream(rgb + 3 * g);
+    b = ld_stream(rgb + 3 * g + 1);
+    c = ld_stream(rgb + 3 * g + 2);
   }
   {
     // 192 x 16-byte constant-bank reads (divergent LDC replays once per
@@ -102,9 +112,9 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
     const uint32_t wv[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
     const uint32_t gn = g + stride;
     if (it + 1 < iters && gn < ngroups) {
-      a = __ldcs(rgb + 3 * gn);
-      b = __ldcs(rgb + 3 * gn + 1);
-      c = __ldcs(rgb + 3 * gn + 2);
+      a = ld_stream(rgb + 3 * gn);
+      b = ld_stream(rgb + 3 * gn + 1);
+      c = ld_stream(rgb + 3 * gn + 2);
     }
     uint32_t ho[4], to[4];
 #pragma unroll
