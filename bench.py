@@ -36,6 +36,8 @@ sys.path.insert(0, ROOT)
 
 TILE = 4096
 METRIC = "tile Mpixel/s (segment+features) at 1/2/4/8 B200, % of HBM roofline"
+WORKLOAD = ("C5: 100k x 100k synthetic WSI as 4K tiles (partition_regular: 576 full, "
+            "48 edge, 1 corner), bag of tasks, per-step NCCL gather of feature tables")
 
 # Algorithmic bytes per pixel of each stage: compulsory inputs
 # read once + outputs written once.
@@ -173,8 +175,9 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C5 100k x 100k WSI as 4K tiles (bounded CPU sample)",
-                   "path": "CPU oracle port (reference ships no pixel code)"},
+        "config": {"workload": WORKLOAD,
+                   "path": "CPU oracle port (reference ships no pixel code); each step a "
+                           "bounded sample of the workload's tiles"},
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
@@ -471,9 +474,7 @@ def main():
             "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded H&E-like tiles generated on device)",
-            "config": {"workload": "C5: 100k x 100k synthetic WSI as 4K tiles "
-                                   "(partition_regular: 576 full, 48 edge, 1 corner), "
-                                   "bag of tasks, per-step NCCL gather of feature tables",
+            "config": {"workload": WORKLOAD,
                        "tiles_per_rank_per_step": T, "streams_per_gpu": S,
                        "pixels_per_step": px_rank * world,
                        "l2": "inputs larger than L2 (48 MiB RGB + ~400 MiB planes per tile)",
