@@ -77,6 +77,26 @@ __device__ __forceinline__ void gather8(const T* a, int w, int32_t p, uint32_t m
   for (int t = 0; t < 8; ++t) v[t] = ((m >> t) & 1u) ? (S)a[nbr_index(w, p, t)] : fill;
 }
 
+// Unions of p with its backward 8-neighbours of the same component (bits
+// 0..3 of `same`: above-left, above, above-right, left), skipping the ones a
+// neighbour's own unions already imply: the left neighbour (when joined)
+// has already joined the above-left and above pixels, and two horizontally
+// adjacent same-component pixels above are joined with each other.  Every
+// component stays connected; the number of union-find operations (and the
+// chain lengths they build) drops from up to four per pixel to about one.
+__device__ __forceinline__ void unite_backward(int32_t* par, int w, int32_t p, uint32_t same) {
+  const bool ul = same & 1u, u = same & 2u, ur = same & 4u, l = same & 8u;
+  if (l) {
+    uf_unite_g(par, p, p - 1);
+    if (ur && !u) uf_unite_g(par, p, p - w + 1);
+  } else if (u) {
+    uf_unite_g(par, p, p - w);
+  } else {
+    if (ul) uf_unite_g(par, p, p - w - 1);
+    if (ur) uf_unite_g(par, p, p - w + 1);
+  }
+}
+
 // Arrows over the foreground list.  Non-flat pixels: steepest ascent
 // (par = -1, flat byte 0).  Flat pixels: par = self, cnt = 0, flat byte 1,
 // appended to the flat list (their seed arrow is set by k_ws_union).
@@ -142,16 +162,17 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
     uint32_t fv[8], fl[8];
     gather8(Fw, w, i, fm, 0u, fv);
     gather8(flat, w, i, fm, 1u, fl);
+    uint32_t same = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       if (!((fm >> t) & 1u) || fv[t] != f) continue;
-      const int32_t j = nbr_index(w, i, t);
       if (!fl[t]) {
-        if (seed == -2) seed = j;
+        if (seed == -2) seed = nbr_index(w, i, t);
       } else if (t < 4) {  // backward neighbour (above or left)
-        uf_unite_g(par, i, j);
+        same |= 1u << t;
       }
     }
+    unite_backward(par, w, i, same);
     if (seed != -2) ptr[i] = seed;
   }
 }
@@ -436,9 +457,10 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mas
     // backward neighbours only (bits 0..3: above row and left)
     uint32_t sv[8];
     gather8(sflag, w, i, fg_nbrs(h, w, mask, i, y, x) & 0xFu, 0u, sv);
+    uint32_t same = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (sv[t]) uf_unite_g(par, i, nbr_index(w, i, t));
+    for (int t = 0; t < 4; ++t) same |= sv[t] ? 1u << t : 0u;
+    unite_backward(par, w, i, same);
   }
 }
 
