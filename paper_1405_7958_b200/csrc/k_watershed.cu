@@ -185,25 +185,12 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
                            int32_t* __restrict__ slot) {
   pdl_enter();
   const int n = *flat_count;
-  const int lane = threadIdx.x & 31;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const unsigned act = __activemask();
     const int32_t i = flat_list[k];
     const int32_t r = uf_find_g(par, i);
     if (r != i) atomicMin(par + i, r);
-    // one count (and seed flag) update per root per warp: consecutive list
-    // entries mostly share a component
-    const unsigned grp = __match_any_sync(act, r);
-    const bool seeded = ptr && ptr[i] >= 0;
-    const unsigned sgrp = __ballot_sync(act, seeded) & grp;
-    const int leader = __ffs(grp) - 1;
-    int32_t base = 0;
-    if (lane == leader) {
-      base = atomicAdd(cnt + r, __popc(grp));
-      if (sgrp) atomicOr(cnt + r, kSeeded);
-    }
-    base = __shfl_sync(grp, base, leader);
-    slot[i] = (base & kCountMask) + __popc(grp & ((1u << lane) - 1u));
+    if (ptr && ptr[i] >= 0) atomicOr(cnt + r, kSeeded);
+    slot[i] = atomicAdd(cnt + r, 1) & kCountMask;
   }
 }
 
