@@ -42,7 +42,7 @@ def _free_port():
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    rows = 3 + 2 * rank
+    rows = 0 if (world > 2 and rank == 1) else 3 + 2 * rank  # an empty shard too
     packed = torch.full((rows + 4, 20), float(rank), dtype=torch.float32)
     packed[:rows, 0] = torch.arange(rows, dtype=torch.float32)
     table, total = wsi.gather_tables(packed, rows, rank, world, dist)
@@ -51,18 +51,29 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.timeout(120)
-def test_gather_world2_gloo():
+def _rows(rank, world):
+    return 0 if (world > 2 and rank == 1) else 3 + 2 * rank
+
+
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gather_gloo(world):
+    """bench.py's only cross-rank exchange at N = 2, 4, 8 (the driver's
+    scaling run), including a rank whose shard produced no feature rows."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    total, col0, col1 = q.get(timeout=100)
+    total, col0, col1 = q.get(timeout=200)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert total == 3 + 5
-    assert col0 == [0, 1, 2, 0, 1, 2, 3, 4]
-    assert col1 == [0.0] * 3 + [1.0] * 5
+    want0, want1 = [], []
+    for r in range(world):
+        want0 += [float(i) for i in range(_rows(r, world))]
+        want1 += [float(r)] * _rows(r, world)
+    assert total == len(want0)
+    assert col0 == want0
+    assert col1 == want1
