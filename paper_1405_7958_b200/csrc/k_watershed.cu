@@ -67,6 +67,19 @@ __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
   return p + (k / 3 - 1) * w + (k % 3 - 1);
 }
 
+// Watershed arrows are stored as one byte per pixel: 0..7 = the row-major
+// 8-neighbour it points to, kDirSelf = a marker pixel (root), kDirNone = no
+// arrow yet.  A byte plane keeps the basin chains' gathers 4x denser than
+// absolute i32 indices (neighbouring chains share sectors).
+constexpr uint8_t kDirSelf = 8;
+constexpr uint8_t kDirNone = 0xFF;
+
+__device__ __forceinline__ int32_t dir_step(int w, int32_t p, uint32_t t) {
+  const int dy = (int)((0x22211000u >> (4 * t)) & 0xFu) - 1;
+  const int dx = (int)((0x21020210u >> (4 * t)) & 0xFu) - 1;
+  return p + dy * w + dx;
+}
+
 // The 8 neighbour values selected by mask m (others = fill), as unrolled
 // predicated loads so all of them are in flight together (a loop over the
 // set bits would serialise one memory latency per neighbour).
@@ -103,7 +116,7 @@ __device__ __forceinline__ void unite_backward(int32_t* par, int w, int32_t p, u
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const uint32_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
-            int32_t* __restrict__ ptr, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
+            uint8_t* __restrict__ dir, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
   pdl_enter();
@@ -119,18 +132,18 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       const int y = fdiv(p, dw), x = p - y * w;
       const uint32_t f = Fw[p];
       uint32_t best = f;
-      int32_t arg = -1;
+      int arg = -1;
       uint32_t fv[8];
       gather8(Fw, w, p, fg_nbrs(h, w, mask, p, y, x), 0u, fv);
 #pragma unroll
       for (int t = 0; t < 8; ++t)  // row-major: first max = min index
-        if (fv[t] > best) { best = fv[t]; arg = nbr_index(w, p, t); }
+        if (fv[t] > best) { best = fv[t]; arg = t; }
       if (arg >= 0) {
-        ptr[p] = arg;
+        dir[p] = (uint8_t)arg;
         par[p] = -1;
         flat[p] = 0;
       } else {
-        ptr[p] = -2;
+        dir[p] = kDirNone;
         par[p] = p;
         cnt[p] = 0;
         flat[p] = 1;
@@ -148,7 +161,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
 __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                            const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
                            const int32_t* __restrict__ flat_list,
-                           const int32_t* __restrict__ flat_count, int32_t* __restrict__ ptr,
+                           const int32_t* __restrict__ flat_count, uint8_t* __restrict__ dir,
                            int32_t* par) {
   pdl_enter();
   const int w = (int)dw.d;
@@ -157,7 +170,7 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
     const int32_t i = flat_list[k];
     const int y = fdiv(i, dw), x = i - y * w;
     const uint16_t f = Fw[i];
-    int32_t seed = -2;
+    int seed = -1;
     const uint32_t fm = fg_nbrs(h, w, mask, i, y, x);
     uint32_t fv[8], fl[8];
     gather8(Fw, w, i, fm, 0u, fv);
@@ -167,13 +180,13 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
     for (int t = 0; t < 8; ++t) {
       if (!((fm >> t) & 1u) || fv[t] != f) continue;
       if (!fl[t]) {
-        if (seed == -2) seed = nbr_index(w, i, t);
+        if (seed < 0) seed = t;
       } else if (t < 4) {  // backward neighbour (above or left)
         same |= 1u << t;
       }
     }
     unite_backward(par, w, i, same);
-    if (seed != -2) ptr[i] = seed;
+    if (seed >= 0) dir[i] = (uint8_t)seed;
   }
 }
 
@@ -181,7 +194,7 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 // pixel a slot in its component (slot stored in the delta plane).
 __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count,
-                           const int32_t* __restrict__ ptr, int32_t* par, int32_t* cnt,
+                           const uint8_t* __restrict__ dir, int32_t* par, int32_t* cnt,
                            int32_t* __restrict__ slot) {
   pdl_enter();
   const int n = *flat_count;
@@ -189,17 +202,17 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
     const int32_t i = flat_list[k];
     const int32_t r = uf_find_g(par, i);
     if (r != i) atomicMin(par + i, r);
-    if (ptr && ptr[i] >= 0) atomicOr(cnt + r, kSeeded);
+    if (dir && dir[i] != kDirNone) atomicOr(cnt + r, kSeeded);
     slot[i] = atomicAdd(cnt + r, 1) & kCountMask;
   }
 }
 
-// Unseeded components are the markers (ptr = self; the root is the marker
+// Unseeded components are the markers (arrow = kDirSelf; the root is the marker
 // label).  Each seeded root reserves its members' range and enters the
 // component list.  alloc = {member cursor, component count} as one u64.
 __global__ void __launch_bounds__(256)
 k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-              const int32_t* __restrict__ par, int32_t* cnt, int32_t* __restrict__ ptr,
+              const int32_t* __restrict__ par, int32_t* cnt, uint8_t* __restrict__ dir,
               unsigned long long* alloc,
               int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
   pdl_enter();
@@ -213,7 +226,7 @@ k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__
       const int32_t r = __ldcg(par + i);
       const int32_t v = __ldcg(cnt + r);
       if (!(v & kSeeded)) {
-        ptr[i] = i;
+        dir[i] = kDirSelf;
       } else if (r == i) {
         root = i;
         sz = v & kCountMask;
@@ -301,7 +314,7 @@ __global__ void __launch_bounds__(256)
 k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
-             int32_t* __restrict__ ptr, int32_t* delta, int2* __restrict__ scratch) {
+             uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch) {
   pdl_enter();
   const int w = (int)dw.d;
   constexpr int kPer = 4;
@@ -324,7 +337,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         nb[q] = 0;
         if (k < e) {
           px[q] = member_px(members[k]);
-          d[q] = ptr[px[q]] >= 0 ? 1 : kInfD;
+          d[q] = dir[px[q]] != kDirNone ? 1 : kInfD;
           nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], Fw[px[q]], par[px[q]]);
           vd[px[q]] = d[q];
         }
@@ -355,13 +368,13 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         gather8(vd, w, px[q], nb[q], kInfD, dv);
 #pragma unroll
         for (int t = 7; t >= 0; --t)  // the first (minimum-index) match wins
-          if (dv[t] == d[q] - 1) ptr[px[q]] = nbr_index(w, px[q], t);
+          if (dv[t] == d[q] - 1) dir[px[q]] = (uint8_t)t;
       }
     } else {
       // long range: per-member (pixel, neighbour mask) cached in scratch
       for (int k = s0 + lane; k < e; k += 32) {
         const int32_t p = member_px(members[k]);
-        vd[p] = ptr[p] >= 0 ? 1 : kInfD;
+        vd[p] = dir[p] != kDirNone ? 1 : kInfD;
         scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, par, p, Fw[p], par[p]));
       }
       __syncwarp();
@@ -391,7 +404,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         gather8(vd, w, pm.x, (uint32_t)pm.y, kInfD, dv);
 #pragma unroll
         for (int t = 7; t >= 0; --t)
-          if (dv[t] == dp - 1) ptr[pm.x] = nbr_index(w, pm.x, t);
+          if (dv[t] == dp - 1) dir[pm.x] = (uint8_t)t;
       }
     }
   }
@@ -608,15 +621,16 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 // in flight per step instead of one (the kernel is latency-bound: every
 // step of an arrow chain is a dependent L2 load).
 __global__ void __launch_bounds__(256)
-k_ws_basins(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const int32_t* __restrict__ ptr, const int32_t* __restrict__ par,
+k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+            const uint8_t* __restrict__ dir, const int32_t* __restrict__ par,
             int32_t* __restrict__ basin) {
   pdl_enter();
   constexpr int kC = 4;
   const int n = *count;
   const int span = gridDim.x * blockDim.x * kC;
   for (int k0 = blockIdx.x * blockDim.x * kC + threadIdx.x; k0 < n; k0 += span) {
-    int32_t p[kC], q[kC], nx[kC];
+    int32_t p[kC], q[kC];
+    uint32_t d[kC];
 #pragma unroll
     for (int j = 0; j < kC; ++j) {
       const int k = k0 + j * (int)blockDim.x;
@@ -625,25 +639,21 @@ k_ws_basins(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
 #pragma unroll
     for (int j = 0; j < kC; ++j) {
       q[j] = p[j];
-      nx[j] = p[j] >= 0 ? ptr[p[j]] : -1;
+      d[j] = p[j] >= 0 ? dir[p[j]] : kDirNone;
     }
-    bool act[kC];
-#pragma unroll
-    for (int j = 0; j < kC; ++j) act[j] = p[j] >= 0 && nx[j] >= 0 && nx[j] != q[j];
-    while (act[0] || act[1] || act[2] || act[3]) {
+    // d < 8: step to that neighbour; kDirSelf: marker reached; kDirNone: none
+    while (d[0] < 8u || d[1] < 8u || d[2] < 8u || d[3] < 8u) {
 #pragma unroll
       for (int j = 0; j < kC; ++j) {
-        if (act[j]) {
-          q[j] = nx[j];
-          nx[j] = ptr[q[j]];
+        if (d[j] < 8u) {
+          q[j] = dir_step(w, q[j], d[j]);
+          d[j] = dir[q[j]];
         }
       }
-#pragma unroll
-      for (int j = 0; j < kC; ++j) act[j] = act[j] && nx[j] >= 0 && nx[j] != q[j];
     }
 #pragma unroll
     for (int j = 0; j < kC; ++j)
-      if (p[j] >= 0) basin[p[j]] = nx[j] == q[j] ? par[q[j]] + 1 : 0;
+      if (p[j] >= 0) basin[p[j]] = d[j] == kDirSelf ? par[q[j]] + 1 : 0;
   }
 }
 
@@ -737,31 +747,31 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_LAUNCH("k_hmax_solve");
   }
   prof_mark(ctx, RTG_STAGE_WATERSHED);
-  int32_t* ptr = ctx->i32a;
+  uint8_t* dir = reinterpret_cast<uint8_t*>(ctx->i32a);  // arrow codes, 1 B/px
   int32_t* delta = ctx->i32b;
   int32_t* par = ctx->i32c;
   uint8_t* flat = ctx->m1;
   int32_t* flat_count = ctx->misc + 1;
   RTG_TRY(zero_async(ctx, ZeroList{{flat_count, alloc},
                                     {sizeof(int32_t), sizeof(unsigned long long)}, 2}));
-  RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, ptr, par, basin,
+  RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, dir, par, basin,
                                           flat, ctx->flat_list, flat_count));
   RTG_LAUNCH("k_ws_arrows");
   RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
-                                         flat_count, ptr, par));
+                                         flat_count, dir, par));
   RTG_LAUNCH("k_ws_union");
-  RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, ptr, par, basin, delta));
+  RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, dir, par, basin, delta));
   RTG_LAUNCH("k_ws_roots");
-  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, ptr, alloc,
+  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir, alloc,
                                             comp_root, comp_size));
   RTG_LAUNCH("k_ws_classify");
   RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots));
   RTG_LAUNCH("k_ws_scatter");
-  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, ptr,
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, dir,
                                            delta, member_scratch));
   RTG_LAUNCH("k_ws_plateau");
-  RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, fgl, fgn, ptr, par, basin));
+  RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
   RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, basin, sep));
   RTG_LAUNCH("k_ws_separate");
