@@ -562,10 +562,14 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 // mask keeps every pixel whose top-level ancestor has an area in range —
 // exactly FillHoles followed by an 8-connected AreaThreshold.
 
+// 7 KB per warp (28 warps per SM): the forest is flattened in place, the
+// per-root accumulators are 16-bit (count <= 1024 | seed 0x8000, two per
+// word, updated with 32-bit atomics), and the flattened forest then holds
+// each run's global root index for the pixel stores.
 template <int kW>
 struct FbSmem {
   int32_t par[kW][1024];
-  uint32_t inf[kW][1024];
+  uint32_t acc[kW][512];
   uint8_t pos[kW][1024];
 };
 
@@ -580,7 +584,8 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const bool active = blockIdx.x * kTileWarps + wid < ntiles;
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   int32_t* par = S.par[wid];
-  uint32_t* inf = S.inf[wid];
+  uint32_t* acc = S.acc[wid];
+  uint16_t* acc16 = reinterpret_cast<uint16_t*>(acc);
   uint8_t* pos = S.pos[wid];
   const FgMask pred{m};
   // 1. foreground row masks (lane r keeps row r)
@@ -665,14 +670,14 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   }
   // 3. flatten; per local root: pixel count + border-background bit
   const int nruns = __popc(allst);
-  for (int k = 0; k < nruns; ++k) inf[rb + k] = (uint32_t)find_root(par, rb + k);
-  __syncwarp();
-  for (int k = 0; k < nruns; ++k) par[rb + k] = (int32_t)inf[rb + k];
+  // in place: a concurrent shortcut store only replaces a parent by an
+  // ancestor, so every find still ends at the same root
+  for (int k = 0; k < nruns; ++k) par[rb + k] = find_root(par, rb + k);
   __syncwarp();
   int nroot = 0;
   for (int k = 0; k < nruns; ++k)
     if (par[rb + k] == rb + k) {
-      inf[rb + k] = 0;
+      acc16[rb + k] = 0;
       ++nroot;
     }
   __syncwarp();
@@ -682,8 +687,9 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       const int b = __ffs(q) - 1;
       const uint32_t run = low_run((((fgb >> b) & 1u) ? fgb : bgb) >> b) << b;
       const int32_t root = par[rb + k];
-      if (seeds & run) atomicOr(&inf[root], kSeedBit);
-      atomicAdd(&inf[root], (uint32_t)__popc(run));
+      const uint32_t sh = (root & 1) * 16;
+      if (seeds & run) atomicOr(&acc[root >> 1], 0x8000u << sh);
+      atomicAdd(&acc[root >> 1], (uint32_t)__popc(run) << sh);
     }
   }
   __shared__ int32_t s_res[kTileWarps + 1];
@@ -693,15 +699,17 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   for (int k = 0; k < nruns; ++k) {
     if (par[rb + k] != rb + k) continue;
     const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
+    const uint32_t a = acc16[rb + k];
     lroots[2 * base] = g;
-    lroots[2 * base + 1] = (int32_t)inf[rb + k];
+    lroots[2 * base + 1] = (int32_t)((a & 0x7FFFu) | ((a & 0x8000u) ? kSeedBit : 0u));
     ++base;
     counts[g] = 0;
   }
   __syncwarp();
+  // each lane rewrites only its own runs' entries
   for (int k = 0; k < nruns; ++k) {
     const int32_t lr = par[rb + k];
-    inf[rb + k] = (uint32_t)((y0 + (lr >> 5)) * w + x0 + pos[lr]);
+    par[rb + k] = (y0 + (lr >> 5)) * w + x0 + pos[lr];
   }
   __syncwarp();
   // 4. every valid pixel's local root
@@ -716,7 +724,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       int32_t o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        o[j] = (int32_t)inf[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
+        o[j] = par[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
       *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
     }
   } else {
@@ -725,7 +733,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       const uint32_t st = __shfl_sync(kFull, allst, r);
       const int y = y0 + r;
       if (y < h && x < w)
-        roots[(int64_t)y * w + x] = (int32_t)inf[r * 32 + __popc(st & ((2u << lane) - 1u)) - 1];
+        roots[(int64_t)y * w + x] = par[r * 32 + __popc(st & ((2u << lane) - 1u)) - 1];
     }
   }
 }
