@@ -549,6 +549,56 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
   return (int)(want < cap ? want : cap);
 }
 
+// 16-bit shared-memory forest (run ids < 1024).  There is no 16-bit
+// atomicMin, so the link is a CAS on the 32-bit word holding the entry; plain
+// 16-bit path-halving stores cannot be lost to it (a CAS whose expected word
+// changed underneath simply retries).
+__device__ __forceinline__ int32_t find_root16(const uint16_t* par, int32_t a) {
+  int32_t p = par[a];
+  while (p != a) {
+    a = p;
+    p = par[a];
+  }
+  return a;
+}
+
+__device__ __forceinline__ int32_t find_root16_c(uint16_t* par, int32_t a) {
+  int32_t p = par[a];
+  while (p != a) {
+    const int32_t gp = par[p];
+    if (gp != p) par[a] = (uint16_t)gp;
+    a = p;
+    p = gp;
+  }
+  return a;
+}
+
+__device__ __forceinline__ int32_t atomic_min16(uint16_t* par, int32_t a, int32_t b) {
+  uint32_t* wp = reinterpret_cast<uint32_t*>(par) + (a >> 1);
+  const uint32_t sh = (uint32_t)(a & 1) * 16u;
+  uint32_t old = *reinterpret_cast<volatile uint32_t*>(wp);
+  while (true) {
+    const int32_t cur = (int32_t)((old >> sh) & 0xFFFFu);
+    if (cur <= b) return cur;
+    const uint32_t nw = (old & ~(0xFFFFu << sh)) | ((uint32_t)b << sh);
+    const uint32_t prev = atomicCAS(wp, old, nw);
+    if (prev == old) return cur;
+    old = prev;
+  }
+}
+
+__device__ __forceinline__ void unite_s16(uint16_t* par, int32_t a, int32_t b) {
+  while (true) {
+    a = find_root16_c(par, a);
+    b = find_root16_c(par, b);
+    if (a == b) return;
+    if (a < b) { const int32_t t = a; a = b; b = t; }  // a is the larger root
+    const int32_t old = atomic_min16(par, a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
 // ---- FillHoles + AreaThreshold in one labelling ------------------------------
 // The candidates' foreground (8-connected) and background (4-connected)
 // components are labelled together: every pixel belongs to exactly one
@@ -562,13 +612,13 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 // mask keeps every pixel whose top-level ancestor has an area in range —
 // exactly FillHoles followed by an 8-connected AreaThreshold.
 
-// 7 KB per warp (28 warps per SM): the forest is flattened in place, the
-// per-root accumulators are 16-bit (count <= 1024 | seed 0x8000, two per
-// word, updated with 32-bit atomics), and the flattened forest then holds
-// each run's global root index for the pixel stores.
+// 5 KB per warp (44 warps per SM): a 16-bit forest flattened in place,
+// 16-bit per-root accumulators (count <= 1024 | seed 0x8000, two per word,
+// updated with 32-bit atomics), and the flattened forest then holds each
+// run's root pixel as a tile-local offset (row * 32 + column) for the stores.
 template <int kW>
 struct FbSmem {
-  int32_t par[kW][1024];
+  uint16_t par[kW][1024];
   uint32_t acc[kW][512];
   uint8_t pos[kW][1024];
 };
@@ -583,7 +633,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
   const bool active = blockIdx.x * kTileWarps + wid < ntiles;
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
-  int32_t* par = S.par[wid];
+  uint16_t* par = S.par[wid];
   uint32_t* acc = S.acc[wid];
   uint16_t* acc16 = reinterpret_cast<uint16_t*>(acc);
   uint8_t* pos = S.pos[wid];
@@ -638,7 +688,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   {
     int k = 0;
     for (uint32_t q = allst; q; q &= q - 1, ++k) {
-      par[rb + k] = rb + k;
+      par[rb + k] = (uint16_t)(rb + k);
       pos[rb + k] = (uint8_t)(__ffs(q) - 1);
     }
   }
@@ -661,7 +711,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
         while (ov) {
           const int t = __ffs(ov) - 1;
           const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
-          unite_s(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
+          unite_s16(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
           ov &= ~(low_run(U >> su) << su);
         }
       }
@@ -672,7 +722,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const int nruns = __popc(allst);
   // in place: a concurrent shortcut store only replaces a parent by an
   // ancestor, so every find still ends at the same root
-  for (int k = 0; k < nruns; ++k) par[rb + k] = find_root(par, rb + k);
+  for (int k = 0; k < nruns; ++k) par[rb + k] = (uint16_t)find_root16(par, rb + k);
   __syncwarp();
   int nroot = 0;
   for (int k = 0; k < nruns; ++k)
@@ -709,7 +759,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   // each lane rewrites only its own runs' entries
   for (int k = 0; k < nruns; ++k) {
     const int32_t lr = par[rb + k];
-    par[rb + k] = (y0 + (lr >> 5)) * w + x0 + pos[lr];
+    par[rb + k] = (uint16_t)((lr & ~31) | pos[lr]);
   }
   __syncwarp();
   // 4. every valid pixel's local root
@@ -723,8 +773,10 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       if (y >= h) continue;
       int32_t o[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        o[j] = par[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
+      for (int j = 0; j < 4; ++j) {
+        const int32_t lo = par[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
+        o[j] = (y0 + (lo >> 5)) * w + x0 + (lo & 31);
+      }
       *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
     }
   } else {
@@ -732,8 +784,10 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
     for (int r = 0; r < 32; ++r) {
       const uint32_t st = __shfl_sync(kFull, allst, r);
       const int y = y0 + r;
-      if (y < h && x < w)
-        roots[(int64_t)y * w + x] = par[r * 32 + __popc(st & ((2u << lane) - 1u)) - 1];
+      if (y < h && x < w) {
+        const int32_t lo = par[r * 32 + __popc(st & ((2u << lane) - 1u)) - 1];
+        roots[(int64_t)y * w + x] = (y0 + (lo >> 5)) * w + x0 + (lo & 31);
+      }
     }
   }
 }
