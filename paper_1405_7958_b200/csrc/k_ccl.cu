@@ -443,52 +443,38 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
   return off + incl - v;
 }
 
-__global__ void __launch_bounds__(1024)
-k_scan_chunks(int nchunks, const int32_t* __restrict__ cnt,
-              int32_t* __restrict__ off, int32_t* __restrict__ d_total) {
-  pdl_enter();
-  __shared__ int warp_tot[32];
-  const int per = (nchunks + 1023) / 1024;
-  const int b = threadIdx.x * per;
-  int s = 0;
-  for (int k = 0; k < per; ++k)
-    if (b + k < nchunks) s += cnt[b + k];
-  int total;
-  int run = block_excl_scan(s, warp_tot, total);
-  for (int k = 0; k < per; ++k) {
-    if (b + k < nchunks) {
-      off[b + k] = run;
-      run += cnt[b + k];
-    }
-  }
-  if (threadIdx.x == 0 && d_total) *d_total = total;
-}
-
-// Canonical ranks from the root bitmap: per-chunk popcounts, chunk offsets,
-// per-word exclusive prefixes, then one rank per global root.
+// Canonical ranks from the root bitmap: per-word exclusive prefixes in one
+// look-back pass, then one rank per global root.
 constexpr int kBmPerThread = 16;
 constexpr int kBmChunk = 256 * kBmPerThread;  // words per chunk
 
-__global__ void __launch_bounds__(256)
-k_bm_count(int64_t nwords, const uint32_t* __restrict__ bm, int32_t* __restrict__ chunk_cnt) {
-  pdl_enter();
-  __shared__ int warp_tot[8];
-  const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < kBmPerThread; ++k)
-    if (base + k < nwords) c += __popc(bm[base + k]);
-  int total;
-  block_excl_scan(c, warp_tot, total);
-  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = total;
+// Single-pass per-word exclusive prefix of the root bitmap (decoupled
+// look-back): each CTA popcounts its chunk, publishes the chunk aggregate,
+// then walks back over its predecessors' published values until it meets an
+// inclusive prefix.  Replaces count / chunk-scan / prefix (three launches).
+// status[c] = flag << 62 | value (flag 1: aggregate, 2: inclusive prefix);
+// status[nchunks] is the CTA ticket (chunks are taken in launch order, so
+// every predecessor is running or done).  status must be zero on entry.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(256)
-k_bm_prefix(int64_t nwords, const uint32_t* __restrict__ bm,
-            const int32_t* __restrict__ chunk_off, int32_t* __restrict__ wprefix) {
+k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
+          unsigned long long* status, int32_t* __restrict__ wprefix, int32_t* __restrict__ d_total) {
   pdl_enter();
   __shared__ int warp_tot[8];
-  const int64_t base = (int64_t)blockIdx.x * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
+  __shared__ int s_bid, s_prefix;
+  if (threadIdx.x == 0)
+    s_bid = atomicAdd(reinterpret_cast<int*>(status + nchunks), 1);
+  __syncthreads();
+  const int bid = s_bid;
+  const int64_t base = (int64_t)bid * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
   uint32_t v[kBmPerThread];
   int c = 0;
 #pragma unroll
@@ -497,7 +483,36 @@ k_bm_prefix(int64_t nwords, const uint32_t* __restrict__ bm,
     c += __popc(v[k]);
   }
   int total;
-  int run = block_excl_scan(c, warp_tot, total) + chunk_off[blockIdx.x];
+  int run = block_excl_scan(c, warp_tot, total);
+  if (threadIdx.x < 32) {
+    // warp 0: publish, then look back over windows of 32 predecessors
+    const int lane = threadIdx.x;
+    if (lane == 0)
+      st_release_u64(status + bid, ((bid == 0 ? 2ull : 1ull) << 62) | (uint32_t)total);
+    int prefix = 0;
+    for (int j = bid - 1; j >= 0;) {
+      const int idx = j - lane;
+      const unsigned long long st = idx >= 0 ? ld_acquire_u64(status + idx) : (2ull << 62);
+      const unsigned flag = (unsigned)(st >> 62);
+      const unsigned incl = __ballot_sync(0xFFFFFFFFu, flag == 2);
+      const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive prefix
+      const unsigned upto = stop == 31 ? 0xFFFFFFFFu : ((2u << stop) - 1u);
+      if (__ballot_sync(0xFFFFFFFFu, flag == 0) & upto) continue;  // not published yet
+      int v = (lane <= stop) ? (int)(st & 0xFFFFFFFFull) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      prefix += v;
+      if (incl) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      if (bid > 0) st_release_u64(status + bid, (2ull << 62) | (uint32_t)(prefix + total));
+      s_prefix = prefix;
+      if (bid == nchunks - 1 && d_total) *d_total = prefix + total;
+    }
+  }
+  __syncthreads();
+  run += s_prefix;
 #pragma unroll
   for (int k = 0; k < kBmPerThread; ++k) {
     if (base + k < nwords) wprefix[base + k] = run;
@@ -987,10 +1002,14 @@ template <class P>
 int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
             int32_t* counts, int32_t* flags, uint32_t* bitmap) {
   int32_t* lcount = ctx->misc + 8;
-  RTG_TRY(zero_async(ctx, ZeroList{{lcount, bitmap},
+  // with a bitmap (the canonical labelling follows): also the look-back
+  // status words of k_bm_scan
+  const size_t nstatus = (size_t)ceil_div(ceil_div(h * w, 32), kBmChunk) + 1;
+  RTG_TRY(zero_async(ctx, ZeroList{{lcount, bitmap, ctx->scan_buf},
                                     {sizeof(int32_t),
-                                     bitmap ? sizeof(uint32_t) * (size_t)ceil_div(h * w, 32) : 0},
-                                    2}));
+                                     bitmap ? sizeof(uint32_t) * (size_t)ceil_div(h * w, 32) : 0,
+                                     bitmap ? sizeof(unsigned long long) * nstatus : 0},
+                                    3}));
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
@@ -1044,15 +1063,11 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   const int64_t n = h * w;
   const int64_t nwords = ceil_div(n, 32);
   const int nchunks = (int)ceil_div(nwords, kBmChunk);
-  int32_t* cnt = ctx->scan_buf;
-  int32_t* off = ctx->scan_buf + nchunks;
+  auto* status = reinterpret_cast<unsigned long long*>(ctx->scan_buf);  // zeroed by ccl_run
   int32_t* rank = ctx->i32c;
-  RTG_CUDA(launch_k(ctx, k_bm_count, nchunks, 256, 0, nwords, ctx->root_bm, cnt));
-  RTG_LAUNCH("k_bm_count");
-  RTG_CUDA(launch_k(ctx, k_scan_chunks, 1, 1024, 0, nchunks, cnt, off, d_n));
-  RTG_LAUNCH("k_scan_chunks");
-  RTG_CUDA(launch_k(ctx, k_bm_prefix, nchunks, 256, 0, nwords, ctx->root_bm, off, ctx->root_wprefix));
-  RTG_LAUNCH("k_bm_prefix");
+  RTG_CUDA(launch_k(ctx, k_bm_scan, nchunks, 256, 0, nwords, nchunks, ctx->root_bm, status,
+                    ctx->root_wprefix, d_n));
+  RTG_LAUNCH("k_bm_scan");
   RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
                                                          ctx->root_bm, ctx->root_wprefix, rank));
   RTG_LAUNCH("k_root_rank");
