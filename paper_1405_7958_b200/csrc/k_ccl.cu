@@ -476,12 +476,20 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
   const int bid = s_bid;
   const int64_t base = (int64_t)bid * kBmChunk + (int64_t)threadIdx.x * kBmPerThread;
   uint32_t v[kBmPerThread];
+  const bool full = base + kBmPerThread <= nwords;  // 16 words = 4 x 16-byte loads
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < kBmPerThread / 4; ++q) {
+      const uint4 t = __ldg(reinterpret_cast<const uint4*>(bm + base) + q);
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kBmPerThread; ++k) v[k] = base + k < nwords ? bm[base + k] : 0u;
+  }
   int c = 0;
 #pragma unroll
-  for (int k = 0; k < kBmPerThread; ++k) {
-    v[k] = base + k < nwords ? bm[base + k] : 0u;
-    c += __popc(v[k]);
-  }
+  for (int k = 0; k < kBmPerThread; ++k) c += __popc(v[k]);
   int total;
   int run = block_excl_scan(c, warp_tot, total);
   if (threadIdx.x < 32) {
@@ -513,10 +521,19 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
   }
   __syncthreads();
   run += s_prefix;
+  int32_t o[kBmPerThread];
 #pragma unroll
   for (int k = 0; k < kBmPerThread; ++k) {
-    if (base + k < nwords) wprefix[base + k] = run;
+    o[k] = run;
     run += __popc(v[k]);
+  }
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < kBmPerThread / 4; ++q)
+      reinterpret_cast<int4*>(wprefix + base)[q] =
+          make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+  } else {
+    for (int k = 0; k < kBmPerThread && base + k < nwords; ++k) wprefix[base + k] = o[k];
   }
 }
 
