@@ -314,14 +314,19 @@ __global__ void __launch_bounds__(256)
 k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
-             uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch) {
+             uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch,
+             uint8_t* slotmap) {
   pdl_enter();
   const int w = (int)dw.d;
   constexpr int kPer = 4;
+  // small ranges relax in shared memory (distances by slot, neighbour slots)
+  __shared__ int32_t s_val[8][32 * kPer];
+  __shared__ uint8_t s_nbs[8][32 * kPer][8];
   const int nmem = (int)(*alloc & 0xFFFFFFFFull);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   volatile int32_t* vd = delta;
+  volatile int32_t* sv = s_val[wl];
   for (int w0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < nmem;
        w0 += nwarps * 32) {
     int s0, e;
@@ -339,8 +344,17 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
           px[q] = member_px(members[k]);
           d[q] = dir[px[q]] != kDirNone ? 1 : kInfD;
           nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], Fw[px[q]], par[px[q]]);
-          vd[px[q]] = d[q];
+          sv[lane + 32 * q] = d[q];
+          slotmap[px[q]] = (uint8_t)(lane + 32 * q);
         }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        if (px[q] < 0) continue;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if ((nb[q] >> t) & 1u) s_nbs[wl][lane + 32 * q][t] = slotmap[nbr_index(w, px[q], t)];
       }
       __syncwarp();
       while (true) {
@@ -348,14 +362,14 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           if (px[q] < 0 || d[q] == 1) continue;
-          int32_t dv[8];
-          gather8(vd, w, px[q], nb[q], kInfD, dv);
+          const uint8_t* ns = s_nbs[wl][lane + 32 * q];
           int32_t best = d[q];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) best = min(best, dv[t] + 1);
+          for (int t = 0; t < 8; ++t)
+            if ((nb[q] >> t) & 1u) best = min(best, sv[ns[t]] + 1);
           if (best < d[q]) {
             d[q] = best;
-            vd[px[q]] = best;
+            sv[lane + 32 * q] = best;
             changed = true;
           }
         }
@@ -364,12 +378,12 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         if (px[q] < 0 || d[q] == 1) continue;
-        int32_t dv[8];
-        gather8(vd, w, px[q], nb[q], kInfD, dv);
+        const uint8_t* ns = s_nbs[wl][lane + 32 * q];
 #pragma unroll
         for (int t = 7; t >= 0; --t)  // the first (minimum-index) match wins
-          if (dv[t] == d[q] - 1) dir[px[q]] = (uint8_t)t;
+          if (((nb[q] >> t) & 1u) && sv[ns[t]] == d[q] - 1) dir[px[q]] = (uint8_t)t;
       }
+      __syncwarp();
     } else {
       // long range: per-member (pixel, neighbour mask) cached in scratch
       for (int k = s0 + lane; k < e; k += 32) {
@@ -531,14 +545,20 @@ __global__ void __launch_bounds__(256)
 k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag, int32_t ws_h,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
-             uint16_t* Fw, int2* __restrict__ scratch) {
+             uint16_t* Fw, int2* __restrict__ scratch, uint8_t* slotmap) {
   pdl_enter();
   const int w = (int)dw.d;
   constexpr int kPer = 4;
+  // small ranges iterate in shared memory: member values by slot (index in
+  // the warp's range) and each member's neighbour slots, so a relaxation
+  // sweep costs shared-memory latency instead of an L2 round trip
+  __shared__ int32_t s_val[8][32 * kPer];
+  __shared__ uint8_t s_nbs[8][32 * kPer][8];
   const int nmem = (int)(*alloc & 0xFFFFFFFFull);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   volatile uint16_t* vf = Fw;
+  volatile int32_t* sv = s_val[wl];
   for (int w0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < nmem;
        w0 += nwarps * 32) {
     int s0, e;
@@ -558,8 +578,17 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
           int32_t fixed;
           nb[q] = hmax_nbrs(h, dw, mask, dq, sflag, px[q], fixed);
           f[q] = min(d[q], max(d[q] > ws_h ? d[q] - ws_h : 0, fixed));
-          vf[px[q]] = (uint16_t)(f[q] + 1);
+          sv[lane + 32 * q] = f[q];
+          slotmap[px[q]] = (uint8_t)(lane + 32 * q);
         }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        if (px[q] < 0) continue;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if ((nb[q] >> t) & 1u) s_nbs[wl][lane + 32 * q][t] = slotmap[nbr_index(w, px[q], t)];
       }
       __syncwarp();
       while (true) {
@@ -567,20 +596,24 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           if (px[q] < 0 || f[q] == d[q]) continue;
-          int32_t fv[8];
-          gather8(vf, w, px[q], nb[q], 0, fv);
           int32_t best = f[q];
+          const uint8_t* ns = s_nbs[wl][lane + 32 * q];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) best = max(best, fv[t] - 1);
+          for (int t = 0; t < 8; ++t)
+            if ((nb[q] >> t) & 1u) best = max(best, sv[ns[t]]);  // s_val holds F (not F + 1)
           best = min(best, d[q]);
           if (best > f[q]) {
             f[q] = best;
-            vf[px[q]] = (uint16_t)(best + 1);
+            sv[lane + 32 * q] = best;
             changed = true;
           }
         }
         if (!__any_sync(0xFFFFFFFFu, changed)) break;
       }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q)
+        if (px[q] >= 0) Fw[px[q]] = (uint16_t)(f[q] + 1);
+      __syncwarp();
     } else {
       // long range: per-member (pixel, neighbour mask | dq << 8) cached in scratch
       for (int k = s0 + lane; k < e; k += 32) {
@@ -743,7 +776,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, list, count, par, basin, slot, ctx->lroots));
     RTG_LAUNCH("k_ws_scatter");
     RTG_CUDA(launch_k(ctx, k_hmax_solve, g, 256, 0, (int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
-                                             alloc, Fw, member_scratch));
+                                             alloc, Fw, member_scratch,
+                                             ctx->m2 /* slot map: the EDT row distances are dead */));
     RTG_LAUNCH("k_hmax_solve");
   }
   prof_mark(ctx, RTG_STAGE_WATERSHED);
@@ -769,7 +803,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                                            ctx->lroots));
   RTG_LAUNCH("k_ws_scatter");
   RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, dir,
-                                           delta, member_scratch));
+                                           delta, member_scratch, ctx->m2 /* slot map */));
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
