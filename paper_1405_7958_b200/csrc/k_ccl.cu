@@ -911,13 +911,34 @@ __global__ void k_fb_total(const int32_t* __restrict__ lroots, const int32_t* __
   }
 }
 
-// Output mask of the joint path, 4 pixels per thread (the four dependent
-// gathers per pixel want many threads in flight), plus the foreground list
-// and 1-bit plane of that mask (what k_fg_list would build).
+// The keep decision of every LOCAL root (global root -> top-level ancestor
+// -> subtree area in range), stored at the local root's pixel: the per-pixel
+// filter then needs one byte gather instead of three dependent i32 ones.
+__global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
+                          const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
+                          const int32_t* __restrict__ total, int32_t lo, int32_t hi,
+                          uint8_t* __restrict__ keep) {
+  pdl_enter();
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t lr = lroots[2 * k];
+    const int32_t t = top[roots[lr]];
+    bool kp = false;
+    if (t >= 0) {
+      const int32_t a = total[t];
+      kp = a >= lo && a <= hi;
+    }
+    keep[lr] = kp ? 1 : 0;
+  }
+}
+
+// Output mask of the joint path, 4 pixels per thread: local root -> its keep
+// byte; plus the foreground list and 1-bit plane of that mask (what
+// k_fg_list would build).
 __global__ void __launch_bounds__(256)
-k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
-            const int32_t* __restrict__ total, int32_t lo, int32_t hi, uint8_t* __restrict__ out,
-            uint32_t* __restrict__ bits, int32_t* __restrict__ list, int32_t* __restrict__ count) {
+k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const uint8_t* __restrict__ keep,
+            uint8_t* __restrict__ out, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
+            int32_t* __restrict__ count) {
   pdl_enter();
   __shared__ int32_t sm[9];
   const bool vec = (reinterpret_cast<uintptr_t>(out) & 3) == 0 &&
@@ -933,18 +954,10 @@ k_fb_filter(int64_t n, const int32_t* __restrict__ roots, const int32_t* __restr
 #pragma unroll
       for (int k = 0; k < 4; ++k) v[k] = p0 + k < n ? roots[p0 + k] : -1;
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;   // global root
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? top[v[k]] : -1;     // top-level ancestor
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (v[k] >= 0) {
-        const int32_t a = total[v[k]];
-        if (a >= lo && a <= hi) m |= 1u << k;
-      }
-    }
+    for (int k = 0; k < 4; ++k)
+      if (v[k] >= 0 && keep[v[k]]) m |= 1u << k;
     if (vec && p0 + 4 <= n) {
       *reinterpret_cast<uint32_t*>(out + p0) =
           (m & 1u) | ((m & 2u) << 7) | ((m & 4u) << 14) | ((m & 8u) << 21);
@@ -1138,7 +1151,11 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
                                     3}));
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
-  RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, top, total, min_area, max_area, out,
+  uint8_t* keep = ctx->m2;  // free until the EDT's row distances
+  RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
+                    max_area, keep));
+  RTG_LAUNCH("k_fb_keep");
+  RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, (const uint8_t*)keep, out,
                                                bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
   RTG_LAUNCH("k_fb_filter");
   return RTG_OK;
