@@ -541,11 +541,13 @@ __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* _
                             const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
                             const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank) {
   pdl_enter();
+  // the final label (rank of the global root + 1) of every LOCAL root, so the
+  // per-pixel relabel needs one gather (local root -> label)
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t r = lroots[2 * k];
-    if (roots[r] != r) continue;
-    rank[r] = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u));
+    const int32_t lr = lroots[2 * k];
+    const int32_t r = roots[lr];
+    rank[lr] = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u)) + 1;
   }
 }
 
@@ -562,14 +564,12 @@ __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
       const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
       int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? rank[v[k]] + 1 : 0;
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? rank[v[k]] : 0;  // label of the local root
       *reinterpret_cast<int4*>(labels + i0) = make_int4(v[0], v[1], v[2], v[3]);
     } else {
       for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
-        const int32_t r = root_of(roots, i);
-        labels[i] = r >= 0 ? rank[r] + 1 : 0;
+        const int32_t lr = roots[i];
+        labels[i] = lr >= 0 ? rank[lr] : 0;
       }
     }
   }
