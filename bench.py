@@ -196,7 +196,7 @@ def main():
     ap.add_argument("--impl", default="rtg", choices=["rtg", "reference"])
     ap.add_argument("--tiles-per-rank", type=int, default=80,
                     help="tiles each rank processes per step (80 x 8 GPUs ~ one 625-tile WSI)")
-    ap.add_argument("--streams", type=int, default=3, help="concurrent contexts per GPU")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent contexts per GPU")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -1138,7 +1138,13 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   int32_t* top = ctx->i32c;
   int32_t* total = ctx->labels;
   int32_t* lcount = ctx->misc + 8;
-  RTG_TRY(zero_async(ctx, ZeroList{{lcount}, {sizeof(int32_t)}, 1}));
+  // one launch for the stage's counters: local-root count, foreground-list
+  // count and the pad words of the foreground bit plane (written by k_fb_filter)
+  uint32_t* bits_base = ctx->fg_bits;
+  RTG_TRY(zero_async(ctx, ZeroList{{lcount, ctx->misc + 4, bits_base, bits_base + kBitPad + n / 32},
+                                    {sizeof(int32_t), sizeof(int32_t), sizeof(uint32_t) * kBitPad,
+                                     sizeof(uint32_t) * (kBitPad + 1)},
+                                    4}));
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 
@@ -1159,11 +1165,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_LAUNCH("k_fb_tree");
   RTG_CUDA(launch_k(ctx, k_fb_total, gl, 256, 0, ctx->lroots, lcount, roots, counts, top, total));
   RTG_LAUNCH("k_fb_total");
-  uint32_t* bits_base = ctx->fg_bits;
-  RTG_TRY(zero_async(ctx, ZeroList{{ctx->misc + 4, bits_base, bits_base + kBitPad + n / 32},
-                                    {sizeof(int32_t), sizeof(uint32_t) * kBitPad,
-                                     sizeof(uint32_t) * (kBitPad + 1)},
-                                    3}));
+
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
   uint8_t* keep = ctx->m2;  // free until the EDT's row distances

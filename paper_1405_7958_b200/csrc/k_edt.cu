@@ -521,7 +521,7 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   int32_t* any_zero = ctx->misc + 2;
   int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;
-  RTG_TRY(zero_async(ctx, ZeroList{{any_zero}, {2 * sizeof(int32_t)}, 1}));
+  // any_zero / need_full were zeroed by the caller (watershed)
   uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
   const FastDiv dwv = make_div((uint32_t)w);
   RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,

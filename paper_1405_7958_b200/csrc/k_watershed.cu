@@ -734,10 +734,18 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* comp_size = comp_root + n;
   // per-member cache of long component ranges (the arena's second half)
   int2* member_scratch = reinterpret_cast<int2*>(ctx->arena + 8 * n);
+  // counters of the whole o6/o7 chain, zeroed here in one launch: misc[1]
+  // HMAX suspect count, misc[2..3] EDT flags (edt_list), misc[5] flat-pixel
+  // count, misc[16..17] HMAX component allocator, misc[18..19] plateau one
+  // (misc[4], the foreground count, was built by the caller or fg_list)
   auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
-  RTG_TRY(zero_async(ctx, ZeroList{{sep, basin},
-                                    {(size_t)n, want_basin ? sizeof(int32_t) * (size_t)n : 0},
-                                    2}));
+  auto* walloc = reinterpret_cast<unsigned long long*>(ctx->misc + 18);
+  RTG_TRY(zero_async(ctx, ZeroList{{sep, ctx->misc + 1, ctx->misc + 5, alloc},
+                                    {(size_t)n, 3 * sizeof(int32_t), sizeof(int32_t),
+                                     2 * sizeof(unsigned long long)},
+                                    4}));
+  if (want_basin)
+    RTG_TRY(zero_async(ctx, ZeroList{{basin}, {sizeof(int32_t) * (size_t)n}, 1}));
   prof_mark(ctx, RTG_STAGE_EDT);
   if (!list_ready) RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
   const uint32_t* fgbits = ctx->fg_bits + kBitPad;  // neighbour tests of the list kernels
@@ -761,8 +769,6 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     int32_t* par = ctx->i32c;
     int32_t* slot = ctx->i32b;
     uint8_t* sflag = ctx->m1;
-    RTG_TRY(zero_async(ctx, ZeroList{{count, alloc},
-                                      {sizeof(int32_t), sizeof(unsigned long long)}, 2}));
     RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
                                             par, basin, list, count));
     RTG_LAUNCH("k_hmax_init");
@@ -785,9 +791,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* delta = ctx->i32b;
   int32_t* par = ctx->i32c;
   uint8_t* flat = ctx->m1;
-  int32_t* flat_count = ctx->misc + 1;
-  RTG_TRY(zero_async(ctx, ZeroList{{flat_count, alloc},
-                                    {sizeof(int32_t), sizeof(unsigned long long)}, 2}));
+  int32_t* flat_count = ctx->misc + 5;
   RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, dir, par, basin,
                                           flat, ctx->flat_list, flat_count));
   RTG_LAUNCH("k_ws_arrows");
@@ -796,13 +800,13 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_union");
   RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, dir, par, basin, delta));
   RTG_LAUNCH("k_ws_roots");
-  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir, alloc,
+  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir, walloc,
                                             comp_root, comp_size));
   RTG_LAUNCH("k_ws_classify");
   RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots));
   RTG_LAUNCH("k_ws_scatter");
-  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, alloc, dir,
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, walloc, dir,
                                            delta, member_scratch, ctx->m2 /* slot map */));
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));

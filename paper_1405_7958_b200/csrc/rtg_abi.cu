@@ -466,7 +466,7 @@ int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[RTG_NUM_STATS]) {
   if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
   RTG_CUDA(cudaSetDevice(ctx->device));
   RTG_CUDA(cudaStreamSynchronize(ctx->stream));
-  int32_t misc[4];
+  int32_t misc[8];
   int64_t st[RTG_NUM_STATS];
   RTG_CUDA(cudaMemcpy(misc, ctx->misc, sizeof(misc), cudaMemcpyDeviceToHost));
   RTG_CUDA(cudaMemcpy(st, ctx->stats, sizeof(st), cudaMemcpyDeviceToHost));
@@ -474,7 +474,7 @@ int rtg_ctx_stats(rtg_ctx* ctx, int64_t out[RTG_NUM_STATS]) {
   for (int i = 0; i < RTG_NUM_STATS; ++i) out[i] = st[i];
   out[0] = misc[0];
   out[1] = st[4] + st[6] + st[8] + st[10];
-  out[2] = misc[1];
+  out[2] = misc[5];  // flat (plateau) pixels of the watershed
   out[3] = misc[3];
   return RTG_OK;
 }
