@@ -178,8 +178,8 @@ void hema_lut(const rtg_params* p, HemaLut* lut);
 
 // Zeroes up to four device regions with one kernel of the launch chain.
 struct ZeroList {
-  void* ptr[4];
-  uint64_t bytes[4];
+  void* ptr[8];
+  uint64_t bytes[8];
   int count;
 };
 int zero_async(rtg_ctx* ctx, const ZeroList& z);
@@ -207,8 +207,12 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
 // (or, for a local root, the global root); root_of(roots, p) is the minimum
 // linear index of p's component (-1 = background).  counts, when given,
 // receives every component's pixel count at its global root.
+// prezeroed: the caller already cleared the counters ccl_label_zero names.
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots, int32_t* counts = nullptr);
+              int conn, int32_t* roots, int32_t* counts = nullptr, bool prezeroed = false);
+// Appends to z the buffers a labelling CCL (ccl_roots + ccl_canonical) of an
+// h x w mask needs cleared: local-root count, root bitmap, look-back status.
+void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z);
 __device__ __forceinline__ int32_t root_of(const int32_t* __restrict__ roots, int64_t i) {
   const int32_t v = roots[i];
   return v < 0 ? -1 : roots[v];

@@ -1042,16 +1042,18 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
 // OR of the seed bits; bitmap (if given, zeroed here) marks global roots.
 template <class P>
 int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
-            int32_t* counts, int32_t* flags, uint32_t* bitmap) {
+            int32_t* counts, int32_t* flags, uint32_t* bitmap, bool prezeroed = false) {
   int32_t* lcount = ctx->misc + 8;
-  // with a bitmap (the canonical labelling follows): also the look-back
-  // status words of k_bm_scan
-  const size_t nstatus = (size_t)ceil_div(ceil_div(h * w, 32), kBmChunk) + 1;
-  RTG_TRY(zero_async(ctx, ZeroList{{lcount, bitmap, ctx->scan_buf},
-                                    {sizeof(int32_t),
-                                     bitmap ? sizeof(uint32_t) * (size_t)ceil_div(h * w, 32) : 0,
-                                     bitmap ? sizeof(unsigned long long) * nstatus : 0},
-                                    3}));
+  if (!prezeroed) {
+    // with a bitmap (the canonical labelling follows): also the look-back
+    // status words of k_bm_scan
+    ZeroList z{{lcount}, {sizeof(int32_t)}, 1};
+    if (bitmap) {
+      z.count = 0;
+      ccl_label_zero(ctx, h, w, z);
+    }
+    RTG_TRY(zero_async(ctx, z));
+  }
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
@@ -1099,8 +1101,19 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
 }
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
-              int32_t* roots, int32_t* counts) {
-  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm);
+              int32_t* roots, int32_t* counts, bool prezeroed) {
+  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed);
+}
+
+void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
+  const int64_t nwords = ceil_div(h * w, 32);
+  const size_t nstatus = (size_t)ceil_div(nwords, kBmChunk) + 1;
+  z.ptr[z.count] = ctx->misc + 8;
+  z.bytes[z.count++] = sizeof(int32_t);
+  z.ptr[z.count] = ctx->root_bm;
+  z.bytes[z.count++] = sizeof(uint32_t) * (size_t)nwords;
+  z.ptr[z.count] = ctx->scan_buf;
+  z.bytes[z.count++] = sizeof(unsigned long long) * nstatus;
 }
 
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,

@@ -740,10 +740,13 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // (misc[4], the foreground count, was built by the caller or fg_list)
   auto* alloc = reinterpret_cast<unsigned long long*>(ctx->misc + 16);
   auto* walloc = reinterpret_cast<unsigned long long*>(ctx->misc + 18);
-  RTG_TRY(zero_async(ctx, ZeroList{{sep, ctx->misc + 1, ctx->misc + 5, alloc},
-                                    {(size_t)n, 3 * sizeof(int32_t), sizeof(int32_t),
-                                     2 * sizeof(unsigned long long)},
-                                    4}));
+  // ... and, in the same launch, what the labelling of the separated mask
+  // (o8, ccl_roots(..., prezeroed)) needs cleared
+  ZeroList z{{sep, ctx->misc + 1, ctx->misc + 5, alloc},
+             {(size_t)n, 3 * sizeof(int32_t), sizeof(int32_t), 2 * sizeof(unsigned long long)},
+             4};
+  ccl_label_zero(ctx, h, w, z);
+  RTG_TRY(zero_async(ctx, z));
   if (want_basin)
     RTG_TRY(zero_async(ctx, ZeroList{{basin}, {sizeof(int32_t) * (size_t)n}, 1}));
   prof_mark(ctx, RTG_STAGE_EDT);

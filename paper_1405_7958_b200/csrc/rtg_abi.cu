@@ -142,7 +142,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   }
   // o8 BWLabel (canonical)
   prof_mark(ctx, RTG_STAGE_LABEL);
-  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a));
+  // the tiled watershed cleared the labelling's counters with its own
+  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0));
   RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out));
   // o9 features
   if (with_features) {
