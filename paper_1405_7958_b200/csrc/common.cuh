@@ -185,9 +185,11 @@ struct ZeroList {
 int zero_async(rtg_ctx* ctx, const ZeroList& z);
 
 // ---- launchers (one translation unit each) ---------------------------------
+// clear (optional): a counter word the next stage needs zeroed, cleared by the
+// streaming kernel itself (one launch fewer in the pipeline).
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                        int64_t pitch, const rtg_params* p, uint8_t* hema,
-                       uint8_t* marker, uint8_t* tissue);
+                       uint8_t* marker, uint8_t* tissue, int32_t* clear = nullptr);
 int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
                      int64_t n, int32_t thresh, uint8_t* out);
 
@@ -357,9 +359,10 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
 // ReconToNuclei candidates = (recon(max(H - h, 0), H) >= t) && tissue by
 // threshold decomposition: union-find components of {H >= t} holding a pixel
 // with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.
+// prezeroed: the local-root counter (misc[8]) is already zero.
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out);
+                       uint8_t* out, bool prezeroed = false);
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);

@@ -1080,7 +1080,7 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
 
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out) {
+                       uint8_t* out, bool prezeroed) {
   (void)scratch;
   const int64_t n = h * w;
   if (t <= 0) {  // R >= t everywhere: the candidates are the tissue mask
@@ -1091,7 +1091,7 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   int32_t* flag = ctx->i32b;
   const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
   const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
-  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr));
+  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed));
   RTG_CUDA(launch_k(ctx, k_seed_local, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
                     flag));
   RTG_LAUNCH("k_seed_local");

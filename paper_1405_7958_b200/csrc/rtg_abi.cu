@@ -103,7 +103,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
   RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, iwpp_recon ? ctx->recon : nullptr,
-                             ctx->tissue));
+                             ctx->tissue, iwpp_recon ? nullptr : ctx->misc + 8));
   // o3 ReconToNuclei: candidates = recon(max(H - h, 0), H) >= nuc_thresh && tissue
   prof_mark(ctx, RTG_STAGE_RECON);
   if (iwpp_recon) {
@@ -111,7 +111,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
   } else {
     RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
-                               p->recon_conn, ctx->m1, ctx->m1));
+                               p->recon_conn, ctx->m1, ctx->m1, /*prezeroed=*/true));
   }
   if (ctx->fill_impl == 0 && ctx->ws_impl == 0) {
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
