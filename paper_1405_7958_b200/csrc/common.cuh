@@ -185,11 +185,18 @@ struct ZeroList {
 int zero_async(rtg_ctx* ctx, const ZeroList& z);
 
 // ---- launchers (one translation unit each) ---------------------------------
-// clear (optional): a counter word the next stage needs zeroed, cleared by the
-// streaming kernel itself (one launch fewer in the pipeline).
+// Up to six small int32 regions (counters, pad words) for a kernel's first
+// CTA to clear on the way.
+struct ClearList {
+  int32_t* p[6];
+  int32_t n[6];
+  int count;
+};
+// clear (optional): counters the next stages need zeroed, cleared by the
+// streaming kernel itself (zeroing launches fewer in the pipeline).
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                        int64_t pitch, const rtg_params* p, uint8_t* hema,
-                       uint8_t* marker, uint8_t* tissue, int32_t* clear = nullptr);
+                       uint8_t* marker, uint8_t* tissue, const ClearList* clear = nullptr);
 int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
                      int64_t n, int32_t thresh, uint8_t* out);
 
@@ -354,8 +361,10 @@ __device__ __forceinline__ void uf_unite_g(int32_t* par, int32_t a, int32_t b) {
 // Canonical compaction: labels = 1 + rank of root in raster order; *d_n.
 // Must directly follow the ccl_roots call that built `roots` (it reuses that
 // call's local-root list and root bitmap).
+// clear_acc (optional): the feature accumulators are reset for every label
+// while the ranks are assigned (the feature stage then skips k_feat_clear).
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
-                  int32_t* labels, int32_t* d_n);
+                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc = nullptr);
 // ReconToNuclei candidates = (recon(max(H - h, 0), H) >= t) && tissue by
 // threshold decomposition: union-find components of {H >= t} holding a pixel
 // with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.
@@ -370,8 +379,12 @@ int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
 // labelling of foreground (8-conn) and background (4-conn) components.
 // Also builds the foreground list + bit plane of `out` (ctx->fg_list,
 // misc[4], ctx->fg_bits) for the sparse watershed.
+// prezeroed: its counters (misc[9], misc[4]) and the bit-plane pads were
+// cleared upstream (the streaming kernel's ClearList).
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out);
+                    int32_t max_area, uint8_t* out, bool prezeroed = false);
+// What fill_area_joint needs cleared, as a ClearList.
+ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
                 int32_t min_area, int32_t max_area, int32_t* counts,
                 uint8_t* out);
@@ -404,7 +417,8 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
 // list (optional): a foreground list covering every labelled pixel.
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              int64_t h, int64_t w, const int32_t* d_n, float* out,
-             const int32_t* list = nullptr, const int32_t* list_count = nullptr);
+             const int32_t* list = nullptr, const int32_t* list_count = nullptr,
+             bool acc_cleared = false);
 
 // f4 Canny edges (u8 0/1) of an intensity plane; uses i32a/i32b and m1/m2.
 int canny(rtg_ctx* ctx, const uint8_t* intensity, int64_t h, int64_t w, int32_t low, int32_t high,

@@ -539,7 +539,8 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
 
 __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                             const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
-                            const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank) {
+                            const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank,
+                            FeatureAcc acc, bool clear_acc) {
   pdl_enter();
   // the final label (rank of the global root + 1) of every LOCAL root, so the
   // per-pixel relabel needs one gather (local root -> label)
@@ -547,7 +548,18 @@ __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* _
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t lr = lroots[2 * k];
     const int32_t r = roots[lr];
-    rank[lr] = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u)) + 1;
+    const int32_t label = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u)) + 1;
+    rank[lr] = label;
+    // each label once (at its global root): reset its feature accumulators
+    if (clear_acc && lr == r && label <= acc.cap) {
+      const int64_t i = label - 1;
+#pragma unroll
+      for (int f = 0; f < kSumFields; ++f) acc.sums[(int64_t)f * acc.cap + i] = 0ull;
+#pragma unroll
+      for (int f = 0; f < kMinFields; ++f) acc.mins[(int64_t)f * acc.cap + i] = INT32_MAX;
+#pragma unroll
+      for (int f = 0; f < kMaxFields; ++f) acc.maxs[(int64_t)f * acc.cap + i] = -1;
+    }
   }
 }
 
@@ -1117,7 +1129,7 @@ void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
 }
 
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
-                  int32_t* labels, int32_t* d_n) {
+                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc) {
   const int64_t n = h * w;
   const int64_t nwords = ceil_div(n, 32);
   const int nchunks = (int)ceil_div(nwords, kBmChunk);
@@ -1127,7 +1139,9 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                     ctx->root_wprefix, d_n));
   RTG_LAUNCH("k_bm_scan");
   RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
-                                                         ctx->root_bm, ctx->root_wprefix, rank));
+                                                         ctx->root_bm, ctx->root_wprefix, rank,
+                                                         clear_acc ? *clear_acc : ctx->acc,
+                                                         clear_acc != nullptr));
   RTG_LAUNCH("k_root_rank");
   RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
@@ -1143,21 +1157,36 @@ int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n, int32_t min_area,
   return RTG_OK;
 }
 
+ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w) {
+  const int64_t n = h * w;
+  uint32_t* bits_base = ctx->fg_bits;
+  return ClearList{{ctx->misc + 4, ctx->misc + 9, reinterpret_cast<int32_t*>(bits_base),
+                    reinterpret_cast<int32_t*>(bits_base + kBitPad + n / 32)},
+                   {1, 1, kBitPad, kBitPad + 1},
+                   4};
+}
+
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out) {
+                    int32_t max_area, uint8_t* out, bool prezeroed) {
   const int64_t n = h * w;
   int32_t* roots = ctx->i32a;
   int32_t* counts = ctx->i32b;
   int32_t* top = ctx->i32c;
   int32_t* total = ctx->labels;
-  int32_t* lcount = ctx->misc + 8;
-  // one launch for the stage's counters: local-root count, foreground-list
-  // count and the pad words of the foreground bit plane (written by k_fb_filter)
+  int32_t* lcount = ctx->misc + 9;  // its own word: cleared with the other counters
+  // the stage's counters: local-root count, foreground-list count and the
+  // pad words of the foreground bit plane (written by k_fb_filter)
   uint32_t* bits_base = ctx->fg_bits;
-  RTG_TRY(zero_async(ctx, ZeroList{{lcount, ctx->misc + 4, bits_base, bits_base + kBitPad + n / 32},
-                                    {sizeof(int32_t), sizeof(int32_t), sizeof(uint32_t) * kBitPad,
-                                     sizeof(uint32_t) * (kBitPad + 1)},
-                                    4}));
+  if (!prezeroed) {
+    const ClearList c = fill_area_clear(ctx, h, w);
+    ZeroList z{};
+    for (int r = 0; r < c.count; ++r) {
+      z.ptr[r] = c.p[r];
+      z.bytes[r] = sizeof(int32_t) * (uint64_t)c.n[r];
+    }
+    z.count = c.count;
+    RTG_TRY(zero_async(ctx, z));
+  }
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 

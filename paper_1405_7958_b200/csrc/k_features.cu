@@ -401,11 +401,13 @@ __global__ void k_feat_finalize(const int32_t* __restrict__ d_n, FeatureAcc acc,
 
 int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
              int64_t h, int64_t w, const int32_t* d_n, float* out, const int32_t* list,
-             const int32_t* list_count) {
+             const int32_t* list_count, bool acc_cleared) {
   const int cap = ctx->acc.cap;
   const int gclear = (int)ceil_div(cap, 256);
-  RTG_CUDA(launch_k(ctx, k_feat_clear, gclear, 256, 0, d_n, ctx->acc));
-  RTG_LAUNCH("k_feat_clear");
+  if (!acc_cleared) {
+    RTG_CUDA(launch_k(ctx, k_feat_clear, gclear, 256, 0, d_n, ctx->acc));
+    RTG_LAUNCH("k_feat_clear");
+  }
   // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
   if (list && h <= 4096 && w <= 4096) {
     RTG_CUDA(launch_k(ctx, k_feat_list, ctx->num_sms * 8, 256, 0, list, list_count, labels, intensity,

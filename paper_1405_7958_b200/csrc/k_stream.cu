@@ -69,9 +69,11 @@ template <bool kMarker>
 __global__ void __launch_bounds__(kCdThreads, kCdBlocksPerSm)
 k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
-                  uint4* __restrict__ marker, uint4* __restrict__ tissue, int32_t* clear) {
+                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear) {
   pdl_enter();
-  if (clear && blockIdx.x == 0 && threadIdx.x == 0) *clear = 0;
+  if (blockIdx.x == 0)
+    for (int r = 0; r < clear.count; ++r)
+      for (int i = threadIdx.x; i < clear.n[r]; i += blockDim.x) clear.p[r][i] = 0;
   extern __shared__ __align__(16) int32_t cd_smem[];
   int32_t* lrep = cd_smem;                   // [3][256][32]
   int32_t* lsmall = cd_smem + 3 * 256 * 32;  // [3][256]
@@ -244,7 +246,9 @@ void hema_lut(const rtg_params* p, HemaLut* lut) {
 
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                        int64_t pitch, const rtg_params* p, uint8_t* hema,
-                       uint8_t* marker, uint8_t* tissue, int32_t* clear) {
+                       uint8_t* marker, uint8_t* tissue, const ClearList* clear) {
+  ClearList cl{};
+  if (clear) cl = *clear;
   CdParams cp;
   hema_lut(p, &cp.lut);
   cp.bg = p->bg_thresh;
@@ -275,8 +279,8 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
       RTG_CUDA(launch_k(ctx, kern, blocks, kCdThreads, kCdSmem,
                         reinterpret_cast<const uint4*>(rgb), (uint32_t)ngroups, iters, cp,
                         reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-                        reinterpret_cast<uint4*>(tissue), clear));
-      clear = nullptr;
+                        reinterpret_cast<uint4*>(tissue), cl));
+      cl.count = 0;
       RTG_LAUNCH("k_colordeconv_vec");
     }
     done = ngroups * 16;
@@ -289,7 +293,15 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                                                       hema, marker, tissue));
     RTG_LAUNCH("k_colordeconv_px");
   }
-  if (clear) RTG_TRY(zero_async(ctx, ZeroList{{clear}, {sizeof(int32_t)}, 1}));
+  if (cl.count) {  // no vector launch: a separate zeroing launch
+    ZeroList z{};
+    for (int r = 0; r < cl.count; ++r) {
+      z.ptr[r] = cl.p[r];
+      z.bytes[r] = sizeof(int32_t) * (uint64_t)cl.n[r];
+    }
+    z.count = cl.count;
+    RTG_TRY(zero_async(ctx, z));
+  }
   return RTG_OK;
 }
 

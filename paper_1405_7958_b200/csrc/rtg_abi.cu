@@ -102,8 +102,16 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   const bool iwpp_recon = ctx->recon_impl == 1;
   // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
+  // the streaming kernel's first CTA clears the reconstruction CCL's
+  // local-root count (uf path) and the joint fill/area stage's counters
+  const bool joint = ctx->fill_impl == 0 && ctx->ws_impl == 0;
+  ClearList cl = joint ? fill_area_clear(ctx, h, w) : ClearList{};
+  if (!iwpp_recon) {
+    cl.p[cl.count] = ctx->misc + 8;
+    cl.n[cl.count++] = 1;
+  }
   RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, iwpp_recon ? ctx->recon : nullptr,
-                             ctx->tissue, iwpp_recon ? nullptr : ctx->misc + 8));
+                             ctx->tissue, &cl));
   // o3 ReconToNuclei: candidates = recon(max(H - h, 0), H) >= nuc_thresh && tissue
   prof_mark(ctx, RTG_STAGE_RECON);
   if (iwpp_recon) {
@@ -117,7 +125,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
     // mask itself is never materialised)
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
-    RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3));
+    RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3,
+                            /*prezeroed=*/true));
   } else {
     // o4 FillHoles of the nucleus candidates
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
@@ -144,7 +153,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   prof_mark(ctx, RTG_STAGE_LABEL);
   // the tiled watershed cleared the labelling's counters with its own
   RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0));
-  RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out));
+  // the ranking pass also resets the feature accumulators of every label
+  RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out, with_features ? &ctx->acc : nullptr));
   // o9 features
   if (with_features) {
     prof_mark(ctx, RTG_STAGE_FEATURES);
@@ -152,7 +162,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // superset of the labelled pixels)
     const bool sparse = ctx->ws_impl == 0;
     RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features, sparse ? ctx->fg_list : nullptr,
-                     sparse ? ctx->misc + 4 : nullptr));
+                     sparse ? ctx->misc + 4 : nullptr, /*acc_cleared=*/true));
   }
   prof_mark(ctx, -1);
   return RTG_OK;
