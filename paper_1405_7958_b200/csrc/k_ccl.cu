@@ -533,7 +533,9 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
       reinterpret_cast<int4*>(wprefix + base)[q] =
           make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
   } else {
-    for (int k = 0; k < kBmPerThread && base + k < nwords; ++k) wprefix[base + k] = o[k];
+#pragma unroll
+    for (int k = 0; k < kBmPerThread; ++k)  // unrolled: o[] stays in registers
+      if (base + k < nwords) wprefix[base + k] = o[k];
   }
 }
 

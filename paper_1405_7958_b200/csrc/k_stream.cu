@@ -71,9 +71,12 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
                   uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear) {
   pdl_enter();
-  if (blockIdx.x == 0)
-    for (int r = 0; r < clear.count; ++r)
-      for (int i = threadIdx.x; i < clear.n[r]; i += blockDim.x) clear.p[r][i] = 0;
+  if (blockIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < 6; ++r)  // constant indices: the list stays in parameter space
+      if (r < clear.count)
+        for (int i = threadIdx.x; i < clear.n[r]; i += blockDim.x) clear.p[r][i] = 0;
+  }
   extern __shared__ __align__(16) int32_t cd_smem[];
   int32_t* lrep = cd_smem;                   // [3][256][32]
   int32_t* lsmall = cd_smem + 3 * 256 * 32;  // [3][256]
