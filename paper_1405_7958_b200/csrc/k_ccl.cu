@@ -672,7 +672,8 @@ struct FbSmem {
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntiles,
               int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
-              int32_t* __restrict__ lcount, int32_t* __restrict__ counts) {
+              int32_t* __restrict__ lcount, int32_t* __restrict__ counts,
+              int32_t* __restrict__ total) {
   pdl_enter();
   __shared__ FbSmem<kTileWarps> S;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -800,6 +801,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
     lroots[2 * base + 1] = (int32_t)((a & 0x7FFFu) | ((a & 0x8000u) ? kSeedBit : 0u));
     ++base;
     counts[g] = 0;
+    total[g] = 0;  // subtree areas are accumulated straight from k_fb_tree
   }
   __syncwarp();
   // each lane rewrites only its own runs' entries
@@ -880,8 +882,8 @@ __global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int 
   }
 }
 
-// Top-level ancestor of every global root (-1 for the outside); totals zeroed
-// at the top-level roots.
+// Top-level ancestor of every global root (-1 for the outside), and each
+// root's area added into its top-level ancestor's subtree total.
 __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                           const uint8_t* __restrict__ m, int w,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
@@ -908,19 +910,7 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
       }
     }
     top[r] = t;
-    if (t == r) total[r] = 0;
-  }
-}
-
-__global__ void k_fb_total(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
-                           const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
-                           const int32_t* __restrict__ top, int32_t* __restrict__ total) {
-  pdl_enter();
-  const int n = *lcount;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t r = lroots[2 * k];
-    if (roots[r] != r) continue;
-    const int32_t t = top[r];
+    // totals were cleared at every local root by k_ccl_tile_fb
     if (t >= 0) atomicAdd(total + t, counts[r] & ~(int32_t)kSeedBit);
   }
 }
@@ -1192,7 +1182,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 
-      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts));
+      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, total));
   RTG_LAUNCH("k_ccl_tile_fb");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
@@ -1207,8 +1197,6 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_CUDA(launch_k(ctx, k_fb_tree, gl, 256, 0, ctx->lroots, lcount, cand, (int)w, roots, counts, top,
                                          total));
   RTG_LAUNCH("k_fb_tree");
-  RTG_CUDA(launch_k(ctx, k_fb_total, gl, 256, 0, ctx->lroots, lcount, roots, counts, top, total));
-  RTG_LAUNCH("k_fb_total");
 
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
