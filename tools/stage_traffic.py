@@ -23,7 +23,7 @@ STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
     ("markers", "k_hmax_init", None),
     ("watershed", "k_ws_arrows", None),
     ("label", "k_ccl_tile", "k_ws_separate"),
-    ("features", "k_feat_clear", None),
+    ("features", "k_feat_list", None),
 ]
 
 
