@@ -294,10 +294,18 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
       if (y >= h) continue;
       const uint32_t st = b & ~(b << 1);
       int32_t o[4];
+      const uint32_t fg4 = (b >> cq) & 0xFu;
+      if (!fg4) {
+        o[0] = o[1] = o[2] = o[3] = -1;
+      } else if (fg4 == 0xFu && !((st >> (cq + 1)) & 7u)) {
+        // four foreground pixels of one run: one lookup
+        o[0] = o[1] = o[2] = o[3] = (int32_t)inf[r * 16 + __popc(st & ((2u << cq) - 1u)) - 1];
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = cq + j;
-        o[j] = ((b >> c) & 1u) ? (int32_t)inf[r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : -1;
+        for (int j = 0; j < 4; ++j) {
+          const int c = cq + j;
+          o[j] = ((b >> c) & 1u) ? (int32_t)inf[r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : -1;
+        }
       }
       *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
     }
@@ -819,11 +827,23 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       const int y = y0 + r;
       const uint32_t st = __shfl_sync(kFull, allst, r);
       if (y >= h) continue;
+      // run of pixel cq, then the runs starting inside cq+1..cq+3 (usually
+      // none: one shared-memory lookup and one index for all four pixels)
+      const int i0 = r * 32 + __popc(st & ((2u << cq) - 1u)) - 1;
+      const uint32_t inner = (st >> (cq + 1)) & 7u;
       int32_t o[4];
+      {
+        const int32_t lo = par[i0];
+        o[0] = (y0 + (lo >> 5)) * w + x0 + (lo & 31);
+      }
+      if (!inner) {
+        o[1] = o[2] = o[3] = o[0];
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int32_t lo = par[r * 32 + __popc(st & ((2u << (cq + j)) - 1u)) - 1];
-        o[j] = (y0 + (lo >> 5)) * w + x0 + (lo & 31);
+        for (int j = 1; j < 4; ++j) {
+          const int32_t lo = par[i0 + __popc(inner & ((1u << j) - 1u))];
+          o[j] = (y0 + (lo >> 5)) * w + x0 + (lo & 31);
+        }
       }
       *reinterpret_cast<int4*>(roots + (int64_t)y * w + x0 + cq) = make_int4(o[0], o[1], o[2], o[3]);
     }
