@@ -67,17 +67,16 @@ __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
   return p + (k / 3 - 1) * w + (k % 3 - 1);
 }
 
-// Watershed arrows are stored as one byte per pixel: 0..7 = the row-major
-// 8-neighbour it points to, kDirSelf = a marker pixel (root), kDirNone = no
-// arrow yet.  A byte plane keeps the basin chains' gathers 4x denser than
-// absolute i32 indices (neighbouring chains share sectors).
-constexpr uint8_t kDirSelf = 8;
+// Watershed arrows are stored as one byte per pixel: the code of the
+// 8-neighbour it points to, (dy + 1) * 4 + (dx + 1), so a chain step is
+// q + (c >> 2) * w + (c & 3) - (w + 1) (four instructions); kDirSelf (the
+// zero offset) = a marker pixel (root), kDirNone = no arrow yet.  A byte
+// plane keeps the basin chains' gathers 4x denser than i32 indices.
+constexpr uint8_t kDirSelf = 5;
 constexpr uint8_t kDirNone = 0xFF;
 
-__device__ __forceinline__ int32_t dir_step(int w, int32_t p, uint32_t t) {
-  const int dy = (int)((0x22211000u >> (4 * t)) & 0xFu) - 1;
-  const int dx = (int)((0x21020210u >> (4 * t)) & 0xFu) - 1;
-  return p + dy * w + dx;
+__device__ __forceinline__ uint8_t dir_code(int t) {  // row-major neighbour t of 8
+  return (uint8_t)((0xA9864210u >> (4 * t)) & 0xFu);
 }
 
 // The 8 neighbour values selected by mask m (others = fill), as unrolled
@@ -139,7 +138,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       for (int t = 0; t < 8; ++t)  // row-major: first max = min index
         if (fv[t] > best) { best = fv[t]; arg = t; }
       if (arg >= 0) {
-        dir[p] = (uint8_t)arg;
+        dir[p] = dir_code(arg);
         par[p] = -1;
         flat[p] = 0;
       } else {
@@ -186,7 +185,7 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
       }
     }
     unite_backward(par, w, i, same);
-    if (seed >= 0) dir[i] = (uint8_t)seed;
+    if (seed >= 0) dir[i] = dir_code(seed);
   }
 }
 
@@ -381,7 +380,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         const uint8_t* ns = s_nbs[wl][lane + 32 * q];
 #pragma unroll
         for (int t = 7; t >= 0; --t)  // the first (minimum-index) match wins
-          if (((nb[q] >> t) & 1u) && sv[ns[t]] == d[q] - 1) dir[px[q]] = (uint8_t)t;
+          if (((nb[q] >> t) & 1u) && sv[ns[t]] == d[q] - 1) dir[px[q]] = dir_code(t);
       }
       __syncwarp();
     } else {
@@ -418,7 +417,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         gather8(vd, w, pm.x, (uint32_t)pm.y, kInfD, dv);
 #pragma unroll
         for (int t = 7; t >= 0; --t)
-          if (dv[t] == dp - 1) dir[pm.x] = (uint8_t)t;
+          if (dv[t] == dp - 1) dir[pm.x] = dir_code(t);
       }
     }
   }
@@ -674,12 +673,14 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
       q[j] = p[j];
       d[j] = p[j] >= 0 ? dir[p[j]] : kDirNone;
     }
-    // d < 8: step to that neighbour; kDirSelf: marker reached; kDirNone: none
-    while (d[0] < 8u || d[1] < 8u || d[2] < 8u || d[3] < 8u) {
+    // a neighbour code: step; kDirSelf: marker reached; kDirNone: no arrow
+    const int32_t wm = w + 1;
+    auto moving = [](uint32_t c) { return c != kDirSelf && c != kDirNone; };
+    while (moving(d[0]) || moving(d[1]) || moving(d[2]) || moving(d[3])) {
 #pragma unroll
       for (int j = 0; j < kC; ++j) {
-        if (d[j] < 8u) {
-          q[j] = dir_step(w, q[j], d[j]);
+        if (moving(d[j])) {
+          q[j] += (int32_t)(d[j] >> 2) * w + (int32_t)(d[j] & 3u) - wm;
           d[j] = dir[q[j]];
         }
       }
