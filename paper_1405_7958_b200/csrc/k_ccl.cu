@@ -1020,20 +1020,6 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
 // that is a pixel with H >= t + h (the seed bit of FgThresh).
 // 4 pixels per thread: the root, global-root and flag gathers are issued
 // stage by stage for the four, so each stage's loads are in flight together.
-// Seed flag of every LOCAL root, written in place into the flag plane at the
-// local root's pixel (a global root's own entry keeps its truth value, the
-// other local roots' entries were unused), so k_seeded_and gathers once.
-__global__ void k_seed_local(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
-                             const int32_t* __restrict__ roots, int32_t* flag) {
-  pdl_enter();
-  const int n = *lcount;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t lr = lroots[2 * k];
-    const int32_t v = __ldcg(flag + roots[lr]) ? 1 : 0;
-    __stcg(flag + lr, v);
-  }
-}
-
 __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
                              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
                              uint8_t* __restrict__ out) {
@@ -1047,15 +1033,17 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
       const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
       const uint32_t t4 = __ldg(reinterpret_cast<const uint32_t*>(tissue + i0));
       int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;  // global root
       uint32_t o = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)  // flag at the local root (k_seed_local)
+      for (int k = 0; k < 4; ++k)
         if (v[k] >= 0 && flag[v[k]] && ((t4 >> (8 * k)) & 0xFFu)) o |= 1u << (8 * k);
       *reinterpret_cast<uint32_t*>(out + i0) = o;
     } else {
       for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
-        const int32_t lr = roots[i];
-        out[i] = (uint8_t)(lr >= 0 && flag[lr] && tissue[i]);
+        const int32_t r = root_of(roots, i);
+        out[i] = (uint8_t)(r >= 0 && flag[r] && tissue[i]);
       }
     }
   }
@@ -1116,9 +1104,6 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
   const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
   RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed));
-  RTG_CUDA(launch_k(ctx, k_seed_local, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
-                    flag));
-  RTG_LAUNCH("k_seed_local");
   RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out));
   RTG_LAUNCH("k_seeded_and");
   return RTG_OK;
