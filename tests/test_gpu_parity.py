@@ -416,6 +416,32 @@ def test_repeatable(rtg, ctx):
             assert x == y
 
 
+def test_stage_state_interleaved_with_operators(rtg, ctx, oracle):
+    """The stage clears its counters inside its own launches (the streaming
+    kernel's first CTA, the watershed's zeroing launch, the ranking pass);
+    per-operator entry points on the same context in between must not leak
+    state into it: every stage call stays bit-exact with the oracle."""
+    h, w = 1024, 1280
+    rng = np.random.default_rng(11)
+    blobs = _rand_blobs(rng, h, w, density=0.3)
+    d_mask = _np_dev(blobs)
+    lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    for k, (r, c) in enumerate([(3, 1), (5, 2), (7, 3)]):
+        rgb = rtg.synth_tile_host(r, c, h, w)
+        ref = oracle.process_tile(rgb, rtg.default_params())
+        mask, labels, hema, feats, nobj = ctx.process_tile(rgb)
+        assert nobj == ref["n"]
+        assert np.array_equal(mask, ref["mask"])
+        assert np.array_equal(labels, ref["labels"])
+        np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+        # operators in between leave counters / bitmaps in arbitrary states
+        ctx.bwlabel_dev(d_mask, h, w, 8 if k % 2 else 4, lab, n)
+        ctx.watershed_dev(d_mask, h, w, rtg.default_params().ws_h, sep)
+        ctx.fill_holes_dev(d_mask, h, w, sep)
+
+
 def test_process_tiles_batch(rtg, ctx):
     """rtg_process_tiles (double-buffered batch) returns exactly what
     rtg_process_tile returns per tile, with pinned (zero-copy rows) and
