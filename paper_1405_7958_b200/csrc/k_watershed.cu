@@ -139,7 +139,6 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
         if (fv[t] > best) { best = fv[t]; arg = t; }
       if (arg >= 0) {
         dir[p] = dir_code(arg);
-        par[p] = -1;
         flat[p] = 0;
       } else {
         dir[p] = kDirNone;
@@ -258,22 +257,30 @@ __global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
 }
 
 // Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8).
+// Only flat neighbours carry a plateau parent (k_ws_arrows leaves par of
+// non-flat pixels unwritten), so the flat byte gates the parent compare.
 __device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                                                  const uint16_t* __restrict__ Fw,
+                                                 const uint8_t* __restrict__ flat,
                                                  const int32_t* __restrict__ par, int32_t p,
                                                  uint16_t f, int32_t r) {
   const int w = (int)dw.d;
   const int y = fdiv(p, dw), x = p - y * w;
   const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
-  uint32_t fv[8];
-  int32_t pv[8];
+  uint32_t fv[8], fl[8];
   gather8(Fw, w, p, fm, 0u, fv);
+  gather8(flat, w, p, fm, 0u, fl);
+  uint32_t cand = 0;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) pv[t] = ((fm >> t) & 1u) ? __ldcg(par + nbr_index(w, p, t)) : -1;
+  for (int t = 0; t < 8; ++t)
+    if (((fm >> t) & 1u) && fl[t] && fv[t] == f) cand |= 1u << t;
+  int32_t pv[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) pv[t] = ((cand >> t) & 1u) ? __ldcg(par + nbr_index(w, p, t)) : -1;
   uint32_t m = 0;
 #pragma unroll
   for (int t = 0; t < 8; ++t)
-    if (((fm >> t) & 1u) && fv[t] == f && pv[t] == r) m |= 1u << t;
+    if (((cand >> t) & 1u) && pv[t] == r) m |= 1u << t;
   return m;
 }
 
@@ -311,7 +318,8 @@ __device__ __forceinline__ int32_t member_px(int32_t m) { return m < 0 ? ~m : m;
 // re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
 k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
-             const uint16_t* __restrict__ Fw, const int32_t* __restrict__ par,
+             const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
+             const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch,
              uint8_t* slotmap) {
@@ -342,7 +350,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         if (k < e) {
           px[q] = member_px(members[k]);
           d[q] = dir[px[q]] != kDirNone ? 1 : kInfD;
-          nb[q] = plateau_nbrs(h, dw, mask, Fw, par, px[q], Fw[px[q]], par[px[q]]);
+          nb[q] = plateau_nbrs(h, dw, mask, Fw, flat, par, px[q], Fw[px[q]], par[px[q]]);
           sv[lane + 32 * q] = d[q];
           slotmap[px[q]] = (uint8_t)(lane + 32 * q);
         }
@@ -388,7 +396,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
       for (int k = s0 + lane; k < e; k += 32) {
         const int32_t p = member_px(members[k]);
         vd[p] = dir[p] != kDirNone ? 1 : kInfD;
-        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, par, p, Fw[p], par[p]));
+        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, flat, par, p, Fw[p], par[p]));
       }
       __syncwarp();
       while (true) {
@@ -810,7 +818,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots));
   RTG_LAUNCH("k_ws_scatter");
-  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, par, ctx->lroots, walloc, dir,
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, par, ctx->lroots, walloc, dir,
                                            delta, member_scratch, ctx->m2 /* slot map */));
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
