@@ -43,7 +43,8 @@ using namespace rt;
 
 namespace {
 
-std::uint64_t fnv(const std::vector<std::uint8_t>& v) {
+template <typename V>
+std::uint64_t fnv(const V& v) {
   std::uint64_t h = 1469598103934665603ull;
   for (auto b : v) h = (h ^ b) * 1099511628211ull;
   return h;
@@ -345,7 +346,7 @@ void write_bytes(const std::string& path, const std::vector<std::uint8_t>& b) {
 }
 
 std::uint64_t record_hash(const DiskRecord& r) {
-  std::vector<std::uint8_t> v(r.payload);
+  std::vector<std::uint8_t> v(r.payload.begin(), r.payload.end());
   const std::string s = r.id.ns + "|" + r.id.key + "|" + r.id.type_tag + "|" +
                         std::to_string(r.id.timestamp) + "|" + std::to_string(r.id.version) + "|" +
                         std::to_string(int(r.kind)) + "|" + std::to_string(int(r.element_kind)) +

@@ -110,13 +110,49 @@ template <> struct element_of<std::int32_t> { static constexpr ElementKind value
 template <> struct element_of<float> { static constexpr ElementKind value = ElementKind::kF32; };
 template <> struct element_of<double> { static constexpr ElementKind value = ElementKind::kF64; };
 
+// ---- payload memory -----------------------------------------
+// Chunk payloads are byte vectors whose allocator routes blocks of at least
+// `min_bytes` through a process-wide hook, so a GPU worker can put them in
+// pinned pages (rtg_host_alloc) and the stage DMAs straight from / into the
+// chunk (the reference's payload is a plain std::vector<uint8_t>,
+// data_region.hpp:87-92, which forces a staged pageable copy).  Every block
+// records the free function it came from, so changing the hook never
+// mismatches alloc and free; hooked blocks are recycled by exact size up to
+// `pool_bytes` (tiles repeat sizes; page-locking costs ms per call).
+using PayloadAllocFn = void* (*)(std::size_t bytes);
+using PayloadFreeFn = void (*)(void* p);
+// alloc == nullptr restores plain heap payloads (and releases the pool).
+void set_payload_allocator(PayloadAllocFn alloc, PayloadFreeFn free, std::size_t min_bytes,
+                           std::size_t pool_bytes);
+// True when `p` (a payload's data()) lives in a block from the hook.
+bool payload_is_hooked(const void* p);
+
+namespace detail {
+void* payload_allocate(std::size_t bytes);
+void payload_deallocate(void* p) noexcept;
+}  // namespace detail
+
+template <typename T>
+struct PayloadAllocator {
+  using value_type = T;
+  PayloadAllocator() noexcept = default;
+  template <typename U>
+  PayloadAllocator(const PayloadAllocator<U>&) noexcept {}
+  T* allocate(std::size_t n) { return static_cast<T*>(detail::payload_allocate(n * sizeof(T))); }
+  void deallocate(T* p, std::size_t) noexcept { detail::payload_deallocate(p); }
+  template <typename U>
+  bool operator==(const PayloadAllocator<U>&) const noexcept { return true; }
+};
+
+using Bytes = std::vector<std::uint8_t, PayloadAllocator<std::uint8_t>>;
+
 // One stored piece: dense payloads are row-major, last axis contiguous, with
 // length volume(bbox) * element_size.
 struct Chunk {
   std::uint64_t chunk_id = 0;
   BoundingBox bbox;
   ElementKind element_kind = ElementKind::kU8;
-  std::vector<std::uint8_t> payload;
+  Bytes payload;
 };
 
 class DataRegion {
@@ -140,7 +176,10 @@ class DataRegion {
 
   const std::map<BoundingBox, Chunk>& chunks() const { return chunks_; }
   // Inserts or replaces (equal box) a chunk; validates box and dense length.
-  Chunk& put_chunk(const BoundingBox& box, std::vector<std::uint8_t> payload);
+  Chunk& put_chunk(const BoundingBox& box, Bytes payload);
+  Chunk& put_chunk(const BoundingBox& box, const std::vector<std::uint8_t>& payload) {
+    return put_chunk(box, Bytes(payload.begin(), payload.end()));
+  }
   const Chunk* find_chunk(const BoundingBox& box) const;
   Chunk* find_chunk(const BoundingBox& box);
   void drop_payload();
@@ -176,7 +215,7 @@ class DenseDataRegion2D {
   // Materialises a zero payload over the whole bbox.
   static DataRegion create(DataRegionId id, const BoundingBox& box, RegionKind kind = RegionKind::kDense2D) {
     DataRegion r(std::move(id), kind, element_of<T>::value, box);
-    r.put_chunk(box, std::vector<std::uint8_t>(std::size_t(box.volume()) * sizeof(T), 0));
+    r.put_chunk(box, Bytes(std::size_t(box.volume()) * sizeof(T), 0));
     return r;
   }
   std::int64_t height() const { return r_->bbox().extent(0); }

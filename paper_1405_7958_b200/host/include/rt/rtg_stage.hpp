@@ -40,6 +40,15 @@ class GpuDevice {
   std::int32_t max_objects_ = 0;
 };
 
+// Routes Chunk payloads of at least `min_bytes` into pinned host pages
+// (rtg_host_alloc), recycling up to `pool_bytes` of them by size, so the GPU
+// variant's H2D of the RGB tile and D2H of Mask / Labels are direct DMAs
+// from / into the chunks.  Call once per process before the
+// tiles are staged; use_pageable_payloads() undoes it.
+void use_pinned_payloads(std::size_t min_bytes = std::size_t(1) << 20,
+                         std::size_t pool_bytes = std::size_t(4) << 30);
+void use_pageable_payloads();
+
 struct SegmentationRegions {
   DataRegionId rgb{"img", "RGB", "raw", 0, 0};
   DataRegionId mask{"img", "Mask", "label", 0, 0};

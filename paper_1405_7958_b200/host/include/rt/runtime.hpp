@@ -59,7 +59,7 @@ class MemoryStore : public StorageBackend {
     BoundingBox box;
     RegionKind kind;
     ElementKind elem;
-    std::vector<std::uint8_t> payload;
+    Bytes payload;
   };
   std::string name_;
   std::mutex mu_;

@@ -23,7 +23,7 @@ struct DiskRecord {
   ElementKind element_kind = ElementKind::kU8;
   BoundingBox box;
   std::uint64_t seq = 0;
-  std::vector<std::uint8_t> payload;
+  Bytes payload;
 };
 
 inline constexpr std::uint32_t kSessionMagic = 0x31535452u;     // "RTS1"

@@ -21,7 +21,7 @@ class Out {
     u32(std::uint32_t(s.size()));
     b_.insert(b_.end(), s.begin(), s.end());
   }
-  void raw(const std::vector<std::uint8_t>& p) { b_.insert(b_.end(), p.begin(), p.end()); }
+  void raw(const Bytes& p) { b_.insert(b_.end(), p.begin(), p.end()); }
   void box(const BoundingBox& b) {
     u8(std::uint8_t(b.dims()));
     for (int a = 0; a < b.dims(); ++a) i64(b.lo(a));
@@ -54,9 +54,9 @@ class In {
     pos_ += n;
     return out;
   }
-  std::vector<std::uint8_t> raw(std::uint64_t n) {
+  Bytes raw(std::uint64_t n) {
     need(n);
-    std::vector<std::uint8_t> out(s_.begin() + std::ptrdiff_t(pos_),
+    Bytes out(s_.begin() + std::ptrdiff_t(pos_),
                                   s_.begin() + std::ptrdiff_t(pos_ + n));
     pos_ += n;
     return out;

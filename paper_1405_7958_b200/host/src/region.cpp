@@ -2,9 +2,121 @@
 #include "rt/region.hpp"
 
 #include <algorithm>
+#include <mutex>
+#include <new>
 #include <sstream>
+#include <unordered_map>
 
 namespace rt {
+
+// ---- payload memory ----------------------------------------------------------
+
+namespace {
+
+// 64-byte prefix in front of every payload block: who frees it and its size.
+struct alignas(64) BlockHeader {
+  PayloadFreeFn free;  // nullptr: aligned operator new
+  std::size_t bytes;
+};
+static_assert(sizeof(BlockHeader) == 64);
+
+struct PayloadHooks {
+  std::mutex mu;
+  PayloadAllocFn alloc = nullptr;
+  PayloadFreeFn free = nullptr;
+  std::size_t min_bytes = 0;
+  std::size_t pool_cap = 0;
+  std::size_t pooled = 0;
+  std::unordered_map<std::size_t, std::vector<BlockHeader*>> pool;  // hook blocks by size
+
+  void release_pool_locked() {
+    for (auto& [n, v] : pool)
+      for (BlockHeader* h : v) h->free(h);
+    pool.clear();
+    pooled = 0;
+  }
+};
+
+PayloadHooks& hooks() {
+  static PayloadHooks* h = new PayloadHooks();  // outlives static payloads
+  return *h;
+}
+
+BlockHeader* header_of(const void* p) {
+  return reinterpret_cast<BlockHeader*>(const_cast<char*>(static_cast<const char*>(p)) -
+                                        sizeof(BlockHeader));
+}
+
+}  // namespace
+
+void set_payload_allocator(PayloadAllocFn alloc, PayloadFreeFn free, std::size_t min_bytes,
+                           std::size_t pool_bytes) {
+  if ((alloc == nullptr) != (free == nullptr))
+    throw ProtocolError("payload allocator needs both alloc and free");
+  PayloadHooks& h = hooks();
+  std::lock_guard<std::mutex> lk(h.mu);
+  h.release_pool_locked();
+  h.alloc = alloc;
+  h.free = free;
+  h.min_bytes = min_bytes;
+  h.pool_cap = alloc ? pool_bytes : 0;
+}
+
+bool payload_is_hooked(const void* p) { return p && header_of(p)->free != nullptr; }
+
+namespace detail {
+
+void* payload_allocate(std::size_t bytes) {
+  PayloadHooks& h = hooks();
+  const std::size_t total = bytes + sizeof(BlockHeader);
+  {
+    std::lock_guard<std::mutex> lk(h.mu);
+    if (h.alloc && bytes >= h.min_bytes) {
+      BlockHeader* b = nullptr;
+      auto it = h.pool.find(bytes);
+      if (it != h.pool.end() && !it->second.empty()) {
+        b = it->second.back();
+        it->second.pop_back();
+        h.pooled -= total;
+      } else {
+        b = static_cast<BlockHeader*>(h.alloc(total));
+        if (!b) throw std::bad_alloc();
+      }
+      b->free = h.free;
+      b->bytes = bytes;
+      return b + 1;
+    }
+  }
+  auto* b = static_cast<BlockHeader*>(::operator new(total, std::align_val_t(64)));
+  b->free = nullptr;
+  b->bytes = bytes;
+  return b + 1;
+}
+
+void payload_deallocate(void* p) noexcept {
+  if (!p) return;
+  BlockHeader* b = header_of(p);
+  if (!b->free) {
+    ::operator delete(b, std::align_val_t(64));
+    return;
+  }
+  PayloadHooks& h = hooks();
+  const std::size_t total = b->bytes + sizeof(BlockHeader);
+  {
+    std::lock_guard<std::mutex> lk(h.mu);
+    if (b->free == h.free && h.pooled + total <= h.pool_cap) {
+      try {
+        h.pool[b->bytes].push_back(b);
+        h.pooled += total;
+        return;
+      } catch (...) {
+      }
+    }
+  }
+  b->free(b);
+}
+
+}  // namespace detail
 
 // ---- BoundingBox ------------------------------------------------------------
 
@@ -154,7 +266,7 @@ void DataRegion::set_roi(const BoundingBox& roi) {
   roi_ = roi;
 }
 
-Chunk& DataRegion::put_chunk(const BoundingBox& box, std::vector<std::uint8_t> payload) {
+Chunk& DataRegion::put_chunk(const BoundingBox& box, Bytes payload) {
   if (box.empty()) throw DimensionError("empty chunk box");
   if (bbox_.empty() || !bbox_.contains(box))
     throw DimensionError("chunk " + box.to_string() + " escapes region " + bbox_.to_string());

@@ -30,6 +30,20 @@ GpuDevice::~GpuDevice() {
   if (ctx_) rtg_ctx_destroy(ctx_);
 }
 
+namespace {
+void* pinned_alloc(std::size_t bytes) {
+  void* p = nullptr;
+  return rtg_host_alloc(bytes, &p) == RTG_OK ? p : nullptr;
+}
+void pinned_free(void* p) { rtg_host_free(p); }
+}  // namespace
+
+void use_pinned_payloads(std::size_t min_bytes, std::size_t pool_bytes) {
+  set_payload_allocator(pinned_alloc, pinned_free, min_bytes, pool_bytes);
+}
+
+void use_pageable_payloads() { set_payload_allocator(nullptr, nullptr, 0, 0); }
+
 DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, RegionKind kind,
                            ElementKind elem, const BoundingBox& box) {
   IoMode mode = IoMode::kOutput;
@@ -40,7 +54,7 @@ DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, Region
     local.remove_data_region(id);
   }
   DataRegion r(id, kind, elem, box);
-  r.put_chunk(box, std::vector<std::uint8_t>(std::size_t(box.volume()) * element_size(elem), 0));
+  r.put_chunk(box, Bytes(std::size_t(box.volume()) * element_size(elem), 0));
   r.set_io_mode(mode);
   r.set_storage_binding(binding);
   return local.insert_data_region(std::move(r));

@@ -34,7 +34,7 @@ DataRegion MemoryStore::read_region(const DataRegionId& id, const BoundingBox& q
       return out;
     }
   }
-  std::vector<std::uint8_t> canvas(std::size_t(query.volume()) * es, 0);
+  Bytes canvas(std::size_t(query.volume()) * es, 0);
   std::vector<std::uint8_t> seen(std::size_t(query.volume()), 0);
   for (const auto& p : it->second) {  // staging order: last writer wins
     if (!p.box.intersects(query)) continue;

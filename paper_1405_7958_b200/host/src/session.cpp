@@ -20,9 +20,9 @@ void put_box(std::string& o, const BoundingBox& b) {
 }
 
 // Whole file in memory; every read is bounds-checked against it.
-class Bytes {
+class FileBytes {
  public:
-  explicit Bytes(const std::string& path) {
+  explicit FileBytes(const std::string& path) {
     std::ifstream f(path, std::ios::binary);
     if (!f) throw IoError("cannot open session file: " + path);
     f.seekg(0, std::ios::end);
@@ -49,10 +49,10 @@ class Bytes {
     pos_ += n;
     return s;
   }
-  std::vector<std::uint8_t> raw(std::uint64_t n) {
+  Bytes raw(std::uint64_t n) {
     if (n > data_.size()) throw DecodeError("session file payload overruns");
     if (n > data_.size() - pos_) throw DecodeError("session file truncated");
-    std::vector<std::uint8_t> b(data_.begin() + std::ptrdiff_t(pos_),
+    Bytes b(data_.begin() + std::ptrdiff_t(pos_),
                                 data_.begin() + std::ptrdiff_t(pos_ + n));
     pos_ += n;
     return b;
@@ -72,7 +72,7 @@ class Bytes {
   std::uint64_t pos_ = 0;
 };
 
-DiskRecord record(Bytes& in) {
+DiskRecord record(FileBytes& in) {
   DiskRecord r;
   r.id.ns = in.str();
   r.id.key = in.str();
@@ -124,7 +124,7 @@ std::vector<std::uint64_t> write_session_file(const std::string& path, std::uint
 }
 
 std::vector<DiskRecord> read_session_file(const std::string& path) {
-  Bytes in(path);
+  FileBytes in(path);
   if (in.size() < 4 + 8 + 4 + 8 + 4) throw DecodeError("session file too short: " + path);
   if (in.get(4) != kSessionMagic) throw DecodeError("session file bad magic");
   in.get(8);  // session seq
@@ -145,7 +145,7 @@ std::vector<DiskRecord> read_session_file(const std::string& path) {
 }
 
 DiskRecord read_record_at(const std::string& path, std::uint64_t offset) {
-  Bytes in(path);
+  FileBytes in(path);
   in.seek(offset);
   return record(in);
 }

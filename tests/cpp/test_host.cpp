@@ -4,6 +4,7 @@
 // stage executed through StageInstance -> WRM -> TaskNode::body -> C-ABI on a
 // B200, checked bit-exactly against the oracle (linked here as the checker).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <random>
@@ -148,6 +149,36 @@ TaskNode task(std::uint64_t id, TaskVariants v, std::optional<double> s = std::n
 }
 
 void scheduling() {
+  check("payload allocator hook: size threshold, recycling by size, per-block free function", [] {
+    static int allocs_a = 0, frees_a = 0, frees_b = 0;
+    struct H {
+      static void* alloc_a(std::size_t n) { ++allocs_a; return std::malloc(n); }
+      static void free_a(void* p) { ++frees_a; std::free(p); }
+      static void* alloc_b(std::size_t n) { return std::malloc(n); }
+      static void free_b(void* p) { ++frees_b; std::free(p); }
+    };
+    set_payload_allocator(H::alloc_a, H::free_a, 1000, 1 << 20);
+    {
+      Bytes small(999, 1), big(4096, 2);
+      require(!payload_is_hooked(small.data()) && payload_is_hooked(big.data()), "threshold");
+      require(reinterpret_cast<std::uintptr_t>(small.data()) % 64 == 0, "heap blocks 64-byte aligned");
+      const std::uint8_t* first = big.data();
+      big = Bytes();
+      Bytes again(4096, 3);  // recycled block, contents value-initialised
+      require(again.data() == first && again[4095] == 3 && allocs_a == 1, "recycled by size");
+      DataRegion r(DataRegionId{"t", "p", "raw", 0, 0}, RegionKind::kDense2D, ElementKind::kU8,
+                   box2(0, 0, 63, 63));
+      r.put_chunk(r.bbox(), std::move(again));
+      require(payload_is_hooked(r.find_chunk(r.bbox())->payload.data()), "chunk keeps the block");
+      set_payload_allocator(H::alloc_b, H::free_b, 1000, 0);  // pool of hook a released
+      Bytes b2(8192, 4);
+      require(payload_is_hooked(b2.data()), "hook b");
+    }  // r's block goes back through free_a, b2 through free_b (pool cap 0)
+    require(frees_a == 1 && frees_b == 1, "each block freed by the hook that made it");
+    set_payload_allocator(nullptr, nullptr, 0, 0);
+    Bytes plain(1 << 16, 0);
+    require(!payload_is_hooked(plain.data()), "hook removed");
+  });
   check("WRM FCFS takes the first compatible ready task", [] {
     WrmState w(SchedulerKind::kFcfs);
     w.submit({task(1, TaskVariants::kCpuOnly), task(2, TaskVariants::kGpuOnly),
@@ -360,6 +391,23 @@ void gpu_stage() {
                   m.labels[i].chunks().begin()->second.payload,
               "labels tile " + std::to_string(i));
     }
+  });
+  check("pinned Chunk payloads (f1): stage reads/writes pinned chunks, outputs bit-identical", [] {
+    ExecutorStats sp, sq;
+    const Run q = run_slide(true, false, &sq);
+    use_pinned_payloads(std::size_t(64) << 10, std::size_t(256) << 20);
+    {
+      const Run p = run_slide(true, false, &sp);
+      require(sp.gpu_tasks == 4, "all tasks on the GPU");
+      for (std::size_t i = 0; i < 4; ++i) {
+        const Bytes& pm = p.masks[i].chunks().begin()->second.payload;
+        const Bytes& pl = p.labels[i].chunks().begin()->second.payload;
+        require(payload_is_hooked(pm.data()) && payload_is_hooked(pl.data()), "outputs pinned");
+        require(pm == q.masks[i].chunks().begin()->second.payload, "mask tile " + std::to_string(i));
+        require(pl == q.labels[i].chunks().begin()->second.payload, "labels tile " + std::to_string(i));
+      }
+    }
+    use_pageable_payloads();
   });
   check("PATS sends a dual-variant task to the GPU worker", [] {
     ExecutorStats s;
