@@ -202,6 +202,10 @@ class DataRegion {
 void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
                       std::span<const std::uint8_t> src, const BoundingBox& src_box,
                       std::size_t elem_size);
+// Sets the cells of `dst` (laid out over dst_box, one byte each) that `box`
+// covers to `value`.
+void fill_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
+                      const BoundingBox& box, std::uint8_t value);
 
 // Typed 2-D dense view of a DataRegion whose single chunk covers its bbox
 // (the hot path's tile / mask / label containers).

@@ -315,14 +315,23 @@ bool DataRegion::operator==(const DataRegion& o) const {
   return true;
 }
 
-void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
-                      std::span<const std::uint8_t> src, const BoundingBox& src_box,
-                      std::size_t elem) {
+namespace {
+
+// Walks the overlap of `dst_box` and `src_box` as contiguous runs: trailing
+// axes both boxes span completely fold into one run (a Dense3D RGB tile read
+// from a slide moves whole 3*w-byte rows, not 3-byte channel triples).
+// fn(dst_offset, src_offset, run_bytes).
+template <typename Fn>
+void walk_overlap(const BoundingBox& dst_box, const BoundingBox& src_box, std::size_t elem, Fn fn) {
   const auto ov = dst_box.intersected(src_box);
   if (!ov) return;
   const int d = ov->dims();
-  const std::size_t run = std::size_t(ov->extent(d - 1)) * elem;
-  // offsets of the overlap's first element along every axis, then walk rows
+  int first = d - 1;  // runs span axes first..d-1
+  while (first > 0 && ov->extent(first) == dst_box.extent(first) &&
+         ov->extent(first) == src_box.extent(first))
+    --first;
+  std::size_t run = elem;
+  for (int a = first; a < d; ++a) run *= std::size_t(ov->extent(a));
   std::array<std::int64_t, BoundingBox::kMaxDims> p{};
   for (int a = 0; a < d; ++a) p[a] = ov->lo(a);
   auto offset = [&](const BoundingBox& b) {
@@ -331,14 +340,31 @@ void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
     return std::size_t(o) * elem;
   };
   for (;;) {
-    std::memcpy(dst.data() + offset(dst_box), src.data() + offset(src_box), run);
-    int a = d - 2;
+    fn(offset(dst_box), offset(src_box), run);
+    int a = first - 1;
     while (a >= 0 && ++p[a] > ov->hi(a)) {
       p[a] = ov->lo(a);
       --a;
     }
     if (a < 0) break;
   }
+}
+
+}  // namespace
+
+void copy_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
+                      std::span<const std::uint8_t> src, const BoundingBox& src_box,
+                      std::size_t elem) {
+  walk_overlap(dst_box, src_box, elem, [&](std::size_t od, std::size_t os, std::size_t n) {
+    std::memcpy(dst.data() + od, src.data() + os, n);
+  });
+}
+
+void fill_box_overlap(std::span<std::uint8_t> dst, const BoundingBox& dst_box,
+                      const BoundingBox& box, std::uint8_t value) {
+  walk_overlap(dst_box, box, 1, [&](std::size_t od, std::size_t, std::size_t n) {
+    std::memset(dst.data() + od, value, n);
+  });
 }
 
 // ---- RegionTemplate -------------------------------------------------------------

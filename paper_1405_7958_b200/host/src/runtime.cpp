@@ -33,16 +33,19 @@ DataRegion MemoryStore::read_region(const DataRegionId& id, const BoundingBox& q
       out.put_chunk(query, p->payload);
       return out;
     }
+    if (p->box.intersects(query)) break;  // a newer piece overwrites part of it
   }
   Bytes canvas(std::size_t(query.volume()) * es, 0);
-  std::vector<std::uint8_t> seen(std::size_t(query.volume()), 0);
+  // one piece containing the query proves coverage without a per-cell map
+  bool covered = false;
+  for (const auto& p : it->second) covered = covered || p.box.contains(query);
+  std::vector<std::uint8_t> seen(covered ? 0 : std::size_t(query.volume()), 0);
   for (const auto& p : it->second) {  // staging order: last writer wins
     if (!p.box.intersects(query)) continue;
     copy_box_overlap(canvas, query, p.payload, p.box, es);
-    std::vector<std::uint8_t> ones(std::size_t(p.box.volume()), 1);
-    copy_box_overlap(seen, query, ones, p.box, 1);
+    if (!covered) fill_box_overlap(seen, query, p.box, 1);
   }
-  if (std::find(seen.begin(), seen.end(), 0) != seen.end())
+  if (!covered && std::find(seen.begin(), seen.end(), 0) != seen.end())
     throw NotFoundError("query " + query.to_string() + " has cells never written for " +
                         id.to_string());
   out.put_chunk(query, std::move(canvas));

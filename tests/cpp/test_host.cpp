@@ -3,6 +3,8 @@
 // line per check).  `test_host` runs the CPU checks; `test_host --gpu` adds the
 // stage executed through StageInstance -> WRM -> TaskNode::body -> C-ABI on a
 // B200, checked bit-exactly against the oracle (linked here as the checker).
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -66,6 +68,54 @@ void containers() {
     for (int i = 0; i < 25; ++i) src[i] = std::uint8_t(i + 1);
     copy_box_overlap(dst, box2(3, 3, 5, 5), src, box2(0, 0, 4, 4), 1);
     require(dst == std::vector<std::uint8_t>{19, 20, 0, 24, 25, 0, 0, 0, 0}, "overlap bytes");
+  });
+  check("copy_box_overlap / fill_box_overlap match a per-cell walk (200 seeded 1-3-D trials)", [] {
+    std::mt19937 rng(7958);
+    auto rnd = [&](int lo, int hi) { return int(rng() % unsigned(hi - lo + 1)) + lo; };
+    for (int trial = 0; trial < 200; ++trial) {
+      const int d = rnd(1, 3);
+      std::vector<std::int64_t> l1(d), h1(d), l2(d), h2(d);
+      for (int a = 0; a < d; ++a) {
+        const bool full = a > 0 && rnd(0, 1);  // trailing axes often identical
+        l1[a] = rnd(0, 4); h1[a] = l1[a] + rnd(0, 5);
+        l2[a] = full ? l1[a] : rnd(0, 4); h2[a] = full ? h1[a] : l2[a] + rnd(0, 5);
+      }
+      const BoundingBox db(d, l1.data(), h1.data()), sb(d, l2.data(), h2.data());
+      const std::size_t es = std::size_t(rnd(1, 3));
+      std::vector<std::uint8_t> src(std::size_t(sb.volume()) * es), dst(std::size_t(db.volume()) * es, 0);
+      for (auto& v : src) v = std::uint8_t(rng());
+      std::vector<std::uint8_t> want = dst, seen(std::size_t(db.volume()), 0), seen_want = seen;
+      for (std::int64_t i = 0; i < db.volume(); ++i) {  // naive: decode every dst cell
+        std::vector<std::int64_t> c(d);
+        std::int64_t r = i;
+        for (int a = d - 1; a >= 0; --a) { c[a] = db.lo(a) + r % db.extent(a); r /= db.extent(a); }
+        bool in = true;
+        std::int64_t o = 0;
+        for (int a = 0; a < d; ++a) {
+          in = in && c[a] >= sb.lo(a) && c[a] <= sb.hi(a);
+          o = o * sb.extent(a) + (c[a] - sb.lo(a));
+        }
+        if (!in) continue;
+        std::memcpy(want.data() + std::size_t(i) * es, src.data() + std::size_t(o) * es, es);
+        seen_want[std::size_t(i)] = 1;
+      }
+      copy_box_overlap(dst, db, src, sb, es);
+      fill_box_overlap(seen, db, sb, 1);
+      require(dst == want && seen == seen_want, "trial " + std::to_string(trial));
+    }
+  });
+  check("MemoryStore read: a newer partial piece wins over an older exact piece", [] {
+    MemoryStore st("s");
+    const DataRegionId id{"t", "p", "raw", 0, 0};
+    DataRegion a(id, RegionKind::kDense2D, ElementKind::kU8, box2(0, 0, 3, 3));
+    a.put_chunk(a.bbox(), std::vector<std::uint8_t>(16, 1));
+    DataRegion b(id, RegionKind::kDense2D, ElementKind::kU8, box2(2, 2, 5, 5));
+    b.put_chunk(b.bbox(), std::vector<std::uint8_t>(16, 2));
+    st.stage_region(a, 0).wait();
+    st.stage_region(b, 0).wait();
+    const DataRegion r = st.read_region(id, box2(0, 0, 3, 3));
+    const Bytes& v = r.chunks().begin()->second.payload;
+    require(v[0] == 1 && v[3 * 4 + 3] == 2 && v[2 * 4 + 1] == 1, "last writer wins");
   });
   check("put_chunk validates box and dense payload length", [] {
     DataRegion r = u8_region("a", box2(0, 0, 9, 9));
@@ -287,6 +337,8 @@ struct Run {
   std::vector<DataRegion> masks, labels, feats;
 };
 
+double g_last_run_ms = 0;  // run_stages wall time of the last run_slide
+
 Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats, int cpu_workers = 0,
               std::int64_t H = 1024, std::int64_t W = 1024, std::int64_t T = 512) {
   rtg_params p;
@@ -322,10 +374,13 @@ Run run_slide(bool use_gpu, bool register_cpu, ExecutorStats* stats, int cpu_wor
   ExecutorConfig cfg;
   cfg.cpu_workers = cpu_workers;
   if (use_gpu) {
-    gpu = std::make_unique<GpuDevice>(0, T, T, 1 << 14);
+    gpu = std::make_unique<GpuDevice>(0, T, T, T >= 2048 ? 1 << 16 : 1 << 14);
     cfg.gpus = {gpu.get()};
   }
+  const auto t0 = std::chrono::steady_clock::now();
   *stats = run_stages(m, reg, cfg);
+  g_last_run_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   Run out;
   std::int64_t k = 0;
   for (std::int64_t y = 0; y < H; y += T) {
@@ -416,9 +471,74 @@ void gpu_stage() {
   });
 }
 
+// f1 evidence: the executor's wall time per 4096^2 tile (worker_prepare's
+// store read + H2D + stage + D2H + finalize's staging) with pageable vs
+// pinned chunk payloads, best of `reps`, one GPU worker.
+void bench_f1(int reps) {
+  const std::int64_t H = 8192, W = 8192, T = 4096;
+  const double tiles = double(H / T) * double(W / T);
+  auto best = [&](bool pinned) {
+    if (pinned) use_pinned_payloads();
+    double ms = 1e30;
+    for (int r = 0; r < reps; ++r) {
+      ExecutorStats st;
+      run_slide(true, false, &st, 0, H, W, T);
+      ms = std::min(ms, g_last_run_ms);
+    }
+    if (pinned) use_pageable_payloads();
+    return ms / tiles;
+  };
+  {  // where the time goes, pageable payloads
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
+    rtg_params p;
+    rtg_check(rtg_params_default(&p));
+    std::vector<std::uint8_t> px(std::size_t(H * W * 3));
+    auto t = clk::now();
+    rtg_check(rtg_synth_tile_host(1405795800ULL, 0, 0, H, W, px.data()));
+    std::printf("synth slide %.1f ms\n", ms(t));
+    MemoryStore st("s");
+    DataRegion slide(SegmentationRegions{}.rgb, RegionKind::kDense3D, ElementKind::kU8,
+                     BoundingBox({0, 0, 0}, {H - 1, W - 1, 2}));
+    t = clk::now();
+    slide.put_chunk(slide.bbox(), px);
+    std::printf("put_chunk slide %.1f ms\n", ms(t));
+    t = clk::now();
+    st.stage_region(slide, 0).wait();
+    std::printf("stage_region slide %.1f ms\n", ms(t));
+    t = clk::now();
+    DataRegion tile = st.read_region(slide.id(), BoundingBox({0, 0, 0}, {T - 1, T - 1, 2}));
+    std::printf("read_region tile %.1f ms\n", ms(t));
+    GpuDevice g(0, T, T, 1 << 16);
+    std::vector<std::uint8_t> mask(std::size_t(T * T));
+    std::vector<std::int32_t> lab(std::size_t(T * T));
+    std::vector<float> f(std::size_t(1 << 16) * RTG_NUM_FEATURES);
+    for (int r = 0; r < 3; ++r) {
+      std::int32_t n = 0;
+      t = clk::now();
+      rtg_check(rtg_process_tile(g.ctx(), tile.chunks().begin()->second.payload.data(), T, T, 3 * T, &p,
+                                 mask.data(), lab.data(), nullptr, f.data(), 1 << 16, &n));
+      std::printf("rtg_process_tile #%d %.1f ms (%d objects)\n", r, ms(t), n);
+    }
+    t = clk::now();
+    {
+      GpuDevice g2(0, T, T, 1 << 16);
+    }
+    std::printf("GpuDevice create+destroy %.1f ms\n", ms(t));
+  }
+  const double pageable = best(false), pinned = best(true);
+  std::printf("{\"bench\": \"f1 executor ms per 4096^2 tile\", \"tiles\": %d, \"reps\": %d, "
+              "\"pageable_ms\": %.3f, \"pinned_ms\": %.3f, \"speedup\": %.2f}\n",
+              int(tiles), reps, pageable, pinned, pageable / pinned);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc > 1 && std::strcmp(argv[1], "--bench-f1") == 0) {
+    bench_f1(argc > 2 ? std::atoi(argv[2]) : 3);
+    return 0;
+  }
   const bool gpu = argc > 1 && std::strcmp(argv[1], "--gpu") == 0;
   containers();
   scheduling();
