@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 namespace rt {
@@ -139,6 +140,17 @@ struct PayloadAllocator {
   template <typename U>
   PayloadAllocator(const PayloadAllocator<U>&) noexcept {}
   T* allocate(std::size_t n) { return static_cast<T*>(detail::payload_allocate(n * sizeof(T))); }
+  // Default-initialises: Bytes(n) / resize(n) leave the bytes unwritten (a
+  // payload the next step overwrites whole costs no zero pass); spell the
+  // value, Bytes(n, 0), when zeros are meant.
+  template <typename U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <typename U, typename... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
   void deallocate(T* p, std::size_t) noexcept { detail::payload_deallocate(p); }
   template <typename U>
   bool operator==(const PayloadAllocator<U>&) const noexcept { return true; }

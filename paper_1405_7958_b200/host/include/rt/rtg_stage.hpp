@@ -79,9 +79,10 @@ StageInstance make_segmentation_stage(std::uint64_t stage_id, const BoundingBox&
 SegmentationRegions resolve_regions(const RegionTemplate& local, const SegmentationRegions& names);
 
 // Output installation helper shared by variants: replaces the metadata-only
-// shell worker_prepare created with a typed, zero-filled dense region that
-// keeps the shell's io mode and storage binding.
+// shell worker_prepare created with a typed dense region that keeps the
+// shell's io mode and storage binding; zero-filled unless the caller writes
+// every cell (zero_fill = false skips the pass).
 DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, RegionKind kind,
-                           ElementKind elem, const BoundingBox& box);
+                           ElementKind elem, const BoundingBox& box, bool zero_fill = true);
 
 }  // namespace rt

@@ -45,7 +45,7 @@ void use_pinned_payloads(std::size_t min_bytes, std::size_t pool_bytes) {
 void use_pageable_payloads() { set_payload_allocator(nullptr, nullptr, 0, 0); }
 
 DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, RegionKind kind,
-                           ElementKind elem, const BoundingBox& box) {
+                           ElementKind elem, const BoundingBox& box, bool zero_fill) {
   IoMode mode = IoMode::kOutput;
   std::string binding;
   if (const DataRegion* shell = local.get_data_region(id)) {
@@ -54,7 +54,8 @@ DataRegion& install_output(RegionTemplate& local, const DataRegionId& id, Region
     local.remove_data_region(id);
   }
   DataRegion r(id, kind, elem, box);
-  r.put_chunk(box, Bytes(std::size_t(box.volume()) * element_size(elem), 0));
+  const std::size_t n = std::size_t(box.volume()) * element_size(elem);
+  r.put_chunk(box, zero_fill ? Bytes(n, 0) : Bytes(n));
   r.set_io_mode(mode);
   r.set_storage_binding(binding);
   return local.insert_data_region(std::move(r));
@@ -95,9 +96,9 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
   // 3 like the RGB tile (a rank mix throws in RegionTemplate's box fold).
   const BoundingBox b2({b3.lo(0), b3.lo(1), 0}, {b3.hi(0), b3.hi(1), 0});
 
-  DataRegion& mask = install_output(local, ids.mask, RegionKind::kDense2D, ElementKind::kU8, b2);
+  DataRegion& mask = install_output(local, ids.mask, RegionKind::kDense2D, ElementKind::kU8, b2, false);
   DataRegion& labels =
-      install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2);
+      install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2, false);
   const std::int32_t cap = wc.gpu->max_objects();
   std::vector<float> feats(std::size_t(cap) * RTG_NUM_FEATURES);
   std::int32_t n = 0;
@@ -107,7 +108,7 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
                              nullptr, feats.data(), cap, &n));
   if (n > 0) {
     const BoundingBox fb({0, 0, 0}, {n - 1, RTG_NUM_FEATURES - 1, 0});
-    DataRegion& f = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb);
+    DataRegion& f = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb, false);
     std::memcpy(f.find_chunk(fb)->payload.data(), feats.data(),
                 sizeof(float) * std::size_t(n) * RTG_NUM_FEATURES);
   }

@@ -35,7 +35,8 @@ DataRegion MemoryStore::read_region(const DataRegionId& id, const BoundingBox& q
     }
     if (p->box.intersects(query)) break;  // a newer piece overwrites part of it
   }
-  Bytes canvas(std::size_t(query.volume()) * es, 0);
+  // every cell is written below (or the read throws), so no zero pass
+  Bytes canvas(std::size_t(query.volume()) * es);
   // one piece containing the query proves coverage without a per-cell map
   bool covered = false;
   for (const auto& p : it->second) covered = covered || p.box.contains(query);
