@@ -33,9 +33,13 @@ class GpuDevice {
   rtg_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   std::int32_t max_objects() const { return max_objects_; }
+  // Pinned max_objects x RTG_NUM_FEATURES rows: rtg_process_tile writes the
+  // n live rows straight into it (zero-copy stores, no cap-row copy).
+  float* feature_staging() const { return features_; }
 
  private:
   rtg_ctx* ctx_ = nullptr;
+  float* features_ = nullptr;
   int device_ = 0;
   std::int32_t max_objects_ = 0;
 };

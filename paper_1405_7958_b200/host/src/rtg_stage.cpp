@@ -24,9 +24,17 @@ GpuDevice::GpuDevice(int device, std::int64_t max_h, std::int64_t max_w,
                      std::int32_t max_objects)
     : device_(device), max_objects_(max_objects) {
   rtg_check(rtg_ctx_create(device, max_h, max_w, max_objects, &ctx_));
+  void* f = nullptr;
+  const int st = rtg_host_alloc(sizeof(float) * std::size_t(max_objects) * RTG_NUM_FEATURES, &f);
+  if (st != RTG_OK) {
+    rtg_ctx_destroy(ctx_);
+    throw_rtg_error(st);
+  }
+  features_ = static_cast<float*>(f);
 }
 
 GpuDevice::~GpuDevice() {
+  if (features_) rtg_host_free(features_);
   if (ctx_) rtg_ctx_destroy(ctx_);
 }
 
@@ -100,16 +108,16 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
   DataRegion& labels =
       install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2, false);
   const std::int32_t cap = wc.gpu->max_objects();
-  std::vector<float> feats(std::size_t(cap) * RTG_NUM_FEATURES);
+  float* feats = wc.gpu->feature_staging();
   std::int32_t n = 0;
   rtg_check(rtg_process_tile(wc.gpu->ctx(), c->payload.data(), h, w, 3 * w, &params,
                              mask.find_chunk(b2)->payload.data(),
                              reinterpret_cast<std::int32_t*>(labels.find_chunk(b2)->payload.data()),
-                             nullptr, feats.data(), cap, &n));
+                             nullptr, feats, cap, &n));
   if (n > 0) {
     const BoundingBox fb({0, 0, 0}, {n - 1, RTG_NUM_FEATURES - 1, 0});
     DataRegion& f = install_output(local, ids.features, RegionKind::kDense2D, ElementKind::kF32, fb, false);
-    std::memcpy(f.find_chunk(fb)->payload.data(), feats.data(),
+    std::memcpy(f.find_chunk(fb)->payload.data(), feats,
                 sizeof(float) * std::size_t(n) * RTG_NUM_FEATURES);
   }
 }
