@@ -41,6 +41,13 @@ class StorageBackend {
   virtual const std::string& name() const = 0;
   // Persists every chunk of a materialised region (last writer wins).
   virtual Completion stage_region(const DataRegion& region, int origin_node) = 0;
+  // Same, for a region the caller is done with: a backend may take the
+  // payloads instead of copying them; the region ends unmaterialised.
+  virtual Completion stage_region_consume(DataRegion& region, int origin_node) {
+    Completion c = stage_region(region, origin_node);
+    region.drop_payload();
+    return c;
+  }
   // Assembles the query box from staged chunks; NotFoundError when any cell
   // was never written.
   virtual DataRegion read_region(const DataRegionId& id, const BoundingBox& query) = 0;
@@ -52,6 +59,7 @@ class MemoryStore : public StorageBackend {
   explicit MemoryStore(std::string name) : name_(std::move(name)) {}
   const std::string& name() const override { return name_; }
   Completion stage_region(const DataRegion& region, int origin_node) override;
+  Completion stage_region_consume(DataRegion& region, int origin_node) override;
   DataRegion read_region(const DataRegionId& id, const BoundingBox& query) override;
 
  private:
@@ -192,8 +200,11 @@ class ManagerState {
 // replace them with correctly typed regions.
 RegionTemplate worker_prepare(const StageInstance& stage, StorageRegistry& storage);
 // Stages materialised outputs and drops inputs; completions in descriptor order.
+// consume = true (the executor, which discards `local` next) lets the store
+// take the output payloads instead of copying them.
 std::vector<Completion> stage_finalize(RegionTemplate& local, const StageInstance& stage,
-                                       StorageRegistry& storage, int origin_node);
+                                       StorageRegistry& storage, int origin_node,
+                                       bool consume = false);
 
 // ---- executor ------------------------------------------------------------------------------
 // Demand-driven loop over the manager's stages (the real counterpart of the

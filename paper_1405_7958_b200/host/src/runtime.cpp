@@ -17,6 +17,20 @@ Completion MemoryStore::stage_region(const DataRegion& region, int /*origin_node
   return Completion();
 }
 
+Completion MemoryStore::stage_region_consume(DataRegion& region, int /*origin_node*/) {
+  std::vector<BoundingBox> boxes;
+  for (const auto& [box, c] : region.chunks()) boxes.push_back(box);
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto& v = pieces_[region.id()];
+    for (const auto& box : boxes)
+      v.push_back(Piece{box, region.kind(), region.element_kind(),
+                        std::move(region.find_chunk(box)->payload)});
+  }
+  region.drop_payload();
+  return Completion();
+}
+
 DataRegion MemoryStore::read_region(const DataRegionId& id, const BoundingBox& query) {
   std::lock_guard<std::mutex> lk(mu_);
   auto it = pieces_.find(id);
@@ -288,7 +302,7 @@ RegionTemplate worker_prepare(const StageInstance& stage, StorageRegistry& stora
 }
 
 std::vector<Completion> stage_finalize(RegionTemplate& local, const StageInstance& stage,
-                                       StorageRegistry& storage, int origin_node) {
+                                       StorageRegistry& storage, int origin_node, bool consume) {
   std::vector<Completion> out;
   for (const auto& d : stage.region_descriptors) {
     const DataRegion* r = local.get_data_region(d.id);
@@ -297,7 +311,10 @@ std::vector<Completion> stage_finalize(RegionTemplate& local, const StageInstanc
       local.remove_data_region(d.id);
       continue;
     }
-    if (r->materialized()) out.push_back(storage.at(d.storage_binding).stage_region(*r, origin_node));
+    if (!r->materialized()) continue;
+    StorageBackend& s = storage.at(d.storage_binding);
+    out.push_back(consume ? s.stage_region_consume(*local.get_data_region(d.id), origin_node)
+                          : s.stage_region(*r, origin_node));
   }
   return out;
 }
@@ -357,7 +374,7 @@ ExecutorStats run_stages(ManagerState& manager, StorageRegistry& storage,
           wrm.complete(*tid);
         }
         wc.local = nullptr;
-        for (auto& c : stage_finalize(local, stage, storage, w)) c.wait();
+        for (auto& c : stage_finalize(local, stage, storage, w, /*consume=*/true)) c.wait();
         std::lock_guard<std::mutex> lk(mu);
         manager.stage_complete(*sid);
         stats.stages += 1;

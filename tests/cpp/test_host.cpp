@@ -104,6 +104,18 @@ void containers() {
       require(dst == want && seen == seen_want, "trial " + std::to_string(trial));
     }
   });
+  check("stage_region_consume moves payloads into the store, region ends unmaterialised", [] {
+    MemoryStore st("s");
+    const DataRegionId id{"t", "c", "raw", 0, 0};
+    DataRegion a(id, RegionKind::kDense2D, ElementKind::kU8, box2(0, 0, 3, 3));
+    std::vector<std::uint8_t> v(16);
+    for (int i = 0; i < 16; ++i) v[std::size_t(i)] = std::uint8_t(i);
+    a.put_chunk(a.bbox(), v);
+    const DataRegion copy = a;
+    st.stage_region_consume(a, 0).wait();
+    require(!a.materialized() && a.chunks().empty(), "region consumed");
+    require(st.read_region(id, box2(0, 0, 3, 3)) == copy, "store holds the bytes");
+  });
   check("MemoryStore read: a newer partial piece wins over an older exact piece", [] {
     MemoryStore st("s");
     const DataRegionId id{"t", "p", "raw", 0, 0};
