@@ -1,179 +1,145 @@
-// RTP1 pack / unpack (see rt/pack.hpp; reference pack.cpp:33-121 defines the
-// same byte layout through its wire::Writer / wire::Reader).
+// RTP1 template packs (rt/pack.hpp; field table in DESIGN.md §8).
+//
+// Decoding is two-phase: parse() turns the bytes into a flat description
+// whose payloads are views into the caller's buffer (every length and enum is
+// checked here, nothing is allocated for payloads), then assemble() builds the
+// RegionTemplate and checks what only the assembled object can tell (dense
+// payload lengths, the materialised flag, the declared box).  The byte layout
+// is the reference's (pack.cpp:33-132); the code structure is not.
 #include "rt/pack.hpp"
 
-#include <cstring>
 #include <string>
+
+#include "wire_codec.hpp"
 
 namespace rt {
 namespace {
 
-class Out {
- public:
-  void u8(std::uint8_t v) { b_.push_back(v); }
-  void le(std::uint64_t v, int n) {
-    for (int i = 0; i < n; ++i) b_.push_back(std::uint8_t(v >> (8 * i)));
-  }
-  void u32(std::uint32_t v) { le(v, 4); }
-  void u64(std::uint64_t v) { le(v, 8); }
-  void i64(std::int64_t v) { le(std::uint64_t(v), 8); }
-  void str(const std::string& s) {
-    u32(std::uint32_t(s.size()));
-    b_.insert(b_.end(), s.begin(), s.end());
-  }
-  void raw(const Bytes& p) { b_.insert(b_.end(), p.begin(), p.end()); }
-  void box(const BoundingBox& b) {
-    u8(std::uint8_t(b.dims()));
-    for (int a = 0; a < b.dims(); ++a) i64(b.lo(a));
-    for (int a = 0; a < b.dims(); ++a) i64(b.hi(a));
-  }
-  std::vector<std::uint8_t> take() { return std::move(b_); }
+constexpr std::uint8_t kFlagPayloads = 0x01;
 
- private:
-  std::vector<std::uint8_t> b_;
+struct ChunkView {
+  std::uint64_t id;
+  BoundingBox box;
+  std::span<const std::uint8_t> bytes;
 };
 
-class In {
- public:
-  explicit In(std::span<const std::uint8_t> s) : s_(s) {}
-  bool at_end() const { return pos_ == s_.size(); }
-  std::uint64_t le(int n) {
-    need(std::uint64_t(n));
-    std::uint64_t v = 0;
-    for (int i = 0; i < n; ++i) v |= std::uint64_t(s_[pos_++]) << (8 * i);
-    return v;
-  }
-  std::uint8_t u8() { return std::uint8_t(le(1)); }
-  std::uint32_t u32() { return std::uint32_t(le(4)); }
-  std::uint64_t u64() { return le(8); }
-  std::int64_t i64() { return std::int64_t(le(8)); }
-  std::string str() {
-    const std::uint32_t n = u32();
-    need(n);
-    std::string out(reinterpret_cast<const char*>(s_.data() + pos_), n);
-    pos_ += n;
-    return out;
-  }
-  Bytes raw(std::uint64_t n) {
-    need(n);
-    Bytes out(s_.begin() + std::ptrdiff_t(pos_),
-                                  s_.begin() + std::ptrdiff_t(pos_ + n));
-    pos_ += n;
-    return out;
-  }
-  BoundingBox box() {
-    const int dims = u8();
-    if (dims == 0) return BoundingBox();
-    if (dims > BoundingBox::kMaxDims) throw DecodeError("bounding box rank out of range");
-    std::int64_t lo[BoundingBox::kMaxDims], hi[BoundingBox::kMaxDims];
-    for (int a = 0; a < dims; ++a) lo[a] = i64();
-    for (int a = 0; a < dims; ++a) hi[a] = i64();
-    return BoundingBox(dims, lo, hi);
-  }
-
- private:
-  void need(std::uint64_t n) const {
-    if (n > s_.size() - pos_) throw DecodeError("buffer truncated");
-  }
-  std::span<const std::uint8_t> s_;
-  std::size_t pos_ = 0;
+struct RegionView {
+  wire::Identity ident;
+  IoMode io = IoMode::kInput;
+  bool lazy = false, materialized = false;
+  BoundingBox box, roi;
+  std::string binding;
+  std::vector<ChunkView> chunks;
 };
 
-std::uint8_t enum_byte(std::uint8_t raw, std::uint8_t max, const char* what) {
-  if (raw > max) throw DecodeError(std::string("bad enum value for ") + what);
-  return raw;
+struct TemplateView {
+  std::string name;
+  BoundingBox declared;
+  std::vector<RegionView> regions;
+};
+
+TemplateView parse(std::span<const std::uint8_t> bytes) {
+  wire::Source in(bytes, "RTP1 header");
+  const auto magic = in.get<std::uint32_t>("magic");
+  if (magic != kPackMagic) in.fail("not an RTP1 pack (magic " + std::to_string(magic) + ")");
+  const auto flags = in.get<std::uint8_t>("flags");
+  if (flags & ~kFlagPayloads) in.fail("undefined flag bits " + std::to_string(flags));
+
+  TemplateView t;
+  t.name = in.get_text("template name");
+  t.declared = in.get_extent("template box");
+  const auto count = in.get<std::uint32_t>("region count");
+  // a region record takes at least 43 bytes: four empty texts, two i64, five
+  // u8, two rank-0 extents and a chunk count
+  if (std::uint64_t(count) * 43 > in.left())
+    in.fail("region count " + std::to_string(count) + " cannot fit in " +
+            std::to_string(in.left()) + " bytes");
+  t.regions.resize(count);
+  for (std::uint32_t k = 0; k < count; ++k) {
+    in.relabel("RTP1 region " + std::to_string(k));
+    RegionView& r = t.regions[k];
+    r.ident = wire::get_identity(in);
+    r.io = in.get_enum("io mode", IoMode::kInputOutput);
+    r.lazy = in.get<std::uint8_t>("lazy") != 0;
+    r.materialized = in.get<std::uint8_t>("materialized") != 0;
+    r.box = in.get_extent("box");
+    r.roi = in.get_extent("roi");
+    r.binding = in.get_text("storage binding");
+    const auto nchunks = in.get<std::uint32_t>("chunk count");
+    for (std::uint32_t c = 0; c < nchunks; ++c) {
+      ChunkView v;
+      v.id = in.get<std::uint64_t>("chunk id");
+      v.box = in.get_extent("chunk box");
+      v.bytes = in.get_blob(in.get<std::uint64_t>("payload length"), "payload");
+      r.chunks.push_back(v);
+    }
+  }
+  if (in.left() != 0) in.fail(std::to_string(in.left()) + " bytes follow the last region");
+  return t;
 }
 
-RegionTemplate decode(std::span<const std::uint8_t> bytes) {
-  In in(bytes);
-  if (in.u32() != kPackMagic) throw DecodeError("bad magic");
-  const std::uint8_t flags = in.u8();
-  if (flags > 1) throw DecodeError("bad flags");
-  RegionTemplate t(in.str());
-  const BoundingBox declared = in.box();
-  const std::uint32_t nregions = in.u32();
-  for (std::uint32_t k = 0; k < nregions; ++k) {
-    DataRegionId id;
-    id.ns = in.str();
-    id.key = in.str();
-    id.type_tag = in.str();
-    id.timestamp = in.i64();
-    id.version = in.i64();
-    const auto kind = RegionKind(enum_byte(in.u8(), 4, "region kind"));
-    const auto elem = ElementKind(enum_byte(in.u8(), 4, "element kind"));
-    const auto io = IoMode(enum_byte(in.u8(), 2, "io mode"));
-    const bool lazy = in.u8() != 0;
-    const bool materialized = in.u8() != 0;
-    const BoundingBox box = in.box();
-    const BoundingBox roi = in.box();
-    std::string binding = in.str();
-    DataRegion r(std::move(id), kind, elem, box);
-    r.set_roi(roi);
-    r.set_io_mode(io);
-    r.set_lazy(lazy);
-    r.set_storage_binding(std::move(binding));
-    const std::uint32_t nchunks = in.u32();
-    for (std::uint32_t c = 0; c < nchunks; ++c) {
-      const std::uint64_t wire_id = in.u64();
-      const BoundingBox cbox = in.box();
-      const std::uint64_t len = in.u64();
-      r.put_chunk(cbox, in.raw(len)).chunk_id = wire_id;  // keep the sender's id
-    }
-    if (materialized != r.materialized())
-      throw DecodeError("materialized flag disagrees with chunk payload");
+RegionTemplate assemble(const TemplateView& v) {
+  RegionTemplate t(v.name);
+  for (const RegionView& rv : v.regions) {
+    DataRegion r(rv.ident.id, rv.ident.kind, rv.ident.element, rv.box);
+    r.set_roi(rv.roi);
+    r.set_io_mode(rv.io);
+    r.set_lazy(rv.lazy);
+    r.set_storage_binding(rv.binding);
+    for (const ChunkView& c : rv.chunks)
+      r.put_chunk(c.box, Bytes(c.bytes.begin(), c.bytes.end())).chunk_id = c.id;
+    if (r.materialized() != rv.materialized)
+      throw DecodeError("RTP1 region " + rv.ident.id.to_string() + " says materialized=" +
+                        std::to_string(int(rv.materialized)) + " but carries " +
+                        std::to_string(rv.chunks.size()) + " chunks");
     t.insert_data_region(std::move(r));
   }
-  if (!in.at_end()) throw DecodeError("trailing bytes after template");
-  if (!(t.bbox() == declared)) throw DecodeError("declared template box disagrees with regions");
+  if (t.bbox() != v.declared)
+    throw DecodeError("RTP1 template box " + v.declared.to_string() +
+                      " differs from its regions' union " + t.bbox().to_string());
   return t;
 }
 
 }  // namespace
 
 std::vector<std::uint8_t> pack_template(const RegionTemplate& t, bool include_payload) {
-  Out out;
-  out.u32(kPackMagic);
-  out.u8(include_payload ? 1 : 0);
-  out.str(t.name());
-  out.box(t.bbox());
-  out.u32(std::uint32_t(t.regions().size()));
+  wire::Sink out;
+  out.put(kPackMagic);
+  out.put(std::uint8_t(include_payload ? kFlagPayloads : 0));
+  out.put_text(t.name());
+  out.put_extent(t.bbox());
+  out.put(std::uint32_t(t.regions().size()));
   for (const auto& [id, r] : t.regions()) {
-    out.str(id.ns);
-    out.str(id.key);
-    out.str(id.type_tag);
-    out.i64(id.timestamp);
-    out.i64(id.version);
-    out.u8(std::uint8_t(r.kind()));
-    out.u8(std::uint8_t(r.element_kind()));
-    out.u8(std::uint8_t(r.io_mode()));
-    out.u8(r.lazy() ? 1 : 0);
-    out.u8(include_payload && r.materialized() ? 1 : 0);
-    out.box(r.bbox());
-    out.box(r.roi());
-    out.str(r.storage_binding());
-    if (!include_payload) {
-      out.u32(0);
-      continue;
-    }
-    out.u32(std::uint32_t(r.chunks().size()));
-    for (const auto& [cbox, chunk] : r.chunks()) {
-      out.u64(chunk.chunk_id);
-      out.box(cbox);
-      out.u64(chunk.payload.size());
-      out.raw(chunk.payload);
+    const bool ship = include_payload && r.materialized();
+    wire::put_identity(out, id, r.kind(), r.element_kind());
+    out.put(r.io_mode());
+    out.put(std::uint8_t(r.lazy()));
+    out.put(std::uint8_t(ship));
+    out.put_extent(r.bbox());
+    out.put_extent(r.roi());
+    out.put_text(r.storage_binding());
+    // metadata-only packs send no chunks even for materialised regions
+    out.put(std::uint32_t(include_payload ? r.chunks().size() : 0));
+    if (!include_payload) continue;
+    for (const auto& [box, c] : r.chunks()) {
+      out.put(c.chunk_id);
+      out.put_extent(box);
+      out.put(std::uint64_t(c.payload.size()));
+      out.put_blob(c.payload.data(), c.payload.size());
     }
   }
-  return out.take();
+  return std::move(out.bytes());
 }
 
 RegionTemplate unpack_template(std::span<const std::uint8_t> bytes) {
   try {
-    return decode(bytes);
+    return assemble(parse(bytes));
   } catch (const DecodeError&) {
     throw;
   } catch (const Error& e) {
-    // a structural violation reached through decoded bytes is corruption
-    throw DecodeError(std::string("corrupt template buffer: ") + e.what());
+    // the bytes describe an object the containers reject (inverted box,
+    // bad dense length, duplicate id, rank mix): that is a corrupt pack
+    throw DecodeError(std::string("RTP1 pack describes an invalid template: ") + e.what());
   }
 }
 

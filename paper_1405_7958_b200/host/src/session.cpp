@@ -1,153 +1,127 @@
-// RTS1 session files (see rt/session.hpp).
+// RTS1 write-session files (rt/session.hpp; field table in DESIGN.md §8).
+//
+// The file is loaded whole and decoded trailer-first: the trailer fixes the
+// record area [16, index) and the index of record offsets; every record is
+// then decoded inside the record area only, so a corrupt offset can never
+// read the index or the trailer as record bytes.  The byte layout is the
+// reference's (disk_store.cpp:150-217); the code structure is not.
 #include "rt/session.hpp"
 
 #include <fstream>
+#include <iterator>
+
+#include "wire_codec.hpp"
 
 namespace rt {
 namespace {
 
-void le(std::string& o, std::uint64_t v, int n) {
-  for (int i = 0; i < n; ++i) o.push_back(char(v >> (8 * i)));
-}
-void put_str(std::string& o, const std::string& s) {
-  le(o, s.size(), 4);
-  o += s;
-}
-void put_box(std::string& o, const BoundingBox& b) {
-  o.push_back(char(b.dims()));
-  for (int a = 0; a < b.dims(); ++a) le(o, std::uint64_t(b.lo(a)), 8);
-  for (int a = 0; a < b.dims(); ++a) le(o, std::uint64_t(b.hi(a)), 8);
+constexpr std::size_t kHeaderBytes = 4 + 8 + 4;  // magic, session seq, record count
+constexpr std::size_t kTrailerBytes = 8 + 4;     // index offset, end magic
+
+std::vector<std::uint8_t> load(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw IoError("session file " + path + " could not be opened for reading");
+  return std::vector<std::uint8_t>(std::istreambuf_iterator<char>(f), {});
 }
 
-// Whole file in memory; every read is bounds-checked against it.
-class FileBytes {
- public:
-  explicit FileBytes(const std::string& path) {
-    std::ifstream f(path, std::ios::binary);
-    if (!f) throw IoError("cannot open session file: " + path);
-    f.seekg(0, std::ios::end);
-    data_.resize(std::size_t(f.tellg()));
-    f.seekg(0);
-    if (!data_.empty()) f.read(data_.data(), std::streamsize(data_.size()));
-  }
-  std::uint64_t size() const { return data_.size(); }
-  void seek(std::uint64_t off) {
-    if (off > data_.size()) throw DecodeError("session file offset out of range");
-    pos_ = off;
-  }
-  std::uint64_t get(int n) {
-    if (std::uint64_t(n) > data_.size() - pos_) throw DecodeError("session file truncated");
-    std::uint64_t v = 0;
-    for (int i = 0; i < n; ++i) v |= std::uint64_t(std::uint8_t(data_[pos_++])) << (8 * i);
-    return v;
-  }
-  std::string str() {
-    const std::uint64_t n = get(4);
-    if (n > data_.size()) throw DecodeError("session file string overruns");
-    if (n > data_.size() - pos_) throw DecodeError("session file truncated");
-    std::string s(data_.data() + pos_, n);
-    pos_ += n;
-    return s;
-  }
-  Bytes raw(std::uint64_t n) {
-    if (n > data_.size()) throw DecodeError("session file payload overruns");
-    if (n > data_.size() - pos_) throw DecodeError("session file truncated");
-    Bytes b(data_.begin() + std::ptrdiff_t(pos_),
-                                data_.begin() + std::ptrdiff_t(pos_ + n));
-    pos_ += n;
-    return b;
-  }
-  BoundingBox box() {
-    const int dims = int(get(1));
-    if (dims == 0) return BoundingBox();
-    if (dims > BoundingBox::kMaxDims) throw DecodeError("session file box rank out of range");
-    std::int64_t lo[BoundingBox::kMaxDims], hi[BoundingBox::kMaxDims];
-    for (int a = 0; a < dims; ++a) lo[a] = std::int64_t(get(8));
-    for (int a = 0; a < dims; ++a) hi[a] = std::int64_t(get(8));
-    return BoundingBox(dims, lo, hi);
-  }
+void put_record(wire::Sink& out, const DiskRecord& r) {
+  wire::put_identity(out, r.id, r.kind, r.element_kind);
+  out.put_extent(r.box);
+  out.put(r.seq);
+  out.put(std::uint64_t(r.payload.size()));
+  out.put_blob(r.payload.data(), r.payload.size());
+}
 
- private:
-  std::string data_;
-  std::uint64_t pos_ = 0;
+DiskRecord get_record(wire::Source& in) {
+  const wire::Identity ident = wire::get_identity(in);
+  DiskRecord r;
+  r.id = ident.id;
+  r.kind = ident.kind;
+  r.element_kind = ident.element;
+  r.box = in.get_extent("box");
+  r.seq = in.get<std::uint64_t>("sequence");
+  const std::span<const std::uint8_t> p = in.get_blob(in.get<std::uint64_t>("payload length"), "payload");
+  r.payload.assign(p.begin(), p.end());
+  return r;
+}
+
+// Where the records of a decoded file lie.
+struct Layout {
+  std::span<const std::uint8_t> records;  // bytes [0, index): offsets index into this window
+  std::vector<std::uint64_t> offsets;
 };
 
-DiskRecord record(FileBytes& in) {
-  DiskRecord r;
-  r.id.ns = in.str();
-  r.id.key = in.str();
-  r.id.type_tag = in.str();
-  r.id.timestamp = std::int64_t(in.get(8));
-  r.id.version = std::int64_t(in.get(8));
-  const auto kind = std::uint8_t(in.get(1)), elem = std::uint8_t(in.get(1));
-  if (kind > 4 || elem > 4) throw DecodeError("session record bad enum");
-  r.kind = RegionKind(kind);
-  r.element_kind = ElementKind(elem);
-  r.box = in.box();
-  r.seq = in.get(8);
-  r.payload = in.raw(in.get(8));
-  return r;
+Layout layout(std::span<const std::uint8_t> file, const std::string& path) {
+  if (file.size() < kHeaderBytes + kTrailerBytes)
+    throw DecodeError("RTS1 file " + path + " holds " + std::to_string(file.size()) +
+                      " bytes, fewer than an empty session");
+  wire::Source head(file.first(kHeaderBytes), "RTS1 header of " + path);
+  if (head.get<std::uint32_t>("magic") != kSessionMagic) head.fail("not an RTS1 session file");
+  head.get<std::uint64_t>("session sequence");
+  const auto count = head.get<std::uint32_t>("record count");
+
+  wire::Source tail(file.last(kTrailerBytes), "RTS1 trailer of " + path);
+  const auto index = tail.get<std::uint64_t>("index offset");
+  if (tail.get<std::uint32_t>("end magic") != kSessionEndMagic) tail.fail("end marker missing");
+  const std::uint64_t body_end = file.size() - kTrailerBytes;
+  if (index < kHeaderBytes || index > body_end || (body_end - index) / 8 < count)
+    tail.fail("index of " + std::to_string(count) + " offsets at " + std::to_string(index) +
+              " does not fit between the header and the trailer");
+
+  Layout out;
+  out.records = file.first(std::size_t(index));
+  wire::Source idx(file.subspan(std::size_t(index), std::size_t(body_end - index)),
+                   "RTS1 index of " + path);
+  out.offsets.resize(count);
+  for (auto& off : out.offsets) off = idx.get<std::uint64_t>("record offset");
+  return out;
 }
 
 }  // namespace
 
 std::vector<std::uint64_t> write_session_file(const std::string& path, std::uint64_t session_seq,
                                               const std::vector<DiskRecord>& records) {
-  std::string o;
-  le(o, kSessionMagic, 4);
-  le(o, session_seq, 8);
-  le(o, records.size(), 4);
+  wire::Sink out;
+  out.put(kSessionMagic);
+  out.put(session_seq);
+  out.put(std::uint32_t(records.size()));
   std::vector<std::uint64_t> offsets;
   offsets.reserve(records.size());
   for (const DiskRecord& r : records) {
-    offsets.push_back(o.size());
-    put_str(o, r.id.ns);
-    put_str(o, r.id.key);
-    put_str(o, r.id.type_tag);
-    le(o, std::uint64_t(r.id.timestamp), 8);
-    le(o, std::uint64_t(r.id.version), 8);
-    o.push_back(char(r.kind));
-    o.push_back(char(r.element_kind));
-    put_box(o, r.box);
-    le(o, r.seq, 8);
-    le(o, r.payload.size(), 8);
-    o.append(reinterpret_cast<const char*>(r.payload.data()), r.payload.size());
+    offsets.push_back(out.size());
+    put_record(out, r);
   }
-  const std::uint64_t footer = o.size();
-  for (std::uint64_t off : offsets) le(o, off, 8);
-  le(o, footer, 8);
-  le(o, kSessionEndMagic, 4);
+  const std::uint64_t index = out.size();
+  for (const std::uint64_t off : offsets) out.put(off);
+  out.put(index);
+  out.put(kSessionEndMagic);
+
   std::ofstream f(path, std::ios::binary | std::ios::trunc);
-  if (!f || !f.write(o.data(), std::streamsize(o.size())))
-    throw IoError("cannot write session file: " + path);
+  const auto& b = out.bytes();
+  f.write(reinterpret_cast<const char*>(b.data()), std::streamsize(b.size()));
+  if (!f.flush()) throw IoError("session file " + path + " could not be written");
   return offsets;
 }
 
 std::vector<DiskRecord> read_session_file(const std::string& path) {
-  FileBytes in(path);
-  if (in.size() < 4 + 8 + 4 + 8 + 4) throw DecodeError("session file too short: " + path);
-  if (in.get(4) != kSessionMagic) throw DecodeError("session file bad magic");
-  in.get(8);  // session seq
-  const std::uint32_t count = std::uint32_t(in.get(4));
-  in.seek(in.size() - 12);
-  const std::uint64_t footer = in.get(8);
-  if (in.get(4) != kSessionEndMagic) throw DecodeError("session file bad end magic");
-  in.seek(footer);
-  std::vector<std::uint64_t> offsets(count);
-  for (auto& off : offsets) off = in.get(8);
+  const std::vector<std::uint8_t> file = load(path);
+  const Layout lay = layout(file, path);
   std::vector<DiskRecord> out;
-  out.reserve(count);
-  for (std::uint64_t off : offsets) {
-    in.seek(off);
-    out.push_back(record(in));
+  out.reserve(lay.offsets.size());
+  wire::Source in(lay.records, "");
+  for (std::size_t k = 0; k < lay.offsets.size(); ++k) {
+    in.relabel("RTS1 record " + std::to_string(k) + " of " + path);
+    in.jump(lay.offsets[k], "record offset");
+    out.push_back(get_record(in));
   }
   return out;
 }
 
 DiskRecord read_record_at(const std::string& path, std::uint64_t offset) {
-  FileBytes in(path);
-  in.seek(offset);
-  return record(in);
+  const std::vector<std::uint8_t> file = load(path);
+  wire::Source in(file, "RTS1 record at " + std::to_string(offset) + " of " + path);
+  in.jump(offset, "record offset");
+  return get_record(in);
 }
 
 std::vector<DiskRecord> template_records(const RegionTemplate& t, std::uint64_t seq0) {
