@@ -274,6 +274,34 @@ int rtg_process_tiles(rtg_ctx* ctx, int32_t count, const uint8_t* const* rgb, in
                       int64_t w, int64_t pitch_bytes, const rtg_params* params,
                       float* const* features_out, int32_t max_rows, int32_t* n_objects);
 
+/* ---- whole tile, host buffers, asynchronous (3-phase pipeline) ----------- */
+
+/* The stage body as the paper's upload / compute / download pipeline
+ * (the reference models it only in virtual time,
+ * src/wrm.cpp:385-415 prefetch_pipeline and src/sim.cpp:672-684).  Enqueues
+ * the H2D copy of `rgb`, the stage and the D2H copies of the requested
+ * outputs (any of mask_out / labels_out / hema_out / features_out may be
+ * NULL) and returns at once with a ticket.  Each context keeps
+ * RTG_ASYNC_SLOTS tiles in flight, each with its own device buffers: the
+ * upload of tile t+1 overlaps the stage of tile t and the download of tile
+ * t-1.  When every slot is busy the call first waits for the oldest ticket
+ * (whose result stays available to rtg_ticket_wait).  Host buffers must stay
+ * valid, and outputs unread, until the ticket is waited.  Host memory from
+ * rtg_host_alloc gives full overlap; pageable outputs make the call block
+ * until their copies finish.  features_out holds max_rows rows. */
+#define RTG_ASYNC_SLOTS 3
+int rtg_process_tile_async(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
+                           int64_t pitch_bytes, const rtg_params* params,
+                           uint8_t* mask_out, int32_t* labels_out, uint8_t* hema_out,
+                           float* features_out, int32_t max_rows, uint64_t* ticket);
+/* Waits for a ticket's outputs; *n_objects receives the tile's object count.
+ * RTG_ERR_OVERFLOW when it exceeds max_rows or the context's max_objects (the
+ * first rows are still written); RTG_ERR_NOT_FOUND for an unknown ticket or
+ * one already waited. */
+int rtg_ticket_wait(rtg_ctx* ctx, uint64_t ticket, int32_t* n_objects);
+/* *done = 1 once the ticket's outputs are in host memory (does not block). */
+int rtg_ticket_query(rtg_ctx* ctx, uint64_t ticket, int* done);
+
 /* ---- whole tile, device buffers (asynchronous on the ctx stream) --------- */
 
 /* d_rgb: device RGB (pitch_bytes >= 3*w).  d_mask (u8), d_labels (i32),

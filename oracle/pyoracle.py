@@ -14,7 +14,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
+NATIVE_PATH = os.path.join(_HERE, "_native", "liboracle.so")
 NUM_FEATURES = 20
+DEFAULT_SEED = 1405795800
 _lib = None
 
 
@@ -22,13 +24,28 @@ def build() -> None:
     subprocess.run(["make", "-C", _HERE, "-s"], check=True)
 
 
-def load() -> ctypes.CDLL:
+def build_native() -> str:
+    """-O3 -march=native build for the host that times it.
+    Always rebuilt: a copy made on another machine may use instructions this
+    CPU lacks."""
+    subprocess.run(["make", "-C", _HERE, "-s", "-B", "native"], check=True,
+                   stdout=subprocess.DEVNULL)
+    return NATIVE_PATH
+
+
+def load(native: bool = False) -> ctypes.CDLL:
+    """The portable build, or (native=True, before any other load) the
+    -march=native build of this host."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        build()
-    lib = ctypes.CDLL(LIB_PATH)
+    if native:
+        path = build_native()
+    else:
+        path = LIB_PATH
+        if not os.path.exists(path):
+            build()
+    lib = ctypes.CDLL(path)
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     sigs = {
         "orc_params_default": ([vp], None),
@@ -45,6 +62,7 @@ def load() -> ctypes.CDLL:
         "orc_texture_row": ([vp, vp, vp, ctypes.c_uint32, vp], None),
         "orc_canny": ([vp, i64, i64, i32, i32, vp], None),
         "orc_process_tile": ([vp, i64, i64, i64, vp, vp, vp, vp, i32, vp], i32),
+        "orc_synth_tile_host": ([ctypes.c_uint64, i64, i64, i64, i64, vp], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -70,12 +88,39 @@ PLANE_DTYPES = {
 }
 
 
+class Params(ctypes.Structure):
+    """rtg_params (include/rtg.h): the oracle and the product consume the same
+    struct layout; declared here so the oracle never imports the product."""
+    _fields_ = [
+        ("h_coef", ctypes.c_double * 3),
+        ("h_scale", ctypes.c_double),
+        ("bg_thresh", ctypes.c_int32),
+        ("rbc_rg10", ctypes.c_int32),
+        ("rbc_rb10", ctypes.c_int32),
+        ("recon_h", ctypes.c_int32),
+        ("recon_conn", ctypes.c_int32),
+        ("nuc_thresh", ctypes.c_int32),
+        ("min_area", ctypes.c_int32),
+        ("max_area", ctypes.c_int32),
+        ("ws_h", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
 def default_params():
-    # the Params struct layout is shared with the product binding
-    from paper_1405_7958_b200.rtg import Params
     p = Params()
     load().orc_params_default(ctypes.byref(p))
     return p
+
+
+def synth_tile_host(tile_row=0, tile_col=0, h=4096, w=4096, seed=DEFAULT_SEED):
+    """The synthetic H&E tile (same generator source as the product's, compiled
+    into the oracle), so the CPU arms never load librtg.so."""
+    out = np.empty((h, w, 3), np.uint8)
+    rc = load().orc_synth_tile_host(seed, tile_row, tile_col, h, w, out.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"orc_synth_tile_host failed ({rc})")
+    return out
 
 
 def colordeconv(rgb, params):

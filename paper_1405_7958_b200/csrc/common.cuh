@@ -6,6 +6,7 @@
 
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "rtg.h"
 
@@ -34,6 +35,13 @@ int cuda_fail(cudaError_t e, const char* what);
     cudaError_t e_ = cudaGetLastError();                          \
     if (e_ != cudaSuccess) return ::rtg::cuda_fail(e_, what);     \
   } while (0)
+
+// Opts `kernel` into `bytes` of dynamic shared memory on `device` once.  The
+// attribute is per device, so it is remembered per (kernel, device) pair
+// under a lock (contexts on different devices and threads share kernels).
+cudaError_t smem_optin(const void* kernel, int device, int bytes);
+#define RTG_SMEM_OPTIN(kernel, bytes) \
+  RTG_CUDA(::rtg::smem_optin(reinterpret_cast<const void*>(kernel), ctx->device, (int)(bytes)))
 
 #define RTG_TRY(call)               \
   do {                              \
@@ -75,6 +83,26 @@ struct HemaLut {
 
 }  // namespace rtg
 
+namespace rtg {
+// One in-flight tile of the asynchronous host-buffer entry point
+// (rtg_process_tile_async): its own device RGB / output planes so the upload
+// of tile t+1, the stage of tile t and the download of tile t-1 overlap (the
+// paper's 3-phase pipeline, reference wrm.cpp:385-415 prefetch_pipeline).
+struct AsyncSlot {
+  uint8_t* rgb = nullptr;     // 3 * max_px
+  uint8_t* mask = nullptr;    // max_px
+  int32_t* labels = nullptr;  // max_px
+  uint8_t* hema = nullptr;    // max_px
+  float* feats = nullptr;     // max_objects x RTG_NUM_FEATURES
+  int32_t* d_n = nullptr;     // object count (device)
+  int32_t* h_n = nullptr;     // object count (pinned host)
+  cudaEvent_t up = nullptr, comp = nullptr, down = nullptr;
+  uint64_t ticket = 0;        // 0 = free
+  int32_t max_rows = 0;       // feature rows the caller asked for (-1: no table)
+};
+constexpr int kAsyncSlots = 3;
+}  // namespace rtg
+
 // The context: every device allocation of the stage lives here (arena).
 struct rtg_ctx {
   int device = 0;
@@ -92,6 +120,16 @@ struct rtg_ctx {
   cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
   int32_t* h_counts = nullptr;  // pinned per-tile object counts (batch entry)
   int32_t h_counts_cap = 0;
+  // rtg_process_tile_async: slots (created on first use), upload / download
+  // streams, and the results of tickets retired before the caller waited
+  rtg::AsyncSlot* slots = nullptr;
+  cudaStream_t up_stream = nullptr, down_stream = nullptr;
+  uint64_t next_ticket = 1;
+  struct Retired {
+    uint64_t ticket;
+    int32_t n, max_rows;
+  };
+  std::vector<Retired> retired;
   uint8_t* hema = nullptr;
   uint8_t* recon = nullptr;   // marker in, reconstruction out
   uint8_t* tissue = nullptr;
@@ -171,6 +209,19 @@ constexpr int kScanChunk = 4096;
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w);
+int check_params(const rtg_params* p);
+// Frees the rtg_process_tile_async slots and streams (rtg_ctx_destroy).
+void release_slots(rtg_ctx* c);
+// The whole stage o1..o9 on device buffers, enqueued on ctx->stream (a
+// cached CUDA graph per argument tuple unless graphs are off / profiling).
+int run_stage(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
+              const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
+              float* d_features, int32_t* d_n);
+// First min(*d_n, cap) feature rows of `src` into host `dst` on `stream`:
+// zero-copy stores of exactly the live rows for pinned destinations, a
+// cudaMemcpyAsync of cap rows otherwise.
+int rows_to_host(rtg_ctx* ctx, cudaStream_t stream, const float* src, const int32_t* d_n,
+                 float* dst, int32_t cap);
 // Stage boundary for rtg_ctx_profile (no-op unless profiling is enabled):
 // stage >= 0 starts that stage, -1 closes the current one.
 void prof_mark(rtg_ctx* ctx, int stage);

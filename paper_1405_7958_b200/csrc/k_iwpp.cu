@@ -491,12 +491,7 @@ int run_iwpp(rtg_ctx* ctx, T* J, MaskF maskf, int64_t h, int64_t w, int border_o
                                                                           border_only);
   RTG_LAUNCH("k_tiles_init");
   const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
-  static bool attr_set[64] = {};  // per instantiation and device
-  if (ctx->device < 64 && !attr_set[ctx->device]) {
-    RTG_CUDA(cudaFuncSetAttribute(k_iwpp<T, CONN, MaskF>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[ctx->device] = true;
-  }
+  RTG_SMEM_OPTIN((k_iwpp<T, CONN, MaskF>), smem);
   int per_sm = 0;
   RTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iwpp<T, CONN, MaskF>,
                                                          kWarpsPerBlock * 32, smem));

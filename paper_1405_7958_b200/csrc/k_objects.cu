@@ -520,24 +520,14 @@ int watershed_objects(rtg_ctx* ctx, const uint8_t* mask, const int32_t* roots,
   RTG_LAUNCH("k_obj_classify");
   {
     const size_t smem = (size_t)kWarpsSmall * (kSmallPx * 9 + 16);
-    static bool attr[64] = {};
-    if (ctx->device < 64 && !attr[ctx->device]) {
-      RTG_CUDA(cudaFuncSetAttribute(k_obj_ws_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-      attr[ctx->device] = true;
-    }
+    RTG_SMEM_OPTIN(k_obj_ws_small, smem);
     k_obj_ws_small<<<ctx->num_sms * 16, 32 * kWarpsSmall, smem, ctx->stream>>>(
         (int)h, (int)w, mask, roots, nobj, ctx->obj_root, ctx->obj_box, ws_h, sep, basin);
     RTG_LAUNCH("k_obj_ws_small");
   }
   {
     const size_t smem = (size_t)kBigPx * 9 + 32;
-    static bool attr[64] = {};
-    if (ctx->device < 64 && !attr[ctx->device]) {
-      RTG_CUDA(cudaFuncSetAttribute(k_obj_ws_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-      attr[ctx->device] = true;
-    }
+    RTG_SMEM_OPTIN(k_obj_ws_big, smem);
     k_obj_ws_big<<<ctx->num_sms, 32, smem, ctx->stream>>>((int)h, (int)w, mask, roots,
                                                          ctx->obj_list, counts2, ctx->obj_root,
                                                          ctx->obj_box, ws_h, sep, basin);

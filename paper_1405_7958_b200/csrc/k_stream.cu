@@ -267,14 +267,8 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
     if (ngroups > 0) {
       // all groups in one resident wave: iters per thread, then as few
       // blocks as cover ngroups at that depth
-      static bool smem_set = false;
-      if (!smem_set) {
-        RTG_CUDA(cudaFuncSetAttribute(k_colordeconv_vec<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCdSmem));
-        RTG_CUDA(cudaFuncSetAttribute(k_colordeconv_vec<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCdSmem));
-        smem_set = true;
-      }
+      RTG_SMEM_OPTIN(k_colordeconv_vec<true>, kCdSmem);
+      RTG_SMEM_OPTIN(k_colordeconv_vec<false>, kCdSmem);
       const int64_t slots = (int64_t)ctx->num_sms * kCdBlocksPerSm * kCdThreads;
       const int iters = (int)ceil_div(ngroups, slots);
       const int blocks = (int)ceil_div(ngroups, (int64_t)kCdThreads * iters);

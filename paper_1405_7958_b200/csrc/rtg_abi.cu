@@ -3,6 +3,8 @@
 // no CPU fallback anywhere in this library.
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "common.cuh"
@@ -30,6 +32,22 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(RTG_ERR_DEVICE, msg);
 }
 
+cudaError_t smem_optin(const void* kernel, int device, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, device})) return cudaSuccess;
+  // the attribute applies to the current device: the caller's ctx device
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return e;
+  if (cur != device && (e = cudaSetDevice(device)) != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (cur != device) cudaSetDevice(cur);
+  if (e == cudaSuccess) done.insert({kernel, device});
+  return e;
+}
+
 int check_ctx(rtg_ctx* ctx, int64_t h, int64_t w) {
   if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null rtg_ctx");
   if (h <= 0 || w <= 0) return fail(RTG_ERR_DIMENSION, "tile extent must be positive");
@@ -51,7 +69,7 @@ void prof_mark(rtg_ctx* ctx, int stage) {
 
 namespace {
 
-int check_params(const rtg_params* p) {
+int check_params_impl(const rtg_params* p) {
   if (!p) return fail(RTG_ERR_INVALID_ARG, "null rtg_params");
   if (p->recon_conn != 4 && p->recon_conn != 8)
     return fail(RTG_ERR_INVALID_ARG, "recon_conn must be 4 or 8");
@@ -258,23 +276,36 @@ __global__ void k_rows_to_host(const float4* __restrict__ src, const int32_t* __
     dst[i] = src[i];
 }
 
-int rows_to_host(rtg_ctx* ctx, float* dst, int32_t cap) {
+}  // namespace
+
+int rows_to_host(rtg_ctx* ctx, cudaStream_t stream, const float* src, const int32_t* d_n,
+                 float* dst, int32_t cap) {
   cudaPointerAttributes a{};
   const cudaError_t e = cudaPointerGetAttributes(&a, dst);
   if (e == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer &&
       (reinterpret_cast<uintptr_t>(a.devicePointer) & 15) == 0) {
-    k_rows_to_host<<<64, 256, 0, ctx->stream>>>(reinterpret_cast<const float4*>(ctx->features),
-                                                ctx->misc, cap,
-                                                static_cast<float4*>(a.devicePointer));
+    k_rows_to_host<<<64, 256, 0, stream>>>(reinterpret_cast<const float4*>(src), d_n, cap,
+                                           static_cast<float4*>(a.devicePointer));
     RTG_LAUNCH("k_rows_to_host");
     return RTG_OK;
   }
   cudaGetLastError();  // clear a failed attribute query on pageable memory
-  RTG_CUDA(cudaMemcpyAsync(dst, ctx->features, sizeof(float) * RTG_NUM_FEATURES * (size_t)cap,
-                           cudaMemcpyDeviceToHost, ctx->stream));
+  RTG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * RTG_NUM_FEATURES * (size_t)cap,
+                           cudaMemcpyDeviceToHost, stream));
   return RTG_OK;
 }
 
+int run_stage(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
+              const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
+              float* d_features, int32_t* d_n) {
+  if (ctx->use_graphs && !ctx->prof)
+    return pipeline_graph(ctx, d_rgb, h, w, pitch, p, d_mask, d_labels, d_hema, d_features, d_n);
+  return pipeline(ctx, d_rgb, h, w, pitch, p, d_mask, d_labels, d_hema, d_features, d_n, true);
+}
+
+int check_params(const rtg_params* p) { return check_params_impl(p); }
+
+namespace {
 }  // namespace
 }  // namespace rtg
 
@@ -410,6 +441,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   if (!c) return RTG_OK;
   cudaSetDevice(c->device);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  release_slots(c);
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
                   c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
@@ -637,7 +669,7 @@ int rtg_process_tiles(rtg_ctx* ctx, int32_t count, const uint8_t* const* rgb, in
     RTG_CUDA(cudaMemcpyAsync(ctx->h_counts + i, ctx->misc, sizeof(int32_t),
                              cudaMemcpyDeviceToHost, ctx->stream));
     if (features_out && features_out[i] && rows > 0)
-      RTG_TRY(rows_to_host(ctx, features_out[i], rows));
+      RTG_TRY(rows_to_host(ctx, ctx->stream, ctx->features, ctx->misc, features_out[i], rows));
   }
   RTG_TRY(rtg_ctx_sync(ctx));
   int over = -1;

@@ -43,7 +43,9 @@ SYMBOLS = [
     "rtg_synth_tile_host", "rtg_synth_tile_dev", "rtg_ctx_profile",
     "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
     "rtg_texture_features", "rtg_texture_features_dev", "rtg_canny_dev",
+    "rtg_process_tile_async", "rtg_ticket_wait", "rtg_ticket_query",
 ]
+ASYNC_SLOTS = 3  # RTG_ASYNC_SLOTS
 OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
 OPT_USE_GRAPHS = 1       # 1 replay cached CUDA graphs in process_tile_dev (default)
 OPT_RECON_IMPL = 2       # 0 threshold decomposition (default), 1 grayscale IWPP
@@ -171,6 +173,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_ctx_profile_read": [vp, vp, vp],
         "rtg_ctx_launches": [vp, vp],
         "rtg_ctx_set_option": [vp, ctypes.c_int, i64],
+        "rtg_process_tile_async": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, i32, vp],
+        "rtg_ticket_wait": [vp, u64, vp],
+        "rtg_ticket_query": [vp, u64, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -209,6 +214,33 @@ def _ptr(a) -> int:
     return int(a.data_ptr())  # torch tensor
 
 
+def _rgb_tile(rgb, shape=None) -> np.ndarray:
+    """Validates one host RGB tile: (H, W, 3) u8 (C-contiguous copy if needed),
+    and the batch's common shape when `shape` is given.  The C side reads
+    3*H*W bytes per tile, so a wrong shape or dtype would be an out-of-bounds
+    read through ctypes."""
+    if not isinstance(rgb, np.ndarray) or rgb.ndim != 3 or rgb.shape[2] != 3:
+        raise ValueError(f"RGB tile must be an (H, W, 3) array, got {getattr(rgb, 'shape', rgb)!r}")
+    if rgb.dtype != np.uint8:
+        raise ValueError(f"RGB tile must be uint8, got {rgb.dtype}")
+    if shape is not None and rgb.shape != shape:
+        raise ValueError(f"tiles of one batch must share a shape: {rgb.shape} != {shape}")
+    if rgb.shape[0] <= 0 or rgb.shape[1] <= 0:
+        raise ValueError(f"empty RGB tile {rgb.shape}")
+    return np.ascontiguousarray(rgb)
+
+
+def _feature_buffer(f, max_rows: int) -> np.ndarray:
+    """A caller-supplied feature table the C side writes up to max_rows rows into."""
+    if (not isinstance(f, np.ndarray) or f.dtype != np.float32 or f.ndim != 2
+            or not f.flags["C_CONTIGUOUS"] or f.shape[1] != NUM_FEATURES
+            or f.shape[0] < max_rows):
+        raise ValueError(f"feature buffer must be C-contiguous float32 (>= {max_rows}, "
+                         f"{NUM_FEATURES}), got {getattr(f, 'dtype', None)} "
+                         f"{getattr(f, 'shape', None)}")
+    return f
+
+
 def synth_tile_host(tile_row: int = 0, tile_col: int = 0, h: int = 4096, w: int = 4096,
                     seed: int = DEFAULT_SEED) -> np.ndarray:
     """Synthetic H&E RGB tile (H, W, 3) u8, byte-identical to synth_tile_dev."""
@@ -227,6 +259,7 @@ class Context:
         check(self.lib.rtg_ctx_create(device, max_h, max_w, max_objects,
                                       ctypes.byref(self.handle)))
         self.device, self.max_h, self.max_w, self.max_objects = device, max_h, max_w, max_objects
+        self._inflight = {}
 
     def close(self) -> None:
         if self.handle:
@@ -286,12 +319,14 @@ class Context:
         """Segmentation + features of one (H, W, 3) u8 tile.
         Returns (mask u8, labels i32, hema u8, features f32 [n, 20], n)."""
         params = params or default_params()
+        rgb = _rgb_tile(rgb)
         h, w, _ = rgb.shape
-        rgb = np.ascontiguousarray(rgb)
         mask = np.empty((h, w), np.uint8)
         labels = np.empty((h, w), np.int32)
         hema = np.empty((h, w), np.uint8)
         max_rows = self.max_objects if max_rows is None else max_rows
+        if max_rows < 0:
+            raise ValueError("max_rows < 0")
         feats = np.empty((max_rows, NUM_FEATURES), np.float32)
         n = ctypes.c_int32(0)
         check(self.lib.rtg_process_tile(self.handle, _ptr(rgb), h, w, 3 * w, ctypes.byref(params),
@@ -311,11 +346,18 @@ class Context:
             check(self.lib.rtg_process_tiles(self.handle, 0, None, 1, 1, 3, ctypes.byref(params),
                                              None, 0, None))
             return [], []
-        h, w, _ = rgbs[0].shape
-        rgbs = [np.ascontiguousarray(r) for r in rgbs]
+        first = _rgb_tile(rgbs[0])
+        h, w, _ = first.shape
+        rgbs = [first] + [_rgb_tile(r, first.shape) for r in rgbs[1:]]
         max_rows = self.max_objects if max_rows is None else max_rows
+        if max_rows < 0:
+            raise ValueError("max_rows < 0")
         if feats is None:
             feats = [np.empty((max_rows, NUM_FEATURES), np.float32) for _ in range(k)]
+        elif len(feats) != k:
+            raise ValueError(f"{len(feats)} feature buffers for {k} tiles")
+        else:
+            feats = [_feature_buffer(f, max_rows) for f in feats]
         rp = (ctypes.c_void_p * k)(*[r.ctypes.data for r in rgbs])
         fp = (ctypes.c_void_p * k)(*[f.ctypes.data for f in feats])
         ns = np.zeros(k, np.int32)
@@ -323,10 +365,56 @@ class Context:
                                          fp, max_rows, _ptr(ns)))
         return [f[:n].copy() for f, n in zip(feats, ns)], [int(n) for n in ns]
 
+    # -- host-buffer entry point, asynchronous (3-phase pipeline) -------------
+    def process_tile_async(self, rgb: np.ndarray, params: Optional[Params] = None, mask=None,
+                           labels=None, hema=None, feats=None, max_rows: Optional[int] = None,
+                           pitch: Optional[int] = None) -> int:
+        """Enqueues one tile (upload, stage, download of the given outputs) and
+        returns a ticket for wait().  Outputs are caller-owned arrays that must
+        stay alive until the ticket is waited: mask (H, W) u8, labels (H, W)
+        i32, hema (H, W) u8, feats (>= max_rows, 20) f32.  `rgb` may be a
+        row-strided (H, W, 3) view of a larger slide (pitch = its row bytes)."""
+        params = params or default_params()
+        if pitch is None:
+            rgb = _rgb_tile(rgb)
+            pitch = 3 * rgb.shape[1]
+        elif not (isinstance(rgb, np.ndarray) and rgb.dtype == np.uint8 and rgb.ndim == 3
+                  and rgb.shape[2] == 3 and rgb.strides[1:] == (3, 1) and rgb.strides[0] == pitch):
+            raise ValueError("a pitched RGB view must be (H, W, 3) u8 with row stride == pitch")
+        h, w, _ = rgb.shape
+        for a, dt, shp in ((mask, np.uint8, (h, w)), (labels, np.int32, (h, w)),
+                           (hema, np.uint8, (h, w))):
+            if a is not None and (a.dtype != dt or a.shape != shp or not a.flags["C_CONTIGUOUS"]):
+                raise ValueError(f"output must be C-contiguous {np.dtype(dt).name} {shp}")
+        max_rows = self.max_objects if max_rows is None else max_rows
+        if feats is not None:
+            feats = _feature_buffer(feats, max_rows)
+        t = ctypes.c_uint64(0)
+        check(self.lib.rtg_process_tile_async(
+            self.handle, rgb.ctypes.data, h, w, pitch, ctypes.byref(params), _ptr(mask),
+            _ptr(labels), _ptr(hema), _ptr(feats), max_rows, ctypes.byref(t)))
+        # the buffers the device reads / writes stay referenced until wait()
+        self._inflight[t.value] = (rgb, mask, labels, hema, feats)
+        return t.value
+
+    def wait(self, ticket: int) -> int:
+        """Waits for a ticket; returns the tile's object count."""
+        n = ctypes.c_int32(0)
+        try:
+            check(self.lib.rtg_ticket_wait(self.handle, ticket, ctypes.byref(n)))
+        finally:
+            self._inflight.pop(ticket, None)
+        return n.value
+
+    def ready(self, ticket: int) -> bool:
+        d = ctypes.c_int(0)
+        check(self.lib.rtg_ticket_query(self.handle, ticket, ctypes.byref(d)))
+        return bool(d.value)
+
     def segment_tile(self, rgb: np.ndarray, params: Optional[Params] = None):
         params = params or default_params()
+        rgb = _rgb_tile(rgb)
         h, w, _ = rgb.shape
-        rgb = np.ascontiguousarray(rgb)
         mask = np.empty((h, w), np.uint8)
         labels = np.empty((h, w), np.int32)
         n = ctypes.c_int32(0)
@@ -336,6 +424,8 @@ class Context:
 
     def features(self, labels: np.ndarray, intensity: np.ndarray, n: int) -> np.ndarray:
         h, w = labels.shape
+        if intensity.shape != (h, w):
+            raise ValueError(f"intensity {intensity.shape} does not match labels {labels.shape}")
         out = np.empty((max(n, 1), NUM_FEATURES), np.float32)
         check(self.lib.rtg_features(self.handle, _ptr(np.ascontiguousarray(labels, np.int32)),
                                     _ptr(np.ascontiguousarray(intensity, np.uint8)), h, w, n,
@@ -345,6 +435,8 @@ class Context:
     def texture(self, labels: np.ndarray, intensity: np.ndarray, n: int) -> np.ndarray:
         """f4 texture table (n x NUM_TEXTURE) for canonical labels 1..n."""
         h, w = labels.shape
+        if intensity.shape != (h, w):
+            raise ValueError(f"intensity {intensity.shape} does not match labels {labels.shape}")
         out = np.empty((max(n, 1), NUM_TEXTURE), np.float32)
         check(self.lib.rtg_texture_features(
             self.handle, _ptr(np.ascontiguousarray(labels, np.int32)),
