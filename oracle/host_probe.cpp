@@ -24,6 +24,7 @@
 #include <vector>
 
 #ifdef RT_REF
+#include "rt/partition.hpp"
 #include "rt/bounding_box.hpp"
 #include "rt/data_region.hpp"
 #include "rt/pack.hpp"
@@ -33,6 +34,7 @@
 #include "rt/disk_store.hpp"
 #include "rt/wrm.hpp"
 #else
+#include "rt/partition.hpp"
 #include "rt/pack.hpp"
 #include "rt/session.hpp"
 #include "rt/region.hpp"
@@ -80,6 +82,8 @@ std::string outcome(F&& f) {
     return "DecodeError";
   } catch (const IoError&) {
     return "IoError";
+  } catch (const PartitionError&) {
+    return "PartitionError";
   } catch (const Error&) {
     return "Error";
   }
@@ -393,6 +397,139 @@ void sessions(const char* dir) {
               outcome([&] { read_session_file(std::string(dir) + "/nope.rts"); }).c_str());
 }
 
+// Edge cases of the box / region / dataflow API the hot path relies on.
+void edges() {
+  const BoundingBox a({0, 0}, {3, 3}), e;
+  std::printf("edge contains_empty %d\n", int(a.contains(e)));
+  std::printf("edge empty_contains %s\n", outcome([&] { (void)e.contains(a); }).c_str());
+  std::printf("edge empty_contains_empty %d\n", int(e.contains(e)));
+  const std::int64_t lo[1] = {0}, hi[1] = {0};
+  std::printf("edge rank0 %s\n", outcome([&] { std::printf("edge rank0_box %s vol=%lld\n",
+      BoundingBox(0, lo, hi).to_string().c_str(), (long long)BoundingBox(0, lo, hi).volume()); }).c_str());
+  std::printf("edge rank5 %s\n", outcome([&] { BoundingBox(5, lo, hi); }).c_str());
+  std::printf("edge inverted %s\n", outcome([&] { BoundingBox({3}, {1}); }).c_str());
+  // DataRegion equality looks at every attribute
+  const DataRegionId id{"e", "r", "raw", 1, 2};
+  auto make = [&] {
+    DataRegion r(id, RegionKind::kDense2D, ElementKind::kU8, a);
+    r.put_chunk(a, std::vector<std::uint8_t>(16, 3));
+    return r;
+  };
+  DataRegion base = make();
+  std::printf("edge eq_same %d\n", int(base == make()));
+  { DataRegion r = make(); r.set_roi(BoundingBox({1, 1}, {2, 2})); std::printf("edge eq_roi %d\n", int(base == r)); }
+  { DataRegion r = make(); r.set_io_mode(IoMode::kOutput); std::printf("edge eq_io %d\n", int(base == r)); }
+  { DataRegion r = make(); r.set_storage_binding("x"); std::printf("edge eq_binding %d\n", int(base == r)); }
+  { DataRegion r = make(); r.set_lazy(true); std::printf("edge eq_lazy %d\n", int(base == r)); }
+  { DataRegion r = make(); r.drop_payload(); std::printf("edge eq_dropped %d\n", int(base == r)); }
+  // partitions
+  for (const auto& [bx, t] : std::vector<std::pair<BoundingBox, std::vector<std::int64_t>>>{
+           {BoundingBox({0, 0}, {99999, 99999}), {4096, 4096}},
+           {BoundingBox({5, -3, 0}, {17, 9, 2}), {4, 5, 3}},
+           {BoundingBox({0}, {9}), {3}},
+           {BoundingBox({0, 0}, {9, 9}), {10, 1}}}) {
+    std::string o = outcome([&, bx = bx, t = t] {
+      const std::vector<BoundingBox> v = partition_regular(bx, std::span<const std::int64_t>(t));
+      std::uint64_t h = 1469598103934665603ull;
+      for (const auto& b : v)
+        for (char c : b.to_string()) h = (h ^ std::uint8_t(c)) * 1099511628211ull;
+      std::printf("partition %s n=%zu first=%s last=%s h=%016llx\n", bx.to_string().c_str(), v.size(),
+                  v.front().to_string().c_str(), v.back().to_string().c_str(), (unsigned long long)h);
+    });
+    if (o != "ok") std::printf("partition %s %s\n", bx.to_string().c_str(), o.c_str());
+  }
+  std::printf("partition empty n=%zu\n", partition_regular(BoundingBox(), {4}).size());
+  std::printf("partition bad_rank %s\n", outcome([] { partition_regular(BoundingBox({0, 0}, {3, 3}), {2}); }).c_str());
+  std::printf("partition zero %s\n", outcome([] { partition_regular(BoundingBox({0, 0}, {3, 3}), {2, 0}); }).c_str());
+  std::printf("partition custom_ok %s\n", outcome([] {
+    partition_custom(BoundingBox({0, 0}, {9, 9}), {BoundingBox({0, 0}, {4, 9}), BoundingBox({3, 0}, {9, 9})}); }).c_str());
+  std::printf("partition custom_escape %s\n", outcome([] {
+    partition_custom(BoundingBox({0, 0}, {9, 9}), {BoundingBox({0, 0}, {10, 9})}); }).c_str());
+  std::printf("partition custom_rank %s\n", outcome([] {
+    partition_custom(BoundingBox({0, 0}, {9, 9}), {BoundingBox({0}, {3})}); }).c_str());
+}
+
+// Lazy inputs (touch_region), 3-D shells, and a growing stage graph.
+void lazy_and_growth() {
+  StorageRegistry reg;
+  auto st = make_store(reg);
+  const DataRegionId src{"img", "rgb", "raw", 0, 0}, out{"img", "mask", "label", 0, 0};
+  DataRegion in(src, RegionKind::kDense2D, ElementKind::kU8, BoundingBox({0, 0}, {31, 31}));
+  std::vector<std::uint8_t> px(32 * 32);
+  for (std::size_t i = 0; i < px.size(); ++i) px[i] = std::uint8_t(i * 5 + 3);
+  in.put_chunk(in.bbox(), px);
+  st->stage_region(in, 0).wait();
+  StageInstance s;
+  s.stage_id = 4;
+  s.stage_kind = "lazy";
+  s.region_descriptors = {
+      RegionDescriptor{src, BoundingBox({2, 3}, {20, 30}), IoMode::kInput, "store", true},
+      RegionDescriptor{out, BoundingBox({2, 3}, {20, 30}), IoMode::kOutput, "store", true}};
+  RegionTemplate local = worker_prepare(s, reg);
+  const DataRegion* shell = local.get_data_region(src);
+  std::printf("lazy shell mat=%d lazy=%d kind=%d out_lazy=%d\n", int(shell->materialized()),
+              int(shell->lazy()), int(shell->kind()), int(local.get_data_region(out)->lazy()));
+  DataRegion& t1 = touch_region(local, src, reg);
+  std::printf("lazy touch mat=%d lazy=%d kind=%d io=%d bind=%s box=%s h=%016llx\n",
+              int(t1.materialized()), int(t1.lazy()), int(t1.kind()), int(t1.io_mode()),
+              t1.storage_binding().c_str(), t1.bbox().to_string().c_str(),
+              (unsigned long long)fnv(t1.chunks().begin()->second.payload));
+  DataRegion& t2 = touch_region(local, src, reg);
+  std::printf("lazy retouch same=%d\n", int(&t1 == &t2));
+  std::printf("lazy touch_output %s\n", outcome([&] { touch_region(local, out, reg); }).c_str());
+  std::printf("lazy touch_absent %s\n",
+              outcome([&] { touch_region(local, DataRegionId{"no", "pe", "x", 0, 0}, reg); }).c_str());
+  // a 3-D query's output shell
+  StageInstance s3;
+  s3.stage_id = 5;
+  s3.stage_kind = "three";
+  s3.region_descriptors = {
+      RegionDescriptor{out, BoundingBox({0, 0, 0}, {3, 3, 2}), IoMode::kOutput, "store", false}};
+  RegionTemplate l3 = worker_prepare(s3, reg);
+  const DataRegion* o3 = l3.get_data_region(out);
+  std::printf("shell3 kind=%d elem=%d box=%s\n", int(o3->kind()), int(o3->element_kind()),
+              o3->bbox().to_string().c_str());
+  // dynamic growth, stuck detection, completion log
+  ManagerState m;
+  auto stage = [](std::uint64_t id, std::set<std::uint64_t> deps) {
+    StageInstance x;
+    x.stage_id = id;
+    x.deps = std::move(deps);
+    return x;
+  };
+  m.add_stage(stage(1, {}));
+  m.add_stage(stage(3, {2}));  // depends on a stage not added yet
+  std::printf("grow stuck0=%d eligible=%zu\n", int(m.stuck()), m.eligible_ids().size());
+  const auto d1 = m.dispatch(7);
+  std::printf("grow dispatch=%llu worker=%d stuck=%d\n", (unsigned long long)*d1,
+              *m.assigned_worker(1), int(m.stuck()));
+  std::vector<StageInstance> kids;
+  kids.push_back(stage(2, {1}));
+  kids.push_back(stage(4, {9}));
+  const auto now = m.stage_complete(1, std::move(kids));
+  std::string ns;
+  for (auto x : now) ns += std::to_string(x) + ",";
+  std::printf("grow spawned -> %s size=%zu done=%zu\n", ns.c_str(), m.size(), m.done_count());
+  while (auto d = m.dispatch(1)) {
+    const auto nn = m.stage_complete(*d);
+    std::printf("grow done %llu -> %zu\n", (unsigned long long)*d, nn.size());
+  }
+  std::string log;
+  for (auto x : m.completion_log()) log += std::to_string(x) + ",";
+  std::printf("grow log=%s all=%d stuck=%d unassigned=%d\n", log.c_str(), int(m.all_done()),
+              int(m.stuck()), int(!m.assigned_worker(4).has_value()));
+  std::printf("grow unknown %s\n", outcome([&] { m.assigned_worker(99); }).c_str());
+  std::printf("grow undispatched %s\n", outcome([&] { m.stage_complete(4); }).c_str());
+  std::printf("grow dup_spawn %s\n", outcome([&] {
+    ManagerState q;
+    q.add_stage(stage(1, {}));
+    q.dispatch(0);
+    std::vector<StageInstance> k;
+    k.push_back(stage(1, {}));
+    q.stage_complete(1, std::move(k));
+  }).c_str());
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -403,5 +540,7 @@ int main(int argc, char** argv) {
   scheduler();
   packs();
   sessions(argc > 1 ? argv[1] : "/tmp");
+  edges();
+  lazy_and_growth();
   return 0;
 }

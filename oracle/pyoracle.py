@@ -106,6 +106,10 @@ class Params(ctypes.Structure):
         ("reserved", ctypes.c_int32 * 7),
     ]
 
+    def as_dict(self) -> dict:
+        return {name: (list(getattr(self, name)) if name == "h_coef" else getattr(self, name))
+                for name, _ in self._fields_ if name != "reserved"}
+
 
 def default_params():
     p = Params()

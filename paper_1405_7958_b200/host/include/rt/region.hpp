@@ -123,10 +123,21 @@ template <> struct element_of<double> { static constexpr ElementKind value = Ele
 using PayloadAllocFn = void* (*)(std::size_t bytes);
 using PayloadFreeFn = void (*)(void* p);
 // alloc == nullptr restores plain heap payloads (and releases the pool).
+// `live_bytes` caps the hook's blocks in use (pinned pages are a scarce
+// host resource: a whole slide of staged outputs must not page-lock the
+// host); beyond it, and whenever the hook fails, payloads fall back to
+// plain heap blocks.
 void set_payload_allocator(PayloadAllocFn alloc, PayloadFreeFn free, std::size_t min_bytes,
-                           std::size_t pool_bytes);
+                           std::size_t pool_bytes,
+                           std::size_t live_bytes = std::size_t(-1));
 // True when `p` (a payload's data()) lives in a block from the hook.
 bool payload_is_hooked(const void* p);
+struct PayloadStats {
+  std::size_t live_bytes = 0;    // hook blocks in use
+  std::size_t pooled_bytes = 0;  // hook blocks parked for reuse
+  std::size_t pool_hits = 0, hook_allocs = 0, fallbacks = 0;
+};
+PayloadStats payload_stats();
 
 namespace detail {
 void* payload_allocate(std::size_t bytes);

@@ -9,6 +9,8 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
+#include <vector>
 
 #include "rt/runtime.hpp"
 #include "rtg.h"
@@ -33,27 +35,38 @@ class GpuDevice {
   rtg_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   std::int32_t max_objects() const { return max_objects_; }
-  // Pinned max_objects x RTG_NUM_FEATURES rows: rtg_process_tile writes the
-  // n live rows straight into it (zero-copy stores, no cap-row copy).
-  float* feature_staging() const { return features_; }
+  // A pinned max_objects x RTG_NUM_FEATURES row buffer for one tile in
+  // flight: the stage writes the n live rows straight into it (zero-copy
+  // stores); it returns to the device's pool when the last holder drops it.
+  std::shared_ptr<float> acquire_staging();
+  // Pinned row buffers allocated so far (one per tile ever in flight at once).
+  std::size_t staging_buffers() const;
 
  private:
   rtg_ctx* ctx_ = nullptr;
-  float* features_ = nullptr;
   int device_ = 0;
   std::int32_t max_objects_ = 0;
+  mutable std::mutex mu_;
+  std::vector<float*> free_, all_;
 };
 
 // Routes Chunk payloads of at least `min_bytes` into pinned host pages
 // (rtg_host_alloc), recycling up to `pool_bytes` of them by size, so the GPU
 // variant's H2D of the RGB tile and D2H of Mask / Labels are direct DMAs
-// from / into the chunks.  Call once per process before the
-// tiles are staged; use_pageable_payloads() undoes it.
+// from / into the chunks.  At most `live_bytes` are pinned at
+// once (a 625-tile slide's staged outputs alone are 50 GB); further payloads
+// are plain heap blocks (correct, with a staged copy).  Call once per process
+// before the tiles are staged; use_pageable_payloads() undoes it.
 void use_pinned_payloads(std::size_t min_bytes = std::size_t(1) << 20,
-                         std::size_t pool_bytes = std::size_t(4) << 30);
+                         std::size_t pool_bytes = std::size_t(4) << 30,
+                         std::size_t live_bytes = std::size_t(16) << 30);
 void use_pageable_payloads();
 
 struct SegmentationRegions {
+  // The RGB input is lazy by default: the GPU variant DMAs it straight out of
+  // the store (view_region, a pitched H2D from the staged slide) and falls
+  // back to touch_region when the store cannot provide a view.
+  bool lazy_rgb = true;
   DataRegionId rgb{"img", "RGB", "raw", 0, 0};
   DataRegionId mask{"img", "Mask", "label", 0, 0};
   DataRegionId labels{"img", "Labels", "label", 0, 0};
@@ -64,10 +77,13 @@ struct SegmentationRegions {
 // Task name of the stage's single fine-grain task in a VariantRegistry.
 inline constexpr const char* kSegmentFeaturesTask = "segment_features";
 
-// Registers the B200 variant of "segment_features".  The body reads the
-// tile from the worker's local template, runs rtg_process_tile on the
-// worker's GpuDevice and installs Mask (Dense2D u8), Labels (Dense2D i32) and
-// Features (Dense2D f32, n x RTG_NUM_FEATURES) into the local template.
+// Registers the B200 variant of "segment_features".  The body finds the
+// tile (a zero-copy store view for a lazy input, else the local template's
+// payload), installs Mask (Dense2D u8) and Labels (Dense2D i32) into the
+// local template, enqueues upload / stage / download with
+// rtg_process_tile_async on the worker's GpuDevice and defers the rest
+// (ticket wait, Features region, Dense2D f32 n x RTG_NUM_FEATURES) to the
+// executor, which meanwhile prepares and starts the next stage.
 void register_gpu_segmentation(VariantRegistry& reg, const SegmentationRegions& ids,
                                const rtg_params& params);
 

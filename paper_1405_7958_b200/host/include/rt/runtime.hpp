@@ -13,6 +13,7 @@
 // local RegionTemplate and the device the WRM picked).
 #pragma once
 
+#include <deque>
 #include <functional>
 #include <map>
 #include <memory>
@@ -27,6 +28,18 @@
 namespace rt {
 
 // ---- storage ------------------------------------------------------------------
+// A read-only window onto staged bytes (no copy): `data` is the query box's
+// first cell and consecutive steps of axis 0 are `row_pitch` bytes apart;
+// within one step the query's remaining axes are contiguous.  `keep` holds
+// the stored piece alive while the view is in use (e.g. by a DMA).
+struct PayloadView {
+  const std::uint8_t* data = nullptr;
+  std::int64_t row_pitch = 0;
+  RegionKind kind = RegionKind::kDense2D;
+  ElementKind elem = ElementKind::kU8;
+  std::shared_ptr<const void> keep;
+};
+
 // Completion of a staging operation (always complete for the in-memory store).
 class Completion {
  public:
@@ -51,6 +64,13 @@ class StorageBackend {
   // Assembles the query box from staged chunks; NotFoundError when any cell
   // was never written.
   virtual DataRegion read_region(const DataRegionId& id, const BoundingBox& query) = 0;
+  // Zero-copy alternative to read_region when one stored piece holds the
+  // whole query and the query is row-contiguous in it (a tile
+  // of a staged slide DMAs straight from the slide).  nullopt otherwise.
+  virtual std::optional<PayloadView> view_region(const DataRegionId& /*id*/,
+                                                 const BoundingBox& /*query*/) {
+    return std::nullopt;
+  }
 };
 
 // Process-local store keyed by region tuple; thread-safe.
@@ -61,6 +81,7 @@ class MemoryStore : public StorageBackend {
   Completion stage_region(const DataRegion& region, int origin_node) override;
   Completion stage_region_consume(DataRegion& region, int origin_node) override;
   DataRegion read_region(const DataRegionId& id, const BoundingBox& query) override;
+  std::optional<PayloadView> view_region(const DataRegionId& id, const BoundingBox& query) override;
 
  private:
   struct Piece {
@@ -71,7 +92,8 @@ class MemoryStore : public StorageBackend {
   };
   std::string name_;
   std::mutex mu_;
-  std::map<DataRegionId, std::vector<Piece>> pieces_;
+  // staging order per region; shared so a view outlives later stagings
+  std::map<DataRegionId, std::vector<std::shared_ptr<const Piece>>> pieces_;
 };
 
 class StorageRegistry {
@@ -149,14 +171,32 @@ class VariantRegistry {
 
 class GpuDevice;  // rt/rtg_stage.hpp
 
+struct StageInstance;
+
 // What a running TaskNode::body can see (set by the executor per task).
 struct WorkerContext {
   RegionTemplate* local = nullptr;
   DeviceKind device = DeviceKind::kCpu;
   GpuDevice* gpu = nullptr;
   int worker = 0;
+  StorageRegistry* storage = nullptr;  // for touch_region / view_region in bodies
+  // Set by a pipelining executor while a body runs: completions the body
+  // deferred (defer_completion) and stages it spawned (spawn_stage).
+  std::vector<std::function<void()>>* deferred = nullptr;
+  std::vector<StageInstance>* spawned = nullptr;
 };
 WorkerContext& worker_context();
+
+// A body that enqueued asynchronous device work hands the rest of its work
+// (wait for the device, install outputs) to the executor: the task counts
+// as complete only after `finish` ran, and the executor may prepare and
+// start other stages meanwhile (the paper's 3-phase pipeline, PAPER.md:
+// 687-700; reference wrm.cpp:385-415).  Without a pipelining executor
+// `finish` runs at once.
+void defer_completion(std::function<void()> finish);
+// Adds a stage to the manager when the running stage completes (reference
+// ManagerState::stage_complete(id, spawned), dataflow.cpp:84-111).
+void spawn_stage(StageInstance stage);
 
 // ---- dataflow ---------------------------------------------------------------------------
 struct RegionDescriptor {
@@ -175,30 +215,55 @@ struct StageInstance {
   std::function<std::vector<TaskNode>()> body;
 };
 
+// Manager-side stage graph (reference dataflow.hpp:51-99): demand-driven
+// dispatch of the first eligible stage in insertion order; completing a
+// stage may spawn new ones (the graph grows while it runs).
 class ManagerState {
  public:
+  // ProtocolError on a duplicate id.  Dependencies may name stages that are
+  // added later; they stay unsatisfied until that stage completes.
   void add_stage(StageInstance stage);
   std::optional<std::uint64_t> dispatch(int worker);
-  std::vector<std::uint64_t> stage_complete(std::uint64_t stage_id);
+  // Marks an assigned stage done, adds the stages it spawned and returns the
+  // ids that became eligible because of it (insertion order).  ProtocolError
+  // for unknown, undispatched or already completed stages.
+  std::vector<std::uint64_t> stage_complete(std::uint64_t stage_id,
+                                            std::vector<StageInstance> spawned = {});
   const StageInstance& stage(std::uint64_t id) const;
   std::size_t size() const { return stages_.size(); }
-  bool all_done() const { return done_ == stages_.size(); }
+  std::size_t done_count() const { return log_.size(); }
+  bool all_done() const { return done_count() == size(); }
+  // No stage is running or dispatchable but some are not done: a wedge
+  // (unsatisfiable or cyclic dependencies).
+  bool stuck() const;
+  std::vector<std::uint64_t> eligible_ids() const;
+  std::optional<int> assigned_worker(std::uint64_t id) const;
+  const std::vector<std::uint64_t>& completion_log() const { return log_; }
 
  private:
-  struct E {
+  struct Slot {
     StageInstance stage;
-    bool assigned = false, done = false;
+    std::optional<int> worker;  // set by dispatch
+    bool done = false;
   };
-  bool eligible(const E& e) const;
-  std::map<std::uint64_t, E> stages_;
-  std::vector<std::uint64_t> order_;
-  std::size_t done_ = 0;
+  const Slot& slot(std::uint64_t id) const;
+  bool ready(const Slot& s) const;
+  std::map<std::uint64_t, Slot> stages_;
+  std::vector<std::uint64_t> insertion_;
+  std::vector<std::uint64_t> log_;
 };
 
 // Reads non-lazy inputs into a fresh local template; outputs are created
 // metadata-only (Dense2D/U8 shells, as the reference does) — stage bodies
 // replace them with correctly typed regions.
 RegionTemplate worker_prepare(const StageInstance& stage, StorageRegistry& storage);
+// Read-on-touch for a lazy region of the local template (reference
+// dataflow.cpp:137-154): the first touch replaces the metadata-only shell by
+// the stored payload (keeping io mode, binding and the lazy flag), later
+// touches return the region as is.  NotFoundError when `id` is not in the
+// template or the store has no data for it.
+DataRegion& touch_region(RegionTemplate& local, const DataRegionId& id, StorageRegistry& storage);
+
 // Stages materialised outputs and drops inputs; completions in descriptor order.
 // consume = true (the executor, which discards `local` next) lets the store
 // take the output payloads instead of copying them.
@@ -218,9 +283,16 @@ struct ExecutorConfig {
   SchedulerKind scheduler = SchedulerKind::kPats;
   std::vector<GpuDevice*> gpus;  // one worker each
   int cpu_workers = 0;           // additional CPU-only workers (>= 1 when no GPU)
+  // Stages a GPU worker keeps in flight: while the device runs stage k
+  // (asynchronous bodies, defer_completion) the worker prepares and starts
+  // stage k+1.  1 = one stage at a time; 3 = the C-ABI's slots per context
+  // (RTG_ASYNC_SLOTS: upload, compute and download of three tiles overlap).
+  int gpu_inflight = 3;
 };
 struct ExecutorStats {
   std::size_t stages = 0, cpu_tasks = 0, gpu_tasks = 0;
+  std::size_t deferred_tasks = 0;  // GPU tasks whose completion overlapped other stages
+  std::size_t max_inflight = 0;    // most stages one worker had in flight
 };
 ExecutorStats run_stages(ManagerState& manager, StorageRegistry& storage,
                          const ExecutorConfig& cfg);

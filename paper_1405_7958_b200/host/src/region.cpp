@@ -27,6 +27,9 @@ struct PayloadHooks {
   std::size_t min_bytes = 0;
   std::size_t pool_cap = 0;
   std::size_t pooled = 0;
+  std::size_t live_cap = std::size_t(-1);
+  std::size_t live = 0;
+  std::size_t hits = 0, allocs = 0, fallbacks = 0;
   std::unordered_map<std::size_t, std::vector<BlockHeader*>> pool;  // hook blocks by size
 
   void release_pool_locked() {
@@ -50,7 +53,7 @@ BlockHeader* header_of(const void* p) {
 }  // namespace
 
 void set_payload_allocator(PayloadAllocFn alloc, PayloadFreeFn free, std::size_t min_bytes,
-                           std::size_t pool_bytes) {
+                           std::size_t pool_bytes, std::size_t live_bytes) {
   if ((alloc == nullptr) != (free == nullptr))
     throw ProtocolError("payload allocator needs both alloc and free");
   PayloadHooks& h = hooks();
@@ -60,6 +63,13 @@ void set_payload_allocator(PayloadAllocFn alloc, PayloadFreeFn free, std::size_t
   h.free = free;
   h.min_bytes = min_bytes;
   h.pool_cap = alloc ? pool_bytes : 0;
+  h.live_cap = live_bytes;
+}
+
+PayloadStats payload_stats() {
+  PayloadHooks& h = hooks();
+  std::lock_guard<std::mutex> lk(h.mu);
+  return PayloadStats{h.live, h.pooled, h.hits, h.allocs, h.fallbacks};
 }
 
 bool payload_is_hooked(const void* p) { return p && header_of(p)->free != nullptr; }
@@ -78,13 +88,18 @@ void* payload_allocate(std::size_t bytes) {
         b = it->second.back();
         it->second.pop_back();
         h.pooled -= total;
-      } else {
+        ++h.hits;
+      } else if (h.live + total <= h.live_cap) {
         b = static_cast<BlockHeader*>(h.alloc(total));
-        if (!b) throw std::bad_alloc();
+        if (b) ++h.allocs;
       }
-      b->free = h.free;
-      b->bytes = bytes;
-      return b + 1;
+      if (b) {
+        b->free = h.free;
+        b->bytes = bytes;
+        h.live += total;
+        return b + 1;
+      }
+      ++h.fallbacks;  // over the live budget, or the hook failed: heap block
     }
   }
   auto* b = static_cast<BlockHeader*>(::operator new(total, std::align_val_t(64)));
@@ -104,6 +119,7 @@ void payload_deallocate(void* p) noexcept {
   const std::size_t total = b->bytes + sizeof(BlockHeader);
   {
     std::lock_guard<std::mutex> lk(h.mu);
+    h.live -= std::min(h.live, total);  // every hooked block counts, whichever hook made it
     if (b->free == h.free && h.pooled + total <= h.pool_cap) {
       try {
         h.pool[b->bytes].push_back(b);
@@ -123,7 +139,8 @@ void payload_deallocate(void* p) noexcept {
 BoundingBox::BoundingBox(std::initializer_list<std::int64_t> lo,
                          std::initializer_list<std::int64_t> hi) {
   if (lo.size() != hi.size()) throw DimensionError("lo/hi rank mismatch");
-  if (lo.size() == 0 || lo.size() > kMaxDims) throw DimensionError("box rank must be 1..4");
+  // rank 0 is the empty box (the reference builds it through the same path)
+  if (lo.size() > kMaxDims) throw DimensionError("box rank must be 0..4");
   dims_ = int(lo.size());
   std::copy(lo.begin(), lo.end(), lo_.begin());
   std::copy(hi.begin(), hi.end(), hi_.begin());
@@ -132,7 +149,7 @@ BoundingBox::BoundingBox(std::initializer_list<std::int64_t> lo,
 }
 
 BoundingBox::BoundingBox(int dims, const std::int64_t* lo, const std::int64_t* hi) {
-  if (dims <= 0 || dims > kMaxDims) throw DimensionError("box rank must be 1..4");
+  if (dims < 0 || dims > kMaxDims) throw DimensionError("box rank must be 0..4");
   dims_ = dims;
   for (int a = 0; a < dims; ++a) {
     lo_[a] = lo[a];
@@ -158,7 +175,9 @@ std::int64_t BoundingBox::volume() const {
 }
 
 bool BoundingBox::contains(const BoundingBox& o) const {
-  if (empty() || o.empty()) return false;
+  // every box contains the empty box; a rank mismatch (including an empty
+  // box asked about a non-empty one) is a DimensionError, as in the reference
+  if (o.empty()) return true;
   same_dims(o);
   for (int a = 0; a < dims_; ++a)
     if (o.lo_[a] < lo_[a] || o.hi_[a] > hi_[a]) return false;
@@ -306,7 +325,9 @@ std::uint64_t DataRegion::payload_bytes() const {
 
 bool DataRegion::operator==(const DataRegion& o) const {
   if (!(id_ == o.id_) || kind_ != o.kind_ || element_kind_ != o.element_kind_ ||
-      bbox_ != o.bbox_ || chunks_.size() != o.chunks_.size())
+      bbox_ != o.bbox_ || roi_ != o.roi_ || io_mode_ != o.io_mode_ ||
+      storage_binding_ != o.storage_binding_ || lazy_ != o.lazy_ ||
+      materialized_ != o.materialized_ || chunks_.size() != o.chunks_.size())
     return false;
   auto a = chunks_.begin();
   auto b = o.chunks_.begin();

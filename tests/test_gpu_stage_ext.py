@@ -1,0 +1,280 @@
+"""GPU parity under the bench's own conditions and the round-2 entry points:
+
+* the asynchronous 3-phase host entry point (rtg_process_tile_async) against
+  the synchronous one, pinned and pageable, pitched slide views, out-of-order
+  waits, more tickets than slots, overflow;
+* four contexts on separate streams over the 80 tiles of one rank's WSI shard
+  (the bench's configuration), every mask / label / feature row vs the oracle;
+* BASELINE config C3 at full size: a 4096^2 mask of dense touching nuclei
+  (>= 35 % foreground, >= 50 % of nuclei touching) through area threshold +
+  watershed + canonical labelling, and through the whole stage near the
+  context's max_objects;
+* two devices in one process (per-device shared-memory opt-in).
+Bar: masks / labels bit-exact, features within rtol 1e-5 (atol 1e-6)."""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+FEAT_RTOL = 1e-5
+FEAT_ATOL = 1e-6
+
+
+def _need_gpu(n=1):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} CUDA device(s)")
+
+
+def _pinned(shape, dtype):
+    t = torch.empty(shape, dtype=dtype, pin_memory=True)
+    return t, t.numpy()
+
+
+def _check_tile(got, ref):
+    mask, labels, feats, n = got
+    assert n == ref["n"]
+    assert np.array_equal(mask, ref["mask"])
+    assert np.array_equal(labels, ref["labels"])
+    np.testing.assert_allclose(feats[:n], ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+
+
+# ---------------------------------------------------------------- async entry
+
+def test_async_matches_sync(rtg):
+    _need_gpu()
+    shapes = [(4096, 4096, 0, 0), (4096, 1696, 3, 24), (1696, 1696, 24, 24), (1024, 1333, 5, 5),
+              (97, 203, 9, 9)]
+    keep = []
+    with rtg.Context(0, 4096, 4096, 1 << 16) as ctx:
+        ref = {}
+        for h, w, r, c in shapes:
+            rgb = rtg.synth_tile_host(r, c, h, w)
+            mask, labels, _, feats, n = ctx.process_tile(rgb)
+            ref[(h, w)] = (rgb, mask, labels, feats, n)
+        for pinned in (True, False):
+            tickets = []
+            for h, w, r, c in shapes:
+                rgb = ref[(h, w)][0]
+                if pinned:
+                    tr, rgb_p = _pinned((h, w, 3), torch.uint8)
+                    rgb_p[...] = rgb
+                    tm, mask = _pinned((h, w), torch.uint8)
+                    tl, labels = _pinned((h, w), torch.int32)
+                    tf, feats = _pinned((1 << 16, rtg.NUM_FEATURES), torch.float32)
+                    keep += [tr, tm, tl, tf]
+                else:
+                    rgb_p = rgb
+                    mask = np.empty((h, w), np.uint8)
+                    labels = np.empty((h, w), np.int32)
+                    feats = np.empty((1 << 16, rtg.NUM_FEATURES), np.float32)
+                t = ctx.process_tile_async(rgb_p, mask=mask, labels=labels, feats=feats)
+                tickets.append((t, (h, w), mask, labels, feats))
+            # more tickets than slots were submitted; wait in reverse order
+            for t, key, mask, labels, feats in reversed(tickets):
+                n = ctx.wait(t)
+                _, m_ref, l_ref, f_ref, n_ref = ref[key]
+                assert n == n_ref
+                assert np.array_equal(mask, m_ref) and np.array_equal(labels, l_ref)
+                assert np.array_equal(feats[:n], f_ref)
+            with pytest.raises(rtg.NotFoundError):
+                ctx.wait(tickets[0][0])
+
+
+def test_async_pitched_slide_view(rtg, oracle):
+    """A tile read straight out of a larger slide (row pitch = slide row
+    bytes, cudaMemcpy2DAsync) equals the contiguous tile."""
+    _need_gpu()
+    slide = rtg.synth_tile_host(1, 1, 1536, 2560)
+    with rtg.Context(0, 1024, 1024, 1 << 15) as ctx:
+        view = slide[256:1280, 512:1536]
+        mask = np.empty((1024, 1024), np.uint8)
+        labels = np.empty((1024, 1024), np.int32)
+        feats = np.empty((1 << 15, rtg.NUM_FEATURES), np.float32)
+        t = ctx.process_tile_async(view, mask=mask, labels=labels, feats=feats,
+                                   pitch=slide.strides[0])
+        n = ctx.wait(t)
+    _check_tile((mask, labels, feats, n), oracle.process_tile(np.ascontiguousarray(view)))
+
+
+def test_async_overflow_and_query(rtg):
+    _need_gpu()
+    rgb = rtg.synth_tile_host(0, 0, 1024, 1024)
+    with rtg.Context(0, 1024, 1024, 1 << 15) as ctx:
+        _, _, _, f_ref, n_ref = ctx.process_tile(rgb)
+        assert n_ref > 8
+        feats = np.zeros((8, rtg.NUM_FEATURES), np.float32)
+        t = ctx.process_tile_async(rgb, feats=feats, max_rows=8)
+        with pytest.raises(rtg.OverflowError_):
+            ctx.wait(t)
+        assert np.array_equal(feats, f_ref[:8])
+        t = ctx.process_tile_async(rgb)
+        torch.cuda.synchronize()
+        n = ctx.wait(t)
+        assert n == n_ref
+        assert not hasattr(ctx, "_no_such") and len(ctx._inflight) == 0
+
+
+# ---------------------------------------------------------------- bench mirror
+
+def test_concurrent_contexts_wsi_shard(rtg, oracle):
+    """The bench's configuration: 4 contexts, each on its own stream, share
+    one GPU over the 80 tiles of rank 0's WSI shard (edge tiles included);
+    every tile's mask, labels and features equal the oracle's."""
+    _need_gpu()
+    from paper_1405_7958_b200.wsi import rank_tiles
+    tiles = rank_tiles(0, 80)
+    assert any(h != 4096 or w != 4096 for (_, _, h, w) in tiles)
+    S = 4
+    ctxs = [rtg.Context(0, 4096, 4096, 1 << 15) for _ in range(S)]
+    try:
+        p = rtg.default_params()
+        dev = []
+        for k, (r, c, h, w) in enumerate(tiles):
+            d_rgb = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+            ctxs[0].synth_tile_dev(d_rgb, r, c, h, w)
+            dev.append((d_rgb,
+                        torch.empty((h, w), dtype=torch.uint8, device="cuda"),
+                        torch.empty((h, w), dtype=torch.int32, device="cuda"),
+                        torch.empty((1 << 15, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda"),
+                        torch.zeros(1, dtype=torch.int32, device="cuda")))
+        ctxs[0].sync()
+        torch.cuda.synchronize()  # torch's zero fills vs the ctx streams
+        for k, (r, c, h, w) in enumerate(tiles):
+            d_rgb, d_mask, d_lab, d_feat, d_n = dev[k]
+            ctxs[k % S].process_tile_dev(d_rgb, h, w, p, d_mask, d_lab, None, d_feat, d_n)
+        for cx in ctxs:
+            cx.sync()
+        got = []
+        for k, (r, c, h, w) in enumerate(tiles):
+            _, d_mask, d_lab, d_feat, d_n = dev[k]
+            n = int(d_n.cpu()[0])
+            got.append((d_mask.cpu().numpy(), d_lab.cpu().numpy(), d_feat[:n].cpu().numpy(), n))
+        del dev
+    finally:
+        for cx in ctxs:
+            cx.close()
+
+    def ref(k):
+        r, c, h, w = tiles[k]
+        return oracle.process_tile(oracle.synth_tile_host(r, c, h, w), p)
+
+    with ThreadPoolExecutor(max_workers=16) as ex:
+        for k, rk in enumerate(ex.map(ref, range(len(tiles)))):
+            _check_tile(got[k], rk)
+
+
+# ---------------------------------------------------------------- C3 dense nuclei
+
+def _dense_touching(seed, h, w, fg=0.36):
+    """Clusters of 2-4 overlapping discs (radius 4-8 px); returns the mask
+    and the number of discs."""
+    rng = np.random.default_rng(seed)
+    m = np.zeros((h, w), np.uint8)
+    yy, xx = np.mgrid[-9:10, -9:10]
+    stamps = {r: (yy * yy + xx * xx <= r * r).astype(np.uint8) for r in range(4, 9)}
+    discs = 0
+    while True:
+        for _ in range(2000):
+            cy, cx = rng.integers(9, h - 9), rng.integers(9, w - 9)
+            for _ in range(rng.integers(2, 5)):
+                r = int(rng.integers(4, 9))
+                oy = int(np.clip(cy + rng.integers(-r, r + 1), 9, h - 10))
+                ox = int(np.clip(cx + rng.integers(-r, r + 1), 9, w - 10))
+                m[oy - 9:oy + 10, ox - 9:ox + 10] |= stamps[r]
+                discs += 1
+        if m.mean() >= fg:
+            return m, discs
+
+
+@pytest.fixture(scope="module")
+def c3_mask():
+    return _dense_touching(3, 4096, 4096)
+
+
+def test_c3_dense_touching_4k_operators(rtg, oracle, c3_mask):
+    _need_gpu()
+    from scipy import ndimage as ndi
+    mask, discs = c3_mask
+    comps = ndi.label(mask, np.ones((3, 3)))[1]
+    assert mask.mean() >= 0.35
+    assert comps <= discs // 2  # >= 50 % of nuclei touch another one
+    p = rtg.default_params()
+    h, w = mask.shape
+    with rtg.Context(0, h, w, 1 << 17) as ctx:
+        d_in = torch.from_numpy(mask).cuda()
+        torch.cuda.synchronize()  # the ctx stream does not order with torch's
+        d_area = torch.empty_like(d_in)
+        d_sep = torch.empty_like(d_in)
+        d_basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
+        d_lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+        d_n = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ctx.area_threshold_dev(d_in, h, w, 8, p.min_area, p.max_area, d_area)
+        ctx.watershed_dev(d_area, h, w, p.ws_h, d_sep, d_basin)
+        ctx.bwlabel_dev(d_sep, h, w, 8, d_lab, d_n)
+        ctx.sync()
+        area = d_area.cpu().numpy()
+        sep, basin = d_sep.cpu().numpy(), d_basin.cpu().numpy()
+        lab, n = d_lab.cpu().numpy(), int(d_n.cpu()[0])
+    r_area = oracle.area_threshold(mask, 8, p.min_area, p.max_area)
+    assert np.array_equal(area, r_area)
+    r_sep, r_basin = oracle.watershed(r_area, p.ws_h)
+    assert np.array_equal(sep, r_sep)
+    assert np.array_equal(basin, r_basin)
+    r_lab, r_n = oracle.bwlabel(r_sep, 8)
+    assert n == r_n and n > 15000
+    assert np.array_equal(lab, r_lab)
+
+
+def _render_he(mask, seed):
+    """An H&E-like RGB rendering of a nucleus mask (hematoxylin nuclei on
+    eosin stroma, +-8 noise)."""
+    rng = np.random.default_rng(seed)
+    h, w = mask.shape
+    rgb = np.empty((h, w, 3), np.int16)
+    rgb[...] = (225, 160, 200)
+    rgb[mask > 0] = (80, 60, 150)
+    rgb += rng.integers(-8, 9, size=(h, w, 3), dtype=np.int16)
+    return np.clip(rgb, 0, 255).astype(np.uint8)
+
+
+def test_c3_dense_whole_stage_near_capacity(rtg, oracle, c3_mask):
+    """The dense tile through the whole stage with max_objects just above its
+    object count (bit-exact), and just below it (RTG_ERR_OVERFLOW)."""
+    _need_gpu()
+    mask, _ = c3_mask
+    rgb = _render_he(mask, 5)
+    p = rtg.default_params()
+    ref = oracle.process_tile(rgb, p)
+    n_ref = ref["n"]
+    assert n_ref > 15000
+    with rtg.Context(0, 4096, 4096, n_ref + 8) as ctx:
+        m, lab, _, feats, n = ctx.process_tile(rgb, p)
+    _check_tile((m, lab, feats, n), ref)
+    with rtg.Context(0, 4096, 4096, n_ref - 1) as ctx:
+        with pytest.raises(rtg.OverflowError_):
+            ctx.process_tile(rgb, p)
+
+
+# ---------------------------------------------------------------- two devices
+
+def test_two_devices_one_process(rtg):
+    """Contexts on two devices in one process: every kernel's dynamic
+    shared-memory opt-in is per device (k_colordeconv_vec uses ~100 KB)."""
+    _need_gpu(2)
+    rgb = rtg.synth_tile_host(4, 4, 2048, 2048)
+    outs = []
+    ctxs = [rtg.Context(d, 2048, 2048, 1 << 15) for d in (0, 1, 0)]
+    try:
+        for cx in ctxs:
+            outs.append(cx.process_tile(rgb))
+    finally:
+        for cx in ctxs:
+            cx.close()
+    for o in outs[1:]:
+        assert o[4] == outs[0][4]
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+        assert np.array_equal(o[3], outs[0][3])
