@@ -5,15 +5,26 @@
 Workload (BASELINE.json configs[4], "C5"): the synthetic 100k x 100k
 whole-slide image cut into 4K tiles exactly as the reference's
 partition_regular does (/root/reference/proj/src/partition.cpp:23-54: 25 x 25
-tiles, 576 full + 48 edge 4096x1696 + 1 corner 1696x1696).  Tiles are a bag of
-tasks: one process per GPU, each rank owns a fixed shard of tiles per step
-(weak scaling), no data-path collective; the per-step feature tables are
-gathered to rank 0 with NCCL (the only cross-GPU traffic).
+tiles, 576 full + 48 edge 4096x1696 + 1 corner 1696x1696).  One process per
+GPU; per-GPU work is fixed as N grows (weak scaling); the only cross-GPU
+traffic is the gather of the feature tables to rank 0 over NCCL.
 
-A step = every rank runs the full stage (o1..o9) over its shard, then the
-gather.  `value` is measured with inputs already resident in HBM; `e2e` goes
-through the C-ABI host-buffer entry point rtg_process_tile with pinned host
-tiles (H2D of RGB and D2H of the feature table inside the timed region).
+A step = every rank runs the full stage (o1..o9) over 80 tiles, then the
+gather.
+  value   inputs resident in HBM (rtg_process_tile_dev on 4 contexts / streams);
+          each rank owns a fixed shard of the slide's tile sequence.
+  e2e     the stage's whole product through the C-ABI host entry point
+          rtg_process_tile_async: pinned host RGB in; mask (u8), labels (i32)
+          and feature rows out; upload / stage / download of three tiles per
+          context overlap.  Tiles are handed out by a demand-driven counter
+          shared by all ranks (reference ManagerState::dispatch,
+          dataflow.cpp:73-82), and the feature tables are gathered to rank 0
+          over NCCL every step.  `e2e_features_only` is the same without the
+          mask / labels download (rtg_process_tiles).
+  configs the other BASELINE configs on one GPU (rank 0, N=1): C1 single-tile
+          latency, C2 IWPP reconstruction (h-dome and maze, 4/8-conn), C3 dense
+          touching nuclei (area + watershed + labels), C4 features; each with
+          its roofline fraction and the oracle's single-thread latency.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -21,7 +32,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -35,6 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 TILE = 4096
+TILES_PER_RANK = 80
 METRIC = "tile Mpixel/s (segment+features) at 1/2/4/8 B200, % of HBM roofline"
 WORKLOAD = ("C5: 100k x 100k synthetic WSI as 4K tiles (partition_regular: 576 full, "
             "48 edge, 1 corner), bag of tasks, per-step NCCL gather of feature tables")
@@ -42,7 +53,7 @@ WORKLOAD = ("C5: 100k x 100k synthetic WSI as 4K tiles (partition_regular: 576 f
 # Algorithmic bytes per pixel of each stage: compulsory inputs
 # read once + outputs written once.
 STAGE_BYTES_PER_PX = {
-    "colordeconv": 5,   # RGB 3 in; hematoxylin + tissue 1 each out (the marker plane is only written on the IWPP option path)
+    "colordeconv": 5,   # RGB 3 in; hematoxylin + tissue 1 each out
     "recon": 3,         # marker + mask in, reconstruction out (u8)
     "fill_holes": 3,    # reconstruction + tissue in, filled mask out
     "area": 2,          # mask in, filtered mask out
@@ -52,9 +63,16 @@ STAGE_BYTES_PER_PX = {
     "label": 5,         # separated mask in, labels i32 out
     "features": 5,      # labels i32 + intensity u8 in (table out is ~0.1 B/px)
 }
-
+WHOLE_STAGE_BYTES_PER_PX = 8  # RGB 3 in + mask 1 + labels 4 out
 
 from paper_1405_7958_b200.wsi import gather_tables, global_tile, rank_tiles  # noqa: E402
+
+
+def bench_config(tiles_per_rank):
+    """The workload description both arms report (identical by construction)."""
+    return {"workload": WORKLOAD, "tiles_per_rank_per_step": tiles_per_rank,
+            "tile": "4096x4096, edge tiles clamped (partition_regular)",
+            "l2": "inputs larger than L2 (48 MiB RGB + ~400 MiB planes per tile)"}
 
 
 def measured_peaks():
@@ -64,6 +82,18 @@ def measured_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def cpu_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count(), "usable": host_cores()}
 
 
 class ClockSampler:
@@ -128,58 +158,87 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def cpu_oracle_sample(n_tiles, threads):
-    """The oracle on the host cores over a bounded sample of WSI tiles (bag of
-    tasks over a thread pool, like ManagerState::dispatch).  Returns
-    (Mpixel/s, seconds, pixels)."""
+def bind_numa(device):
+    """Pins this rank's threads to the host cores of its GPU's NUMA node
+    (NUMA-aware placement took 3 GPUs from 2.27x to
+    2.82x).  Returns the node, or None when the topology has one node."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(device)
+        path = (f"/sys/bus/pci/devices/{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:"
+                f"{pr.pci_device_id:02x}.0/numa_node")
+        node = int(open(path).read().strip())
+        if node < 0:
+            return None
+        cpus = open(f"/sys/devices/system/node/node{node}/cpulist").read().strip()
+        allowed = set()
+        for part in cpus.split(","):
+            a, _, b = part.partition("-")
+            allowed.update(range(int(a), int(b or a) + 1))
+        if allowed:
+            os.sched_setaffinity(0, allowed)
+        return node
+    except Exception:
+        return None
+
+
+def oracle_tiles(tiles):
+    """Host RGB of `tiles` from the oracle's copy of the generator (the CPU
+    legs never load librtg.so)."""
+    from oracle import pyoracle
+    return [pyoracle.synth_tile_host(r, c, h, w) for (r, c, h, w) in tiles]
+
+
+def cpu_oracle_run(rgbs, threads):
+    """The oracle over `rgbs` on a thread pool (bag of tasks, one tile per
+    thread at a time, like ManagerState::dispatch).  Returns (s, pixels)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import pyoracle
-    from paper_1405_7958_b200 import rtg
 
-    pyoracle.load()
     params = pyoracle.default_params()
-    tiles = [global_tile(g) for g in range(n_tiles)]
-    rgbs = [rtg.synth_tile_host(r, c, h, w) for (r, c, h, w) in tiles]
-    px = sum(h * w for (_, _, h, w) in tiles)
-
-    def run(k):
-        pyoracle.process_tile(rgbs[k], params, max_rows=1 << 16)
-
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(run, range(n_tiles)))
-    dt = time.perf_counter() - t0
-    return px / dt / 1e6, dt, px
+        list(ex.map(lambda a: pyoracle.process_tile(a, params, max_rows=1 << 16), rgbs))
+    return time.perf_counter() - t0, sum(a.shape[0] * a.shape[1] for a in rgbs)
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference has no implementation of this path
-    (SPEC.md:15), so its CPU arm is the oracle port timed on the host cores."""
+    (SPEC.md:15), so its CPU arm is the oracle port (-O3 -march=native,
+    built on this host), timed on all host cores over a bounded sample of
+    the same workload: step k runs `cores` tiles taken cyclically from rank
+    0's 80-tile shard (full, edge and corner tiles alike)."""
     if rank != 0:
         return
+    from oracle import pyoracle
+    pyoracle.load(native=True)
     cores = host_cores()
-    n_tiles = max(1, min(cores, 64))
-    for _ in range(args.warmup):
-        cpu_oracle_sample(min(n_tiles, cores), cores)
-    vals, secs, pxs = [], 0.0, 0
-    for _ in range(args.steps):
-        v, dt, px = cpu_oracle_sample(n_tiles, cores)
-        vals.append(v)
+    shard = rank_tiles(0, args.tiles_per_rank)
+    per_step = min(cores, len(shard))
+    need = (args.warmup + args.steps) * per_step
+    order = [shard[i % len(shard)] for i in range(need)]
+    rgbs = oracle_tiles(order[: min(need, len(shard))])
+    pick = lambda k: [rgbs[(k * per_step + j) % len(rgbs)] for j in range(per_step)]  # noqa: E731
+    for k in range(args.warmup):
+        cpu_oracle_run(pick(k), cores)
+    secs = pxs = 0
+    for k in range(args.warmup, args.warmup + args.steps):
+        dt, px = cpu_oracle_run(pick(k), cores)
         secs += dt
         pxs += px
     value = pxs / secs / 1e6
-    sample = (f"{n_tiles} WSI tiles (first {n_tiles} of the 625-tile 100k^2 slide) per step, "
-              f"oracle pipeline o1..o9, {cores} threads")
+    sample = (f"{per_step} tiles per step, cycling through rank 0's {len(shard)}-tile shard "
+              f"of the 625-tile 100k^2 slide; oracle o1..o9 (-O3 -march=native), "
+              f"{cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOAD,
-                   "path": "CPU oracle port (reference ships no pixel code); each step a "
-                           "bounded sample of the workload's tiles"},
+        "config": bench_config(args.tiles_per_rank),
+        "path": "CPU oracle port (the reference ships no pixel code, SPEC.md:15)",
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "cpu": cpu_info()},
         "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -188,18 +247,156 @@ def run_reference(args, rank, world):
 
 # --------------------------------------------------------------------------- GPU arm
 
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def run_configs(rtg, torch, ctx, params, peak, cpu_reps):
+    """BASELINE configs C1..C4 on one GPU with the oracle's single-thread
+    latency beside each (BASELINE.md §2 mode 1).  Device times are CUDA
+    events on the launching stream over repeated launches."""
+    from oracle import pyoracle
+    out = {}
+    stream = torch.cuda.Stream()
+    old = ctx.stream()
+    ctx.set_stream(stream.cuda_stream)
+    H = W = TILE
+    px = H * W
+
+    def dev_ms(fn, reps):
+        fn()
+        stream.synchronize()
+        e0, e1 = _events(torch)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        stream.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def cpu_ms(fn, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts)
+
+    def roof(bpp, ms):
+        ach = bpp * px / (ms / 1e3) / 1e9
+        return {"bytes_per_px": bpp, "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4)}
+
+    rgb_h = pyoracle.synth_tile_host(0, 0, H, W)
+    d_rgb = torch.from_numpy(rgb_h).cuda()
+    d_mask = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    d_lab = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    d_hema = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    d_feat = torch.empty((ctx.max_objects, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+    d_n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+
+    # C1: one tile, whole stage
+    ms = dev_ms(lambda: ctx.process_tile_dev(d_rgb, H, W, params, d_mask, d_lab, d_hema,
+                                             d_feat, d_n), 20)
+    pin = {k: torch.empty(s, dtype=dt, pin_memory=True).numpy() for k, s, dt in (
+        ("rgb", (H, W, 3), torch.uint8), ("mask", (H, W), torch.uint8),
+        ("labels", (H, W), torch.int32), ("feats", (ctx.max_objects, rtg.NUM_FEATURES),
+                                          torch.float32))}
+    pin["rgb"][...] = rgb_h
+    ctx.set_stream(0)
+    ctx.wait(ctx.process_tile_async(pin["rgb"], params, mask=pin["mask"], labels=pin["labels"],
+                                    feats=pin["feats"]))
+    lat = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        ctx.wait(ctx.process_tile_async(pin["rgb"], params, mask=pin["mask"],
+                                        labels=pin["labels"], feats=pin["feats"]))
+        lat.append((time.perf_counter() - t0) * 1e3)
+    ctx.set_stream(stream.cuda_stream)
+    c1_cpu = cpu_ms(lambda: pyoracle.process_tile(rgb_h, max_rows=1 << 16), cpu_reps)
+    out["C1"] = {"what": "one 4096^2 synthetic H&E tile, whole stage o1..o9",
+                 "device_ms": round(ms, 4), "mpx_s": round(px / ms / 1e3, 1),
+                 "roofline": roof(WHOLE_STAGE_BYTES_PER_PX, ms),
+                 "e2e_latency_ms": round(statistics.median(lat), 3),
+                 "e2e_path": "rtg_process_tile_async + wait, pinned host RGB in, mask + labels "
+                             "+ features out (H2D 48 MiB, D2H 80 MiB)",
+                 "cpu_single_thread_ms": round(c1_cpu, 1)}
+
+    # C4: features over the C1 labels (~20k objects)
+    ctx.process_tile_dev(d_rgb, H, W, params, d_mask, d_lab, d_hema, d_feat, d_n)
+    stream.synchronize()
+    n = int(d_n.cpu()[0])
+    ms = dev_ms(lambda: ctx.features_dev(d_lab, d_hema, H, W, d_n, d_feat), 20)
+    lab_h, hema_h = d_lab.cpu().numpy(), d_hema.cpu().numpy()
+    c4_cpu = cpu_ms(lambda: pyoracle.features(lab_h, hema_h, n), cpu_reps)
+    out["C4"] = {"what": f"per-object features over {n} labelled nuclei (C1 tile)",
+                 "device_ms": round(ms, 4), "roofline": roof(5, ms),
+                 "cpu_single_thread_ms": round(c4_cpu, 1)}
+
+    # C2: IWPP grayscale reconstruction microbench
+    hema_c, marker_c, _ = pyoracle.colordeconv(rgb_h, pyoracle.default_params())
+    marker_c = np.maximum(hema_c.astype(np.int16) - 32, 0).astype(np.uint8)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from synthetic_inputs import dense_touching, serpentine_maze
+    maze, maze_seed = serpentine_maze(H, W)
+    d_out = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    c2 = {}
+    for case, (mk, msk, reps) in {"hdome_h32": (marker_c, hema_c, 10),
+                                  "maze_single_seed": (maze_seed, maze, 1)}.items():
+        d_mk, d_ms = torch.from_numpy(mk).cuda(), torch.from_numpy(msk).cuda()
+        torch.cuda.synchronize()
+        for conn in (4, 8):
+            ms = dev_ms(lambda: ctx.recon_dev(d_mk, d_ms, H, W, conn, d_out), reps)
+            t0 = time.perf_counter()
+            ref = pyoracle.recon(mk, msk, conn)
+            ref_ms = (time.perf_counter() - t0) * 1e3
+            ok = bool(np.array_equal(d_out.cpu().numpy(), ref))
+            c2[f"{case}_conn{conn}"] = {"device_ms": round(ms, 4), "roofline": roof(3, ms),
+                                        "bit_exact_vs_oracle": ok,
+                                        "cpu_single_thread_ms": round(ref_ms, 1)}
+    out["C2"] = {"what": "rtg_recon_u8_dev (IWPP tile queue) at 4096^2: h-dome marker = "
+                         "max(H - 32, 0) under the H plane of tile (0,0), and a serpentine "
+                         "1-px maze (2048 corridors) from one seed", **c2}
+
+    # C3: dense touching nuclei (>= 35 % foreground, >= 50 % of nuclei touching)
+    m3, discs = dense_touching(3, H, W)
+    d_m3 = torch.from_numpy(m3).cuda()
+    d_a, d_s = torch.empty_like(d_m3), torch.empty_like(d_m3)
+    torch.cuda.synchronize()
+
+    def c3():
+        ctx.area_threshold_dev(d_m3, H, W, 8, params.min_area, params.max_area, d_a)
+        ctx.watershed_dev(d_a, H, W, params.ws_h, d_s)
+        ctx.bwlabel_dev(d_s, H, W, 8, d_lab, d_n)
+    ms = dev_ms(c3, 10)
+
+    def c3_cpu():
+        a = pyoracle.area_threshold(m3, 8, params.min_area, params.max_area)
+        s_, _ = pyoracle.watershed(a, params.ws_h)
+        pyoracle.bwlabel(s_, 8)
+    out["C3"] = {"what": f"area threshold + EDT/HMAX watershed + canonical CCL on a 4096^2 "
+                         f"mask of {discs} overlapping discs ({m3.mean():.1%} foreground)",
+                 "device_ms": round(ms, 4), "roofline": roof(5, ms),
+                 "objects": int(d_n.cpu()[0]),
+                 "cpu_single_thread_ms": round(cpu_ms(c3_cpu, 1), 1)}
+    ctx.set_stream(old)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rtg", choices=["rtg", "reference"])
-    ap.add_argument("--tiles-per-rank", type=int, default=80,
+    ap.add_argument("--tiles-per-rank", type=int, default=TILES_PER_RANK,
                     help="tiles each rank processes per step (80 x 8 GPUs ~ one 625-tile WSI)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent contexts per GPU")
-    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1..C4 lines")
+    ap.add_argument("--cpu-reps", type=int, default=1,
+                    help="single-thread oracle repetitions per config (median)")
     ap.add_argument("--pdl", action="store_true",
                     help="programmatic dependent launch between kernels (A/B; off by default)")
     args = ap.parse_args()
@@ -217,6 +414,7 @@ def main():
     from paper_1405_7958_b200 import rtg
 
     torch.cuda.set_device(local)
+    numa = bind_numa(local)
     if world > 1:
         # keep stdout to the one JSON line: NCCL prints its version banner on
         # fd 1 when the first communicator comes up, so fd 1 points at stderr
@@ -237,6 +435,18 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t)
+        return float(t.item())
 
     T = args.tiles_per_rank
     S = max(1, args.streams)
@@ -259,6 +469,7 @@ def main():
     ctxs[0].sync()
     feats = torch.empty((T, cap, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
     counts = torch.zeros((T,), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
 
     def gather(n_host):
         """Pack this rank's per-tile tables and gather them on rank 0 (NCCL)."""
@@ -298,8 +509,7 @@ def main():
     clocks.start()
     barrier()
     torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    t_start, t_end = _events(torch)
     t_start.record(cur)
     total_rows = 0
     for _ in range(args.steps):
@@ -311,10 +521,7 @@ def main():
     clk = clocks.stop()
     ms = t_start.elapsed_time(t_end)
     gpu_launches = sum(c.launches() for c in ctxs) - launches0
-    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = max_over_ranks(ms)
     total_px = px_rank * world * args.steps
     value = total_px / (ms_max / 1e3) / 1e6
 
@@ -351,8 +558,7 @@ def main():
     # The streaming kernel alone: back-to-back launches of k_colordeconv_vec
     # (rtg_colordeconv_dev, the stage's own kernel and parameters) cycling
     # over the resident tiles (inputs larger than L2), CUDA events on the
-    # launching stream.  A single-kernel stage window in the eager profiling
-    # pass also holds the launch gap before it (~5 us of a ~25 us kernel).
+    # launching stream.
     full = [k for k in range(min(T, 16)) if my_tiles[k][2:] == (TILE, TILE)]
     if full:
         sk = torch.cuda.Stream()
@@ -363,8 +569,7 @@ def main():
         reps = 4 * len(full)
         for k in full[:3]:
             ctx.colordeconv_dev(rgbs[k], TILE, TILE, params, hema_b, None, tis_b)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = _events(torch)
         e0.record(sk)
         for i in range(reps):
             ctx.colordeconv_dev(rgbs[full[i % len(full)]], TILE, TILE, params, hema_b, None, tis_b)
@@ -386,86 +591,34 @@ def main():
         for rf in (roofline, roof_stream):
             if rf["stage"] in tr:
                 rf["traffic"] = tr[rf["stage"]]
+    whole = {"bound": "hbm", "bytes_per_px": WHOLE_STAGE_BYTES_PER_PX,
+             "achieved": round(value / world * WHOLE_STAGE_BYTES_PER_PX / 1e3, 1),
+             "peak": peak, "unit": "GB/s",
+             "frac": round(value / world * WHOLE_STAGE_BYTES_PER_PX / 1e3 / peak, 4),
+             "note": "per-GPU value x SURVEY §8d C1's 8 B/px (RGB in, mask + labels out)"}
 
-    # ---- e2e through the C-ABI host-buffer entry point (pinned host tiles)
-    e2e = None
+    # ---- e2e through the C-ABI host entry points (pinned host buffers)
+    e2e = e2e_feat = None
     if not args.no_e2e:
-        pool = min(T, 8)
-        host = []
-        for k in range(pool):
-            r, c, h, w = my_tiles[k]
-            hb = torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True)
-            hb.copy_(rgbs[k].cpu())
-            host.append(hb.numpy())
-        fbufs = [torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy()
-                 for _ in range(S)]
-        d2h = [0] * S
-        e2e_tiles = list(range(T))
-
-        def worker(si, ks):
-            cx = ctxs[si]
-            cx.set_stream(0)
-            # rtg_process_tiles: same-shape runs of the rank's tiles in one call
-            # (H2D RGB of tile i+1 overlaps o1..o9 of tile i; feature rows go
-            # to pinned host memory)
-            j = 0
-            while j < len(ks):
-                r, c, h, w = my_tiles[ks[j]]
-                e = j
-                while e < len(ks) and my_tiles[ks[e]][2:] == (h, w):
-                    e += 1
-                # edge tiles reuse a prefix of a pinned full-tile buffer
-                batch = [host[k % pool].reshape(-1)[:h * w * 3].reshape(h, w, 3)
-                         for k in ks[j:e]]
-                _, ns = cx.process_tiles(batch, feats=[fbufs[si]] * len(batch), max_rows=cap)
-                d2h[si] += sum(n * rtg.NUM_FEATURES * 4 + 4 for n in ns)
-                j = e
-
-        def run_e2e():
-            th = [threading.Thread(target=worker, args=(si, e2e_tiles[si::S])) for si in range(S)]
-            for t in th:
-                t.start()
-            for t in th:
-                t.join()
-
-        run_e2e()  # warm-up
-        barrier()
-        torch.cuda.synchronize()
-        for i in range(S):
-            d2h[i] = 0
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(cur)
-        for _ in range(args.e2e_steps):
-            run_e2e()
-        e1.record(cur)
-        torch.cuda.synchronize()
-        barrier()
-        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e_ms = float(ems.item())
-        # whole-job bytes per step (all ranks), like `value`
-        d2h_all = torch.tensor([float(sum(d2h))], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(d2h_all)
-        e2e = {"value": round(px_rank * world * args.e2e_steps / (e_ms / 1e3) / 1e6, 3),
-               "unit": "Mpixel/s",
-               "h2d_bytes_per_step": int(3 * px_rank * world),
-               "d2h_bytes_per_step": int(float(d2h_all.item()) / args.e2e_steps),
-               "steps": args.e2e_steps,
-               "path": "rtg_process_tiles (host buffers, pinned; H2D RGB + D2H features, "
-                       "double-buffered upload)",
-               "host_tile_pool": pool}
+        e2e, e2e_feat = run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank,
+                                world, barrier, max_over_ranks, sum_over_ranks)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = host_cores()
-        n_s = max(1, min(cores, 32))
-        v, dt, px = cpu_oracle_sample(n_s, cores)
-        cpu = {"value": round(v, 3), "unit": "Mpixel/s", "cores": cores, "kind": "port",
-               "sample": f"{n_s} WSI tiles through the oracle (o1..o9) on {cores} threads, "
-                         f"{dt:.1f} s"}
+    configs = None
+    if rank == 0 and world == 1:
+        if not args.no_configs:
+            configs = run_configs(rtg, torch, ctxs[0], params, peak, args.cpu_reps)
+        if not args.no_cpu_baseline:
+            from oracle import pyoracle
+            pyoracle.load(native=True)
+            cores = host_cores()
+            n_s = max(1, min(cores, 32))
+            sample_tiles = my_tiles[:n_s]
+            dt, px = cpu_oracle_run(oracle_tiles(sample_tiles), cores)
+            cpu = {"value": round(px / dt / 1e6, 3), "unit": "Mpixel/s", "cores": cores,
+                   "kind": "port", "cpu": cpu_info(),
+                   "sample": f"the first {n_s} tiles of this rank's shard through the oracle "
+                             f"(o1..o9, -O3 -march=native) on {cores} threads, {dt:.1f} s"}
 
     if rank == 0:
         line = {
@@ -474,16 +627,18 @@ def main():
             "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded H&E-like tiles generated on device)",
-            "config": {"workload": WORKLOAD,
-                       "tiles_per_rank_per_step": T, "streams_per_gpu": S,
-                       "pixels_per_step": px_rank * world,
-                       "l2": "inputs larger than L2 (48 MiB RGB + ~400 MiB planes per tile)",
-                       "feature_rows_per_step": int(total_rows / max(args.steps, 1))},
+            "config": bench_config(T),
+            "run": {"streams_per_gpu": S, "pixels_per_step": px_rank * world,
+                    "feature_rows_per_step": int(total_rows / max(args.steps, 1)),
+                    "numa_node": numa},
             "roofline": roofline,
             "roofline_streaming": roof_stream,
+            "roofline_whole_stage": whole,
             "stage_ms_per_tile": {s: round(v / n_prof, 4) for s, v in stage_ms.items()},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_features_only": e2e_feat,
+            "configs": configs,
             "gpu_launches": int(gpu_launches),
             "clocks": clk,
         }
@@ -494,25 +649,172 @@ def main():
         dist.destroy_process_group()
 
 
-def ctypes_process(ctx, rgb, h, w, fbuf):
-    import ctypes
-    from paper_1405_7958_b200 import rtg
-    n = ctypes.c_int32(0)
-    rtg.check(ctx.lib.rtg_process_tile(ctx.handle, rgb.ctypes.data, h, w, 3 * w,
-                                       ctypes.byref(_PARAMS()), None, None, None,
-                                       fbuf.ctypes.data, fbuf.shape[0], ctypes.byref(n)))
-    return n.value
+def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, barrier,
+            max_over_ranks, sum_over_ranks):
+    """The stage's product through the host-buffer C-ABI.
 
+    Full product: rtg_process_tile_async with pinned RGB in and pinned mask /
+    labels / feature rows out, three tiles in flight per context, tiles
+    handed out by a counter shared by every rank (demand-driven), then the
+    per-step NCCL gather of the feature tables.  Features only: the
+    double-buffered batch entry rtg_process_tiles over the rank's shard."""
+    S = len(ctxs)
+    T = len(my_tiles)
+    steps = args.steps
+    pool = min(T, 8)
+    # pinned host tiles (a pool of distinct synthetic tiles; an edge tile
+    # reuses a prefix of a full-tile buffer)
+    host = []
+    for k in range(pool):
+        r, c, h, w = my_tiles[k]
+        hb = torch.empty((TILE, TILE, 3), dtype=torch.uint8, pin_memory=True)
+        d = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
+        ctxs[0].synth_tile_dev(d, r, c, h, w)
+        ctxs[0].sync()
+        hb.view(-1)[: h * w * 3].copy_(d.view(-1).cpu())
+        host.append(hb.numpy())
 
-_P = None
+    def host_tile(k, h, w):
+        return host[k % pool].reshape(-1)[: h * w * 3].reshape(h, w, 3)
 
+    slots = rtg.ASYNC_SLOTS
+    outs = [[(torch.empty((TILE * TILE,), dtype=torch.uint8, pin_memory=True).numpy(),
+              torch.empty((TILE * TILE,), dtype=torch.int32, pin_memory=True).numpy(),
+              torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy())
+             for _ in range(slots)] for _ in range(S)]
+    store = dist.distributed_c10d._get_default_store() if world > 1 else None
+    # every rank gets the same number of tiles per step in total (weak
+    # scaling: T per rank), but which rank runs which tile is decided at run
+    # time by the shared counter
+    global_tiles = [global_tile(g) for g in range(T * world)]
+    lock = threading.Lock()
+    local_next = [0]
 
-def _PARAMS():
-    global _P
-    if _P is None:
-        from paper_1405_7958_b200 import rtg
-        _P = rtg.default_params()
-    return _P
+    def grab(step_key):
+        if store is not None:
+            return int(store.add(step_key, 1)) - 1
+        with lock:
+            v = local_next[0]
+            local_next[0] += 1
+            return v
+
+    d2h = [0] * S
+    h2d = [0] * S
+    rows_out = [[] for _ in range(S)]  # this step's feature tables, per context
+
+    def worker(si, step_key):
+        cx = ctxs[si]
+        inflight = []  # (ticket, feature buffer)
+
+        def retire():
+            t, f = inflight.pop(0)
+            n = cx.wait(t)
+            rows_out[si].append(f[:n].copy())  # the slot's buffer is reused next
+            d2h[si] += 4 + n * rtg.NUM_FEATURES * 4
+
+        j = 0
+        while True:
+            g = grab(step_key)
+            if g >= len(global_tiles):
+                break
+            r, c, h, w = global_tiles[g]
+            if len(inflight) == slots:
+                retire()
+            m, lab, f = outs[si][j % slots]
+            t = cx.process_tile_async(host_tile(g, h, w), params, mask=m[: h * w].reshape(h, w),
+                                      labels=lab[: h * w].reshape(h, w), feats=f, max_rows=cap)
+            inflight.append((t, f))
+            h2d[si] += 3 * h * w
+            d2h[si] += 5 * h * w
+            j += 1
+        while inflight:
+            retire()
+
+    def one_step(k):
+        key = f"rtg_e2e_{k}"
+        for si in range(S):
+            rows_out[si].clear()
+        local_next[0] = 0
+        th = [threading.Thread(target=worker, args=(si, key)) for si in range(S)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        # this rank's feature tables -> one device table -> NCCL gather to rank 0
+        tables = [a for si in range(S) for a in rows_out[si]]
+        rows = sum(len(a) for a in tables)
+        packed = torch.from_numpy(np.concatenate(tables) if rows else
+                                  np.zeros((1, rtg.NUM_FEATURES), np.float32))
+        gather_tables(packed.cuda(), rows, rank, world, dist)
+
+    for c in ctxs:
+        c.set_stream(0)
+    one_step(-1)  # warm-up: graphs, slots, pinned pages
+    barrier()
+    torch.cuda.synchronize()
+    for si in range(S):
+        d2h[si] = h2d[si] = 0
+    t0 = time.perf_counter()
+    for k in range(steps):
+        one_step(k)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()
+    wall = max_over_ranks(wall)
+    px_all = sum(h * w for (_, _, h, w) in global_tiles) * steps
+    full = {"value": round(px_all / wall / 1e6, 3), "unit": "Mpixel/s",
+            "h2d_bytes_per_step": int(sum_over_ranks(sum(h2d)) / steps),
+            "d2h_bytes_per_step": int(sum_over_ranks(sum(d2h)) / steps),
+            "steps": steps,
+            "timing": "host wall clock around the steps (the C-ABI returns host-visible "
+                      "results), max over ranks",
+            "path": "rtg_process_tile_async: pinned RGB in; mask u8 + labels i32 + feature "
+                    "rows out; 3 tiles in flight per context, 4 contexts; demand-driven "
+                    "tile counter across ranks; NCCL gather of the feature tables per step",
+            "pcie_per_gpu_gbs": {"h2d": round(sum_over_ranks(sum(h2d)) / wall / 1e9 / world, 1),
+                                 "d2h": round(sum_over_ranks(sum(d2h)) / wall / 1e9 / world, 1)}}
+
+    # features only: rtg_process_tiles over the rank's own shard
+    fbufs = [torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy()
+             for _ in range(S)]
+    fd2h = [0] * S
+
+    def fworker(si, ks):
+        cx = ctxs[si]
+        j = 0
+        while j < len(ks):
+            r, c, h, w = my_tiles[ks[j]]
+            e = j
+            while e < len(ks) and my_tiles[ks[e]][2:] == (h, w):
+                e += 1
+            batch = [host_tile(k, h, w) for k in ks[j:e]]
+            _, ns = cx.process_tiles(batch, feats=[fbufs[si]] * len(batch), max_rows=cap)
+            fd2h[si] += sum(n * rtg.NUM_FEATURES * 4 + 4 for n in ns)
+            j = e
+
+    def fstep():
+        th = [threading.Thread(target=fworker, args=(si, list(range(T))[si::S]))
+              for si in range(S)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    fstep()
+    barrier()
+    for si in range(S):
+        fd2h[si] = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fstep()
+    wall_f = max_over_ranks(time.perf_counter() - t0)
+    px_rank = sum(h * w for (_, _, h, w) in my_tiles)
+    feat = {"value": round(px_rank * world * steps / wall_f / 1e6, 3), "unit": "Mpixel/s",
+            "h2d_bytes_per_step": int(3 * px_rank * world),
+            "d2h_bytes_per_step": int(sum_over_ranks(sum(fd2h)) / steps), "steps": steps,
+            "path": "rtg_process_tiles (pinned RGB in, feature rows out, double-buffered "
+                    "upload; no mask / labels download)"}
+    return full, feat
 
 
 if __name__ == "__main__":

@@ -169,25 +169,7 @@ def test_concurrent_contexts_wsi_shard(rtg, oracle):
 
 # ---------------------------------------------------------------- C3 dense nuclei
 
-def _dense_touching(seed, h, w, fg=0.36):
-    """Clusters of 2-4 overlapping discs (radius 4-8 px); returns the mask
-    and the number of discs."""
-    rng = np.random.default_rng(seed)
-    m = np.zeros((h, w), np.uint8)
-    yy, xx = np.mgrid[-9:10, -9:10]
-    stamps = {r: (yy * yy + xx * xx <= r * r).astype(np.uint8) for r in range(4, 9)}
-    discs = 0
-    while True:
-        for _ in range(2000):
-            cy, cx = rng.integers(9, h - 9), rng.integers(9, w - 9)
-            for _ in range(rng.integers(2, 5)):
-                r = int(rng.integers(4, 9))
-                oy = int(np.clip(cy + rng.integers(-r, r + 1), 9, h - 10))
-                ox = int(np.clip(cx + rng.integers(-r, r + 1), 9, w - 10))
-                m[oy - 9:oy + 10, ox - 9:ox + 10] |= stamps[r]
-                discs += 1
-        if m.mean() >= fg:
-            return m, discs
+from synthetic_inputs import dense_touching as _dense_touching  # noqa: E402
 
 
 @pytest.fixture(scope="module")
