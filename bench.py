@@ -649,6 +649,33 @@ def main():
         dist.destroy_process_group()
 
 
+def pcie_peak(torch, nbytes=512 << 20, reps=8):
+    """Copy-engine bandwidth of this GPU's host link with pinned buffers:
+    H2D alone, D2H alone, and both at once (GB/s)."""
+    host_a = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    host_b = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dev_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    dev_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d, d2h):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    dev_a.copy_(host_a, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    host_b.copy_(dev_b, non_blocking=True)
+        torch.cuda.synchronize()
+        return nbytes * reps / (time.perf_counter() - t0) / 1e9
+
+    run(True, True)
+    return {"h2d_gbs": round(run(True, False), 1), "d2h_gbs": round(run(False, True), 1),
+            "duplex_gbs_each": round(run(True, True), 1)}
+
+
 def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, barrier,
             max_over_ranks, sum_over_ranks):
     """The stage's product through the host-buffer C-ABI.
@@ -747,6 +774,7 @@ def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, ba
                                   np.zeros((1, rtg.NUM_FEATURES), np.float32))
         gather_tables(packed.cuda(), rows, rank, world, dist)
 
+    link = pcie_peak(torch)
     for c in ctxs:
         c.set_stream(0)
     one_step(-1)  # warm-up: graphs, slots, pinned pages
@@ -772,7 +800,14 @@ def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, ba
                     "rows out; 3 tiles in flight per context, 4 contexts; demand-driven "
                     "tile counter across ranks; NCCL gather of the feature tables per step",
             "pcie_per_gpu_gbs": {"h2d": round(sum_over_ranks(sum(h2d)) / wall / 1e9 / world, 1),
-                                 "d2h": round(sum_over_ranks(sum(d2h)) / wall / 1e9 / world, 1)}}
+                                 "d2h": round(sum_over_ranks(sum(d2h)) / wall / 1e9 / world, 1)},
+            "pcie_link_peak_gbs": link}
+    d2h_gbs = full["pcie_per_gpu_gbs"]["d2h"]
+    full["roofline"] = {"bound": "pcie_d2h", "achieved": d2h_gbs,
+                        "peak": link["duplex_gbs_each"], "unit": "GB/s",
+                        "frac": round(d2h_gbs / max(link["duplex_gbs_each"], 1e-9), 4),
+                        "note": "5 B/px of mask + labels back over the host link while 3 B/px "
+                                "of RGB go up; peak = this link's measured duplex copy rate"}
 
     # features only: rtg_process_tiles over the rank's own shard
     fbufs = [torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy()

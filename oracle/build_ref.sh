@@ -26,3 +26,16 @@ PKG="$HERE/../paper_1405_7958_b200"
 g++ -std=c++20 -O2 -I"$PKG/host/include" -I"$HERE/../include" "$HERE/host_probe.cpp" \
     "$PKG/librt_host.a" -lpthread -o "$OUT/host_probe_ours"
 echo "built $OUT"
+# Drop-in proof: the INTEGRATION.md task body run through the reference
+# runtime itself (its ManagerState / WrmState / worker_prepare / DmsStore /
+# stage_finalize), linked with librtg.so; the oracle is compiled in as the
+# checker.  Runs on a GPU box (./oracle/_ref/ref_integration) or with --cpu.
+gcc -O2 -ffp-contract=off -std=c11 -I"$HERE/../include" -c "$HERE/rtg_oracle.c" -o "$OUT/obj/oracle_checker.o"
+gcc -O2 -std=c11 -I"$HERE/../include" -Drtg_synth_max_shapes=orc_synth_max_shapes \
+    -Drtg_synth_shapes=orc_synth_shapes -Drtg_synth_raster_host=orc_synth_raster_host \
+    -Drtg_synth_tile_host=orc_synth_tile_host -c "$PKG/csrc/synth.c" -o "$OUT/obj/oracle_synth.o"
+g++ -std=c++20 -O2 -I"$REF/include" -I"$HERE/../include" -I"$HERE" "$HERE/ref_integration.cpp" \
+    "$OUT/obj/oracle_checker.o" "$OUT/obj/oracle_synth.o" "$OUT/librt_ref.a" \
+    -L"$PKG" -lrtg -Wl,-rpath,'$ORIGIN/../../paper_1405_7958_b200' -lpthread -lm \
+    -o "$OUT/ref_integration"
+echo "built $OUT/ref_integration"

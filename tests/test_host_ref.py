@@ -39,3 +39,37 @@ def test_host_layer_matches_reference_runtime():
     assert len(ref) > 540
     diffs = [(i, a, b) for i, (a, b) in enumerate(zip(ref, ours)) if a != b]
     assert len(ref) == len(ours) and not diffs, diffs[:5]
+
+
+INTEG = os.path.join(ROOT, "oracle", "_ref", "ref_integration")
+
+
+def _integration_binary():
+    if not os.path.exists(INTEG):
+        if os.path.isdir("/root/reference"):
+            subprocess.run(["bash", os.path.join(ROOT, "oracle", "build_ref.sh")], check=True,
+                           capture_output=True)
+        else:
+            pytest.skip("reference runtime not built here (no /root/reference)")
+    return INTEG
+
+
+def test_reference_runtime_harness_cpu():
+    """oracle/ref_integration.cpp runs the INTEGRATION.md task body through the
+    reference's own ManagerState / WrmState / worker_prepare / 3-D DmsStore /
+    stage_finalize; with --cpu the body is the oracle (harness self-check)."""
+    r = subprocess.run([_integration_binary(), "--cpu"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK 6 stages" in r.stdout
+
+
+@pytest.mark.gpu
+def test_drop_in_through_reference_runtime_gpu():
+    """The same pipeline with the B200 body (librtg.so rtg_process_tile): every
+    tile's Mask / Labels read back from the reference DmsStore equal the
+    oracle's bit for bit, Features within rtol 1e-5."""
+    r = subprocess.run([_integration_binary()], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK 6 stages" in r.stdout and "B200" in r.stdout
