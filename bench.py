@@ -65,7 +65,8 @@ STAGE_BYTES_PER_PX = {
 }
 WHOLE_STAGE_BYTES_PER_PX = 8  # RGB 3 in + mask 1 + labels 4 out
 
-from paper_1405_7958_b200.wsi import gather_tables, global_tile, rank_tiles  # noqa: E402
+from paper_1405_7958_b200.wsi import (  # noqa: E402
+    TileDispenser, gather_tables, global_tile, rank_tiles)
 
 
 def bench_config(tiles_per_rank):
@@ -709,27 +710,18 @@ def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, ba
               torch.empty((TILE * TILE,), dtype=torch.int32, pin_memory=True).numpy(),
               torch.empty((cap, rtg.NUM_FEATURES), dtype=torch.float32, pin_memory=True).numpy())
              for _ in range(slots)] for _ in range(S)]
-    store = dist.distributed_c10d._get_default_store() if world > 1 else None
-    # every rank gets the same number of tiles per step in total (weak
-    # scaling: T per rank), but which rank runs which tile is decided at run
-    # time by the shared counter
+    # every step processes T tiles per rank in total (weak scaling), but which
+    # rank runs which tile is decided at run time by the shared counter
     global_tiles = [global_tile(g) for g in range(T * world)]
-    lock = threading.Lock()
-    local_next = [0]
-
-    def grab(step_key):
-        if store is not None:
-            return int(store.add(step_key, 1)) - 1
-        with lock:
-            v = local_next[0]
-            local_next[0] += 1
-            return v
+    dispenser = TileDispenser(len(global_tiles),
+                              dist.distributed_c10d._get_default_store() if world > 1 else None,
+                              prefix="rtg_e2e")
 
     d2h = [0] * S
     h2d = [0] * S
     rows_out = [[] for _ in range(S)]  # this step's feature tables, per context
 
-    def worker(si, step_key):
+    def worker(si, step):
         cx = ctxs[si]
         inflight = []  # (ticket, feature buffer)
 
@@ -741,8 +733,8 @@ def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, ba
 
         j = 0
         while True:
-            g = grab(step_key)
-            if g >= len(global_tiles):
+            g = dispenser.next(step)
+            if g is None:
                 break
             r, c, h, w = global_tiles[g]
             if len(inflight) == slots:
@@ -758,11 +750,9 @@ def run_e2e(args, rtg, torch, dist, ctxs, my_tiles, params, cap, rank, world, ba
             retire()
 
     def one_step(k):
-        key = f"rtg_e2e_{k}"
         for si in range(S):
             rows_out[si].clear()
-        local_next[0] = 0
-        th = [threading.Thread(target=worker, args=(si, key)) for si in range(S)]
+        th = [threading.Thread(target=worker, args=(si, k)) for si in range(S)]
         for t in th:
             t.start()
         for t in th:

@@ -50,6 +50,36 @@ def rank_tiles(rank: int, tiles_per_rank: int) -> List[Tuple[int, int, int, int]
     return [global_tile(rank * tiles_per_rank + k) for k in range(tiles_per_rank)]
 
 
+class TileDispenser:
+    """Demand-driven tile dispatch shared by every rank and every feeder
+    thread (the reference's ManagerState::dispatch hands the next eligible
+    stage to whichever worker asks, dataflow.cpp:73-82): one counter per
+    step, incremented atomically through the process group's key-value store
+    (a lock-protected local counter when there is no group).  A rank that
+    finishes its tiles early simply takes more, so edge tiles and slow GPUs
+    do not stretch the step.
+
+    next(step) returns the next global tile index of that step, or None once
+    `tiles_per_step` have been handed out."""
+
+    def __init__(self, tiles_per_step: int, store=None, prefix: str = "rtg_tiles"):
+        import threading
+        self.n = int(tiles_per_step)
+        self.store = store
+        self.prefix = prefix
+        self._lock = threading.Lock()
+        self._local = {}
+
+    def next(self, step) -> Optional[int]:
+        if self.store is not None:
+            g = int(self.store.add(f"{self.prefix}_{step}", 1)) - 1
+        else:
+            with self._lock:
+                g = self._local.get(step, 0)
+                self._local[step] = g + 1
+        return g if g < self.n else None
+
+
 def gather_tables(packed, rows: int, rank: int, world: int, dist=None):
     """Gathers every rank's packed (rows, F) table on rank 0.
 

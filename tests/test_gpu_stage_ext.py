@@ -260,3 +260,108 @@ def test_two_devices_one_process(rtg):
         assert o[4] == outs[0][4]
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
         assert np.array_equal(o[3], outs[0][3])
+
+
+# ---------------------------------------------------------------- memory-safety / race evidence
+# compute-sanitizer is not available on the GPU pool, so out-of-bounds writes
+# into caller buffers are caught with guard bands, and races with repeated
+# concurrent runs that must stay bit-identical.
+
+_GUARD = 4096
+
+
+def _guarded(n_bytes, fill=0xA5):
+    buf = torch.full((_GUARD * 2 + n_bytes,), fill, dtype=torch.uint8, device="cuda")
+    return buf, buf[_GUARD:_GUARD + n_bytes]
+
+
+def _guards_intact(buf, fill=0xA5):
+    g = torch.cat([buf[:_GUARD], buf[-_GUARD:]])
+    return bool((g == fill).all())
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 5), (33, 31), (97, 203), (1000, 1333),
+                                   (4096, 1696)])
+def test_entry_points_write_inside_their_outputs(rtg, oracle, shape):
+    _need_gpu()
+    h, w = shape
+    rgb = rtg.synth_tile_host(3, 3, h, w)
+    p = rtg.default_params()
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        bufs = {}
+        for name, nbytes in (("rgb", 3 * h * w), ("mask", h * w), ("labels", 4 * h * w),
+                             ("hema", h * w), ("feats", (1 << 15) * rtg.NUM_FEATURES * 4),
+                             ("n", 4), ("tissue", h * w), ("marker", h * w), ("rec", h * w),
+                             ("fill", h * w), ("area", h * w), ("dist", 4 * h * w),
+                             ("sep", h * w), ("basin", 4 * h * w), ("lab2", 4 * h * w),
+                             ("n2", 4), ("tex", (1 << 15) * rtg.NUM_TEXTURE * 4),
+                             ("edges", h * w)):
+            bufs[name] = _guarded(nbytes)
+        v = {k: b[1] for k, b in bufs.items()}
+        v["rgb"].copy_(torch.from_numpy(rgb.reshape(-1)))
+        u8 = lambda k: v[k].view(h, w)  # noqa: E731
+        i32 = lambda k: v[k].view(torch.int32).view(h, w)  # noqa: E731
+        ctx.process_tile_dev(v["rgb"], h, w, p, v["mask"], v["labels"].view(torch.int32),
+                             v["hema"], v["feats"].view(torch.float32), v["n"].view(torch.int32))
+        ctx.colordeconv_dev(v["rgb"], h, w, p, v["hema"], v["marker"], v["tissue"])
+        ctx.recon_dev(u8("marker"), u8("hema"), h, w, 8, v["rec"])
+        ctx.fill_holes_dev(u8("mask"), h, w, v["fill"])
+        ctx.area_threshold_dev(u8("mask"), h, w, 8, p.min_area, p.max_area, v["area"])
+        ctx.edt_dev(u8("mask"), h, w, i32("dist"))
+        ctx.watershed_dev(u8("area"), h, w, p.ws_h, v["sep"], i32("basin"))
+        ctx.bwlabel_dev(u8("sep"), h, w, 8, i32("lab2"), v["n2"].view(torch.int32))
+        ctx.features_dev(i32("labels"), u8("hema"), h, w, v["n"].view(torch.int32),
+                         v["feats"].view(torch.float32))
+        ctx.texture_dev(i32("labels"), u8("hema"), h, w, v["n"].view(torch.int32),
+                        v["tex"].view(torch.float32))
+        ctx.canny_dev(u8("hema"), h, w, v["edges"])
+        ctx.sync()
+        torch.cuda.synchronize()
+        bad = [k for k, (buf, _) in bufs.items() if not _guards_intact(buf)]
+        assert not bad, f"writes outside the output buffers: {bad}"
+        ref = oracle.process_tile(rgb, p)
+        assert np.array_equal(u8("mask").cpu().numpy(), ref["mask"])
+        assert np.array_equal(i32("labels").cpu().numpy(), ref["labels"])
+
+
+def test_concurrent_runs_are_deterministic(rtg):
+    """The same two tiles on four contexts at once, five rounds, with and
+    without CUDA graphs and programmatic dependent launch: every run must be
+    bit-identical (a race in the union-find / queue / look-back kernels would
+    show up as run-to-run differences)."""
+    _need_gpu()
+    tiles = [rtg.synth_tile_host(0, 0, 2048, 2048), rtg.synth_tile_host(24, 24, 1696, 1696)]
+    p = rtg.default_params()
+    ctxs = [rtg.Context(0, 2048, 2048, 1 << 15) for _ in range(4)]
+    try:
+        d = [torch.from_numpy(t).cuda() for t in tiles]
+        torch.cuda.synchronize()
+        first = None
+        for rnd in range(5):
+            for k, cx in enumerate(ctxs):
+                cx.set_option(rtg.OPT_USE_GRAPHS, (rnd + k) % 2)
+                cx.set_option(rtg.OPT_PDL, (rnd // 2 + k) % 2)
+            outs = []
+            for k, cx in enumerate(ctxs):
+                for ti, t in enumerate(tiles):
+                    h, w = t.shape[:2]
+                    lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+                    f = torch.empty((1 << 15, rtg.NUM_FEATURES), dtype=torch.float32, device="cuda")
+                    n = torch.empty(1, dtype=torch.int32, device="cuda")
+                    cx.process_tile_dev(d[ti], h, w, p, None, lab, None, f, n)
+                    outs.append((ti, lab, f, n))
+            for cx in ctxs:
+                cx.sync()
+            got = {}
+            for ti, lab, f, n in outs:
+                nn = int(n.cpu()[0])
+                key = (lab.cpu().numpy().tobytes(), f[:nn].cpu().numpy().tobytes(), nn)
+                got.setdefault(ti, set()).add(key)
+            assert all(len(s) == 1 for s in got.values()), f"round {rnd}: runs differ"
+            if first is None:
+                first = got
+            assert got == first, f"round {rnd} differs from round 0"
+    finally:
+        for cx in ctxs:
+            cx.close()

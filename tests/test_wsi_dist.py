@@ -77,3 +77,59 @@ def test_gather_gloo(world):
     assert total == len(want0)
     assert col0 == want0
     assert col1 == want1
+
+
+def _dispense_worker(rank, world, port, q, threads):
+    import threading
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    store = dist.distributed_c10d._get_default_store()
+    disp = wsi.TileDispenser(80 * world, store, prefix="t")
+    got = {0: [], 1: []}
+    lock = threading.Lock()
+
+    def feeder(step):
+        while True:
+            g = disp.next(step)
+            if g is None:
+                return
+            with lock:
+                got[step].append(g)
+
+    for step in (0, 1):
+        th = [threading.Thread(target=feeder, args=(step,)) for _ in range(threads)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    dist.barrier()
+    q.put((rank, got[0], got[1]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("world", [2, 4])
+def test_dispenser_hands_out_every_tile_once(world):
+    """bench.py's e2e leg: feeder threads of every rank pull global tile
+    indices from one store-backed counter per step; every tile of every step
+    is processed exactly once across all ranks and threads."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dispense_worker, args=(r, world, port, q, 4))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=200) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for step in (1, 2):
+        seen = sorted(g for r in res for g in r[step])
+        assert seen == list(range(80 * world))
+
+
+def test_dispenser_local():
+    d = wsi.TileDispenser(5)
+    assert [d.next(0) for _ in range(7)] == [0, 1, 2, 3, 4, None, None]
+    assert d.next(1) == 0
