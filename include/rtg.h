@@ -228,7 +228,14 @@ enum rtg_option {
    * latency, ~5 %), 0 = plain stream order (default: with several contexts
    * sharing a GPU the waiting CTAs of early-launched kernels cost more
    * throughput than the overlap gains).  Results are identical either way. */
-  RTG_OPT_PDL = 5
+  RTG_OPT_PDL = 5,
+  /* rtg_recon_u8_dev: 0 = choose per input (default): when marker and mask
+   * hold at most 4 distinct non-zero values, one seeded union-find labelling
+   * per value (reconstruction by level decomposition; a long single
+   * wavefront, e.g. a maze, costs no more than a short one); otherwise the
+   * IWPP tile queue.  The choice reads 64 bytes back (one stream
+   * synchronisation) and is skipped under graph capture.  1 = always IWPP. */
+  RTG_OPT_RECON_ENTRY_IMPL = 6
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 
@@ -321,7 +328,7 @@ int rtg_colordeconv_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h,
                         const rtg_params* params, uint8_t* d_hema,
                         uint8_t* d_marker, uint8_t* d_tissue);
 /* o3: grayscale reconstruction by dilation (marker <= mask enforced), 4/8-conn.
- * d_out may alias d_marker. */
+ * d_out may alias d_marker.  Algorithm per RTG_OPT_RECON_ENTRY_IMPL. */
 int rtg_recon_u8_dev(rtg_ctx* ctx, const uint8_t* d_marker,
                      const uint8_t* d_mask, int64_t h, int64_t w, int conn,
                      uint8_t* d_out);

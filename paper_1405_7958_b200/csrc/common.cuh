@@ -164,6 +164,7 @@ struct rtg_ctx {
   int32_t* misc = nullptr;         // [0] n_objects, [1] flat count, [2] any_zero, [3] changed, ...
   uint32_t* status = nullptr;      // sticky status bits
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
+  uint32_t* level_bits = nullptr;  // value-presence bitmaps (rtg_recon_u8_dev)
   rtg::TileQueue tq{};
   rtg::FeatureAcc acc{};
   // texture intermediates (max_objects each): bbox, histogram, GLCM, moments
@@ -178,6 +179,7 @@ struct rtg_ctx {
   int recon_impl = 0; // 0: threshold decomposition (union-find), 1: IWPP grayscale
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
+  int recon_entry_impl = 0;  // rtg_recon_u8_dev: 0 auto (levels / IWPP), 1 IWPP
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
@@ -416,6 +418,16 @@ __device__ __forceinline__ void uf_unite_g(int32_t* par, int32_t a, int32_t b) {
 // while the ranks are assigned (the feature stage then skips k_feat_clear).
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc = nullptr);
+// Grayscale reconstruction by level decomposition (k_ccl.cu): when J and I
+// hold at most kMaxReconLevels distinct non-zero values, R is one seeded
+// labelling per value.  recon_level_count reads the values back (a stream
+// synchronisation) and sets *count = -1 when there are more.
+constexpr int kMaxReconLevels = 4;
+int recon_level_count(rtg_ctx* ctx, const uint8_t* J, const uint8_t* I, int64_t h, int64_t w,
+                      uint8_t levels[kMaxReconLevels], int* count);
+// J (clipped to I on entry) becomes recon(J, I); uses ctx->m1, m2, i32a, i32b.
+int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t w, int conn,
+                 const uint8_t* levels, int count);
 // ReconToNuclei candidates = (recon(max(H - h, 0), H) >= t) && tissue by
 // threshold decomposition: union-find components of {H >= t} holding a pixel
 // with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.

@@ -112,6 +112,20 @@ struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
   }
   __device__ __forceinline__ const uint8_t* plane() const { return v; }
 };
+struct FgCode {  // a precomputed code plane: bit 0 foreground, bit 1 seed
+  static constexpr bool kSeed = true;
+  const uint8_t* c;
+  __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool& sd) const {
+    const uint32_t a = c[i];
+    fg = a & 1u;
+    sd = (a >> 1) & 1u;
+  }
+  __device__ __forceinline__ void eval4(uint32_t a, int, int, uint32_t& fg, uint32_t& sd) const {
+    fg = byte_msbs(__vcmpne4(a & 0x01010101u, 0u));
+    sd = byte_msbs(__vcmpne4(a & 0x02020202u, 0u));
+  }
+  __device__ __forceinline__ const uint8_t* plane() const { return c; }
+};
 struct FgBackground {  // m == 0; seed: on the image border
   static constexpr bool kSeed = true;
   const uint8_t* m;
@@ -1106,6 +1120,106 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed));
   RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out));
   RTG_LAUNCH("k_seeded_and");
+  return RTG_OK;
+}
+
+// ---- grayscale reconstruction by level decomposition -------------------------
+// R = recon(J, I) (J <= I) satisfies, for every value v:
+//   R(x) >= v  <=>  x's conn-component of {I >= v} holds a pixel with J >= v,
+// and R only takes values of J or I.  So when J and I hold few distinct
+// non-zero values (binary and few-level masks: a maze, a fill-holes style
+// complement, a quantised map), R is a handful of seeded labellings, one per
+// value, highest first - no wavefront, however long the propagation path.
+// (The stage's ReconToNuclei uses the one-threshold case, recon_threshold_uf.)
+namespace {
+
+// Presence bitmaps of the non-zero values of I (words 0-7) and J (8-15).
+__global__ void k_level_presence(const uint8_t* __restrict__ I, const uint8_t* __restrict__ J,
+                                 int64_t n, uint32_t* __restrict__ bits) {
+  __shared__ uint32_t s[16];
+  if (threadIdx.x < 16) s[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = I[i], b = J[i];
+    // test before setting: each value costs one shared atomic per block
+    if (a && !(s[a >> 5] & (1u << (a & 31)))) atomicOr(&s[a >> 5], 1u << (a & 31));
+    if (b && !(s[8 + (b >> 5)] & (1u << (b & 31)))) atomicOr(&s[8 + (b >> 5)], 1u << (b & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x < 16 && s[threadIdx.x]) atomicOr(bits + threadIdx.x, s[threadIdx.x]);
+}
+
+// code = (I >= v) | (J >= v) << 1, four pixels per thread.
+__global__ void k_level_code(const uint8_t* __restrict__ I, const uint8_t* __restrict__ J,
+                             int64_t n, uint32_t v, uint8_t* __restrict__ code) {
+  const uint32_t vv = 0x01010101u * v;
+  const int64_t n4 = n / 4;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(I) + k);
+    const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(J) + k);
+    reinterpret_cast<uint32_t*>(code)[k] =
+        (__vcmpgeu4(a, vv) & 0x01010101u) | (__vcmpgeu4(b, vv) & 0x02020202u);
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    code[i] = (uint8_t)((I[i] >= v ? 1u : 0u) | (J[i] >= v ? 2u : 0u));
+}
+
+// out = max(out, v) on the foreground pixels of seeded components.
+__global__ void k_level_assign(int64_t n, const int32_t* __restrict__ roots,
+                               const int32_t* __restrict__ flag, const uint8_t* __restrict__ code,
+                               uint8_t v, uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!(code[i] & 1u)) continue;
+    const int32_t r = root_of(roots, i);
+    if (r >= 0 && flag[r] && out[i] < v) out[i] = v;
+  }
+}
+
+}  // namespace
+
+int recon_level_count(rtg_ctx* ctx, const uint8_t* J, const uint8_t* I, int64_t h, int64_t w,
+                      uint8_t levels[kMaxReconLevels], int* count) {
+  const int64_t n = h * w;
+  *count = -1;
+  RTG_CUDA(cudaMemsetAsync(ctx->level_bits, 0, 16 * sizeof(uint32_t), ctx->stream));
+  k_level_presence<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(I, J, n, ctx->level_bits);
+  RTG_LAUNCH("k_level_presence");
+  uint32_t bits[16];
+  RTG_CUDA(cudaMemcpyAsync(bits, ctx->level_bits, sizeof(bits), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  int k = 0;
+  for (int v = 255; v >= 1; --v) {
+    const bool present = ((bits[v >> 5] | bits[8 + (v >> 5)]) >> (v & 31)) & 1u;
+    if (!present) continue;
+    if (k == kMaxReconLevels) return RTG_OK;  // too many values: not this path
+    levels[k++] = (uint8_t)v;
+  }
+  *count = k;
+  return RTG_OK;
+}
+
+int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t w, int conn,
+                 const uint8_t* levels, int count) {
+  const int64_t n = h * w;
+  uint8_t* jcopy = ctx->m1;  // J is overwritten by the result
+  uint8_t* code = ctx->m2;
+  int32_t* roots = ctx->i32a;
+  int32_t* flag = ctx->i32b;
+  RTG_CUDA(cudaMemcpyAsync(jcopy, J, (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
+  RTG_CUDA(cudaMemsetAsync(J, 0, (size_t)n, ctx->stream));
+  for (int k = 0; k < count; ++k) {  // highest value first
+    k_level_code<<<grid_for(ctx, ceil_div(n, 4)), 256, 0, ctx->stream>>>(I, jcopy, n, levels[k],
+                                                                        code);
+    RTG_LAUNCH("k_level_code");
+    RTG_TRY(ccl_run(ctx, FgCode{code}, h, w, conn, roots, nullptr, flag, nullptr, false));
+    k_level_assign<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, roots, flag, code, levels[k], J);
+    RTG_LAUNCH("k_level_assign");
+  }
   return RTG_OK;
 }
 

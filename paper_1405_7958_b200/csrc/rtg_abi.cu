@@ -412,6 +412,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
         RTG_TRY(dalloc(&c->status, 1));
         RTG_TRY(dalloc(&c->stats, RTG_NUM_STATS));
+        RTG_TRY(dalloc(&c->level_bits, 16));
         const int64_t ntiles = ceil_div(max_h, kTile) * ceil_div(max_w, kTile);
         c->tq.capacity = (int32_t)(2 * ntiles);
         RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
@@ -447,7 +448,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
                   c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
                   c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
-                  c->status, c->stats, c->tq.state, c->tq.slots, c->tq.counters,
+                  c->status, c->stats, c->level_bits, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs, c->tex_bbox, c->tex_hist,
                   c->tex_glcm, c->tex_mom};
   for (void* b : bufs)
@@ -578,6 +579,10 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
       return RTG_OK;
     case RTG_OPT_PDL:
       ctx->use_pdl = value != 0;
+      return RTG_OK;
+    case RTG_OPT_RECON_ENTRY_IMPL:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "recon entry impl must be 0 or 1");
+      ctx->recon_entry_impl = (int)value;
       return RTG_OK;
     case RTG_OPT_HMAX_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "hmax impl must be 0 or 1");
@@ -805,6 +810,18 @@ int rtg_recon_u8_dev(rtg_ctx* ctx, const uint8_t* d_marker, const uint8_t* d_mas
   k_clip_copy<uint8_t><<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(d_marker, d_mask, h * w,
                                                                       d_out);
   RTG_LAUNCH("k_clip_copy");
+  // Few distinct values (a maze, a binary or quantised mask): one seeded
+  // labelling per value, immune to long propagation paths that make the
+  // wavefront engine crawl tile by tile.  The choice reads 64 bytes back, so
+  // it is skipped while the stream is being captured into a graph.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RTG_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
+  if (cap == cudaStreamCaptureStatusNone && ctx->recon_entry_impl != 1) {
+    uint8_t levels[kMaxReconLevels];
+    int count = -1;
+    RTG_TRY(recon_level_count(ctx, d_out, d_mask, h, w, levels, &count));
+    if (count >= 0) return recon_levels(ctx, d_out, d_mask, h, w, conn, levels, count);
+  }
   return iwpp_recon_u8(ctx, d_out, d_mask, h, w, conn);
 }
 

@@ -365,3 +365,51 @@ def test_concurrent_runs_are_deterministic(rtg):
     finally:
         for cx in ctxs:
             cx.close()
+
+
+# ---------------------------------------------------------------- C2 reconstruction paths
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_recon_maze_4k_level_decomposition(rtg, oracle, conn):
+    """C2's adversarial input at full size: a 1-px serpentine corridor through
+    every other row of a 4096^2 tile, one seed.  Two values -> the level
+    path (one seeded labelling); bit-exact with the oracle and the wave
+    reaches the far end."""
+    _need_gpu()
+    from synthetic_inputs import serpentine_maze
+    maze, seed = serpentine_maze(4096, 4096)
+    ref = oracle.recon(seed, maze, conn)
+    with rtg.Context(0, 4096, 4096, 1 << 12) as ctx:
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        out = torch.empty((4096, 4096), dtype=torch.uint8, device="cuda")
+        ctx.recon_dev(torch.from_numpy(seed).cuda(), torch.from_numpy(maze).cuda(), 4096, 4096,
+                      conn, out)
+        got = out.cpu().numpy()
+    assert np.array_equal(got, ref)
+    assert (got == 200).sum() == (maze > 0).sum()
+
+
+@pytest.mark.parametrize("levels", [1, 3, 4, 5, 9])
+@pytest.mark.parametrize("conn", [4, 8])
+def test_recon_few_levels_vs_iwpp(rtg, oracle, levels, conn):
+    """Quantised masks / markers with `levels` distinct non-zero values: up to
+    4 take the level-decomposition path, more the IWPP queue; both paths and
+    the forced-IWPP option are bit-exact with the oracle."""
+    _need_gpu()
+    rng = np.random.default_rng(100 * levels + conn)
+    h, w = 777, 1025
+    vals = np.sort(rng.choice(np.arange(1, 256), size=levels, replace=False)).astype(np.uint8)
+    from scipy import ndimage as ndi
+    f = ndi.gaussian_filter(rng.random((h, w)), 3)
+    q = np.digitize(f, np.quantile(f, np.linspace(0.2, 1, levels + 1)[:-1]))
+    mask = np.where(q > 0, vals[np.clip(q - 1, 0, levels - 1)], 0).astype(np.uint8)
+    marker = (mask * (rng.random((h, w)) < 0.001)).astype(np.uint8)
+    ref = oracle.recon(marker, mask, conn)
+    with rtg.Context(0, h, w, 1 << 12) as ctx:
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        d_mk, d_ms = torch.from_numpy(marker).cuda(), torch.from_numpy(mask).cuda()
+        for impl in (0, 1):
+            ctx.set_option(rtg.OPT_RECON_ENTRY_IMPL, impl)
+            out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+            ctx.recon_dev(d_mk, d_ms, h, w, conn, out)
+            assert np.array_equal(out.cpu().numpy(), ref), impl
