@@ -33,8 +33,15 @@ def ctx(rtg):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     c = rtg.Context(0, 4096, 4096, 1 << 17)
-    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    # one stream for torch's copies and the ctx's kernels (the default stream
+    # handle 0 would select the ctx's own stream, unordered with torch's)
+    s = torch.cuda.Stream()
+    prev = torch.cuda.current_stream()
+    torch.cuda.set_stream(s)
+    c.set_stream(s.cuda_stream)
     yield c
+    torch.cuda.synchronize()
+    torch.cuda.set_stream(prev)
     c.close()
 
 

@@ -288,7 +288,6 @@ def test_entry_points_write_inside_their_outputs(rtg, oracle, shape):
     rgb = rtg.synth_tile_host(3, 3, h, w)
     p = rtg.default_params()
     with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
-        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         bufs = {}
         for name, nbytes in (("rgb", 3 * h * w), ("mask", h * w), ("labels", 4 * h * w),
                              ("hema", h * w), ("feats", (1 << 15) * rtg.NUM_FEATURES * 4),
@@ -300,6 +299,7 @@ def test_entry_points_write_inside_their_outputs(rtg, oracle, shape):
             bufs[name] = _guarded(nbytes)
         v = {k: b[1] for k, b in bufs.items()}
         v["rgb"].copy_(torch.from_numpy(rgb.reshape(-1)))
+        torch.cuda.synchronize()  # the ctx's own stream does not order with torch's
         u8 = lambda k: v[k].view(h, w)  # noqa: E731
         i32 = lambda k: v[k].view(torch.int32).view(h, w)  # noqa: E731
         ctx.process_tile_dev(v["rgb"], h, w, p, v["mask"], v["labels"].view(torch.int32),
@@ -380,10 +380,11 @@ def test_recon_maze_4k_level_decomposition(rtg, oracle, conn):
     maze, seed = serpentine_maze(4096, 4096)
     ref = oracle.recon(seed, maze, conn)
     with rtg.Context(0, 4096, 4096, 1 << 12) as ctx:
-        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         out = torch.empty((4096, 4096), dtype=torch.uint8, device="cuda")
-        ctx.recon_dev(torch.from_numpy(seed).cuda(), torch.from_numpy(maze).cuda(), 4096, 4096,
-                      conn, out)
+        d_seed, d_maze = torch.from_numpy(seed).cuda(), torch.from_numpy(maze).cuda()
+        torch.cuda.synchronize()  # the ctx's own stream does not order with torch's
+        ctx.recon_dev(d_seed, d_maze, 4096, 4096, conn, out)
+        ctx.sync()
         got = out.cpu().numpy()
     assert np.array_equal(got, ref)
     assert (got == 200).sum() == (maze > 0).sum()
@@ -406,10 +407,32 @@ def test_recon_few_levels_vs_iwpp(rtg, oracle, levels, conn):
     marker = (mask * (rng.random((h, w)) < 0.001)).astype(np.uint8)
     ref = oracle.recon(marker, mask, conn)
     with rtg.Context(0, h, w, 1 << 12) as ctx:
-        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         d_mk, d_ms = torch.from_numpy(marker).cuda(), torch.from_numpy(mask).cuda()
         for impl in (0, 1):
             ctx.set_option(rtg.OPT_RECON_ENTRY_IMPL, impl)
             out = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()  # the ctx's own stream does not order with torch's
             ctx.recon_dev(d_mk, d_ms, h, w, conn, out)
+            ctx.sync()
             assert np.array_equal(out.cpu().numpy(), ref), impl
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (1696, 4096), (1000, 1333), (31, 77)])
+def test_feature_step_impls_agree(rtg, oracle, shape):
+    """Feature step 1 as a warp per 32x32 tile (default) and as the
+    foreground-run list: integer intermediates, so identical rows; both
+    within 1e-5 of the oracle."""
+    _need_gpu()
+    h, w = shape
+    rgb = rtg.synth_tile_host(6, 1, h, w)
+    p = rtg.default_params()
+    ref = oracle.process_tile(rgb, p)
+    got = []
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        for impl in (0, 1):
+            ctx.set_option(rtg.OPT_FEATURES_IMPL, impl)
+            _, labels, _, feats, n = ctx.process_tile(rgb, p)
+            assert n == ref["n"] and np.array_equal(labels, ref["labels"])
+            np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+            got.append(feats)
+    assert np.array_equal(got[0], got[1])
