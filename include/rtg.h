@@ -235,11 +235,7 @@ enum rtg_option {
    * wavefront, e.g. a maze, costs no more than a short one); otherwise the
    * IWPP tile queue.  The choice reads 64 bytes back (one stream
    * synchronisation) and is skipped under graph capture.  1 = always IWPP. */
-  RTG_OPT_RECON_ENTRY_IMPL = 6,
-  /* Feature step 1: 0 = one warp per 32x32 tile walks the tile's objects
-   * with warp reductions, one set of atomics per (object, tile) (default);
-   * 1 = the foreground-list kernel (one set per row run). */
-  RTG_OPT_FEATURES_IMPL = 7
+  RTG_OPT_RECON_ENTRY_IMPL = 6
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

@@ -180,7 +180,6 @@ struct rtg_ctx {
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
   int recon_entry_impl = 0;  // rtg_recon_u8_dev: 0 auto (levels / IWPP), 1 IWPP
-  int feat_impl = 0;  // features step 1: 0 warp per 32x32 tile, 1 run list / dense blocks
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument

@@ -337,180 +337,6 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
   }
 }
 
-// Step 1, one warp per 32x32 tile, no per-pixel atomics: the tile's labels
-// and intensities (+ 1-pixel halo) are staged in shared memory; lane r owns
-// row r.  The warp walks the tile's objects one at a time (the label of the
-// first unvisited pixel of the lowest row holding one): every lane builds the
-// 32-bit mask of that object's pixels in its row, derives the shape moments,
-// bbox and perimeter from the masks (the rows above and below by shuffles,
-// the halo at the tile edges), loops over the mask bits for the intensity
-// and Sobel sums, and the warp reduces each field once; lane j then issues
-// the global atomic of field j.  One set of atomics per (object, tile) -
-// about 40k per 4096^2 tile instead of one per row run (7.3M with the list
-// kernel).  Moments are tile-local (small integers) until the flush.
-constexpr int kFT = 32;        // tile edge
-constexpr int kLS = 35;        // staged label row stride (34 used; 35: conflict-free columns)
-constexpr int kIS8 = 36;       // staged intensity row stride in bytes
-
-struct FeatTileSmem {
-  int32_t L[kFT + 2][kLS];
-  uint8_t I[kFT + 2][kIS8];
-};
-
-__global__ void __launch_bounds__(128)
-k_feat_tiles(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I, int h, int w,
-             int tiles_x, int ntiles, const int32_t* __restrict__ d_n, FeatureAcc acc) {
-  pdl_enter();
-  __shared__ FeatTileSmem S4[4];
-  const unsigned full = 0xFFFFFFFFu;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * 4 + wid;
-  if (tile >= ntiles) return;  // warps work independently (no block barrier)
-  FeatTileSmem& S = S4[wid];
-  const int nobj = min(*d_n, acc.cap);
-  const int x0 = (tile % tiles_x) * kFT, y0 = (tile / tiles_x) * kFT;
-  auto lab = [&](int y, int x) -> int32_t {
-    if (y < 0 || y >= h || x < 0 || x >= w) return 0;
-    const int32_t l = labels[(int64_t)y * w + x];
-    return l > 0 && l <= nobj ? l : 0;
-  };
-  // 1. stage: row r of the tile is staged row r + 1, column c is c + 1
-  const int y = y0 + lane;
-  uint32_t rowbits = 0;  // this lane's labelled pixels
-  if (y < h && x0 + kFT <= w && (w & 3) == 0) {
-    const int4* src = reinterpret_cast<const int4*>(labels + (int64_t)y * w + x0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int4 v = __ldg(src + q);
-      const int32_t e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int32_t l = e[j] > 0 && e[j] <= nobj ? e[j] : 0;
-        S.L[lane + 1][4 * q + j + 1] = l;
-        rowbits |= (l ? 1u : 0u) << (4 * q + j);
-      }
-    }
-  } else {
-    for (int c = 0; c < kFT; ++c) {
-      const int32_t l = lab(y, x0 + c);
-      S.L[lane + 1][c + 1] = l;
-      rowbits |= (l ? 1u : 0u) << c;
-    }
-  }
-  if (!__any_sync(full, rowbits != 0)) return;  // no object in this tile
-  S.L[lane + 1][0] = lab(y, x0 - 1);
-  S.L[lane + 1][kFT + 1] = lab(y, x0 + kFT);
-  for (int c = lane; c < kFT + 2; c += 32) {
-    S.L[0][c] = lab(y0 - 1, x0 - 1 + c);
-    S.L[kFT + 1][c] = lab(y0 + kFT, x0 - 1 + c);
-  }
-  // intensities with the Sobel border rule (replicated edges)
-  for (int k = lane; k < (kFT + 2) * (kFT + 2); k += 32) {
-    const int r = k / (kFT + 2), c = k - r * (kFT + 2);
-    const int yy = min(max(y0 - 1 + r, 0), h - 1), xx = min(max(x0 - 1 + c, 0), w - 1);
-    S.I[r][c] = I[(int64_t)yy * w + xx];
-  }
-  __syncwarp();
-  // 2. one object at a time
-  uint32_t rem = rowbits;
-  const uint32_t yl = (uint32_t)lane;  // tile-local row
-  while (true) {
-    const unsigned has = __ballot_sync(full, rem != 0);
-    if (!has) break;
-    const int src = __ffs(has) - 1;
-    int32_t pick = 0;
-    if (lane == src) pick = S.L[lane + 1][__ffs(rem)];
-    const int32_t L = __shfl_sync(full, pick, src);
-    uint32_t m = 0;
-    for (uint32_t q = rem; q; q &= q - 1) {
-      const int c = __ffs(q) - 1;
-      if (S.L[lane + 1][c + 1] == L) m |= 1u << c;
-    }
-    rem &= ~m;
-    // masks of L in the rows above / below (tile rows by shuffle, halo rows
-    // from shared memory) and left / right of the tile
-    uint32_t up = __shfl_up_sync(full, m, 1), dn = __shfl_down_sync(full, m, 1);
-    if (lane == 0 || lane == 31) {
-      const int hr = lane == 0 ? 0 : kFT + 1;
-      uint32_t hm = 0;
-      for (int c = 0; c < kFT; ++c) hm |= (S.L[hr][c + 1] == L ? 1u : 0u) << c;
-      if (lane == 0) up = hm;
-      else dn = hm;
-    }
-    const uint32_t lb = S.L[lane + 1][0] == L ? 1u : 0u;
-    const uint32_t rb = S.L[lane + 1][kFT + 1] == L ? 0x80000000u : 0u;
-    const uint32_t n = __popc(m);
-    uint32_t per = __popc(m & ~up) + __popc(m & ~dn) + __popc(m & ~((m << 1) | lb)) +
-                   __popc(m & ~((m >> 1) | rb));
-    uint32_t sx = 0, sxx = 0, si = 0, sii = 0, sg = 0, mni = 0xFFFFFFFFu, mxi = 0;
-    unsigned long long sgg = 0;
-    for (uint32_t q = m; q; q &= q - 1) {
-      const int c = __ffs(q) - 1;
-      const uint8_t* r0 = &S.I[lane][c];
-      const uint8_t* r1 = &S.I[lane + 1][c];
-      const uint8_t* r2 = &S.I[lane + 2][c];
-      const int gx = ((int)r0[2] + 2 * (int)r1[2] + (int)r2[2]) -
-                     ((int)r0[0] + 2 * (int)r1[0] + (int)r2[0]);
-      const int gy = ((int)r2[0] + 2 * (int)r2[1] + (int)r2[2]) -
-                     ((int)r0[0] + 2 * (int)r0[1] + (int)r0[2]);
-      const uint32_t gq = isqrt_small(16u * (uint32_t)(gx * gx + gy * gy));
-      const uint32_t v = r1[1];
-      sx += (uint32_t)c;
-      sxx += (uint32_t)(c * c);
-      si += v;
-      sii += v * v;
-      sg += gq;
-      sgg += (unsigned long long)(gq * gq);
-      mni = min(mni, v);
-      mxi = max(mxi, v);
-    }
-    // 3. warp reductions (tile-local coordinates: every u32 sum fits)
-    const uint32_t tn = __reduce_add_sync(full, n);
-    const uint32_t ty = __reduce_add_sync(full, n * yl);
-    const uint32_t tyy = __reduce_add_sync(full, n * yl * yl);
-    const uint32_t tx = __reduce_add_sync(full, sx);
-    const uint32_t txx = __reduce_add_sync(full, sxx);
-    const uint32_t txy = __reduce_add_sync(full, sx * yl);
-    const uint32_t ti = __reduce_add_sync(full, si);
-    const uint32_t tii = __reduce_add_sync(full, sii);
-    const uint32_t tg = __reduce_add_sync(full, sg);
-    const uint32_t tp = __reduce_add_sync(full, per);
-    unsigned long long tgg = sgg;
-#pragma unroll
-    for (int off = 16; off; off >>= 1) tgg += __shfl_xor_sync(full, tgg, off);
-    const uint32_t tmni = __reduce_min_sync(full, mni);
-    const uint32_t tmxi = __reduce_max_sync(full, mxi);
-    const uint32_t tminy = __reduce_min_sync(full, m ? yl : 0xFFFFFFFFu);
-    const uint32_t tmaxy = __reduce_max_sync(full, m ? yl : 0u);
-    const uint32_t tminx = __reduce_min_sync(full, m ? (uint32_t)(__ffs(m) - 1) : 0xFFFFFFFFu);
-    const uint32_t tmaxx = __reduce_max_sync(full, m ? (uint32_t)(31 - __clz(m)) : 0u);
-    // 4. lane j flushes field j (global coordinates, exact u64 arithmetic)
-    const int64_t c = acc.cap, k = L - 1;
-    const unsigned long long N = tn, Y = (unsigned long long)y0, X = (unsigned long long)x0;
-    unsigned long long* Sm = acc.sums;
-    switch (lane) {
-      case 0: atomicAdd(&Sm[kSumArea * c + k], N); break;
-      case 1: atomicAdd(&Sm[kSumY * c + k], ty + N * Y); break;
-      case 2: atomicAdd(&Sm[kSumX * c + k], tx + N * X); break;
-      case 3: atomicAdd(&Sm[kSumYY * c + k], tyy + 2 * Y * ty + N * Y * Y); break;
-      case 4: atomicAdd(&Sm[kSumXX * c + k], txx + 2 * X * tx + N * X * X); break;
-      case 5: atomicAdd(&Sm[kSumXY * c + k], txy + X * ty + Y * tx + N * X * Y); break;
-      case 6: atomicAdd(&Sm[kSumI * c + k], (unsigned long long)ti); break;
-      case 7: atomicAdd(&Sm[kSumII * c + k], (unsigned long long)tii); break;
-      case 8: atomicAdd(&Sm[kSumG * c + k], (unsigned long long)tg); break;
-      case 9: atomicAdd(&Sm[kSumGG * c + k], tgg); break;
-      case 10: atomicAdd(&Sm[kSumPerim * c + k], (unsigned long long)tp); break;
-      case 11: atomicMin(&acc.mins[kMinI * c + k], (int32_t)tmni); break;
-      case 12: atomicMin(&acc.mins[kMinY * c + k], y0 + (int32_t)tminy); break;
-      case 13: atomicMin(&acc.mins[kMinX * c + k], x0 + (int32_t)tminx); break;
-      case 14: atomicMax(&acc.maxs[kMaxI * c + k], (int32_t)tmxi); break;
-      case 15: atomicMax(&acc.maxs[kMaxY * c + k], y0 + (int32_t)tmaxy); break;
-      case 16: atomicMax(&acc.maxs[kMaxX * c + k], x0 + (int32_t)tmaxx); break;
-      default: break;
-    }
-  }
-}
-
 // Step 2: one thread per object.  Expression order mirrors the oracle
 // (oracle/rtg_oracle.c orc_features) term by term.
 __global__ void k_feat_finalize(const int32_t* __restrict__ d_n, FeatureAcc acc,
@@ -582,13 +408,8 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
     RTG_CUDA(launch_k(ctx, k_feat_clear, gclear, 256, 0, d_n, ctx->acc));
     RTG_LAUNCH("k_feat_clear");
   }
-  if (ctx->feat_impl == 0) {
-    const int tiles_x = (int)ceil_div(w, kFT), ntiles = tiles_x * (int)ceil_div(h, kFT);
-    RTG_CUDA(launch_k(ctx, k_feat_tiles, (unsigned)ceil_div(ntiles, 4), 128, 0, labels, intensity,
-                      (int)h, (int)w, tiles_x, ntiles, d_n, ctx->acc));
-    RTG_LAUNCH("k_feat_tiles");
-  } else if (list && h <= 4096 && w <= 4096) {
-    // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
+  // the list kernel reduces global coordinates in 32 bits: tiles up to 4096^2
+  if (list && h <= 4096 && w <= 4096) {
     RTG_CUDA(launch_k(ctx, k_feat_list, ctx->num_sms * 8, 256, 0, list, list_count, labels, intensity,
                                                            (int)h, make_div((uint32_t)w), d_n,
                                                            ctx->acc));

@@ -415,24 +415,3 @@ def test_recon_few_levels_vs_iwpp(rtg, oracle, levels, conn):
             ctx.recon_dev(d_mk, d_ms, h, w, conn, out)
             ctx.sync()
             assert np.array_equal(out.cpu().numpy(), ref), impl
-
-
-@pytest.mark.parametrize("shape", [(4096, 4096), (1696, 4096), (1000, 1333), (31, 77)])
-def test_feature_step_impls_agree(rtg, oracle, shape):
-    """Feature step 1 as a warp per 32x32 tile (default) and as the
-    foreground-run list: integer intermediates, so identical rows; both
-    within 1e-5 of the oracle."""
-    _need_gpu()
-    h, w = shape
-    rgb = rtg.synth_tile_host(6, 1, h, w)
-    p = rtg.default_params()
-    ref = oracle.process_tile(rgb, p)
-    got = []
-    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
-        for impl in (0, 1):
-            ctx.set_option(rtg.OPT_FEATURES_IMPL, impl)
-            _, labels, _, feats, n = ctx.process_tile(rgb, p)
-            assert n == ref["n"] and np.array_equal(labels, ref["labels"])
-            np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
-            got.append(feats)
-    assert np.array_equal(got[0], got[1])
