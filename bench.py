@@ -535,9 +535,21 @@ def main():
         r, c, h, w = my_tiles[k]
         ctx.process_tile_dev(rgbs[k], h, w, params, None, None, None, feats[k], counts[k:k + 1])
     prof = ctx.profile_read()
+    # the same pass with the f4 texture columns appended to every row
+    # (params.texture = 1, 34 floats per row): its extra stage time
+    p_tex = rtg.default_params()
+    p_tex.texture = 1
+    feats_tex = torch.empty((cap, rtg.NUM_FEATURES + rtg.NUM_TEXTURE), dtype=torch.float32,
+                            device="cuda")
+    n_tex = min(T, 8)
+    for k in range(n_tex):
+        r, c, h, w = my_tiles[k]
+        ctx.process_tile_dev(rgbs[k], h, w, p_tex, None, None, None, feats_tex, counts[k:k + 1])
+    prof_tex = ctx.profile_read()
     ctx.profile(False)
+    texture_ms = {s: round(v[0] / n_tex, 4) for s, v in prof_tex.items()}
     prof_px = sum(h * w for (_, _, h, w) in my_tiles[:n_prof])
-    stage_ms = {s: v[0] for s, v in prof.items()}
+    stage_ms = {s: v[0] for s, v in prof.items() if s != "texture"}
     tot_stage = sum(stage_ms.values())
     dom = max(stage_ms, key=stage_ms.get)
     peak, peak_kind = measured_peaks()
@@ -636,6 +648,7 @@ def main():
             "roofline_streaming": roof_stream,
             "roofline_whole_stage": whole,
             "stage_ms_per_tile": {s: round(v / n_prof, 4) for s, v in stage_ms.items()},
+            "stage_ms_per_tile_with_texture": texture_ms,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_features_only": e2e_feat,

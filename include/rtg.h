@@ -88,7 +88,12 @@ typedef struct rtg_params {
   int32_t max_area;
   /* o6 PreWatershed: d = floor(4 * EDT); F = reconstruct(max(d - ws_h, 0), d). */
   int32_t ws_h;
-  int32_t reserved[7];
+  /* o9: 1 appends the RTG_NUM_TEXTURE texture columns (histogram, GLCM,
+   * Canny edge statistics, PAPER.md:343-345 / :1161-1177) to every feature
+   * row, 0 (default) gives the RTG_NUM_FEATURES shape / intensity columns.
+   * Row width: rtg_feature_columns(). */
+  int32_t texture;
+  int32_t reserved[6];
 } rtg_params;
 
 /* Per-object feature row (float32, RTG_NUM_FEATURES columns). */
@@ -149,6 +154,11 @@ enum rtg_texture_feature {
 
 /* Default parameters tuned for H&E tiles (Ruifrok-Johnston stain matrix). */
 int rtg_params_default(rtg_params* out);
+/* Floats per feature row of the stage under `params`: RTG_NUM_FEATURES, plus
+ * RTG_NUM_TEXTURE when params->texture is set (texture columns follow the
+ * shape / intensity ones).  Every stage entry point's feature table uses it. */
+#define RTG_MAX_FEATURE_COLUMNS (RTG_NUM_FEATURES + RTG_NUM_TEXTURE)
+int rtg_feature_columns(const rtg_params* params, int32_t* cols);
 
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
 int rtg_device_count(int* n);
@@ -190,7 +200,8 @@ enum rtg_stage {
   RTG_STAGE_WATERSHED = 6,   /* arrows, marker CCL, plateaus, basins (o7) */
   RTG_STAGE_LABEL = 7,       /* final CCL + canonical relabel (o8)        */
   RTG_STAGE_FEATURES = 8,    /* two-step features (o9)                    */
-  RTG_NUM_STAGES = 9
+  RTG_STAGE_TEXTURE = 9,     /* Canny + texture columns (params->texture)  */
+  RTG_NUM_STAGES = 10
 };
 int rtg_ctx_profile(rtg_ctx* ctx, int enable);
 int rtg_ctx_profile_read(rtg_ctx* ctx, double ms[RTG_NUM_STAGES],
@@ -262,8 +273,9 @@ int rtg_features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
                  int64_t h, int64_t w, int32_t n_objects, float* out);
 
 /* Segmentation + features in one call (the stage body).  features_out holds
- * max_rows rows; *n_objects receives the object count (RTG_ERR_OVERFLOW when
- * it exceeds max_rows).  mask_out / labels_out / hema_out may be NULL. */
+ * max_rows rows of rtg_feature_columns(params) floats; *n_objects receives
+ * the object count (RTG_ERR_OVERFLOW when it exceeds max_rows).  mask_out /
+ * labels_out / hema_out may be NULL. */
 int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                      int64_t pitch_bytes, const rtg_params* params,
                      uint8_t* mask_out, int32_t* labels_out, uint8_t* hema_out,
@@ -312,8 +324,9 @@ int rtg_ticket_query(rtg_ctx* ctx, uint64_t ticket, int* done);
 /* ---- whole tile, device buffers (asynchronous on the ctx stream) --------- */
 
 /* d_rgb: device RGB (pitch_bytes >= 3*w).  d_mask (u8), d_labels (i32),
- * d_hema (u8) may be NULL.  d_features: max_objects x RTG_NUM_FEATURES f32
- * (ctx capacity), d_n_objects: one device int32. */
+ * d_hema (u8) may be NULL.  d_features: max_objects x
+ * rtg_feature_columns(params) f32 (ctx capacity), d_n_objects: one device
+ * int32. */
 int rtg_process_tile_dev(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h,
                          int64_t w, int64_t pitch_bytes,
                          const rtg_params* params, uint8_t* d_mask,

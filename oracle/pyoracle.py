@@ -103,7 +103,8 @@ class Params(ctypes.Structure):
         ("min_area", ctypes.c_int32),
         ("max_area", ctypes.c_int32),
         ("ws_h", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("texture", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
     ]
 
     def as_dict(self) -> dict:
@@ -235,7 +236,8 @@ def process_tile(rgb, params=None, want_planes=False, max_rows=1 << 20):
     rgb = np.ascontiguousarray(rgb)
     mask = np.empty((h, w), np.uint8)
     labels = np.empty((h, w), np.int32)
-    feats = np.zeros((max_rows, NUM_FEATURES), np.float32)
+    cols = NUM_FEATURES + (NUM_TEXTURE if params.texture else 0)
+    feats = np.zeros((max_rows, cols), np.float32)
     arrs = {}
     planes = None
     if want_planes:

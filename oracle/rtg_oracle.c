@@ -816,11 +816,24 @@ int32_t orc_process_tile(const uint8_t* rgb, int64_t h, int64_t w,
   orc_watershed(m3, h, w, p->ws_h, m4, basin, planes);
   const int32_t nobj = orc_bwlabel(m4, h, w, 8, lab);
   if (features) {
+    /* rows of RTG_NUM_FEATURES shape / intensity columns, followed by the
+     * RTG_NUM_TEXTURE texture columns when p->texture is set */
+    const int cols = RTG_NUM_FEATURES + (p->texture ? RTG_NUM_TEXTURE : 0);
     float* tmp = (float*)malloc(sizeof(float) * RTG_NUM_FEATURES * ((size_t)nobj + 1));
+    float* tex = p->texture ? (float*)malloc(sizeof(float) * RTG_NUM_TEXTURE * ((size_t)nobj + 1))
+                            : NULL;
     orc_features(lab, hema, h, w, nobj, tmp);
+    if (tex) orc_texture(lab, hema, h, w, nobj, tex);
     const int32_t rows = nobj < max_rows ? nobj : max_rows;
-    memcpy(features, tmp, sizeof(float) * RTG_NUM_FEATURES * (size_t)rows);
+    for (int32_t k = 0; k < rows; ++k) {
+      memcpy(features + (size_t)k * cols, tmp + (size_t)k * RTG_NUM_FEATURES,
+             sizeof(float) * RTG_NUM_FEATURES);
+      if (tex)
+        memcpy(features + (size_t)k * cols + RTG_NUM_FEATURES, tex + (size_t)k * RTG_NUM_TEXTURE,
+               sizeof(float) * RTG_NUM_TEXTURE);
+    }
     free(tmp);
+    free(tex);
   }
   if (mask) memcpy(mask, m4, (size_t)n);
   if (planes) {

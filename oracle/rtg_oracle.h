@@ -85,6 +85,8 @@ void orc_texture_row(const uint32_t hist[16], const uint32_t glcm[64], const int
 void orc_canny(const uint8_t* I, int64_t h, int64_t w, int32_t low, int32_t high,
                uint8_t* edges);
 /* Full stage.  Returns object count (features written for min(n, max_rows)). */
+/* features: max_rows rows of RTG_NUM_FEATURES (+ RTG_NUM_TEXTURE when
+ * p->texture) floats. */
 int32_t orc_process_tile(const uint8_t* rgb, int64_t h, int64_t w,
                          int64_t pitch, const rtg_params* p, uint8_t* mask,
                          int32_t* labels, float* features, int32_t max_rows,

@@ -145,7 +145,9 @@ struct rtg_ctx {
   int32_t* i32b = nullptr;
   int32_t* i32c = nullptr;
   int32_t* labels = nullptr;
-  float* features = nullptr;  // max_objects x RTG_NUM_FEATURES
+  float* features = nullptr;  // max_objects x RTG_MAX_FEATURE_COLUMNS (host-entry staging)
+  float* feat20 = nullptr;    // max_objects x RTG_NUM_FEATURES (texture runs: the shape part)
+  float* tex14 = nullptr;     // max_objects x RTG_NUM_TEXTURE (texture runs: the texture part)
 
   // small scratch
   int32_t* seg_summary = nullptr;  // EDT column-segment summaries
@@ -219,11 +221,16 @@ void release_slots(rtg_ctx* c);
 int run_stage(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
               const rtg_params* p, uint8_t* d_mask, int32_t* d_labels, uint8_t* d_hema,
               float* d_features, int32_t* d_n);
-// First min(*d_n, cap) feature rows of `src` into host `dst` on `stream`:
+// First min(*d_n, cap) feature rows (`cols` floats each) of `src` into host
+// `dst` on `stream`:
 // zero-copy stores of exactly the live rows for pinned destinations, a
 // cudaMemcpyAsync of cap rows otherwise.
 int rows_to_host(rtg_ctx* ctx, cudaStream_t stream, const float* src, const int32_t* d_n,
-                 float* dst, int32_t cap);
+                 float* dst, int32_t cap, int cols);
+// Feature-row width of the stage under p (RTG_NUM_FEATURES [+ RTG_NUM_TEXTURE]).
+inline int feature_cols(const rtg_params* p) {
+  return RTG_NUM_FEATURES + (p->texture ? RTG_NUM_TEXTURE : 0);
+}
 // Stage boundary for rtg_ctx_profile (no-op unless profiling is enabled):
 // stage >= 0 starts that stage, -1 closes the current one.
 void prof_mark(rtg_ctx* ctx, int stage);

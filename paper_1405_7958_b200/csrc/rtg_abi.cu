@@ -70,6 +70,8 @@ void prof_mark(rtg_ctx* ctx, int stage) {
 namespace {
 
 int check_params_impl(const rtg_params* p) {
+  if (p && p->texture != 0 && p->texture != 1)
+    return fail(RTG_ERR_INVALID_ARG, "params.texture must be 0 or 1");
   if (!p) return fail(RTG_ERR_INVALID_ARG, "null rtg_params");
   if (p->recon_conn != 4 && p->recon_conn != 8)
     return fail(RTG_ERR_INVALID_ARG, "recon_conn must be 4 or 8");
@@ -108,6 +110,10 @@ int run_fill_holes(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w, uint8
   if (ctx->fill_impl == 1) return iwpp_fill_holes(ctx, bin, out == bin ? ctx->m2 : out, h, w, out);
   return fill_holes_uf(ctx, bin, h, w, out, out);
 }
+
+__global__ void k_rows_pack(const int32_t* __restrict__ d_n, int32_t cap,
+                            const float* __restrict__ shape, const float* __restrict__ tex,
+                            float* __restrict__ out);
 
 // The stage: o1 .. o9 on device buffers, all asynchronous on ctx->stream.
 int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t pitch,
@@ -179,8 +185,17 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // the tiled watershed left the foreground list of the area mask (a
     // superset of the labelled pixels)
     const bool sparse = ctx->ws_impl == 0;
-    RTG_TRY(features(ctx, labels, hema, h, w, n_out, d_features, sparse ? ctx->fg_list : nullptr,
+    float* shape_rows = p->texture ? ctx->feat20 : d_features;
+    RTG_TRY(features(ctx, labels, hema, h, w, n_out, shape_rows, sparse ? ctx->fg_list : nullptr,
                      sparse ? ctx->misc + 4 : nullptr, /*acc_cleared=*/true));
+    if (p->texture) {
+      // f4: Canny + histogram / co-occurrence columns appended to every row
+      prof_mark(ctx, RTG_STAGE_TEXTURE);
+      RTG_TRY(texture(ctx, labels, hema, h, w, n_out, ctx->tex14));
+      RTG_CUDA(launch_k(ctx, k_rows_pack, (unsigned)ceil_div(ctx->max_objects, 256), 256, 0,
+                        n_out, ctx->max_objects, ctx->feat20, ctx->tex14, d_features));
+      RTG_LAUNCH("k_rows_pack");
+    }
   }
   prof_mark(ctx, -1);
   return RTG_OK;
@@ -267,30 +282,48 @@ int upload_rgb(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w, int64_t p
 // Copies the first min(n, cap) feature rows (n = device object count) into
 // pinned host memory with a kernel (zero-copy stores: exactly the rows that
 // exist cross PCIe); pageable destinations get a cudaMemcpyAsync of cap rows.
-__global__ void k_rows_to_host(const float4* __restrict__ src, const int32_t* __restrict__ d_n,
-                               int32_t cap, float4* __restrict__ dst) {
+// Rows are an even number of floats (20 or 34): float2 stores.
+__global__ void k_rows_to_host(const float2* __restrict__ src, const int32_t* __restrict__ d_n,
+                               int32_t cap, int cols, float2* __restrict__ dst) {
   const int64_t rows = min(*d_n, cap);
-  const int64_t n4 = rows * (RTG_NUM_FEATURES / 4);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+  const int64_t n2 = rows * (cols / 2);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
+}
+
+// Interleaves the shape / intensity rows and the texture rows of the first
+// min(n, cap) objects into RTG_MAX_FEATURE_COLUMNS-wide rows.
+__global__ void k_rows_pack(const int32_t* __restrict__ d_n, int32_t cap,
+                            const float* __restrict__ shape, const float* __restrict__ tex,
+                            float* __restrict__ out) {
+  pdl_enter();
+  const int n = min(*d_n, cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    float* o = out + (int64_t)k * RTG_MAX_FEATURE_COLUMNS;
+#pragma unroll
+    for (int j = 0; j < RTG_NUM_FEATURES; ++j) o[j] = shape[(int64_t)k * RTG_NUM_FEATURES + j];
+#pragma unroll
+    for (int j = 0; j < RTG_NUM_TEXTURE; ++j)
+      o[RTG_NUM_FEATURES + j] = tex[(int64_t)k * RTG_NUM_TEXTURE + j];
+  }
 }
 
 }  // namespace
 
 int rows_to_host(rtg_ctx* ctx, cudaStream_t stream, const float* src, const int32_t* d_n,
-                 float* dst, int32_t cap) {
+                 float* dst, int32_t cap, int cols) {
   cudaPointerAttributes a{};
   const cudaError_t e = cudaPointerGetAttributes(&a, dst);
   if (e == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer &&
-      (reinterpret_cast<uintptr_t>(a.devicePointer) & 15) == 0) {
-    k_rows_to_host<<<64, 256, 0, stream>>>(reinterpret_cast<const float4*>(src), d_n, cap,
-                                           static_cast<float4*>(a.devicePointer));
+      (reinterpret_cast<uintptr_t>(a.devicePointer) & 7) == 0) {
+    k_rows_to_host<<<64, 256, 0, stream>>>(reinterpret_cast<const float2*>(src), d_n, cap, cols,
+                                           static_cast<float2*>(a.devicePointer));
     RTG_LAUNCH("k_rows_to_host");
     return RTG_OK;
   }
   cudaGetLastError();  // clear a failed attribute query on pageable memory
-  RTG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * RTG_NUM_FEATURES * (size_t)cap,
+  RTG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * (size_t)cols * (size_t)cap,
                            cudaMemcpyDeviceToHost, stream));
   return RTG_OK;
 }
@@ -332,6 +365,13 @@ int rtg_params_default(rtg_params* p) {
   p->min_area = 24;
   p->max_area = 2500;
   p->ws_h = 3;
+  return RTG_OK;
+}
+
+int rtg_feature_columns(const rtg_params* p, int32_t* cols) {
+  if (!p || !cols) return fail(RTG_ERR_INVALID_ARG, "null argument");
+  RTG_TRY(check_params(p));
+  *cols = feature_cols(p);
   return RTG_OK;
 }
 
@@ -395,7 +435,9 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->i32b, n));
         RTG_TRY(dalloc(&c->i32c, n));
         RTG_TRY(dalloc(&c->labels, n));
-        RTG_TRY(dalloc(&c->features, (size_t)max_objects * RTG_NUM_FEATURES));
+        RTG_TRY(dalloc(&c->features, (size_t)max_objects * RTG_MAX_FEATURE_COLUMNS));
+        RTG_TRY(dalloc(&c->feat20, (size_t)max_objects * RTG_NUM_FEATURES));
+        RTG_TRY(dalloc(&c->tex14, (size_t)max_objects * RTG_NUM_TEXTURE));
         RTG_TRY(dalloc(&c->seg_summary, (size_t)ceil_div(max_h, 32) * (size_t)max_w));
         RTG_TRY(dalloc(&c->scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
         RTG_TRY(dalloc(&c->flat_list, n));
@@ -445,7 +487,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   release_slots(c);
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
-                  c->features, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
+                  c->features, c->feat20, c->tex14, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
                   c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
                   c->status, c->stats, c->level_bits, c->tq.state, c->tq.slots, c->tq.counters,
@@ -674,7 +716,8 @@ int rtg_process_tiles(rtg_ctx* ctx, int32_t count, const uint8_t* const* rgb, in
     RTG_CUDA(cudaMemcpyAsync(ctx->h_counts + i, ctx->misc, sizeof(int32_t),
                              cudaMemcpyDeviceToHost, ctx->stream));
     if (features_out && features_out[i] && rows > 0)
-      RTG_TRY(rows_to_host(ctx, ctx->stream, ctx->features, ctx->misc, features_out[i], rows));
+      RTG_TRY(rows_to_host(ctx, ctx->stream, ctx->features, ctx->misc, features_out[i], rows,
+                           feature_cols(params)));
   }
   RTG_TRY(rtg_ctx_sync(ctx));
   int over = -1;
@@ -722,7 +765,7 @@ int rtg_process_tile(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
   const int32_t dev_rows = rows < ctx->max_objects ? rows : ctx->max_objects;
   if (features_out && dev_rows > 0)
     RTG_CUDA(cudaMemcpyAsync(features_out, ctx->features,
-                             sizeof(float) * RTG_NUM_FEATURES * (size_t)dev_rows,
+                             sizeof(float) * (size_t)feature_cols(params) * (size_t)dev_rows,
                              cudaMemcpyDeviceToHost, ctx->stream));
   RTG_TRY(rtg_ctx_sync(ctx));
   if (features_out && (n > max_rows || n > ctx->max_objects))

@@ -32,7 +32,7 @@ int ensure_slots(rtg_ctx* ctx) {
     RTG_CUDA(cudaMalloc((void**)&s[k].labels, 4 * n));
     RTG_CUDA(cudaMalloc((void**)&s[k].hema, n));
     RTG_CUDA(cudaMalloc((void**)&s[k].feats,
-                        sizeof(float) * RTG_NUM_FEATURES * (size_t)ctx->max_objects));
+                        sizeof(float) * RTG_MAX_FEATURE_COLUMNS * (size_t)ctx->max_objects));
     RTG_CUDA(cudaMalloc((void**)&s[k].d_n, sizeof(int32_t)));
     RTG_CUDA(cudaHostAlloc((void**)&s[k].h_n, sizeof(int32_t), cudaHostAllocPortable));
     RTG_CUDA(cudaEventCreateWithFlags(&s[k].up, cudaEventDisableTiming));
@@ -141,7 +141,8 @@ int rtg_process_tile_async(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t 
     RTG_CUDA(cudaMemcpyAsync(hema_out, s.hema, px, cudaMemcpyDeviceToHost, ctx->down_stream));
   const int32_t rows = max_rows < ctx->max_objects ? max_rows : ctx->max_objects;
   if (features_out && rows > 0)
-    RTG_TRY(rows_to_host(ctx, ctx->down_stream, s.feats, s.d_n, features_out, rows));
+    RTG_TRY(rows_to_host(ctx, ctx->down_stream, s.feats, s.d_n, features_out, rows,
+                         feature_cols(params)));
   RTG_CUDA(cudaEventRecord(s.down, ctx->down_stream));
   s.max_rows = features_out ? max_rows : -1;
   s.ticket = ctx->next_ticket++;

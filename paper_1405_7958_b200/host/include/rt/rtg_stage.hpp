@@ -35,7 +35,7 @@ class GpuDevice {
   rtg_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   std::int32_t max_objects() const { return max_objects_; }
-  // A pinned max_objects x RTG_NUM_FEATURES row buffer for one tile in
+  // A pinned max_objects x RTG_MAX_FEATURE_COLUMNS row buffer for one tile in
   // flight: the stage writes the n live rows straight into it (zero-copy
   // stores); it returns to the device's pool when the last holder drops it.
   std::shared_ptr<float> acquire_staging();
@@ -82,8 +82,8 @@ inline constexpr const char* kSegmentFeaturesTask = "segment_features";
 // payload), installs Mask (Dense2D u8) and Labels (Dense2D i32) into the
 // local template, enqueues upload / stage / download with
 // rtg_process_tile_async on the worker's GpuDevice and defers the rest
-// (ticket wait, Features region, Dense2D f32 n x RTG_NUM_FEATURES) to the
-// executor, which meanwhile prepares and starts the next stage.
+// (ticket wait, Features region, Dense2D f32 n x rtg_feature_columns(params))
+// to the executor, which meanwhile prepares and starts the next stage.
 void register_gpu_segmentation(VariantRegistry& reg, const SegmentationRegions& ids,
                                const rtg_params& params);
 

@@ -43,7 +43,7 @@ std::shared_ptr<float> GpuDevice::acquire_staging() {
   }
   if (!f) {
     void* p = nullptr;
-    rtg_check(rtg_host_alloc(sizeof(float) * std::size_t(max_objects_) * RTG_NUM_FEATURES, &p));
+    rtg_check(rtg_host_alloc(sizeof(float) * std::size_t(max_objects_) * RTG_MAX_FEATURE_COLUMNS, &p));
     f = static_cast<float*>(p);
     std::lock_guard<std::mutex> lk(mu_);
     all_.push_back(f);
@@ -151,6 +151,8 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
   DataRegion& labels =
       install_output(local, ids.labels, RegionKind::kDense2D, ElementKind::kI32, b2, false);
   GpuDevice* dev = wc.gpu;
+  std::int32_t cols = 0;
+  rtg_check(rtg_feature_columns(&params, &cols));
   std::shared_ptr<float> rows = dev->acquire_staging();
   std::uint64_t ticket = 0;
   rtg_check(rtg_process_tile_async(
@@ -159,15 +161,15 @@ void gpu_segment_features(const SegmentationRegions& names, const rtg_params& pa
       dev->max_objects(), &ticket));
   // the device owns the tile's buffers until the ticket is waited; `src.keep`
   // holds a viewed store piece alive for the upload
-  defer_completion([dev, ticket, rows, keep = std::move(src.keep), fid = ids.features] {
+  defer_completion([dev, ticket, rows, cols, keep = std::move(src.keep), fid = ids.features] {
     std::int32_t n = 0;
     rtg_check(rtg_ticket_wait(dev->ctx(), ticket, &n));
     if (n <= 0) return;
     RegionTemplate& tpl = *worker_context().local;
-    const BoundingBox fb({0, 0, 0}, {n - 1, RTG_NUM_FEATURES - 1, 0});
+    const BoundingBox fb({0, 0, 0}, {n - 1, cols - 1, 0});
     DataRegion& f = install_output(tpl, fid, RegionKind::kDense2D, ElementKind::kF32, fb, false);
     std::memcpy(f.find_chunk(fb)->payload.data(), rows.get(),
-                sizeof(float) * std::size_t(n) * RTG_NUM_FEATURES);
+                sizeof(float) * std::size_t(n) * std::size_t(cols));
   });
 }
 

@@ -43,7 +43,7 @@ SYMBOLS = [
     "rtg_synth_tile_host", "rtg_synth_tile_dev", "rtg_ctx_profile",
     "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
     "rtg_texture_features", "rtg_texture_features_dev", "rtg_canny_dev",
-    "rtg_process_tile_async", "rtg_ticket_wait", "rtg_ticket_query",
+    "rtg_process_tile_async", "rtg_ticket_wait", "rtg_ticket_query", "rtg_feature_columns",
 ]
 ASYNC_SLOTS = 3  # RTG_ASYNC_SLOTS
 OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
@@ -54,7 +54,7 @@ OPT_HMAX_IMPL = 4        # 0 sparse components (default), 1 IWPP tile queue
 OPT_PDL = 5              # 1 programmatic dependent launch between kernels, 0 off (default)
 OPT_RECON_ENTRY_IMPL = 6  # recon_dev: 0 levels-or-IWPP by input (default), 1 always IWPP
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
-          "label", "features"]
+          "label", "features", "texture"]
 
 
 class Error(RuntimeError):
@@ -113,7 +113,8 @@ class Params(ctypes.Structure):
         ("min_area", ctypes.c_int32),
         ("max_area", ctypes.c_int32),
         ("ws_h", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("texture", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
     ]
 
     def as_dict(self) -> dict:
@@ -177,6 +178,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_process_tile_async": [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, i32, vp],
         "rtg_ticket_wait": [vp, u64, vp],
         "rtg_ticket_query": [vp, u64, vp],
+        "rtg_feature_columns": [vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -198,6 +200,14 @@ def default_params() -> Params:
     p = Params()
     check(load().rtg_params_default(ctypes.byref(p)))
     return p
+
+
+def feature_columns(params: Optional[Params] = None) -> int:
+    """Floats per feature row under `params` (20, or 34 with texture)."""
+    params = params or default_params()
+    c = ctypes.c_int32(0)
+    check(load().rtg_feature_columns(ctypes.byref(params), ctypes.byref(c)))
+    return c.value
 
 
 def device_count() -> int:
@@ -231,13 +241,14 @@ def _rgb_tile(rgb, shape=None) -> np.ndarray:
     return np.ascontiguousarray(rgb)
 
 
-def _feature_buffer(f, max_rows: int) -> np.ndarray:
-    """A caller-supplied feature table the C side writes up to max_rows rows into."""
+def _feature_buffer(f, max_rows: int, cols: int = NUM_FEATURES) -> np.ndarray:
+    """A caller-supplied feature table the C side writes up to max_rows rows
+    of `cols` floats into."""
     if (not isinstance(f, np.ndarray) or f.dtype != np.float32 or f.ndim != 2
-            or not f.flags["C_CONTIGUOUS"] or f.shape[1] != NUM_FEATURES
+            or not f.flags["C_CONTIGUOUS"] or f.shape[1] != cols
             or f.shape[0] < max_rows):
         raise ValueError(f"feature buffer must be C-contiguous float32 (>= {max_rows}, "
-                         f"{NUM_FEATURES}), got {getattr(f, 'dtype', None)} "
+                         f"{cols}), got {getattr(f, 'dtype', None)} "
                          f"{getattr(f, 'shape', None)}")
     return f
 
@@ -328,7 +339,7 @@ class Context:
         max_rows = self.max_objects if max_rows is None else max_rows
         if max_rows < 0:
             raise ValueError("max_rows < 0")
-        feats = np.empty((max_rows, NUM_FEATURES), np.float32)
+        feats = np.empty((max_rows, feature_columns(params)), np.float32)
         n = ctypes.c_int32(0)
         check(self.lib.rtg_process_tile(self.handle, _ptr(rgb), h, w, 3 * w, ctypes.byref(params),
                                         _ptr(mask), _ptr(labels), _ptr(hema), _ptr(feats),
@@ -353,12 +364,13 @@ class Context:
         max_rows = self.max_objects if max_rows is None else max_rows
         if max_rows < 0:
             raise ValueError("max_rows < 0")
+        cols = feature_columns(params)
         if feats is None:
-            feats = [np.empty((max_rows, NUM_FEATURES), np.float32) for _ in range(k)]
+            feats = [np.empty((max_rows, cols), np.float32) for _ in range(k)]
         elif len(feats) != k:
             raise ValueError(f"{len(feats)} feature buffers for {k} tiles")
         else:
-            feats = [_feature_buffer(f, max_rows) for f in feats]
+            feats = [_feature_buffer(f, max_rows, cols) for f in feats]
         rp = (ctypes.c_void_p * k)(*[r.ctypes.data for r in rgbs])
         fp = (ctypes.c_void_p * k)(*[f.ctypes.data for f in feats])
         ns = np.zeros(k, np.int32)
@@ -389,7 +401,7 @@ class Context:
                 raise ValueError(f"output must be C-contiguous {np.dtype(dt).name} {shp}")
         max_rows = self.max_objects if max_rows is None else max_rows
         if feats is not None:
-            feats = _feature_buffer(feats, max_rows)
+            feats = _feature_buffer(feats, max_rows, feature_columns(params))
         t = ctypes.c_uint64(0)
         check(self.lib.rtg_process_tile_async(
             self.handle, rgb.ctypes.data, h, w, pitch, ctypes.byref(params), _ptr(mask),

@@ -415,3 +415,42 @@ def test_recon_few_levels_vs_iwpp(rtg, oracle, levels, conn):
             ctx.recon_dev(d_mk, d_ms, h, w, conn, out)
             ctx.sync()
             assert np.array_equal(out.cpu().numpy(), ref), impl
+
+
+# ---------------------------------------------------------------- f4 in the stage product
+
+TEX_RTOL, TEX_ATOL = 1e-5, 1e-6
+
+
+@pytest.mark.parametrize("shape,rc", [((4096, 4096), (0, 0)), ((1696, 4096), (24, 3)),
+                                      ((333, 517), (2, 2))])
+def test_stage_with_texture_columns(rtg, oracle, shape, rc):
+    """params.texture = 1: every feature row carries the 14 texture columns
+    after the 20 shape / intensity ones, through the synchronous, batch and
+    asynchronous host entry points; equal to the oracle's rows."""
+    _need_gpu()
+    h, w = shape
+    rgb = rtg.synth_tile_host(rc[0], rc[1], h, w)
+    p = rtg.default_params()
+    p.texture = 1
+    assert rtg.feature_columns(p) == rtg.NUM_FEATURES + rtg.NUM_TEXTURE
+    from oracle import pyoracle
+    op = pyoracle.default_params()
+    op.texture = 1
+    ref = oracle.process_tile(rgb, op)
+    assert ref["features"].shape[1] == 34
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        mask, labels, _, feats, n = ctx.process_tile(rgb, p)
+        assert n == ref["n"] and np.array_equal(labels, ref["labels"])
+        np.testing.assert_allclose(feats[:, :20], ref["features"][:, :20], rtol=FEAT_RTOL,
+                                   atol=FEAT_ATOL)
+        np.testing.assert_allclose(feats[:, 20:], ref["features"][:, 20:], rtol=TEX_RTOL,
+                                   atol=TEX_ATOL)
+        got, ns = ctx.process_tiles([rgb, rgb], p)
+        assert ns == [n, n] and all(np.array_equal(g, feats) for g in got)
+        f2 = np.empty((1 << 15, 34), np.float32)
+        t = ctx.process_tile_async(rgb, p, feats=f2)
+        assert ctx.wait(t) == n and np.array_equal(f2[:n], feats)
+        # the same context without texture still gives 20-column rows
+        _, _, _, f20, n20 = ctx.process_tile(rgb)
+        assert n20 == n and f20.shape[1] == 20 and np.array_equal(f20, feats[:, :20])
