@@ -588,8 +588,19 @@ def main():
             ctx.colordeconv_dev(rgbs[full[i % len(full)]], TILE, TILE, params, hema_b, None, tis_b)
         e1.record(sk)
         sk.synchronize()
-        ctx.set_stream(old_stream)
         k_ms = e0.elapsed_time(e1) / reps
+        # the same launches with the TMA bulk-copy ring variant (A/B)
+        ctx.set_option(rtg.OPT_STREAM_IMPL, 1)
+        for k in full[:3]:
+            ctx.colordeconv_dev(rgbs[k], TILE, TILE, params, hema_b, None, tis_b)
+        e0.record(sk)
+        for i in range(reps):
+            ctx.colordeconv_dev(rgbs[full[i % len(full)]], TILE, TILE, params, hema_b, None, tis_b)
+        e1.record(sk)
+        sk.synchronize()
+        tma_ms = e0.elapsed_time(e1) / reps
+        ctx.set_option(rtg.OPT_STREAM_IMPL, 0)
+        ctx.set_stream(old_stream)
         bpl = STAGE_BYTES_PER_PX["colordeconv"] * TILE * TILE
         ach = bpl / (k_ms / 1e3) / 1e9
         roof_stream.update({"achieved": round(ach, 1), "frac": round(ach / peak, 4),
@@ -597,7 +608,13 @@ def main():
                             "stage_window_ms": round(stage_ms["colordeconv"] /
                                                      max(prof["colordeconv"][1], 1), 4),
                             "timing": f"{reps} back-to-back launches over {len(full)} "
-                                      "resident 4096^2 tiles, CUDA events on the launching stream"})
+                                      "resident 4096^2 tiles, CUDA events on the launching stream",
+                            "tma_variant": {
+                                "kernel": "k_colordeconv_tma (RTG_OPT_STREAM_IMPL=1: 3-stage "
+                                          "cp.async.bulk ring, one CTA per SM)",
+                                "avg_launch_ms": round(tma_ms, 4),
+                                "achieved": round(bpl / (tma_ms / 1e3) / 1e9, 1),
+                                "frac": round(bpl / (tma_ms / 1e3) / 1e9 / peak, 4)}})
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
             tr = json.load(f)

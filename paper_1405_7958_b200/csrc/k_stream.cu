@@ -61,6 +61,70 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t v0, int32_t v1, int32_t 
   return d;
 }
 
+// 16 pixels (48 interleaved RGB bytes in wv) -> 16 hematoxylin, tissue (and
+// marker) bytes with the lane-replicated LUTs.
+template <bool kMarker>
+__device__ __forceinline__ void cd_group(const uint32_t (&wv)[12], const int32_t* l0,
+                                         const int32_t* l1, const int32_t* l2, int32_t bgt,
+                                         int32_t rg10, int32_t rb10, int32_t rh, uint4* hema,
+                                         uint4* marker, uint4* tissue, uint32_t g) {
+  uint32_t ho[4], to[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int32_t hv[4], tv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int px = 4 * k + q;
+      const int i0 = 3 * px, i1 = 3 * px + 1, i2 = 3 * px + 2;
+      const int32_t r = (int32_t)__byte_perm(wv[i0 >> 2], 0, 0x4440 | (i0 & 3));
+      const int32_t gg = (int32_t)__byte_perm(wv[i1 >> 2], 0, 0x4440 | (i1 & 3));
+      const int32_t bb = (int32_t)__byte_perm(wv[i2 >> 2], 0, 0x4440 | (i2 & 3));
+      hv[q] = (l0[r * 32] + l1[gg * 32] + l2[bb * 32]) >> 16;
+      // tissue = !(min(r,g,b) > bg) && !(10r > rg10*g && 10r > rb10*b)
+      //        = min(bg - min(r,g,b), max(rg10*g, rb10*b) - 10r) >= 0
+      const int32_t nb = bgt - min(min(r, gg), bb);
+      const int32_t nr = max(rg10 * gg, rb10 * bb) - 10 * r;
+      tv[q] = (int32_t)((~(uint32_t)(nb | nr)) >> 31);
+    }
+    ho[k] = pack_sat_u8(hv[0], hv[1], hv[2], hv[3]);
+    to[k] = pack_sat_u8(tv[0], tv[1], tv[2], tv[3]);
+  }
+  hema[g] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
+  tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
+  if (kMarker) {
+    // max(H - recon_h, 0) per byte (H in [0,255], recon_h >= 0)
+    uint32_t mo[4];
+    const uint32_t hrep = (uint32_t)(rh > 255 ? 255 : rh) * 0x01010101u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mo[k] = __vsubus4(ho[k], hrep);
+    marker[g] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
+  }
+}
+
+// The three LUTs into shared memory: lsmall [3][256] (+32768 rounding in
+// lut[0]) and the lane-replicated copy lrep [3][256][32].
+__device__ __forceinline__ void cd_stage_luts(const CdParams& p, int32_t* lrep, int32_t* lsmall) {
+  // 192 x 16-byte constant-bank reads (divergent LDC replays once per
+  // distinct address, so wide reads keep the staging short) ...
+  const int4* src = reinterpret_cast<const int4*>(&p.lut.v[0][0]);
+  int4* dst = reinterpret_cast<int4*>(lsmall);
+  for (int i = threadIdx.x; i < 192; i += blockDim.x) {
+    int4 v = src[i];
+    if (i < 64) {  // lut[0] carries the +32768 of the rounding shift
+      v.x += 32768; v.y += 32768; v.z += 32768; v.w += 32768;
+    }
+    dst[i] = v;
+  }
+  __syncthreads();
+  // ... then 32 lane copies of each entry, 16 bytes per store
+  int4* rep = reinterpret_cast<int4*>(lrep);
+  for (int i = threadIdx.x; i < 3 * 256 * 8; i += blockDim.x) {
+    const int32_t v = lsmall[i >> 3];
+    rep[i] = make_int4(v, v, v, v);
+  }
+  __syncthreads();
+}
+
 constexpr int kCdThreads = 512;
 constexpr int kCdBlocksPerSm = 2;
 constexpr size_t kCdSmem = 3 * 256 * 32 * sizeof(int32_t) + 3 * 256 * sizeof(int32_t);
@@ -88,27 +152,7 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
     b = ld_stream(rgb + 3 * g + 1);
     c = ld_stream(rgb + 3 * g + 2);
   }
-  {
-    // 192 x 16-byte constant-bank reads (divergent LDC replays once per
-    // distinct address, so wide reads keep the staging short) ...
-    const int4* src = reinterpret_cast<const int4*>(&p.lut.v[0][0]);
-    int4* dst = reinterpret_cast<int4*>(lsmall);
-    for (int i = threadIdx.x; i < 192; i += blockDim.x) {
-      int4 v = src[i];
-      if (i < 64) {  // lut[0] carries the +32768 of the rounding shift
-        v.x += 32768; v.y += 32768; v.z += 32768; v.w += 32768;
-      }
-      dst[i] = v;
-    }
-    __syncthreads();
-    // ... then 32 lane copies of each entry, 16 bytes per store
-    int4* rep = reinterpret_cast<int4*>(lrep);
-    for (int i = threadIdx.x; i < 3 * 256 * 8; i += blockDim.x) {
-      const int32_t v = lsmall[i >> 3];
-      rep[i] = make_int4(v, v, v, v);
-    }
-  }
-  __syncthreads();
+  cd_stage_luts(p, lrep, lsmall);
   const int lane = threadIdx.x & 31;
   const int32_t* l0 = lrep + lane;
   const int32_t* l1 = lrep + 256 * 32 + lane;
@@ -122,37 +166,121 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
       b = ld_stream(rgb + 3 * gn + 1);
       c = ld_stream(rgb + 3 * gn + 2);
     }
-    uint32_t ho[4], to[4];
+    cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g);
+  }
+}
+
+
+// TMA-staged variant (RTG_OPT_STREAM_IMPL = 1): one CTA per SM streams
+// chunks of 512 x 16 px (24 KB of RGB) through a 3-stage shared-memory ring
+// filled by 1-D bulk async copies (cp.async.bulk, completion on an mbarrier);
+// thread 0 refills a stage as soon as every thread has read it, so three
+// chunks are in flight per SM without any load instruction in the consumer
+// warps (their 48 bytes come from three conflict-free LDS.128).  Same
+// per-pixel arithmetic as k_colordeconv_vec (cd_group).
+constexpr int kTmaThreads = 512;
+constexpr int kTmaStages = 3;
+constexpr uint32_t kTmaChunk = kTmaThreads * 48u;  // bytes of RGB per stage
+constexpr size_t kTmaSmem = kCdSmem + kTmaStages * (size_t)kTmaChunk + kTmaStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool kMarker>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_colordeconv_tma(const uint8_t* __restrict__ rgb, uint32_t ngroups,
+                  const __grid_constant__ CdParams p, uint4* __restrict__ hema,
+                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear) {
+  pdl_enter();
+  if (blockIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int32_t hv[4], tv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int px = 4 * k + q;
-        const int i0 = 3 * px, i1 = 3 * px + 1, i2 = 3 * px + 2;
-        const int32_t r = (int32_t)__byte_perm(wv[i0 >> 2], 0, 0x4440 | (i0 & 3));
-        const int32_t gg = (int32_t)__byte_perm(wv[i1 >> 2], 0, 0x4440 | (i1 & 3));
-        const int32_t bb = (int32_t)__byte_perm(wv[i2 >> 2], 0, 0x4440 | (i2 & 3));
-        hv[q] = (l0[r * 32] + l1[gg * 32] + l2[bb * 32]) >> 16;
-        // tissue = !(min(r,g,b) > bg) && !(10r > rg10*g && 10r > rb10*b)
-        //        = min(bg - min(r,g,b), max(rg10*g, rb10*b) - 10r) >= 0
-        const int32_t nb = bgt - min(min(r, gg), bb);
-        const int32_t nr = max(rg10 * gg, rb10 * bb) - 10 * r;
-        tv[q] = (int32_t)((~(uint32_t)(nb | nr)) >> 31);
+    for (int r = 0; r < 6; ++r)
+      if (r < clear.count)
+        for (int i = threadIdx.x; i < clear.n[r]; i += blockDim.x) clear.p[r][i] = 0;
+  }
+  extern __shared__ __align__(16) int32_t cd_smem[];
+  int32_t* lrep = cd_smem;
+  int32_t* lsmall = cd_smem + 3 * 256 * 32;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(cd_smem) + kCdSmem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTmaStages * (size_t)kTmaChunk);
+  const uint32_t nchunks = (ngroups + kTmaThreads - 1) / kTmaThreads;
+  const uint64_t total = (uint64_t)ngroups * 48u;
+  auto chunk_bytes = [&](uint32_t c) -> uint32_t {
+    const uint64_t off = (uint64_t)c * kTmaChunk;
+    const uint64_t left = total - off;
+    return left < kTmaChunk ? (uint32_t)left : kTmaChunk;
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the first chunks are in flight while the LUTs are staged
+    for (int st = 0; st < kTmaStages; ++st) {
+      const uint32_t c = blockIdx.x + (uint32_t)st * gridDim.x;
+      if (c < nchunks) {
+        mbar_expect_tx(&bars[st], chunk_bytes(c));
+        bulk_load(ring + st * (size_t)kTmaChunk, rgb + (uint64_t)c * kTmaChunk, chunk_bytes(c),
+                  &bars[st]);
       }
-      ho[k] = pack_sat_u8(hv[0], hv[1], hv[2], hv[3]);
-      to[k] = pack_sat_u8(tv[0], tv[1], tv[2], tv[3]);
     }
-    hema[g] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
-    tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
-    if (kMarker) {
-      // max(H - recon_h, 0) per byte (H in [0,255], recon_h >= 0)
-      uint32_t mo[4];
-      const uint32_t hrep = (uint32_t)(rh > 255 ? 255 : rh) * 0x01010101u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mo[k] = __vsubus4(ho[k], hrep);
-      marker[g] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
+  }
+  cd_stage_luts(p, lrep, lsmall);  // ends with __syncthreads (barrier init visible)
+  const int lane = threadIdx.x & 31;
+  const int32_t* l0 = lrep + lane;
+  const int32_t* l1 = lrep + 256 * 32 + lane;
+  const int32_t* l2 = lrep + 2 * 256 * 32 + lane;
+  const int32_t bgt = p.bg, rg10 = p.rg10, rb10 = p.rb10, rh = p.recon_h;
+  uint32_t it = 0;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int st = (int)(it % kTmaStages);
+    mbar_wait(&bars[st], (it / kTmaStages) & 1u);
+    const uint32_t g = c * kTmaThreads + threadIdx.x;
+    uint32_t wv[12];
+    if (g < ngroups) {
+      const uint4* src = reinterpret_cast<const uint4*>(ring + st * (size_t)kTmaChunk) + 3 * threadIdx.x;
+      const uint4 a = src[0], b = src[1], d = src[2];
+      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
+      wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
+      wv[8] = d.x; wv[9] = d.y; wv[10] = d.z; wv[11] = d.w;
     }
+    __syncthreads();  // every thread has its bytes: the stage may be refilled
+    if (threadIdx.x == 0) {
+      const uint32_t cn = c + (uint32_t)kTmaStages * gridDim.x;
+      if (cn < nchunks) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[st], chunk_bytes(cn));
+        bulk_load(ring + st * (size_t)kTmaChunk, rgb + (uint64_t)cn * kTmaChunk, chunk_bytes(cn),
+                  &bars[st]);
+      }
+    }
+    if (g < ngroups) cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g);
   }
 }
 
@@ -267,18 +395,31 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
     if (ngroups > 0) {
       // all groups in one resident wave: iters per thread, then as few
       // blocks as cover ngroups at that depth
-      RTG_SMEM_OPTIN(k_colordeconv_vec<true>, kCdSmem);
-      RTG_SMEM_OPTIN(k_colordeconv_vec<false>, kCdSmem);
-      const int64_t slots = (int64_t)ctx->num_sms * kCdBlocksPerSm * kCdThreads;
-      const int iters = (int)ceil_div(ngroups, slots);
-      const int blocks = (int)ceil_div(ngroups, (int64_t)kCdThreads * iters);
-      auto kern = marker ? k_colordeconv_vec<true> : k_colordeconv_vec<false>;
-      RTG_CUDA(launch_k(ctx, kern, blocks, kCdThreads, kCdSmem,
-                        reinterpret_cast<const uint4*>(rgb), (uint32_t)ngroups, iters, cp,
-                        reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-                        reinterpret_cast<uint4*>(tissue), cl));
-      cl.count = 0;
-      RTG_LAUNCH("k_colordeconv_vec");
+      if (ctx->stream_impl == 1) {
+        RTG_SMEM_OPTIN(k_colordeconv_tma<true>, kTmaSmem);
+        RTG_SMEM_OPTIN(k_colordeconv_tma<false>, kTmaSmem);
+        auto kern = marker ? k_colordeconv_tma<true> : k_colordeconv_tma<false>;
+        const uint32_t nchunks = (uint32_t)ceil_div(ngroups, kTmaThreads);
+        const int blocks = (int)(nchunks < (uint32_t)ctx->num_sms ? nchunks : ctx->num_sms);
+        RTG_CUDA(launch_k(ctx, kern, blocks, kTmaThreads, kTmaSmem, rgb, (uint32_t)ngroups, cp,
+                          reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
+                          reinterpret_cast<uint4*>(tissue), cl));
+        cl.count = 0;
+        RTG_LAUNCH("k_colordeconv_tma");
+      } else {
+        RTG_SMEM_OPTIN(k_colordeconv_vec<true>, kCdSmem);
+        RTG_SMEM_OPTIN(k_colordeconv_vec<false>, kCdSmem);
+        const int64_t slots = (int64_t)ctx->num_sms * kCdBlocksPerSm * kCdThreads;
+        const int iters = (int)ceil_div(ngroups, slots);
+        const int blocks = (int)ceil_div(ngroups, (int64_t)kCdThreads * iters);
+        auto kern = marker ? k_colordeconv_vec<true> : k_colordeconv_vec<false>;
+        RTG_CUDA(launch_k(ctx, kern, blocks, kCdThreads, kCdSmem,
+                          reinterpret_cast<const uint4*>(rgb), (uint32_t)ngroups, iters, cp,
+                          reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
+                          reinterpret_cast<uint4*>(tissue), cl));
+        cl.count = 0;
+        RTG_LAUNCH("k_colordeconv_vec");
+      }
     }
     done = ngroups * 16;
   }

@@ -216,7 +216,8 @@ int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int
                               (int64_t)ctx->fill_impl, (int64_t)ctx->stream,
                               (int64_t)ctx->recon_impl | ((int64_t)ctx->ws_impl << 8) |
                                   ((int64_t)ctx->hmax_impl << 16) |
-                                  ((int64_t)ctx->use_pdl << 24)};
+                                  ((int64_t)ctx->use_pdl << 24) |
+                                  ((int64_t)ctx->stream_impl << 32)};
   std::memcpy(&key[0], fields, sizeof(fields));
   std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
   if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
@@ -621,6 +622,10 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
       return RTG_OK;
     case RTG_OPT_PDL:
       ctx->use_pdl = value != 0;
+      return RTG_OK;
+    case RTG_OPT_STREAM_IMPL:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "stream impl must be 0 or 1");
+      ctx->stream_impl = (int)value;
       return RTG_OK;
     case RTG_OPT_RECON_ENTRY_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "recon entry impl must be 0 or 1");

@@ -454,3 +454,29 @@ def test_stage_with_texture_columns(rtg, oracle, shape, rc):
         # the same context without texture still gives 20-column rows
         _, _, _, f20, n20 = ctx.process_tile(rgb)
         assert n20 == n and f20.shape[1] == 20 and np.array_equal(f20, feats[:, :20])
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (1696, 4096), (1000, 1333), (64, 48)])
+def test_colordeconv_tma_ring_matches_stream(rtg, oracle, shape):
+    """RTG_OPT_STREAM_IMPL = 1 (cp.async.bulk ring) gives the same planes as
+    the LDG.128 stream kernel and the oracle, and the same stage output."""
+    _need_gpu()
+    h, w = shape
+    rgb = rtg.synth_tile_host(8, 2, h, w)
+    p = rtg.default_params()
+    want = oracle.colordeconv(rgb, oracle.default_params())
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        d_rgb = torch.from_numpy(rgb).cuda()
+        outs = []
+        for impl in (0, 1):
+            ctx.set_option(rtg.OPT_STREAM_IMPL, impl)
+            planes = [torch.empty((h, w), dtype=torch.uint8, device="cuda") for _ in range(3)]
+            torch.cuda.synchronize()
+            ctx.colordeconv_dev(d_rgb, h, w, p, planes[0], planes[1], planes[2])
+            ctx.sync()
+            got = [t.cpu().numpy() for t in planes]
+            for g, wnt in zip(got, want):
+                assert np.array_equal(g, wnt), impl
+            outs.append(ctx.process_tile(rgb, p))
+        assert outs[0][4] == outs[1][4] and np.array_equal(outs[0][1], outs[1][1])
+        assert np.array_equal(outs[0][3], outs[1][3])
