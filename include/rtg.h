@@ -247,10 +247,10 @@ enum rtg_option {
    * IWPP tile queue.  The choice reads 64 bytes back (one stream
    * synchronisation) and is skipped under graph capture.  1 = always IWPP. */
   RTG_OPT_RECON_ENTRY_IMPL = 6,
-  /* Colour deconvolution (o1+o2): 0 = 128-bit streaming loads with register
-   * prefetch, two 512-thread CTAs per SM (default); 1 = one CTA per SM fed by
-   * a 3-stage ring of 24 KB bulk async copies (TMA, cp.async.bulk + mbarrier).
-   * Identical results. */
+  /* Colour deconvolution (o1+o2): 1 = one CTA per SM fed by a 4-stage ring
+   * of 24 KB bulk async copies (TMA, cp.async.bulk + mbarrier) (default);
+   * 0 = 128-bit streaming loads with register prefetch, two 512-thread CTAs
+   * per SM.  Identical results. */
   RTG_OPT_STREAM_IMPL = 7
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);

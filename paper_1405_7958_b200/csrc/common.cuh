@@ -182,7 +182,7 @@ struct rtg_ctx {
   int ws_impl = 0;    // 0: tiled whole-tile watershed, 1: object-parallel
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
   int recon_entry_impl = 0;  // rtg_recon_u8_dev: 0 auto (levels / IWPP), 1 IWPP
-  int stream_impl = 0;  // colour deconvolution: 0 LDG.128 stream, 1 TMA bulk-copy ring
+  int stream_impl = 1;  // colour deconvolution: 1 TMA bulk-copy ring (default), 0 LDG.128 stream
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument

@@ -172,14 +172,14 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
 
 
 // TMA-staged variant (RTG_OPT_STREAM_IMPL = 1): one CTA per SM streams
-// chunks of 512 x 16 px (24 KB of RGB) through a 3-stage shared-memory ring
+// chunks of 512 x 16 px (24 KB of RGB) through a 4-stage shared-memory ring
 // filled by 1-D bulk async copies (cp.async.bulk, completion on an mbarrier);
-// thread 0 refills a stage as soon as every thread has read it, so three
+// thread 0 refills a stage as soon as every thread has read it, so four
 // chunks are in flight per SM without any load instruction in the consumer
 // warps (their 48 bytes come from three conflict-free LDS.128).  Same
 // per-pixel arithmetic as k_colordeconv_vec (cd_group).
 constexpr int kTmaThreads = 512;
-constexpr int kTmaStages = 3;
+constexpr int kTmaStages = 4;
 constexpr uint32_t kTmaChunk = kTmaThreads * 48u;  // bytes of RGB per stage
 constexpr size_t kTmaSmem = kCdSmem + kTmaStages * (size_t)kTmaChunk + kTmaStages * 8;
 

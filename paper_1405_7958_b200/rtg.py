@@ -53,7 +53,7 @@ OPT_WATERSHED_IMPL = 3   # 0 tiled whole-tile passes (default), 1 object-paralle
 OPT_HMAX_IMPL = 4        # 0 sparse components (default), 1 IWPP tile queue
 OPT_PDL = 5              # 1 programmatic dependent launch between kernels, 0 off (default)
 OPT_RECON_ENTRY_IMPL = 6  # recon_dev: 0 levels-or-IWPP by input (default), 1 always IWPP
-OPT_STREAM_IMPL = 7       # colour deconvolution: 0 LDG.128 stream (default), 1 TMA bulk ring
+OPT_STREAM_IMPL = 7       # colour deconvolution: 1 TMA bulk ring (default), 0 LDG.128 stream
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features", "texture"]
 

@@ -15,7 +15,7 @@ import re
 import sys
 
 STARTS = [  # (stage, first kernel of the stage, kernel that must precede it)
-    ("colordeconv", "k_colordeconv_vec", None),
+    ("colordeconv", "k_colordeconv_tma", None),
     ("recon", "k_ccl_tile", None),
     ("fill_holes", "k_ccl_tile_fb", None),
     ("area", "k_fb_tree", None),
@@ -45,7 +45,7 @@ def load(path):
 
 def split_stages(launches):
     """Assigns the LAST complete pipeline pass of the list to stages."""
-    starts = [i for i, l in enumerate(launches) if l["name"] == "k_colordeconv_vec"]
+    starts = [i for i, l in enumerate(launches) if l["name"].startswith("k_colordeconv")]
     seq = launches[starts[-1]:] if starts else launches
     out, si, seen = [], -1, set()
     for l in seq:
