@@ -494,9 +494,11 @@ int features(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity,
 // f4 Canny edges (u8 0/1) of an intensity plane; uses i32a/i32b and m1/m2.
 int canny(rtg_ctx* ctx, const uint8_t* intensity, int64_t h, int64_t w, int32_t low, int32_t high,
           uint8_t* edges);
-// f4 texture table for labels 1..*d_n (out: n x RTG_NUM_TEXTURE).
+// f4 texture table for labels 1..*d_n (out: n x RTG_NUM_TEXTURE).  boxes:
+// the feature stage's accumulators (their min / max y, x are the objects'
+// bounding boxes), or null to reduce the boxes here.
 int texture(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
-            const int32_t* d_n, float* out);
+            const int32_t* d_n, float* out, const FeatureAcc* boxes = nullptr);
 
 int synth_dev(rtg_ctx* ctx, uint64_t global_seed, int64_t tile_row,
               int64_t tile_col, int64_t h, int64_t w, uint8_t* d_rgb);

@@ -59,13 +59,23 @@ k_tex_bbox(const int32_t* __restrict__ labels, int h, int w, const int32_t* __re
     }
 }
 
-// Step 1: one warp per object over its bounding box.
+// Where the bounding boxes come from: the packed boxes of k_tex_bbox
+// (stride 4) or the feature stage's per-object accumulators (stride 1, SoA).
+struct TexBoxes {
+  const int32_t *y0, *x0, *y1, *x1;
+  int stride;
+};
+
+// Step 1: one warp per object over its bounding box; the 32 lanes walk the
+// box's pixels in raster order (lane + 32 i), so narrow boxes keep every lane
+// busy.
 __global__ void __launch_bounds__(256)
 k_tex_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
             const uint8_t* __restrict__ E, int h, int w,
-            const int32_t* __restrict__ d_n, int32_t cap, const int32_t* __restrict__ bb,
+            const int32_t* __restrict__ d_n, int32_t cap, TexBoxes bb,
             uint32_t* __restrict__ hist_out, uint32_t* __restrict__ glcm_out,
             unsigned long long* __restrict__ mom_out) {
+  pdl_enter();
   __shared__ uint32_t s_hist[8][17];  // 16 bins + Canny edge pixels
   __shared__ uint32_t s_glcm[8][64];
   const int nobj = min(*d_n, cap);
@@ -78,14 +88,17 @@ k_tex_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
     glcm[lane] = 0;
     glcm[lane + 32] = 0;
     __syncwarp();
-    const int32_t y0 = bb[4 * k], x0 = bb[4 * k + 1], y1 = bb[4 * k + 2], x1 = bb[4 * k + 3];
+    const int64_t kb = (int64_t)k * bb.stride;
+    const int32_t y0 = bb.y0[kb], x0 = bb.x0[kb], y1 = bb.y1[kb], x1 = bb.x1[kb];
     const int32_t l = k + 1;
     unsigned long long m1 = 0, m2 = 0, m3 = 0, m4 = 0;
-    if (y1 >= 0) {
-      for (int y = y0; y <= y1; ++y) {
+    if (y1 >= 0 && x1 >= x0) {
+      const int bw = x1 - x0 + 1;
+      const int sdy = 32 / bw, sdx = 32 - sdy * bw;  // one step of 32 pixels
+      int y = y0 + lane / bw, x = x0 + lane % bw;
+      for (; y <= y1;) {
         const int64_t rb = (int64_t)y * w;
-        for (int x = x0 + lane; x <= x1; x += 32) {
-          if (labels[rb + x] != l) continue;
+        if (labels[rb + x] == l) {
           const uint32_t v = I[rb + x];
           atomicAdd(&hist[v >> 4], 1u);
           if (E[rb + x]) atomicAdd(&hist[16], 1u);
@@ -95,30 +108,26 @@ k_tex_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
           m3 += v2 * v;
           m4 += v2 * v2;
           const uint32_t q = v >> 5;
-          // forward offsets: right, down, down-right, down-left
-          if (x + 1 < w && labels[rb + x + 1] == l) {
-            const uint32_t q2 = I[rb + x + 1] >> 5;
+          auto pair = [&](int64_t j) {
+            if (labels[j] != l) return;
+            const uint32_t q2 = I[j] >> 5;
             atomicAdd(&glcm[q * 8 + q2], 1u);
             atomicAdd(&glcm[q2 * 8 + q], 1u);
-          }
+          };
+          // forward offsets: right, down, down-right, down-left
+          if (x + 1 < w) pair(rb + x + 1);
           if (y + 1 < h) {
             const int64_t nb = rb + w;
-            if (labels[nb + x] == l) {
-              const uint32_t q2 = I[nb + x] >> 5;
-              atomicAdd(&glcm[q * 8 + q2], 1u);
-              atomicAdd(&glcm[q2 * 8 + q], 1u);
-            }
-            if (x + 1 < w && labels[nb + x + 1] == l) {
-              const uint32_t q2 = I[nb + x + 1] >> 5;
-              atomicAdd(&glcm[q * 8 + q2], 1u);
-              atomicAdd(&glcm[q2 * 8 + q], 1u);
-            }
-            if (x > 0 && labels[nb + x - 1] == l) {
-              const uint32_t q2 = I[nb + x - 1] >> 5;
-              atomicAdd(&glcm[q * 8 + q2], 1u);
-              atomicAdd(&glcm[q2 * 8 + q], 1u);
-            }
+            pair(nb + x);
+            if (x + 1 < w) pair(nb + x + 1);
+            if (x > 0) pair(nb + x - 1);
           }
+        }
+        x += sdx;
+        y += sdy;
+        if (x > x1) {
+          x -= bw;
+          ++y;
         }
       }
     }
@@ -143,54 +152,67 @@ k_tex_accum(const int32_t* __restrict__ labels, const uint8_t* __restrict__ I,
   }
 }
 
-// Step 2: one thread per object; term order of orc_texture_row.
-__global__ void k_tex_finalize(const int32_t* __restrict__ d_n, int32_t cap,
-                               const uint32_t* __restrict__ hist_in,
-                               const uint32_t* __restrict__ glcm_in,
-                               const unsigned long long* __restrict__ mom_in,
-                               float* __restrict__ out) {
+// Step 2: one warp per object (one thread per object left most of the GPU
+// idle on the fp64 log2 chains): lanes 0-15 take a histogram bin, every lane
+// two co-occurrence cells; fp64 warp sums.  The terms are orc_texture_row's;
+// only the summation order differs (fp64, far inside the 1e-5 bar).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+k_tex_finalize(const int32_t* __restrict__ d_n, int32_t cap,
+               const uint32_t* __restrict__ hist_in, const uint32_t* __restrict__ glcm_in,
+               const unsigned long long* __restrict__ mom_in, float* __restrict__ out) {
+  pdl_enter();
   const int n = min(*d_n, cap);
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n; k += warps) {
     const uint32_t* hist = hist_in + (int64_t)k * 17;
     const uint32_t* glcm = glcm_in + (int64_t)k * 64;
     const unsigned long long* mom = mom_in + 4 * (int64_t)k;
     float* o = out + (int64_t)k * RTG_NUM_TEXTURE;
-    for (int j = 0; j < RTG_NUM_TEXTURE; ++j) o[j] = 0.f;
-    long long nn = 0;
-    for (int b = 0; b < 16; ++b) nn += hist[b];
+    const uint32_t hb = lane < 16 ? hist[lane] : 0u;
+    const uint32_t edge = hist[16];
+    const uint32_t c0 = glcm[lane], c1 = glcm[lane + 32];
+    const long long nn = (long long)__reduce_add_sync(0xFFFFFFFFu, hb);
+    if (lane < RTG_NUM_TEXTURE) o[lane] = 0.f;
     if (nn == 0) continue;
     const double N = (double)nn;
     double hent = 0.0, hen = 0.0;
-    for (int b = 0; b < 16; ++b) {
-      if (!hist[b]) continue;
-      const double p = (double)hist[b] / N;
-      hent -= p * log2(p);
-      hen += p * p;
+    if (hb) {
+      const double p = (double)hb / N;
+      hent = -p * log2(p);
+      hen = p * p;
     }
+    hent = warp_sum(hent);
+    hen = warp_sum(hen);
+    const long long tt = (long long)__reduce_add_sync(0xFFFFFFFFu, c0 + c1);
+    double fl[RTG_NUM_TEXTURE] = {};
+    fl[RTG_T_HIST_ENTROPY] = hent;
+    fl[RTG_T_HIST_ENERGY] = hen;
     const double mu = (double)(long long)mom[0] / N, e2 = (double)(long long)mom[1] / N;
     const double e3 = (double)(long long)mom[2] / N, e4 = (double)(long long)mom[3] / N;
     const double var = e2 - mu * mu;
-    double skew = 0.0, kurt = 0.0;
     if (var > 0.0) {
       const double sd = sqrt(var);
-      skew = (e3 - 3.0 * mu * e2 + 2.0 * mu * mu * mu) / (var * sd);
-      kurt = (e4 - 4.0 * mu * e3 + 6.0 * mu * mu * e2 - 3.0 * mu * mu * mu * mu) / (var * var) - 3.0;
+      fl[RTG_T_SKEWNESS] = (e3 - 3.0 * mu * e2 + 2.0 * mu * mu * mu) / (var * sd);
+      fl[RTG_T_KURTOSIS] =
+          (e4 - 4.0 * mu * e3 + 6.0 * mu * mu * e2 - 3.0 * mu * mu * mu * mu) / (var * var) - 3.0;
     }
-    o[RTG_T_HIST_ENTROPY] = (float)hent;
-    o[RTG_T_HIST_ENERGY] = (float)hen;
-    o[RTG_T_SKEWNESS] = (float)skew;
-    o[RTG_T_KURTOSIS] = (float)kurt;
-    o[RTG_T_EDGE_PIXELS] = (float)hist[16];
-    o[RTG_T_EDGE_DENSITY] = (float)((double)hist[16] / N);
-    long long tt = 0;
-    for (int j = 0; j < 64; ++j) tt += glcm[j];
-    if (tt == 0) continue;
-    const double T = (double)tt;
-    double asm_ = 0.0, con = 0.0, hom = 0.0, ent = 0.0, mui = 0.0, dis = 0.0, mx = 0.0;
-    for (int i = 0; i < 8; ++i) {
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t c = glcm[i * 8 + j];
+    fl[RTG_T_EDGE_PIXELS] = (double)edge;
+    fl[RTG_T_EDGE_DENSITY] = (double)edge / N;
+    if (tt > 0) {
+      const double T = (double)tt;
+      double asm_ = 0.0, con = 0.0, hom = 0.0, ent = 0.0, mui = 0.0, dis = 0.0, mx = 0.0;
+      for (int half = 0; half < 2; ++half) {
+        const int cell = lane + 32 * half;
+        const uint32_t c = half ? c1 : c0;
         if (!c) continue;
+        const int i = cell >> 3, j = cell & 7;
         const double P = (double)c / T;
         const int d = i - j;
         asm_ += P * P;
@@ -201,12 +223,20 @@ __global__ void k_tex_finalize(const int32_t* __restrict__ d_n, int32_t cap,
         dis += (double)(d < 0 ? -d : d) * P;
         if (P > mx) mx = P;
       }
-    }
-    double vari = 0.0, sij = 0.0, shade = 0.0;
-    for (int i = 0; i < 8; ++i) {
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t c = glcm[i * 8 + j];
+      asm_ = warp_sum(asm_);
+      con = warp_sum(con);
+      hom = warp_sum(hom);
+      ent = warp_sum(ent);
+      mui = warp_sum(mui);
+      dis = warp_sum(dis);
+#pragma unroll
+      for (int of = 16; of > 0; of >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, of));
+      double vari = 0.0, sij = 0.0, shade = 0.0;
+      for (int half = 0; half < 2; ++half) {
+        const int cell = lane + 32 * half;
+        const uint32_t c = half ? c1 : c0;
         if (!c) continue;
+        const int i = cell >> 3, j = cell & 7;
         const double P = (double)c / T;
         const double di = (double)i - mui;
         const double t = (double)(i + j) - 2.0 * mui;
@@ -214,15 +244,22 @@ __global__ void k_tex_finalize(const int32_t* __restrict__ d_n, int32_t cap,
         sij += (double)(i * j) * P;
         shade += t * t * t * P;
       }
+      vari = warp_sum(vari);
+      sij = warp_sum(sij);
+      shade = warp_sum(shade);
+      fl[RTG_T_GLCM_ASM] = asm_;
+      fl[RTG_T_GLCM_CONTRAST] = con;
+      fl[RTG_T_GLCM_HOMOGENEITY] = hom;
+      fl[RTG_T_GLCM_ENTROPY] = ent;
+      fl[RTG_T_GLCM_CORRELATION] = vari > 0.0 ? (sij - mui * mui) / vari : 0.0;
+      fl[RTG_T_GLCM_DISSIMILARITY] = dis;
+      fl[RTG_T_GLCM_MAX_PROB] = mx;
+      fl[RTG_T_GLCM_CLUSTER_SHADE] = shade;
     }
-    o[RTG_T_GLCM_ASM] = (float)asm_;
-    o[RTG_T_GLCM_CONTRAST] = (float)con;
-    o[RTG_T_GLCM_HOMOGENEITY] = (float)hom;
-    o[RTG_T_GLCM_ENTROPY] = (float)ent;
-    o[RTG_T_GLCM_CORRELATION] = (float)(vari > 0.0 ? (sij - mui * mui) / vari : 0.0);
-    o[RTG_T_GLCM_DISSIMILARITY] = (float)dis;
-    o[RTG_T_GLCM_MAX_PROB] = (float)mx;
-    o[RTG_T_GLCM_CLUSTER_SHADE] = (float)shade;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < RTG_NUM_TEXTURE; ++j)
+      if (lane == j) o[j] = (float)fl[j];
   }
 }
 
@@ -237,44 +274,64 @@ __global__ void k_tex_finalize(const int32_t* __restrict__ d_n, int32_t cap,
 __global__ void __launch_bounds__(256)
 k_canny_nms(const uint8_t* __restrict__ I, int h, int w, int32_t lo2, int32_t hi2,
             uint8_t* __restrict__ cls) {
+  pdl_enter();
   __shared__ uint8_t sI[40][41];
+  __shared__ uint16_t sH[40][37];  // horizontal 5-tap sums, 36 columns
   __shared__ uint8_t sS[36][37];
   __shared__ int32_t sM[34][34];
   __shared__ int32_t sG[34][34];  // gx (high 16) | gy (low 16), tile + 1 ring
   const int y0 = blockIdx.y * 32, x0 = blockIdx.x * 32;
   const int tid = threadIdx.x;
+  // stage: 40 rows of 40 clamped bytes, one row per 8 threads
   for (int k = tid; k < 40 * 40; k += 256) {
     const int yy = k / 40, xx = k - yy * 40;
     const int y = min(max(y0 - 4 + yy, 0), h - 1), x = min(max(x0 - 4 + xx, 0), w - 1);
     sI[yy][xx] = I[(int64_t)y * w + x];
   }
   __syncthreads();
-  const int K[5] = {1, 4, 6, 4, 1};
+  // separable 5x5 binomial: (1 4 6 4 1) across, then down
+  for (int k = tid; k < 40 * 36; k += 256) {
+    const int yy = k / 36, xx = k - yy * 36;
+    const uint8_t* r = &sI[yy][xx];
+    sH[yy][xx] = (uint16_t)(r[0] + 4 * r[1] + 6 * r[2] + 4 * r[3] + r[4]);
+  }
+  __syncthreads();
   for (int k = tid; k < 36 * 36; k += 256) {
-    const int yy = k / 36, xx = k - yy * 36;  // global (y0 - 2 + yy, x0 - 2 + xx)
-    int32_t acc = 0;
-#pragma unroll
-    for (int dy = 0; dy < 5; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < 5; ++dx) acc += K[dy] * K[dx] * sI[yy + dy][xx + dx];
+    const int yy = k / 36, xx = k - yy * 36;
+    const int32_t acc = sH[yy][xx] + 4 * sH[yy + 1][xx] + 6 * sH[yy + 2][xx] +
+                        4 * sH[yy + 3][xx] + sH[yy + 4][xx];
     sS[yy][xx] = (uint8_t)((acc + 128) >> 8);
   }
   __syncthreads();
-  // smoothed value at a clamped global position (inside the staged window)
-  auto S = [&](int y, int x) -> int32_t {
-    y = min(max(y, 0), h - 1);
-    x = min(max(x, 0), w - 1);
-    return sS[y - (y0 - 2)][x - (x0 - 2)];
-  };
+  // Sobel reads the smoothed value at the CLAMPED position: at the image
+  // border, copy the in-image entries over the outside ones (rows first,
+  // then columns) so the Sobel below reads the window directly
+  const bool edge_tile = y0 < 2 || x0 < 2 || y0 + 34 > h || x0 + 34 > w;
+  if (edge_tile) {
+    for (int k = tid; k < 36 * 36; k += 256) {
+      const int yy = k / 36, xx = k - yy * 36;
+      const int y = y0 - 2 + yy, yc = min(max(y, 0), h - 1);
+      if (yc != y) sS[yy][xx] = sS[yc - (y0 - 2)][xx];
+    }
+    __syncthreads();
+    for (int k = tid; k < 36 * 36; k += 256) {
+      const int yy = k / 36, xx = k - yy * 36;
+      const int x = x0 - 2 + xx, xc = min(max(x, 0), w - 1);
+      if (xc != x) sS[yy][xx] = sS[yy][xc - (x0 - 2)];
+    }
+    __syncthreads();
+  }
   for (int k = tid; k < 34 * 34; k += 256) {
     const int yy = k / 34, xx = k - yy * 34;
     const int y = y0 - 1 + yy, x = x0 - 1 + xx;
     int32_t m = 0, g = 0;
     if (y >= 0 && y < h && x >= 0 && x < w) {
-      const int32_t gx = (S(y - 1, x + 1) + 2 * S(y, x + 1) + S(y + 1, x + 1)) -
-                         (S(y - 1, x - 1) + 2 * S(y, x - 1) + S(y + 1, x - 1));
-      const int32_t gy = (S(y + 1, x - 1) + 2 * S(y + 1, x) + S(y + 1, x + 1)) -
-                         (S(y - 1, x - 1) + 2 * S(y - 1, x) + S(y - 1, x + 1));
+      // window row yy .. yy + 2, column xx .. xx + 2 (sS origin is y0 - 2, x0 - 2)
+      const uint8_t* a = &sS[yy][xx];
+      const uint8_t* b = &sS[yy + 1][xx];
+      const uint8_t* c = &sS[yy + 2][xx];
+      const int32_t gx = (a[2] + 2 * b[2] + c[2]) - (a[0] + 2 * b[0] + c[0]);
+      const int32_t gy = (c[0] + 2 * c[1] + c[2]) - (a[0] + 2 * a[1] + a[2]);
       m = gx * gx + gy * gy;
       g = (int32_t)((uint32_t)(gx & 0xFFFF) << 16 | (uint32_t)(gy & 0xFFFF));
     }
@@ -308,32 +365,38 @@ int canny(rtg_ctx* ctx, const uint8_t* intensity, int64_t h, int64_t w, int32_t 
           uint8_t* edges) {
   uint8_t* cls = ctx->m1 == edges ? ctx->m2 : ctx->m1;
   const dim3 tiles((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32));
-  k_canny_nms<<<tiles, 256, 0, ctx->stream>>>(intensity, (int)h, (int)w, low * low, high * high,
-                                              cls);
+  RTG_CUDA(launch_k(ctx, k_canny_nms, tiles, 256, 0, intensity, (int)h, (int)w, low * low,
+                    high * high, cls));
   RTG_LAUNCH("k_canny_nms");
   // hysteresis: weak (1) pixels 8-connected to a strong (2) one
   return recon_threshold_uf(ctx, cls, cls, h, w, 1, 1, 8, nullptr, edges);
 }
 
 int texture(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
-            const int32_t* d_n, float* out) {
+            const int32_t* d_n, float* out, const FeatureAcc* boxes) {
   uint8_t* edges = ctx->m3;
   RTG_TRY(canny(ctx, intensity, h, w, RTG_CANNY_LOW, RTG_CANNY_HIGH, edges));
   const int32_t cap = ctx->max_objects;
   const int g = (int)ceil_div(cap, 256);
-  k_tex_clear<<<g, 256, 0, ctx->stream>>>(d_n, cap, ctx->tex_bbox, ctx->tex_hist, ctx->tex_glcm,
-                                          ctx->tex_mom);
-  RTG_LAUNCH("k_tex_clear");
-  const dim3 gb((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
-  k_tex_bbox<<<gb, 256, 0, ctx->stream>>>(labels, (int)h, (int)w, d_n, cap, ctx->tex_bbox);
-  RTG_LAUNCH("k_tex_bbox");
-  k_tex_accum<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(labels, intensity, edges, (int)h,
-                                                         (int)w, d_n, cap, ctx->tex_bbox,
-                                                         ctx->tex_hist, ctx->tex_glcm,
-                                                         ctx->tex_mom);
+  TexBoxes bb{ctx->tex_bbox + 0, ctx->tex_bbox + 1, ctx->tex_bbox + 2, ctx->tex_bbox + 3, 4};
+  if (boxes) {
+    // the feature stage already reduced every object's bounding box
+    const int64_t c = boxes->cap;
+    bb = TexBoxes{boxes->mins + kMinY * c, boxes->mins + kMinX * c, boxes->maxs + kMaxY * c,
+                  boxes->maxs + kMaxX * c, 1};
+  } else {
+    k_tex_clear<<<g, 256, 0, ctx->stream>>>(d_n, cap, ctx->tex_bbox, ctx->tex_hist,
+                                            ctx->tex_glcm, ctx->tex_mom);
+    RTG_LAUNCH("k_tex_clear");
+    const dim3 gb((unsigned)ceil_div(w, 256), (unsigned)(h < 1024 ? h : 1024));
+    k_tex_bbox<<<gb, 256, 0, ctx->stream>>>(labels, (int)h, (int)w, d_n, cap, ctx->tex_bbox);
+    RTG_LAUNCH("k_tex_bbox");
+  }
+  RTG_CUDA(launch_k(ctx, k_tex_accum, ctx->num_sms * 8, 256, 0, labels, intensity, edges, (int)h,
+                    (int)w, d_n, cap, bb, ctx->tex_hist, ctx->tex_glcm, ctx->tex_mom));
   RTG_LAUNCH("k_tex_accum");
-  k_tex_finalize<<<g, 256, 0, ctx->stream>>>(d_n, cap, ctx->tex_hist, ctx->tex_glcm, ctx->tex_mom,
-                                             out);
+  RTG_CUDA(launch_k(ctx, k_tex_finalize, (unsigned)ceil_div(cap, 8), 256, 0, d_n, cap,
+                    ctx->tex_hist, ctx->tex_glcm, ctx->tex_mom, out));
   RTG_LAUNCH("k_tex_finalize");
   return RTG_OK;
 }

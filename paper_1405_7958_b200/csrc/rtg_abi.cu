@@ -191,7 +191,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     if (p->texture) {
       // f4: Canny + histogram / co-occurrence columns appended to every row
       prof_mark(ctx, RTG_STAGE_TEXTURE);
-      RTG_TRY(texture(ctx, labels, hema, h, w, n_out, ctx->tex14));
+      RTG_TRY(texture(ctx, labels, hema, h, w, n_out, ctx->tex14, &ctx->acc));
       RTG_CUDA(launch_k(ctx, k_rows_pack, (unsigned)ceil_div(ctx->max_objects, 256), 256, 0,
                         n_out, ctx->max_objects, ctx->feat20, ctx->tex14, d_features));
       RTG_LAUNCH("k_rows_pack");
