@@ -180,8 +180,8 @@ static void recon_i32(int32_t* J, const int32_t* I, int64_t h, int64_t w,
 void orc_recon_u8(const uint8_t* marker, const uint8_t* mask, int64_t h,
                   int64_t w, int conn, uint8_t* out) {
   const int64_t n = h * w;
-  int32_t* J = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
-  int32_t* I = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* J = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t* I = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
   for (int64_t i = 0; i < n; ++i) { J[i] = marker[i]; I[i] = mask[i]; }
   recon_i32(J, I, h, w, conn);
   for (int64_t i = 0; i < n; ++i) out[i] = (uint8_t)J[i];
@@ -192,8 +192,8 @@ void orc_recon_u8(const uint8_t* marker, const uint8_t* mask, int64_t h,
 void orc_recon_u16(const uint16_t* marker, const uint16_t* mask, int64_t h,
                    int64_t w, int conn, uint16_t* out) {
   const int64_t n = h * w;
-  int32_t* J = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
-  int32_t* I = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* J = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t* I = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
   for (int64_t i = 0; i < n; ++i) { J[i] = marker[i]; I[i] = mask[i]; }
   recon_i32(J, I, h, w, conn);
   for (int64_t i = 0; i < n; ++i) out[i] = (uint16_t)J[i];
