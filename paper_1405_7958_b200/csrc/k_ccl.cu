@@ -95,7 +95,7 @@ struct FgMask {  // mask != 0
   __device__ __forceinline__ void eval4(uint32_t v, int, int, uint32_t& fg, uint32_t&) const {
     fg = byte_msbs(~__vcmpeq4(v, 0u));
   }
-  __device__ __forceinline__ const uint8_t* plane() const { return m; }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return m; }
 };
 struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
   static constexpr bool kSeed = true;
@@ -110,7 +110,7 @@ struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
     fg = t > 255 ? 0u : byte_msbs(__vcmpgeu4(a, 0x01010101u * (uint32_t)t));
     sd = ts > 255 ? 0u : byte_msbs(__vcmpgeu4(a, 0x01010101u * (uint32_t)ts));
   }
-  __device__ __forceinline__ const uint8_t* plane() const { return v; }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return v; }
 };
 struct FgCode {  // a precomputed code plane: bit 0 foreground, bit 1 seed
   static constexpr bool kSeed = true;
@@ -124,7 +124,7 @@ struct FgCode {  // a precomputed code plane: bit 0 foreground, bit 1 seed
     fg = byte_msbs(__vcmpne4(a & 0x01010101u, 0u));
     sd = byte_msbs(__vcmpne4(a & 0x02020202u, 0u));
   }
-  __device__ __forceinline__ const uint8_t* plane() const { return c; }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return c; }
 };
 struct FgBackground {  // m == 0; seed: on the image border
   static constexpr bool kSeed = true;
@@ -139,7 +139,7 @@ struct FgBackground {  // m == 0; seed: on the image border
     fg = byte_msbs(__vcmpeq4(v, 0u));
     sd = border_nib(y, x, h, w);
   }
-  __device__ __forceinline__ const uint8_t* plane() const { return m; }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return m; }
 };
 
 constexpr int kTileWarps = 4;
