@@ -167,8 +167,6 @@ struct rtg_ctx {
   uint32_t* status = nullptr;      // sticky status bits
   int64_t* stats = nullptr;        // device-side counters for rtg_ctx_stats
   uint32_t* level_bits = nullptr;  // value-presence bitmaps (rtg_recon_u8_dev)
-  uint32_t* ccl_bits = nullptr;    // 1-bit foreground plane of a sparse-root CCL (max_px / 32)
-  uint32_t* ccl_fgbits = nullptr;  //   = ccl_bits when the last CCL ran sparse, else null
   rtg::TileQueue tq{};
   rtg::FeatureAcc acc{};
   // texture intermediates (max_objects each): bbox, histogram, GLCM, moments
@@ -280,11 +278,8 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
 // linear index of p's component (-1 = background).  counts, when given,
 // receives every component's pixel count at its global root.
 // prezeroed: the caller already cleared the counters ccl_label_zero names.
-// sparse: the root plane may leave background pixels inside tiles unwritten
-// (only for a following ccl_canonical, which reads ctx->ccl_fgbits).
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots, int32_t* counts = nullptr, bool prezeroed = false,
-              bool sparse = false);
+              int conn, int32_t* roots, int32_t* counts = nullptr, bool prezeroed = false);
 // Appends to z the buffers a labelling CCL (ccl_roots + ccl_canonical) of an
 // h x w mask needs cleared: local-root count, root bitmap, look-back status.
 void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z);

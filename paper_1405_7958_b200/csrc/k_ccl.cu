@@ -155,8 +155,7 @@ template <int CONN, class P>
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ roots,
            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount,
-           int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b,
-           uint32_t* __restrict__ fgbits) {
+           int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b) {
   pdl_enter();
   __shared__ int32_t s_par[kTileWarps][512];
   __shared__ uint32_t s_inf[kTileWarps][512];
@@ -297,13 +296,8 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
     inf[rb + k] = (uint32_t)((y0 + (lr >> 4)) * w + x0 + pos[lr]);
   }
   __syncwarp();
-  // 4. every pixel's local root (global index), coalesced stores.  Sparse
-  // mode (fgbits, set only when every tile takes this vector path): the
-  // row masks go to a 1-bit plane and background groups inside the tile are
-  // not stored at all — consumers test the bit plane first; the tile's
-  // border rows / columns are always stored, since the seams read them.
+  // 4. every pixel's local root (global index), coalesced stores
   if (vec) {
-    if (fgbits && y0 + lane < h) fgbits[((int64_t)(y0 + lane) * w + x0) >> 5] = bits;
     // 4 pixels per lane (one 16-byte store): 8 lanes per row, 4 rows per step
     const int g = lane >> 3, cq = (lane & 7) * 4;
 #pragma unroll 2
@@ -315,7 +309,6 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
       const uint32_t st = b & ~(b << 1);
       int32_t o[4];
       const uint32_t fg4 = (b >> cq) & 0xFu;
-      if (!fg4 && fgbits && r != 0 && r != 31 && cq != 0 && cq != 28) continue;
       if (!fg4) {
         o[0] = o[1] = o[2] = o[3] = -1;
       } else if (fg4 == 0xFu && !((st >> (cq + 1)) & 7u)) {
@@ -597,29 +590,21 @@ __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* _
 // 4 pixels per thread with 16-byte loads/stores and staged gathers.
 __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
                           const int32_t* __restrict__ rank,
-                          int32_t* __restrict__ labels, const uint32_t* __restrict__ fgbits) {
+                          int32_t* __restrict__ labels) {
   pdl_enter();
   const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(labels)) &
                     15) == 0;
   for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n;
        i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
     if (vec && i0 + 4 <= n) {
-      // sparse root plane: background groups are not even read
-      const uint32_t nib = fgbits ? (__ldg(fgbits + (i0 >> 5)) >> (i0 & 31)) & 0xFu : 0xFu;
-      if (!nib) {
-        *reinterpret_cast<int4*>(labels + i0) = make_int4(0, 0, 0, 0);
-        continue;
-      }
       const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
       int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k)  // label of the local root
-        v[k] = ((nib >> k) & 1u) && v[k] >= 0 ? rank[v[k]] : 0;
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? rank[v[k]] : 0;  // label of the local root
       *reinterpret_cast<int4*>(labels + i0) = make_int4(v[0], v[1], v[2], v[3]);
     } else {
       for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
-        const bool fg = !fgbits || ((fgbits[i >> 5] >> (i & 31)) & 1u);
-        const int32_t lr = fg ? roots[i] : -1;
+        const int32_t lr = roots[i];
         labels[i] = lr >= 0 ? rank[lr] : 0;
       }
     }
@@ -1051,7 +1036,7 @@ __global__ void k_fill_uf_final(int64_t n, const uint8_t* __restrict__ bin,
 // stage by stage for the four, so each stage's loads are in flight together.
 __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
                              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
-                             uint8_t* __restrict__ out, const uint32_t* __restrict__ fgbits) {
+                             uint8_t* __restrict__ out) {
   pdl_enter();
   const bool vec = ((reinterpret_cast<uintptr_t>(roots) | reinterpret_cast<uintptr_t>(tissue) |
                      reinterpret_cast<uintptr_t>(out)) & 3) == 0 &&
@@ -1059,18 +1044,11 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
   for (int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n;
        i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
     if (vec && i0 + 4 <= n) {
-      // sparse root plane: background groups are not even read
-      const uint32_t nib = fgbits ? (__ldg(fgbits + (i0 >> 5)) >> (i0 & 31)) & 0xFu : 0xFu;
-      if (!nib) {
-        *reinterpret_cast<uint32_t*>(out + i0) = 0u;
-        continue;
-      }
       const int4 r4 = __ldg(reinterpret_cast<const int4*>(roots + i0));
       const uint32_t t4 = __ldg(reinterpret_cast<const uint32_t*>(tissue + i0));
       int32_t v[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        v[k] = ((nib >> k) & 1u) && v[k] >= 0 ? roots[v[k]] : -1;  // global root
+      for (int k = 0; k < 4; ++k) v[k] = v[k] >= 0 ? roots[v[k]] : -1;  // global root
       uint32_t o = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -1078,8 +1056,7 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
       *reinterpret_cast<uint32_t*>(out + i0) = o;
     } else {
       for (int64_t i = i0; i < n && i < i0 + 4; ++i) {
-        const bool fg = !fgbits || ((fgbits[i >> 5] >> (i & 31)) & 1u);
-        const int32_t r = fg ? root_of(roots, i) : -1;
+        const int32_t r = root_of(roots, i);
         out[i] = (uint8_t)(r >= 0 && flag[r] && tissue[i]);
       }
     }
@@ -1091,15 +1068,7 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
 // OR of the seed bits; bitmap (if given, zeroed here) marks global roots.
 template <class P>
 int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
-            int32_t* counts, int32_t* flags, uint32_t* bitmap, bool prezeroed = false,
-            bool want_sparse = false) {
-  // sparse root plane (k_ccl_tile step 4) only when every tile is a vector
-  // tile; the consumers learn it from ctx->ccl_fgbits
-  const bool sparse = want_sparse && w % 32 == 0 &&
-                      (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0 &&
-                      (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
-  uint32_t* fgbits = sparse ? ctx->ccl_bits : nullptr;
-  ctx->ccl_fgbits = fgbits;
+            int32_t* counts, int32_t* flags, uint32_t* bitmap, bool prezeroed = false) {
   int32_t* lcount = ctx->misc + 8;
   if (!prezeroed) {
     // with a bitmap (the canonical labelling follows): also the look-back
@@ -1115,11 +1084,11 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
   if (conn == 8)
-    RTG_CUDA(launch_k(ctx, k_ccl_tile<8, P>, grid, 32 * kTileWarps, 0, pred, (int)h, (int)w,
-                      tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags, fgbits));
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<8, P>, grid, 32 * kTileWarps, 0, 
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
   else
-    RTG_CUDA(launch_k(ctx, k_ccl_tile<4, P>, grid, 32 * kTileWarps, 0, pred, (int)h, (int)w,
-                      tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags, fgbits));
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<4, P>, grid, 32 * kTileWarps, 0, 
+        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
   RTG_LAUNCH("k_ccl_tile");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
@@ -1148,10 +1117,8 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   int32_t* flag = ctx->i32b;
   const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
   const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
-  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed,
-                  /*want_sparse=*/true));
-  RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out,
-                    (const uint32_t*)ctx->ccl_fgbits));
+  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed));
+  RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out));
   RTG_LAUNCH("k_seeded_and");
   return RTG_OK;
 }
@@ -1257,9 +1224,8 @@ int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t 
 }
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
-              int32_t* roots, int32_t* counts, bool prezeroed, bool sparse) {
-  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed,
-                 sparse);
+              int32_t* roots, int32_t* counts, bool prezeroed) {
+  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed);
 }
 
 void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
@@ -1288,8 +1254,7 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                                                          clear_acc ? *clear_acc : ctx->acc,
                                                          clear_acc != nullptr));
   RTG_LAUNCH("k_root_rank");
-  RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels,
-                    (const uint32_t*)ctx->ccl_fgbits));
+  RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
   return RTG_OK;
 }

@@ -176,8 +176,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o8 BWLabel (canonical)
   prof_mark(ctx, RTG_STAGE_LABEL);
   // the tiled watershed cleared the labelling's counters with its own
-  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0,
-                    /*sparse=*/true));
+  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0));
   // the ranking pass also resets the feature accumulators of every label
   RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out, with_features ? &ctx->acc : nullptr));
   // o9 features
@@ -457,7 +456,6 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->status, 1));
         RTG_TRY(dalloc(&c->stats, RTG_NUM_STATS));
         RTG_TRY(dalloc(&c->level_bits, 16));
-        RTG_TRY(dalloc(&c->ccl_bits, n / 32 + 8));
         const int64_t ntiles = ceil_div(max_h, kTile) * ceil_div(max_w, kTile);
         c->tq.capacity = (int32_t)(2 * ntiles);
         RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
@@ -493,7 +491,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
                   c->features, c->feat20, c->tex14, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
                   c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
-                  c->status, c->stats, c->level_bits, c->ccl_bits, c->tq.state, c->tq.slots, c->tq.counters,
+                  c->status, c->stats, c->level_bits, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs, c->tex_bbox, c->tex_hist,
                   c->tex_glcm, c->tex_mom};
   for (void* b : bufs)
@@ -899,7 +897,7 @@ int rtg_bwlabel_dev(rtg_ctx* ctx, const uint8_t* d_mask, int64_t h, int64_t w, i
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_mask || !d_labels) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
-  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a, nullptr, false, /*sparse=*/true));
+  RTG_TRY(ccl_roots(ctx, d_mask, h, w, conn, ctx->i32a));
   return ccl_canonical(ctx, ctx->i32a, h, w, d_labels, d_n ? d_n : ctx->misc);
 }
 
