@@ -428,11 +428,12 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
                   int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc = nullptr);
 // Grayscale reconstruction by level decomposition (k_ccl.cu): when J and I
 // hold at most kMaxReconLevels distinct non-zero values, R is one seeded
-// labelling per value.  recon_level_count reads the values back (a stream
-// synchronisation) and sets *count = -1 when there are more.
+// labelling per value.  recon_clip_levels writes J = min(marker, I) and reads
+// the values of J and I back in the same pass (a stream synchronisation);
+// *count = -1 when there are more than kMaxReconLevels.
 constexpr int kMaxReconLevels = 4;
-int recon_level_count(rtg_ctx* ctx, const uint8_t* J, const uint8_t* I, int64_t h, int64_t w,
-                      uint8_t levels[kMaxReconLevels], int* count);
+int recon_clip_levels(rtg_ctx* ctx, const uint8_t* marker, const uint8_t* I, int64_t h,
+                      int64_t w, uint8_t* J, uint8_t levels[kMaxReconLevels], int* count);
 // J (clipped to I on entry) becomes recon(J, I); uses ctx->m1, m2, i32a, i32b.
 int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t w, int conn,
                  const uint8_t* levels, int count);

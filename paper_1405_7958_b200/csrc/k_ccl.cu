@@ -1133,18 +1133,39 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
 // (The stage's ReconToNuclei uses the one-threshold case, recon_threshold_uf.)
 namespace {
 
-// Presence bitmaps of the non-zero values of I (words 0-7) and J (8-15).
-__global__ void k_level_presence(const uint8_t* __restrict__ I, const uint8_t* __restrict__ J,
-                                 int64_t n, uint32_t* __restrict__ bits) {
+// The marker clip J = min(marker, I) fused with the presence bitmaps of the
+// non-zero values of I (words 0-7) and J (8-15), four pixels per thread.
+__device__ __forceinline__ void mark_present(uint32_t* s, uint32_t v) {
+  // test before setting: each value costs one shared atomic per block
+  if (v && !(s[v >> 5] & (1u << (v & 31)))) atomicOr(&s[v >> 5], 1u << (v & 31));
+}
+
+__global__ void k_clip_presence(const uint8_t* __restrict__ marker, const uint8_t* __restrict__ I,
+                                int64_t n, uint8_t* __restrict__ J, uint32_t* __restrict__ bits) {
   __shared__ uint32_t s[16];
   if (threadIdx.x < 16) s[threadIdx.x] = 0;
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+  const bool vec = ((reinterpret_cast<uintptr_t>(marker) | reinterpret_cast<uintptr_t>(I) |
+                     reinterpret_cast<uintptr_t>(J)) & 3) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(marker) + k);
+    const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(I) + k);
+    const uint32_t j = __vminu4(a, b);
+    reinterpret_cast<uint32_t*>(J)[k] = j;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mark_present(s, (b >> (8 * q)) & 0xFFu);
+      mark_present(s + 8, (j >> (8 * q)) & 0xFFu);
+    }
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = I[i], b = J[i];
-    // test before setting: each value costs one shared atomic per block
-    if (a && !(s[a >> 5] & (1u << (a & 31)))) atomicOr(&s[a >> 5], 1u << (a & 31));
-    if (b && !(s[8 + (b >> 5)] & (1u << (b & 31)))) atomicOr(&s[8 + (b >> 5)], 1u << (b & 31));
+    const uint32_t b = I[i], j = min((uint32_t)marker[i], b);
+    J[i] = (uint8_t)j;
+    mark_present(s, b);
+    mark_present(s + 8, j);
   }
   __syncthreads();
   if (threadIdx.x < 16 && s[threadIdx.x]) atomicOr(bits + threadIdx.x, s[threadIdx.x]);
@@ -1181,13 +1202,14 @@ __global__ void k_level_assign(int64_t n, const int32_t* __restrict__ roots,
 
 }  // namespace
 
-int recon_level_count(rtg_ctx* ctx, const uint8_t* J, const uint8_t* I, int64_t h, int64_t w,
-                      uint8_t levels[kMaxReconLevels], int* count) {
+int recon_clip_levels(rtg_ctx* ctx, const uint8_t* marker, const uint8_t* I, int64_t h,
+                      int64_t w, uint8_t* J, uint8_t levels[kMaxReconLevels], int* count) {
   const int64_t n = h * w;
   *count = -1;
   RTG_CUDA(cudaMemsetAsync(ctx->level_bits, 0, 16 * sizeof(uint32_t), ctx->stream));
-  k_level_presence<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(I, J, n, ctx->level_bits);
-  RTG_LAUNCH("k_level_presence");
+  k_clip_presence<<<grid_for(ctx, ceil_div(n, 4)), 256, 0, ctx->stream>>>(marker, I, n, J,
+                                                                          ctx->level_bits);
+  RTG_LAUNCH("k_clip_presence");
   uint32_t bits[16];
   RTG_CUDA(cudaMemcpyAsync(bits, ctx->level_bits, sizeof(bits), cudaMemcpyDeviceToHost,
                            ctx->stream));

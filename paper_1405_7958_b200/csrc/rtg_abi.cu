@@ -855,20 +855,22 @@ int rtg_recon_u8_dev(rtg_ctx* ctx, const uint8_t* d_marker, const uint8_t* d_mas
   RTG_TRY(check_ctx(ctx, h, w));
   if (!d_marker || !d_mask || !d_out) return fail(RTG_ERR_INVALID_ARG, "null buffer");
   if (conn != 4 && conn != 8) return fail(RTG_ERR_INVALID_ARG, "conn must be 4 or 8");
-  k_clip_copy<uint8_t><<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(d_marker, d_mask, h * w,
-                                                                      d_out);
-  RTG_LAUNCH("k_clip_copy");
   // Few distinct values (a maze, a binary or quantised mask): one seeded
   // labelling per value, immune to long propagation paths that make the
-  // wavefront engine crawl tile by tile.  The choice reads 64 bytes back, so
-  // it is skipped while the stream is being captured into a graph.
+  // wavefront engine crawl tile by tile.  The clip pass also collects the
+  // values present; reading them back synchronises, so the choice is skipped
+  // while the stream is being captured into a graph.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   RTG_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
   if (cap == cudaStreamCaptureStatusNone && ctx->recon_entry_impl != 1) {
     uint8_t levels[kMaxReconLevels];
     int count = -1;
-    RTG_TRY(recon_level_count(ctx, d_out, d_mask, h, w, levels, &count));
+    RTG_TRY(recon_clip_levels(ctx, d_marker, d_mask, h, w, d_out, levels, &count));
     if (count >= 0) return recon_levels(ctx, d_out, d_mask, h, w, conn, levels, count);
+  } else {
+    k_clip_copy<uint8_t><<<grid_for(ctx, h * w), 256, 0, ctx->stream>>>(d_marker, d_mask, h * w,
+                                                                        d_out);
+    RTG_LAUNCH("k_clip_copy");
   }
   return iwpp_recon_u8(ctx, d_out, d_mask, h, w, conn);
 }
