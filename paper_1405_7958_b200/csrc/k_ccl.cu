@@ -764,11 +764,12 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const uint32_t upf = __shfl_up_sync(kFull, fgb, 1), upb = __shfl_up_sync(kFull, bgb, 1);
   const uint32_t upall = (upf & ~(upf << 1)) | (upb & ~(upb << 1));
   __syncwarp();
-  // rows join their upper neighbour in log2(32) rounds (row r in the round
-  // of its lowest set bit), so every union links two already-merged row
-  // blocks and the trees stay shallow
-  for (int sblk = 1; sblk < 32; sblk <<= 1) {
-    if ((lane & (2 * sblk - 1)) == sblk && (upf | upb)) {
+  // every row joins its upper neighbour at once (concurrent CAS unions on
+  // the 16-bit forest); a schedule of log2(32) rounds (row r in the round of
+  // its lowest set bit) kept the trees shallower but left 3/4 of the lanes
+  // idle on average: 12 us more per 4096^2 tile
+  {
+    if (lane > 0 && (upf | upb)) {
       int k = 0;
       for (uint32_t q = allst; q; q &= q - 1, ++k) {
         const int b = __ffs(q) - 1;
