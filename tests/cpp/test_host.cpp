@@ -339,6 +339,35 @@ void scheduling() {
     st.stage_region(patch, 0).wait();
     require(!st.view_region(id, q), "a newer partial piece hides the old one: no view");
   });
+  check("MemoryStore views of 2-D / 1-D pieces; defer_completion runs in place on CPU workers", [] {
+    MemoryStore st("s");
+    const DataRegionId id{"t", "lab", "label", 0, 0};
+    DataRegion lab(id, RegionKind::kDense2D, ElementKind::kI32, box2(10, 20, 49, 99));
+    std::vector<std::uint8_t> px(40 * 80 * 4);
+    for (std::size_t i = 0; i < px.size(); ++i) px[i] = std::uint8_t(i * 13 + 5);
+    lab.put_chunk(lab.bbox(), px);
+    st.stage_region(lab, 0).wait();
+    const BoundingBox q = box2(15, 30, 24, 59);
+    const auto v = st.view_region(id, q);
+    require(v && v->row_pitch == 80 * 4 && v->elem == ElementKind::kI32, "2-D view");
+    const DataRegion r = st.read_region(id, q);
+    for (std::int64_t y = 0; y < 10; ++y)
+      require(std::memcmp(v->data + y * v->row_pitch,
+                          r.chunks().begin()->second.payload.data() + y * 30 * 4, 30 * 4) == 0,
+              "2-D row " + std::to_string(y));
+    const DataRegionId id1{"t", "vec", "raw", 0, 0};
+    DataRegion one(id1, RegionKind::kDense1D, ElementKind::kU16, BoundingBox({0}, {99}));
+    std::vector<std::uint8_t> b1(200);
+    for (std::size_t i = 0; i < b1.size(); ++i) b1[i] = std::uint8_t(i);
+    one.put_chunk(one.bbox(), b1);
+    st.stage_region(one, 0).wait();
+    const auto v1 = st.view_region(id1, BoundingBox({40}, {59}));
+    require(v1 && v1->data[0] == 80 && v1->data[39] == 119, "1-D view");
+    require(!st.view_region(DataRegionId{"t", "none", "x", 0, 0}, q), "no data: no view");
+    int ran = 0;
+    defer_completion([&] { ++ran; });
+    require(ran == 1, "no pipelining executor: the completion runs at once");
+  });
   check("executor: spawned stages run, lazy inputs are touched, a wedged graph throws", [] {
     StorageRegistry reg;
     auto st = std::make_shared<MemoryStore>("store");
