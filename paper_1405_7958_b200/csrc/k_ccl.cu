@@ -40,16 +40,6 @@
 namespace rtg {
 namespace {
 
-// Read-only shared-memory find.
-__device__ __forceinline__ int32_t find_root(const int32_t* par, int32_t a) {
-  int32_t p = par[a];
-  while (p != a) {
-    a = p;
-    p = par[a];
-  }
-  return a;
-}
-
 // Shared-memory find with path halving, used while unions are running (only
 // connectivity matters there; a stale halving store can only move an entry
 // to another ancestor).
@@ -73,6 +63,28 @@ __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
     const int32_t old = atomicMin(&par[a], b);
     if (old == a) return;
     a = old;
+  }
+}
+
+// Flattens a warp's run forest (lane owns entries rb .. rb+nruns-1) by
+// pointer jumping until no entry changes.  The rows unite with the row above
+// all at once, so chains can be as deep as the tile; jumping halves every
+// chain per round where per-entry finds walk them link by link.  A
+// concurrent store only replaces a parent by an ancestor, and roots never
+// change, so "par[par[k]] == par[k]" read at any time means par[k] is final.
+__device__ __forceinline__ void flatten_jump(int32_t* par, int rb, int nruns) {
+  while (true) {
+    bool changed = false;
+    for (int k = 0; k < nruns; ++k) {
+      const int32_t p = par[rb + k];
+      const int32_t gp = par[p];
+      if (gp != p) {
+        par[rb + k] = gp;
+        changed = true;
+      }
+    }
+    __syncwarp();
+    if (!__any_sync(0xFFFFFFFFu, changed)) break;
   }
 }
 
@@ -253,10 +265,7 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   // 3. flatten the run forest (read-only finds, then own-entry writes), then
   //    accumulate pixel counts / seed bits at the local roots
   const int nruns = __popc(starts);
-  for (int k = 0; k < nruns; ++k) inf[rb + k] = (uint32_t)find_root(par, rb + k);
-  __syncwarp();
-  for (int k = 0; k < nruns; ++k) par[rb + k] = (int32_t)inf[rb + k];
-  __syncwarp();
+  flatten_jump(par, rb, nruns);
   int nroot = 0;
   for (int k = 0; k < nruns; ++k) {
     if (par[rb + k] == rb + k) {
@@ -621,15 +630,6 @@ int grid_for(rtg_ctx* ctx, int64_t n) {
 // atomicMin, so the link is a CAS on the 32-bit word holding the entry; plain
 // 16-bit path-halving stores cannot be lost to it (a CAS whose expected word
 // changed underneath simply retries).
-__device__ __forceinline__ int32_t find_root16(const uint16_t* par, int32_t a) {
-  int32_t p = par[a];
-  while (p != a) {
-    a = p;
-    p = par[a];
-  }
-  return a;
-}
-
 __device__ __forceinline__ int32_t find_root16_c(uint16_t* par, int32_t a) {
   int32_t p = par[a];
   while (p != a) {
@@ -639,6 +639,23 @@ __device__ __forceinline__ int32_t find_root16_c(uint16_t* par, int32_t a) {
     p = gp;
   }
   return a;
+}
+
+// flatten_jump on the 16-bit forest.
+__device__ __forceinline__ void flatten_jump16(uint16_t* par, int rb, int nruns) {
+  while (true) {
+    bool changed = false;
+    for (int k = 0; k < nruns; ++k) {
+      const int32_t p = par[rb + k];
+      const int32_t gp = par[p];
+      if (gp != p) {
+        par[rb + k] = (uint16_t)gp;
+        changed = true;
+      }
+    }
+    __syncwarp();
+    if (!__any_sync(0xFFFFFFFFu, changed)) break;
+  }
 }
 
 __device__ __forceinline__ int32_t atomic_min16(uint16_t* par, int32_t a, int32_t b) {
@@ -685,17 +702,39 @@ __device__ __forceinline__ void unite_s16(uint16_t* par, int32_t a, int32_t b) {
 // updated with 32-bit atomics), and the flattened forest then holds each
 // run's root pixel as a tile-local offset (row * 32 + column) for the stores.
 template <int kW>
-struct FbSmem {
+struct __align__(16) FbSmem {
   uint16_t par[kW][1024];
   uint32_t acc[kW][512];
   uint8_t pos[kW][1024];
+};
+
+// Run-table form (w % 32 == 0): instead of a root for every pixel, each tile
+// leaves its row bit masks and the tile-local offset of every run's local
+// root; the per-pixel roots plane then only holds the tile-border pixels
+// (all the seams read) and the local roots themselves (the global forest).
+// A pixel's local root is re-derived from the row mask (run index = number
+// of run starts up to its column) and one table entry.
+struct RunTable {
+  const uint32_t* rowbits;  // [tile * 32 + r]: foreground bits of row r of the tile
+  const uint16_t* rtab;     // [tile * 1024 + r * 32 + k]: row * 32 + col of run k's local root
+  int w, tiles_x;
+  __device__ __forceinline__ int32_t local_root(int32_t q) const {
+    const int y = q / w, x = q - y * w;
+    const int tile = (y >> 5) * tiles_x + (x >> 5), r = y & 31, c = x & 31;
+    const uint32_t fgb = rowbits[tile * 32 + r], bgb = ~fgb;
+    const uint32_t st = (fgb & ~(fgb << 1)) | (bgb & ~(bgb << 1));
+    const int k = __popc(st & ((2u << c) - 1u)) - 1;
+    const int32_t off = rtab[(int64_t)tile * 1024 + r * 32 + k];
+    return (y - r + (off >> 5)) * w + (x - c) + (off & 31);
+  }
 };
 
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntiles,
               int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
               int32_t* __restrict__ lcount, int32_t* __restrict__ counts,
-              int32_t* __restrict__ total) {
+              int32_t* __restrict__ total, uint32_t* __restrict__ rowbits,
+              uint16_t* __restrict__ rtab, int32_t* __restrict__ border) {
   pdl_enter();
   __shared__ FbSmem<kTileWarps> S;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -790,10 +829,10 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   }
   // 3. flatten; per local root: pixel count + border-background bit
   const int nruns = __popc(allst);
-  // in place: a concurrent shortcut store only replaces a parent by an
-  // ancestor, so every find still ends at the same root
-  for (int k = 0; k < nruns; ++k) par[rb + k] = (uint16_t)find_root16(par, rb + k);
-  __syncwarp();
+  // pointer jumping in place (a concurrent store only replaces a parent by an
+  // ancestor): the all-at-once unions leave chains up to 31 rows deep, which
+  // per-run finds walk link by link; jumping halves every chain per round
+  flatten_jump16(par, rb, nruns);
   int nroot = 0;
   for (int k = 0; k < nruns; ++k)
     if (par[rb + k] == rb + k) {
@@ -825,6 +864,7 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
     ++base;
     counts[g] = 0;
     total[g] = 0;  // subtree areas are accumulated straight from k_fb_tree
+    if (rtab) roots[g] = g;
   }
   __syncwarp();
   // each lane rewrites only its own runs' entries
@@ -833,6 +873,29 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
     par[rb + k] = (uint16_t)((lr & ~31) | pos[lr]);
   }
   __syncwarp();
+  if (rtab) {
+    // 4'. row masks, run table (the whole 2 KB forest, coalesced), and the
+    //     local roots of the tile-border pixels
+    rowbits[tile * 32 + lane] = fgb;
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(par);
+      uint4* dst = reinterpret_cast<uint4*>(rtab + (int64_t)tile * 1024);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[lane + 32 * j] = src[lane + 32 * j];
+    }
+    auto glob = [&](int32_t lo) { return (y0 + (lo >> 5)) * w + x0 + (lo & 31); };
+    int32_t* bd = border + (int64_t)tile * 128;
+    // rows 0 and 31 (lane = column; a partial last row has no seam below),
+    // columns 0 and 31 (lane = row: the row's first and last runs)
+    const uint32_t below = (2u << lane) - 1u;
+    bd[lane] = glob(par[__popc(__shfl_sync(kFull, allst, 0) & below) - 1]);
+    bd[32 + lane] = glob(par[31 * 32 + __popc(__shfl_sync(kFull, allst, 31) & below) - 1]);
+    if (yr < h) {
+      bd[64 + lane] = glob(par[rb]);
+      bd[96 + lane] = glob(par[rb + nruns - 1]);
+    }
+    return;
+  }
   // 4. every valid pixel's local root
   if (vec) {
     const int g = lane >> 3, cq = (lane & 7) * 4;
@@ -877,28 +940,41 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
 
 // Seams of the joint labelling: foreground pairs 8-connected, background
 // pairs 4-connected, with the same redundancy skips as k_ccl_seams.
-__device__ __forceinline__ void seam_fb(const uint8_t* __restrict__ m, int h, int w,
-                                        int32_t* __restrict__ roots, int32_t p, int32_t q,
-                                        int32_t p2, int32_t q2, bool has_prev, int32_t qa,
-                                        bool has_qa, int32_t qb, bool has_qb, bool pref_b,
-                                        bool next_b) {
+// node(pixel, which) names the forest node a pixel unites through: the
+// pixel itself in the per-pixel form, its local root (read from the tile
+// border arrays) in the run-table form; which = 0 for p, 1 for q, 2 for qa,
+// 3 for qb.
+template <class Node>
+__device__ __forceinline__ void seam_fb(const uint8_t* __restrict__ m, int32_t* __restrict__ roots,
+                                        int32_t p, int32_t q, int32_t p2, int32_t q2,
+                                        bool has_prev, int32_t qa, bool has_qa, int32_t qb,
+                                        bool has_qb, bool pref_b, bool next_b, const Node& node) {
   // p: seam pixel, q: its partner across the seam; p2/q2: the pair one step
   // back along the seam (valid when has_prev, same tiles); qa/qb: q's
   // neighbours one step back/forward along the seam (the 8-conn diagonals)
   const bool fp = m[p] != 0;
   const bool fq = m[q] != 0;
   if (!fp) {  // background: 4-connected straight pair only
-    if (!fq && !(has_prev && !m[p2] && !m[q2])) uf_unite_g(roots, p, q);
+    if (!fq && !(has_prev && !m[p2] && !m[q2])) uf_unite_g(roots, node(p, 0), node(q, 1));
     return;
   }
   const bool in_prev = has_prev && m[p2] != 0;  // p ~ p2 (same tile, same kind)
   const bool fqa = has_qa && m[qa] != 0;
-  if (fq && !(in_prev && fqa)) uf_unite_g(roots, p, q);
-  if (fqa && !in_prev && !(fq && pref_b)) uf_unite_g(roots, p, qa);
-  if (has_qb && m[qb] != 0 && !(fq && next_b)) uf_unite_g(roots, p, qb);
+  const bool uq = fq && !(in_prev && fqa);
+  const bool uqa = fqa && !in_prev && !(fq && pref_b);
+  const bool uqb = has_qb && m[qb] != 0 && !(fq && next_b);
+  if (!(uq | uqa | uqb)) return;
+  const int32_t np = node(p, 0);
+  if (uq) uf_unite_g(roots, np, node(q, 1));
+  if (uqa) uf_unite_g(roots, np, node(qa, 2));
+  if (uqb) uf_unite_g(roots, np, node(qb, 3));
 }
 
-__global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int row_seams,
+// border (run-table form, nullptr otherwise): per tile 128 local roots (global
+// indices) of its top row, bottom row, left column and right column, in that
+// order, 32 each.
+__global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x,
+                               int row_seams, const int32_t* __restrict__ border,
                                int32_t* __restrict__ roots) {
   pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -906,25 +982,43 @@ __global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int 
     const int y = ((int)blockIdx.y + 1) * 32, x = t;
     if (x >= w || y >= h) return;
     const int32_t p = y * w + x, u = p - w;
-    seam_fb(m, h, w, roots, p, u, p - 1, u - 1, (x & 31) != 0, u - 1, x > 0, u + 1, x + 1 < w,
-            (x & 31) != 0, ((x + 1) & 31) != 0);
+    const int tb = (y >> 5) * tiles_x;  // first tile of the row below the seam
+    auto node = [&](int32_t q, int which) -> int32_t {
+      if (!border) return q;
+      if (which == 0) return __ldg(border + (tb + (x >> 5)) * 128 + (x & 31));
+      const int xx = q - u + x;  // q lies in the row above: bottom rows of that tile row
+      return __ldg(border + (tb - tiles_x + (xx >> 5)) * 128 + 32 + (xx & 31));
+    };
+    seam_fb(m, roots, p, u, p - 1, u - 1, (x & 31) != 0, u - 1, x > 0, u + 1, x + 1 < w,
+            (x & 31) != 0, ((x + 1) & 31) != 0, node);
   } else {
     const int x = ((int)blockIdx.y - row_seams + 1) * 32, y = t;
     if (y >= h || x >= w) return;
     const int32_t p = y * w + x, l = p - 1;
-    seam_fb(m, h, w, roots, p, l, p - w, l - w, (y & 31) != 0, l - w, y > 0, l + w, y + 1 < h,
-            (y & 31) != 0, ((y + 1) & 31) != 0);
+    const int tc = x >> 5;  // tile column right of the seam
+    auto node = [&](int32_t q, int which) -> int32_t {
+      if (!border) return q;
+      if (which == 0) return __ldg(border + ((y >> 5) * tiles_x + tc) * 128 + 64 + (y & 31));
+      const int yy = y + (which == 2 ? -1 : which == 3 ? 1 : 0);  // right column of the left tile
+      return __ldg(border + ((yy >> 5) * tiles_x + tc - 1) * 128 + 96 + (yy & 31));
+    };
+    seam_fb(m, roots, p, l, p - w, l - w, (y & 31) != 0, l - w, y > 0, l + w, y + 1 < h,
+            (y & 31) != 0, ((y + 1) & 31) != 0, node);
   }
 }
 
 // Top-level ancestor of every global root (-1 for the outside), and each
-// root's area added into its top-level ancestor's subtree total.
+// root's area added into its top-level ancestor's subtree total.  With a run
+// table (rt.rtab), the pixel above a root finds its local root through it.
 __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                           const uint8_t* __restrict__ m, int w,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ counts,
-                          int32_t* __restrict__ top, int32_t* __restrict__ total) {
+                          int32_t* __restrict__ top, int32_t* __restrict__ total, RunTable rt) {
   pdl_enter();
   const int n = *lcount;
+  auto above = [&](int32_t q) {  // global root of the pixel above q
+    return rt.rtab ? roots[rt.local_root(q - w)] : root_of(roots, q - w);
+  };
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
     if (roots[r] != r) continue;
@@ -933,13 +1027,13 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
     if (fg || !(counts[r] & (int32_t)kSeedBit)) {
       for (int guard = 0; guard < (1 << 20); ++guard) {  // nesting depth, never reached
         if (fg) {
-          if (cur < w) { t = cur; break; }          // touches the top border
-          const int32_t b = root_of(roots, cur - w);  // enclosing background
+          if (cur < w) { t = cur; break; }  // touches the top border
+          const int32_t b = above(cur);    // enclosing background
           if (counts[b] & (int32_t)kSeedBit) { t = cur; break; }
           cur = b;
           fg = false;
         } else {
-          cur = root_of(roots, cur - w);            // enclosing foreground
+          cur = above(cur);                 // enclosing foreground
           fg = true;
         }
       }
@@ -953,10 +1047,13 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
 // The keep decision of every LOCAL root (global root -> top-level ancestor
 // -> subtree area in range), stored at the local root's pixel: the per-pixel
 // filter then needs one byte gather instead of three dependent i32 ones.
+// With a run table (tiles_x > 0) it is stored in tile-major order instead
+// (tile * 1024 + row * 32 + col), so k_fb_emit reads a tile's bytes as one
+// contiguous kilobyte.
 __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
                           const int32_t* __restrict__ total, int32_t lo, int32_t hi,
-                          uint8_t* __restrict__ keep) {
+                          uint8_t* __restrict__ keep, int w, int tiles_x) {
   pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -967,8 +1064,116 @@ __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __r
       const int32_t a = total[t];
       kp = a >= lo && a <= hi;
     }
-    keep[lr] = kp ? 1 : 0;
+    int64_t at = lr;
+    if (tiles_x > 0) {
+      const int y = lr / w, x = lr - y * w;
+      at = (int64_t)((y >> 5) * tiles_x + (x >> 5)) * 1024 + (y & 31) * 32 + (x & 31);
+    }
+    keep[at] = kp ? 1 : 0;
   }
+}
+
+// Output of the run-table form: one warp per tile, lane = row.  A run is
+// kept when its local root's keep byte (the tile's kilobyte, staged in
+// shared memory) is set; the row's kept bits become its 32 mask bytes, its
+// word of the 1-bit plane, and its foreground-list entries.  List slots are
+// ordered row-major over the block's tiles, so list neighbours stay row
+// neighbours (the feature pass reduces runs of them); the block's entries
+// are staged in shared memory and leave as one contiguous range.
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rtab,
+          const uint8_t* __restrict__ keep, int h, int w, int tiles_x, int ntiles,
+          uint8_t* __restrict__ out, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
+          int32_t* __restrict__ count) {
+  pdl_enter();
+  __shared__ __align__(16) uint8_t s_keep[kTileWarps][1024];
+  __shared__ int32_t s_cnt[32 * kTileWarps];
+  __shared__ uint32_t s_kept[kTileWarps][32];
+  __shared__ int32_t s_list[1024 * kTileWarps];
+  __shared__ int32_t s_tot[2];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = min(blockIdx.x * kTileWarps + wid, ntiles - 1);
+  const bool active = blockIdx.x * kTileWarps + wid < ntiles;
+  const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
+  const int y = y0 + lane;
+  const bool row = active && y < h;
+  {
+    const uint4* kt = reinterpret_cast<const uint4*>(keep + (int64_t)tile * 1024);
+    uint4* sk = reinterpret_cast<uint4*>(s_keep[wid]);
+    sk[lane] = __ldg(kt + lane);
+    sk[lane + 32] = __ldg(kt + lane + 32);
+  }
+  const uint32_t fgb = row ? __ldg(rowbits + tile * 32 + lane) : 0u;
+  const uint32_t bgb = row ? ~fgb : 0u;
+  uint32_t st = (fgb & ~(fgb << 1)) | (bgb & ~(bgb << 1));
+  const int nruns = __popc(st);
+  __syncwarp();
+  uint32_t kept = 0;
+  const uint16_t* rt = rtab + (int64_t)tile * 1024 + lane * 32;
+  for (int k0 = 0; k0 < nruns; k0 += 8) {
+    const uint4 e = __ldg(reinterpret_cast<const uint4*>(rt + k0));
+    const uint32_t ew[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (k0 + j >= nruns) break;
+      const uint32_t off = (ew[j >> 1] >> (16 * (j & 1))) & 0x3FFu;
+      const int b = __ffs(st) - 1;
+      st &= st - 1;
+      const uint32_t upto = st ? (1u << (__ffs(st) - 1)) - 1u : kFull;  // run = [b, next start)
+      if (s_keep[wid][off]) kept |= upto & ~((1u << b) - 1u);
+    }
+  }
+  s_kept[wid][lane] = kept;
+  if (row) bits[((int64_t)y * w + x0) >> 5] = kept;
+  __syncwarp();
+  // mask bytes: 8 lanes per row, four rows per store (full 32-byte sectors)
+  if (active) {
+    const int g = lane >> 3, cq = (lane & 7) * 4;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + g;
+      if (y0 + r >= h) break;
+      const uint32_t nib = (s_kept[wid][r] >> cq) & 0xFu;
+      *reinterpret_cast<uint32_t*>(out + (int64_t)(y0 + r) * w + x0 + cq) =
+          (nib * 0x00204081u) & 0x01010101u;
+    }
+  }
+  // list slots: exclusive prefix over (row, warp) in row-major order; the
+  // block's entries are staged in shared memory and stored contiguously
+  s_cnt[lane * kTileWarps + wid] = __popc(kept);
+  __syncthreads();
+  if (wid == 0) {
+    int32_t c[kTileWarps], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kTileWarps; ++j) {
+      c[j] = s_cnt[lane * kTileWarps + j];
+      sum += c[j];
+    }
+    int32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int32_t tot = __shfl_sync(kFull, incl, 31);
+    int32_t base = incl - sum;
+#pragma unroll
+    for (int j = 0; j < kTileWarps; ++j) {
+      s_cnt[lane * kTileWarps + j] = base;
+      base += c[j];
+    }
+    if (lane == 31) {
+      s_tot[0] = tot;
+      s_tot[1] = tot ? atomicAdd(count, tot) : 0;
+    }
+  }
+  __syncthreads();
+  int32_t slot = s_cnt[lane * kTileWarps + wid];
+  const int32_t p0 = y * w + x0;
+  for (uint32_t r = kept; r; r &= r - 1) s_list[slot++] = p0 + __ffs(r) - 1;
+  __syncthreads();
+  const int32_t tot = s_tot[0], gbase = s_tot[1];
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) list[gbase + i] = s_list[i];
 }
 
 // Output mask of the joint path, 4 pixels per thread: local root -> its keep
@@ -1309,7 +1514,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   int32_t* total = ctx->labels;
   int32_t* lcount = ctx->misc + 9;  // its own word: cleared with the other counters
   // the stage's counters: local-root count, foreground-list count and the
-  // pad words of the foreground bit plane (written by k_fb_filter)
+  // pad words of the foreground bit plane (written by k_fb_emit / k_fb_filter)
   uint32_t* bits_base = ctx->fg_bits;
   if (!prezeroed) {
     const ClearList c = fill_area_clear(ctx, h, w);
@@ -1323,12 +1528,21 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   }
   const int tiles_x = (int)ceil_div(w, 32), tiles_y = (int)ceil_div(h, 32);
   const int ntiles = tiles_x * tiles_y;
-  RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps, 0, 
-      cand, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, total));
+  // run-table form when rows of tiles are whole words of the bit plane and
+  // the tables fit their planes (u16a: 1024 entries per tile; u16b: row
+  // masks, then the border arrays; m2: keep bytes; all free until the EDT)
+  const bool runs = (w & 31) == 0 && (int64_t)ntiles * 1024 <= ctx->max_px;
+  uint32_t* rowbits = runs ? reinterpret_cast<uint32_t*>(ctx->u16b) : nullptr;
+  uint16_t* rtab = runs ? ctx->u16a : nullptr;
+  int32_t* border = runs ? reinterpret_cast<int32_t*>(rowbits + (int64_t)ntiles * 32) : nullptr;
+  const unsigned tgrid = (unsigned)ceil_div(ntiles, kTileWarps);
+  RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, tgrid, 32 * kTileWarps, 0, cand, (int)h, (int)w, tiles_x,
+                    ntiles, roots, ctx->lroots, lcount, counts, total, rowbits, rtab, border));
   RTG_LAUNCH("k_ccl_tile_fb");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
-    RTG_CUDA(launch_k(ctx, k_ccl_seams_fb, g, 256, 0, cand, (int)h, (int)w, tiles_y - 1, roots));
+    RTG_CUDA(launch_k(ctx, k_ccl_seams_fb, g, 256, 0, cand, (int)h, (int)w, tiles_x, tiles_y - 1,
+                      (const int32_t*)border, roots));
     RTG_LAUNCH("k_ccl_seams_fb");
   }
   const int gl = ctx->num_sms * 4;
@@ -1336,16 +1550,23 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
                     (int32_t*)nullptr, (uint32_t*)nullptr, true));
   RTG_LAUNCH("k_ccl_flatten");
   prof_mark(ctx, RTG_STAGE_AREA);  // enclosure tree, subtree areas, filter
+  const RunTable rt{rowbits, rtab, (int)w, tiles_x};
   RTG_CUDA(launch_k(ctx, k_fb_tree, gl, 256, 0, ctx->lroots, lcount, cand, (int)w, roots, counts, top,
-                                         total));
+                    total, rt));
   RTG_LAUNCH("k_fb_tree");
-
-  int blocks = (int)ceil_div(n, 1024);
-  if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
   uint8_t* keep = ctx->m2;  // free until the EDT's row distances
   RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
-                    max_area, keep));
+                    max_area, keep, (int)w, runs ? tiles_x : 0));
   RTG_LAUNCH("k_fb_keep");
+  if (runs) {
+    RTG_CUDA(launch_k(ctx, k_fb_emit, tgrid, 32 * kTileWarps, 0, (const uint32_t*)rowbits,
+                      (const uint16_t*)rtab, (const uint8_t*)keep, (int)h, (int)w, tiles_x, ntiles,
+                      out, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
+    RTG_LAUNCH("k_fb_emit");
+    return RTG_OK;
+  }
+  int blocks = (int)ceil_div(n, 1024);
+  if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
   RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, (const uint8_t*)keep, out,
                                                bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
   RTG_LAUNCH("k_fb_filter");

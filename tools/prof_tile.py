@@ -15,9 +15,12 @@ ap.add_argument("--tiles", type=int, default=2)
 ap.add_argument("--passes", type=int, default=2)
 ap.add_argument("--size", type=int, default=4096)
 ap.add_argument("--pdl", action="store_true")
+ap.add_argument("--time", action="store_true",
+                help="graph-mode wall time of the passes on one stream (no stage events)")
 a = ap.parse_args()
 h = w = a.size
-ctx = rtg.Context(0, h, w, 32768)
+cap = 32768 * max(1, (h * w) // (4096 * 4096))
+ctx = rtg.Context(0, h, w, cap)
 if a.pdl:
     ctx.set_option(rtg.OPT_PDL, 1)
 p = rtg.default_params()
@@ -26,9 +29,22 @@ for k in range(a.tiles):
     t = torch.empty((h, w, 3), dtype=torch.uint8, device="cuda")
     ctx.synth_tile_dev(t, k, 0, h, w)
     rgbs.append(t)
-feat = torch.empty((32768, 20), dtype=torch.float32, device="cuda")
+feat = torch.empty((cap, 20), dtype=torch.float32, device="cuda")
 n = torch.zeros(1, dtype=torch.int32, device="cuda")
 ctx.sync()
+if a.time:
+    for t in rgbs:  # warm-up (graph capture)
+        ctx.process_tile_dev(t, h, w, p, None, None, None, feat, n)
+    ctx.sync()
+    import time
+    t0 = time.perf_counter()
+    for ps in range(a.passes):
+        for t in rgbs:
+            ctx.process_tile_dev(t, h, w, p, None, None, None, feat, n)
+    ctx.sync()
+    dt = (time.perf_counter() - t0) / (a.passes * a.tiles)
+    print(f"{h}x{w}: {dt * 1e3:.4f} ms/tile -> {h * w / dt / 1e6:.0f} Mpixel/s (objects {int(n.item())})")
+    sys.exit(0)
 for ps in range(a.passes):
     if ps == a.passes - 1:
         ctx.profile(True)
