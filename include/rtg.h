@@ -251,7 +251,14 @@ enum rtg_option {
    * of 24 KB bulk async copies (TMA, cp.async.bulk + mbarrier) (default);
    * 0 = 128-bit streaming loads with register prefetch, two 512-thread CTAs
    * per SM.  Identical results. */
-  RTG_OPT_STREAM_IMPL = 7
+  RTG_OPT_STREAM_IMPL = 7,
+  /* Stage labellings (ReconToNuclei, the joint FillHoles + AreaThreshold,
+   * BWLabel): 1 = run-table form where the tile width is a multiple of 32
+   * (default): each 32x32 tile keeps its row masks, a table of its runs'
+   * local roots and its border pixels' roots instead of a root per pixel,
+   * and a per-tile pass writes the outputs; 0 = a root per pixel.
+   * Identical results. */
+  RTG_OPT_LABEL_RUNS = 8
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 

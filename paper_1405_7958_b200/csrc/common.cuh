@@ -183,6 +183,8 @@ struct rtg_ctx {
   int hmax_impl = 0;  // 0: sparse components, 1: IWPP
   int recon_entry_impl = 0;  // rtg_recon_u8_dev: 0 auto (levels / IWPP), 1 IWPP
   int stream_impl = 1;  // colour deconvolution: 1 TMA bulk-copy ring (default), 0 LDG.128 stream
+  int label_runs = 1;   // stage labellings in run-table form (k_ccl.cu CclRuns) when the shape allows
+  bool ccl_runs_live = false;  // the last ccl_roots left run tables for ccl_canonical
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
@@ -278,8 +280,12 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
 // linear index of p's component (-1 = background).  counts, when given,
 // receives every component's pixel count at its global root.
 // prezeroed: the caller already cleared the counters ccl_label_zero names.
+// runs: the run-table form (k_ccl.cu CclRuns; the roots plane then only
+// holds the local roots' entries) when the shape allows it; only for a
+// ccl_canonical that follows directly.
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
-              int conn, int32_t* roots, int32_t* counts = nullptr, bool prezeroed = false);
+              int conn, int32_t* roots, int32_t* counts = nullptr, bool prezeroed = false,
+              bool runs = false);
 // Appends to z the buffers a labelling CCL (ccl_roots + ccl_canonical) of an
 // h x w mask needs cleared: local-root count, root bitmap, look-back status.
 void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z);
@@ -441,9 +447,10 @@ int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t 
 // threshold decomposition: union-find components of {H >= t} holding a pixel
 // with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.
 // prezeroed: the local-root counter (misc[8]) is already zero.
+// runs: run-table form (uses u16a, u16b and m2 as scratch) when the shape allows.
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out, bool prezeroed = false);
+                       uint8_t* out, bool prezeroed = false, bool runs = false);
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);

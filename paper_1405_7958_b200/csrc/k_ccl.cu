@@ -161,13 +161,28 @@ constexpr uint32_t kSeedBit = 0x80000000u;
 // lowest run of ones of v (bit 0 of v set)
 __device__ __forceinline__ uint32_t low_run(uint32_t v) { return v & ~(v + 1u); }
 
+// Run-table form of a labelling (w % 32 == 0; cf. the joint fill/area
+// labelling's RunTable): instead of a local root for every pixel, each tile
+// leaves its row masks, the ordinal of every run's local root within the
+// tile's contiguous range of the local-root list, and the local roots of its
+// border pixels (all the seams read).  The roots plane then only holds the
+// local roots' own entries (the global forest), and the consumers re-derive a
+// pixel's run from the row mask.
+struct CclRuns {
+  uint32_t* rowbits = nullptr;  // [tile * 32 + r]: foreground bits of row r
+  uint16_t* rtab = nullptr;     // [tile * 512 + r * 16 + k]: ordinal of run k's local root
+  int2* tinfo = nullptr;        // [tile]: (first local-root slot, local-root count)
+  int32_t* border = nullptr;    // [tile * 128 + side * 32 + i]: top row, bottom row, left
+                                // column, right column: local root (global index) or -1
+};
+
 // Runs are named compactly: run k of tile row r is node r * 16 + k (a 32-pixel
 // row holds at most 16 runs), so the per-warp forest is 512 entries.
 template <int CONN, class P>
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ roots,
            int32_t* __restrict__ lroots, int32_t* __restrict__ lcount,
-           int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b) {
+           int32_t* __restrict__ zero_a, int32_t* __restrict__ zero_b, CclRuns rt) {
   pdl_enter();
   __shared__ int32_t s_par[kTileWarps][512];
   __shared__ uint32_t s_inf[kTileWarps][512];
@@ -289,14 +304,47 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   __syncwarp();
   int base = block_reserve(active ? nroot : 0, lcount, s_res);
   if (!active) return;
+  const int32_t tbase = __shfl_sync(kFull, base, 0);  // the tile's roots are contiguous
   for (int k = 0; k < nruns; ++k) {
     if (par[rb + k] != rb + k) continue;
     const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
     lroots[2 * base] = g;
     lroots[2 * base + 1] = (int32_t)inf[rb + k];
+    if (rt.rtab) {
+      inf[rb + k] = (uint32_t)(base - tbase);  // the root's ordinal in the tile
+      roots[g] = g;
+    }
     ++base;
     if (zero_a) zero_a[g] = 0;
     if (zero_b) zero_b[g] = 0;
+  }
+  if (rt.rtab) {
+    __syncwarp();
+    const int32_t tend = __shfl_sync(kFull, base, 31);
+    if (lane == 0) rt.tinfo[tile] = make_int2(tbase, tend - tbase);
+    rt.rowbits[tile * 32 + lane] = bits;
+    // this row's 16 table entries (two 16-byte stores; the warp's are contiguous)
+    uint32_t pk[8];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t o = k < nruns ? inf[par[rb + k]] : 0u;
+      if (k & 1) pk[k >> 1] |= o << 16;
+      else pk[k >> 1] = o;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(rt.rtab + (int64_t)tile * 512 + rb);
+    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    // border pixels: rows 0 and 31 (lane = column), columns 0 and 31 (lane = row)
+    auto glob = [&](int32_t lr) { return (y0 + (lr >> 4)) * w + x0 + (int32_t)pos[lr]; };
+    int32_t* bd = rt.border + (int64_t)tile * 128;
+    const uint32_t below = (2u << lane) - 1u;
+    const uint32_t b0 = __shfl_sync(kFull, bits, 0), b31 = __shfl_sync(kFull, bits, 31);
+    bd[lane] = ((b0 >> lane) & 1u) ? glob(par[__popc(b0 & ~(b0 << 1) & below) - 1]) : -1;
+    bd[32 + lane] =
+        ((b31 >> lane) & 1u) ? glob(par[31 * 16 + __popc(b31 & ~(b31 << 1) & below) - 1]) : -1;
+    bd[64 + lane] = (bits & 1u) ? glob(par[rb]) : -1;
+    bd[96 + lane] = (bits >> 31) ? glob(par[rb + nruns - 1]) : -1;
+    return;
   }
   // global index of every run's local root (inf is free again)
   __syncwarp();
@@ -401,6 +449,59 @@ __global__ void k_ccl_seams(int h, int w, int row_seams, int32_t* __restrict__ r
     seam_row_px<CONN>(h, w, roots, ((int)blockIdx.y + 1) * 32, t);
   else
     seam_col_px<CONN>(h, w, roots, t, ((int)blockIdx.y - row_seams + 1) * 32);
+}
+
+// Seams of the run-table form: the same pairs and skips as seam_row_px /
+// seam_col_px, read from the tiles' border arrays (compact, coalesced) and
+// united through the local roots themselves.
+template <int CONN>
+__global__ void k_ccl_seams_rt(int h, int w, int tiles_x, int row_seams,
+                               const int32_t* __restrict__ border, int32_t* __restrict__ roots) {
+  pdl_enter();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)blockIdx.y < row_seams) {
+    const int y = ((int)blockIdx.y + 1) * 32, x = t;
+    if (x >= w || y >= h) return;
+    const int tb = (y >> 5) * tiles_x;  // the tile row below the seam
+    const int32_t* top = border + (int64_t)(tb + (x >> 5)) * 128;
+    auto bot = [&](int xx) {  // bottom rows of the tile row above
+      return __ldg(border + (int64_t)(tb - tiles_x + (xx >> 5)) * 128 + 32 + (xx & 31));
+    };
+    const int32_t vp = __ldg(top + (x & 31));
+    if (vp < 0) return;
+    const bool in_run_l = (x & 31) != 0 && __ldg(top + (x & 31) - 1) >= 0;  // p ~ left
+    const int32_t vu = bot(x), vul = x > 0 ? bot(x - 1) : -1;
+    const bool fu = vu >= 0, ful = vul >= 0;
+    if (fu && !(in_run_l && ful)) uf_unite_g(roots, vp, vu);
+    if (CONN == 8) {
+      if (ful && !in_run_l && !(fu && (x & 31) != 0)) uf_unite_g(roots, vp, vul);
+      if (x + 1 < w) {
+        const int32_t vur = bot(x + 1);
+        if (vur >= 0 && !(fu && ((x + 1) & 31) != 0)) uf_unite_g(roots, vp, vur);
+      }
+    }
+  } else {
+    const int x = ((int)blockIdx.y - row_seams + 1) * 32, y = t;
+    if (y >= h || x >= w) return;
+    const int tc = x >> 5;  // the tile column right of the seam
+    const int32_t* left = border + (int64_t)((y >> 5) * tiles_x + tc) * 128 + 64;
+    auto rcol = [&](int yy) {  // right columns of the tile column left of the seam
+      return __ldg(border + (int64_t)((yy >> 5) * tiles_x + tc - 1) * 128 + 96 + (yy & 31));
+    };
+    const int32_t vp = __ldg(left + (y & 31));
+    if (vp < 0) return;
+    const bool in_col_u = (y & 31) != 0 && __ldg(left + (y & 31) - 1) >= 0;  // p ~ up
+    const int32_t vl = rcol(y), vul = y > 0 ? rcol(y - 1) : -1;
+    const bool fl = vl >= 0, ful = vul >= 0;
+    if (fl && !(in_col_u && ful)) uf_unite_g(roots, vp, vl);
+    if (CONN == 8) {
+      if (ful && !in_col_u && !(fl && (y & 31) != 0)) uf_unite_g(roots, vp, vul);
+      if (y + 1 < h) {
+        const int32_t vdl = rcol(y + 1);
+        if (vdl >= 0 && !(fl && ((y + 1) & 31) != 0)) uf_unite_g(roots, vp, vdl);
+      }
+    }
+  }
 }
 
 // Flattens the local roots onto the global roots and folds the local
@@ -573,16 +674,17 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
 __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                             const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
                             const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank,
-                            FeatureAcc acc, bool clear_acc) {
+                            FeatureAcc acc, bool clear_acc, bool by_slot) {
   pdl_enter();
   // the final label (rank of the global root + 1) of every LOCAL root, so the
-  // per-pixel relabel needs one gather (local root -> label)
+  // per-pixel relabel needs one gather (local root -> label); by_slot: stored
+  // at the local root's list slot (what k_label_emit stages per tile)
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t lr = lroots[2 * k];
     const int32_t r = roots[lr];
     const int32_t label = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u)) + 1;
-    rank[lr] = label;
+    rank[by_slot ? k : lr] = label;  // run-table form: by local-root slot
     // each label once (at its global root): reset its feature accumulators
     if (clear_acc && lr == r && label <= acc.cap) {
       const int64_t i = label - 1;
@@ -617,6 +719,107 @@ __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
         labels[i] = lr >= 0 ? rank[lr] : 0;
       }
     }
+  }
+}
+
+// Labels of the run-table form: one warp per tile.  The tile's labels (its
+// slice of the by-slot rank array) are staged in shared memory; lane = row
+// resolves its runs' labels, then 8 lanes per row write 4 pixels each
+// (16-byte stores, four rows per step).
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int tiles_x, int ntiles,
+             int32_t* __restrict__ labels, bool vec) {
+  pdl_enter();
+  __shared__ int32_t s_rank[kTileWarps][512];
+  __shared__ int32_t s_lab[kTileWarps][512];
+  __shared__ uint32_t s_bits[kTileWarps][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kTileWarps + wid;
+  if (tile >= ntiles) return;  // no block-wide barrier below
+  const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
+  const int2 ti = __ldg(rt.tinfo + tile);
+  for (int j = lane; j < ti.y; j += 32) s_rank[wid][j] = __ldg(rank + ti.x + j);
+  const uint32_t bits = __ldg(rt.rowbits + tile * 32 + lane);
+  const uint4* src = reinterpret_cast<const uint4*>(rt.rtab + (int64_t)tile * 512 + lane * 16);
+  const uint4 e0 = __ldg(src), e1 = __ldg(src + 1);
+  const uint32_t ew[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+  const int nruns = __popc(bits & ~(bits << 1));
+  s_bits[wid][lane] = bits;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k < nruns) s_lab[wid][lane * 16 + k] = s_rank[wid][(ew[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
+  __syncwarp();
+  const int g = lane >> 3, cq = (lane & 7) * 4;
+#pragma unroll 2
+  for (int k = 0; k < 8; ++k) {
+    const int r = 4 * k + g;
+    if (y0 + r >= h) break;
+    const uint32_t b = s_bits[wid][r], st = b & ~(b << 1);
+    int32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = cq + j;
+      o[j] = ((b >> c) & 1u) ? s_lab[wid][r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : 0;
+    }
+    int32_t* dst = labels + (int64_t)(y0 + r) * w + x0 + cq;
+    if (vec) {
+      *reinterpret_cast<int4*>(dst) = make_int4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = o[j];
+    }
+  }
+}
+
+// Seeded-component mask of the run-table form (ReconToNuclei): keep byte of
+// every local root by slot, then per tile: kept runs & tissue -> out bytes.
+__global__ void k_slot_flag(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
+                            const int32_t* __restrict__ roots, const int32_t* __restrict__ flag,
+                            uint8_t* __restrict__ keep) {
+  pdl_enter();
+  const int n = *lcount;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    keep[k] = flag[roots[lroots[2 * k]]] != 0;
+}
+
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ tissue,
+              int h, int w, int tiles_x, int ntiles, uint8_t* __restrict__ out) {
+  pdl_enter();
+  __shared__ uint8_t s_kp[kTileWarps][512];
+  __shared__ uint32_t s_kept[kTileWarps][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kTileWarps + wid;
+  if (tile >= ntiles) return;
+  const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
+  const int2 ti = __ldg(rt.tinfo + tile);
+  for (int j = lane; j < ti.y; j += 32) s_kp[wid][j] = __ldg(keep + ti.x + j);
+  const uint32_t bits = __ldg(rt.rowbits + tile * 32 + lane);
+  const uint4* src = reinterpret_cast<const uint4*>(rt.rtab + (int64_t)tile * 512 + lane * 16);
+  const uint4 e0 = __ldg(src), e1 = __ldg(src + 1);
+  const uint32_t ew[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+  __syncwarp();
+  uint32_t st = bits & ~(bits << 1), kept = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (!st) break;
+    const int b = __ffs(st) - 1;
+    st &= st - 1;
+    if (s_kp[wid][(ew[k >> 1] >> (16 * (k & 1))) & 0xFFFFu]) kept |= low_run(bits >> b) << b;
+  }
+  s_kept[wid][lane] = kept;
+  __syncwarp();
+  const int g = lane >> 3, cq = (lane & 7) * 4;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int r = 4 * k + g;
+    if (y0 + r >= h) break;
+    const int64_t i = (int64_t)(y0 + r) * w + x0 + cq;
+    const uint32_t nib = (s_kept[wid][r] >> cq) & 0xFu;
+    const uint32_t tv = __ldg(reinterpret_cast<const uint32_t*>(tissue + i));
+    *reinterpret_cast<uint32_t*>(out + i) =
+        (nib * 0x00204081u) & 0x01010101u & __vcmpne4(tv, 0u);
   }
 }
 
@@ -1272,9 +1475,26 @@ __global__ void k_seeded_and(int64_t n, const int32_t* __restrict__ roots,
 // Tile pass + seams + flatten for any foreground predicate.  counts (if
 // given) receive component sizes at the global roots, flags (if given) the
 // OR of the seed bits; bitmap (if given, zeroed here) marks global roots.
+// The run-table buffers for an h x w labelling (u16a: the run table, u16b:
+// row masks, tile ranges and border arrays), or all-null when the form does
+// not apply (w not a multiple of 32, or the tables would not fit).  The
+// planes must be free from the labelling to its consumer (they are between
+// the streaming kernel and the EDT, and after the watershed).
+CclRuns ccl_runs_for(rtg_ctx* ctx, int64_t h, int64_t w) {
+  const int64_t ntiles = ceil_div(w, 32) * ceil_div(h, 32);
+  CclRuns r;
+  if ((w & 31) != 0 || ntiles * 1024 > ctx->max_px) return r;
+  r.rtab = ctx->u16a;
+  r.rowbits = reinterpret_cast<uint32_t*>(ctx->u16b);
+  r.tinfo = reinterpret_cast<int2*>(r.rowbits + ntiles * 32);
+  r.border = reinterpret_cast<int32_t*>(r.tinfo + ntiles);
+  return r;
+}
+
 template <class P>
 int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t* roots,
-            int32_t* counts, int32_t* flags, uint32_t* bitmap, bool prezeroed = false) {
+            int32_t* counts, int32_t* flags, uint32_t* bitmap, bool prezeroed = false,
+            const CclRuns& rt = CclRuns{}) {
   int32_t* lcount = ctx->misc + 8;
   if (!prezeroed) {
     // with a bitmap (the canonical labelling follows): also the look-back
@@ -1290,16 +1510,25 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
   const int ntiles = tiles_x * tiles_y;
   const unsigned grid = (unsigned)ceil_div(ntiles, kTileWarps);
   if (conn == 8)
-    RTG_CUDA(launch_k(ctx, k_ccl_tile<8, P>, grid, 32 * kTileWarps, 0, 
-        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<8, P>, grid, 32 * kTileWarps, 0, pred, (int)h, (int)w,
+                      tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags, rt));
   else
-    RTG_CUDA(launch_k(ctx, k_ccl_tile<4, P>, grid, 32 * kTileWarps, 0, 
-        pred, (int)h, (int)w, tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags));
+    RTG_CUDA(launch_k(ctx, k_ccl_tile<4, P>, grid, 32 * kTileWarps, 0, pred, (int)h, (int)w,
+                      tiles_x, ntiles, roots, ctx->lroots, lcount, counts, flags, rt));
   RTG_LAUNCH("k_ccl_tile");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
-    if (conn == 8) RTG_CUDA(launch_k(ctx, k_ccl_seams<8>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
-    else RTG_CUDA(launch_k(ctx, k_ccl_seams<4>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
+    const int32_t* bd = rt.border;
+    if (rt.rtab && conn == 8)
+      RTG_CUDA(launch_k(ctx, k_ccl_seams_rt<8>, g, 256, 0, (int)h, (int)w, tiles_x, tiles_y - 1,
+                        bd, roots));
+    else if (rt.rtab)
+      RTG_CUDA(launch_k(ctx, k_ccl_seams_rt<4>, g, 256, 0, (int)h, (int)w, tiles_x, tiles_y - 1,
+                        bd, roots));
+    else if (conn == 8)
+      RTG_CUDA(launch_k(ctx, k_ccl_seams<8>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
+    else
+      RTG_CUDA(launch_k(ctx, k_ccl_seams<4>, g, 256, 0, (int)h, (int)w, tiles_y - 1, roots));
     RTG_LAUNCH("k_ccl_seams");
   }
   RTG_CUDA(launch_k(ctx, k_ccl_flatten, ctx->num_sms * 4, 256, 0, ctx->lroots, lcount, roots,
@@ -1312,7 +1541,7 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
 
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out, bool prezeroed) {
+                       uint8_t* out, bool prezeroed, bool runs) {
   (void)scratch;
   const int64_t n = h * w;
   if (t <= 0) {  // R >= t everywhere: the candidates are the tissue mask
@@ -1323,7 +1552,22 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   int32_t* flag = ctx->i32b;
   const int64_t seed_t = (int64_t)t + recon_h;  // > 255: no seed, nothing is reconstructed
   const FgThresh pred{hema, t, seed_t <= 255 ? (int32_t)seed_t : 256};
-  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed));
+  const bool aligned = ((reinterpret_cast<uintptr_t>(tissue) | reinterpret_cast<uintptr_t>(out) |
+                         reinterpret_cast<uintptr_t>(hema)) & 3) == 0;
+  const CclRuns rt = runs && aligned ? ccl_runs_for(ctx, h, w) : CclRuns{};
+  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed, rt));
+  if (rt.rtab) {
+    uint8_t* keep = ctx->m2;  // one byte per local-root slot (free until the joint fill/area)
+    RTG_CUDA(launch_k(ctx, k_slot_flag, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8,
+                      (const int32_t*)roots, (const int32_t*)flag, keep));
+    RTG_LAUNCH("k_slot_flag");
+    const int tiles_x = (int)(w / 32);
+    const int ntiles = tiles_x * (int)ceil_div(h, 32);
+    RTG_CUDA(launch_k(ctx, k_seeded_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
+                      0, rt, (const uint8_t*)keep, tissue, (int)h, (int)w, tiles_x, ntiles, out));
+    RTG_LAUNCH("k_seeded_emit");
+    return RTG_OK;
+  }
   RTG_CUDA(launch_k(ctx, k_seeded_and, grid_for(ctx, n), 256, 0, n, roots, flag, tissue, out));
   RTG_LAUNCH("k_seeded_and");
   return RTG_OK;
@@ -1452,8 +1696,11 @@ int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t 
 }
 
 int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
-              int32_t* roots, int32_t* counts, bool prezeroed) {
-  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed);
+              int32_t* roots, int32_t* counts, bool prezeroed, bool runs) {
+  ctx->ccl_runs_live = runs && counts == nullptr && ccl_runs_for(ctx, h, w).rtab != nullptr;
+  const CclRuns rt = ctx->ccl_runs_live ? ccl_runs_for(ctx, h, w) : CclRuns{};
+  return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed,
+                 rt);
 }
 
 void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
@@ -1477,11 +1724,23 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   RTG_CUDA(launch_k(ctx, k_bm_scan, nchunks, 256, 0, nwords, nchunks, ctx->root_bm, status,
                     ctx->root_wprefix, d_n));
   RTG_LAUNCH("k_bm_scan");
+  // run-table form (ccl_roots left the tables): labels written per tile
+  const bool by_slot = ctx->ccl_runs_live;
+  ctx->ccl_runs_live = false;
   RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
                                                          ctx->root_bm, ctx->root_wprefix, rank,
                                                          clear_acc ? *clear_acc : ctx->acc,
-                                                         clear_acc != nullptr));
+                                                         clear_acc != nullptr, by_slot));
   RTG_LAUNCH("k_root_rank");
+  if (by_slot) {
+    const int tiles_x = (int)(w / 32);
+    const int ntiles = tiles_x * (int)ceil_div(h, 32);
+    RTG_CUDA(launch_k(ctx, k_label_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
+                      0, ccl_runs_for(ctx, h, w), (const int32_t*)rank, (int)h, (int)w, tiles_x,
+                      ntiles, labels, (reinterpret_cast<uintptr_t>(labels) & 15) == 0));
+    RTG_LAUNCH("k_label_emit");
+    return RTG_OK;
+  }
   RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
   return RTG_OK;
@@ -1531,7 +1790,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   // run-table form when rows of tiles are whole words of the bit plane and
   // the tables fit their planes (u16a: 1024 entries per tile; u16b: row
   // masks, then the border arrays; m2: keep bytes; all free until the EDT)
-  const bool runs = (w & 31) == 0 && (int64_t)ntiles * 1024 <= ctx->max_px;
+  const bool runs = ctx->label_runs && (w & 31) == 0 && (int64_t)ntiles * 1024 <= ctx->max_px;
   uint32_t* rowbits = runs ? reinterpret_cast<uint32_t*>(ctx->u16b) : nullptr;
   uint16_t* rtab = runs ? ctx->u16a : nullptr;
   int32_t* border = runs ? reinterpret_cast<int32_t*>(rowbits + (int64_t)ntiles * 32) : nullptr;

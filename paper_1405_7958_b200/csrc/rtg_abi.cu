@@ -143,7 +143,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     RTG_TRY(launch_candidate(ctx, ctx->recon, ctx->tissue, h * w, p->nuc_thresh, ctx->m1));
   } else {
     RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
-                               p->recon_conn, ctx->m1, ctx->m1, /*prezeroed=*/true));
+                               p->recon_conn, ctx->m1, ctx->m1, /*prezeroed=*/true,
+                               ctx->label_runs != 0));
   }
   if (ctx->fill_impl == 0 && ctx->ws_impl == 0) {
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
@@ -176,7 +177,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o8 BWLabel (canonical)
   prof_mark(ctx, RTG_STAGE_LABEL);
   // the tiled watershed cleared the labelling's counters with its own
-  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0));
+  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0,
+                    ctx->label_runs != 0));
   // the ranking pass also resets the feature accumulators of every label
   RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out, with_features ? &ctx->acc : nullptr));
   // o9 features
@@ -217,7 +219,8 @@ int pipeline_graph(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int
                               (int64_t)ctx->recon_impl | ((int64_t)ctx->ws_impl << 8) |
                                   ((int64_t)ctx->hmax_impl << 16) |
                                   ((int64_t)ctx->use_pdl << 24) |
-                                  ((int64_t)ctx->stream_impl << 32)};
+                                  ((int64_t)ctx->stream_impl << 32) |
+                                  ((int64_t)ctx->label_runs << 40)};
   std::memcpy(&key[0], fields, sizeof(fields));
   std::memcpy(&key[sizeof(fields)], p, sizeof(rtg_params));
   if (!ctx->graphs) ctx->graphs = new rtg_ctx::GraphEntry[kGraphCap];
@@ -626,6 +629,10 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
     case RTG_OPT_STREAM_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "stream impl must be 0 or 1");
       ctx->stream_impl = (int)value;
+      return RTG_OK;
+    case RTG_OPT_LABEL_RUNS:
+      if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "label runs must be 0 or 1");
+      ctx->label_runs = (int)value;
       return RTG_OK;
     case RTG_OPT_RECON_ENTRY_IMPL:
       if (value != 0 && value != 1) return fail(RTG_ERR_INVALID_ARG, "recon entry impl must be 0 or 1");

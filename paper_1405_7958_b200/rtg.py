@@ -54,6 +54,7 @@ OPT_HMAX_IMPL = 4        # 0 sparse components (default), 1 IWPP tile queue
 OPT_PDL = 5              # 1 programmatic dependent launch between kernels, 0 off (default)
 OPT_RECON_ENTRY_IMPL = 6  # recon_dev: 0 levels-or-IWPP by input (default), 1 always IWPP
 OPT_STREAM_IMPL = 7       # colour deconvolution: 1 TMA bulk ring (default), 0 LDG.128 stream
+OPT_LABEL_RUNS = 8        # stage labellings in run-table form (1, default) or a root per pixel (0)
 STAGES = ["colordeconv", "recon", "fill_holes", "area", "edt", "markers", "watershed",
           "label", "features", "texture"]
 

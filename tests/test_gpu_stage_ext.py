@@ -480,3 +480,47 @@ def test_colordeconv_tma_ring_matches_stream(rtg, oracle, shape):
             outs.append(ctx.process_tile(rgb, p))
         assert outs[0][4] == outs[1][4] and np.array_equal(outs[0][1], outs[1][1])
         assert np.array_equal(outs[0][3], outs[1][3])
+
+
+# ------------------------------------------------- run-table labellings (RTG_OPT_LABEL_RUNS)
+
+@pytest.mark.parametrize("shape,rc,conn", [((4096, 4096), (5, 7), 8), ((1000, 1024), (3, 9), 8),
+                                           ((777, 1696), (24, 1), 4), ((96, 64), (1, 1), 8),
+                                           ((33, 32), (2, 5), 8), ((1000, 1000), (4, 4), 8)])
+def test_label_runs_match_per_pixel_roots(rtg, oracle, shape, rc, conn):
+    """The run-table labellings (row masks + run tables + border roots, per-
+    tile output passes) give the same mask, labels and feature rows as the
+    per-pixel-root form, and both equal the oracle (w % 32 != 0 runs the
+    per-pixel form either way)."""
+    _need_gpu()
+    h, w = shape
+    rgb = rtg.synth_tile_host(rc[0], rc[1], h, w)
+    p = rtg.default_params()
+    p.recon_conn = conn
+    outs = []
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        for runs in (1, 0):
+            ctx.set_option(rtg.OPT_LABEL_RUNS, runs)
+            outs.append(ctx.process_tile(rgb, p))
+            # the device entry point (graph replay) and the async one agree
+            d_rgb = torch.from_numpy(rgb).cuda()
+            d_mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+            d_lab = torch.empty((h, w), dtype=torch.int32, device="cuda")
+            d_feat = torch.empty((1 << 15, 20), dtype=torch.float32, device="cuda")
+            d_n = torch.zeros(1, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            for _ in range(2):
+                ctx.process_tile_dev(d_rgb, h, w, p, d_mask, d_lab, None, d_feat, d_n)
+            ctx.sync()
+            assert int(d_n.item()) == outs[-1][4]
+            assert np.array_equal(d_mask.cpu().numpy(), outs[-1][0])
+            assert np.array_equal(d_lab.cpu().numpy(), outs[-1][1])
+    a, b = outs
+    assert a[4] == b[4] and np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[3], b[3])
+    if h * w <= 1 << 20:
+        op = oracle.default_params()
+        op.recon_conn = conn
+        ref = oracle.process_tile(rgb, op)
+        assert a[4] == ref["n"] and np.array_equal(a[1], ref["labels"])
+        np.testing.assert_allclose(a[3], ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
