@@ -185,6 +185,7 @@ struct rtg_ctx {
   int stream_impl = 1;  // colour deconvolution: 1 TMA bulk-copy ring (default), 0 LDG.128 stream
   int label_runs = 1;   // stage labellings in run-table form (k_ccl.cu CclRuns) when the shape allows
   bool ccl_runs_live = false;  // the last ccl_roots left run tables for ccl_canonical
+  bool cand_bits = false;      // recon left the candidates as row masks (fill_area_joint reads them)
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
@@ -447,10 +448,13 @@ int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t 
 // threshold decomposition: union-find components of {H >= t} holding a pixel
 // with H >= t + h.  scratch may alias out; scratch must differ from hema/tissue.
 // prezeroed: the local-root counter (misc[8]) is already zero.
-// runs: run-table form (uses u16a, u16b and m2 as scratch) when the shape allows.
+// runs: run-table form (uses u16a, u16b and m2 as scratch) when the shape allows;
+// bits_out: in that form `out` receives the candidates as tile row masks
+// (ctx->cand_bits says whether it did) for the joint fill/area labelling.
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out, bool prezeroed = false, bool runs = false);
+                       uint8_t* out, bool prezeroed = false, bool runs = false,
+                       bool bits_out = false);
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);

@@ -785,10 +785,12 @@ __global__ void k_slot_flag(const int32_t* __restrict__ lroots, const int32_t* _
 
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ tissue,
-              int h, int w, int tiles_x, int ntiles, uint8_t* __restrict__ out) {
+              int h, int w, int tiles_x, int ntiles, uint8_t* __restrict__ out,
+              uint32_t* __restrict__ out_bits) {
   pdl_enter();
   __shared__ uint8_t s_kp[kTileWarps][512];
   __shared__ uint32_t s_kept[kTileWarps][32];
+  __shared__ uint32_t s_tis[kTileWarps][32];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kTileWarps + wid;
   if (tile >= ntiles) return;
@@ -811,6 +813,27 @@ k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __res
   s_kept[wid][lane] = kept;
   __syncwarp();
   const int g = lane >> 3, cq = (lane & 7) * 4;
+  if (out_bits) {
+    // row masks of (kept & tissue) for the joint fill/area tile kernel
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + g;
+      uint32_t tn = 0;
+      if (y0 + r < h) {
+        const uint32_t tv = __ldg(reinterpret_cast<const uint32_t*>(
+            tissue + (int64_t)(y0 + r) * w + x0 + cq));
+        tn = ((~__vcmpeq4(tv, 0u) & 0x80808080u) * 0x00204081u) >> 28;  // byte MSBs -> nibble
+      }
+      uint32_t v = tn << cq;
+      v |= __shfl_xor_sync(kFull, v, 1);
+      v |= __shfl_xor_sync(kFull, v, 2);
+      v |= __shfl_xor_sync(kFull, v, 4);
+      if ((lane & 7) == 0) s_tis[wid][r] = v;
+    }
+    __syncwarp();
+    out_bits[tile * 32 + lane] = kept & s_tis[wid][lane];
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int r = 4 * k + g;
@@ -930,6 +953,10 @@ struct RunTable {
     const int32_t off = rtab[(int64_t)tile * 1024 + r * 32 + k];
     return (y - r + (off >> 5)) * w + (x - c) + (off & 31);
   }
+  __device__ __forceinline__ bool fg(int32_t q) const {
+    const int y = q / w, x = q - y * w;
+    return (rowbits[((y >> 5) * tiles_x + (x >> 5)) * 32 + (y & 31)] >> (x & 31)) & 1u;
+  }
 };
 
 __global__ void __launch_bounds__(32 * kTileWarps)
@@ -937,7 +964,8 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
               int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
               int32_t* __restrict__ lcount, int32_t* __restrict__ counts,
               int32_t* __restrict__ total, uint32_t* __restrict__ rowbits,
-              uint16_t* __restrict__ rtab, int32_t* __restrict__ border) {
+              uint16_t* __restrict__ rtab, int32_t* __restrict__ border,
+              const uint32_t* __restrict__ in_bits) {
   pdl_enter();
   __shared__ FbSmem<kTileWarps> S;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -954,7 +982,10 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const int x = x0 + lane;
   const bool vec = (w & 3) == 0 && x0 + 32 <= w && (reinterpret_cast<uintptr_t>(m) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
-  if (vec) {
+  if (in_bits) {
+    // the candidates as row masks (k_seeded_emit), the run-table layout
+    fgb = __ldg(in_bits + tile * 32 + lane);
+  } else if (vec) {
     const int g = lane >> 3, cq = (lane & 7) * 4;
     uint32_t word[8];
 #pragma unroll
@@ -1079,23 +1110,28 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   if (rtab) {
     // 4'. row masks, run table (the whole 2 KB forest, coalesced), and the
     //     local roots of the tile-border pixels
-    rowbits[tile * 32 + lane] = fgb;
+    if (rowbits != in_bits) rowbits[tile * 32 + lane] = fgb;
     {
       const uint4* src = reinterpret_cast<const uint4*>(par);
       uint4* dst = reinterpret_cast<uint4*>(rtab + (int64_t)tile * 1024);
 #pragma unroll
       for (int j = 0; j < 4; ++j) dst[lane + 32 * j] = src[lane + 32 * j];
     }
-    auto glob = [&](int32_t lo) { return (y0 + (lo >> 5)) * w + x0 + (lo & 31); };
+    // border entries: local root (global index), bit 31 set for foreground
+    auto glob = [&](int32_t lo, uint32_t fg) {
+      return (int32_t)((uint32_t)((y0 + (lo >> 5)) * w + x0 + (lo & 31)) | (fg << 31));
+    };
     int32_t* bd = border + (int64_t)tile * 128;
     // rows 0 and 31 (lane = column; a partial last row has no seam below),
     // columns 0 and 31 (lane = row: the row's first and last runs)
     const uint32_t below = (2u << lane) - 1u;
-    bd[lane] = glob(par[__popc(__shfl_sync(kFull, allst, 0) & below) - 1]);
-    bd[32 + lane] = glob(par[31 * 32 + __popc(__shfl_sync(kFull, allst, 31) & below) - 1]);
+    const uint32_t f0 = __shfl_sync(kFull, fgb, 0), f31 = __shfl_sync(kFull, fgb, 31);
+    bd[lane] = glob(par[__popc(__shfl_sync(kFull, allst, 0) & below) - 1], (f0 >> lane) & 1u);
+    bd[32 + lane] =
+        glob(par[31 * 32 + __popc(__shfl_sync(kFull, allst, 31) & below) - 1], (f31 >> lane) & 1u);
     if (yr < h) {
-      bd[64 + lane] = glob(par[rb]);
-      bd[96 + lane] = glob(par[rb + nruns - 1]);
+      bd[64 + lane] = glob(par[rb], fgb & 1u);
+      bd[96 + lane] = glob(par[rb + nruns - 1], fgb >> 31);
     }
     return;
   }
@@ -1143,41 +1179,27 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
 
 // Seams of the joint labelling: foreground pairs 8-connected, background
 // pairs 4-connected, with the same redundancy skips as k_ccl_seams.
-// node(pixel, which) names the forest node a pixel unites through: the
-// pixel itself in the per-pixel form, its local root (read from the tile
-// border arrays) in the run-table form; which = 0 for p, 1 for q, 2 for qa,
-// 3 for qb.
-template <class Node>
 __device__ __forceinline__ void seam_fb(const uint8_t* __restrict__ m, int32_t* __restrict__ roots,
                                         int32_t p, int32_t q, int32_t p2, int32_t q2,
                                         bool has_prev, int32_t qa, bool has_qa, int32_t qb,
-                                        bool has_qb, bool pref_b, bool next_b, const Node& node) {
+                                        bool has_qb, bool pref_b, bool next_b) {
   // p: seam pixel, q: its partner across the seam; p2/q2: the pair one step
   // back along the seam (valid when has_prev, same tiles); qa/qb: q's
   // neighbours one step back/forward along the seam (the 8-conn diagonals)
   const bool fp = m[p] != 0;
   const bool fq = m[q] != 0;
   if (!fp) {  // background: 4-connected straight pair only
-    if (!fq && !(has_prev && !m[p2] && !m[q2])) uf_unite_g(roots, node(p, 0), node(q, 1));
+    if (!fq && !(has_prev && !m[p2] && !m[q2])) uf_unite_g(roots, p, q);
     return;
   }
   const bool in_prev = has_prev && m[p2] != 0;  // p ~ p2 (same tile, same kind)
   const bool fqa = has_qa && m[qa] != 0;
-  const bool uq = fq && !(in_prev && fqa);
-  const bool uqa = fqa && !in_prev && !(fq && pref_b);
-  const bool uqb = has_qb && m[qb] != 0 && !(fq && next_b);
-  if (!(uq | uqa | uqb)) return;
-  const int32_t np = node(p, 0);
-  if (uq) uf_unite_g(roots, np, node(q, 1));
-  if (uqa) uf_unite_g(roots, np, node(qa, 2));
-  if (uqb) uf_unite_g(roots, np, node(qb, 3));
+  if (fq && !(in_prev && fqa)) uf_unite_g(roots, p, q);
+  if (fqa && !in_prev && !(fq && pref_b)) uf_unite_g(roots, p, qa);
+  if (has_qb && m[qb] != 0 && !(fq && next_b)) uf_unite_g(roots, p, qb);
 }
 
-// border (run-table form, nullptr otherwise): per tile 128 local roots (global
-// indices) of its top row, bottom row, left column and right column, in that
-// order, 32 each.
-__global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x,
-                               int row_seams, const int32_t* __restrict__ border,
+__global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int row_seams,
                                int32_t* __restrict__ roots) {
   pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1185,28 +1207,65 @@ __global__ void k_ccl_seams_fb(const uint8_t* __restrict__ m, int h, int w, int 
     const int y = ((int)blockIdx.y + 1) * 32, x = t;
     if (x >= w || y >= h) return;
     const int32_t p = y * w + x, u = p - w;
-    const int tb = (y >> 5) * tiles_x;  // first tile of the row below the seam
-    auto node = [&](int32_t q, int which) -> int32_t {
-      if (!border) return q;
-      if (which == 0) return __ldg(border + (tb + (x >> 5)) * 128 + (x & 31));
-      const int xx = q - u + x;  // q lies in the row above: bottom rows of that tile row
-      return __ldg(border + (tb - tiles_x + (xx >> 5)) * 128 + 32 + (xx & 31));
-    };
     seam_fb(m, roots, p, u, p - 1, u - 1, (x & 31) != 0, u - 1, x > 0, u + 1, x + 1 < w,
-            (x & 31) != 0, ((x + 1) & 31) != 0, node);
+            (x & 31) != 0, ((x + 1) & 31) != 0);
   } else {
     const int x = ((int)blockIdx.y - row_seams + 1) * 32, y = t;
     if (y >= h || x >= w) return;
     const int32_t p = y * w + x, l = p - 1;
-    const int tc = x >> 5;  // tile column right of the seam
-    auto node = [&](int32_t q, int which) -> int32_t {
-      if (!border) return q;
-      if (which == 0) return __ldg(border + ((y >> 5) * tiles_x + tc) * 128 + 64 + (y & 31));
-      const int yy = y + (which == 2 ? -1 : which == 3 ? 1 : 0);  // right column of the left tile
-      return __ldg(border + ((yy >> 5) * tiles_x + tc - 1) * 128 + 96 + (yy & 31));
-    };
     seam_fb(m, roots, p, l, p - w, l - w, (y & 31) != 0, l - w, y > 0, l + w, y + 1 < h,
-            (y & 31) != 0, ((y + 1) & 31) != 0, node);
+            (y & 31) != 0, ((y + 1) & 31) != 0);
+  }
+}
+
+// The same seams in the run-table form, from the tiles' border arrays alone
+// (per tile 128 entries: top row, bottom row, left column, right column;
+// local root with bit 31 = foreground): coalesced loads, no mask reads.  The
+// pair one step back across the seam (q2) is always qa.
+__device__ __forceinline__ void seam_fb_rt(int32_t* __restrict__ roots, int32_t vp, int32_t vq,
+                                           int32_t vp2, bool has_prev, int32_t vqa, bool has_qa,
+                                           int32_t vqb, bool has_qb, bool pref_b, bool next_b) {
+  constexpr int32_t kIdx = 0x7FFFFFFF;
+  const bool fp = vp < 0, fq = vq < 0;
+  if (!fp) {
+    if (!fq && !(has_prev && vp2 >= 0 && vqa >= 0)) uf_unite_g(roots, vp, vq);
+    return;
+  }
+  const bool in_prev = has_prev && vp2 < 0;
+  const bool fqa = has_qa && vqa < 0;
+  if (fq && !(in_prev && fqa)) uf_unite_g(roots, vp & kIdx, vq & kIdx);
+  if (fqa && !in_prev && !(fq && pref_b)) uf_unite_g(roots, vp & kIdx, vqa & kIdx);
+  if (has_qb && vqb < 0 && !(fq && next_b)) uf_unite_g(roots, vp & kIdx, vqb & kIdx);
+}
+
+__global__ void k_ccl_seams_fb_rt(int h, int w, int tiles_x, int row_seams,
+                                  const int32_t* __restrict__ border, int32_t* __restrict__ roots) {
+  pdl_enter();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)blockIdx.y < row_seams) {
+    const int y = ((int)blockIdx.y + 1) * 32, x = t;
+    if (x >= w || y >= h) return;
+    const int tb = (y >> 5) * tiles_x;  // the tile row below the seam
+    const int32_t* top = border + (int64_t)(tb + (x >> 5)) * 128;
+    auto bot = [&](int xx) {
+      return __ldg(border + (int64_t)(tb - tiles_x + (xx >> 5)) * 128 + 32 + (xx & 31));
+    };
+    const bool has_prev = (x & 31) != 0, has_qa = x > 0, has_qb = x + 1 < w;
+    seam_fb_rt(roots, __ldg(top + (x & 31)), bot(x), has_prev ? __ldg(top + (x & 31) - 1) : 0,
+               has_prev, has_qa ? bot(x - 1) : 0, has_qa, has_qb ? bot(x + 1) : 0, has_qb,
+               (x & 31) != 0, ((x + 1) & 31) != 0);
+  } else {
+    const int x = ((int)blockIdx.y - row_seams + 1) * 32, y = t;
+    if (y >= h || x >= w) return;
+    const int tc = x >> 5;  // the tile column right of the seam
+    const int32_t* left = border + (int64_t)((y >> 5) * tiles_x + tc) * 128 + 64;
+    auto rcol = [&](int yy) {
+      return __ldg(border + (int64_t)((yy >> 5) * tiles_x + tc - 1) * 128 + 96 + (yy & 31));
+    };
+    const bool has_prev = (y & 31) != 0, has_qa = y > 0, has_qb = y + 1 < h;
+    seam_fb_rt(roots, __ldg(left + (y & 31)), rcol(y), has_prev ? __ldg(left + (y & 31) - 1) : 0,
+               has_prev, has_qa ? rcol(y - 1) : 0, has_qa, has_qb ? rcol(y + 1) : 0, has_qb,
+               (y & 31) != 0, ((y + 1) & 31) != 0);
   }
 }
 
@@ -1226,7 +1285,7 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
     const int32_t r = lroots[2 * k];
     if (roots[r] != r) continue;
     int32_t cur = r, t = -1;
-    bool fg = m[r] != 0;
+    bool fg = rt.rtab ? rt.fg(r) : m[r] != 0;
     if (fg || !(counts[r] & (int32_t)kSeedBit)) {
       for (int guard = 0; guard < (1 << 20); ++guard) {  // nesting depth, never reached
         if (fg) {
@@ -1541,9 +1600,10 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
 
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out, bool prezeroed, bool runs) {
+                       uint8_t* out, bool prezeroed, bool runs, bool bits_out) {
   (void)scratch;
   const int64_t n = h * w;
+  ctx->cand_bits = false;
   if (t <= 0) {  // R >= t everywhere: the candidates are the tissue mask
     RTG_CUDA(cudaMemcpyAsync(out, tissue, (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
     return RTG_OK;
@@ -1563,8 +1623,10 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
     RTG_LAUNCH("k_slot_flag");
     const int tiles_x = (int)(w / 32);
     const int ntiles = tiles_x * (int)ceil_div(h, 32);
+    ctx->cand_bits = bits_out;
     RTG_CUDA(launch_k(ctx, k_seeded_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
-                      0, rt, (const uint8_t*)keep, tissue, (int)h, (int)w, tiles_x, ntiles, out));
+                      0, rt, (const uint8_t*)keep, tissue, (int)h, (int)w, tiles_x, ntiles, out,
+                      bits_out ? reinterpret_cast<uint32_t*>(out) : (uint32_t*)nullptr));
     RTG_LAUNCH("k_seeded_emit");
     return RTG_OK;
   }
@@ -1791,17 +1853,25 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   // the tables fit their planes (u16a: 1024 entries per tile; u16b: row
   // masks, then the border arrays; m2: keep bytes; all free until the EDT)
   const bool runs = ctx->label_runs && (w & 31) == 0 && (int64_t)ntiles * 1024 <= ctx->max_px;
+  // the candidates may arrive as row masks (recon_threshold_uf, bits_out)
+  const uint32_t* in_bits = ctx->cand_bits ? reinterpret_cast<const uint32_t*>(cand) : nullptr;
+  ctx->cand_bits = false;
+  if (in_bits && !runs) return fail(RTG_ERR_INTERNAL, "candidate row masks without run tables");
   uint32_t* rowbits = runs ? reinterpret_cast<uint32_t*>(ctx->u16b) : nullptr;
+  if (in_bits) rowbits = const_cast<uint32_t*>(in_bits);
   uint16_t* rtab = runs ? ctx->u16a : nullptr;
   int32_t* border = runs ? reinterpret_cast<int32_t*>(rowbits + (int64_t)ntiles * 32) : nullptr;
   const unsigned tgrid = (unsigned)ceil_div(ntiles, kTileWarps);
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, tgrid, 32 * kTileWarps, 0, cand, (int)h, (int)w, tiles_x,
-                    ntiles, roots, ctx->lroots, lcount, counts, total, rowbits, rtab, border));
+                    ntiles, roots, ctx->lroots, lcount, counts, total, rowbits, rtab, border, in_bits));
   RTG_LAUNCH("k_ccl_tile_fb");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
-    RTG_CUDA(launch_k(ctx, k_ccl_seams_fb, g, 256, 0, cand, (int)h, (int)w, tiles_x, tiles_y - 1,
-                      (const int32_t*)border, roots));
+    if (runs)
+      RTG_CUDA(launch_k(ctx, k_ccl_seams_fb_rt, g, 256, 0, (int)h, (int)w, tiles_x, tiles_y - 1,
+                        (const int32_t*)border, roots));
+    else
+      RTG_CUDA(launch_k(ctx, k_ccl_seams_fb, g, 256, 0, cand, (int)h, (int)w, tiles_y - 1, roots));
     RTG_LAUNCH("k_ccl_seams_fb");
   }
   const int gl = ctx->num_sms * 4;

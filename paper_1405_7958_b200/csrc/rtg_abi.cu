@@ -124,6 +124,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   int32_t* labels = d_labels ? d_labels : ctx->labels;
   int32_t* n_out = d_n ? d_n : ctx->misc;
   const bool iwpp_recon = ctx->recon_impl == 1;
+  ctx->cand_bits = false;
+  ctx->ccl_runs_live = false;
   // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
   // the streaming kernel's first CTA clears the reconstruction CCL's
@@ -144,7 +146,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   } else {
     RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
                                p->recon_conn, ctx->m1, ctx->m1, /*prezeroed=*/true,
-                               ctx->label_runs != 0));
+                               ctx->label_runs != 0, /*bits_out=*/joint));
   }
   if (ctx->fill_impl == 0 && ctx->ws_impl == 0) {
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
