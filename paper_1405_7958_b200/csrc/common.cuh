@@ -464,8 +464,10 @@ int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
 // misc[4], ctx->fg_bits) for the sparse watershed.
 // prezeroed: its counters (misc[9], misc[4]) and the bit-plane pads were
 // cleared upstream (the streaming kernel's ClearList).
+// out_bytes = false: in the run-table form `out` is not written (the list
+// and the bit plane are the output; the sparse watershed reads only those).
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out, bool prezeroed = false);
+                    int32_t max_area, uint8_t* out, bool prezeroed = false, bool out_bytes = true);
 // What fill_area_joint needs cleared, as a ClearList.
 ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,
@@ -483,7 +485,7 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 constexpr int kBitPad = 2;
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base);
-int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int32_t* list,
+int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
              const int32_t* count, const uint32_t* bits_base, uint16_t* dq);
 // basin doubles as i32 scratch; the ids are only written when want_basin.
 // list_ready: ctx->fg_list / misc[4] / fg_bits already describe `mask`.

@@ -935,14 +935,16 @@ struct __align__(16) FbSmem {
 };
 
 // Run-table form (w % 32 == 0): instead of a root for every pixel, each tile
-// leaves its row bit masks and the tile-local offset of every run's local
-// root; the per-pixel roots plane then only holds the tile-border pixels
-// (all the seams read) and the local roots themselves (the global forest).
-// A pixel's local root is re-derived from the row mask (run index = number
-// of run starts up to its column) and one table entry.
+// leaves its row bit masks, the ordinal of every run's local root within the
+// tile's contiguous slice of the local-root list, and its border pixels'
+// local roots; the roots plane then only holds the local roots themselves
+// (the global forest).  A pixel's local root is re-derived from the row mask
+// (run index = number of run starts up to its column) and one table entry.
 struct RunTable {
   const uint32_t* rowbits;  // [tile * 32 + r]: foreground bits of row r of the tile
-  const uint16_t* rtab;     // [tile * 1024 + r * 32 + k]: row * 32 + col of run k's local root
+  const uint16_t* rtab;     // [tile * 1024 + r * 32 + k]: ordinal of run k's local root
+  const int2* tinfo;        // [tile]: (first local-root slot, local-root count)
+  const int32_t* lroots;    // the local-root list (global index, accumulator) pairs
   int w, tiles_x;
   __device__ __forceinline__ int32_t local_root(int32_t q) const {
     const int y = q / w, x = q - y * w;
@@ -950,8 +952,7 @@ struct RunTable {
     const uint32_t fgb = rowbits[tile * 32 + r], bgb = ~fgb;
     const uint32_t st = (fgb & ~(fgb << 1)) | (bgb & ~(bgb << 1));
     const int k = __popc(st & ((2u << c) - 1u)) - 1;
-    const int32_t off = rtab[(int64_t)tile * 1024 + r * 32 + k];
-    return (y - r + (off >> 5)) * w + (x - c) + (off & 31);
+    return lroots[2 * (tinfo[tile].x + rtab[(int64_t)tile * 1024 + r * 32 + k])];
   }
   __device__ __forceinline__ bool fg(int32_t q) const {
     const int y = q / w, x = q - y * w;
@@ -964,8 +965,8 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
               int32_t* __restrict__ roots, int32_t* __restrict__ lroots,
               int32_t* __restrict__ lcount, int32_t* __restrict__ counts,
               int32_t* __restrict__ total, uint32_t* __restrict__ rowbits,
-              uint16_t* __restrict__ rtab, int32_t* __restrict__ border,
-              const uint32_t* __restrict__ in_bits) {
+              uint16_t* __restrict__ rtab, int2* __restrict__ tinfo,
+              int32_t* __restrict__ border, const uint32_t* __restrict__ in_bits) {
   pdl_enter();
   __shared__ FbSmem<kTileWarps> S;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1089,37 +1090,31 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   __syncwarp();
   int base = block_reserve(active ? nroot : 0, lcount, s_res);
   if (!active) return;
+  const int32_t tbase = __shfl_sync(kFull, base, 0);  // the tile's roots are contiguous
   for (int k = 0; k < nruns; ++k) {
     if (par[rb + k] != rb + k) continue;
     const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
     const uint32_t a = acc16[rb + k];
     lroots[2 * base] = g;
     lroots[2 * base + 1] = (int32_t)((a & 0x7FFFu) | ((a & 0x8000u) ? kSeedBit : 0u));
-    ++base;
     counts[g] = 0;
     total[g] = 0;  // subtree areas are accumulated straight from k_fb_tree
-    if (rtab) roots[g] = g;
-  }
-  __syncwarp();
-  // each lane rewrites only its own runs' entries
-  for (int k = 0; k < nruns; ++k) {
-    const int32_t lr = par[rb + k];
-    par[rb + k] = (uint16_t)((lr & ~31) | pos[lr]);
+    if (rtab) {
+      roots[g] = g;
+      acc16[rb + k] = (uint16_t)(base - tbase);  // the root's ordinal in the tile
+    }
+    ++base;
   }
   __syncwarp();
   if (rtab) {
-    // 4'. row masks, run table (the whole 2 KB forest, coalesced), and the
-    //     local roots of the tile-border pixels
+    // 4'. row masks, tile range, border local roots, and the run table (the
+    //     ordinal of every run's local root: the 2 KB forest, coalesced)
     if (rowbits != in_bits) rowbits[tile * 32 + lane] = fgb;
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(par);
-      uint4* dst = reinterpret_cast<uint4*>(rtab + (int64_t)tile * 1024);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dst[lane + 32 * j] = src[lane + 32 * j];
-    }
+    const int32_t tend = __shfl_sync(kFull, base, 31);
+    if (lane == 0) tinfo[tile] = make_int2(tbase, tend - tbase);
     // border entries: local root (global index), bit 31 set for foreground
-    auto glob = [&](int32_t lo, uint32_t fg) {
-      return (int32_t)((uint32_t)((y0 + (lo >> 5)) * w + x0 + (lo & 31)) | (fg << 31));
+    auto glob = [&](int32_t lr, uint32_t fg) {
+      return (int32_t)((uint32_t)((y0 + (lr >> 5)) * w + x0 + pos[lr]) | (fg << 31));
     };
     int32_t* bd = border + (int64_t)tile * 128;
     // rows 0 and 31 (lane = column; a partial last row has no seam below),
@@ -1127,14 +1122,27 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
     const uint32_t below = (2u << lane) - 1u;
     const uint32_t f0 = __shfl_sync(kFull, fgb, 0), f31 = __shfl_sync(kFull, fgb, 31);
     bd[lane] = glob(par[__popc(__shfl_sync(kFull, allst, 0) & below) - 1], (f0 >> lane) & 1u);
-    bd[32 + lane] =
-        glob(par[31 * 32 + __popc(__shfl_sync(kFull, allst, 31) & below) - 1], (f31 >> lane) & 1u);
+    const uint32_t st31 = __shfl_sync(kFull, allst, 31);
+    if (y0 + 31 < h) bd[32 + lane] = glob(par[31 * 32 + __popc(st31 & below) - 1], (f31 >> lane) & 1u);
     if (yr < h) {
       bd[64 + lane] = glob(par[rb], fgb & 1u);
       bd[96 + lane] = glob(par[rb + nruns - 1], fgb >> 31);
     }
+    __syncwarp();
+    for (int k = 0; k < nruns; ++k) par[rb + k] = acc16[par[rb + k]];  // own entries only
+    __syncwarp();
+    const uint4* src = reinterpret_cast<const uint4*>(par);
+    uint4* dst = reinterpret_cast<uint4*>(rtab + (int64_t)tile * 1024);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dst[lane + 32 * j] = src[lane + 32 * j];
     return;
   }
+  // each lane rewrites only its own runs' entries
+  for (int k = 0; k < nruns; ++k) {
+    const int32_t lr = par[rb + k];
+    par[rb + k] = (uint16_t)((lr & ~31) | pos[lr]);
+  }
+  __syncwarp();
   // 4. every valid pixel's local root
   if (vec) {
     const int g = lane >> 3, cq = (lane & 7) * 4;
@@ -1309,13 +1317,12 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
 // The keep decision of every LOCAL root (global root -> top-level ancestor
 // -> subtree area in range), stored at the local root's pixel: the per-pixel
 // filter then needs one byte gather instead of three dependent i32 ones.
-// With a run table (tiles_x > 0) it is stored in tile-major order instead
-// (tile * 1024 + row * 32 + col), so k_fb_emit reads a tile's bytes as one
-// contiguous kilobyte.
+// Run-table form (by_slot): stored at the local root's list slot instead,
+// so k_fb_emit reads a tile's keep bytes as one contiguous slice.
 __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
                           const int32_t* __restrict__ total, int32_t lo, int32_t hi,
-                          uint8_t* __restrict__ keep, int w, int tiles_x) {
+                          uint8_t* __restrict__ keep, bool by_slot) {
   pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -1326,25 +1333,21 @@ __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __r
       const int32_t a = total[t];
       kp = a >= lo && a <= hi;
     }
-    int64_t at = lr;
-    if (tiles_x > 0) {
-      const int y = lr / w, x = lr - y * w;
-      at = (int64_t)((y >> 5) * tiles_x + (x >> 5)) * 1024 + (y & 31) * 32 + (x & 31);
-    }
-    keep[at] = kp ? 1 : 0;
+    keep[by_slot ? k : lr] = kp ? 1 : 0;
   }
 }
 
 // Output of the run-table form: one warp per tile, lane = row.  A run is
-// kept when its local root's keep byte (the tile's kilobyte, staged in
-// shared memory) is set; the row's kept bits become its 32 mask bytes, its
+// kept when its local root's keep byte (the tile's slice, staged in shared
+// memory) is set; the row's kept bits become its 32 mask bytes, its
 // word of the 1-bit plane, and its foreground-list entries.  List slots are
 // ordered row-major over the block's tiles, so list neighbours stay row
 // neighbours (the feature pass reduces runs of them); the block's entries
 // are staged in shared memory and leave as one contiguous range.
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rtab,
-          const uint8_t* __restrict__ keep, int h, int w, int tiles_x, int ntiles,
+          const int2* __restrict__ tinfo, const uint8_t* __restrict__ keep, int h, int w,
+          int tiles_x, int ntiles,
           uint8_t* __restrict__ out, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
           int32_t* __restrict__ count) {
   pdl_enter();
@@ -1360,10 +1363,8 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
   const int y = y0 + lane;
   const bool row = active && y < h;
   {
-    const uint4* kt = reinterpret_cast<const uint4*>(keep + (int64_t)tile * 1024);
-    uint4* sk = reinterpret_cast<uint4*>(s_keep[wid]);
-    sk[lane] = __ldg(kt + lane);
-    sk[lane + 32] = __ldg(kt + lane + 32);
+    const int2 ti = __ldg(tinfo + tile);  // the tile's keep bytes (by local-root slot)
+    for (int j = lane; j < ti.y; j += 32) s_keep[wid][j] = __ldg(keep + ti.x + j);
   }
   const uint32_t fgb = row ? __ldg(rowbits + tile * 32 + lane) : 0u;
   const uint32_t bgb = row ? ~fgb : 0u;
@@ -1388,8 +1389,9 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
   s_kept[wid][lane] = kept;
   if (row) bits[((int64_t)y * w + x0) >> 5] = kept;
   __syncwarp();
-  // mask bytes: 8 lanes per row, four rows per store (full 32-byte sectors)
-  if (active) {
+  // mask bytes (when a consumer reads them): 8 lanes per row, four rows per
+  // store (full 32-byte sectors)
+  if (active && out) {
     const int g = lane >> 3, cq = (lane & 7) * 4;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -1827,7 +1829,7 @@ ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w) {
 }
 
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out, bool prezeroed) {
+                    int32_t max_area, uint8_t* out, bool prezeroed, bool out_bytes) {
   const int64_t n = h * w;
   int32_t* roots = ctx->i32a;
   int32_t* counts = ctx->i32b;
@@ -1860,10 +1862,14 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   uint32_t* rowbits = runs ? reinterpret_cast<uint32_t*>(ctx->u16b) : nullptr;
   if (in_bits) rowbits = const_cast<uint32_t*>(in_bits);
   uint16_t* rtab = runs ? ctx->u16a : nullptr;
-  int32_t* border = runs ? reinterpret_cast<int32_t*>(rowbits + (int64_t)ntiles * 32) : nullptr;
+  int2* tinfo = runs ? reinterpret_cast<int2*>(reinterpret_cast<uint32_t*>(ctx->u16b) +
+                                               (int64_t)ntiles * 32)
+                    : nullptr;
+  int32_t* border = runs ? reinterpret_cast<int32_t*>(tinfo + ntiles) : nullptr;
   const unsigned tgrid = (unsigned)ceil_div(ntiles, kTileWarps);
   RTG_CUDA(launch_k(ctx, k_ccl_tile_fb, tgrid, 32 * kTileWarps, 0, cand, (int)h, (int)w, tiles_x,
-                    ntiles, roots, ctx->lroots, lcount, counts, total, rowbits, rtab, border, in_bits));
+                    ntiles, roots, ctx->lroots, lcount, counts, total, rowbits, rtab, tinfo, border,
+                    in_bits));
   RTG_LAUNCH("k_ccl_tile_fb");
   if (tiles_x + tiles_y > 2) {
     const dim3 g((unsigned)ceil_div(h > w ? h : w, 256), (unsigned)(tiles_y - 1 + tiles_x - 1));
@@ -1879,18 +1885,18 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
                     (int32_t*)nullptr, (uint32_t*)nullptr, true));
   RTG_LAUNCH("k_ccl_flatten");
   prof_mark(ctx, RTG_STAGE_AREA);  // enclosure tree, subtree areas, filter
-  const RunTable rt{rowbits, rtab, (int)w, tiles_x};
+  const RunTable rt{rowbits, rtab, tinfo, ctx->lroots, (int)w, tiles_x};
   RTG_CUDA(launch_k(ctx, k_fb_tree, gl, 256, 0, ctx->lroots, lcount, cand, (int)w, roots, counts, top,
                     total, rt));
   RTG_LAUNCH("k_fb_tree");
   uint8_t* keep = ctx->m2;  // free until the EDT's row distances
   RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
-                    max_area, keep, (int)w, runs ? tiles_x : 0));
+                    max_area, keep, runs));
   RTG_LAUNCH("k_fb_keep");
   if (runs) {
     RTG_CUDA(launch_k(ctx, k_fb_emit, tgrid, 32 * kTileWarps, 0, (const uint32_t*)rowbits,
-                      (const uint16_t*)rtab, (const uint8_t*)keep, (int)h, (int)w, tiles_x, ntiles,
-                      out, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
+                      (const uint16_t*)rtab, (const int2*)tinfo, (const uint8_t*)keep, (int)h, (int)w, tiles_x, ntiles,
+                      out_bytes ? out : nullptr, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
     RTG_LAUNCH("k_fb_emit");
     return RTG_OK;
   }

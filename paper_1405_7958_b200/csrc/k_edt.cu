@@ -37,7 +37,19 @@ constexpr int kEW = kET + 2 * kER;    //   window edge (96 = 3 words)
 constexpr uint32_t kInfG = 0xFFFFu;
 constexpr int kCap = 96;
 
-__global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
+// Foreground test of pixel i from the mask bytes or from the 1-bit plane
+// (the sparse path's plane; the joint fill/area stage writes only that).
+struct ByteFg {
+  const uint8_t* m;
+  __device__ __forceinline__ bool operator()(int64_t i) const { return m[i] != 0; }
+};
+struct BitFg {
+  const uint32_t* b;  // the plane after its kBitPad pad words
+  __device__ __forceinline__ bool operator()(int64_t i) const { return (b[i >> 5] >> (i & 31)) & 1u; }
+};
+
+template <class Fg>
+__global__ void k_edt_seg(Fg mask, int h, int w,
                           uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero,
                           const int32_t* __restrict__ gate) {
   pdl_enter();
@@ -52,7 +64,7 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
       int first = 0xFF, last = 0xFF;
       const int y0 = s * kSeg;
       for (int r = 0; r < kSeg && y0 + r < h; ++r) {
-        if (!mask[(int64_t)(y0 + r) * w + x]) {
+        if (!mask((int64_t)(y0 + r) * w + x)) {
           if (first == 0xFF) first = r;
           last = r;
         }
@@ -64,7 +76,8 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ mask, int h, int w,
   }
 }
 
-__global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
+template <class Fg>
+__global__ void k_edt_col(Fg mask, int h, int w,
                           const uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
                           const int32_t* __restrict__ gate) {
   pdl_enter();
@@ -91,7 +104,7 @@ __global__ void k_edt_col(const uint8_t* __restrict__ mask, int h, int w,
   for (int r = 0; r < kSeg; ++r) {
     if (r < rows) {
       const int y = y0 + r;
-      if (!mask[(int64_t)y * w + x]) { zbits |= 1u << r; above = y; }
+      if (!mask((int64_t)y * w + x)) { zbits |= 1u << r; above = y; }
       du[r] = above >= 0 ? (uint32_t)(y - above) : kInfG;
     }
   }
@@ -407,13 +420,13 @@ k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ coun
 }
 
 // Pass 2: d2 = min over rows y +- dy of dy^2 + hd^2 (background pixels have
-// hd = 0; the mask bytes tell them apart), scanned outwards until dy^2 >=
+// hd = 0; the 1-bit plane tells them apart), scanned outwards until dy^2 >=
 // best.  Exact while the result is <= 32^2 (every background pixel within
 // Chebyshev distance 32 is seen); beyond that need_full is raised and the
 // whole-tile pass runs.
 __global__ void __launch_bounds__(256)
 k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-           const uint8_t* __restrict__ mask, const uint8_t* __restrict__ hd, int h, FastDiv dw,
+           const uint32_t* __restrict__ bits, const uint8_t* __restrict__ hd, int h, FastDiv dw,
            int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
            int32_t* __restrict__ need_full) {
   pdl_enter();
@@ -438,9 +451,9 @@ k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
         const uint32_t dy = dy0 + j;
         const bool vu = y >= (int)dy, vd = y + (int)dy < h;
         const int32_t qu = p - (int32_t)dy * w, qd = p + (int32_t)dy * w;
-        mu[j] = vu ? mask[qu] : 1u;
+        mu[j] = vu ? (bits[qu >> 5] >> (qu & 31)) & 1u : 1u;
         hu[j] = vu ? hd[qu] : 255u;
-        md[j] = vd ? mask[qd] : 1u;
+        md[j] = vd ? (bits[qd >> 5] >> (qd & 31)) & 1u : 1u;
         hdn[j] = vd ? hd[qd] : 255u;
       }
 #pragma unroll
@@ -478,9 +491,11 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // exact whole-tile pass, gated on need_full (empty launches otherwise)
   const int64_t gblk = ceil_div(w, 128) * nseg;
   const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
-  RTG_CUDA(launch_k(ctx, k_edt_seg, gs, 128, 0, mask, (int)h, (int)w, seg, any_zero, need_full));
+  RTG_CUDA(launch_k(ctx, k_edt_seg<ByteFg>, gs, 128, 0, ByteFg{mask}, (int)h, (int)w, seg,
+                    any_zero, (const int32_t*)need_full));
   RTG_LAUNCH("k_edt_seg");
-  RTG_CUDA(launch_k(ctx, k_edt_col, gs, 128, 0, mask, (int)h, (int)w, seg, g, need_full));
+  RTG_CUDA(launch_k(ctx, k_edt_col<ByteFg>, gs, 128, 0, ByteFg{mask}, (int)h, (int)w,
+                    (const uint16_t*)seg, g, (const int32_t*)need_full));
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
   const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
@@ -513,7 +528,7 @@ int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* li
   return RTG_OK;
 }
 
-int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int32_t* list,
+int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
              const int32_t* count, const uint32_t* bits_base, uint16_t* dq) {
   const int nseg = (int)ceil_div(h, kSeg);
   uint16_t* seg = reinterpret_cast<uint16_t*>(ctx->seg_summary);
@@ -527,14 +542,17 @@ int edt_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, const int3
   RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,
                                                            hd));
   RTG_LAUNCH("k_edt_rowdist");
-  RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, mask, hd, (int)h, dwv,
+  const uint32_t* bits = bits_base + kBitPad;
+  RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, bits, hd, (int)h, dwv,
                                                         nullptr, dq, need_full));
   RTG_LAUNCH("k_edt_list");
   const int64_t gblk = ceil_div(w, 128) * nseg;
   const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
-  RTG_CUDA(launch_k(ctx, k_edt_seg, gs, 128, 0, mask, (int)h, (int)w, seg, any_zero, need_full));
+  RTG_CUDA(launch_k(ctx, k_edt_seg<BitFg>, gs, 128, 0, BitFg{bits}, (int)h, (int)w, seg, any_zero,
+                    (const int32_t*)need_full));
   RTG_LAUNCH("k_edt_seg");
-  RTG_CUDA(launch_k(ctx, k_edt_col, gs, 128, 0, mask, (int)h, (int)w, seg, g, need_full));
+  RTG_CUDA(launch_k(ctx, k_edt_col<BitFg>, gs, 128, 0, BitFg{bits}, (int)h, (int)w,
+                    (const uint16_t*)seg, g, (const int32_t*)need_full));
   RTG_LAUNCH("k_edt_col");
   const size_t smem = sizeof(uint16_t) * (size_t)w;
   const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);

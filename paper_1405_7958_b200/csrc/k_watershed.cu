@@ -765,7 +765,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   if (iwpp_hmax) {
     RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));  // every pixel (IWPP reads all)
   } else {
-    RTG_TRY(edt_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits, dq));
+    RTG_TRY(edt_list(ctx, h, w, fgl, fgn, ctx->fg_bits, dq));
   }
   prof_mark(ctx, RTG_STAGE_MARKERS);
   uint16_t* Fw;

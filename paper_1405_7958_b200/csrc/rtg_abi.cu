@@ -152,8 +152,9 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
     // mask itself is never materialised)
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
+    // the mask bytes are only read by the IWPP HMAX path (whole-tile EDT)
     RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3,
-                            /*prezeroed=*/true));
+                            /*prezeroed=*/true, /*out_bytes=*/ctx->hmax_impl == 1));
   } else {
     // o4 FillHoles of the nucleus candidates
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
