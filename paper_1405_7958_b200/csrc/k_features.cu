@@ -282,33 +282,34 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
     const int y_prev = __shfl_up_sync(full, y, 1);
     const unsigned heads = __ballot_sync(full, lane == 0 || l != l_prev || y != y_prev);
     // segmented reduction towards the run head: lanes (lane, lane + off] must
-    // hold no head
-    uint32_t sx = l ? (uint32_t)x : 0u, sxx = sx * sx, si = v, sii = v * v, sg = gq,
-             sgg = gq * gq, sp = per, mni = l ? v : 0xFFFFFFFFu, mxi = v;
+    // hold no head.  Nine fields travel in six shuffles: sum x (< 2^18, x <
+    // 8192) with the perimeter count (<= 128), sum I (< 2^13) with sum of
+    // gradients (< 2^18), and min I with 255 - max I as two bytes combined by
+    // one byte-wise min; no packed field can carry into its neighbour.
+    uint32_t A = (l ? (uint32_t)x : 0u) | (per << 18);
+    uint32_t B = v | (gq << 13);
+    uint32_t sxx = l ? (uint32_t)x * (uint32_t)x : 0u, sii = v * v, sgg = gq * gq;
+    uint32_t M = l ? (v | ((255u - v) << 8)) : 0xFFFFu;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t ox = __shfl_down_sync(full, sx, off);
+      const uint32_t oA = __shfl_down_sync(full, A, off);
+      const uint32_t oB = __shfl_down_sync(full, B, off);
       const uint32_t oxx = __shfl_down_sync(full, sxx, off);
-      const uint32_t oi = __shfl_down_sync(full, si, off);
       const uint32_t oii = __shfl_down_sync(full, sii, off);
-      const uint32_t og = __shfl_down_sync(full, sg, off);
       const uint32_t ogg = __shfl_down_sync(full, sgg, off);
-      const uint32_t op = __shfl_down_sync(full, sp, off);
-      const uint32_t omn = __shfl_down_sync(full, mni, off);
-      const uint32_t omx = __shfl_down_sync(full, mxi, off);
+      const uint32_t oM = __shfl_down_sync(full, M, off);
       const uint32_t span = ((heads >> 1) >> lane) & ((1u << off) - 1u);  // heads in (lane, lane+off]
       if (lane + off < 32 && span == 0) {
-        sx += ox;
+        A += oA;
+        B += oB;
         sxx += oxx;
-        si += oi;
         sii += oii;
-        sg += og;
         sgg += ogg;
-        sp += op;
-        mni = min(mni, omn);
-        mxi = max(mxi, omx);
+        M = __vminu4(M, oM);
       }
     }
+    const uint32_t sx = A & 0x3FFFFu, sp = A >> 18, si = B & 0x1FFFu, sg = B >> 13;
+    const uint32_t mni = M & 0xFFu, mxi = 255u - ((M >> 8) & 0xFFu);
     // run = lanes [lane, end] for a head lane; its last pixel has the largest x
     const unsigned after = (heads >> 1) >> lane;  // heads strictly after this lane
     const int end = after ? lane + __ffs(after) - 1 : 31;
