@@ -157,6 +157,7 @@ struct rtg_ctx {
   uint32_t* root_bm = nullptr;     // CCL global-root bitmap (max_px / 32 words)
   int32_t* fg_list = nullptr;      // watershed foreground pixel list (max_px)
   uint32_t* fg_bits = nullptr;     //   and 1-bit plane (+ pad words)
+  uint32_t* sep_bits = nullptr;    // the separated mask as a 1-bit plane (run-table path)
   int32_t* root_wprefix = nullptr; //   and its per-word exclusive prefix
   int32_t* obj_root = nullptr;     // object-parallel watershed: object roots
   int32_t* obj_box = nullptr;      //   and bounding boxes (4 per object)
@@ -186,6 +187,8 @@ struct rtg_ctx {
   int label_runs = 1;   // stage labellings in run-table form (k_ccl.cu CclRuns) when the shape allows
   bool ccl_runs_live = false;  // the last ccl_roots left run tables for ccl_canonical
   bool cand_bits = false;      // recon left the candidates as row masks (fill_area_joint reads them)
+  bool sep_bits_live = false;  // fill_area_joint cleared sep_bits: the watershed writes the
+                               // separated mask there, the labelling reads it and writes the bytes
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
 
   // CUDA-graph cache of whole-tile pipelines, keyed by every argument
@@ -431,8 +434,15 @@ __device__ __forceinline__ void uf_unite_g(int32_t* par, int32_t a, int32_t b) {
 // call's local-root list and root bitmap).
 // clear_acc (optional): the feature accumulators are reset for every label
 // while the ranks are assigned (the feature stage then skips k_feat_clear).
+// mask_out (run-table form after ccl_roots_bits): also writes the labelled
+// mask's bytes (label != 0).
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
-                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc = nullptr);
+                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc = nullptr,
+                  uint8_t* mask_out = nullptr);
+// ccl_roots in the run-table form over a mask given as a 1-bit plane
+// (linear words, w % 32 == 0); the caller checked ccl_runs_for.
+int ccl_roots_bits(rtg_ctx* ctx, const uint32_t* bits, int64_t h, int64_t w, int conn,
+                   int32_t* roots, bool prezeroed);
 // Grayscale reconstruction by level decomposition (k_ccl.cu): when J and I
 // hold at most kMaxReconLevels distinct non-zero values, R is one seeded
 // labelling per value.  recon_clip_levels writes J = min(marker, I) and reads
@@ -466,8 +476,11 @@ int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
 // cleared upstream (the streaming kernel's ClearList).
 // out_bytes = false: in the run-table form `out` is not written (the list
 // and the bit plane are the output; the sparse watershed reads only those).
+// sep_bits: in that form also clear ctx->sep_bits for the watershed's
+// separated mask (ctx->sep_bits_live says whether it did).
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out, bool prezeroed = false, bool out_bytes = true);
+                    int32_t max_area, uint8_t* out, bool prezeroed = false, bool out_bytes = true,
+                    bool sep_bits = false);
 // What fill_area_joint needs cleared, as a ClearList.
 ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w);
 int area_filter(rtg_ctx* ctx, const int32_t* roots, int64_t n,

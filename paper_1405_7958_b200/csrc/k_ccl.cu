@@ -100,6 +100,7 @@ __device__ __forceinline__ uint32_t border_nib(int y, int x, int h, int w) {
 }
 struct FgMask {  // mask != 0
   static constexpr bool kSeed = false;
+  static constexpr bool kRows = false;
   const uint8_t* m;
   __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool&) const {
     fg = m[i] != 0;
@@ -111,6 +112,7 @@ struct FgMask {  // mask != 0
 };
 struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
   static constexpr bool kSeed = true;
+  static constexpr bool kRows = false;
   const uint8_t* v;
   int32_t t, ts;
   __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool& sd) const {
@@ -126,6 +128,7 @@ struct FgThresh {  // v >= t; seed: v >= ts (ts > 255: no seeds)
 };
 struct FgCode {  // a precomputed code plane: bit 0 foreground, bit 1 seed
   static constexpr bool kSeed = true;
+  static constexpr bool kRows = false;
   const uint8_t* c;
   __device__ __forceinline__ void eval(int64_t i, int, int, bool& fg, bool& sd) const {
     const uint32_t a = c[i];
@@ -140,6 +143,7 @@ struct FgCode {  // a precomputed code plane: bit 0 foreground, bit 1 seed
 };
 struct FgBackground {  // m == 0; seed: on the image border
   static constexpr bool kSeed = true;
+  static constexpr bool kRows = false;
   const uint8_t* m;
   int h, w;
   __device__ __forceinline__ void eval(int64_t i, int y, int x, bool& fg, bool& sd) const {
@@ -152,6 +156,17 @@ struct FgBackground {  // m == 0; seed: on the image border
     sd = border_nib(y, x, h, w);
   }
   __host__ __device__ __forceinline__ const uint8_t* plane() const { return m; }
+};
+
+// A mask given as a 1-bit plane (linear words; w % 32 == 0, so a tile row is
+// one word): phase 1 of the tile kernel is a single load per row.
+struct FgBitRows {
+  static constexpr bool kSeed = false;
+  static constexpr bool kRows = true;
+  const uint32_t* b;
+  int wpr;  // words per image row
+  __device__ __forceinline__ uint32_t row(int y, int x0) const { return b[y * wpr + (x0 >> 5)]; }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return nullptr; }
 };
 
 constexpr int kTileWarps = 4;
@@ -199,10 +214,12 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   // 1. row bit masks; lane r keeps row r
   uint32_t bits = 0, seeds = 0;
   const int x = x0 + lane;
-  const bool vec = (w & 3) == 0 && x0 + 32 <= w &&
+  const bool vec = !P::kRows && (w & 3) == 0 && x0 + 32 <= w &&
                    (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
-  if (vec) {
+  if constexpr (P::kRows) {
+    if (y0 + lane < h) bits = pred.row(y0 + lane, x0);
+  } else if (vec) {
     // 4 pixels per load: lane covers row 4k + lane/8, columns 4 (lane % 8) ..
     // + 3; the 8 lanes of a row OR their nibbles together
     const uint8_t* pl = pred.plane();
@@ -728,7 +745,7 @@ __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
 // (16-byte stores, four rows per step).
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int tiles_x, int ntiles,
-             int32_t* __restrict__ labels, bool vec) {
+             int32_t* __restrict__ labels, bool vec, uint8_t* __restrict__ mask_out) {
   pdl_enter();
   __shared__ int32_t s_rank[kTileWarps][512];
   __shared__ int32_t s_lab[kTileWarps][512];
@@ -763,6 +780,9 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int til
       o[j] = ((b >> c) & 1u) ? s_lab[wid][r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : 0;
     }
     int32_t* dst = labels + (int64_t)(y0 + r) * w + x0 + cq;
+    if (mask_out)
+      *reinterpret_cast<uint32_t*>(mask_out + (int64_t)(y0 + r) * w + x0 + cq) =
+          (((b >> cq) & 0xFu) * 0x00204081u) & 0x01010101u;
     if (vec) {
       *reinterpret_cast<int4*>(dst) = make_int4(o[0], o[1], o[2], o[3]);
     } else {
@@ -1349,7 +1369,7 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
           const int2* __restrict__ tinfo, const uint8_t* __restrict__ keep, int h, int w,
           int tiles_x, int ntiles,
           uint8_t* __restrict__ out, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
-          int32_t* __restrict__ count) {
+          int32_t* __restrict__ count, uint32_t* __restrict__ sep_bits) {
   pdl_enter();
   __shared__ __align__(16) uint8_t s_keep[kTileWarps][1024];
   __shared__ int32_t s_cnt[32 * kTileWarps];
@@ -1387,7 +1407,10 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
     }
   }
   s_kept[wid][lane] = kept;
-  if (row) bits[((int64_t)y * w + x0) >> 5] = kept;
+  if (row) {
+    bits[((int64_t)y * w + x0) >> 5] = kept;
+    if (sep_bits) sep_bits[((int64_t)y * w + x0) >> 5] = 0u;  // the watershed ORs into it
+  }
   __syncwarp();
   // mask bytes (when a consumer reads them): 8 lanes per row, four rows per
   // store (full 32-byte sectors)
@@ -1767,6 +1790,15 @@ int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
                  rt);
 }
 
+int ccl_roots_bits(rtg_ctx* ctx, const uint32_t* bits, int64_t h, int64_t w, int conn,
+                   int32_t* roots, bool prezeroed) {
+  const CclRuns rt = ccl_runs_for(ctx, h, w);
+  if (!rt.rtab) return fail(RTG_ERR_INTERNAL, "bit-plane labelling without run tables");
+  ctx->ccl_runs_live = true;
+  return ccl_run(ctx, FgBitRows{bits, (int)(w / 32)}, h, w, conn, roots, nullptr, nullptr,
+                 ctx->root_bm, prezeroed, rt);
+}
+
 void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
   const int64_t nwords = ceil_div(h * w, 32);
   const size_t nstatus = (size_t)ceil_div(nwords, kBmChunk) + 1;
@@ -1779,7 +1811,8 @@ void ccl_label_zero(rtg_ctx* ctx, int64_t h, int64_t w, ZeroList& z) {
 }
 
 int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
-                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc) {
+                  int32_t* labels, int32_t* d_n, const FeatureAcc* clear_acc,
+                  uint8_t* mask_out) {
   const int64_t n = h * w;
   const int64_t nwords = ceil_div(n, 32);
   const int nchunks = (int)ceil_div(nwords, kBmChunk);
@@ -1801,10 +1834,12 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
     const int ntiles = tiles_x * (int)ceil_div(h, 32);
     RTG_CUDA(launch_k(ctx, k_label_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
                       0, ccl_runs_for(ctx, h, w), (const int32_t*)rank, (int)h, (int)w, tiles_x,
-                      ntiles, labels, (reinterpret_cast<uintptr_t>(labels) & 15) == 0));
+                      ntiles, labels, (reinterpret_cast<uintptr_t>(labels) & 15) == 0,
+                      mask_out));
     RTG_LAUNCH("k_label_emit");
     return RTG_OK;
   }
+  if (mask_out) return fail(RTG_ERR_INTERNAL, "mask bytes requested without run tables");
   RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
   return RTG_OK;
@@ -1829,7 +1864,8 @@ ClearList fill_area_clear(rtg_ctx* ctx, int64_t h, int64_t w) {
 }
 
 int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int32_t min_area,
-                    int32_t max_area, uint8_t* out, bool prezeroed, bool out_bytes) {
+                    int32_t max_area, uint8_t* out, bool prezeroed, bool out_bytes,
+                    bool sep_bits) {
   const int64_t n = h * w;
   int32_t* roots = ctx->i32a;
   int32_t* counts = ctx->i32b;
@@ -1896,8 +1932,10 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   if (runs) {
     RTG_CUDA(launch_k(ctx, k_fb_emit, tgrid, 32 * kTileWarps, 0, (const uint32_t*)rowbits,
                       (const uint16_t*)rtab, (const int2*)tinfo, (const uint8_t*)keep, (int)h, (int)w, tiles_x, ntiles,
-                      out_bytes ? out : nullptr, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4));
+                      out_bytes ? out : nullptr, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4,
+                      sep_bits ? ctx->sep_bits : nullptr));
     RTG_LAUNCH("k_fb_emit");
+    ctx->sep_bits_live = sep_bits;
     return RTG_OK;
   }
   int blocks = (int)ceil_div(n, 1024);

@@ -700,24 +700,43 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
 }
 
 // Separation: a listed pixel survives unless an 8-neighbour has a higher
-// basin id (background pixels of sep are cleared beforehand).
+// basin id (background pixels of sep are cleared beforehand).  With
+// sep_bits (cleared by the joint fill/area stage) the result goes into that
+// 1-bit plane instead: the lanes of a warp that share a word OR their bits
+// together and one of them issues the atomic (the list is row-ordered, so a
+// warp touches one or two words).
 __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ list,
                               const int32_t* __restrict__ count,
                               const uint32_t* __restrict__ mask,
-                              const int32_t* __restrict__ basin, uint8_t* __restrict__ sep) {
+                              const int32_t* __restrict__ basin, uint8_t* __restrict__ sep,
+                              uint32_t* __restrict__ sep_bits) {
   pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t p = list[k];
-    const int y = fdiv(p, dw), x = p - y * w;
-    const int32_t b = basin[p];
-    int32_t bv[8];
-    gather8(basin, w, p, fg_nbrs(h, w, mask, p, y, x), 0, bv);
-    bool keep = b > 0;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the bit path's match/reduce needs every lane)
+  for (int k0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; k0 < n;
+       k0 += gridDim.x * blockDim.x) {
+    const int k = k0 + lane;
+    int32_t p = -1;
+    bool keep = false;
+    if (k < n) {
+      p = list[k];
+      const int y = fdiv(p, dw), x = p - y * w;
+      const int32_t b = basin[p];
+      int32_t bv[8];
+      gather8(basin, w, p, fg_nbrs(h, w, mask, p, y, x), 0, bv);
+      keep = b > 0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) keep &= bv[t] <= b;
-    sep[p] = keep;
+      for (int t = 0; t < 8; ++t) keep &= bv[t] <= b;
+      if (!sep_bits) sep[p] = keep;
+    }
+    if (sep_bits) {
+      const int32_t wi = p >= 0 ? (p >> 5) : -1;
+      const unsigned grp = __match_any_sync(0xFFFFFFFFu, wi);
+      const uint32_t v = __reduce_or_sync(grp, keep ? 1u << (p & 31) : 0u);
+      if (wi >= 0 && v && lane == __ffs(grp) - 1) atomicOr(sep_bits + wi, v);
+    }
   }
 }
 
@@ -751,9 +770,12 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   auto* walloc = reinterpret_cast<unsigned long long*>(ctx->misc + 18);
   // ... and, in the same launch, what the labelling of the separated mask
   // (o8, ccl_roots(..., prezeroed)) needs cleared
-  ZeroList z{{sep, ctx->misc + 1, ctx->misc + 5, alloc},
-             {(size_t)n, 3 * sizeof(int32_t), sizeof(int32_t), 2 * sizeof(unsigned long long)},
-             4};
+  // (the separated mask itself only when it is written as bytes; the bit
+  // plane was cleared by the joint fill/area stage)
+  const bool sep_bits = ctx->sep_bits_live;
+  ZeroList z{{ctx->misc + 1, ctx->misc + 5, alloc, sep},
+             {3 * sizeof(int32_t), sizeof(int32_t), 2 * sizeof(unsigned long long), (size_t)n},
+             sep_bits ? 3 : 4};
   ccl_label_zero(ctx, h, w, z);
   RTG_TRY(zero_async(ctx, z));
   if (want_basin)
@@ -823,7 +845,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
-  RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, basin, sep));
+  RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, basin, sep,
+                    sep_bits ? ctx->sep_bits : (uint32_t*)nullptr));
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
 }

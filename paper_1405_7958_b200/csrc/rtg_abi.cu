@@ -126,6 +126,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   const bool iwpp_recon = ctx->recon_impl == 1;
   ctx->cand_bits = false;
   ctx->ccl_runs_live = false;
+  ctx->sep_bits_live = false;
   // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
   // the streaming kernel's first CTA clears the reconstruction CCL's
@@ -153,8 +154,11 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // mask itself is never materialised)
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
     // the mask bytes are only read by the IWPP HMAX path (whole-tile EDT)
+    // the separated mask goes through a bit plane when the labelling can
+    // write its bytes (4-byte stores)
     RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3,
-                            /*prezeroed=*/true, /*out_bytes=*/ctx->hmax_impl == 1));
+                            /*prezeroed=*/true, /*out_bytes=*/ctx->hmax_impl == 1,
+                            /*sep_bits=*/(reinterpret_cast<uintptr_t>(mask) & 3) == 0));
   } else {
     // o4 FillHoles of the nucleus candidates
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
@@ -180,10 +184,18 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   // o8 BWLabel (canonical)
   prof_mark(ctx, RTG_STAGE_LABEL);
   // the tiled watershed cleared the labelling's counters with its own
-  RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0,
-                    ctx->label_runs != 0));
+  // (run-table path: the watershed left the separated mask as a bit plane;
+  // the labelling reads it and writes the mask bytes with the labels)
+  const bool sep_bits = ctx->sep_bits_live;
+  ctx->sep_bits_live = false;
+  if (sep_bits)
+    RTG_TRY(ccl_roots_bits(ctx, ctx->sep_bits, h, w, 8, ctx->i32a, /*prezeroed=*/true));
+  else
+    RTG_TRY(ccl_roots(ctx, mask, h, w, 8, ctx->i32a, nullptr, ctx->ws_impl == 0,
+                      ctx->label_runs != 0));
   // the ranking pass also resets the feature accumulators of every label
-  RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out, with_features ? &ctx->acc : nullptr));
+  RTG_TRY(ccl_canonical(ctx, ctx->i32a, h, w, labels, n_out, with_features ? &ctx->acc : nullptr,
+                        sep_bits ? mask : nullptr));
   // o9 features
   if (with_features) {
     prof_mark(ctx, RTG_STAGE_FEATURES);
@@ -453,6 +465,7 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_TRY(dalloc(&c->root_wprefix, n / 32 + 1));
         RTG_TRY(dalloc(&c->fg_list, n));
         RTG_TRY(dalloc(&c->fg_bits, n / 32 + 8));
+        RTG_TRY(dalloc(&c->sep_bits, n / 32 + 8));
         c->obj_cap = (int64_t)n / 4 + 16;  // 8-connected objects are >= 1 px, <= 1 per 2x2
         RTG_TRY(dalloc(&c->obj_root, (size_t)c->obj_cap));
         RTG_TRY(dalloc(&c->obj_box, 4 * (size_t)c->obj_cap));
@@ -495,7 +508,7 @@ int rtg_ctx_destroy(rtg_ctx* c) {
   void* bufs[] = {c->rgb, c->hema, c->recon, c->tissue, c->m1, c->m2, c->m3, c->m4, c->rm,
                   c->u16a, c->u16b, c->u16c, c->i32a, c->i32b, c->i32c, c->labels,
                   c->features, c->feat20, c->tex14, c->seg_summary, c->scan_buf, c->flat_list, c->lroots,
-                  c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits,
+                  c->root_bm, c->root_wprefix, c->fg_list, c->fg_bits, c->sep_bits,
                   c->obj_root, c->obj_box, c->obj_list, c->arena, c->misc,
                   c->status, c->stats, c->level_bits, c->tq.state, c->tq.slots, c->tq.counters,
                   c->acc.sums, c->acc.mins, c->acc.maxs, c->tex_bbox, c->tex_hist,
