@@ -25,7 +25,11 @@
 // The row pass also emits dq = floor(4*sqrt(d2)) and the HMAX marker.
 //
 // Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + dq/marker 4 B out.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rtg {
 namespace {
@@ -48,14 +52,12 @@ struct BitFg {
   __device__ __forceinline__ bool operator()(int64_t i) const { return (b[i >> 5] >> (i & 31)) & 1u; }
 };
 
+// Column segments: first/last zero row of every (32-row segment, column).
 template <class Fg>
-__global__ void k_edt_seg(Fg mask, int h, int w,
-                          uint16_t* __restrict__ seg, int32_t* __restrict__ any_zero,
-                          const int32_t* __restrict__ gate) {
-  pdl_enter();
-  if (gate && !*gate) return;
-  // grid-stride over (segment, 128-column block) pairs: a capped grid keeps
-  // the gated (normally empty) launch cheap
+__device__ __forceinline__ void edt_seg_phase(const Fg& mask, int h, int w, uint16_t* seg,
+                                              int32_t* any_zero) {
+  // grid-stride over (segment, column block) pairs: a capped grid keeps the
+  // gated (normally empty) launch cheap
   const int nbx = (w + blockDim.x - 1) / blockDim.x, nseg = (h + kSeg - 1) / kSeg;
   for (int blk = blockIdx.x; blk < nbx * nseg; blk += gridDim.x) {
     const int s = blk / nbx, x = (blk - s * nbx) * blockDim.x + threadIdx.x;
@@ -77,47 +79,61 @@ __global__ void k_edt_seg(Fg mask, int h, int w,
 }
 
 template <class Fg>
-__global__ void k_edt_col(Fg mask, int h, int w,
-                          const uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
-                          const int32_t* __restrict__ gate) {
+__global__ void k_edt_seg(Fg mask, int h, int w, uint16_t* __restrict__ seg,
+                          int32_t* __restrict__ any_zero, const int32_t* __restrict__ gate) {
   pdl_enter();
   if (gate && !*gate) return;
+  edt_seg_phase(mask, h, w, seg, any_zero);
+}
+
+// Column distances g through the segment summaries.
+template <class Fg>
+__device__ __forceinline__ void edt_col_phase(const Fg& mask, int h, int w, const uint16_t* seg,
+                                              uint16_t* g) {
   const int nbx = (w + blockDim.x - 1) / blockDim.x, nseg = (h + kSeg - 1) / kSeg;
   for (int blk = blockIdx.x; blk < nbx * nseg; blk += gridDim.x) {
-  const int s = blk / nbx, x = (blk - s * nbx) * blockDim.x + threadIdx.x;
-  if (x >= w) continue;
-  const int y0 = s * kSeg;
-  int above = -1;  // row of the nearest zero above the segment
-  for (int t = s - 1; t >= 0; --t) {
-    const int last = seg[(int64_t)t * w + x] >> 8;
-    if (last != 0xFF) { above = t * kSeg + last; break; }
-  }
-  int below = -1;
-  for (int t = s + 1; t < nseg; ++t) {
-    const int first = seg[(int64_t)t * w + x] & 0xFF;
-    if (first != 0xFF) { below = t * kSeg + first; break; }
-  }
-  const int rows = min(kSeg, h - y0);
-  uint32_t zbits = 0;
-  uint32_t du[kSeg];
+    const int s = blk / nbx, x = (blk - s * nbx) * blockDim.x + threadIdx.x;
+    if (x >= w) continue;
+    const int y0 = s * kSeg;
+    int above = -1;  // row of the nearest zero above the segment
+    for (int t = s - 1; t >= 0; --t) {
+      const int last = seg[(int64_t)t * w + x] >> 8;
+      if (last != 0xFF) { above = t * kSeg + last; break; }
+    }
+    int below = -1;
+    for (int t = s + 1; t < nseg; ++t) {
+      const int first = seg[(int64_t)t * w + x] & 0xFF;
+      if (first != 0xFF) { below = t * kSeg + first; break; }
+    }
+    const int rows = min(kSeg, h - y0);
+    uint32_t zbits = 0;
+    uint32_t du[kSeg];
 #pragma unroll
-  for (int r = 0; r < kSeg; ++r) {
-    if (r < rows) {
-      const int y = y0 + r;
-      if (!mask((int64_t)y * w + x)) { zbits |= 1u << r; above = y; }
-      du[r] = above >= 0 ? (uint32_t)(y - above) : kInfG;
+    for (int r = 0; r < kSeg; ++r) {
+      if (r < rows) {
+        const int y = y0 + r;
+        if (!mask((int64_t)y * w + x)) { zbits |= 1u << r; above = y; }
+        du[r] = above >= 0 ? (uint32_t)(y - above) : kInfG;
+      }
+    }
+#pragma unroll
+    for (int r = kSeg - 1; r >= 0; --r) {
+      if (r < rows) {
+        const int y = y0 + r;
+        if (zbits & (1u << r)) below = y;
+        const uint32_t dd = below >= 0 ? (uint32_t)(below - y) : kInfG;
+        g[(int64_t)y * w + x] = (uint16_t)min(du[r], dd);
+      }
     }
   }
-#pragma unroll
-  for (int r = kSeg - 1; r >= 0; --r) {
-    if (r < rows) {
-      const int y = y0 + r;
-      if (zbits & (1u << r)) below = y;
-      const uint32_t dd = below >= 0 ? (uint32_t)(below - y) : kInfG;
-      g[(int64_t)y * w + x] = (uint16_t)min(du[r], dd);
-    }
-  }
-  }
+}
+
+template <class Fg>
+__global__ void k_edt_col(Fg mask, int h, int w, const uint16_t* __restrict__ seg,
+                          uint16_t* __restrict__ g, const int32_t* __restrict__ gate) {
+  pdl_enter();
+  if (gate && !*gate) return;
+  edt_col_phase(mask, h, w, seg, g);
 }
 
 __device__ __forceinline__ uint32_t isqrt64(uint64_t v) {
@@ -136,14 +152,12 @@ __device__ __forceinline__ void edt_emit(int64_t i, int64_t d2, int32_t* dist2,
   if (mk) mk[i] = (uint16_t)(v > (uint32_t)ws_h ? v - (uint32_t)ws_h : 0u);
 }
 
-__global__ void __launch_bounds__(256)
-k_edt_row(const uint16_t* __restrict__ g, int h, int w,
-          const int32_t* __restrict__ any_zero, int32_t* __restrict__ dist2,
-          uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
-          int32_t* __restrict__ row_flag, const int32_t* __restrict__ gate) {
-  pdl_enter();
-  extern __shared__ uint16_t gs[];
-  if (gate && !*gate) return;  // k_edt_row_exact checks the same gate
+// Row search over the column distances (one CTA per row, g staged in shared
+// memory); rows that hit kCap are flagged for the exact pass.
+__device__ __forceinline__ void edt_row_phase(const uint16_t* g, int h, int w,
+                                              const int32_t* any_zero, int32_t* dist2,
+                                              uint16_t* dq, uint16_t* mk, int32_t ws_h,
+                                              int32_t* row_flag, uint16_t* gs) {
   const bool none = *any_zero == 0;
   for (int y = blockIdx.x; y < h; y += gridDim.x) {  // grid-stride over rows
     const int64_t rb = (int64_t)y * w;
@@ -178,24 +192,28 @@ k_edt_row(const uint16_t* __restrict__ g, int h, int w,
   }
 }
 
+__global__ void __launch_bounds__(256)
+k_edt_row(const uint16_t* __restrict__ g, int h, int w,
+          const int32_t* __restrict__ any_zero, int32_t* __restrict__ dist2,
+          uint16_t* __restrict__ dq, uint16_t* __restrict__ mk, int32_t ws_h,
+          int32_t* __restrict__ row_flag, const int32_t* __restrict__ gate) {
+  pdl_enter();
+  extern __shared__ uint16_t gs[];
+  if (gate && !*gate) return;  // k_edt_row_exact checks the same gate
+  edt_row_phase(g, h, w, any_zero, dist2, dq, mk, ws_h, row_flag, gs);
+}
+
 __device__ __forceinline__ int64_t floordiv64(int64_t a, int64_t b) {
   int64_t q = a / b;
   if ((a % b != 0) && (a < 0)) --q;
   return q;
 }
 
-// Exact per-row lower envelope (Meijster phase 2) for flagged rows.
-__global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
-                                const int32_t* __restrict__ row_flag,
-                                int32_t* __restrict__ s_buf, int32_t* __restrict__ t_buf,
-                                int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
-                                uint16_t* __restrict__ mk, int32_t ws_h,
-                                uint32_t* __restrict__ status,
-                                const int32_t* __restrict__ gate = nullptr) {
-  pdl_enter();
-  if (gate && !*gate) return;
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  if (y >= h || !row_flag[y]) return;
+// Exact per-row lower envelope (Meijster phase 2) of one flagged row.
+__device__ __forceinline__ void edt_row_exact_one(int y, const uint16_t* g, int h, int w,
+                                                  int32_t* s_buf, int32_t* t_buf, int32_t* dist2,
+                                                  uint16_t* dq, uint16_t* mk, int32_t ws_h,
+                                                  uint32_t* status) {
   atomicOr(status, kStatusEdtFallback);
   const int64_t rb = (int64_t)y * w;
   const int64_t INF = (int64_t)h + w + 1;
@@ -233,6 +251,43 @@ __global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
     edt_emit(rb + u, F(u, s[q]), dist2, dq, mk, ws_h);
     if (u == t[q]) --q;
   }
+}
+
+__global__ void k_edt_row_exact(const uint16_t* __restrict__ g, int h, int w,
+                                const int32_t* __restrict__ row_flag,
+                                int32_t* __restrict__ s_buf, int32_t* __restrict__ t_buf,
+                                int32_t* __restrict__ dist2, uint16_t* __restrict__ dq,
+                                uint16_t* __restrict__ mk, int32_t ws_h,
+                                uint32_t* __restrict__ status,
+                                const int32_t* __restrict__ gate = nullptr) {
+  pdl_enter();
+  if (gate && !*gate) return;
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= h || !row_flag[y]) return;
+  edt_row_exact_one(y, g, h, w, s_buf, t_buf, dist2, dq, mk, ws_h, status);
+}
+
+// The whole-tile pass as ONE cooperative launch (grid-wide barriers between
+// the phases) for the sparse path: when the gate is clear - the normal case
+// - the stage pays one empty launch instead of four.
+template <class Fg>
+__global__ void __launch_bounds__(256)
+k_edt_fallback(Fg mask, int h, int w, uint16_t* __restrict__ seg, uint16_t* __restrict__ g,
+               int32_t* __restrict__ any_zero, uint16_t* __restrict__ dq,
+               int32_t* __restrict__ row_flag, int32_t* __restrict__ s_buf,
+               int32_t* __restrict__ t_buf, uint32_t* __restrict__ status,
+               const int32_t* __restrict__ gate) {
+  extern __shared__ uint16_t gs[];
+  if (!*gate) return;  // the same value for every CTA: all leave together
+  cg::grid_group grid = cg::this_grid();
+  edt_seg_phase(mask, h, w, seg, any_zero);
+  grid.sync();
+  edt_col_phase(mask, h, w, seg, g);
+  grid.sync();
+  edt_row_phase(g, h, w, any_zero, nullptr, dq, nullptr, 0, row_flag, gs);
+  grid.sync();
+  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < h; y += gridDim.x * blockDim.x)
+    if (row_flag[y]) edt_row_exact_one(y, g, h, w, s_buf, t_buf, nullptr, dq, nullptr, 0, status);
 }
 
 __device__ __forceinline__ uint32_t isqrt_small(uint32_t v) {  // v < 2^24
@@ -546,23 +601,31 @@ int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
   RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, bits, hd, (int)h, dwv,
                                                         nullptr, dq, need_full));
   RTG_LAUNCH("k_edt_list");
-  const int64_t gblk = ceil_div(w, 128) * nseg;
-  const unsigned gs = (unsigned)(gblk < ctx->num_sms * 4 ? gblk : ctx->num_sms * 4);
-  RTG_CUDA(launch_k(ctx, k_edt_seg<BitFg>, gs, 128, 0, BitFg{bits}, (int)h, (int)w, seg, any_zero,
-                    (const int32_t*)need_full));
-  RTG_LAUNCH("k_edt_seg");
-  RTG_CUDA(launch_k(ctx, k_edt_col<BitFg>, gs, 128, 0, BitFg{bits}, (int)h, (int)w,
-                    (const uint16_t*)seg, g, (const int32_t*)need_full));
-  RTG_LAUNCH("k_edt_col");
+  // the exact whole-tile pass, gated on need_full, as one cooperative launch
+  (void)nseg;
   const size_t smem = sizeof(uint16_t) * (size_t)w;
-  const unsigned grows = (unsigned)(h < ctx->num_sms * 4 ? h : ctx->num_sms * 4);
-  RTG_CUDA(launch_k(ctx, k_edt_row, grows, 256, smem, g, (int)h, (int)w, any_zero, nullptr, dq,
-                                                      nullptr, 0, row_flag, need_full));
-  RTG_LAUNCH("k_edt_row");
-  RTG_CUDA(launch_k(ctx, k_edt_row_exact, (unsigned)ceil_div(h, 128), 128, 0, 
-      g, (int)h, (int)w, row_flag, ctx->i32b, ctx->i32c, nullptr, dq, nullptr, 0, ctx->status,
-      need_full));
-  RTG_LAUNCH("k_edt_row_exact");
+  static int occ_dev[64] = {0};  // co-resident CTAs per SM (per device)
+  int& occ = occ_dev[ctx->device & 63];
+  if (!occ) {
+    int o = 0;
+    RTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edt_fallback<BitFg>, 256, smem));
+    if (o < 1) return fail(RTG_ERR_INTERNAL, "k_edt_fallback does not fit on an SM");
+    occ = o > 2 ? 2 : o;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(ctx->num_sms * occ));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RTG_CUDA(cudaLaunchKernelEx(&cfg, k_edt_fallback<BitFg>, BitFg{bits}, (int)h, (int)w, seg, g,
+                              any_zero, dq, row_flag, ctx->i32b, ctx->i32c, ctx->status,
+                              (const int32_t*)need_full));
+  RTG_LAUNCH("k_edt_fallback");
   return RTG_OK;
 }
 

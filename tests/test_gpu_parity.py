@@ -344,6 +344,24 @@ def test_watershed_objects_size_classes(rtg, ctx, oracle, case):
     assert np.array_equal(_dev_np(sep), sep_ref)
 
 
+def test_sparse_edt_whole_tile_fallback(rtg, ctx, oracle):
+    """A blob far wider than the sparse EDT's 32-row window: the gated
+    whole-tile pass (one cooperative launch) must run (need_full flag) and
+    the watershed still equals the oracle."""
+    h, w = 512, 640
+    yy, xx = np.mgrid[0:h, 0:w]
+    m = (((yy - 250) / 150.0) ** 2 + ((xx - 300) / 120.0) ** 2 <= 1).astype(np.uint8)
+    m[400:430, 500:530] = 1
+    sep_ref, basin_ref = oracle.watershed(m, 3)
+    sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    ctx.stats()  # clear the counters
+    ctx.watershed_dev(_np_dev(m), h, w, 3, sep, basin)
+    assert ctx.stats()[3] == 1  # the sparse EDT raised need_full
+    assert np.array_equal(_dev_np(basin), basin_ref)
+    assert np.array_equal(_dev_np(sep), sep_ref)
+
+
 # ---------------------------------------------------------------- o9
 
 def test_features(ctx, oracle, tile4k):
