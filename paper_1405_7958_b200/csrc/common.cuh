@@ -261,9 +261,14 @@ struct ClearList {
 };
 // clear (optional): counters the next stages need zeroed, cleared by the
 // streaming kernel itself (zeroing launches fewer in the pipeline).
+// recon_bits (optional): {fg, seed, tissue} 1-bit planes for ReconToNuclei
+// (H >= nuc_thresh, H >= nuc_thresh + recon_h, tissue), written by the vector
+// kernels; *bits_written says whether they were (contiguous, 16-aligned,
+// unpitched input).  tissue may then be nullptr (no tissue bytes).
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                        int64_t pitch, const rtg_params* p, uint8_t* hema,
-                       uint8_t* marker, uint8_t* tissue, const ClearList* clear = nullptr);
+                       uint8_t* marker, uint8_t* tissue, const ClearList* clear = nullptr,
+                       uint32_t* const* recon_bits = nullptr, bool* bits_written = nullptr);
 int launch_candidate(rtg_ctx* ctx, const uint8_t* recon, const uint8_t* tissue,
                      int64_t n, int32_t thresh, uint8_t* out);
 
@@ -284,6 +289,9 @@ int iwpp_fill_holes(rtg_ctx* ctx, const uint8_t* bin, uint8_t* J, int64_t h,
 // linear index of p's component (-1 = background).  counts, when given,
 // receives every component's pixel count at its global root.
 // prezeroed: the caller already cleared the counters ccl_label_zero names.
+// Whether an h x w labelling can take the run-table form (w % 32 == 0 and
+// the tables fit the context's planes).
+bool run_tables_fit(rtg_ctx* ctx, int64_t h, int64_t w);
 // runs: the run-table form (k_ccl.cu CclRuns; the roots plane then only
 // holds the local roots' entries) when the shape allows it; only for a
 // ccl_canonical that follows directly.
@@ -461,10 +469,12 @@ int recon_levels(rtg_ctx* ctx, uint8_t* J, const uint8_t* I, int64_t h, int64_t 
 // runs: run-table form (uses u16a, u16b and m2 as scratch) when the shape allows;
 // bits_out: in that form `out` receives the candidates as tile row masks
 // (ctx->cand_bits says whether it did) for the joint fill/area labelling.
+// in_bits (run-table form only): the {fg, seed, tissue} planes of
+// launch_colordeconv replace the hema / tissue bytes.
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
                        uint8_t* out, bool prezeroed = false, bool runs = false,
-                       bool bits_out = false);
+                       bool bits_out = false, uint32_t* const* in_bits = nullptr);
 // FillHoles via union-find of the 4-connected background; scratch may alias out.
 int fill_holes_uf(rtg_ctx* ctx, const uint8_t* bin, int64_t h, int64_t w,
                   uint8_t* scratch, uint8_t* out);

@@ -169,6 +169,21 @@ struct FgBitRows {
   __host__ __device__ __forceinline__ const uint8_t* plane() const { return nullptr; }
 };
 
+// The ReconToNuclei threshold pair as 1-bit planes (the streaming kernel's
+// recon_bits): foreground and seed rows are one load each.
+struct FgSeedRows {
+  static constexpr bool kSeed = true;
+  static constexpr bool kRows = true;
+  const uint32_t* fg;
+  const uint32_t* sd;
+  int wpr;
+  __device__ __forceinline__ uint32_t row(int y, int x0) const { return fg[y * wpr + (x0 >> 5)]; }
+  __device__ __forceinline__ uint32_t seed_row(int y, int x0) const {
+    return sd[y * wpr + (x0 >> 5)];
+  }
+  __host__ __device__ __forceinline__ const uint8_t* plane() const { return nullptr; }
+};
+
 constexpr int kTileWarps = 4;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr uint32_t kSeedBit = 0x80000000u;
@@ -218,7 +233,10 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
                    (reinterpret_cast<uintptr_t>(pred.plane()) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(roots) & 15) == 0;
   if constexpr (P::kRows) {
-    if (y0 + lane < h) bits = pred.row(y0 + lane, x0);
+    if (y0 + lane < h) {
+      bits = pred.row(y0 + lane, x0);
+      if constexpr (P::kSeed) seeds = pred.seed_row(y0 + lane, x0) & bits;
+    }
   } else if (vec) {
     // 4 pixels per load: lane covers row 4k + lane/8, columns 4 (lane % 8) ..
     // + 3; the 8 lanes of a row OR their nibbles together
@@ -806,7 +824,7 @@ __global__ void k_slot_flag(const int32_t* __restrict__ lroots, const int32_t* _
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ tissue,
               int h, int w, int tiles_x, int ntiles, uint8_t* __restrict__ out,
-              uint32_t* __restrict__ out_bits) {
+              uint32_t* __restrict__ out_bits, const uint32_t* __restrict__ tis_bits) {
   pdl_enter();
   __shared__ uint8_t s_kp[kTileWarps][512];
   __shared__ uint32_t s_kept[kTileWarps][32];
@@ -833,6 +851,11 @@ k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __res
   s_kept[wid][lane] = kept;
   __syncwarp();
   const int g = lane >> 3, cq = (lane & 7) * 4;
+  if (out_bits && tis_bits) {  // tissue as a 1-bit plane too: one word per row
+    const uint32_t tw = y0 + lane < h ? __ldg(tis_bits + (y0 + lane) * (w >> 5) + (x0 >> 5)) : 0u;
+    out_bits[tile * 32 + lane] = kept & tw;
+    return;
+  }
   if (out_bits) {
     // row masks of (kept & tissue) for the joint fill/area tile kernel
 #pragma unroll
@@ -1625,7 +1648,8 @@ int ccl_run(rtg_ctx* ctx, const P& pred, int64_t h, int64_t w, int conn, int32_t
 
 int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue, int64_t h,
                        int64_t w, int32_t t, int32_t recon_h, int conn, uint8_t* scratch,
-                       uint8_t* out, bool prezeroed, bool runs, bool bits_out) {
+                       uint8_t* out, bool prezeroed, bool runs, bool bits_out,
+                       uint32_t* const* in_bits) {
   (void)scratch;
   const int64_t n = h * w;
   ctx->cand_bits = false;
@@ -1640,7 +1664,13 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   const bool aligned = ((reinterpret_cast<uintptr_t>(tissue) | reinterpret_cast<uintptr_t>(out) |
                          reinterpret_cast<uintptr_t>(hema)) & 3) == 0;
   const CclRuns rt = runs && aligned ? ccl_runs_for(ctx, h, w) : CclRuns{};
-  RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed, rt));
+  if (in_bits && (!rt.rtab || !bits_out))
+    return fail(RTG_ERR_INTERNAL, "threshold planes without the run-table form");
+  if (in_bits)
+    RTG_TRY(ccl_run(ctx, FgSeedRows{in_bits[0], in_bits[1], (int)(w / 32)}, h, w, conn, roots,
+                    nullptr, flag, nullptr, prezeroed, rt));
+  else
+    RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed, rt));
   if (rt.rtab) {
     uint8_t* keep = ctx->m2;  // one byte per local-root slot (free until the joint fill/area)
     RTG_CUDA(launch_k(ctx, k_slot_flag, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8,
@@ -1651,7 +1681,8 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
     ctx->cand_bits = bits_out;
     RTG_CUDA(launch_k(ctx, k_seeded_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
                       0, rt, (const uint8_t*)keep, tissue, (int)h, (int)w, tiles_x, ntiles, out,
-                      bits_out ? reinterpret_cast<uint32_t*>(out) : (uint32_t*)nullptr));
+                      bits_out ? reinterpret_cast<uint32_t*>(out) : (uint32_t*)nullptr,
+                      in_bits ? (const uint32_t*)in_bits[2] : (const uint32_t*)nullptr));
     RTG_LAUNCH("k_seeded_emit");
     return RTG_OK;
   }
@@ -1788,6 +1819,10 @@ int ccl_roots(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int conn,
   const CclRuns rt = ctx->ccl_runs_live ? ccl_runs_for(ctx, h, w) : CclRuns{};
   return ccl_run(ctx, FgMask{mask}, h, w, conn, roots, counts, nullptr, ctx->root_bm, prezeroed,
                  rt);
+}
+
+bool run_tables_fit(rtg_ctx* ctx, int64_t h, int64_t w) {
+  return ccl_runs_for(ctx, h, w).rtab != nullptr;
 }
 
 int ccl_roots_bits(rtg_ctx* ctx, const uint32_t* bits, int64_t h, int64_t w, int conn,

@@ -15,6 +15,17 @@ struct CdParams {
   int32_t bg, rg10, rb10, recon_h;
 };
 
+// Optional 1-bit outputs of the vector kernels (uint16 pieces, one per
+// 16-pixel group): ReconToNuclei's foreground (H >= t) and seed (H >= t + h)
+// planes and the tissue plane.  fg == nullptr: none.
+struct CdBits {
+  uint16_t* fg = nullptr;
+  uint16_t* sd = nullptr;
+  uint16_t* ts = nullptr;
+  uint32_t t4 = 0, s4 = 0;  // thresholds replicated into the four bytes
+  int fg_on = 0, sd_on = 0;  // 0: threshold above 255, no pixel qualifies
+};
+
 __device__ __forceinline__ void cd_pixel(const int32_t (*lut)[256],
                                          const CdParams& p, uint32_t r,
                                          uint32_t g, uint32_t b, uint32_t& hv,
@@ -61,13 +72,26 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int32_t v0, int32_t v1, int32_t 
   return d;
 }
 
+// byte MSBs (0xFF / 0x00 lanes of a SIMD compare) -> 4-bit mask, and bit 0
+// of each byte (0 / 1 bytes) -> 4-bit mask: one multiply gathers the four
+// bits without carries.
+__device__ __forceinline__ uint32_t msb_nib(uint32_t v) {
+  return ((v & 0x80808080u) * 0x00204081u) >> 28;
+}
+__device__ __forceinline__ uint32_t lsb_nib(uint32_t v) {
+  return (((v & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
+}
+
 // 16 pixels (48 interleaved RGB bytes in wv) -> 16 hematoxylin, tissue (and
-// marker) bytes with the lane-replicated LUTs.
+// marker) bytes with the lane-replicated LUTs; with bits.fg also the
+// ReconToNuclei threshold planes as 16-bit pieces of 1-bit planes (group g
+// = bits 16g .. 16g+15): H >= t, (H >= t + h) && H >= t, tissue.
 template <bool kMarker>
 __device__ __forceinline__ void cd_group(const uint32_t (&wv)[12], const int32_t* l0,
                                          const int32_t* l1, const int32_t* l2, int32_t bgt,
                                          int32_t rg10, int32_t rb10, int32_t rh, uint4* hema,
-                                         uint4* marker, uint4* tissue, uint32_t g) {
+                                         uint4* marker, uint4* tissue, uint32_t g,
+                                         const CdBits& bits) {
   uint32_t ho[4], to[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -90,7 +114,19 @@ __device__ __forceinline__ void cd_group(const uint32_t (&wv)[12], const int32_t
     to[k] = pack_sat_u8(tv[0], tv[1], tv[2], tv[3]);
   }
   hema[g] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
-  tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
+  if (tissue) tissue[g] = make_uint4(to[0], to[1], to[2], to[3]);
+  if (bits.fg) {
+    uint32_t f = 0, sd = 0, t = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (bits.fg_on) f |= msb_nib(__vcmpgeu4(ho[k], bits.t4)) << (4 * k);
+      if (bits.sd_on) sd |= msb_nib(__vcmpgeu4(ho[k], bits.s4)) << (4 * k);
+      t |= lsb_nib(to[k]) << (4 * k);
+    }
+    bits.fg[g] = (uint16_t)f;
+    bits.sd[g] = (uint16_t)(sd & f);
+    bits.ts[g] = (uint16_t)t;
+  }
   if (kMarker) {
     // max(H - recon_h, 0) per byte (H in [0,255], recon_h >= 0)
     uint32_t mo[4];
@@ -133,7 +169,8 @@ template <bool kMarker>
 __global__ void __launch_bounds__(kCdThreads, kCdBlocksPerSm)
 k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
-                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear) {
+                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear,
+                  const CdBits bits) {
   pdl_enter();
   if (blockIdx.x == 0) {
 #pragma unroll
@@ -166,7 +203,7 @@ k_colordeconv_vec(const uint4* __restrict__ rgb, uint32_t ngroups, int iters,
       b = ld_stream(rgb + 3 * gn + 1);
       c = ld_stream(rgb + 3 * gn + 2);
     }
-    cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g);
+    cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g, bits);
   }
 }
 
@@ -218,7 +255,8 @@ template <bool kMarker>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_colordeconv_tma(const uint8_t* __restrict__ rgb, uint32_t ngroups,
                   const __grid_constant__ CdParams p, uint4* __restrict__ hema,
-                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear) {
+                  uint4* __restrict__ marker, uint4* __restrict__ tissue, const ClearList clear,
+                  const CdBits bits) {
   pdl_enter();
   if (blockIdx.x == 0) {
 #pragma unroll
@@ -280,7 +318,8 @@ k_colordeconv_tma(const uint8_t* __restrict__ rgb, uint32_t ngroups,
                   &bars[st]);
       }
     }
-    if (g < ngroups) cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g);
+    if (g < ngroups)
+      cd_group<kMarker>(wv, l0, l1, l2, bgt, rg10, rb10, rh, hema, marker, tissue, g, bits);
   }
 }
 
@@ -377,7 +416,8 @@ void hema_lut(const rtg_params* p, HemaLut* lut) {
 
 int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
                        int64_t pitch, const rtg_params* p, uint8_t* hema,
-                       uint8_t* marker, uint8_t* tissue, const ClearList* clear) {
+                       uint8_t* marker, uint8_t* tissue, const ClearList* clear,
+                       uint32_t* const* recon_bits, bool* bits_written) {
   ClearList cl{};
   if (clear) cl = *clear;
   CdParams cp;
@@ -387,8 +427,26 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
   cp.rb10 = p->rbc_rb10;
   cp.recon_h = p->recon_h;
   const int64_t n = h * w;
-  const bool flat = pitch == 3 * w && aligned16(rgb) && hema && aligned16(hema) && tissue &&
-                    aligned16(tissue) && (!marker || aligned16(marker));
+  const bool flat = pitch == 3 * w && aligned16(rgb) && hema && aligned16(hema) &&
+                    (tissue || recon_bits) && (!tissue || aligned16(tissue)) &&
+                    (!marker || aligned16(marker)) && n % 16 == 0;
+  CdBits bits;
+  if (bits_written) *bits_written = false;
+  if (recon_bits && flat) {
+    // recon_bits = {fg, seed, tissue} planes; thresholds as FgThresh
+    const int64_t t = p->nuc_thresh, ts = (int64_t)p->nuc_thresh + p->recon_h;
+    bits.fg = reinterpret_cast<uint16_t*>(recon_bits[0]);
+    bits.sd = reinterpret_cast<uint16_t*>(recon_bits[1]);
+    bits.ts = reinterpret_cast<uint16_t*>(recon_bits[2]);
+    bits.fg_on = t <= 255;
+    bits.sd_on = ts <= 255;
+    bits.t4 = 0x01010101u * (uint32_t)(t <= 255 ? (t < 0 ? 0 : t) : 0);
+    bits.s4 = 0x01010101u * (uint32_t)(ts <= 255 ? (ts < 0 ? 0 : ts) : 0);
+    if (bits_written) *bits_written = true;
+    tissue = nullptr;  // the tissue plane goes out as bits only
+  } else if (!tissue) {
+    return fail(RTG_ERR_INTERNAL, "colour deconvolution without a tissue output");
+  }
   int64_t done = 0;
   if (flat) {
     const int64_t ngroups = n / 16 < INT32_MAX ? n / 16 : 0;
@@ -403,7 +461,7 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
         const int blocks = (int)(nchunks < (uint32_t)ctx->num_sms ? nchunks : ctx->num_sms);
         RTG_CUDA(launch_k(ctx, kern, blocks, kTmaThreads, kTmaSmem, rgb, (uint32_t)ngroups, cp,
                           reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-                          reinterpret_cast<uint4*>(tissue), cl));
+                          reinterpret_cast<uint4*>(tissue), cl, bits));
         cl.count = 0;
         RTG_LAUNCH("k_colordeconv_tma");
       } else {
@@ -416,7 +474,7 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
         RTG_CUDA(launch_k(ctx, kern, blocks, kCdThreads, kCdSmem,
                           reinterpret_cast<const uint4*>(rgb), (uint32_t)ngroups, iters, cp,
                           reinterpret_cast<uint4*>(hema), reinterpret_cast<uint4*>(marker),
-                          reinterpret_cast<uint4*>(tissue), cl));
+                          reinterpret_cast<uint4*>(tissue), cl, bits));
         cl.count = 0;
         RTG_LAUNCH("k_colordeconv_vec");
       }

@@ -137,8 +137,18 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     cl.p[cl.count] = ctx->misc + 8;
     cl.n[cl.count++] = 1;
   }
+  // run-table path: the streaming kernel also emits ReconToNuclei's two
+  // threshold planes and the tissue plane as 1-bit planes (in m3, free
+  // until the joint fill/area stage) instead of the tissue bytes
+  const int64_t nw32 = h * w / 32;
+  uint32_t* rbits[3] = {reinterpret_cast<uint32_t*>(ctx->m3),
+                        reinterpret_cast<uint32_t*>(ctx->m3) + nw32,
+                        reinterpret_cast<uint32_t*>(ctx->m3) + 2 * nw32};
+  const bool want_bits = !iwpp_recon && joint && ctx->label_runs && p->nuc_thresh > 0 &&
+                         run_tables_fit(ctx, h, w);
+  bool have_bits = false;
   RTG_TRY(launch_colordeconv(ctx, d_rgb, h, w, pitch, p, hema, iwpp_recon ? ctx->recon : nullptr,
-                             ctx->tissue, &cl));
+                             ctx->tissue, &cl, want_bits ? rbits : nullptr, &have_bits));
   // o3 ReconToNuclei: candidates = recon(max(H - h, 0), H) >= nuc_thresh && tissue
   prof_mark(ctx, RTG_STAGE_RECON);
   if (iwpp_recon) {
@@ -147,7 +157,8 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   } else {
     RTG_TRY(recon_threshold_uf(ctx, hema, ctx->tissue, h, w, p->nuc_thresh, p->recon_h,
                                p->recon_conn, ctx->m1, ctx->m1, /*prezeroed=*/true,
-                               ctx->label_runs != 0, /*bits_out=*/joint));
+                               ctx->label_runs != 0, /*bits_out=*/joint,
+                               have_bits ? rbits : nullptr));
   }
   if (ctx->fill_impl == 0 && ctx->ws_impl == 0) {
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
