@@ -282,32 +282,53 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
       }
     }
   }
-  // 2. lane = row: one union per pair of overlapping runs of adjacent rows
+  // 2. lane = row: one link per pair of overlapping runs of adjacent rows.
+  //    A run's first overlapping run above becomes its parent with a plain
+  //    store (every run has at most one such link, pointing to a smaller
+  //    index, so these links alone form a forest); only further overlaps
+  //    need shared-memory unions.
   const int rb = lane * 16;
   const uint32_t starts = bits & ~(bits << 1);
+  uint32_t up = __shfl_up_sync(kFull, bits, 1);
+  if (lane == 0) up = 0;
+  const uint32_t upstarts = up & ~(up << 1);
+  // run of the row above that holds column t (t in up), as a node id
+  auto upper = [&](int t) -> int {
+    const uint32_t below = upstarts & (t == 31 ? kFull : ((2u << t) - 1u));
+    const int su = 31 - __clz(below);
+    return rb - 16 + __popc(upstarts & ((1u << su) - 1u));
+  };
+  uint32_t more = 0;  // runs (by index bit) with further overlaps
   {
     int k = 0;
     for (uint32_t m = starts; m; m &= m - 1, ++k) {
-      par[rb + k] = rb + k;
-      pos[rb + k] = (uint8_t)(__ffs(m) - 1);
+      const int b = __ffs(m) - 1;
+      pos[rb + k] = (uint8_t)b;
+      const uint32_t run = low_run(bits >> b) << b;
+      uint32_t ov = up & (CONN == 8 ? (run | (run << 1) | (run >> 1)) : run);
+      if (!ov) {
+        par[rb + k] = rb + k;
+        continue;
+      }
+      const int t = __ffs(ov) - 1;
+      par[rb + k] = upper(t);
+      ov &= ~(low_run(up >> t) << t);
+      if (ov) more |= 1u << k;
     }
   }
-  const uint32_t up = __shfl_up_sync(kFull, bits, 1);
   __syncwarp();
-  if (lane > 0 && up) {
-    const uint32_t upstarts = up & ~(up << 1);
+  if (more) {
     int k = 0;
     for (uint32_t m = starts; m; m &= m - 1, ++k) {
+      if (!((more >> k) & 1u)) continue;
       const int b = __ffs(m) - 1;
       const uint32_t run = low_run(bits >> b) << b;
       uint32_t ov = up & (CONN == 8 ? (run | (run << 1) | (run >> 1)) : run);
+      ov &= ~(low_run(up >> (__ffs(ov) - 1)) << (__ffs(ov) - 1));  // the linked one
       while (ov) {
         const int t = __ffs(ov) - 1;
-        const uint32_t below = upstarts & (t == 31 ? kFull : ((2u << t) - 1u));
-        const int su = 31 - __clz(below);
-        const int ku = __popc(upstarts & ((1u << su) - 1u));
-        unite_s(par, rb + k, rb - 16 + ku);
-        ov &= ~(low_run(up >> su) << su);
+        unite_s(par, rb + k, upper(t));
+        ov &= ~(low_run(up >> t) << t);
       }
     }
   }
@@ -1071,40 +1092,65 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   const int rb = lane * 32;
   const uint32_t fst = fgb & ~(fgb << 1), bst = bgb & ~(bgb << 1);
   const uint32_t allst = fst | bst;
+  uint32_t upf = __shfl_up_sync(kFull, fgb, 1), upb = __shfl_up_sync(kFull, bgb, 1);
+  if (lane == 0) upf = upb = 0;
+  const uint32_t upall = (upf & ~(upf << 1)) | (upb & ~(upb << 1));
+  // the run of the row above holding column t (t in upf | upb), as a node id
+  auto upper = [&](int t) -> int {
+    const uint32_t U = ((upf >> t) & 1u) ? upf : upb;
+    const uint32_t ust = U & ~(U << 1);
+    const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
+    return rb - 32 + __popc(upall & ((1u << su) - 1u));
+  };
+  auto overlaps = [&](int b) -> uint32_t {  // the row above's pixels touching run b
+    const bool isf = (fgb >> b) & 1u;
+    const uint32_t run = low_run((isf ? fgb : bgb) >> b) << b;
+    return isf ? upf & (run | (run << 1) | (run >> 1)) : upb & run;
+  };
+  // every row joins its upper neighbour at once: a run's first overlapping
+  // run above becomes its parent with a plain store (these links alone form
+  // a forest); only further overlaps need the CAS unions on the 16-bit
+  // forest.  (A schedule of log2(32) rounds kept the trees shallower but
+  // left 3/4 of the lanes idle: 12 us more per 4096^2 tile.)
+  uint32_t more = 0;  // runs (by index bit) with further overlaps
   {
     int k = 0;
     for (uint32_t q = allst; q; q &= q - 1, ++k) {
-      par[rb + k] = (uint16_t)(rb + k);
-      pos[rb + k] = (uint8_t)(__ffs(q) - 1);
+      const int b = __ffs(q) - 1;
+      pos[rb + k] = (uint8_t)b;
+      uint32_t ov = overlaps(b);
+      if (!ov) {
+        par[rb + k] = (uint16_t)(rb + k);
+        continue;
+      }
+      const int t = __ffs(ov) - 1;
+      const uint32_t U = ((upf >> t) & 1u) ? upf : upb;
+      par[rb + k] = (uint16_t)upper(t);
+      ov &= ~(low_run(U >> t) << t);
+      if (ov) more |= 1u << k;
     }
   }
-  const uint32_t upf = __shfl_up_sync(kFull, fgb, 1), upb = __shfl_up_sync(kFull, bgb, 1);
-  const uint32_t upall = (upf & ~(upf << 1)) | (upb & ~(upb << 1));
   __syncwarp();
-  // every row joins its upper neighbour at once (concurrent CAS unions on
-  // the 16-bit forest); a schedule of log2(32) rounds (row r in the round of
-  // its lowest set bit) kept the trees shallower but left 3/4 of the lanes
-  // idle on average: 12 us more per 4096^2 tile
-  {
-    if (lane > 0 && (upf | upb)) {
-      int k = 0;
-      for (uint32_t q = allst; q; q &= q - 1, ++k) {
-        const int b = __ffs(q) - 1;
-        const bool isf = (fgb >> b) & 1u;
-        const uint32_t cur = isf ? fgb : bgb, U = isf ? upf : upb;
-        const uint32_t run = low_run(cur >> b) << b;
-        uint32_t ov = U & (isf ? (run | (run << 1) | (run >> 1)) : run);
-        const uint32_t ust = U & ~(U << 1);
-        while (ov) {
-          const int t = __ffs(ov) - 1;
-          const int su = 31 - __clz(ust & (t == 31 ? kFull : ((2u << t) - 1u)));
-          unite_s16(par, rb + k, rb - 32 + __popc(upall & ((1u << su) - 1u)));
-          ov &= ~(low_run(U >> su) << su);
-        }
+  if (more) {
+    int k = 0;
+    for (uint32_t q = allst; q; q &= q - 1, ++k) {
+      if (!((more >> k) & 1u)) continue;
+      const int b = __ffs(q) - 1;
+      uint32_t ov = overlaps(b);
+      {
+        const int t = __ffs(ov) - 1;  // the linked one
+        const uint32_t U = ((upf >> t) & 1u) ? upf : upb;
+        ov &= ~(low_run(U >> t) << t);
+      }
+      while (ov) {
+        const int t = __ffs(ov) - 1;
+        const uint32_t U = ((upf >> t) & 1u) ? upf : upb;
+        unite_s16(par, rb + k, upper(t));
+        ov &= ~(low_run(U >> t) << t);
       }
     }
-    __syncwarp();
   }
+  __syncwarp();
   // 3. flatten; per local root: pixel count + border-background bit
   const int nruns = __popc(allst);
   // pointer jumping in place (a concurrent store only replaces a parent by an
