@@ -524,3 +524,29 @@ def test_label_runs_match_per_pixel_roots(rtg, oracle, shape, rc, conn):
         ref = oracle.process_tile(rgb, op)
         assert a[4] == ref["n"] and np.array_equal(a[1], ref["labels"])
         np.testing.assert_allclose(a[3], ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+
+
+@pytest.mark.parametrize("nuc,rh", [(250, 10), (300, 0), (1, 0), (40, 300), (0, 5), (-3, 2)])
+def test_label_runs_threshold_planes_params(rtg, oracle, nuc, rh):
+    """The streaming kernel's threshold / seed / tissue bit planes (run-table
+    path) across the corners of the ReconToNuclei parameters: seed threshold
+    above 255 (no seeds), foreground threshold above 255 (nothing), a
+    threshold of 1, and t <= 0 (the candidates are the tissue mask, bytes
+    path).  Same output as the per-pixel form and as the oracle."""
+    _need_gpu()
+    h, w = 512, 768
+    rgb = rtg.synth_tile_host(6, 3, h, w)
+    p = rtg.default_params()
+    p.nuc_thresh, p.recon_h = nuc, rh
+    op = oracle.default_params()
+    op.nuc_thresh, op.recon_h = nuc, rh
+    ref = oracle.process_tile(rgb, op)
+    outs = []
+    with rtg.Context(0, 1024, 1024, 1 << 15) as ctx:
+        for runs in (1, 0):
+            ctx.set_option(rtg.OPT_LABEL_RUNS, runs)
+            outs.append(ctx.process_tile(rgb, p))
+    for mask, labels, _, feats, n in outs:
+        assert n == ref["n"]
+        assert np.array_equal(mask, ref["mask"]) and np.array_equal(labels, ref["labels"])
+        np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
