@@ -506,10 +506,39 @@ int edt(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
 // (dq of background pixels is not written; a gated whole-tile pass takes over
 // when some distance exceeds the windowed search).
 constexpr int kBitPad = 2;
+// 8-neighbour foreground mask of p (bit t = row-major neighbour t of 8) from
+// the 1-bit foreground plane: three funnel-shifted 3-bit windows instead of
+// eight byte loads (fgb: the plane after its kBitPad leading pad words).
+__device__ __forceinline__ uint32_t fg_nbrs(int h, int w, const uint32_t* __restrict__ fgb,
+                                            int32_t p, int y, int x) {
+  auto row3 = [&](int32_t q) -> uint32_t {  // bits of columns x-1, x, x+1 of the row of q
+    const int32_t b = q - 1;
+    const int32_t wi = b >> 5;  // arithmetic shift: -1 before the first word (pad)
+    return __funnelshift_r(fgb[wi], fgb[wi + 1], (uint32_t)b & 31u) & 7u;
+  };
+  const uint32_t edge = (x == 0 ? 1u : 0u) | (x == w - 1 ? 4u : 0u);  // columns outside
+  const uint32_t up = y > 0 ? row3(p - w) & ~edge : 0u;
+  const uint32_t mid = row3(p) & ~edge;
+  const uint32_t dn = y + 1 < h ? row3(p + w) & ~edge : 0u;
+  return up | ((mid & 1u) << 3) | ((mid & 4u) << 2) | (dn << 5);
+}
+
+// fg_nbrs of the k-th listed pixel p: from the per-list-index cache nbm
+// (k_edt_rowdist fills it) or recomputed.
+__device__ __forceinline__ uint32_t list_nbrs(int h, const FastDiv& dw,
+                                              const uint32_t* __restrict__ fgb,
+                                              const uint8_t* __restrict__ nbm, int k, int32_t p) {
+  if (nbm) return nbm[k];
+  const int w = (int)dw.d;
+  const int y = fdiv(p, dw), x = p - y * w;
+  return fg_nbrs(h, w, fgb, p, y, x);
+}
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base);
+// nbm (optional): receives fg_nbrs of every listed pixel by list index.
 int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
-             const int32_t* count, const uint32_t* bits_base, uint16_t* dq);
+             const int32_t* count, const uint32_t* bits_base, uint16_t* dq,
+             uint8_t* nbm = nullptr);
 // basin doubles as i32 scratch; the ids are only written when want_basin.
 // list_ready: ctx->fg_list / misc[4] / fg_bits already describe `mask`.
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,

@@ -463,7 +463,8 @@ __device__ __forceinline__ uint32_t row_nearest_bg(const uint32_t* __restrict__ 
 // columns, 255 beyond), from two funnel-shifted words of the 1-bit plane.
 __global__ void __launch_bounds__(256)
 k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-              const uint32_t* __restrict__ bits, FastDiv dw, uint8_t* __restrict__ hd) {
+              const uint32_t* __restrict__ bits, FastDiv dw, uint8_t* __restrict__ hd, int h,
+              uint8_t* __restrict__ nbm) {
   pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
@@ -471,6 +472,7 @@ k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ coun
     const int32_t p = list[k];
     const int y = fdiv(p, dw), x = p - y * w;
     hd[p] = (uint8_t)row_nearest_bg(bits, y * w, x, w);
+    if (nbm) nbm[k] = (uint8_t)fg_nbrs(h, w, bits, p, y, x);
   }
 }
 
@@ -584,7 +586,7 @@ int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* li
 }
 
 int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
-             const int32_t* count, const uint32_t* bits_base, uint16_t* dq) {
+             const int32_t* count, const uint32_t* bits_base, uint16_t* dq, uint8_t* nbm) {
   const int nseg = (int)ceil_div(h, kSeg);
   uint16_t* seg = reinterpret_cast<uint16_t*>(ctx->seg_summary);
   uint16_t* g = ctx->u16c;
@@ -595,7 +597,7 @@ int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
   uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
   const FastDiv dwv = make_div((uint32_t)w);
   RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,
-                                                           hd));
+                                                           hd, (int)h, nbm));
   RTG_LAUNCH("k_edt_rowdist");
   const uint32_t* bits = bits_base + kBitPad;
   RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, bits, hd, (int)h, dwv,

@@ -44,24 +44,6 @@ __global__ void k_ws_prep(int64_t n, const uint8_t* __restrict__ mask,
     Fw[i] = (uint16_t)(mask[i] ? (uint32_t)F[i] + 1u : 0u);
 }
 
-// 8-neighbour foreground mask of p (bit t = row-major neighbour t of 8).
-// 8-neighbour foreground mask of p (bit t = row-major neighbour t of 8) from
-// the 1-bit foreground plane: three funnel-shifted 3-bit windows instead of
-// eight byte loads (fgb: the plane after its kBitPad leading pad words).
-__device__ __forceinline__ uint32_t fg_nbrs(int h, int w, const uint32_t* __restrict__ fgb,
-                                            int32_t p, int y, int x) {
-  auto row3 = [&](int32_t q) -> uint32_t {  // bits of columns x-1, x, x+1 of the row of q
-    const int32_t b = q - 1;
-    const int32_t wi = b >> 5;  // arithmetic shift: -1 before the first word (pad)
-    return __funnelshift_r(fgb[wi], fgb[wi + 1], (uint32_t)b & 31u) & 7u;
-  };
-  const uint32_t edge = (x == 0 ? 1u : 0u) | (x == w - 1 ? 4u : 0u);  // columns outside
-  const uint32_t up = y > 0 ? row3(p - w) & ~edge : 0u;
-  const uint32_t mid = row3(p) & ~edge;
-  const uint32_t dn = y + 1 < h ? row3(p + w) & ~edge : 0u;
-  return up | ((mid & 1u) << 3) | ((mid & 4u) << 2) | (dn << 5);
-}
-
 __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
   const int k = t < 4 ? t : t + 1;  // skip the centre
   return p + (k / 3 - 1) * w + (k % 3 - 1);
@@ -114,7 +96,8 @@ __device__ __forceinline__ void unite_backward(int32_t* par, int w, int32_t p, u
 // appended to the flat list (their seed arrow is set by k_ws_union).
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const uint32_t* __restrict__ mask, const uint16_t* __restrict__ Fw,
+            const uint32_t* __restrict__ mask, const uint8_t* __restrict__ nbm,
+            const uint16_t* __restrict__ Fw,
             uint8_t* __restrict__ dir, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
             uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
@@ -128,12 +111,11 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
     int32_t p = 0;
     if (k < n) {
       p = list[k];
-      const int y = fdiv(p, dw), x = p - y * w;
       const uint32_t f = Fw[p];
       uint32_t best = f;
       int arg = -1;
       uint32_t fv[8];
-      gather8(Fw, w, p, fg_nbrs(h, w, mask, p, y, x), 0u, fv);
+      gather8(Fw, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0u, fv);
 #pragma unroll
       for (int t = 0; t < 8; ++t)  // row-major: first max = min index
         if (fv[t] > best) { best = fv[t]; arg = t; }
@@ -441,7 +423,8 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
 // warp iterates it to its fixed point.  Output: Fw = fg ? F + 1 : 0.
 __global__ void __launch_bounds__(256)
 k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-            const uint32_t* __restrict__ mask, const uint16_t* __restrict__ dq, int32_t ws_h,
+            const uint32_t* __restrict__ mask, const uint8_t* __restrict__ nbm,
+            const uint16_t* __restrict__ dq, int32_t ws_h,
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
             int32_t* __restrict__ scount) {
@@ -455,10 +438,9 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
     int32_t p = 0;
     if (k < n) {
       p = list[k];
-      const int y = fdiv(p, dw), x = p - y * w;
       const int32_t v = dq[p];
       int32_t dv[8];
-      gather8(dq, w, p, fg_nbrs(h, w, mask, p, y, x), 0, dv);
+      gather8(dq, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0, dv);
       int32_t mx = 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) mx = max(mx, dv[t]);
@@ -707,7 +689,7 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
 // warp touches one or two words).
 __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ list,
                               const int32_t* __restrict__ count,
-                              const uint32_t* __restrict__ mask,
+                              const uint32_t* __restrict__ mask, const uint8_t* __restrict__ nbm,
                               const int32_t* __restrict__ basin, uint8_t* __restrict__ sep,
                               uint32_t* __restrict__ sep_bits) {
   pdl_enter();
@@ -722,10 +704,9 @@ __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ lis
     bool keep = false;
     if (k < n) {
       p = list[k];
-      const int y = fdiv(p, dw), x = p - y * w;
       const int32_t b = basin[p];
       int32_t bv[8];
-      gather8(basin, w, p, fg_nbrs(h, w, mask, p, y, x), 0, bv);
+      gather8(basin, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0, bv);
       keep = b > 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) keep &= bv[t] <= b;
@@ -784,10 +765,14 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   if (!list_ready) RTG_TRY(fg_list(ctx, mask, h, w, fgl, fgn, ctx->fg_bits));
   const uint32_t* fgbits = ctx->fg_bits + kBitPad;  // neighbour tests of the list kernels
   const bool iwpp_hmax = ctx->hmax_impl == 1;
+  // 8-neighbour masks of the listed pixels, by list index (k_edt_rowdist
+  // builds them; the recon plane is dead by now); the IWPP HMAX path has
+  // no list EDT and recomputes them
+  uint8_t* nbm = iwpp_hmax ? nullptr : ctx->recon;
   if (iwpp_hmax) {
     RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));  // every pixel (IWPP reads all)
   } else {
-    RTG_TRY(edt_list(ctx, h, w, fgl, fgn, ctx->fg_bits, dq));
+    RTG_TRY(edt_list(ctx, h, w, fgl, fgn, ctx->fg_bits, dq, nbm));
   }
   prof_mark(ctx, RTG_STAGE_MARKERS);
   uint16_t* Fw;
@@ -803,7 +788,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     int32_t* par = ctx->i32c;
     int32_t* slot = ctx->i32b;
     uint8_t* sflag = ctx->m1;
-    RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, dq, ws_h, Fw, sflag,
+    RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
+                      (const uint8_t*)nbm, dq, ws_h, Fw, sflag,
                                             par, basin, list, count));
     RTG_LAUNCH("k_hmax_init");
     RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)h, dwv, fgbits, sflag, list, count, par));
@@ -826,7 +812,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* par = ctx->i32c;
   uint8_t* flat = ctx->m1;
   int32_t* flat_count = ctx->misc + 5;
-  RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, Fw, dir, par, basin,
+  RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
+                    (const uint8_t*)nbm, Fw, dir, par, basin,
                                           flat, ctx->flat_list, flat_count));
   RTG_LAUNCH("k_ws_arrows");
   RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
@@ -845,7 +832,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
-  RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits, basin, sep,
+  RTG_CUDA(launch_k(ctx, k_ws_separate, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
+                    (const uint8_t*)nbm, basin, sep,
                     sep_bits ? ctx->sep_bits : (uint32_t*)nullptr));
   RTG_LAUNCH("k_ws_separate");
   return RTG_OK;
