@@ -72,20 +72,24 @@ __device__ __forceinline__ void unite_s(int32_t* par, int32_t a, int32_t b) {
 // chain per round where per-entry finds walk them link by link.  A
 // concurrent store only replaces a parent by an ancestor, and roots never
 // change, so "par[par[k]] == par[k]" read at any time means par[k] is final.
-__device__ __forceinline__ void flatten_jump(int32_t* par, int rb, int nruns) {
+// Only entries not yet pointing at a root are revisited (a mask per lane).
+template <typename T>
+__device__ __forceinline__ void flatten_jump_t(T* par, int rb, int nruns) {
+  uint32_t pend = nruns >= 32 ? 0xFFFFFFFFu : (1u << nruns) - 1u;
   while (true) {
-    bool changed = false;
-    for (int k = 0; k < nruns; ++k) {
+    for (uint32_t m = pend; m; m &= m - 1) {
+      const int k = __ffs(m) - 1;
       const int32_t p = par[rb + k];
       const int32_t gp = par[p];
-      if (gp != p) {
-        par[rb + k] = gp;
-        changed = true;
-      }
+      if (gp != p) par[rb + k] = (T)gp;
+      else pend &= ~(1u << k);
     }
     __syncwarp();
-    if (!__any_sync(0xFFFFFFFFu, changed)) break;
+    if (!__any_sync(0xFFFFFFFFu, pend != 0)) break;
   }
+}
+__device__ __forceinline__ void flatten_jump(int32_t* par, int rb, int nruns) {
+  flatten_jump_t(par, rb, nruns);
 }
 
 // ---- foreground predicates ----------------------------------------------------
@@ -933,19 +937,7 @@ __device__ __forceinline__ int32_t find_root16_c(uint16_t* par, int32_t a) {
 
 // flatten_jump on the 16-bit forest.
 __device__ __forceinline__ void flatten_jump16(uint16_t* par, int rb, int nruns) {
-  while (true) {
-    bool changed = false;
-    for (int k = 0; k < nruns; ++k) {
-      const int32_t p = par[rb + k];
-      const int32_t gp = par[p];
-      if (gp != p) {
-        par[rb + k] = (uint16_t)gp;
-        changed = true;
-      }
-    }
-    __syncwarp();
-    if (!__any_sync(0xFFFFFFFFu, changed)) break;
-  }
+  flatten_jump_t(par, rb, nruns);
 }
 
 __device__ __forceinline__ int32_t atomic_min16(uint16_t* par, int32_t a, int32_t b) {
