@@ -284,12 +284,12 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
     // segmented reduction towards the run head: lanes (lane, lane + off] must
     // hold no head.  Nine fields travel in six shuffles: sum x (< 2^18, x <
     // 8192) with the perimeter count (<= 128), sum I (< 2^13) with sum of
-    // gradients (< 2^18), and min I with 255 - max I as two bytes combined by
-    // one byte-wise min; no packed field can carry into its neighbour.
+    // gradients (< 2^18), and min I with 255 - max I as two 16-bit halves
+    // combined by one 16x2 min; no packed field can carry into its neighbour.
     uint32_t A = (l ? (uint32_t)x : 0u) | (per << 18);
     uint32_t B = v | (gq << 13);
     uint32_t sxx = l ? (uint32_t)x * (uint32_t)x : 0u, sii = v * v, sgg = gq * gq;
-    uint32_t M = l ? (v | ((255u - v) << 8)) : 0xFFFFu;
+    uint32_t M = l ? (v | ((255u - v) << 16)) : 0xFFFFFFFFu;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t oA = __shfl_down_sync(full, A, off);
@@ -305,11 +305,11 @@ k_feat_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
         sxx += oxx;
         sii += oii;
         sgg += ogg;
-        M = __vminu4(M, oM);
+        M = __vminu2(M, oM);  // one VIMNMX.U16x2 (the 8-bit form is emulated)
       }
     }
     const uint32_t sx = A & 0x3FFFFu, sp = A >> 18, si = B & 0x1FFFu, sg = B >> 13;
-    const uint32_t mni = M & 0xFFu, mxi = 255u - ((M >> 8) & 0xFFu);
+    const uint32_t mni = M & 0xFFFFu, mxi = 255u - (M >> 16);
     // run = lanes [lane, end] for a head lane; its last pixel has the largest x
     const unsigned after = (heads >> 1) >> lane;  // heads strictly after this lane
     const int end = after ? lane + __ffs(after) - 1 : 31;

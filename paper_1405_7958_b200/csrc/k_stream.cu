@@ -22,7 +22,7 @@ struct CdBits {
   uint16_t* fg = nullptr;
   uint16_t* sd = nullptr;
   uint16_t* ts = nullptr;
-  uint32_t t4 = 0, s4 = 0;  // thresholds replicated into the four bytes
+  uint32_t t4 = 0, s4 = 0;  // 256 - threshold, replicated into the four bytes
   int fg_on = 0, sd_on = 0;  // 0: threshold above 255, no pixel qualifies
 };
 
@@ -81,6 +81,15 @@ __device__ __forceinline__ uint32_t msb_nib(uint32_t v) {
 __device__ __forceinline__ uint32_t lsb_nib(uint32_t v) {
   return (((v & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
 }
+// Byte-wise x >= t as byte MSBs, tc = (256 - t) in every byte (1 <= t <=
+// 255): bit 7 of each byte of x + tc carried out iff x >= t.  The low seven
+// bits add without crossing bytes; the carry out of bit 7 is the majority of
+// the two bit-7 inputs and the carry into it (three logic ops; the
+// __vcmpgeu4 intrinsic is emulated in ~7).
+__device__ __forceinline__ uint32_t ge_msbs(uint32_t x, uint32_t tc) {
+  const uint32_t lo = (x & 0x7F7F7F7Fu) + (tc & 0x7F7F7F7Fu);
+  return ((x & tc) | (x & lo) | (tc & lo)) & 0x80808080u;
+}
 
 // 16 pixels (48 interleaved RGB bytes in wv) -> 16 hematoxylin, tissue (and
 // marker) bytes with the lane-replicated LUTs; with bits.fg also the
@@ -119,8 +128,8 @@ __device__ __forceinline__ void cd_group(const uint32_t (&wv)[12], const int32_t
     uint32_t f = 0, sd = 0, t = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (bits.fg_on) f |= msb_nib(__vcmpgeu4(ho[k], bits.t4)) << (4 * k);
-      if (bits.sd_on) sd |= msb_nib(__vcmpgeu4(ho[k], bits.s4)) << (4 * k);
+      if (bits.fg_on) f |= msb_nib(ge_msbs(ho[k], bits.t4)) << (4 * k);
+      if (bits.sd_on) sd |= msb_nib(ge_msbs(ho[k], bits.s4)) << (4 * k);
       t |= lsb_nib(to[k]) << (4 * k);
     }
     bits.fg[g] = (uint16_t)f;
@@ -440,8 +449,10 @@ int launch_colordeconv(rtg_ctx* ctx, const uint8_t* rgb, int64_t h, int64_t w,
     bits.ts = reinterpret_cast<uint16_t*>(recon_bits[2]);
     bits.fg_on = t <= 255;
     bits.sd_on = ts <= 255;
-    bits.t4 = 0x01010101u * (uint32_t)(t <= 255 ? (t < 0 ? 0 : t) : 0);
-    bits.s4 = 0x01010101u * (uint32_t)(ts <= 255 ? (ts < 0 ? 0 : ts) : 0);
+    // (256 - t) per byte for ge_msbs; t >= 1 here (nuc_thresh > 0, recon_h >= 0)
+    bits.t4 = 0x01010101u * (uint32_t)(t >= 1 && t <= 255 ? 256 - t : 0);
+    bits.s4 = 0x01010101u * (uint32_t)(ts >= 1 && ts <= 255 ? 256 - ts : 0);
+    if (t < 1) return fail(RTG_ERR_INTERNAL, "threshold planes need nuc_thresh >= 1");
     if (bits_written) *bits_written = true;
     tissue = nullptr;  // the tissue plane goes out as bits only
   } else if (!tissue) {
