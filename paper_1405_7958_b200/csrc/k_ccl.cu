@@ -816,11 +816,23 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int til
     const int r = 4 * k + g;
     if (y0 + r >= h) break;
     const uint32_t b = s_bits[wid][r], st = b & ~(b << 1);
-    int32_t o[4];
+    const uint32_t nib = (b >> cq) & 0xFu;
+    int32_t o[4] = {0, 0, 0, 0};
+    if (nib) {
+      // no run starting inside cq+1 .. cq+3 (the common case): every set
+      // pixel of the four lies in the run holding column cq - one lookup
+      const uint32_t inner = (st >> (cq + 1)) & 7u;
+      if (!inner) {
+        const int32_t lab = s_lab[wid][r * 16 + __popc(st & ((2u << cq) - 1u)) - 1];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = cq + j;
-      o[j] = ((b >> c) & 1u) ? s_lab[wid][r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : 0;
+        for (int j = 0; j < 4; ++j) o[j] = ((nib >> j) & 1u) ? lab : 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = cq + j;
+          o[j] = ((b >> c) & 1u) ? s_lab[wid][r * 16 + __popc(st & ((2u << c) - 1u)) - 1] : 0;
+        }
+      }
     }
     int32_t* dst = labels + (int64_t)(y0 + r) * w + x0 + cq;
     if (mask_out)
