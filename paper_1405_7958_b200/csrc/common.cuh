@@ -187,6 +187,7 @@ struct rtg_ctx {
   int label_runs = 1;   // stage labellings in run-table form (k_ccl.cu CclRuns) when the shape allows
   bool ccl_runs_live = false;  // the last ccl_roots left run tables for ccl_canonical
   bool cand_bits = false;      // recon left the candidates as row masks (fill_area_joint reads them)
+  bool mask_bytes_live = false;  // fill_area_joint wrote its mask bytes (the EDT reuses them)
   bool sep_bits_live = false;  // fill_area_joint cleared sep_bits: the watershed writes the
                                // separated mask there, the labelling reads it and writes the bytes
   int use_pdl = 0;    // programmatic dependent launch between the stage's kernels
@@ -536,9 +537,12 @@ __device__ __forceinline__ uint32_t list_nbrs(int h, const FastDiv& dw,
 int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* list,
             int32_t* count, uint32_t* bits_base);
 // nbm (optional): receives fg_nbrs of every listed pixel by list index.
+// hd_mask (optional): the mask's bytes (0 = background), reused in place as
+// the row-distance plane (foreground bytes are overwritten with values >= 1,
+// so it stays a valid mask).
 int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
              const int32_t* count, const uint32_t* bits_base, uint16_t* dq,
-             uint8_t* nbm = nullptr);
+             uint8_t* nbm = nullptr, uint8_t* hd_mask = nullptr);
 // basin doubles as i32 scratch; the ids are only written when want_basin.
 // list_ready: ctx->fg_list / misc[4] / fg_bits already describe `mask`.
 int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,

@@ -2021,6 +2021,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
                       sep_bits ? ctx->sep_bits : nullptr));
     RTG_LAUNCH("k_fb_emit");
     ctx->sep_bits_live = sep_bits;
+    ctx->mask_bytes_live = out_bytes;
     return RTG_OK;
   }
   int blocks = (int)ceil_div(n, 1024);

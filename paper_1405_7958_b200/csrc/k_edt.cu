@@ -481,6 +481,7 @@ k_edt_rowdist(const int32_t* __restrict__ list, const int32_t* __restrict__ coun
 // best.  Exact while the result is <= 32^2 (every background pixel within
 // Chebyshev distance 32 is seen); beyond that need_full is raised and the
 // whole-tile pass runs.
+template <bool kBgZero>
 __global__ void __launch_bounds__(256)
 k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
            const uint32_t* __restrict__ bits, const uint8_t* __restrict__ hd, int h, FastDiv dw,
@@ -508,9 +509,11 @@ k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
         const uint32_t dy = dy0 + j;
         const bool vu = y >= (int)dy, vd = y + (int)dy < h;
         const int32_t qu = p - (int32_t)dy * w, qd = p + (int32_t)dy * w;
-        mu[j] = vu ? (bits[qu >> 5] >> (qu & 31)) & 1u : 1u;
+        // kBgZero: the hd plane holds 0 at background pixels (the joint
+        // fill/area stage wrote the mask bytes there), no bit tests
+        mu[j] = kBgZero ? 1u : vu ? (bits[qu >> 5] >> (qu & 31)) & 1u : 1u;
         hu[j] = vu ? hd[qu] : 255u;
-        md[j] = vd ? (bits[qd >> 5] >> (qd & 31)) & 1u : 1u;
+        md[j] = kBgZero ? 1u : vd ? (bits[qd >> 5] >> (qd & 31)) & 1u : 1u;
         hdn[j] = vd ? hd[qd] : 255u;
       }
 #pragma unroll
@@ -586,7 +589,8 @@ int fg_list(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w, int32_t* li
 }
 
 int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
-             const int32_t* count, const uint32_t* bits_base, uint16_t* dq, uint8_t* nbm) {
+             const int32_t* count, const uint32_t* bits_base, uint16_t* dq, uint8_t* nbm,
+             uint8_t* hd_mask) {
   const int nseg = (int)ceil_div(h, kSeg);
   uint16_t* seg = reinterpret_cast<uint16_t*>(ctx->seg_summary);
   uint16_t* g = ctx->u16c;
@@ -594,13 +598,16 @@ int edt_list(rtg_ctx* ctx, int64_t h, int64_t w, const int32_t* list,
   int32_t* need_full = ctx->misc + 3;
   int32_t* row_flag = ctx->misc + 64;
   // any_zero / need_full were zeroed by the caller (watershed)
-  uint8_t* hd = ctx->m2;  // row distances (free while the watershed runs)
+  // row distances: into the mask bytes themselves when given (background
+  // stays 0, foreground becomes its distance >= 1), else into m2
+  uint8_t* hd = hd_mask ? hd_mask : ctx->m2;
   const FastDiv dwv = make_div((uint32_t)w);
   RTG_CUDA(launch_k(ctx, k_edt_rowdist, ctx->num_sms * 8, 256, 0, list, count, bits_base + kBitPad, dwv,
                                                            hd, (int)h, nbm));
   RTG_LAUNCH("k_edt_rowdist");
   const uint32_t* bits = bits_base + kBitPad;
-  RTG_CUDA(launch_k(ctx, k_edt_list, ctx->num_sms * 8, 256, 0, list, count, bits, hd, (int)h, dwv,
+  RTG_CUDA(launch_k(ctx, hd_mask ? k_edt_list<true> : k_edt_list<false>, ctx->num_sms * 8, 256, 0,
+                    list, count, bits, (const uint8_t*)hd, (int)h, dwv,
                                                         nullptr, dq, need_full));
   RTG_LAUNCH("k_edt_list");
   // the exact whole-tile pass, gated on need_full, as one cooperative launch

@@ -772,7 +772,9 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   if (iwpp_hmax) {
     RTG_TRY(edt(ctx, mask, h, w, nullptr, dq, F, ws_h));  // every pixel (IWPP reads all)
   } else {
-    RTG_TRY(edt_list(ctx, h, w, fgl, fgn, ctx->fg_bits, dq, nbm));
+    // the joint stage's mask bytes double as the row-distance plane
+    RTG_TRY(edt_list(ctx, h, w, fgl, fgn, ctx->fg_bits, dq, nbm,
+                     list_ready && ctx->mask_bytes_live ? const_cast<uint8_t*>(mask) : nullptr));
   }
   prof_mark(ctx, RTG_STAGE_MARKERS);
   uint16_t* Fw;

@@ -127,6 +127,7 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
   ctx->cand_bits = false;
   ctx->ccl_runs_live = false;
   ctx->sep_bits_live = false;
+  ctx->mask_bytes_live = false;
   // o1+o2: hematoxylin, tissue (+ the HMAX marker for the grayscale IWPP path)
   prof_mark(ctx, RTG_STAGE_COLORDECONV);
   // the streaming kernel's first CTA clears the reconstruction CCL's
@@ -164,11 +165,12 @@ int pipeline(rtg_ctx* ctx, const uint8_t* d_rgb, int64_t h, int64_t w, int64_t p
     // o4 FillHoles + o5 AreaThreshold as one joint labelling (the filled
     // mask itself is never materialised)
     prof_mark(ctx, RTG_STAGE_FILL_HOLES);
-    // the mask bytes are only read by the IWPP HMAX path (whole-tile EDT)
+    // the mask bytes: the IWPP HMAX path reads them (whole-tile EDT), the
+    // sparse EDT reuses them in place as its row-distance plane
     // the separated mask goes through a bit plane when the labelling can
     // write its bytes (4-byte stores)
     RTG_TRY(fill_area_joint(ctx, ctx->m1, h, w, p->min_area, p->max_area, ctx->m3,
-                            /*prezeroed=*/true, /*out_bytes=*/ctx->hmax_impl == 1,
+                            /*prezeroed=*/true, /*out_bytes=*/true,
                             /*sep_bits=*/(reinterpret_cast<uintptr_t>(mask) & 3) == 0));
   } else {
     // o4 FillHoles of the nucleus candidates
