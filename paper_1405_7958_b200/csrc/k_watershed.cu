@@ -647,7 +647,7 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
             const uint8_t* __restrict__ dir, const int32_t* __restrict__ par,
             int32_t* __restrict__ basin) {
   pdl_enter();
-  constexpr int kC = 4;
+  constexpr int kC = 2;
   const int n = *count;
   const int span = gridDim.x * blockDim.x * kC;
   for (int k0 = blockIdx.x * blockDim.x * kC + threadIdx.x; k0 < n; k0 += span) {
@@ -666,7 +666,11 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
     // a neighbour code: step; kDirSelf: marker reached; kDirNone: no arrow
     const int32_t wm = w + 1;
     auto moving = [](uint32_t c) { return c != kDirSelf && c != kDirNone; };
-    while (moving(d[0]) || moving(d[1]) || moving(d[2]) || moving(d[3])) {
+    while (true) {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < kC; ++j) any |= moving(d[j]);
+      if (!any) break;
 #pragma unroll
       for (int j = 0; j < kC; ++j) {
         if (moving(d[j])) {
