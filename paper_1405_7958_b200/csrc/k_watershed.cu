@@ -647,7 +647,7 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
             const uint8_t* __restrict__ dir, const int32_t* __restrict__ par,
             int32_t* __restrict__ basin) {
   pdl_enter();
-  constexpr int kC = 2;
+  constexpr int kC = 4;
   const int n = *count;
   const int span = gridDim.x * blockDim.x * kC;
   for (int k0 = blockIdx.x * blockDim.x * kC + threadIdx.x; k0 < n; k0 += span) {
