@@ -757,7 +757,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // (o8, ccl_roots(..., prezeroed)) needs cleared
   // (the separated mask itself only when it is written as bytes; the bit
   // plane was cleared by the joint fill/area stage)
-  const bool sep_bits = ctx->sep_bits_live;
+  const bool sep_bits = ctx->sep_bits_live && list_ready;  // only the stage path sets it
   ZeroList z{{ctx->misc + 1, ctx->misc + 5, alloc, sep},
              {3 * sizeof(int32_t), sizeof(int32_t), 2 * sizeof(unsigned long long), (size_t)n},
              sep_bits ? 3 : 4};
