@@ -787,8 +787,10 @@ __global__ void k_relabel(int64_t n, const int32_t* __restrict__ roots,
 // resolves its runs' labels, then 8 lanes per row write 4 pixels each
 // (16-byte stores, four rows per step).
 __global__ void __launch_bounds__(32 * kTileWarps)
-k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int tiles_x, int ntiles,
-             int32_t* __restrict__ labels, bool vec, uint8_t* __restrict__ mask_out) {
+k_label_emit(CclRuns rt, const int32_t* __restrict__ lroots, const int32_t* __restrict__ roots,
+             const uint32_t* __restrict__ bm, const int32_t* __restrict__ wprefix, FeatureAcc acc,
+             bool clear_acc, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ labels,
+             bool vec, uint8_t* __restrict__ mask_out) {
   pdl_enter();
   __shared__ int32_t s_rank[kTileWarps][512];
   __shared__ int32_t s_lab[kTileWarps][512];
@@ -798,7 +800,26 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int til
   if (tile >= ntiles) return;  // no block-wide barrier below
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   const int2 ti = __ldg(rt.tinfo + tile);
-  for (int j = lane; j < ti.y; j += 32) s_rank[wid][j] = __ldg(rank + ti.x + j);
+  // the final label of each of the tile's local roots (rank of its global
+  // root in the root bitmap + 1, what k_root_rank computes for the
+  // per-pixel form), and each label's feature accumulators reset once (at
+  // the local root that is the global root)
+  for (int j = lane; j < ti.y; j += 32) {
+    const int32_t lr = __ldg(lroots + 2 * (ti.x + j));
+    const int32_t r = __ldcg(roots + lr);
+    const int32_t label =
+        __ldg(wprefix + (r >> 5)) + __popc(__ldg(bm + (r >> 5)) & ((1u << (r & 31)) - 1u)) + 1;
+    s_rank[wid][j] = label;
+    if (clear_acc && lr == r && label <= acc.cap) {
+      const int64_t i = label - 1;
+#pragma unroll
+      for (int f = 0; f < kSumFields; ++f) acc.sums[(int64_t)f * acc.cap + i] = 0ull;
+#pragma unroll
+      for (int f = 0; f < kMinFields; ++f) acc.mins[(int64_t)f * acc.cap + i] = INT32_MAX;
+#pragma unroll
+      for (int f = 0; f < kMaxFields; ++f) acc.maxs[(int64_t)f * acc.cap + i] = -1;
+    }
+  }
   const uint32_t bits = __ldg(rt.rowbits + tile * 32 + lane);
   const uint4* src = reinterpret_cast<const uint4*>(rt.rtab + (int64_t)tile * 512 + lane * 16);
   const uint4 e0 = __ldg(src), e1 = __ldg(src + 1);
@@ -847,19 +868,12 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ rank, int h, int w, int til
   }
 }
 
-// Seeded-component mask of the run-table form (ReconToNuclei): keep byte of
-// every local root by slot, then per tile: kept runs & tissue -> out bytes.
-__global__ void k_slot_flag(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
-                            const int32_t* __restrict__ roots, const int32_t* __restrict__ flag,
-                            uint8_t* __restrict__ keep) {
-  pdl_enter();
-  const int n = *lcount;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-    keep[k] = flag[roots[lroots[2 * k]]] != 0;
-}
-
+// Seeded-component mask of the run-table form (ReconToNuclei), per tile:
+// each local root's component is kept when its global root carries the
+// seed flag; kept runs & tissue -> out bytes (or row masks).
 __global__ void __launch_bounds__(32 * kTileWarps)
-k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __restrict__ tissue,
+k_seeded_emit(CclRuns rt, const int32_t* __restrict__ lroots, const int32_t* __restrict__ roots,
+              const int32_t* __restrict__ flag, const uint8_t* __restrict__ tissue,
               int h, int w, int tiles_x, int ntiles, uint8_t* __restrict__ out,
               uint32_t* __restrict__ out_bits, const uint32_t* __restrict__ tis_bits) {
   pdl_enter();
@@ -871,7 +885,8 @@ k_seeded_emit(CclRuns rt, const uint8_t* __restrict__ keep, const uint8_t* __res
   if (tile >= ntiles) return;
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   const int2 ti = __ldg(rt.tinfo + tile);
-  for (int j = lane; j < ti.y; j += 32) s_kp[wid][j] = __ldg(keep + ti.x + j);
+  for (int j = lane; j < ti.y; j += 32)  // seeded component? (its global root's flag)
+    s_kp[wid][j] = __ldcg(flag + __ldcg(roots + __ldg(lroots + 2 * (ti.x + j)))) != 0;
   const uint32_t bits = __ldg(rt.rowbits + tile * 32 + lane);
   const uint4* src = reinterpret_cast<const uint4*>(rt.rtab + (int64_t)tile * 512 + lane * 16);
   const uint4 e0 = __ldg(src), e1 = __ldg(src + 1);
@@ -1439,7 +1454,9 @@ __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __r
 // are staged in shared memory and leave as one contiguous range.
 __global__ void __launch_bounds__(32 * kTileWarps)
 k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rtab,
-          const int2* __restrict__ tinfo, const uint8_t* __restrict__ keep, int h, int w,
+          const int2* __restrict__ tinfo, const int32_t* __restrict__ lroots,
+          const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
+          const int32_t* __restrict__ total, int32_t lo, int32_t hi, int h, int w,
           int tiles_x, int ntiles,
           uint8_t* __restrict__ out, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
           int32_t* __restrict__ count, uint32_t* __restrict__ sep_bits) {
@@ -1456,8 +1473,18 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
   const int y = y0 + lane;
   const bool row = active && y < h;
   {
-    const int2 ti = __ldg(tinfo + tile);  // the tile's keep bytes (by local-root slot)
-    for (int j = lane; j < ti.y; j += 32) s_keep[wid][j] = __ldg(keep + ti.x + j);
+    // keep decision of each of the tile's local roots (k_fb_keep's, inline):
+    // global root -> top-level ancestor -> subtree area in range
+    const int2 ti = __ldg(tinfo + tile);
+    for (int j = lane; j < ti.y; j += 32) {
+      const int32_t t = __ldcg(top + __ldcg(roots + __ldg(lroots + 2 * (ti.x + j))));
+      bool kp = false;
+      if (t >= 0) {
+        const int32_t a = __ldcg(total + t);
+        kp = a >= lo && a <= hi;
+      }
+      s_keep[wid][j] = kp;
+    }
   }
   const uint32_t fgb = row ? __ldg(rowbits + tile * 32 + lane) : 0u;
   const uint32_t bgb = row ? ~fgb : 0u;
@@ -1722,15 +1749,12 @@ int recon_threshold_uf(rtg_ctx* ctx, const uint8_t* hema, const uint8_t* tissue,
   else
     RTG_TRY(ccl_run(ctx, pred, h, w, conn, roots, nullptr, flag, nullptr, prezeroed, rt));
   if (rt.rtab) {
-    uint8_t* keep = ctx->m2;  // one byte per local-root slot (free until the joint fill/area)
-    RTG_CUDA(launch_k(ctx, k_slot_flag, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8,
-                      (const int32_t*)roots, (const int32_t*)flag, keep));
-    RTG_LAUNCH("k_slot_flag");
     const int tiles_x = (int)(w / 32);
     const int ntiles = tiles_x * (int)ceil_div(h, 32);
     ctx->cand_bits = bits_out;
     RTG_CUDA(launch_k(ctx, k_seeded_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
-                      0, rt, (const uint8_t*)keep, tissue, (int)h, (int)w, tiles_x, ntiles, out,
+                      0, rt, (const int32_t*)ctx->lroots, (const int32_t*)roots,
+                      (const int32_t*)flag, tissue, (int)h, (int)w, tiles_x, ntiles, out,
                       bits_out ? reinterpret_cast<uint32_t*>(out) : (uint32_t*)nullptr,
                       in_bits ? (const uint32_t*)in_bits[2] : (const uint32_t*)nullptr));
     RTG_LAUNCH("k_seeded_emit");
@@ -1906,24 +1930,27 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   RTG_CUDA(launch_k(ctx, k_bm_scan, nchunks, 256, 0, nwords, nchunks, ctx->root_bm, status,
                     ctx->root_wprefix, d_n));
   RTG_LAUNCH("k_bm_scan");
-  // run-table form (ccl_roots left the tables): labels written per tile
+  // run-table form (ccl_roots left the tables): labels (and the ranks
+  // behind them) written per tile
   const bool by_slot = ctx->ccl_runs_live;
   ctx->ccl_runs_live = false;
-  RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
-                                                         ctx->root_bm, ctx->root_wprefix, rank,
-                                                         clear_acc ? *clear_acc : ctx->acc,
-                                                         clear_acc != nullptr, by_slot));
-  RTG_LAUNCH("k_root_rank");
   if (by_slot) {
     const int tiles_x = (int)(w / 32);
     const int ntiles = tiles_x * (int)ceil_div(h, 32);
     RTG_CUDA(launch_k(ctx, k_label_emit, (unsigned)ceil_div(ntiles, kTileWarps), 32 * kTileWarps,
-                      0, ccl_runs_for(ctx, h, w), (const int32_t*)rank, (int)h, (int)w, tiles_x,
-                      ntiles, labels, (reinterpret_cast<uintptr_t>(labels) & 15) == 0,
+                      0, ccl_runs_for(ctx, h, w), (const int32_t*)ctx->lroots, roots,
+                      (const uint32_t*)ctx->root_bm, (const int32_t*)ctx->root_wprefix,
+                      clear_acc ? *clear_acc : ctx->acc, clear_acc != nullptr, (int)h, (int)w,
+                      tiles_x, ntiles, labels, (reinterpret_cast<uintptr_t>(labels) & 15) == 0,
                       mask_out));
     RTG_LAUNCH("k_label_emit");
     return RTG_OK;
   }
+  RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
+                                                         ctx->root_bm, ctx->root_wprefix, rank,
+                                                         clear_acc ? *clear_acc : ctx->acc,
+                                                         clear_acc != nullptr, false));
+  RTG_LAUNCH("k_root_rank");
   if (mask_out) return fail(RTG_ERR_INTERNAL, "mask bytes requested without run tables");
   RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
   RTG_LAUNCH("k_relabel");
@@ -2010,13 +2037,11 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   RTG_CUDA(launch_k(ctx, k_fb_tree, gl, 256, 0, ctx->lroots, lcount, cand, (int)w, roots, counts, top,
                     total, rt));
   RTG_LAUNCH("k_fb_tree");
-  uint8_t* keep = ctx->m2;  // free until the EDT's row distances
-  RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
-                    max_area, keep, runs));
-  RTG_LAUNCH("k_fb_keep");
   if (runs) {
     RTG_CUDA(launch_k(ctx, k_fb_emit, tgrid, 32 * kTileWarps, 0, (const uint32_t*)rowbits,
-                      (const uint16_t*)rtab, (const int2*)tinfo, (const uint8_t*)keep, (int)h, (int)w, tiles_x, ntiles,
+                      (const uint16_t*)rtab, (const int2*)tinfo, (const int32_t*)ctx->lroots,
+                      (const int32_t*)roots, (const int32_t*)top, (const int32_t*)total,
+                      min_area, max_area, (int)h, (int)w, tiles_x, ntiles,
                       out_bytes ? out : nullptr, bits_base + kBitPad, ctx->fg_list, ctx->misc + 4,
                       sep_bits ? ctx->sep_bits : nullptr));
     RTG_LAUNCH("k_fb_emit");
@@ -2024,6 +2049,10 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
     ctx->mask_bytes_live = out_bytes;
     return RTG_OK;
   }
+  uint8_t* keep = ctx->m2;  // free until the EDT's row distances
+  RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
+                    max_area, keep, false));
+  RTG_LAUNCH("k_fb_keep");
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
   RTG_CUDA(launch_k(ctx, k_fb_filter, blocks, 256, 0, n, roots, (const uint8_t*)keep, out,
