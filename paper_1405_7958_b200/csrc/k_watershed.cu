@@ -193,8 +193,7 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
 __global__ void __launch_bounds__(256)
 k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
               const int32_t* __restrict__ par, int32_t* cnt, uint8_t* __restrict__ dir,
-              unsigned long long* alloc,
-              int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+              unsigned long long* alloc) {
   pdl_enter();
   __shared__ unsigned long long sm[9];
   const int n = *flat_count;
@@ -214,10 +213,8 @@ k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__
     }
     const unsigned long long slot = block_reserve2(root >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
     if (root >= 0) {
-      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull), c = (int32_t)(slot >> 32);
+      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull);
       __stcg(cnt + root, kSeeded | base);  // members still read the flag: it stays set
-      comp_root[c] = root;
-      comp_size[c] = sz;
     }
   }
 }
@@ -484,8 +481,7 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mas
 // the form k_ws_scatter reads) and enters the component list.
 __global__ void __launch_bounds__(256)
 k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-             const int32_t* __restrict__ par, int32_t* cnt, unsigned long long* alloc,
-             int32_t* __restrict__ comp_root, int32_t* __restrict__ comp_size) {
+             const int32_t* __restrict__ par, int32_t* cnt, unsigned long long* alloc) {
   pdl_enter();
   __shared__ unsigned long long sm[9];
   const int n = *count;
@@ -499,10 +495,8 @@ k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count
     }
     const unsigned long long slot = block_reserve2(i >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
     if (i >= 0) {
-      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull), c = (int32_t)(slot >> 32);
+      const int32_t base = (int32_t)(slot & 0xFFFFFFFFull);
       cnt[i] = kSeeded | base;
-      comp_root[c] = i;
-      comp_size[c] = sz;
     }
   }
 }
@@ -742,9 +736,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   const FastDiv dwv = make_div((uint32_t)w);
   int32_t* fgl = ctx->fg_list;
   int32_t* fgn = ctx->misc + 4;  // foreground count
-  // component lists (root, size): the arena holds 16 B per pixel
-  int32_t* comp_root = reinterpret_cast<int32_t*>(ctx->arena);
-  int32_t* comp_size = comp_root + n;
+
   // per-member cache of long component ranges (the arena's second half)
   int2* member_scratch = reinterpret_cast<int2*>(ctx->arena + 8 * n);
   // counters of the whole o6/o7 chain, zeroed here in one launch: misc[1]
@@ -802,8 +794,7 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     RTG_LAUNCH("k_hmax_union");
     RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, list, count, nullptr, par, basin, slot));
     RTG_LAUNCH("k_ws_roots");
-    RTG_CUDA(launch_k(ctx, k_hmax_alloc, g, 256, 0, list, count, par, basin, alloc, comp_root,
-                                             comp_size));
+    RTG_CUDA(launch_k(ctx, k_hmax_alloc, g, 256, 0, list, count, par, basin, alloc));
     RTG_LAUNCH("k_hmax_alloc");
     RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, list, count, par, basin, slot, ctx->lroots));
     RTG_LAUNCH("k_ws_scatter");
@@ -827,8 +818,8 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   RTG_LAUNCH("k_ws_union");
   RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, dir, par, basin, delta));
   RTG_LAUNCH("k_ws_roots");
-  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir, walloc,
-                                            comp_root, comp_size));
+  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir,
+                    walloc));
   RTG_LAUNCH("k_ws_classify");
   RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
                                            ctx->lroots));
