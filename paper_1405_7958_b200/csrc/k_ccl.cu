@@ -734,17 +734,17 @@ k_bm_scan(int64_t nwords, int nchunks, const uint32_t* __restrict__ bm,
 __global__ void k_root_rank(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                             const int32_t* __restrict__ roots, const uint32_t* __restrict__ bm,
                             const int32_t* __restrict__ wprefix, int32_t* __restrict__ rank,
-                            FeatureAcc acc, bool clear_acc, bool by_slot) {
+                            FeatureAcc acc, bool clear_acc) {
   pdl_enter();
   // the final label (rank of the global root + 1) of every LOCAL root, so the
-  // per-pixel relabel needs one gather (local root -> label); by_slot: stored
-  // at the local root's list slot (what k_label_emit stages per tile)
+  // per-pixel relabel needs one gather (local root -> label); the run-table
+  // form computes the same inside k_label_emit
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t lr = lroots[2 * k];
     const int32_t r = roots[lr];
     const int32_t label = wprefix[r >> 5] + __popc(bm[r >> 5] & ((1u << (r & 31)) - 1u)) + 1;
-    rank[by_slot ? k : lr] = label;  // run-table form: by local-root slot
+    rank[lr] = label;
     // each label once (at its global root): reset its feature accumulators
     if (clear_acc && lr == r && label <= acc.cap) {
       const int64_t i = label - 1;
@@ -1425,12 +1425,10 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
 // The keep decision of every LOCAL root (global root -> top-level ancestor
 // -> subtree area in range), stored at the local root's pixel: the per-pixel
 // filter then needs one byte gather instead of three dependent i32 ones.
-// Run-table form (by_slot): stored at the local root's list slot instead,
-// so k_fb_emit reads a tile's keep bytes as one contiguous slice.
 __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __restrict__ lcount,
                           const int32_t* __restrict__ roots, const int32_t* __restrict__ top,
                           const int32_t* __restrict__ total, int32_t lo, int32_t hi,
-                          uint8_t* __restrict__ keep, bool by_slot) {
+                          uint8_t* __restrict__ keep) {
   pdl_enter();
   const int n = *lcount;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -1441,7 +1439,7 @@ __global__ void k_fb_keep(const int32_t* __restrict__ lroots, const int32_t* __r
       const int32_t a = total[t];
       kp = a >= lo && a <= hi;
     }
-    keep[by_slot ? k : lr] = kp ? 1 : 0;
+    keep[lr] = kp ? 1 : 0;
   }
 }
 
@@ -1949,7 +1947,7 @@ int ccl_canonical(rtg_ctx* ctx, const int32_t* roots, int64_t h, int64_t w,
   RTG_CUDA(launch_k(ctx, k_root_rank, ctx->num_sms * 4, 256, 0, ctx->lroots, ctx->misc + 8, roots,
                                                          ctx->root_bm, ctx->root_wprefix, rank,
                                                          clear_acc ? *clear_acc : ctx->acc,
-                                                         clear_acc != nullptr, false));
+                                                         clear_acc != nullptr));
   RTG_LAUNCH("k_root_rank");
   if (mask_out) return fail(RTG_ERR_INTERNAL, "mask bytes requested without run tables");
   RTG_CUDA(launch_k(ctx, k_relabel, grid_for(ctx, n), 256, 0, n, roots, rank, labels));
@@ -2051,7 +2049,7 @@ int fill_area_joint(rtg_ctx* ctx, const uint8_t* cand, int64_t h, int64_t w, int
   }
   uint8_t* keep = ctx->m2;  // free until the EDT's row distances
   RTG_CUDA(launch_k(ctx, k_fb_keep, gl, 256, 0, ctx->lroots, lcount, roots, top, total, min_area,
-                    max_area, keep, false));
+                    max_area, keep));
   RTG_LAUNCH("k_fb_keep");
   int blocks = (int)ceil_div(n, 1024);
   if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
