@@ -275,32 +275,63 @@ __global__ void __launch_bounds__(256)
 k_canny_nms(const uint8_t* __restrict__ I, int h, int w, int32_t lo2, int32_t hi2,
             uint8_t* __restrict__ cls) {
   pdl_enter();
-  __shared__ uint8_t sI[40][41];
-  __shared__ uint16_t sH[40][37];  // horizontal 5-tap sums, 36 columns
-  __shared__ uint8_t sS[36][37];
+  // rows padded to whole words: sI 40 bytes = 10 words, sH 36 + 4 u16
+  __shared__ __align__(16) uint8_t sI[40][44];
+  __shared__ __align__(16) uint16_t sH[40][40];  // horizontal 5-tap sums, 36 columns
+  __shared__ __align__(16) uint8_t sS[36][40];
   __shared__ int32_t sM[34][34];
   __shared__ int32_t sG[34][34];  // gx (high 16) | gy (low 16), tile + 1 ring
   const int y0 = blockIdx.y * 32, x0 = blockIdx.x * 32;
   const int tid = threadIdx.x;
-  // stage: 40 rows of 40 clamped bytes, one row per 8 threads
-  for (int k = tid; k < 40 * 40; k += 256) {
-    const int yy = k / 40, xx = k - yy * 40;
-    const int y = min(max(y0 - 4 + yy, 0), h - 1), x = min(max(x0 - 4 + xx, 0), w - 1);
-    sI[yy][xx] = I[(int64_t)y * w + x];
+  // stage: 40 rows of 40 clamped bytes (whole words inside the image)
+  const bool inner = y0 >= 4 && x0 >= 4 && y0 + 36 <= h && x0 + 36 <= w && (w & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(I) & 3) == 0;
+  if (inner) {
+    for (int k = tid; k < 40 * 10; k += 256) {
+      const int yy = k / 10, q = k - yy * 10;
+      *reinterpret_cast<uint32_t*>(&sI[yy][4 * q]) =
+          __ldg(reinterpret_cast<const uint32_t*>(I + (int64_t)(y0 - 4 + yy) * w + x0 - 4) + q);
+    }
+  } else {
+    for (int k = tid; k < 40 * 40; k += 256) {
+      const int yy = k / 40, xx = k - yy * 40;
+      const int y = min(max(y0 - 4 + yy, 0), h - 1), x = min(max(x0 - 4 + xx, 0), w - 1);
+      sI[yy][xx] = I[(int64_t)y * w + x];
+    }
   }
   __syncthreads();
-  // separable 5x5 binomial: (1 4 6 4 1) across, then down
-  for (int k = tid; k < 40 * 36; k += 256) {
-    const int yy = k / 36, xx = k - yy * 36;
-    const uint8_t* r = &sI[yy][xx];
-    sH[yy][xx] = (uint16_t)(r[0] + 4 * r[1] + 6 * r[2] + 4 * r[3] + r[4]);
+  // separable 5x5 binomial: (1 4 6 4 1) across, then down; four outputs per
+  // thread from two / five word reads
+  for (int k = tid; k < 40 * 9; k += 256) {
+    const int yy = k / 9, q = k - yy * 9;
+    const uint32_t a = *reinterpret_cast<const uint32_t*>(&sI[yy][4 * q]);
+    const uint32_t b = *reinterpret_cast<const uint32_t*>(&sI[yy][4 * q + 4]);
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[j] = (a >> (8 * j)) & 0xFFu;
+      v[j + 4] = (b >> (8 * j)) & 0xFFu;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = v[j] + 4 * v[j + 1] + 6 * v[j + 2] + 4 * v[j + 3] + v[j + 4];
+    *reinterpret_cast<uint2*>(&sH[yy][4 * q]) = make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
   }
   __syncthreads();
-  for (int k = tid; k < 36 * 36; k += 256) {
-    const int yy = k / 36, xx = k - yy * 36;
-    const int32_t acc = sH[yy][xx] + 4 * sH[yy + 1][xx] + 6 * sH[yy + 2][xx] +
-                        4 * sH[yy + 3][xx] + sH[yy + 4][xx];
-    sS[yy][xx] = (uint8_t)((acc + 128) >> 8);
+  for (int k = tid; k < 36 * 9; k += 256) {
+    const int yy = k / 9, q = k - yy * 9;
+    uint32_t acc[4] = {128u, 128u, 128u, 128u};
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      const uint2 u = *reinterpret_cast<const uint2*>(&sH[yy + t][4 * q]);
+      const uint32_t wgt = t == 2 ? 6u : (t == 1 || t == 3) ? 4u : 1u;
+      acc[0] += wgt * (u.x & 0xFFFFu);
+      acc[1] += wgt * (u.x >> 16);
+      acc[2] += wgt * (u.y & 0xFFFFu);
+      acc[3] += wgt * (u.y >> 16);
+    }
+    *reinterpret_cast<uint32_t*>(&sS[yy][4 * q]) =
+        (acc[0] >> 8) | ((acc[1] >> 8) << 8) | ((acc[2] >> 8) << 16) | ((acc[3] >> 8) << 24);
   }
   __syncthreads();
   // Sobel reads the smoothed value at the CLAMPED position: at the image
@@ -339,15 +370,18 @@ k_canny_nms(const uint8_t* __restrict__ I, int h, int w, int32_t lo2, int32_t hi
     sG[yy][xx] = g;
   }
   __syncthreads();
-  for (int k = tid; k < 32 * 32; k += 256) {
-    const int r = k >> 5, c = k & 31;
+  // four pixels per thread: row tid / 8, columns 4 (tid % 8) .. + 3
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = tid >> 3, c = ((tid & 7) << 2) + j;
     const int y = y0 + r, x = x0 + c;
     if (y >= h || x >= w) continue;
     const int32_t m = sM[r + 1][c + 1];
     const int32_t g = sG[r + 1][c + 1];
     const int32_t gx = (int32_t)(int16_t)(g >> 16), gy = (int32_t)(int16_t)(g & 0xFFFF);
-    const int64_t ax = gx < 0 ? -gx : gx, ay = gy < 0 ? -gy : gy;
-    const int64_t t22 = ax * 13573, ay15 = ay << 15;  // tan(22.5 deg) * 2^15
+    // |g| <= 4 * 255, so every product below fits 32 bits
+    const uint32_t ax = gx < 0 ? -gx : gx, ay = gy < 0 ? -gy : gy;
+    const uint32_t t22 = ax * 13573u, ay15 = ay << 15;  // tan(22.5 deg) * 2^15
     int da_y, da_x;  // offset of the "previous" neighbour; the next one is its mirror
     if (ay15 < t22) { da_y = 0; da_x = -1; }
     else if (ay15 > t22 + (ax << 16)) { da_y = -1; da_x = 0; }
@@ -368,8 +402,11 @@ int canny(rtg_ctx* ctx, const uint8_t* intensity, int64_t h, int64_t w, int32_t 
   RTG_CUDA(launch_k(ctx, k_canny_nms, tiles, 256, 0, intensity, (int)h, (int)w, low * low,
                     high * high, cls));
   RTG_LAUNCH("k_canny_nms");
-  // hysteresis: weak (1) pixels 8-connected to a strong (2) one
-  return recon_threshold_uf(ctx, cls, cls, h, w, 1, 1, 8, nullptr, edges);
+  // hysteresis: weak (1) pixels 8-connected to a strong (2) one (run-table
+  // labelling where the width allows: the u16 planes are free after the
+  // watershed)
+  return recon_threshold_uf(ctx, cls, cls, h, w, 1, 1, 8, nullptr, edges, false,
+                            /*runs=*/true);
 }
 
 int texture(rtg_ctx* ctx, const int32_t* labels, const uint8_t* intensity, int64_t h, int64_t w,
