@@ -550,3 +550,30 @@ def test_label_runs_threshold_planes_params(rtg, oracle, nuc, rh):
         assert n == ref["n"]
         assert np.array_equal(mask, ref["mask"]) and np.array_equal(labels, ref["labels"])
         np.testing.assert_allclose(feats, ref["features"], rtol=FEAT_RTOL, atol=FEAT_ATOL)
+
+
+def test_stage_outputs_at_unaligned_addresses(rtg):
+    """process_tile_dev into a mask buffer at an odd byte offset and a label
+    buffer 4 bytes off a 16-byte boundary: the run-table path takes its
+    scalar-store / byte-plane variants, with the same results as aligned
+    outputs."""
+    _need_gpu()
+    h, w = 1024, 1024
+    rgb = torch.from_numpy(rtg.synth_tile_host(3, 5, h, w)).cuda()
+    p = rtg.default_params()
+    with rtg.Context(0, h, w, 1 << 14) as ctx:
+        outs = []
+        for off_m, off_l in ((0, 0), (1, 1)):
+            mbuf = torch.zeros(h * w + 16, dtype=torch.uint8, device="cuda")
+            lbuf = torch.zeros(h * w + 16, dtype=torch.int32, device="cuda")
+            m = mbuf[off_m:off_m + h * w].view(h, w)
+            lab = lbuf[off_l:off_l + h * w].view(h, w)
+            feat = torch.zeros((1 << 14, 20), dtype=torch.float32, device="cuda")
+            n = torch.zeros(1, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            ctx.process_tile_dev(rgb, h, w, p, m, lab, None, feat, n)
+            ctx.sync()
+            k = int(n.item())
+            outs.append((k, m.cpu().numpy(), lab.cpu().numpy(), feat[:k].cpu().numpy()))
+    (na, ma, la, fa), (nb, mb, lb, fb) = outs
+    assert na == nb and np.array_equal(ma, mb) and np.array_equal(la, lb) and np.array_equal(fa, fb)
