@@ -424,7 +424,7 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
             const uint16_t* __restrict__ dq, int32_t ws_h,
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
-            int32_t* __restrict__ scount) {
+            int32_t* __restrict__ scount, int32_t* __restrict__ smap) {
   pdl_enter();
   const int w = (int)dw.d;
   __shared__ int32_t sm[9];
@@ -448,19 +448,24 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
         sus = true;
         Fw[p] = (uint16_t)((v > ws_h ? v - ws_h : 0) + 1);
         sflag[p] = 1;
-        par[p] = p;
-        cnt[p] = 0;
       }
     }
     const int32_t slot = block_reserve(sus ? 1 : 0, scount, sm);
-    if (sus) slist[slot] = p;
+    if (sus) {
+      // the component machinery runs on compact suspect indices (slot k):
+      // its forest and counters stay a few hundred KB, L2-resident
+      slist[slot] = p;
+      smap[p] = slot;
+      par[slot] = slot;
+      cnt[slot] = 0;
+    }
   }
 }
 
 __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                              const uint8_t* __restrict__ sflag,
                              const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-                             int32_t* par) {
+                             const int32_t* __restrict__ smap, int32_t* par) {
   pdl_enter();
   const int w = (int)dw.d;
   const int n = *count;
@@ -470,10 +475,42 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mas
     // backward neighbours only (bits 0..3: above row and left)
     uint32_t sv[8];
     gather8(sflag, w, i, fg_nbrs(h, w, mask, i, y, x) & 0xFu, 0u, sv);
-    uint32_t same = 0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) same |= sv[t] ? 1u << t : 0u;
-    unite_backward(par, w, i, same);
+    // unite_backward's skips, on compact indices (smap: pixel -> suspect slot)
+    const bool ul = sv[0], u = sv[1], ur = sv[2], l = sv[3];
+    if (l) {
+      uf_unite_g(par, k, __ldg(smap + i - 1));
+      if (ur && !u) uf_unite_g(par, k, __ldg(smap + i - w + 1));
+    } else if (u) {
+      uf_unite_g(par, k, __ldg(smap + i - w));
+    } else {
+      if (ul) uf_unite_g(par, k, __ldg(smap + i - w - 1));
+      if (ur) uf_unite_g(par, k, __ldg(smap + i - w + 1));
+    }
+  }
+}
+
+// Roots / slots / member placement of the compact suspect forest (the HMAX
+// counterparts of k_ws_roots / k_ws_scatter, indexed by suspect slot).
+__global__ void k_hmax_roots(const int32_t* __restrict__ count, int32_t* par, int32_t* cnt,
+                             int32_t* __restrict__ slot) {
+  pdl_enter();
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t r = uf_find_g(par, k);
+    if (r != k) atomicMin(par + k, r);
+    slot[k] = atomicAdd(cnt + r, 1) & kCountMask;
+  }
+}
+
+__global__ void k_hmax_scatter(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                               const int32_t* __restrict__ par, const int32_t* __restrict__ cnt,
+                               const int32_t* __restrict__ slot, int32_t* __restrict__ members) {
+  pdl_enter();
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int32_t v = cnt[par[k]];
+    const int32_t sl = slot[k], i = list[k];
+    members[(v & kCountMask) + sl] = sl == 0 ? ~i : i;  // ~: first member of a component
   }
 }
 
@@ -487,11 +524,10 @@ k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count
   const int n = *count;
   for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
     const int k = k0 + threadIdx.x;
-    int32_t i = -1, sz = 0;
-    if (k < n) {
-      i = list[k];
-      if (__ldcg(par + i) == i) sz = __ldcg(cnt + i) & kCountMask;
-      else i = -1;
+    int32_t i = -1, sz = 0;  // compact: i = suspect slot k when it is a root
+    if (k < n && __ldcg(par + k) == k) {
+      i = k;
+      sz = __ldcg(cnt + k) & kCountMask;
     }
     const unsigned long long slot = block_reserve2(i >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
     if (i >= 0) {
@@ -786,18 +822,25 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     int32_t* par = ctx->i32c;
     int32_t* slot = ctx->i32b;
     uint8_t* sflag = ctx->m1;
+    int32_t* smap = ctx->i32a;  // pixel -> suspect slot (the label plane is dead here)
+    // compact counters in the arena's first half (the basin plane may be the
+    // caller's output, whose background must stay as cleared)
+    int32_t* hcnt = reinterpret_cast<int32_t*>(ctx->arena);
     RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
                       (const uint8_t*)nbm, dq, ws_h, Fw, sflag,
-                                            par, basin, list, count));
+                                            par, hcnt, list, count, smap));
     RTG_LAUNCH("k_hmax_init");
-    RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)h, dwv, fgbits, sflag, list, count, par));
+    RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)h, dwv, fgbits, sflag, list, count,
+                      (const int32_t*)smap, par));
     RTG_LAUNCH("k_hmax_union");
-    RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, list, count, nullptr, par, basin, slot));
-    RTG_LAUNCH("k_ws_roots");
-    RTG_CUDA(launch_k(ctx, k_hmax_alloc, g, 256, 0, list, count, par, basin, alloc));
+    RTG_CUDA(launch_k(ctx, k_hmax_roots, g, 256, 0, (const int32_t*)count, par, hcnt, slot));
+    RTG_LAUNCH("k_hmax_roots");
+    RTG_CUDA(launch_k(ctx, k_hmax_alloc, g, 256, 0, list, count, par, hcnt, alloc));
     RTG_LAUNCH("k_hmax_alloc");
-    RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, list, count, par, basin, slot, ctx->lroots));
-    RTG_LAUNCH("k_ws_scatter");
+    RTG_CUDA(launch_k(ctx, k_hmax_scatter, g, 256, 0, (const int32_t*)list, (const int32_t*)count,
+                      (const int32_t*)par, (const int32_t*)hcnt, (const int32_t*)slot,
+                      ctx->lroots));
+    RTG_LAUNCH("k_hmax_scatter");
     RTG_CUDA(launch_k(ctx, k_hmax_solve, g, 256, 0, (int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
                                              alloc, Fw, member_scratch,
                                              ctx->m2 /* slot map: the EDT row distances are dead */));
