@@ -71,35 +71,24 @@ __device__ __forceinline__ void gather8(const T* a, int w, int32_t p, uint32_t m
   for (int t = 0; t < 8; ++t) v[t] = ((m >> t) & 1u) ? (S)a[nbr_index(w, p, t)] : fill;
 }
 
-// Unions of p with its backward 8-neighbours of the same component (bits
-// 0..3 of `same`: above-left, above, above-right, left), skipping the ones a
-// neighbour's own unions already imply: the left neighbour (when joined)
+// Backward unions (k_ws_union, k_hmax_union): p joins its backward
+// 8-neighbours of the same component (above-left, above, above-right, left),
+// skipping the ones a neighbour's own unions already imply: the left neighbour (when joined)
 // has already joined the above-left and above pixels, and two horizontally
 // adjacent same-component pixels above are joined with each other.  Every
 // component stays connected; the number of union-find operations (and the
 // chain lengths they build) drops from up to four per pixel to about one.
-__device__ __forceinline__ void unite_backward(int32_t* par, int w, int32_t p, uint32_t same) {
-  const bool ul = same & 1u, u = same & 2u, ur = same & 4u, l = same & 8u;
-  if (l) {
-    uf_unite_g(par, p, p - 1);
-    if (ur && !u) uf_unite_g(par, p, p - w + 1);
-  } else if (u) {
-    uf_unite_g(par, p, p - w);
-  } else {
-    if (ul) uf_unite_g(par, p, p - w - 1);
-    if (ur) uf_unite_g(par, p, p - w + 1);
-  }
-}
 
-// Arrows over the foreground list.  Non-flat pixels: steepest ascent
-// (par = -1, flat byte 0).  Flat pixels: par = self, cnt = 0, flat byte 1,
-// appended to the flat list (their seed arrow is set by k_ws_union).
+// Arrows over the foreground list.  Non-flat pixels: steepest ascent (flat
+// byte 0).  Flat pixels: flat byte 1, appended to the flat list at slot k
+// (fmap[p] = k, parK[k] = k, cntK[k] = 0); their seed arrow is set by
+// k_ws_union.
 __global__ void __launch_bounds__(256)
 k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
             const uint32_t* __restrict__ mask, const uint8_t* __restrict__ nbm,
             const uint16_t* __restrict__ Fw,
-            uint8_t* __restrict__ dir, int32_t* __restrict__ par, int32_t* __restrict__ cnt,
-            uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
+            uint8_t* __restrict__ dir, int32_t* __restrict__ fmap, int32_t* __restrict__ parK,
+            int32_t* __restrict__ cntK, uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
             int32_t* __restrict__ flat_count) {
   pdl_enter();
   const int w = (int)dw.d;
@@ -124,14 +113,43 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
         flat[p] = 0;
       } else {
         dir[p] = kDirNone;
-        par[p] = p;
-        cnt[p] = 0;
         flat[p] = 1;
         is_flat = true;
       }
     }
     const int32_t slot = block_reserve(is_flat ? 1 : 0, flat_count, sm);
-    if (is_flat) flat_list[slot] = p;
+    if (is_flat) {
+      // the plateau machinery runs on compact flat-pixel slots
+      flat_list[slot] = p;
+      fmap[p] = slot;
+      parK[slot] = slot;
+      cntK[slot] = 0;
+    }
+  }
+}
+
+// Union-find over compact slots whose root is the slot of the smallest
+// PIXEL index (keys = the flat list): a marker keeps the label a CCL of the
+// marker mask would give it (its minimum pixel).  Roots are linked by CAS,
+// larger key under smaller, so keys strictly decrease towards a root.
+__device__ __forceinline__ int32_t ukey_find(int32_t* par, int32_t a) {
+  int32_t p = __ldcg(par + a);
+  while (p != a) {
+    const int32_t gp = __ldcg(par + p);
+    if (gp != p) par[a] = gp;  // halving: an ancestor replaces the parent
+    a = p;
+    p = gp;
+  }
+  return a;
+}
+__device__ __forceinline__ void ukey_unite(int32_t* par, const int32_t* __restrict__ key,
+                                           int32_t a, int32_t b) {
+  while (true) {
+    a = ukey_find(par, a);
+    b = ukey_find(par, b);
+    if (a == b) return;
+    if (__ldg(key + a) < __ldg(key + b)) { const int32_t t = a; a = b; b = t; }
+    if (atomicCAS(par + a, a, b) == a) return;  // a was still a root
   }
 }
 
@@ -142,7 +160,7 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                            const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
                            const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count, uint8_t* __restrict__ dir,
-                           int32_t* par) {
+                           const int32_t* __restrict__ fmap, int32_t* parK) {
   pdl_enter();
   const int w = (int)dw.d;
   const int n = *flat_count;
@@ -165,25 +183,40 @@ __global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         same |= 1u << t;
       }
     }
-    unite_backward(par, w, i, same);
+    // unite_backward's skips, on compact slots (fmap: pixel -> slot)
+    const bool ul = same & 1u, u = same & 2u, ur = same & 4u, l = same & 8u;
+    if (l) {
+      ukey_unite(parK, flat_list, k, __ldg(fmap + i - 1));
+      if (ur && !u) ukey_unite(parK, flat_list, k, __ldg(fmap + i - w + 1));
+    } else if (u) {
+      ukey_unite(parK, flat_list, k, __ldg(fmap + i - w));
+    } else {
+      if (ul) ukey_unite(parK, flat_list, k, __ldg(fmap + i - w - 1));
+      if (ur) ukey_unite(parK, flat_list, k, __ldg(fmap + i - w + 1));
+    }
     if (seed >= 0) dir[i] = dir_code(seed);
   }
 }
 
-// Flattens every flat pixel onto its root, flags seeded roots and hands each
-// pixel a slot in its component (slot stored in the delta plane).
-__global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
-                           const int32_t* __restrict__ flat_count,
-                           const uint8_t* __restrict__ dir, int32_t* par, int32_t* cnt,
-                           int32_t* __restrict__ slot) {
+// Compact plateau roots: flatten, seeded flags, a slot per member.  The find
+// is read-only: slots are not key-ordered, so a halving store (unlike the
+// pixel forests' atomicMin) could overwrite an already flattened parent with
+// a stale ancestor.
+__global__ void k_ws_roots_c(const int32_t* __restrict__ flat_list,
+                             const int32_t* __restrict__ flat_count,
+                             const uint8_t* __restrict__ dir, int32_t* parK, int32_t* cntK,
+                             int32_t* __restrict__ slot) {
   pdl_enter();
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = flat_list[k];
-    const int32_t r = uf_find_g(par, i);
-    if (r != i) atomicMin(par + i, r);
-    if (dir && dir[i] != kDirNone) atomicOr(cnt + r, kSeeded);
-    slot[i] = atomicAdd(cnt + r, 1) & kCountMask;
+    int32_t r = k, p = __ldcg(parK + k);
+    while (p != r) {
+      r = p;
+      p = __ldcg(parK + p);
+    }
+    if (r != k) parK[k] = r;
+    if (dir[flat_list[k]] != kDirNone) atomicOr(cntK + r, kSeeded);
+    slot[k] = atomicAdd(cntK + r, 1) & kCountMask;
   }
 }
 
@@ -192,8 +225,8 @@ __global__ void k_ws_roots(const int32_t* __restrict__ flat_list,
 // component list.  alloc = {member cursor, component count} as one u64.
 __global__ void __launch_bounds__(256)
 k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__ flat_count,
-              const int32_t* __restrict__ par, int32_t* cnt, uint8_t* __restrict__ dir,
-              unsigned long long* alloc) {
+              const int32_t* __restrict__ parK, int32_t* cntK, uint8_t* __restrict__ dir,
+              int32_t* __restrict__ parP, unsigned long long* alloc) {
   pdl_enter();
   __shared__ unsigned long long sm[9];
   const int n = *flat_count;
@@ -202,47 +235,49 @@ k_ws_classify(const int32_t* __restrict__ flat_list, const int32_t* __restrict__
     int32_t root = -1, sz = 0;
     if (k < n) {
       const int32_t i = flat_list[k];
-      const int32_t r = __ldcg(par + i);
-      const int32_t v = __ldcg(cnt + r);
+      const int32_t r = __ldcg(parK + k);
+      const int32_t v = __ldcg(cntK + r);
       if (!(v & kSeeded)) {
+        // a marker: its label is its root's pixel (the minimum), read by
+        // k_ws_basins at the marker pixels
         dir[i] = kDirSelf;
-      } else if (r == i) {
-        root = i;
+        parP[i] = __ldg(flat_list + r);
+      } else if (r == k) {
+        root = k;
         sz = v & kCountMask;
       }
     }
     const unsigned long long slot = block_reserve2(root >= 0 ? 1u : 0u, (uint32_t)sz, alloc, sm);
     if (root >= 0) {
       const int32_t base = (int32_t)(slot & 0xFFFFFFFFull);
-      __stcg(cnt + root, kSeeded | base);  // members still read the flag: it stays set
+      __stcg(cntK + root, kSeeded | base);  // members still read the flag: it stays set
     }
   }
 }
 
-__global__ void k_ws_scatter(const int32_t* __restrict__ flat_list,
-                             const int32_t* __restrict__ flat_count,
-                             const int32_t* __restrict__ par, const int32_t* __restrict__ cnt,
-                             const int32_t* __restrict__ slot, int32_t* __restrict__ members) {
+// Members of the seeded components, back to back by component (compact).
+__global__ void k_ws_scatter_c(const int32_t* __restrict__ flat_list,
+                               const int32_t* __restrict__ flat_count,
+                               const int32_t* __restrict__ parK, const int32_t* __restrict__ cntK,
+                               const int32_t* __restrict__ slot, int32_t* __restrict__ members) {
   pdl_enter();
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int32_t i = flat_list[k];
-    const int32_t v = cnt[par[i]];
+    const int32_t v = cntK[parK[k]];
     if (v & kSeeded) {
-      const int32_t sl = slot[i];
+      const int32_t sl = slot[k], i = flat_list[k];
       members[(v & kCountMask) + sl] = sl == 0 ? ~i : i;  // ~: first member of a component
     }
   }
 }
 
-// Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8).
-// Only flat neighbours carry a plateau parent (k_ws_arrows leaves par of
-// non-flat pixels unwritten), so the flat byte gates the parent compare.
+// Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8): the
+// flat neighbours at p's level.  That is exactly its plateau component's
+// neighbours, since k_ws_union unites every such pair.
 __device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
                                                  const uint16_t* __restrict__ Fw,
-                                                 const uint8_t* __restrict__ flat,
-                                                 const int32_t* __restrict__ par, int32_t p,
-                                                 uint16_t f, int32_t r) {
+                                                 const uint8_t* __restrict__ flat, int32_t p,
+                                                 uint16_t f) {
   const int w = (int)dw.d;
   const int y = fdiv(p, dw), x = p - y * w;
   const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
@@ -253,14 +288,7 @@ __device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint32
 #pragma unroll
   for (int t = 0; t < 8; ++t)
     if (((fm >> t) & 1u) && fl[t] && fv[t] == f) cand |= 1u << t;
-  int32_t pv[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) pv[t] = ((cand >> t) & 1u) ? __ldcg(par + nbr_index(w, p, t)) : -1;
-  uint32_t m = 0;
-#pragma unroll
-  for (int t = 0; t < 8; ++t)
-    if (((cand >> t) & 1u) && pv[t] == r) m |= 1u << t;
-  return m;
+  return cand;
 }
 
 // Components are laid out back to back in `members` (component order), each
@@ -298,7 +326,6 @@ __device__ __forceinline__ int32_t member_px(int32_t m) { return m < 0 ? ~m : m;
 __global__ void __launch_bounds__(256)
 k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
              const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
-             const int32_t* __restrict__ par,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch,
              uint8_t* slotmap) {
@@ -329,7 +356,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         if (k < e) {
           px[q] = member_px(members[k]);
           d[q] = dir[px[q]] != kDirNone ? 1 : kInfD;
-          nb[q] = plateau_nbrs(h, dw, mask, Fw, flat, par, px[q], Fw[px[q]], par[px[q]]);
+          nb[q] = plateau_nbrs(h, dw, mask, Fw, flat, px[q], Fw[px[q]]);
           sv[lane + 32 * q] = d[q];
           slotmap[px[q]] = (uint8_t)(lane + 32 * q);
         }
@@ -375,7 +402,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
       for (int k = s0 + lane; k < e; k += 32) {
         const int32_t p = member_px(members[k]);
         vd[p] = dir[p] != kDirNone ? 1 : kInfD;
-        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, flat, par, p, Fw[p], par[p]));
+        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, flat, p, Fw[p]));
       }
       __syncwarp();
       while (true) {
@@ -490,7 +517,7 @@ __global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mas
 }
 
 // Roots / slots / member placement of the compact suspect forest (the HMAX
-// counterparts of k_ws_roots / k_ws_scatter, indexed by suspect slot).
+// counterparts of k_ws_roots_c / k_ws_scatter_c, indexed by suspect slot).
 __global__ void k_hmax_roots(const int32_t* __restrict__ count, int32_t* par, int32_t* cnt,
                              int32_t* __restrict__ slot) {
   pdl_enter();
@@ -515,7 +542,7 @@ __global__ void k_hmax_scatter(const int32_t* __restrict__ list, const int32_t* 
 }
 
 // Every component root reserves its members' range (cnt[r] := kSeeded | base,
-// the form k_ws_scatter reads) and enters the component list.
+// the form k_ws_scatter_c reads) and enters the component list.
 __global__ void __launch_bounds__(256)
 k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
              const int32_t* __restrict__ par, int32_t* cnt, unsigned long long* alloc) {
@@ -852,23 +879,31 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   int32_t* par = ctx->i32c;
   uint8_t* flat = ctx->m1;
   int32_t* flat_count = ctx->misc + 5;
+  // compact plateau machinery: forest / counters in the arena's first half
+  // (the HMAX ones there are dead), pixel -> slot map in the par plane, which
+  // k_ws_classify then overwrites with each marker pixel's label for
+  // k_ws_basins
+  int32_t* parK = reinterpret_cast<int32_t*>(ctx->arena);
+  int32_t* cntK = parK + n;
   RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
-                    (const uint8_t*)nbm, Fw, dir, par, basin,
-                                          flat, ctx->flat_list, flat_count));
+                    (const uint8_t*)nbm, Fw, dir, par, parK, cntK, flat, ctx->flat_list,
+                    flat_count));
   RTG_LAUNCH("k_ws_arrows");
   RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
-                                         flat_count, dir, par));
+                    flat_count, dir, (const int32_t*)par, parK));
   RTG_LAUNCH("k_ws_union");
-  RTG_CUDA(launch_k(ctx, k_ws_roots, g, 256, 0, ctx->flat_list, flat_count, dir, par, basin, delta));
-  RTG_LAUNCH("k_ws_roots");
-  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, ctx->flat_list, flat_count, par, basin, dir,
-                    walloc));
+  RTG_CUDA(launch_k(ctx, k_ws_roots_c, g, 256, 0, (const int32_t*)ctx->flat_list, flat_count,
+                    (const uint8_t*)dir, parK, cntK, delta));
+  RTG_LAUNCH("k_ws_roots_c");
+  RTG_CUDA(launch_k(ctx, k_ws_classify, g, 256, 0, (const int32_t*)ctx->flat_list, flat_count,
+                    (const int32_t*)parK, cntK, dir, par, walloc));
   RTG_LAUNCH("k_ws_classify");
-  RTG_CUDA(launch_k(ctx, k_ws_scatter, g, 256, 0, ctx->flat_list, flat_count, par, basin, delta,
-                                           ctx->lroots));
-  RTG_LAUNCH("k_ws_scatter");
-  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, par, ctx->lroots, walloc, dir,
-                                           delta, member_scratch, ctx->m2 /* slot map */));
+  RTG_CUDA(launch_k(ctx, k_ws_scatter_c, g, 256, 0, (const int32_t*)ctx->flat_list, flat_count,
+                    (const int32_t*)parK, (const int32_t*)cntK, (const int32_t*)delta,
+                    ctx->lroots));
+  RTG_LAUNCH("k_ws_scatter_c");
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->lroots,
+                    walloc, dir, delta, member_scratch, ctx->m2 /* slot map */));
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
