@@ -9,7 +9,7 @@ h = rows[hi]
 ki, vi, ii = h.index('Kernel Name'), h.index('Metric Value'), h.index('ID')
 per = []
 for r in rows[hi + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or ('Metric Name' in h and r[h.index('Metric Name')] != 'gpu__time_duration.sum'):
         continue
     k = r[ki]
     m = re.search(r'(k_[a-z0-9_]+)', k)
