@@ -51,11 +51,11 @@ __device__ __forceinline__ int32_t nbr_index(int w, int32_t p, int t) {
 
 // Watershed arrows are stored as one byte per pixel: the code of the
 // 8-neighbour it points to, (dy + 1) * 4 + (dx + 1), so a chain step is
-// q + (c >> 2) * w + (c & 3) - (w + 1) (four instructions); kDirSelf (the
-// zero offset) = a marker pixel (root), kDirNone = no arrow yet.  A byte
+// q + ((c >> 2) & 3) * w + (c & 3) - (w + 1); kDirSelf (the zero offset) = a
+// marker pixel (root), kDirNone = no arrow yet.  A byte
 // plane keeps the basin chains' gathers 4x denser than i32 indices.
 constexpr uint8_t kDirSelf = 5;
-constexpr uint8_t kDirNone = 0xFF;
+constexpr uint8_t kDirNone = 0xF5;  // decodes, masked, to the zero offset too
 
 __device__ __forceinline__ uint8_t dir_code(int t) {  // row-major neighbour t of 8
   return (uint8_t)((0xA9864210u >> (4 * t)) & 0xFu);
@@ -717,10 +717,13 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
     }
 #pragma unroll
     for (int j = 0; j < kC; ++j) {
-      q[j] = p[j];
-      d[j] = p[j] >= 0 ? dir[p[j]] : kDirNone;
+      q[j] = p[j] >= 0 ? p[j] : p[0];  // a spare slot walks a real chain
+      d[j] = dir[q[j]];
     }
-    // a neighbour code: step; kDirSelf: marker reached; kDirNone: no arrow
+    // Codes decode with (c >> 2) & 3, under which kDirSelf and kDirNone are
+    // both the zero offset: a finished chain stays put, so the chains take
+    // kSteps steps between convergence tests with no per-step predicate.
+    constexpr int kSteps = 4;
     const int32_t wm = w + 1;
     auto moving = [](uint32_t c) { return c != kDirSelf && c != kDirNone; };
     while (true) {
@@ -729,9 +732,10 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
       for (int j = 0; j < kC; ++j) any |= moving(d[j]);
       if (!any) break;
 #pragma unroll
-      for (int j = 0; j < kC; ++j) {
-        if (moving(d[j])) {
-          q[j] += (int32_t)(d[j] >> 2) * w + (int32_t)(d[j] & 3u) - wm;
+      for (int s = 0; s < kSteps; ++s) {
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+          q[j] += (int32_t)((d[j] >> 2) & 3u) * w + (int32_t)(d[j] & 3u) - wm;
           d[j] = dir[q[j]];
         }
       }
