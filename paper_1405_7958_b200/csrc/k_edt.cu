@@ -25,6 +25,7 @@
 // The row pass also emits dq = floor(4*sqrt(d2)) and the HMAX marker.
 //
 // Roofline: HBM/L2 bound; algorithmic bytes mask 1 B in + dq/marker 4 B out.
+#include <type_traits>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -502,27 +503,35 @@ k_edt_list(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
     // rows past the stopping point only add candidates >= dy^2 >= best, so
     // the result is the same as the row-by-row scan
     constexpr uint32_t kB = 4;
-    for (uint32_t dy0 = 1; dy0 <= kR && dy0 * dy0 < best; dy0 += kB) {
-      uint32_t mu[kB], hu[kB], md[kB], hdn[kB];
+    // a row without background within range has hd = 255: its candidate is
+    // >= 255^2 > kR^2, which ends in the need_full branch exactly as a
+    // skipped row would, so no test is needed; pixels >= kR rows from both
+    // image edges (nearly all) skip the bounds tests too
+    auto scan = [&](auto checked) {
+      for (uint32_t dy0 = 1; dy0 <= kR && dy0 * dy0 < best; dy0 += kB) {
+        uint32_t mu[kB], hu[kB], md[kB], hdn[kB];
 #pragma unroll
-      for (uint32_t j = 0; j < kB; ++j) {
-        const uint32_t dy = dy0 + j;
-        const bool vu = y >= (int)dy, vd = y + (int)dy < h;
-        const int32_t qu = p - (int32_t)dy * w, qd = p + (int32_t)dy * w;
-        // kBgZero: the hd plane holds 0 at background pixels (the joint
-        // fill/area stage wrote the mask bytes there), no bit tests
-        mu[j] = kBgZero ? 1u : vu ? (bits[qu >> 5] >> (qu & 31)) & 1u : 1u;
-        hu[j] = vu ? hd[qu] : 255u;
-        md[j] = kBgZero ? 1u : vd ? (bits[qd >> 5] >> (qd & 31)) & 1u : 1u;
-        hdn[j] = vd ? hd[qd] : 255u;
-      }
+        for (uint32_t j = 0; j < kB; ++j) {
+          const uint32_t dy = dy0 + j;
+          const bool vu = !checked.value || y >= (int)dy, vd = !checked.value || y + (int)dy < h;
+          const int32_t qu = p - (int32_t)dy * w, qd = p + (int32_t)dy * w;
+          // kBgZero: the hd plane holds 0 at background pixels (the joint
+          // fill/area stage wrote the mask bytes there), no bit tests
+          mu[j] = kBgZero ? 1u : vu ? (bits[qu >> 5] >> (qu & 31)) & 1u : 1u;
+          hu[j] = vu ? hd[qu] : 255u;
+          md[j] = kBgZero ? 1u : vd ? (bits[qd >> 5] >> (qd & 31)) & 1u : 1u;
+          hdn[j] = vd ? hd[qd] : 255u;
+        }
 #pragma unroll
-      for (uint32_t j = 0; j < kB; ++j) {
-        const uint32_t dy = dy0 + j;
-        const uint32_t dm = min(mu[j] ? hu[j] : 0u, md[j] ? hdn[j] : 0u);
-        if (dm != 255u) best = min(best, dy * dy + dm * dm);
+        for (uint32_t j = 0; j < kB; ++j) {
+          const uint32_t dy = dy0 + j;
+          const uint32_t dm = min(mu[j] ? hu[j] : 0u, md[j] ? hdn[j] : 0u);
+          best = min(best, dy * dy + dm * dm);
+        }
       }
-    }
+    };
+    if (y >= (int)kR && y + (int)kR < h) scan(std::false_type{});
+    else scan(std::true_type{});
     if (best > kR * kR) {
       far = true;
       continue;
