@@ -382,6 +382,28 @@ __device__ __forceinline__ int32_t block_reserve(int32_t cnt, int32_t* counter, 
   return r;
 }
 
+// block_reserve for one slot per flagged thread (a ballot instead of the
+// shuffle scan).
+__device__ __forceinline__ int32_t block_reserve_flag(bool f, int32_t* counter, int32_t* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t b = __ballot_sync(0xFFFFFFFFu, f);
+  if (lane == 0) sm[wid] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t tot = 0;
+    for (int k = 0; k < nw; ++k) {
+      const int32_t t = sm[k];
+      sm[k] = tot;
+      tot += t;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0;
+  }
+  __syncthreads();
+  const int32_t r = sm[nw] + sm[wid] + __popc(b & ((1u << lane) - 1u));
+  __syncthreads();
+  return r;
+}
+
 // Same for (a, b) pairs packed in one u64 counter (hi: a, lo: b); the block's
 // sums must stay below 2^32.  Returns the packed first slots.
 __device__ __forceinline__ unsigned long long block_reserve2(uint32_t a, uint32_t b,

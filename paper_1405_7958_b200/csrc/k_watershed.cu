@@ -100,16 +100,17 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
     int32_t p = 0;
     if (k < n) {
       p = list[k];
-      const uint32_t f = Fw[p];
-      uint32_t best = f;
-      int arg = -1;
       uint32_t fv[8];
       gather8(Fw, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0u, fv);
+      // steepest ascent as one max over keys value << 3 | (7 - t): the first
+      // (row-major) maximum wins ties, and p's own key (f << 3 | 7) beats
+      // every neighbour at its level or below
+      const uint32_t self = (uint32_t)Fw[p] << 3 | 7u;
+      uint32_t best = self;
 #pragma unroll
-      for (int t = 0; t < 8; ++t)  // row-major: first max = min index
-        if (fv[t] > best) { best = fv[t]; arg = t; }
-      if (arg >= 0) {
-        dir[p] = dir_code(arg);
+      for (int t = 0; t < 8; ++t) best = max(best, fv[t] << 3 | (7u - t));
+      if (best != self) {
+        dir[p] = dir_code(7 - (int)(best & 7u));
         flat[p] = 0;
       } else {
         dir[p] = kDirNone;
@@ -117,7 +118,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
         is_flat = true;
       }
     }
-    const int32_t slot = block_reserve(is_flat ? 1 : 0, flat_count, sm);
+    const int32_t slot = block_reserve_flag(is_flat, flat_count, sm);
     if (is_flat) {
       // the plateau machinery runs on compact flat-pixel slots
       flat_list[slot] = p;
@@ -477,7 +478,7 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
         sflag[p] = 1;
       }
     }
-    const int32_t slot = block_reserve(sus ? 1 : 0, scount, sm);
+    const int32_t slot = block_reserve_flag(sus, scount, sm);
     if (sus) {
       // the component machinery runs on compact suspect indices (slot k):
       // its forest and counters stay a few hundred KB, L2-resident
