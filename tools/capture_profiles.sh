@@ -25,6 +25,11 @@ timeout 300 python tools/prof_tile.py --tiles 1 --passes 1 > $O/prof_tile1.log 2
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed.sum,lts__t_bytes.sum,lts__t_sectors_op_red.sum,lts__t_sectors_op_atom.sum \
     --clock-control none --csv --log-file $O/stage_launches.csv \
     python tools/prof_tile.py --tiles 1 --passes 1 > $O/ncu_stage.log 2>&1
+# the same counters without ncu's cache flush (second of two tiles: the L2
+# keeps producers' outputs for their consumers as in the pipeline)
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed.sum,lts__t_bytes.sum,lts__t_sectors_op_red.sum,lts__t_sectors_op_atom.sum \
+    --clock-control none --cache-control none --csv --log-file $O/stage_launches_warm_l2.csv \
+    python tools/prof_tile.py --tiles 2 --passes 1 > $O/ncu_stage_warm.log 2>&1
 # full captures: the streaming kernel and the dominant stage's kernels
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k "regex:k_colordeconv_tma|k_ws_arrows|k_ws_basins|k_ws_separate|k_ws_union|k_ws_plateau" -c 6 \
