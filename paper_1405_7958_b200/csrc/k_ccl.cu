@@ -341,13 +341,14 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   //    accumulate pixel counts / seed bits at the local roots
   const int nruns = __popc(starts);
   flatten_jump(par, rb, nruns);
-  int nroot = 0;
+  uint32_t rootm = 0;  // this row's local roots, by run index
   for (int k = 0; k < nruns; ++k) {
     if (par[rb + k] == rb + k) {
       inf[rb + k] = 0;
-      ++nroot;
+      rootm |= 1u << k;
     }
   }
+  const int nroot = __popc(rootm);
   __syncwarp();
   {
     int k = 0;
@@ -365,8 +366,8 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
   int base = block_reserve(active ? nroot : 0, lcount, s_res);
   if (!active) return;
   const int32_t tbase = __shfl_sync(kFull, base, 0);  // the tile's roots are contiguous
-  for (int k = 0; k < nruns; ++k) {
-    if (par[rb + k] != rb + k) continue;
+  for (uint32_t m = rootm; m; m &= m - 1) {
+    const int k = __ffs(m) - 1;
     const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
     lroots[2 * base] = g;
     lroots[2 * base + 1] = (int32_t)inf[rb + k];
@@ -1176,12 +1177,13 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   // ancestor): the all-at-once unions leave chains up to 31 rows deep, which
   // per-run finds walk link by link; jumping halves every chain per round
   flatten_jump16(par, rb, nruns);
-  int nroot = 0;
+  uint32_t rootm = 0;  // this row's local roots, by run index
   for (int k = 0; k < nruns; ++k)
     if (par[rb + k] == rb + k) {
       acc16[rb + k] = 0;
-      ++nroot;
+      rootm |= 1u << k;
     }
+  const int nroot = __popc(rootm);
   __syncwarp();
   {
     int k = 0;
@@ -1199,8 +1201,8 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
   int base = block_reserve(active ? nroot : 0, lcount, s_res);
   if (!active) return;
   const int32_t tbase = __shfl_sync(kFull, base, 0);  // the tile's roots are contiguous
-  for (int k = 0; k < nruns; ++k) {
-    if (par[rb + k] != rb + k) continue;
+  for (uint32_t m = rootm; m; m &= m - 1) {
+    const int k = __ffs(m) - 1;
     const int32_t g = (y0 + lane) * w + x0 + pos[rb + k];
     const uint32_t a = acc16[rb + k];
     lroots[2 * base] = g;
