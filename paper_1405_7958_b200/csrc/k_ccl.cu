@@ -1239,7 +1239,17 @@ k_ccl_tile_fb(const uint8_t* __restrict__ m, int h, int w, int tiles_x, int ntil
       bd[96 + lane] = glob(par[rb + nruns - 1], fgb >> 31);
     }
     __syncwarp();
-    for (int k = 0; k < nruns; ++k) par[rb + k] = acc16[par[rb + k]];  // own entries only
+    // own entries only, four at a time with their loads in flight together
+    for (int k0 = 0; k0 < nruns; k0 += 4) {
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = k0 + j < nruns ? par[rb + k0 + j] : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = acc16[v[j]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (k0 + j < nruns) par[rb + k0 + j] = (uint16_t)v[j];
+    }
     __syncwarp();
     const uint4* src = reinterpret_cast<const uint4*>(par);
     uint4* dst = reinterpret_cast<uint4*>(rtab + (int64_t)tile * 1024);

@@ -779,10 +779,18 @@ __global__ void k_ws_separate(int h, FastDiv dw, const int32_t* __restrict__ lis
       if (!sep_bits) sep[p] = keep;
     }
     if (sep_bits) {
+      // the list holds each bit word's pixels back to back (fg_list appends a
+      // word's set bits together), so the lanes sharing a word are a run of
+      // lanes: its bounds come from a ballot of run heads (no match_any)
       const int32_t wi = p >= 0 ? (p >> 5) : -1;
-      const unsigned grp = __match_any_sync(0xFFFFFFFFu, wi);
+      const int32_t wprev = __shfl_up_sync(0xFFFFFFFFu, wi, 1);
+      const uint32_t heads = __ballot_sync(0xFFFFFFFFu, lane == 0 || wprev != wi);
+      const uint32_t upto = lane == 31 ? 0xFFFFFFFFu : (2u << lane) - 1u;
+      const int first = 31 - __clz(heads & upto);
+      const uint32_t after = heads & ~upto;
+      const uint32_t grp = (after ? (after & (0u - after)) - 1u : 0xFFFFFFFFu) & ~((1u << first) - 1u);
       const uint32_t v = __reduce_or_sync(grp, keep ? 1u << (p & 31) : 0u);
-      if (wi >= 0 && v && lane == __ffs(grp) - 1) atomicOr(sep_bits + wi, v);
+      if (wi >= 0 && v && lane == first) atomicOr(sep_bits + wi, v);
     }
   }
 }
