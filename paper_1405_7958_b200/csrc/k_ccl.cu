@@ -829,8 +829,10 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ lroots, const int32_t* __re
   s_bits[wid][lane] = bits;
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < 16; ++k)
-    if (k < nruns) s_lab[wid][lane * 16 + k] = s_rank[wid][(ew[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
+  for (int k = 0; k < 16; ++k) {  // the warp stops at its longest row's run count
+    if (k >= nruns) break;
+    s_lab[wid][lane * 16 + k] = s_rank[wid][(ew[k >> 1] >> (16 * (k & 1))) & 0xFFFFu];
+  }
   __syncwarp();
   const int g = lane >> 3, cq = (lane & 7) * 4;
 #pragma unroll 2
