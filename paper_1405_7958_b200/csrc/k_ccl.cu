@@ -385,12 +385,11 @@ k_ccl_tile(P pred, int h, int w, int tiles_x, int ntiles, int32_t* __restrict__ 
     if (lane == 0) rt.tinfo[tile] = make_int2(tbase, tend - tbase);
     rt.rowbits[tile * 32 + lane] = bits;
     // this row's 16 table entries (two 16-byte stores; the warp's are contiguous)
-    uint32_t pk[8];
+    uint32_t pk[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t o = k < nruns ? inf[par[rb + k]] : 0u;
-      if (k & 1) pk[k >> 1] |= o << 16;
-      else pk[k >> 1] = o;
+    for (int k = 0; k < 16; ++k) {  // the warp stops at its longest row's run count
+      if (k >= nruns) break;
+      pk[k >> 1] |= inf[par[rb + k]] << (16 * (k & 1));
     }
     uint4* dst = reinterpret_cast<uint4*>(rt.rtab + (int64_t)tile * 512 + rb);
     dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
