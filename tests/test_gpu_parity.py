@@ -313,6 +313,21 @@ def test_watershed(rtg, ctx, oracle, ws_h, impl, hmax):
     assert np.array_equal(_dev_np(sep), sep_ref)
 
 
+@pytest.mark.parametrize("ws_h", [1, 5])
+def test_watershed_4k(rtg, ctx, oracle, ws_h):
+    """The default watershed (sparse-component HMAX, compact plateau forests,
+    masked-code basin chains) on a full 4096^2 tile of touching blobs."""
+    rng = np.random.default_rng(ws_h + 4096)
+    h = w = 4096
+    m = _rand_blobs(rng, h, w, 0.4, 3.0)
+    sep_ref, basin_ref = oracle.watershed(m, ws_h)
+    sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
+    ctx.watershed_dev(_np_dev(m), h, w, ws_h, sep, basin)
+    assert np.array_equal(_dev_np(basin), basin_ref)
+    assert np.array_equal(_dev_np(sep), sep_ref)
+
+
 @pytest.mark.parametrize("case", ["big_blob", "thin_diagonal", "border_touching", "all_fg"])
 def test_watershed_objects_size_classes(rtg, ctx, oracle, case):
     """Object-parallel watershed on objects beyond the 12 KB per-warp class:
