@@ -262,6 +262,15 @@ enum rtg_option {
 };
 int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value);
 
+/* Debug check of the context's scratch (no reference counterpart: test
+ * infrastructure standing in for compute-sanitizer, which this GPU pool does
+ * not run).  With RTG_GUARD_BYTES=N in the environment at rtg_ctx_create,
+ * every scratch buffer is allocated N bytes larger and the tail filled with
+ * a canary; this call synchronises the context's stream and fails with
+ * RTG_ERR_INTERNAL (naming the buffer) if any canary byte changed.
+ * *n_checked = the number of guarded buffers (0 without RTG_GUARD_BYTES). */
+int rtg_ctx_guard_check(rtg_ctx* ctx, int32_t* n_checked);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* rtg_last_error(void);
 

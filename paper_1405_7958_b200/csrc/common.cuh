@@ -105,6 +105,14 @@ constexpr int kAsyncSlots = 3;
 
 // The context: every device allocation of the stage lives here (arena).
 struct rtg_ctx {
+  // debug guard bands (RTG_GUARD_BYTES at creation): every scratch buffer is
+  // followed by this many canary bytes that rtg_ctx_guard_check verifies
+  struct Guard {
+    unsigned char* end;
+    const char* name;
+  };
+  std::vector<Guard> guards;
+  size_t guard_bytes = 0;
   int device = 0;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr;

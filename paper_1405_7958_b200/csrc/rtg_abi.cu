@@ -82,11 +82,20 @@ int check_params_impl(const rtg_params* p) {
   return RTG_OK;
 }
 
+constexpr unsigned char kGuardByte = 0xA5;
+
 template <typename T>
-int dalloc(T** p, size_t count) {
-  RTG_CUDA(cudaMalloc((void**)p, sizeof(T) * (count ? count : 1)));
+int dalloc(rtg_ctx* c, T** p, size_t count, const char* name) {
+  const size_t bytes = sizeof(T) * (count ? count : 1);
+  RTG_CUDA(cudaMalloc((void**)p, bytes + c->guard_bytes));
+  if (c->guard_bytes) {
+    unsigned char* end = reinterpret_cast<unsigned char*>(*p) + bytes;
+    RTG_CUDA(cudaMemset(end, kGuardByte, c->guard_bytes));
+    c->guards.push_back({end, name});
+  }
   return RTG_OK;
 }
+#define DALLOC(field, count) dalloc(c, &c->field, (count), #field)
 
 template <typename T>
 __global__ void k_clip_copy(const T* __restrict__ marker, const T* __restrict__ mask,
@@ -442,6 +451,10 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
   c->max_w = max_w;
   c->max_px = max_h * max_w;
   c->max_objects = max_objects;
+  if (const char* g = getenv("RTG_GUARD_BYTES")) {
+    const long long v = atoll(g);
+    c->guard_bytes = v > 0 ? (size_t)v : 0;
+  }
   auto cleanup = [&](int st) {
     rtg_ctx_destroy(c);
     return st;
@@ -451,56 +464,60 @@ int rtg_ctx_create(int device, int64_t max_h, int64_t max_w, int32_t max_objects
         RTG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
         const size_t n = (size_t)c->max_px;
-        RTG_TRY(dalloc(&c->rgb, 3 * n));
-        RTG_TRY(dalloc(&c->hema, n));
-        RTG_TRY(dalloc(&c->recon, n));
-        RTG_TRY(dalloc(&c->tissue, n));
-        RTG_TRY(dalloc(&c->m1, n));
-        RTG_TRY(dalloc(&c->m2, n));
-        RTG_TRY(dalloc(&c->m3, n));
-        RTG_TRY(dalloc(&c->m4, n));
-        RTG_TRY(dalloc(&c->rm, n));
-        RTG_TRY(dalloc(&c->u16a, n));
-        RTG_TRY(dalloc(&c->u16b, n));
-        RTG_TRY(dalloc(&c->u16c, n));
-        RTG_TRY(dalloc(&c->i32a, n));
-        RTG_TRY(dalloc(&c->i32b, n));
-        RTG_TRY(dalloc(&c->i32c, n));
-        RTG_TRY(dalloc(&c->labels, n));
-        RTG_TRY(dalloc(&c->features, (size_t)max_objects * RTG_MAX_FEATURE_COLUMNS));
-        RTG_TRY(dalloc(&c->feat20, (size_t)max_objects * RTG_NUM_FEATURES));
-        RTG_TRY(dalloc(&c->tex14, (size_t)max_objects * RTG_NUM_TEXTURE));
-        RTG_TRY(dalloc(&c->seg_summary, (size_t)ceil_div(max_h, 32) * (size_t)max_w));
-        RTG_TRY(dalloc(&c->scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
-        RTG_TRY(dalloc(&c->flat_list, n));
-        RTG_TRY(dalloc(&c->lroots, n));
-        RTG_TRY(dalloc(&c->root_bm, n / 32 + 1));
-        RTG_TRY(dalloc(&c->root_wprefix, n / 32 + 1));
-        RTG_TRY(dalloc(&c->fg_list, n));
-        RTG_TRY(dalloc(&c->fg_bits, n / 32 + 8));
-        RTG_TRY(dalloc(&c->sep_bits, n / 32 + 8));
+        RTG_TRY(DALLOC(rgb, 3 * n));
+        RTG_TRY(DALLOC(hema, n));
+        RTG_TRY(DALLOC(recon, n));
+        RTG_TRY(DALLOC(tissue, n));
+        RTG_TRY(DALLOC(m1, n));
+        RTG_TRY(DALLOC(m2, n));
+        RTG_TRY(DALLOC(m3, n));
+        RTG_TRY(DALLOC(m4, n));
+        RTG_TRY(DALLOC(rm, n));
+        RTG_TRY(DALLOC(u16a, n));
+        RTG_TRY(DALLOC(u16b, n));
+        RTG_TRY(DALLOC(u16c, n));
+        RTG_TRY(DALLOC(i32a, n));
+        RTG_TRY(DALLOC(i32b, n));
+        RTG_TRY(DALLOC(i32c, n));
+        RTG_TRY(DALLOC(labels, n));
+        RTG_TRY(DALLOC(features, (size_t)max_objects * RTG_MAX_FEATURE_COLUMNS));
+        RTG_TRY(DALLOC(feat20, (size_t)max_objects * RTG_NUM_FEATURES));
+        RTG_TRY(DALLOC(tex14, (size_t)max_objects * RTG_NUM_TEXTURE));
+        RTG_TRY(DALLOC(seg_summary, (size_t)ceil_div(max_h, 32) * (size_t)max_w));
+        RTG_TRY(DALLOC(scan_buf, 2 * (size_t)ceil_div(c->max_px, kScanChunk) + 2));
+        RTG_TRY(DALLOC(flat_list, n));
+        RTG_TRY(DALLOC(lroots, n));
+        RTG_TRY(DALLOC(root_bm, n / 32 + 1));
+        RTG_TRY(DALLOC(root_wprefix, n / 32 + 1));
+        RTG_TRY(DALLOC(fg_list, n));
+        RTG_TRY(DALLOC(fg_bits, n / 32 + 8));
+        RTG_TRY(DALLOC(sep_bits, n / 32 + 8));
         c->obj_cap = (int64_t)n / 4 + 16;  // 8-connected objects are >= 1 px, <= 1 per 2x2
-        RTG_TRY(dalloc(&c->obj_root, (size_t)c->obj_cap));
-        RTG_TRY(dalloc(&c->obj_box, 4 * (size_t)c->obj_cap));
-        RTG_TRY(dalloc(&c->obj_list, (size_t)c->obj_cap));
-        RTG_TRY(dalloc(&c->arena, 16 * n + 64));
-        RTG_TRY(dalloc(&c->misc, 128 + (size_t)max_h));
-        RTG_TRY(dalloc(&c->status, 1));
-        RTG_TRY(dalloc(&c->stats, RTG_NUM_STATS));
-        RTG_TRY(dalloc(&c->level_bits, 16));
+        RTG_TRY(DALLOC(obj_root, (size_t)c->obj_cap));
+        RTG_TRY(DALLOC(obj_box, 4 * (size_t)c->obj_cap));
+        RTG_TRY(DALLOC(obj_list, (size_t)c->obj_cap));
+        RTG_TRY(DALLOC(arena, 16 * n + 64));
+        RTG_TRY(DALLOC(misc, 128 + (size_t)max_h));
+        RTG_TRY(DALLOC(status, 1));
+        RTG_TRY(DALLOC(stats, RTG_NUM_STATS));
+        RTG_TRY(DALLOC(level_bits, 16));
         const int64_t ntiles = ceil_div(max_h, kTile) * ceil_div(max_w, kTile);
         c->tq.capacity = (int32_t)(2 * ntiles);
-        RTG_TRY(dalloc(&c->tq.state, (size_t)ntiles));
-        RTG_TRY(dalloc(&c->tq.slots, (size_t)(2 * ntiles)));
-        RTG_TRY(dalloc(&c->tq.counters, 8));
+        RTG_TRY(DALLOC(tq.state, (size_t)ntiles));
+        RTG_TRY(DALLOC(tq.slots, (size_t)(2 * ntiles)));
+        RTG_TRY(DALLOC(tq.counters, 8));
         c->acc.cap = max_objects;
-        RTG_TRY(dalloc(&c->acc.sums, (size_t)kSumFields * max_objects));
-        RTG_TRY(dalloc(&c->acc.mins, (size_t)kMinFields * max_objects));
-        RTG_TRY(dalloc(&c->acc.maxs, (size_t)kMaxFields * max_objects));
-        RTG_TRY(dalloc(&c->tex_bbox, 4 * (size_t)max_objects));
-        RTG_TRY(dalloc(&c->tex_hist, 17 * (size_t)max_objects));
-        RTG_TRY(dalloc(&c->tex_glcm, 64 * (size_t)max_objects));
-        RTG_TRY(dalloc(&c->tex_mom, 4 * (size_t)max_objects));
+        RTG_TRY(DALLOC(acc.sums, (size_t)kSumFields * max_objects));
+        RTG_TRY(DALLOC(acc.mins, (size_t)kMinFields * max_objects));
+        RTG_TRY(DALLOC(acc.maxs, (size_t)kMaxFields * max_objects));
+        RTG_TRY(DALLOC(tex_bbox, 4 * (size_t)max_objects));
+        RTG_TRY(DALLOC(tex_hist, 17 * (size_t)max_objects));
+        RTG_TRY(DALLOC(tex_glcm, 64 * (size_t)max_objects));
+        RTG_TRY(DALLOC(tex_mom, 4 * (size_t)max_objects));
+        // the checker's own control: one byte into the arena's band
+        if (c->guard_bytes && getenv("RTG_GUARD_SELFTEST"))
+          for (const auto& g : c->guards)
+            if (std::string(g.name) == "arena") RTG_CUDA(cudaMemset(g.end + 5, 0, 1));
         RTG_CUDA(cudaMemsetAsync(c->misc, 0, sizeof(int32_t) * (128 + (size_t)max_h), c->stream));
         RTG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(uint32_t), c->stream));
         RTG_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(int64_t) * RTG_NUM_STATS, c->stream));
@@ -683,6 +700,24 @@ int rtg_ctx_set_option(rtg_ctx* ctx, int option, int64_t value) {
 int rtg_ctx_launches(rtg_ctx* ctx, int64_t* out) {
   if (!ctx || !out) return fail(RTG_ERR_INVALID_ARG, "null argument");
   *out = ctx->launches;
+  return RTG_OK;
+}
+
+int rtg_ctx_guard_check(rtg_ctx* ctx, int32_t* n_checked) {
+  if (!ctx) return fail(RTG_ERR_INVALID_ARG, "null context");
+  RTG_CUDA(cudaSetDevice(ctx->device));
+  RTG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<unsigned char> host(ctx->guard_bytes);
+  int32_t n = 0;
+  for (const auto& g : ctx->guards) {
+    RTG_CUDA(cudaMemcpy(host.data(), g.end, ctx->guard_bytes, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < ctx->guard_bytes; ++i)
+      if (host[i] != kGuardByte)
+        return fail(RTG_ERR_INTERNAL, std::string("guard band after scratch buffer '") + g.name +
+                                          "' overwritten at +" + std::to_string(i));
+    ++n;
+  }
+  if (n_checked) *n_checked = n;
   return RTG_OK;
 }
 

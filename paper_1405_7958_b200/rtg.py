@@ -44,6 +44,7 @@ SYMBOLS = [
     "rtg_ctx_profile_read", "rtg_ctx_launches", "rtg_ctx_set_option",
     "rtg_texture_features", "rtg_texture_features_dev", "rtg_canny_dev",
     "rtg_process_tile_async", "rtg_ticket_wait", "rtg_ticket_query", "rtg_feature_columns",
+    "rtg_ctx_guard_check",
 ]
 ASYNC_SLOTS = 3  # RTG_ASYNC_SLOTS
 OPT_FILL_HOLES_IMPL = 0  # 0 union-find (default), 1 IWPP tile queue
@@ -152,6 +153,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "rtg_ctx_set_stream": [vp, vp],
         "rtg_ctx_sync": [vp],
         "rtg_ctx_stats": [vp, vp],
+        "rtg_ctx_guard_check": [vp, vp],
         "rtg_host_alloc": [ctypes.c_size_t, vp],
         "rtg_host_free": [vp],
         "rtg_segment_tile": [vp, vp, i64, i64, i64, vp, vp, vp, vp],
@@ -321,6 +323,13 @@ class Context:
 
     def set_option(self, option: int, value: int) -> None:
         check(self.lib.rtg_ctx_set_option(self.handle, option, value))
+
+    def guard_check(self) -> int:
+        """Verifies the scratch buffers' guard bands (context created with
+        RTG_GUARD_BYTES set); returns how many buffers were checked."""
+        n = ctypes.c_int32(0)
+        check(self.lib.rtg_ctx_guard_check(self.handle, ctypes.byref(n)))
+        return n.value
 
     def launches(self) -> int:
         n = ctypes.c_int64(0)

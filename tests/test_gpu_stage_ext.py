@@ -325,6 +325,67 @@ def test_entry_points_write_inside_their_outputs(rtg, oracle, shape):
         assert np.array_equal(i32("labels").cpu().numpy(), ref["labels"])
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096), (97, 203), (1696, 1696)])
+def test_internal_scratch_guard_bands(rtg, oracle, shape, monkeypatch):
+    """Every internal scratch buffer of the context followed by a canary band
+    (RTG_GUARD_BYTES): the whole stage under every implementation option and
+    with texture columns, then every per-operator entry point, must leave all
+    bands intact (rtg_ctx_guard_check) and the stage must still match the
+    oracle."""
+    _need_gpu()
+    h, w = shape
+    monkeypatch.setenv("RTG_GUARD_BYTES", "65536")
+    rgb = rtg.synth_tile_host(5, 2, h, w)
+    p = rtg.default_params()
+    ref = oracle.process_tile(rgb, p)
+    with rtg.Context(0, 4096, 4096, 1 << 15) as ctx:
+        assert ctx.guard_check() > 30
+        for opts in ({}, {rtg.OPT_LABEL_RUNS: 0}, {rtg.OPT_USE_GRAPHS: 0, rtg.OPT_PDL: 1},
+                     {rtg.OPT_WATERSHED_IMPL: 1}, {rtg.OPT_HMAX_IMPL: 1},
+                     {rtg.OPT_FILL_HOLES_IMPL: 1}, {rtg.OPT_RECON_IMPL: 1},
+                     {rtg.OPT_STREAM_IMPL: 0}):
+            for k, val in opts.items():
+                ctx.set_option(k, val)
+            mask, labels, hema_np, feats, n = ctx.process_tile(rgb, p)
+            for k in opts:
+                ctx.set_option(k, {rtg.OPT_USE_GRAPHS: 1, rtg.OPT_STREAM_IMPL: 1,
+                                   rtg.OPT_LABEL_RUNS: 1}.get(k, 0))
+            ctx.guard_check()
+            assert n == ref["n"] and np.array_equal(labels, ref["labels"]), opts
+        pt = rtg.default_params()
+        pt.texture = 1
+        ctx.process_tile(rgb, pt)
+        ctx.guard_check()
+        # the per-operator entry points on device buffers
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        hema = d(hema_np)
+        m = d(ref["mask"])
+        o8 = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+        o32 = torch.empty((h, w), dtype=torch.int32, device="cuda")
+        n1 = torch.empty(1, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        ctx.fill_holes_dev(m, h, w, o8)
+        ctx.area_threshold_dev(m, h, w, 8, p.min_area, p.max_area, o8)
+        ctx.edt_dev(m, h, w, o32)
+        ctx.watershed_dev(m, h, w, p.ws_h, o8, o32)
+        ctx.bwlabel_dev(m, h, w, 8, o32, n1)
+        ctx.recon_dev(hema, hema, h, w, 8, o8)
+        ctx.canny_dev(hema, h, w, o8)
+        ctx.sync()
+        assert ctx.guard_check() > 30
+
+
+def test_internal_scratch_guard_check_detects(rtg, monkeypatch):
+    """The checker's control: a context whose arena band is corrupted at
+    creation (RTG_GUARD_SELFTEST) must fail the check, naming the buffer."""
+    _need_gpu()
+    monkeypatch.setenv("RTG_GUARD_BYTES", "4096")
+    monkeypatch.setenv("RTG_GUARD_SELFTEST", "1")
+    with rtg.Context(0, 256, 256, 1 << 10) as ctx:
+        with pytest.raises(rtg.Error, match="arena' overwritten at \\+5"):
+            ctx.guard_check()
+
+
 def test_concurrent_runs_are_deterministic(rtg):
     """The same two tiles on four contexts at once, five rounds, with and
     without CUDA graphs and programmatic dependent launch: every run must be
