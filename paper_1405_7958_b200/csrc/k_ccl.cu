@@ -81,8 +81,15 @@ __device__ __forceinline__ void flatten_jump_t(T* par, int rb, int nruns) {
       const int k = __ffs(m) - 1;
       const int32_t p = par[rb + k];
       const int32_t gp = par[p];
-      if (gp != p) par[rb + k] = (T)gp;
-      else pend &= ~(1u << k);
+      if (gp == p) {
+        pend &= ~(1u << k);
+        continue;
+      }
+      // three links per step; an entry that lands on a root is done now
+      // rather than after one more round
+      const int32_t ggp = par[gp];
+      par[rb + k] = (T)ggp;
+      if (ggp == gp) pend &= ~(1u << k);
     }
     __syncwarp();
     if (!__any_sync(0xFFFFFFFFu, pend != 0)) break;
