@@ -328,12 +328,17 @@ def test_watershed_4k(rtg, ctx, oracle, ws_h):
     assert np.array_equal(_dev_np(sep), sep_ref)
 
 
-@pytest.mark.parametrize("case", ["big_blob", "thin_diagonal", "border_touching", "all_fg"])
-def test_watershed_objects_size_classes(rtg, ctx, oracle, case):
-    """Object-parallel watershed on objects beyond the 12 KB per-warp class:
-    a large blob (227 KB CTA class), a long diagonal thread whose bbox region
-    is huge (global-arena class), objects cut by the tile border, and a tile
-    with no background at all."""
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("case", ["big_blob", "thin_diagonal", "border_touching", "all_fg",
+                                  "bands", "squares"])
+def test_watershed_objects_size_classes(rtg, ctx, oracle, case, impl):
+    """Both watershed implementations (tiled default, object-parallel) on
+    objects beyond the object-parallel path's 12 KB per-warp class: a large
+    blob (227 KB CTA class), a long diagonal thread whose bbox region is huge
+    (global-arena class), objects cut by the tile border, a tile with no
+    background at all, and plateau-heavy shapes (thick bands and squares:
+    long flat EDT ridges, i.e. large plateau components in the compact
+    plateau forest)."""
     h, w = 600, 700
     m = np.zeros((h, w), np.uint8)
     if case == "big_blob":
@@ -349,12 +354,26 @@ def test_watershed_objects_size_classes(rtg, ctx, oracle, case):
         yy, xx = np.mgrid[0:h, 0:w]
         m[(yy ** 2 + xx ** 2) < 120 ** 2] = 1
         m[((yy - h) ** 2 + (xx - 350) ** 2) < 90 ** 2] = 1
+    elif case == "bands":
+        m[40:71, 10:690] = 1
+        m[120:160, 50:650] = 1
+        m[200:400, 300:340] = 1
+        m[420:451, :] = 1
+    elif case == "squares":
+        for y0 in range(10, 560, 70):
+            for x0 in range(10, 660, 70):
+                m[y0:y0 + 41 + (x0 % 3), x0:x0 + 41 + (y0 % 5)] = 1
+        m[100:140, 45:90] = 1  # joins two squares
     else:
         m[:] = 1
     sep_ref, basin_ref = oracle.watershed(m, 3)
     sep = torch.empty((h, w), dtype=torch.uint8, device="cuda")
     basin = torch.empty((h, w), dtype=torch.int32, device="cuda")
-    ctx.watershed_dev(_np_dev(m), h, w, 3, sep, basin)
+    ctx.set_option(rtg.OPT_WATERSHED_IMPL, impl)
+    try:
+        ctx.watershed_dev(_np_dev(m), h, w, 3, sep, basin)
+    finally:
+        ctx.set_option(rtg.OPT_WATERSHED_IMPL, 0)
     assert np.array_equal(_dev_np(basin), basin_ref)
     assert np.array_equal(_dev_np(sep), sep_ref)
 
