@@ -573,7 +573,7 @@ __global__ void k_ccl_seams_rt(int h, int w, int tiles_x, int row_seams,
 
 // Flattens the local roots onto the global roots and folds the local
 // accumulators into them; global roots are marked in the bitmap.
-__global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
+__global__ void k_ccl_flatten(int32_t* __restrict__ lroots,
                               const int32_t* __restrict__ lcount, int32_t* roots,
                               int32_t* __restrict__ counts, int32_t* __restrict__ flags,
                               uint32_t* __restrict__ bitmap, bool seed_in_counts = false) {
@@ -592,6 +592,9 @@ __global__ void k_ccl_flatten(const int32_t* __restrict__ lroots,
       const int32_t r = lroots[2 * k];
       info = (uint32_t)lroots[2 * k + 1];
       g = uf_find_g(roots, r);
+      // the accumulator slot is consumed here: it becomes the global root,
+      // so the emit kernels skip the roots[] gather
+      lroots[2 * k + 1] = g;
       if (g != r) atomicMin(roots + r, g);
       else if (bitmap) atomicOr(bitmap + (r >> 5), 1u << (r & 31));
     }
@@ -812,8 +815,9 @@ k_label_emit(CclRuns rt, const int32_t* __restrict__ lroots, const int32_t* __re
   // per-pixel form), and each label's feature accumulators reset once (at
   // the local root that is the global root)
   for (int j = lane; j < ti.y; j += 32) {
-    const int32_t lr = __ldg(lroots + 2 * (ti.x + j));
-    const int32_t r = __ldcg(roots + lr);
+    // (local root, global root): k_ccl_flatten wrote the global root
+    const int2 e = __ldg(reinterpret_cast<const int2*>(lroots) + ti.x + j);
+    const int32_t lr = e.x, r = e.y;
     const int32_t label =
         __ldg(wprefix + (r >> 5)) + __popc(__ldg(bm + (r >> 5)) & ((1u << (r & 31)) - 1u)) + 1;
     s_rank[wid][j] = label;
@@ -895,7 +899,7 @@ k_seeded_emit(CclRuns rt, const int32_t* __restrict__ lroots, const int32_t* __r
   const int x0 = (tile % tiles_x) * 32, y0 = (tile / tiles_x) * 32;
   const int2 ti = __ldg(rt.tinfo + tile);
   for (int j = lane; j < ti.y; j += 32)  // seeded component? (its global root's flag)
-    s_kp[wid][j] = __ldcg(flag + __ldcg(roots + __ldg(lroots + 2 * (ti.x + j)))) != 0;
+    s_kp[wid][j] = __ldcg(flag + __ldg(lroots + 2 * (ti.x + j) + 1)) != 0;
   const uint32_t bits = __ldg(rt.rowbits + tile * 32 + lane);
   const uint4* src = reinterpret_cast<const uint4*>(rt.rtab + (int64_t)tile * 512 + lane * 16);
   const uint4 e0 = __ldg(src), e1 = __ldg(src + 1);
@@ -1036,15 +1040,17 @@ struct RunTable {
   const uint32_t* rowbits;  // [tile * 32 + r]: foreground bits of row r of the tile
   const uint16_t* rtab;     // [tile * 1024 + r * 32 + k]: ordinal of run k's local root
   const int2* tinfo;        // [tile]: (first local-root slot, local-root count)
-  const int32_t* lroots;    // the local-root list (global index, accumulator) pairs
+  const int32_t* lroots;    // the local-root list: (global index, accumulator) pairs,
+                            // (global index, global root) after k_ccl_flatten
   int w, tiles_x;
-  __device__ __forceinline__ int32_t local_root(int32_t q) const {
+  // the global root of q's component (valid after k_ccl_flatten)
+  __device__ __forceinline__ int32_t global_root(int32_t q) const {
     const int y = q / w, x = q - y * w;
     const int tile = (y >> 5) * tiles_x + (x >> 5), r = y & 31, c = x & 31;
     const uint32_t fgb = rowbits[tile * 32 + r], bgb = ~fgb;
     const uint32_t st = (fgb & ~(fgb << 1)) | (bgb & ~(bgb << 1));
     const int k = __popc(st & ((2u << c) - 1u)) - 1;
-    return lroots[2 * (tinfo[tile].x + rtab[(int64_t)tile * 1024 + r * 32 + k])];
+    return lroots[2 * (tinfo[tile].x + rtab[(int64_t)tile * 1024 + r * 32 + k]) + 1];
   }
   __device__ __forceinline__ bool fg(int32_t q) const {
     const int y = q / w, x = q - y * w;
@@ -1415,11 +1421,11 @@ __global__ void k_fb_tree(const int32_t* __restrict__ lroots, const int32_t* __r
   pdl_enter();
   const int n = *lcount;
   auto above = [&](int32_t q) {  // global root of the pixel above q
-    return rt.rtab ? roots[rt.local_root(q - w)] : root_of(roots, q - w);
+    return rt.rtab ? rt.global_root(q - w) : root_of(roots, q - w);
   };
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t r = lroots[2 * k];
-    if (roots[r] != r) continue;
+    if (lroots[2 * k + 1] != r) continue;  // not the global root
     int32_t cur = r, t = -1;
     bool fg = rt.rtab ? rt.fg(r) : m[r] != 0;
     if (fg || !(counts[r] & (int32_t)kSeedBit)) {
@@ -1495,7 +1501,7 @@ k_fb_emit(const uint32_t* __restrict__ rowbits, const uint16_t* __restrict__ rta
     // global root -> top-level ancestor -> subtree area in range
     const int2 ti = __ldg(tinfo + tile);
     for (int j = lane; j < ti.y; j += 32) {
-      const int32_t t = __ldcg(top + __ldcg(roots + __ldg(lroots + 2 * (ti.x + j))));
+      const int32_t t = __ldcg(top + __ldg(lroots + 2 * (ti.x + j) + 1));
       bool kp = false;
       if (t >= 0) {
         const int32_t a = __ldcg(total + t);
