@@ -89,7 +89,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
             const uint16_t* __restrict__ Fw,
             uint8_t* __restrict__ dir, int32_t* __restrict__ fmap, int32_t* __restrict__ parK,
             int32_t* __restrict__ cntK, uint8_t* __restrict__ flat, int32_t* __restrict__ flat_list,
-            int32_t* __restrict__ flat_count) {
+            int32_t* __restrict__ flat_count, uint8_t* __restrict__ eqm) {
   pdl_enter();
   const int w = (int)dw.d;
   __shared__ int32_t sm[9];
@@ -98,10 +98,12 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
     const int k = k0 + threadIdx.x;
     bool is_flat = false;
     int32_t p = 0;
+    uint32_t eq = 0;  // foreground neighbours at p's level
     if (k < n) {
       p = list[k];
       uint32_t fv[8];
-      gather8(Fw, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0u, fv);
+      const uint32_t fm = list_nbrs(h, dw, mask, nbm, k, p);
+      gather8(Fw, w, p, fm, 0u, fv);
       // steepest ascent as one max over keys value << 3 | (7 - t): the first
       // (row-major) maximum wins ties, and p's own key (f << 3 | 7) beats
       // every neighbour at its level or below
@@ -109,6 +111,8 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       uint32_t best = self;
 #pragma unroll
       for (int t = 0; t < 8; ++t) best = max(best, fv[t] << 3 | (7u - t));
+#pragma unroll
+      for (int t = 0; t < 8; ++t) eq |= (((fm >> t) & 1u) && fv[t] == (self >> 3) ? 1u : 0u) << t;
       if (best != self) {
         dir[p] = dir_code(7 - (int)(best & 7u));
         flat[p] = 0;
@@ -125,6 +129,7 @@ k_ws_arrows(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       fmap[p] = slot;
       parK[slot] = slot;
       cntK[slot] = 0;
+      eqm[slot] = (uint8_t)eq;  // same-level neighbours: the plateau kernels' only gather
     }
   }
 }
@@ -157,27 +162,23 @@ __device__ __forceinline__ void ukey_unite(int32_t* par, const int32_t* __restri
 // Flat pixels: the seed arrow (first row-major same-level non-flat
 // neighbour: distance 1) and plateau unions with the backward same-level flat
 // neighbours.
-__global__ void k_ws_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
-                           const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
+__global__ void k_ws_union(int w, const uint8_t* __restrict__ flat,
                            const int32_t* __restrict__ flat_list,
                            const int32_t* __restrict__ flat_count, uint8_t* __restrict__ dir,
-                           const int32_t* __restrict__ fmap, int32_t* parK) {
+                           const int32_t* __restrict__ fmap, int32_t* parK,
+                           const uint8_t* __restrict__ eqm) {
   pdl_enter();
-  const int w = (int)dw.d;
   const int n = *flat_count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = flat_list[k];
-    const int y = fdiv(i, dw), x = i - y * w;
-    const uint16_t f = Fw[i];
     int seed = -1;
-    const uint32_t fm = fg_nbrs(h, w, mask, i, y, x);
-    uint32_t fv[8], fl[8];
-    gather8(Fw, w, i, fm, 0u, fv);
-    gather8(flat, w, i, fm, 1u, fl);
+    const uint32_t eq = eqm[k];  // same-level neighbours (k_ws_arrows)
+    uint32_t fl[8];
+    gather8(flat, w, i, eq, 1u, fl);
     uint32_t same = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      if (!((fm >> t) & 1u) || fv[t] != f) continue;
+      if (!((eq >> t) & 1u)) continue;
       if (!fl[t]) {
         if (seed < 0) seed = t;
       } else if (t < 4) {  // backward neighbour (above or left)
@@ -275,20 +276,16 @@ __global__ void k_ws_scatter_c(const int32_t* __restrict__ flat_list,
 // Same-plateau neighbour mask of p (bit t = row-major neighbour t of 8): the
 // flat neighbours at p's level.  That is exactly its plateau component's
 // neighbours, since k_ws_union unites every such pair.
-__device__ __forceinline__ uint32_t plateau_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
-                                                 const uint16_t* __restrict__ Fw,
-                                                 const uint8_t* __restrict__ flat, int32_t p,
-                                                 uint16_t f) {
-  const int w = (int)dw.d;
-  const int y = fdiv(p, dw), x = p - y * w;
-  const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
-  uint32_t fv[8], fl[8];
-  gather8(Fw, w, p, fm, 0u, fv);
-  gather8(flat, w, p, fm, 0u, fl);
+__device__ __forceinline__ uint32_t plateau_nbrs(int w, const uint8_t* __restrict__ flat,
+                                                 const int32_t* __restrict__ fmap,
+                                                 const uint8_t* __restrict__ eqm, int32_t p) {
+  const uint32_t eq = eqm[__ldg(fmap + p)];  // p's same-level neighbours (k_ws_arrows)
+  uint32_t fl[8];
+  gather8(flat, w, p, eq, 0u, fl);
   uint32_t cand = 0;
 #pragma unroll
   for (int t = 0; t < 8; ++t)
-    if (((fm >> t) & 1u) && fl[t] && fv[t] == f) cand |= 1u << t;
+    if (fl[t]) cand |= 1u << t;
   return cand;
 }
 
@@ -325,13 +322,12 @@ __device__ __forceinline__ int32_t member_px(int32_t m) { return m < 0 ? ~m : m;
 // d - 1.  Up to 32 * kPer members per warp in registers; longer ranges
 // re-derive their neighbour masks every pass.
 __global__ void __launch_bounds__(256)
-k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
-             const uint16_t* __restrict__ Fw, const uint8_t* __restrict__ flat,
+k_ws_plateau(int w, const uint8_t* __restrict__ flat, const int32_t* __restrict__ fmap,
+             const uint8_t* __restrict__ eqm,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint8_t* __restrict__ dir, int32_t* delta, int2* __restrict__ scratch,
              uint8_t* slotmap) {
   pdl_enter();
-  const int w = (int)dw.d;
   constexpr int kPer = 4;
   // small ranges relax in shared memory (distances by slot, neighbour slots)
   __shared__ int32_t s_val[8][32 * kPer];
@@ -357,7 +353,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         if (k < e) {
           px[q] = member_px(members[k]);
           d[q] = dir[px[q]] != kDirNone ? 1 : kInfD;
-          nb[q] = plateau_nbrs(h, dw, mask, Fw, flat, px[q], Fw[px[q]]);
+          nb[q] = plateau_nbrs(w, flat, fmap, eqm, px[q]);
           sv[lane + 32 * q] = d[q];
           slotmap[px[q]] = (uint8_t)(lane + 32 * q);
         }
@@ -403,7 +399,7 @@ k_ws_plateau(int h, FastDiv dw, const uint32_t* __restrict__ mask,
       for (int k = s0 + lane; k < e; k += 32) {
         const int32_t p = member_px(members[k]);
         vd[p] = dir[p] != kDirNone ? 1 : kInfD;
-        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(h, dw, mask, Fw, flat, p, Fw[p]));
+        scratch[k] = make_int2(p, (int32_t)plateau_nbrs(w, flat, fmap, eqm, p));
       }
       __syncwarp();
       while (true) {
@@ -898,12 +894,14 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
   // k_ws_basins
   int32_t* parK = reinterpret_cast<int32_t*>(ctx->arena);
   int32_t* cntK = parK + n;
+  uint8_t* eqm = reinterpret_cast<uint8_t*>(ctx->u16c);  // per flat slot (the EDT plane is dead)
   RTG_CUDA(launch_k(ctx, k_ws_arrows, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
                     (const uint8_t*)nbm, Fw, dir, par, parK, cntK, flat, ctx->flat_list,
-                    flat_count));
+                    flat_count, eqm));
   RTG_LAUNCH("k_ws_arrows");
-  RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->flat_list,
-                    flat_count, dir, (const int32_t*)par, parK));
+  RTG_CUDA(launch_k(ctx, k_ws_union, g, 256, 0, (int)w, (const uint8_t*)flat,
+                    (const int32_t*)ctx->flat_list, (const int32_t*)flat_count, dir,
+                    (const int32_t*)par, parK, (const uint8_t*)eqm));
   RTG_LAUNCH("k_ws_union");
   RTG_CUDA(launch_k(ctx, k_ws_roots_c, g, 256, 0, (const int32_t*)ctx->flat_list, flat_count,
                     (const uint8_t*)dir, parK, cntK, delta));
@@ -915,8 +913,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                     (const int32_t*)parK, (const int32_t*)cntK, (const int32_t*)delta,
                     ctx->lroots));
   RTG_LAUNCH("k_ws_scatter_c");
-  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)h, dwv, fgbits, Fw, flat, ctx->lroots,
-                    walloc, dir, delta, member_scratch, ctx->m2 /* slot map */));
+  RTG_CUDA(launch_k(ctx, k_ws_plateau, g, 256, 0, (int)w, (const uint8_t*)flat,
+                    (const int32_t*)par /* pixel -> flat slot */, (const uint8_t*)eqm,
+                    (const int32_t*)ctx->lroots, (const unsigned long long*)walloc, dir, delta,
+                    member_scratch, ctx->m2 /* slot map */));
   RTG_LAUNCH("k_ws_plateau");
   RTG_CUDA(launch_k(ctx, k_ws_basins, g, 256, 0, (int)w, fgl, fgn, dir, par, basin));
   RTG_LAUNCH("k_ws_basins");
