@@ -448,7 +448,8 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
             const uint16_t* __restrict__ dq, int32_t ws_h,
             uint16_t* __restrict__ Fw, uint8_t* __restrict__ sflag, int32_t* __restrict__ par,
             int32_t* __restrict__ cnt, int32_t* __restrict__ slist,
-            int32_t* __restrict__ scount, int32_t* __restrict__ smap) {
+            int32_t* __restrict__ scount, int32_t* __restrict__ smap,
+            uint8_t* __restrict__ smask) {
   pdl_enter();
   const int w = (int)dw.d;
   __shared__ int32_t sm[9];
@@ -457,11 +458,13 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
     const int k = k0 + threadIdx.x;
     bool sus = false;
     int32_t p = 0;
+    uint32_t fm = 0;
     if (k < n) {
       p = list[k];
       const int32_t v = dq[p];
       int32_t dv[8];
-      gather8(dq, w, p, list_nbrs(h, dw, mask, nbm, k, p), 0, dv);
+      fm = list_nbrs(h, dw, mask, nbm, k, p);
+      gather8(dq, w, p, fm, 0, dv);
       int32_t mx = 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) mx = max(mx, dv[t]);
@@ -482,23 +485,22 @@ k_hmax_init(int h, FastDiv dw, const int32_t* __restrict__ list, const int32_t* 
       smap[p] = slot;
       par[slot] = slot;
       cnt[slot] = 0;
+      smask[slot] = (uint8_t)fm;  // foreground neighbours: no bit-plane tests downstream
     }
   }
 }
 
-__global__ void k_hmax_union(int h, FastDiv dw, const uint32_t* __restrict__ mask,
-                             const uint8_t* __restrict__ sflag,
+__global__ void k_hmax_union(int w, const uint8_t* __restrict__ sflag,
                              const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-                             const int32_t* __restrict__ smap, int32_t* par) {
+                             const int32_t* __restrict__ smap, int32_t* par,
+                             const uint8_t* __restrict__ smask) {
   pdl_enter();
-  const int w = (int)dw.d;
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int32_t i = list[k];
-    const int y = fdiv(i, dw), x = i - y * w;
     // backward neighbours only (bits 0..3: above row and left)
     uint32_t sv[8];
-    gather8(sflag, w, i, fg_nbrs(h, w, mask, i, y, x) & 0xFu, 0u, sv);
+    gather8(sflag, w, i, smask[k] & 0xFu, 0u, sv);
     // unite_backward's skips, on compact indices (smap: pixel -> suspect slot)
     const bool ul = sv[0], u = sv[1], ur = sv[2], l = sv[3];
     if (l) {
@@ -563,13 +565,12 @@ k_hmax_alloc(const int32_t* __restrict__ list, const int32_t* __restrict__ count
 
 // Neighbour summary of suspect p: bit t set = row-major neighbour t is a
 // suspect (same component); fixed = max F over the other neighbours.
-__device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint32_t* __restrict__ mask,
+__device__ __forceinline__ uint32_t hmax_nbrs(int w, const int32_t* __restrict__ smap,
+                                              const uint8_t* __restrict__ smask,
                                               const uint16_t* __restrict__ dq,
                                               const uint8_t* __restrict__ sflag, int32_t p,
                                               int32_t& fixed) {
-  const int w = (int)dw.d;
-  const int y = fdiv(p, dw), x = p - y * w;
-  const uint32_t fm = fg_nbrs(h, w, mask, p, y, x);
+  const uint32_t fm = smask[__ldg(smap + p)];  // k_hmax_init's foreground-neighbour mask
   uint32_t sv[8];
   int32_t dv[8];
   gather8(sflag, w, p, fm, 0u, sv);
@@ -585,12 +586,11 @@ __device__ __forceinline__ uint32_t hmax_nbrs(int h, FastDiv dw, const uint32_t*
 }
 
 __global__ void __launch_bounds__(256)
-k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
+k_hmax_solve(int w, const int32_t* __restrict__ smap, const uint8_t* __restrict__ smask,
              const uint16_t* __restrict__ dq, const uint8_t* __restrict__ sflag, int32_t ws_h,
              const int32_t* __restrict__ members, const unsigned long long* __restrict__ alloc,
              uint16_t* Fw, int2* __restrict__ scratch, uint8_t* slotmap) {
   pdl_enter();
-  const int w = (int)dw.d;
   constexpr int kPer = 4;
   // small ranges iterate in shared memory: member values by slot (index in
   // the warp's range) and each member's neighbour slots, so a relaxation
@@ -619,7 +619,7 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
           px[q] = member_px(members[k]);
           d[q] = dq[px[q]];
           int32_t fixed;
-          nb[q] = hmax_nbrs(h, dw, mask, dq, sflag, px[q], fixed);
+          nb[q] = hmax_nbrs(w, smap, smask, dq, sflag, px[q], fixed);
           f[q] = min(d[q], max(d[q] > ws_h ? d[q] - ws_h : 0, fixed));
           sv[lane + 32 * q] = f[q];
           slotmap[px[q]] = (uint8_t)(lane + 32 * q);
@@ -663,7 +663,7 @@ k_hmax_solve(int h, FastDiv dw, const uint32_t* __restrict__ mask,
         const int32_t p = member_px(members[k]);
         const int32_t dp = dq[p];
         int32_t fixed;
-        const uint32_t nbm = hmax_nbrs(h, dw, mask, dq, sflag, p, fixed);
+        const uint32_t nbm = hmax_nbrs(w, smap, smask, dq, sflag, p, fixed);
         vf[p] = (uint16_t)(min(dp, max(dp > ws_h ? dp - ws_h : 0, fixed)) + 1);
         scratch[k] = make_int2(p, (int32_t)(nbm | ((uint32_t)dp << 8)));
       }
@@ -862,12 +862,14 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
     // compact counters in the arena's first half (the basin plane may be the
     // caller's output, whose background must stay as cleared)
     int32_t* hcnt = reinterpret_cast<int32_t*>(ctx->arena);
+    uint8_t* smask = reinterpret_cast<uint8_t*>(ctx->u16c);  // per suspect slot (EDT plane dead)
     RTG_CUDA(launch_k(ctx, k_hmax_init, g, 256, 0, (int)h, dwv, fgl, fgn, fgbits,
                       (const uint8_t*)nbm, dq, ws_h, Fw, sflag,
-                                            par, hcnt, list, count, smap));
+                                            par, hcnt, list, count, smap, smask));
     RTG_LAUNCH("k_hmax_init");
-    RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)h, dwv, fgbits, sflag, list, count,
-                      (const int32_t*)smap, par));
+    RTG_CUDA(launch_k(ctx, k_hmax_union, g, 256, 0, (int)w, (const uint8_t*)sflag,
+                      (const int32_t*)list, (const int32_t*)count, (const int32_t*)smap, par,
+                      (const uint8_t*)smask));
     RTG_LAUNCH("k_hmax_union");
     RTG_CUDA(launch_k(ctx, k_hmax_roots, g, 256, 0, (const int32_t*)count, par, hcnt, slot));
     RTG_LAUNCH("k_hmax_roots");
@@ -877,8 +879,10 @@ int watershed(rtg_ctx* ctx, const uint8_t* mask, int64_t h, int64_t w,
                       (const int32_t*)par, (const int32_t*)hcnt, (const int32_t*)slot,
                       ctx->lroots));
     RTG_LAUNCH("k_hmax_scatter");
-    RTG_CUDA(launch_k(ctx, k_hmax_solve, g, 256, 0, (int)h, dwv, fgbits, dq, sflag, ws_h, ctx->lroots,
-                                             alloc, Fw, member_scratch,
+    RTG_CUDA(launch_k(ctx, k_hmax_solve, g, 256, 0, (int)w, (const int32_t*)smap,
+                      (const uint8_t*)smask, (const uint16_t*)dq, (const uint8_t*)sflag, ws_h,
+                      (const int32_t*)ctx->lroots, (const unsigned long long*)alloc, Fw,
+                      member_scratch,
                                              ctx->m2 /* slot map: the EDT row distances are dead */));
     RTG_LAUNCH("k_hmax_solve");
   }
