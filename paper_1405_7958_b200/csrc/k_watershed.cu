@@ -702,6 +702,14 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
             int32_t* __restrict__ basin) {
   pdl_enter();
   constexpr int kC = 4;
+  // the step of every code (index c & 15): one shared load per step instead
+  // of the decode arithmetic
+  __shared__ int32_t s_off[16];
+  if (threadIdx.x < 16) {
+    const int c = (int)threadIdx.x;
+    s_off[c] = ((c >> 2) & 3) * w + (c & 3) - (w + 1);
+  }
+  __syncthreads();
   const int n = *count;
   const int span = gridDim.x * blockDim.x * kC;
   for (int k0 = blockIdx.x * blockDim.x * kC + threadIdx.x; k0 < n; k0 += span) {
@@ -721,7 +729,6 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
     // both the zero offset: a finished chain stays put, so the chains take
     // kSteps steps between convergence tests with no per-step predicate.
     constexpr int kSteps = 4;
-    const int32_t wm = w + 1;
     auto moving = [](uint32_t c) { return c != kDirSelf && c != kDirNone; };
     while (true) {
       bool any = false;
@@ -732,7 +739,7 @@ k_ws_basins(int w, const int32_t* __restrict__ list, const int32_t* __restrict__
       for (int s = 0; s < kSteps; ++s) {
 #pragma unroll
         for (int j = 0; j < kC; ++j) {
-          q[j] += (int32_t)((d[j] >> 2) & 3u) * w + (int32_t)(d[j] & 3u) - wm;
+          q[j] += s_off[d[j] & 15u];
           d[j] = dir[q[j]];
         }
       }
